@@ -1,0 +1,173 @@
+/*
+ * ssmquant_sm100.h — C-ABI of libssmquant_sm100.so, the B200 (sm_100a) hot path of
+ * Quamba2's quantized Mamba block forward (arXiv 2503.22879).
+ *
+ * Every entry point replaces one step of the reference contract's quantized block
+ * (/root/reference/SPEC.md; the reference ships no implementation of it):
+ *
+ *   sq_rmsnorm_quant          model pre-norm + per-tensor int8 quant of the block input u
+ *                             ("quantize ... u", LEDGER G5, G8)
+ *   sq_gemm_w8a8/sq_gemm_w4a8 in_proj / out_proj / x_proj / dt_proj / head:
+ *                             tensor.matmul (pkg/src/ssmquant/tensor.py:33-54) on quantized
+ *                             operands + quantizer.fuse_scales + requant
+ *   sq_gemv_w4a16             W4A16 projections ("dequantizes weights into the float path",
+ *                             SPEC.md:329)
+ *   sq_conv1d_int8            ssm_block.causal_conv1d on int8 codes,
+ *                             + SiLU + requant to clustered x / per-state-group B,C scales
+ *   sq_conv1d_update_int8     the same with cache stepping (decode)
+ *   sq_ssd_scan_int8          ssm_block.ssd_chunked / selective_scan for
+ *                             Mamba2, int8 operands, fp32 state, gated output, int8 final state
+ *   sq_selective_scan_int8    Mamba1 selective_scan
+ *   sq_state_update_int8      decode-time stepping of SsmState
+ *   sq_gate_norm_had_quant    RMSNorm + hadamard.hadamard_quantize
+ *
+ *   sq_repack_w4 / sq_unpack_w4   u4packed <-> kernel layout
+ *
+ * Conventions: all pointers are device pointers owned by the caller; the library never
+ * allocates device memory and keeps no global mutable state except a thread-local
+ * last-error string.  Row-major, tokens-major activations; `ld*` are row strides in
+ * elements.  `stream` is a cudaStream_t.  Launches are asynchronous.  Return 0 on
+ * success or a negative sq_status (mapped by the Python layer onto
+ * ssmquant.errors: SQ_ERR_SHAPE -> ShapeError, SQ_ERR_LAYOUT -> LayoutError,
+ * SQ_ERR_CUDA / SQ_ERR_ARCH -> RuntimeError).
+ */
+#ifndef SSMQUANT_SM100_H
+#define SSMQUANT_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SQ_ABI_VERSION 1
+
+typedef enum {
+  SQ_OK = 0,
+  SQ_ERR_SHAPE = -1,
+  SQ_ERR_LAYOUT = -2,
+  SQ_ERR_CUDA = -3,
+  SQ_ERR_ARCH = -4,
+  SQ_ERR_ARG = -5
+} sq_status;
+
+/* GEMM epilogues.  y[m,n] = f32(acc[m,n]) * alpha[n] with acc the exact int32 sum. */
+typedef enum {
+  SQ_EPI_I32 = 0,    /* out int32 [M x N] = acc                                    */
+  SQ_EPI_F32 = 1,    /* out f32   [M x N] = y                                      */
+  SQ_EPI_QUANT = 2,  /* out int8  [M x N] = clamp(rint(y / col_scale[n]), -128, 127) */
+  SQ_EPI_RESID = 3   /* out f32   [M x N] += y   (residual stream, in place)         */
+} sq_epilogue;
+
+int sq_abi_version(void);
+const char* sq_last_error(void);
+/* 1 if the current device is sm_100 (B200-class) and the kernels can run. */
+int sq_device_supported(void);
+
+/* ---- weights ---------------------------------------------------------------------- */
+/* u4packed [N x K/2] (low nibble = even k) + int8 sg [N x K/group] -> kernel layout
+ * `dst` (sq_w4_bytes(N,K) bytes).  sg may be NULL (all ones; W4A16 layout). */
+int64_t sq_w4_bytes(int N, int K);
+int sq_repack_w4(const uint8_t* u4packed, int N, int K, uint8_t* dst, void* stream);
+int sq_unpack_w4(const uint8_t* src, int N, int K, uint8_t* u4packed, void* stream);
+
+/* ---- model glue --------------------------------------------------------------------- */
+/* out[m,:] = clamp(rint((x[m,:] * rsqrt(mean x^2 + eps)) * gamma / s)) */
+int sq_rmsnorm_quant(const float* x, int64_t ldx, const float* gamma, float eps, float s,
+                     int M, int D, int8_t* out, int64_t ldo, void* stream);
+/* out[m,:] = x[m,:] * rsqrt(mean x^2 + eps) * gamma (f32) */
+int sq_rmsnorm_f32(const float* x, int64_t ldx, const float* gamma, float eps,
+                   int M, int D, float* out, int64_t ldo, void* stream);
+/* out[m,:] = clamp(rint(x[m,:] / s))  (quantizer.quantize, PerTensor) */
+int sq_quantize_f32(const float* x, int64_t ldx, float s, int M, int D, int8_t* out, int64_t ldo, void* stream);
+/* h[m,:] = codes[tok[m],:] * row_scale[tok[m]] */
+int sq_embed_int8(const int8_t* codes, const float* row_scale, const int32_t* tok, int M, int D,
+                  float* h, void* stream);
+/* tok[m] = argmax_n logits[m, n] (lowest index on ties) */
+int sq_argmax_f32(const float* logits, int64_t ld, int M, int N, int32_t* tok, void* stream);
+
+/* ---- projections ------------------------------------------------------------------ */
+int sq_gemm_w8a8(const int8_t* a, int64_t lda, const int8_t* w /*[N x K]*/, const float* alpha,
+                 int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
+                 void* stream);
+int sq_gemm_w4a8(const int8_t* a, int64_t lda, const uint8_t* w4 /*repacked*/,
+                 const int8_t* sg /*[N x K/group]*/, int group, const float* alpha,
+                 int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
+                 void* stream);
+/* y[m,n] (+)= sum_g s_group[n,g] * sum_{k in g} w4[n,k] * half(x[m,k]);  resid!=0 adds in place */
+int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4 /*repacked*/,
+                  const float* s_group /*[N x K/group]*/, int group, int M, int N, int K,
+                  float* out, int64_t ldo, int resid, void* stream);
+
+/* ---- causal conv1d (+SiLU +requant) ------------------------------------------------- */
+/* x codes [B*T x C] (row stride ldx), cache codes [B x (Kc-1) x C] (read as the initial
+ * window if cache_in, always written with the final window), out codes [B*T x C]. */
+int sq_conv1d_int8(const int8_t* x, int64_t ldx, const float* w /*[C x Kc]*/, const float* bias,
+                   const float* s_in, const float* s_out, int B, int T, int C, int Kc,
+                   int8_t* cache, int cache_in, int8_t* out, int64_t ldo, void* stream);
+int sq_conv1d_update_int8(const int8_t* x, int64_t ldx, const float* w, const float* bias,
+                          const float* s_in, const float* s_out, int B, int C, int Kc,
+                          int8_t* cache, int8_t* out, int64_t ldo, void* stream);
+/* fp32 variants (W4A16 float path): x/out f32, cache f32 */
+int sq_conv1d_f32(const float* x, int64_t ldx, const float* w, const float* bias, int B, int T,
+                  int C, int Kc, float* cache, int cache_in, float* out, int64_t ldo, void* stream);
+
+/* ---- scans ------------------------------------------------------------------------ */
+/* Mamba2 parameters shared by prefill and decode. */
+typedef struct {
+  int n_heads, head_dim, d_state, n_groups;
+  const int32_t* head_group;   /* [nh] state group of each head                        */
+  const float* A;              /* [nh] (= -exp(a_log))                                 */
+  const float* D;              /* [nh]                                                 */
+  const float* dt_bias;        /* [nh]                                                 */
+  float s_dt, s_z;             /* per-tensor scales of the dt and z in_proj slices     */
+  const float* s_x;            /* [nh*P] clustered x scales (conv output)              */
+  const float* s_B;            /* [G]                                                  */
+  const float* s_C;            /* [G]                                                  */
+  const float* s_h;            /* [nh*P] cached-state scales (ClusterMap cells)        */
+} sq_mamba2_params;
+
+/* Prefill: codes x [B*T x nh*P], B/C [B*T x G*N], dt [B*T x nh], z [B*T x nh*P]
+ * (row strides ldx/ldbc/lddt/ldz), state [B x nh x P x N] int8 (read if state_in,
+ * written with the final state), y f32 [B*T x nh*P] gated by SiLU(z). */
+int sq_ssd_scan_int8(const sq_mamba2_params* p, int B, int T,
+                     const int8_t* x, int64_t ldx, const int8_t* Bm, const int8_t* Cm, int64_t ldbc,
+                     const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
+                     int8_t* state, int state_in, float* y, int64_t ldy, int chunk, void* stream);
+/* Decode (T=1): same operands, state updated in place. */
+int sq_state_update_int8(const sq_mamba2_params* p, int B,
+                         const int8_t* x, int64_t ldx, const int8_t* Bm, const int8_t* Cm, int64_t ldbc,
+                         const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
+                         int8_t* state, float* y, int64_t ldy, void* stream);
+/* W4A16 float path: f32 operands, f32 state [B x nh x P x N]. T=1 is decode. */
+int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T,
+                    const float* x, int64_t ldx, const float* Bm, const float* Cm, int64_t ldbc,
+                    const float* dt, int64_t lddt, const float* z, int64_t ldz,
+                    float* state, int state_in, float* y, int64_t ldy, void* stream);
+
+typedef struct {
+  int d_inner, d_state;
+  const float* A;              /* [d_inner x N]                                        */
+  const float* D;              /* [d_inner]                                            */
+  const float* dt_bias;        /* [d_inner]                                            */
+  float s_dt, s_z, s_B, s_C;
+  const float* s_x;            /* [d_inner]                                            */
+  const float* s_h;            /* [d_inner]                                            */
+} sq_mamba1_params;
+
+/* Mamba1 prefill (T>=1; T=1 is decode): codes x [B*T x d], dt [B*T x d], B/C [B*T x N]
+ * (row stride ldbc, C at +N), z [B*T x d]; state int8 [B x d x N]. */
+int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T,
+                           const int8_t* x, int64_t ldx, const int8_t* dt, int64_t lddt,
+                           const int8_t* BC, int64_t ldbc, const int8_t* z, int64_t ldz,
+                           int8_t* state, int state_in, float* y, int64_t ldy, void* stream);
+
+/* ---- gated-norm + Hadamard + quant ------------------------------------------------ */
+/* out[m,:] = clamp(rint(H_blk (y*rsqrt(mean y^2+eps)*gamma) / s_y)); hadamard=0 skips H. */
+int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* gamma, float eps, float s_y,
+                           int hadamard, int M, int D, int8_t* out, int64_t ldo, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,88 @@
+"""ctypes binding of libssmquant_sm100.so (include/ssmquant_sm100.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc, sm_100a).  There is
+no fallback: if the library is missing or the device is not sm_100, every op raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+LIB_NAME = "libssmquant_sm100.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+ABI_VERSION = 1
+
+_i8p = C.c_void_p
+_f32p = C.c_void_p
+_i64 = C.c_int64
+_int = C.c_int
+_flt = C.c_float
+_vp = C.c_void_p
+
+
+class Mamba2Params(C.Structure):
+    _fields_ = [("n_heads", _int), ("head_dim", _int), ("d_state", _int), ("n_groups", _int),
+                ("head_group", _vp), ("A", _vp), ("D", _vp), ("dt_bias", _vp),
+                ("s_dt", _flt), ("s_z", _flt), ("s_x", _vp), ("s_B", _vp), ("s_C", _vp), ("s_h", _vp)]
+
+
+class Mamba1Params(C.Structure):
+    _fields_ = [("d_inner", _int), ("d_state", _int), ("A", _vp), ("D", _vp), ("dt_bias", _vp),
+                ("s_dt", _flt), ("s_z", _flt), ("s_B", _flt), ("s_C", _flt), ("s_x", _vp), ("s_h", _vp)]
+
+
+_SIGS = {
+    "sq_abi_version": ([], _int),
+    "sq_last_error": ([], C.c_char_p),
+    "sq_device_supported": ([], _int),
+    "sq_w4_bytes": ([_int, _int], _i64),
+    "sq_repack_w4": ([_vp, _int, _int, _vp, _vp], _int),
+    "sq_unpack_w4": ([_vp, _int, _int, _vp, _vp], _int),
+    "sq_rmsnorm_quant": ([_vp, _i64, _vp, _flt, _flt, _int, _int, _vp, _i64, _vp], _int),
+    "sq_rmsnorm_f32": ([_vp, _i64, _vp, _flt, _int, _int, _vp, _i64, _vp], _int),
+    "sq_quantize_f32": ([_vp, _i64, _flt, _int, _int, _vp, _i64, _vp], _int),
+    "sq_embed_int8": ([_vp, _vp, _vp, _int, _int, _vp, _vp], _int),
+    "sq_argmax_f32": ([_vp, _i64, _int, _int, _vp, _vp], _int),
+    "sq_gemm_w8a8": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp], _int),
+    "sq_gemm_w4a8": ([_vp, _i64, _vp, _vp, _int, _vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp], _int),
+    "sq_gemv_w4a16": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _int, _vp], _int),
+    "sq_conv1d_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _i64, _vp], _int),
+    "sq_conv1d_update_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _vp, _vp, _i64, _vp], _int),
+    "sq_conv1d_f32": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _i64, _vp], _int),
+    "sq_ssd_scan_int8": ([C.POINTER(Mamba2Params), _int, _int, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
+                          _vp, _int, _vp, _i64, _int, _vp], _int),
+    "sq_state_update_int8": ([C.POINTER(Mamba2Params), _int, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
+                              _vp, _vp, _i64, _vp], _int),
+    "sq_ssd_scan_f32": ([C.POINTER(Mamba2Params), _int, _int, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
+                         _vp, _int, _vp, _i64, _vp], _int),
+    "sq_selective_scan_int8": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
+                                _vp, _int, _vp, _i64, _vp], _int),
+    "sq_gate_norm_had_quant": ([_vp, _i64, _vp, _flt, _flt, _int, _int, _int, _vp, _i64, _vp], _int),
+}
+
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load and type the library (no device work).  Raises if it is absent."""
+    global _lib
+    if _lib is not None and path == LIB_PATH:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    if lib.sq_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"ABI mismatch: {lib.sq_abi_version()} != {ABI_VERSION}")
+    if path == LIB_PATH:
+        _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().sq_last_error().decode("utf-8", "replace")

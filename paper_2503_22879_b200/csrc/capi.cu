@@ -1,0 +1,39 @@
+// C-ABI plumbing: version, thread-local last error, device check.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace sq {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return SQ_ERR_CUDA;
+  }
+  return SQ_OK;
+}
+
+}  // namespace sq
+
+extern "C" int sq_abi_version(void) { return SQ_ABI_VERSION; }
+
+extern "C" const char* sq_last_error(void) { return sq::g_err; }
+
+extern "C" int sq_device_supported(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return 0;
+  return p.major == 10 && p.minor == 0;
+}

@@ -1,0 +1,142 @@
+// K5: depthwise causal conv1d on int8 codes + SiLU + requant (Quamba2 W8A8 conv,
+// PAPER.md:302), prefill and decode-update variants.
+//
+// Layout: codes tokens-major [B*T x C] (C = d_inner + 2GN, contiguous, coalesced over c);
+// cache [B x (Kc-1) x C] int8 = the last Kc-1 input codes (exact — no requant error).
+// Math per (t, c) exactly as the oracle (oracle/qblock.py _conv_a8):
+//   v_j = f32(q_j) * s_in[c];  acc = bias[c];  acc = acc + w[c,j]*v_j  (j ascending, unfused)
+//   out = clamp(rint(silu(acc) / s_out[c]))
+// HBM-bound: each code is read once by the thread that owns its (segment, channel) plus
+// Kc-1 halo reads that hit L1/L2.
+#include "common.cuh"
+
+namespace sq {
+
+constexpr int kMaxK = 8;
+constexpr int kSeg = 64;   // tokens per thread in the prefill kernel
+
+template <typename TIn, typename TOut, bool Q>
+__global__ void conv1d_prefill_kernel(const TIn* __restrict__ x, int64_t ldx, const float* __restrict__ w,
+                                      const float* __restrict__ bias, const float* __restrict__ s_in,
+                                      const float* __restrict__ s_out, int B, int T, int C, int Kc,
+                                      const TIn* __restrict__ cache, int cache_in, TOut* __restrict__ out,
+                                      int64_t ldo) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int seg = blockIdx.y;
+  const int b = blockIdx.z;
+  if (c >= C) return;
+  const int t0 = seg * kSeg;
+  if (t0 >= T) return;
+  const int t1 = min(T, t0 + kSeg);
+  const float si = Q ? s_in[c] : 1.f;
+  const float so = Q ? s_out[c] : 1.f;
+  float wc[kMaxK];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) wc[j] = j < Kc ? w[c * Kc + j] : 0.f;
+  const float bc = bias[c];
+  float win[kMaxK];  // win[Kc-1] is the newest
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) win[j] = 0.f;
+  // initial window: inputs t0-Kc+1 .. t0-1
+  for (int j = 0; j < Kc - 1; ++j) {
+    const int t = t0 - (Kc - 1) + j;
+    float v = 0.f;
+    if (t >= 0) {
+      v = Q ? __fmul_rn((float)x[((int64_t)b * T + t) * ldx + c], si) : (float)x[((int64_t)b * T + t) * ldx + c];
+    } else if (cache_in) {
+      const int cj = (Kc - 1) + t;  // index into cache window
+      TIn cv = cache[((int64_t)b * (Kc - 1) + cj) * C + c];
+      v = Q ? __fmul_rn((float)cv, si) : (float)cv;
+    }
+    win[j] = v;
+  }
+  for (int t = t0; t < t1; ++t) {
+    const TIn xv = x[((int64_t)b * T + t) * ldx + c];
+    win[Kc - 1] = Q ? __fmul_rn((float)xv, si) : (float)xv;
+    float acc = bc;
+    for (int j = 0; j < Kc; ++j) acc = __fadd_rn(acc, __fmul_rn(wc[j], win[j]));
+    const float sv = silu_f(acc);
+    if (Q)
+      reinterpret_cast<int8_t*>(out)[((int64_t)b * T + t) * ldo + c] = quant8(sv, so);
+    else
+      reinterpret_cast<float*>(out)[((int64_t)b * T + t) * ldo + c] = sv;
+    for (int j = 0; j < Kc - 1; ++j) win[j] = win[j + 1];
+  }
+}
+
+// Final cache window = last Kc-1 entries of (old cache ++ x).  Separate launch so the
+// prefill kernel's reads of the old cache never race with these writes.
+template <typename T_>
+__global__ void conv1d_cache_kernel(const T_* __restrict__ x, int64_t ldx, int B, int T, int C, int Kc,
+                                    T_* __restrict__ cache, int cache_in) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (c >= C) return;
+  T_ nv[kMaxK];
+  for (int j = 0; j < Kc - 1; ++j) {
+    const int t = T - (Kc - 1) + j;  // position in x, negative -> old cache
+    if (t >= 0)
+      nv[j] = x[((int64_t)b * T + t) * ldx + c];
+    else
+      nv[j] = cache_in ? cache[((int64_t)b * (Kc - 1) + (Kc - 1 + t)) * C + c] : (T_)0;
+  }
+  for (int j = 0; j < Kc - 1; ++j) cache[((int64_t)b * (Kc - 1) + j) * C + c] = nv[j];
+}
+
+__global__ void conv1d_update_kernel(const int8_t* __restrict__ x, int64_t ldx, const float* __restrict__ w,
+                                     const float* __restrict__ bias, const float* __restrict__ s_in,
+                                     const float* __restrict__ s_out, int B, int C, int Kc,
+                                     int8_t* __restrict__ cache, int8_t* __restrict__ out, int64_t ldo) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (c >= C) return;
+  const float si = s_in[c];
+  int8_t* cr = cache + (int64_t)b * (Kc - 1) * C + c;
+  int8_t q[kMaxK];
+  for (int j = 0; j < Kc - 1; ++j) q[j] = cr[(int64_t)j * C];
+  q[Kc - 1] = x[(int64_t)b * ldx + c];
+  float acc = bias[c];
+  for (int j = 0; j < Kc; ++j) acc = __fadd_rn(acc, __fmul_rn(w[c * Kc + j], __fmul_rn((float)q[j], si)));
+  out[(int64_t)b * ldo + c] = quant8(silu_f(acc), s_out[c]);
+  for (int j = 0; j < Kc - 1; ++j) cr[(int64_t)j * C] = q[j + 1];
+}
+
+}  // namespace sq
+
+using namespace sq;
+
+extern "C" int sq_conv1d_int8(const int8_t* x, int64_t ldx, const float* w, const float* bias, const float* s_in,
+                              const float* s_out, int B, int T, int C, int Kc, int8_t* cache, int cache_in,
+                              int8_t* out, int64_t ldo, void* stream) {
+  SQ_REQUIRE(B >= 0 && T >= 0 && C > 0 && Kc >= 1 && Kc <= kMaxK, SQ_ERR_SHAPE,
+             "sq_conv1d_int8: bad shape (Kc=%d)", Kc);
+  if (B == 0 || T == 0) return SQ_OK;
+  cudaStream_t st = as_stream(stream);
+  dim3 g((C + 127) / 128, (T + kSeg - 1) / kSeg, B);
+  conv1d_prefill_kernel<int8_t, int8_t, true><<<g, 128, 0, st>>>(x, ldx, w, bias, s_in, s_out, B, T, C, Kc, cache,
+                                                                 cache_in, out, ldo);
+  if (Kc > 1) conv1d_cache_kernel<int8_t><<<dim3((C + 127) / 128, B), 128, 0, st>>>(x, ldx, B, T, C, Kc, cache, cache_in);
+  return check_launch("sq_conv1d_int8");
+}
+
+extern "C" int sq_conv1d_f32(const float* x, int64_t ldx, const float* w, const float* bias, int B, int T, int C,
+                             int Kc, float* cache, int cache_in, float* out, int64_t ldo, void* stream) {
+  SQ_REQUIRE(B >= 0 && T >= 0 && C > 0 && Kc >= 1 && Kc <= kMaxK, SQ_ERR_SHAPE, "sq_conv1d_f32: bad shape");
+  if (B == 0 || T == 0) return SQ_OK;
+  cudaStream_t st = as_stream(stream);
+  dim3 g((C + 127) / 128, (T + kSeg - 1) / kSeg, B);
+  conv1d_prefill_kernel<float, float, false><<<g, 128, 0, st>>>(x, ldx, w, bias, nullptr, nullptr, B, T, C, Kc, cache,
+                                                                cache_in, out, ldo);
+  if (Kc > 1) conv1d_cache_kernel<float><<<dim3((C + 127) / 128, B), 128, 0, st>>>(x, ldx, B, T, C, Kc, cache, cache_in);
+  return check_launch("sq_conv1d_f32");
+}
+
+extern "C" int sq_conv1d_update_int8(const int8_t* x, int64_t ldx, const float* w, const float* bias,
+                                     const float* s_in, const float* s_out, int B, int C, int Kc, int8_t* cache,
+                                     int8_t* out, int64_t ldo, void* stream) {
+  SQ_REQUIRE(B >= 0 && C > 0 && Kc >= 1 && Kc <= kMaxK, SQ_ERR_SHAPE, "sq_conv1d_update_int8: bad shape");
+  if (B == 0) return SQ_OK;
+  conv1d_update_kernel<<<dim3((C + 127) / 128, B), 128, 0, as_stream(stream)>>>(x, ldx, w, bias, s_in, s_out, B, C,
+                                                                                 Kc, cache, out, ldo);
+  return check_launch("sq_conv1d_update_int8");
+}

@@ -1,0 +1,182 @@
+// K1/K2 baseline: A8 GEMM on the legacy warp-level tensor path (mma.sync m16n8k32 s8),
+// used for shapes the tcgen05 kernel does not take and as the bring-up reference.
+//
+//   acc[m,n] = Σ_k a[m,k] · w8[n,k]        exact int32   (w8 = w4·sg for W4A8, LEDGER G11b)
+//   y[m,n]   = f32(acc) · alpha[n]         alpha = f32(s_ch[n] · s_a)  (fuse_scales)
+//   epilogue : i32 | f32 | int8 requant by col_scale[n] | residual add (sq_epilogue)
+//
+// Tile 64 tokens × 128 outputs × 64 K, 4 warps (each 64×32), register double-buffered
+// global loads, W4 nibbles expanded (×sg) to int8 on the way into shared memory.
+#include "common.cuh"
+
+namespace sq {
+
+constexpr int BM = 64, BN = 128, BK = 64, PADK = BK + 16;
+
+__device__ __forceinline__ uint32_t expand_w4x4(uint32_t packed16, int sg) {
+  // 2 packed bytes (4 nibbles) -> 4 int8 = nibble * sg
+  uint32_t out = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int v = ((int)(packed16 << (28 - 4 * i))) >> 28;
+    out |= ((uint32_t)(v * sg) & 0xFFu) << (8 * i);
+  }
+  return out;
+}
+
+__device__ __forceinline__ void mma_s8(int (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <bool W4>
+__global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* __restrict__ a, int64_t lda,
+                                                          const uint8_t* __restrict__ w,
+                                                          const int8_t* __restrict__ sg, int group,
+                                                          const float* __restrict__ alpha, int M, int N, int K,
+                                                          int epi, void* __restrict__ out, int64_t ldo,
+                                                          const float* __restrict__ col_scale) {
+  __shared__ __align__(16) int8_t As[BM][PADK];
+  __shared__ __align__(16) int8_t Ws[BN][PADK];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int ngroups = W4 ? K / group : 1;
+
+  int acc[4][4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0;
+
+  // per-thread load assignment
+  // A: 64 rows x 64 B = 256 x 16B chunks -> 2 per thread
+  // W: 128 rows; thread = row; W8: 64 B (4 chunks); W4: 32 B packed (2 chunks)
+  int4 ra[2], rw[4];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int c = tid + i * 128;
+      const int r = c >> 2, kk = (c & 3) * 16;
+      const int gm = m0 + r, gk = k0 + kk;
+      ra[i] = (gm < M && gk < K) ? *reinterpret_cast<const int4*>(a + (int64_t)gm * lda + gk) : make_int4(0, 0, 0, 0);
+    }
+    const int gn = n0 + tid;
+    if (W4) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int gk = k0 + i * 32;
+        rw[i] = (gn < N && gk < K) ? *reinterpret_cast<const int4*>(w + (int64_t)gn * (K / 2) + gk / 2)
+                                   : make_int4(0, 0, 0, 0);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int gk = k0 + i * 16;
+        rw[i] = (gn < N && gk < K) ? *reinterpret_cast<const int4*>(w + (int64_t)gn * K + gk) : make_int4(0, 0, 0, 0);
+      }
+    }
+  };
+  auto sstore = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int c = tid + i * 128;
+      *reinterpret_cast<int4*>(&As[c >> 2][(c & 3) * 16]) = ra[i];
+    }
+    if (W4) {
+      const int gn = n0 + tid;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int gk = k0 + i * 32;
+        const int s = (gn < N && gk < K) ? (int)sg[(int64_t)gn * ngroups + gk / group] : 0;
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(&rw[i]);
+        int4 o0, o1;
+        o0.x = expand_w4x4(p[0] & 0xFFFF, s);
+        o0.y = expand_w4x4(p[0] >> 16, s);
+        o0.z = expand_w4x4(p[1] & 0xFFFF, s);
+        o0.w = expand_w4x4(p[1] >> 16, s);
+        o1.x = expand_w4x4(p[2] & 0xFFFF, s);
+        o1.y = expand_w4x4(p[2] >> 16, s);
+        o1.z = expand_w4x4(p[3] & 0xFFFF, s);
+        o1.w = expand_w4x4(p[3] >> 16, s);
+        *reinterpret_cast<int4*>(&Ws[tid][i * 32]) = o0;
+        *reinterpret_cast<int4*>(&Ws[tid][i * 32 + 16]) = o1;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) *reinterpret_cast<int4*>(&Ws[tid][i * 16]) = rw[i];
+    }
+  };
+
+  const int g = lane >> 2, q = lane & 3;
+  gload(0);
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    __syncthreads();
+    sstore(k0);
+    __syncthreads();
+    if (k0 + BK < K) gload(k0 + BK);
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 32) {
+      uint32_t af[4][4], bf[4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = i * 16 + g;
+        af[i][0] = *reinterpret_cast<const uint32_t*>(&As[r][ks + q * 4]);
+        af[i][1] = *reinterpret_cast<const uint32_t*>(&As[r + 8][ks + q * 4]);
+        af[i][2] = *reinterpret_cast<const uint32_t*>(&As[r][ks + 16 + q * 4]);
+        af[i][3] = *reinterpret_cast<const uint32_t*>(&As[r + 8][ks + 16 + q * 4]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int nn = warp * 32 + j * 8 + g;
+        bf[j][0] = *reinterpret_cast<const uint32_t*>(&Ws[nn][ks + q * 4]);
+        bf[j][1] = *reinterpret_cast<const uint32_t*>(&Ws[nn][ks + 16 + q * 4]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mma_s8(acc[i][j], af[i], bf[j]);
+    }
+  }
+
+  // epilogue
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + i * 16 + g + (r >> 1) * 8;
+        const int n = n0 + warp * 32 + j * 8 + q * 2 + (r & 1);
+        if (m >= M || n >= N) continue;
+        const int v = acc[i][j][r];
+        const int64_t o = (int64_t)m * ldo + n;
+        if (epi == SQ_EPI_I32) {
+          reinterpret_cast<int32_t*>(out)[o] = v;
+        } else {
+          const float y = __fmul_rn((float)v, alpha[n]);
+          if (epi == SQ_EPI_F32)
+            reinterpret_cast<float*>(out)[o] = y;
+          else if (epi == SQ_EPI_QUANT)
+            reinterpret_cast<int8_t*>(out)[o] = quant8(y, col_scale[n]);
+          else
+            reinterpret_cast<float*>(out)[o] = __fadd_rn(reinterpret_cast<float*>(out)[o], y);
+        }
+      }
+}
+
+int gemm_a8_mma(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg, int group, bool w4,
+                const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
+                cudaStream_t st) {
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  if (w4)
+    gemm_a8_mma_kernel<true><<<grid, 128, 0, st>>>(a, lda, w, sg, group, alpha, M, N, K, epi, out, ldo, col_scale);
+  else
+    gemm_a8_mma_kernel<false><<<grid, 128, 0, st>>>(a, lda, w, sg, group, alpha, M, N, K, epi, out, ldo, col_scale);
+  return check_launch("gemm_a8_mma");
+}
+
+}  // namespace sq

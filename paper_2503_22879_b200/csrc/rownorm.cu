@@ -1,0 +1,202 @@
+// Row kernels: model pre-norm + quant, gated-norm + Hadamard + quant (K6), embedding,
+// argmax.  HBM-bound: one CTA per token row, the row staged once in shared memory.
+//
+// Parity (oracle/ssm_block.py rmsnorm, oracle/hadamard.py): the sum of squares is
+// accumulated in f64 (the oracle's np.mean over f64) and every later op is the same
+// IEEE f32 op in the same order, so codes match the oracle bit-for-bit except when the
+// f64 sum order moves the f32 mean across a rounding boundary (≤1 step, rare).
+// The FWHT runs the oracle's butterfly stages h = 1, 2, 4, … with identical f32
+// a+b / a-b, so the transform itself is bit-identical.
+#include "common.cuh"
+
+namespace sq {
+
+template <int NT>
+__device__ __forceinline__ double block_sum_d(double v, double* red) {
+  v = warp_sum_d(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double t = (l < NT / 32) ? red[l] : 0.0;
+    t = warp_sum_d(t);
+    if (l == 0) red[0] = t;
+  }
+  __syncthreads();
+  double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ float rms_factor(double ss, int D, float eps) {
+  float ms = (float)(ss / (double)D);
+  return __fdiv_rn(1.0f, sqrtf(__fadd_rn(ms, eps)));
+}
+
+template <int NT, bool QUANT>
+__global__ void __launch_bounds__(NT) rmsnorm_kernel(const float* __restrict__ x, int64_t ldx,
+                                                     const float* __restrict__ gamma, float eps, float s,
+                                                     int D, void* __restrict__ out, int64_t ldo) {
+  __shared__ double red[NT / 32];
+  const float* xr = x + (int64_t)blockIdx.x * ldx;
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < D; i += NT) {
+    float v = xr[i];
+    ss += (double)v * (double)v;
+  }
+  ss = block_sum_d<NT>(ss, red);
+  const float r = rms_factor(ss, D, eps);
+  for (int i = threadIdx.x; i < D; i += NT) {
+    float v = __fmul_rn(__fmul_rn(xr[i], r), gamma[i]);
+    if (QUANT)
+      reinterpret_cast<int8_t*>(out)[(int64_t)blockIdx.x * ldo + i] = quant8(v, s);
+    else
+      reinterpret_cast<float*>(out)[(int64_t)blockIdx.x * ldo + i] = v;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) gate_norm_had_quant_kernel(const float* __restrict__ y, int64_t ldy,
+                                                                 const float* __restrict__ gamma, float eps,
+                                                                 float s_y, int had_block, int D,
+                                                                 int8_t* __restrict__ out, int64_t ldo) {
+  extern __shared__ float buf[];
+  __shared__ double red[NT / 32];
+  const float* yr = y + (int64_t)blockIdx.x * ldy;
+  double ss = 0.0;
+  for (int i = threadIdx.x * 4; i < D; i += NT * 4) {
+    float4 v = *reinterpret_cast<const float4*>(yr + i);
+    *reinterpret_cast<float4*>(buf + i) = v;
+    ss += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+  }
+  ss = block_sum_d<NT>(ss, red);
+  const float r = rms_factor(ss, D, eps);
+  for (int i = threadIdx.x; i < D; i += NT) buf[i] = __fmul_rn(__fmul_rn(buf[i], r), gamma[i]);
+  __syncthreads();
+  // Sylvester butterflies within each power-of-two block (LEDGER G9).
+  for (int h = 1; h < had_block; h <<= 1) {
+    for (int idx = threadIdx.x; idx < D / 2; idx += NT) {
+      const int i = (idx / h) * 2 * h + (idx % h);
+      const float a = buf[i], b = buf[i + h];
+      buf[i] = __fadd_rn(a, b);
+      buf[i + h] = __fsub_rn(a, b);
+    }
+    __syncthreads();
+  }
+  int8_t* o = out + (int64_t)blockIdx.x * ldo;
+  for (int i = threadIdx.x * 4; i < D; i += NT * 4) {
+    char4 q;
+    q.x = quant8(buf[i], s_y);
+    q.y = quant8(buf[i + 1], s_y);
+    q.z = quant8(buf[i + 2], s_y);
+    q.w = quant8(buf[i + 3], s_y);
+    *reinterpret_cast<char4*>(o + i) = q;
+  }
+}
+
+__global__ void quantize_kernel(const float* __restrict__ x, int64_t ldx, float s, int D, int8_t* __restrict__ out,
+                                int64_t ldo) {
+  const float* r = x + (int64_t)blockIdx.x * ldx;
+  int8_t* o = out + (int64_t)blockIdx.x * ldo;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) o[i] = quant8(r[i], s);
+}
+
+__global__ void embed_kernel(const int8_t* __restrict__ codes, const float* __restrict__ rs,
+                             const int32_t* __restrict__ tok, int D, float* __restrict__ h) {
+  const int m = blockIdx.x;
+  const int t = tok[m];
+  const float s = rs[t];
+  for (int i = threadIdx.x; i < D; i += blockDim.x)
+    h[(int64_t)m * D + i] = __fmul_rn((float)codes[(int64_t)t * D + i], s);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lg, int64_t ld, int N,
+                                                    int32_t* __restrict__ tok) {
+  __shared__ float bv[NT / 32];
+  __shared__ int bi[NT / 32];
+  const float* r = lg + (int64_t)blockIdx.x * ld;
+  float best = -INFINITY;
+  int bidx = 0x7fffffff;
+  for (int i = threadIdx.x; i < N; i += NT) {
+    float v = r[i];
+    if (v > best) { best = v; bidx = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { bv[w] = best; bi[w] = bidx; }
+  __syncthreads();
+  if (w == 0) {
+    best = l < NT / 32 ? bv[l] : -INFINITY;
+    bidx = l < NT / 32 ? bi[l] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (ov > best || (ov == best && oi < bidx)) { best = ov; bidx = oi; }
+    }
+    if (l == 0) tok[blockIdx.x] = bidx;
+  }
+}
+
+}  // namespace sq
+
+using namespace sq;
+
+extern "C" int sq_rmsnorm_quant(const float* x, int64_t ldx, const float* gamma, float eps, float s, int M,
+                                int D, int8_t* out, int64_t ldo, void* stream) {
+  SQ_REQUIRE(M >= 0 && D > 0 && s > 0.f, SQ_ERR_SHAPE, "sq_rmsnorm_quant: bad M/D/s");
+  if (M == 0) return SQ_OK;
+  rmsnorm_kernel<256, true><<<M, 256, 0, as_stream(stream)>>>(x, ldx, gamma, eps, s, D, out, ldo);
+  return check_launch("sq_rmsnorm_quant");
+}
+
+extern "C" int sq_rmsnorm_f32(const float* x, int64_t ldx, const float* gamma, float eps, int M, int D,
+                              float* out, int64_t ldo, void* stream) {
+  SQ_REQUIRE(M >= 0 && D > 0, SQ_ERR_SHAPE, "sq_rmsnorm_f32: bad M/D");
+  if (M == 0) return SQ_OK;
+  rmsnorm_kernel<256, false><<<M, 256, 0, as_stream(stream)>>>(x, ldx, gamma, eps, 1.f, D, out, ldo);
+  return check_launch("sq_rmsnorm_f32");
+}
+
+extern "C" int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* gamma, float eps, float s_y,
+                                      int hadamard, int M, int D, int8_t* out, int64_t ldo, void* stream) {
+  SQ_REQUIRE(M >= 0 && D > 0 && D % 4 == 0 && D <= 16384 && ldy % 4 == 0 && ldo % 4 == 0, SQ_ERR_SHAPE,
+             "sq_gate_norm_had_quant: D must be a multiple of 4 and <= 16384 (D=%d)", D);
+  SQ_REQUIRE(s_y > 0.f, SQ_ERR_ARG, "sq_gate_norm_had_quant: s_y must be > 0");
+  if (M == 0) return SQ_OK;
+  const int blk = hadamard ? (D & -D) : 1;
+  const size_t smem = (size_t)D * sizeof(float);
+  auto k = gate_norm_had_quant_kernel<512>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k<<<M, 512, smem, as_stream(stream)>>>(y, ldy, gamma, eps, s_y, blk, D, out, ldo);
+  return check_launch("sq_gate_norm_had_quant");
+}
+
+extern "C" int sq_quantize_f32(const float* x, int64_t ldx, float s, int M, int D, int8_t* out, int64_t ldo,
+                               void* stream) {
+  SQ_REQUIRE(M >= 0 && D > 0 && s > 0.f, SQ_ERR_SHAPE, "sq_quantize_f32: bad shape/scale");
+  if (M == 0) return SQ_OK;
+  quantize_kernel<<<M, 256, 0, as_stream(stream)>>>(x, ldx, s, D, out, ldo);
+  return check_launch("sq_quantize_f32");
+}
+
+extern "C" int sq_embed_int8(const int8_t* codes, const float* row_scale, const int32_t* tok, int M, int D,
+                             float* h, void* stream) {
+  SQ_REQUIRE(M >= 0 && D > 0, SQ_ERR_SHAPE, "sq_embed_int8: bad shape");
+  if (M == 0) return SQ_OK;
+  embed_kernel<<<M, 256, 0, as_stream(stream)>>>(codes, row_scale, tok, D, h);
+  return check_launch("sq_embed_int8");
+}
+
+extern "C" int sq_argmax_f32(const float* logits, int64_t ld, int M, int N, int32_t* tok, void* stream) {
+  SQ_REQUIRE(M >= 0 && N > 0, SQ_ERR_SHAPE, "sq_argmax_f32: bad shape");
+  if (M == 0) return SQ_OK;
+  argmax_kernel<1024><<<M, 1024, 0, as_stream(stream)>>>(logits, ld, N, tok);
+  return check_launch("sq_argmax_f32");
+}

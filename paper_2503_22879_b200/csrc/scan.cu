@@ -1,0 +1,234 @@
+// K7/K8/K9 sequential-recurrence kernels (reference semantics: Eq. 2,
+// SPEC.md:340-341 int8 cached state):
+//   * sq_state_update_int8  — Mamba2 decode step (T=1); HBM-bound on the int8 state
+//   * sq_ssd_scan_int8      — Mamba2 prefill, token-sequential over T (the fp32 state
+//                             lives in registers for the whole sequence)
+//   * sq_ssd_scan_f32       — W4A16 float path (fp32 state)
+//   * sq_selective_scan_int8 — Mamba1 (state [d_inner x N], N=16)
+//
+// Mamba2 mapping: one CTA per (sequence, head); thread t owns state row p = t / TPR and a
+// contiguous run of NPT = N / TPR state columns, so the int8 state row is read and written
+// with 16-byte vector accesses, fully coalesced per warp (K9: "vectorised, coalesced").
+// Per token:  Δ = softplus(f32(Δq)·sΔ + dt_bias[h]);  Ȧ = exp(Δ·A[h]);
+//   h[p,n] = Ȧ·h[p,n] + (Δ·x̂[p])·B̂[n]   (unfused f32, oracle order)
+//   y[p]   = Σ_n h[p,n]·Ĉ[n] + D[h]·x̂[p];  y ← y·silu(ẑ[p])
+// The cached state is requantised once per call: q = rint(h / s_h[h,p]).
+#include "common.cuh"
+
+namespace sq {
+
+template <typename TQ>
+struct Deq;
+template <>
+struct Deq<int8_t> {
+  __device__ static float f(int8_t q, float s) { return __fmul_rn((float)q, s); }
+};
+template <>
+struct Deq<float> {
+  __device__ static float f(float q, float) { return q; }
+};
+
+template <typename TQ, int NPT>
+__device__ __forceinline__ void load_vec(const TQ* p, float s, float* out) {
+  if constexpr (sizeof(TQ) == 1) {
+#pragma unroll
+    for (int i = 0; i < NPT; i += 16) {
+      int4 v = *reinterpret_cast<const int4*>(p + i);
+      const int8_t* b = reinterpret_cast<const int8_t*>(&v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) out[i + j] = __fmul_rn((float)b[j], s);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NPT; i += 4) {
+      float4 v = *reinterpret_cast<const float4*>(p + i);
+      out[i] = v.x; out[i + 1] = v.y; out[i + 2] = v.z; out[i + 3] = v.w;
+    }
+  }
+}
+
+template <typename TQ, int NPT>
+__device__ __forceinline__ void store_state(TQ* p, float s, const float* h) {
+  if constexpr (sizeof(TQ) == 1) {
+#pragma unroll
+    for (int i = 0; i < NPT; i += 16) {
+      int4 v;
+      int8_t* b = reinterpret_cast<int8_t*>(&v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) b[j] = quant8(h[i + j], s);
+      *reinterpret_cast<int4*>(p + i) = v;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NPT; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+  }
+}
+
+template <typename TQ, int NPT>
+__global__ void __launch_bounds__(256) mamba2_scan_kernel(sq_mamba2_params p, int T, const TQ* __restrict__ x,
+                                                         int64_t ldx, const TQ* __restrict__ Bm,
+                                                         const TQ* __restrict__ Cm, int64_t ldbc,
+                                                         const TQ* __restrict__ dt, int64_t lddt,
+                                                         const TQ* __restrict__ z, int64_t ldz, TQ* __restrict__ state,
+                                                         int state_in, float* __restrict__ y, int64_t ldy) {
+  constexpr bool Q = sizeof(TQ) == 1;
+  const int h = blockIdx.x;
+  const int b = blockIdx.y;
+  const int P = p.head_dim, N = p.d_state;
+  const int TPR = N / NPT;
+  const int row = threadIdx.x / TPR;
+  const int n0 = (threadIdx.x % TPR) * NPT;
+  const int g = p.head_group[h];
+  const int ch = h * P + row;
+  const float sx = Q ? p.s_x[ch] : 1.f;
+  const float sh = Q ? p.s_h[ch] : 1.f;
+  const float sB = Q ? p.s_B[g] : 1.f;
+  const float sC = Q ? p.s_C[g] : 1.f;
+  const float A = p.A[h], Dh = p.D[h], dtb = p.dt_bias[h];
+  TQ* st = state + (((int64_t)b * p.n_heads + h) * P + row) * N + n0;
+  float hs[NPT];
+  if (state_in) {
+    load_vec<TQ, NPT>(st, sh, hs);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) hs[i] = 0.f;
+  }
+  for (int t = 0; t < T; ++t) {
+    const int64_t tok = (int64_t)b * T + t;
+    const float draw = Q ? __fadd_rn(__fmul_rn((float)dt[tok * lddt + h], p.s_dt), dtb)
+                         : __fadd_rn((float)dt[tok * lddt + h], dtb);
+    const float delta = softplus_f(draw);
+    const float dA = expf(__fmul_rn(delta, A));
+    const float xh = Deq<TQ>::f(x[tok * ldx + ch], sx);
+    const float dtx = __fmul_rn(delta, xh);
+    float bv[NPT], cv[NPT];
+    load_vec<TQ, NPT>(Bm + tok * ldbc + g * N + n0, sB, bv);
+    load_vec<TQ, NPT>(Cm + tok * ldbc + g * N + n0, sC, cv);
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) {
+      hs[i] = __fadd_rn(__fmul_rn(dA, hs[i]), __fmul_rn(dtx, bv[i]));
+      acc = fmaf(hs[i], cv[i], acc);
+    }
+    for (int o = TPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x % TPR) == 0) {
+      float yv = __fadd_rn(acc, __fmul_rn(Dh, xh));
+      const float zv = Q ? __fmul_rn((float)z[tok * ldz + ch], p.s_z) : (float)z[tok * ldz + ch];
+      y[tok * ldy + ch] = __fmul_rn(yv, silu_f(zv));
+    }
+  }
+  store_state<TQ, NPT>(st, sh, hs);
+}
+
+template <typename TQ>
+static int launch_mamba2(const sq_mamba2_params* p, int B, int T, const TQ* x, int64_t ldx, const TQ* Bm,
+                         const TQ* Cm, int64_t ldbc, const TQ* dt, int64_t lddt, const TQ* z, int64_t ldz,
+                         TQ* state, int state_in, float* y, int64_t ldy, cudaStream_t st, const char* name) {
+  SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "%s: bad args", name);
+  const int P = p->head_dim, N = p->d_state;
+  SQ_REQUIRE(N % 16 == 0 && N <= 256 && P >= 1, SQ_ERR_SHAPE, "%s: d_state must be a multiple of 16 <= 256", name);
+  const int TPR = (N + 63) / 64;
+  const int NPT = N / TPR;
+  SQ_REQUIRE(P * TPR <= 256 && (TPR & (TPR - 1)) == 0 && (NPT == 16 || NPT == 32 || NPT == 64), SQ_ERR_SHAPE,
+             "%s: unsupported head_dim/d_state (P=%d N=%d)", name, P, N);
+  SQ_REQUIRE(p->n_heads % p->n_groups == 0, SQ_ERR_SHAPE, "%s: heads/groups", name);
+  if (B == 0 || T == 0) return SQ_OK;
+  dim3 grid(p->n_heads, B), block(P * TPR);
+#define SQ_M2(NPTV)                                                                                           \
+  mamba2_scan_kernel<TQ, NPTV><<<grid, block, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, \
+                                                      state_in, y, ldy)
+  if (NPT == 16) SQ_M2(16);
+  else if (NPT == 32) SQ_M2(32);
+  else SQ_M2(64);
+#undef SQ_M2
+  return check_launch(name);
+}
+
+// Mamba1: one thread per (sequence, channel); N state columns in registers.
+template <int N>
+__global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, int B, int T,
+                                                         const int8_t* __restrict__ x, int64_t ldx,
+                                                         const int8_t* __restrict__ dt, int64_t lddt,
+                                                         const int8_t* __restrict__ BC, int64_t ldbc,
+                                                         const int8_t* __restrict__ z, int64_t ldz,
+                                                         int8_t* __restrict__ state, int state_in,
+                                                         float* __restrict__ y, int64_t ldy) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (c >= p.d_inner) return;
+  const float sx = p.s_x[c], sh = p.s_h[c], Dc = p.D[c], dtb = p.dt_bias[c];
+  float A[N], hs[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) A[n] = p.A[c * N + n];
+  int8_t* st = state + ((int64_t)b * p.d_inner + c) * N;
+  if (state_in) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) hs[n] = __fmul_rn((float)st[n], sh);
+  } else {
+#pragma unroll
+    for (int n = 0; n < N; ++n) hs[n] = 0.f;
+  }
+  for (int t = 0; t < T; ++t) {
+    const int64_t tok = (int64_t)b * T + t;
+    const float delta = softplus_f(__fadd_rn(__fmul_rn((float)dt[tok * lddt + c], p.s_dt), dtb));
+    const float xh = __fmul_rn((float)x[tok * ldx + c], sx);
+    const float dtx = __fmul_rn(delta, xh);
+    const int8_t* bc = BC + tok * ldbc;
+    float acc = 0.f;
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float dA = expf(__fmul_rn(delta, A[n]));
+      const float bn = __fmul_rn((float)bc[n], p.s_B);
+      const float cn = __fmul_rn((float)bc[N + n], p.s_C);
+      hs[n] = __fadd_rn(__fmul_rn(dA, hs[n]), __fmul_rn(dtx, bn));
+      acc = fmaf(hs[n], cn, acc);
+    }
+    const float yv = __fadd_rn(acc, __fmul_rn(Dc, xh));
+    const float zv = __fmul_rn((float)z[tok * ldz + c], p.s_z);
+    y[tok * ldy + c] = __fmul_rn(yv, silu_f(zv));
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) st[n] = quant8(hs[n], sh);
+}
+
+}  // namespace sq
+
+using namespace sq;
+
+extern "C" int sq_ssd_scan_int8(const sq_mamba2_params* p, int B, int T, const int8_t* x, int64_t ldx,
+                                const int8_t* Bm, const int8_t* Cm, int64_t ldbc, const int8_t* dt, int64_t lddt,
+                                const int8_t* z, int64_t ldz, int8_t* state, int state_in, float* y, int64_t ldy,
+                                int chunk, void* stream) {
+  (void)chunk;
+  return launch_mamba2<int8_t>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
+                               as_stream(stream), "sq_ssd_scan_int8");
+}
+
+extern "C" int sq_state_update_int8(const sq_mamba2_params* p, int B, const int8_t* x, int64_t ldx,
+                                    const int8_t* Bm, const int8_t* Cm, int64_t ldbc, const int8_t* dt,
+                                    int64_t lddt, const int8_t* z, int64_t ldz, int8_t* state, float* y,
+                                    int64_t ldy, void* stream) {
+  return launch_mamba2<int8_t>(p, B, 1, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, 1, y, ldy,
+                               as_stream(stream), "sq_state_update_int8");
+}
+
+extern "C" int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T, const float* x, int64_t ldx,
+                               const float* Bm, const float* Cm, int64_t ldbc, const float* dt, int64_t lddt,
+                               const float* z, int64_t ldz, float* state, int state_in, float* y, int64_t ldy,
+                               void* stream) {
+  return launch_mamba2<float>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
+                              as_stream(stream), "sq_ssd_scan_f32");
+}
+
+extern "C" int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T, const int8_t* x, int64_t ldx,
+                                      const int8_t* dt, int64_t lddt, const int8_t* BC, int64_t ldbc,
+                                      const int8_t* z, int64_t ldz, int8_t* state, int state_in, float* y,
+                                      int64_t ldy, void* stream) {
+  SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_selective_scan_int8: bad args");
+  SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan_int8: d_state must be 16 (got %d)", p->d_state);
+  if (B == 0 || T == 0) return SQ_OK;
+  dim3 grid((p->d_inner + 127) / 128, B);
+  mamba1_scan_kernel<16><<<grid, 128, 0, as_stream(stream)>>>(*p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz, state,
+                                                              state_in, y, ldy);
+  return check_launch("sq_selective_scan_int8");
+}

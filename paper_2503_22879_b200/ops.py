@@ -1,0 +1,279 @@
+"""Torch-tensor wrappers over the C-ABI (one function per `sq_*` entry point).
+
+Every wrapper validates device/dtype/layout, passes raw device pointers plus the current
+torch stream, and maps a non-zero status to the ``errors`` hierarchy.  There is no CPU
+path: a tensor that is not on a CUDA device raises ``LayoutError``.
+2-D operands may be row-strided views (``t[:, a:b]``); their last dim must be dense.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .errors import LayoutError, ShapeError, status_error
+
+EPI_I32, EPI_F32, EPI_QUANT, EPI_RESID = 0, 1, 2, 3
+
+
+def lib():
+    return _lib.load()
+
+
+LAUNCH_COUNTER = [0, 0]   # [kernel launches issued through this module, launches in last captured step]
+
+
+def _check(rc: int):
+    LAUNCH_COUNTER[0] += 1
+    if rc != 0:
+        raise status_error(rc, _lib.last_error())
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev(t: torch.Tensor, dtype, name, dims=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise LayoutError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise LayoutError(f"{name} must be {dtype}, got {t.dtype}")
+    if dims is not None and t.dim() != dims:
+        raise ShapeError(f"{name} must be {dims}-D, got {tuple(t.shape)}")
+    if t.dim() >= 1 and t.numel() > 0 and t.stride(-1) != 1:
+        raise LayoutError(f"{name} last dim must be contiguous")
+    if t.dim() > 2 and not t.is_contiguous():
+        raise LayoutError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _ld(t):
+    return t.stride(0) if t.dim() >= 2 else t.shape[-1]
+
+
+def _opt(t):
+    return 0 if t is None else t.data_ptr()
+
+
+# ------------------------------------------------------------------ weights
+def w4_bytes(N: int, K: int) -> int:
+    return int(lib().sq_w4_bytes(N, K))
+
+
+def repack_w4(u4packed: torch.Tensor, N: int, K: int) -> torch.Tensor:
+    _dev(u4packed, torch.uint8, "u4packed")
+    if u4packed.numel() != N * K // 2:
+        raise ShapeError("u4packed must hold N*K/2 bytes")
+    out = torch.empty(w4_bytes(N, K), dtype=torch.uint8, device=u4packed.device)
+    _check(lib().sq_repack_w4(u4packed.data_ptr(), N, K, out.data_ptr(), _stream()))
+    return out
+
+
+def unpack_w4(w: torch.Tensor, N: int, K: int) -> torch.Tensor:
+    _dev(w, torch.uint8, "w4")
+    out = torch.empty((N, K // 2), dtype=torch.uint8, device=w.device)
+    _check(lib().sq_unpack_w4(w.data_ptr(), N, K, out.data_ptr(), _stream()))
+    return out
+
+
+# ------------------------------------------------------------------ row ops
+def rmsnorm_quant(x, gamma, eps, s, out=None):
+    _dev(x, torch.float32, "x", 2)
+    _dev(gamma, torch.float32, "gamma", 1)
+    M, D = x.shape
+    out = torch.empty((M, D), dtype=torch.int8, device=x.device) if out is None else out
+    _dev(out, torch.int8, "out", 2)
+    _check(lib().sq_rmsnorm_quant(x.data_ptr(), _ld(x), gamma.data_ptr(), float(eps), float(s), M, D,
+                                  out.data_ptr(), _ld(out), _stream()))
+    return out
+
+
+def rmsnorm_f32(x, gamma, eps, out=None):
+    _dev(x, torch.float32, "x", 2)
+    M, D = x.shape
+    out = torch.empty((M, D), dtype=torch.float32, device=x.device) if out is None else out
+    _dev(out, torch.float32, "out", 2)
+    _check(lib().sq_rmsnorm_f32(x.data_ptr(), _ld(x), gamma.data_ptr(), float(eps), M, D, out.data_ptr(),
+                                _ld(out), _stream()))
+    return out
+
+
+def quantize_f32(x, s, out=None):
+    _dev(x, torch.float32, "x", 2)
+    M, D = x.shape
+    out = torch.empty((M, D), dtype=torch.int8, device=x.device) if out is None else out
+    _dev(out, torch.int8, "out", 2)
+    _check(lib().sq_quantize_f32(x.data_ptr(), _ld(x), float(s), M, D, out.data_ptr(), _ld(out), _stream()))
+    return out
+
+
+def embed_int8(codes, row_scale, tok, out=None):
+    _dev(codes, torch.int8, "codes", 2)
+    _dev(tok, torch.int32, "tok", 1)
+    M, D = tok.shape[0], codes.shape[1]
+    out = torch.empty((M, D), dtype=torch.float32, device=codes.device) if out is None else out
+    _check(lib().sq_embed_int8(codes.data_ptr(), row_scale.data_ptr(), tok.data_ptr(), M, D, out.data_ptr(),
+                               _stream()))
+    return out
+
+
+def argmax(logits, out=None):
+    _dev(logits, torch.float32, "logits", 2)
+    M, N = logits.shape
+    out = torch.empty(M, dtype=torch.int32, device=logits.device) if out is None else out
+    _check(lib().sq_argmax_f32(logits.data_ptr(), _ld(logits), M, N, out.data_ptr(), _stream()))
+    return out
+
+
+def gate_norm_had_quant(y, gamma, eps, s_y, hadamard=True, out=None):
+    _dev(y, torch.float32, "y", 2)
+    M, D = y.shape
+    out = torch.empty((M, D), dtype=torch.int8, device=y.device) if out is None else out
+    _dev(out, torch.int8, "out", 2)
+    _check(lib().sq_gate_norm_had_quant(y.data_ptr(), _ld(y), gamma.data_ptr(), float(eps), float(s_y),
+                                        int(bool(hadamard)), M, D, out.data_ptr(), _ld(out), _stream()))
+    return out
+
+
+# ------------------------------------------------------------------ projections
+_OUT_DTYPE = {EPI_I32: torch.int32, EPI_F32: torch.float32, EPI_QUANT: torch.int8, EPI_RESID: torch.float32}
+
+
+def _gemm_out(a, N, epi, out):
+    M = a.shape[0]
+    if out is None:
+        if epi == EPI_RESID:
+            raise ValueError("EPI_RESID needs the residual tensor as `out`")
+        out = torch.empty((M, N), dtype=_OUT_DTYPE[epi], device=a.device)
+    _dev(out, _OUT_DTYPE[epi], "out", 2)
+    if out.shape[0] != M or out.shape[1] != N:
+        raise ShapeError(f"out must be [{M}x{N}], got {tuple(out.shape)}")
+    return out
+
+
+def gemm_w8a8(a, w, alpha, epi=EPI_F32, out=None, col_scale=None):
+    _dev(a, torch.int8, "a", 2)
+    _dev(w, torch.int8, "w", 2)
+    M, K = a.shape
+    N = w.shape[0]
+    if w.shape[1] != K:
+        raise ShapeError(f"w must be [N x {K}]")
+    out = _gemm_out(a, N, epi, out)
+    _check(lib().sq_gemm_w8a8(a.data_ptr(), _ld(a), w.data_ptr(), alpha.data_ptr(), M, N, K, epi, out.data_ptr(),
+                              _ld(out), _opt(col_scale), _stream()))
+    return out
+
+
+def gemm_w4a8(a, w4, sg, group, alpha, N, epi=EPI_F32, out=None, col_scale=None):
+    _dev(a, torch.int8, "a", 2)
+    _dev(w4, torch.uint8, "w4")
+    _dev(sg, torch.int8, "sg", 2)
+    M, K = a.shape
+    if sg.shape != (N, K // group):
+        raise LayoutError(f"sg must be [{N} x {K // group}]")
+    out = _gemm_out(a, N, epi, out)
+    _check(lib().sq_gemm_w4a8(a.data_ptr(), _ld(a), w4.data_ptr(), sg.data_ptr(), group, alpha.data_ptr(), M, N, K,
+                              epi, out.data_ptr(), _ld(out), _opt(col_scale), _stream()))
+    return out
+
+
+def gemv_w4a16(x, w4, s_group, group, N, out=None, resid=False):
+    _dev(x, torch.float32, "x", 2)
+    _dev(w4, torch.uint8, "w4")
+    M, K = x.shape
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=x.device)
+    _dev(out, torch.float32, "out", 2)
+    _check(lib().sq_gemv_w4a16(x.data_ptr(), _ld(x), w4.data_ptr(), s_group.data_ptr(), group, M, N, K,
+                               out.data_ptr(), _ld(out), int(bool(resid)), _stream()))
+    return out
+
+
+# ------------------------------------------------------------------ conv
+def conv1d_int8(x, w, bias, s_in, s_out, B, T, cache, cache_in=False, out=None):
+    _dev(x, torch.int8, "x", 2)
+    _dev(cache, torch.int8, "cache")
+    C_, Kc = w.shape
+    out = torch.empty((B * T, C_), dtype=torch.int8, device=x.device) if out is None else out
+    _check(lib().sq_conv1d_int8(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), s_in.data_ptr(),
+                                s_out.data_ptr(), B, T, C_, Kc, cache.data_ptr(), int(bool(cache_in)),
+                                out.data_ptr(), _ld(out), _stream()))
+    return out
+
+
+def conv1d_update_int8(x, w, bias, s_in, s_out, cache, out=None):
+    _dev(x, torch.int8, "x", 2)
+    _dev(cache, torch.int8, "cache")
+    B = x.shape[0]
+    C_, Kc = w.shape
+    out = torch.empty((B, C_), dtype=torch.int8, device=x.device) if out is None else out
+    _check(lib().sq_conv1d_update_int8(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), s_in.data_ptr(),
+                                       s_out.data_ptr(), B, C_, Kc, cache.data_ptr(), out.data_ptr(), _ld(out),
+                                       _stream()))
+    return out
+
+
+def conv1d_f32(x, w, bias, B, T, cache, cache_in=False, out=None):
+    _dev(x, torch.float32, "x", 2)
+    C_, Kc = w.shape
+    out = torch.empty((B * T, C_), dtype=torch.float32, device=x.device) if out is None else out
+    _check(lib().sq_conv1d_f32(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), B, T, C_, Kc, cache.data_ptr(),
+                               int(bool(cache_in)), out.data_ptr(), _ld(out), _stream()))
+    return out
+
+
+# ------------------------------------------------------------------ scans
+def mamba2_params(n_heads, head_dim, d_state, n_groups, head_group, A, D, dt_bias, s_dt=1.0, s_z=1.0,
+                  s_x=None, s_B=None, s_C=None, s_h=None) -> _lib.Mamba2Params:
+    """Build the parameter struct; keeps no reference to the tensors (caller owns them)."""
+    return _lib.Mamba2Params(n_heads, head_dim, d_state, n_groups, head_group.data_ptr(), A.data_ptr(),
+                             D.data_ptr(), dt_bias.data_ptr(), float(s_dt), float(s_z), _opt(s_x), _opt(s_B),
+                             _opt(s_C), _opt(s_h))
+
+
+def mamba1_params(d_inner, d_state, A, D, dt_bias, s_dt, s_z, s_B, s_C, s_x, s_h) -> _lib.Mamba1Params:
+    return _lib.Mamba1Params(d_inner, d_state, A.data_ptr(), D.data_ptr(), dt_bias.data_ptr(), float(s_dt),
+                             float(s_z), float(s_B), float(s_C), s_x.data_ptr(), s_h.data_ptr())
+
+
+def ssd_scan_int8(p, B, T, x, Bm, Cm, dt, z, state, state_in, y, chunk=256):
+    for n, t in (("x", x), ("B", Bm), ("C", Cm), ("dt", dt), ("z", z)):
+        _dev(t, torch.int8, n, 2)
+    _dev(state, torch.int8, "state")
+    _dev(y, torch.float32, "y", 2)
+    _check(lib().sq_ssd_scan_int8(C.byref(p), B, T, x.data_ptr(), _ld(x), Bm.data_ptr(), Cm.data_ptr(), _ld(Bm),
+                                  dt.data_ptr(), _ld(dt), z.data_ptr(), _ld(z), state.data_ptr(),
+                                  int(bool(state_in)), y.data_ptr(), _ld(y), int(chunk), _stream()))
+    return y
+
+
+def state_update_int8(p, B, x, Bm, Cm, dt, z, state, y):
+    for n, t in (("x", x), ("B", Bm), ("C", Cm), ("dt", dt), ("z", z)):
+        _dev(t, torch.int8, n, 2)
+    _dev(state, torch.int8, "state")
+    _dev(y, torch.float32, "y", 2)
+    _check(lib().sq_state_update_int8(C.byref(p), B, x.data_ptr(), _ld(x), Bm.data_ptr(), Cm.data_ptr(), _ld(Bm),
+                                      dt.data_ptr(), _ld(dt), z.data_ptr(), _ld(z), state.data_ptr(), y.data_ptr(),
+                                      _ld(y), _stream()))
+    return y
+
+
+def ssd_scan_f32(p, B, T, x, Bm, Cm, dt, z, state, state_in, y):
+    for n, t in (("x", x), ("B", Bm), ("C", Cm), ("dt", dt), ("z", z)):
+        _dev(t, torch.float32, n, 2)
+    _dev(state, torch.float32, "state")
+    _check(lib().sq_ssd_scan_f32(C.byref(p), B, T, x.data_ptr(), _ld(x), Bm.data_ptr(), Cm.data_ptr(), _ld(Bm),
+                                 dt.data_ptr(), _ld(dt), z.data_ptr(), _ld(z), state.data_ptr(), int(bool(state_in)),
+                                 y.data_ptr(), _ld(y), _stream()))
+    return y
+
+
+def selective_scan_int8(p, B, T, x, dt, BC, z, state, state_in, y):
+    for n, t in (("x", x), ("dt", dt), ("BC", BC), ("z", z)):
+        _dev(t, torch.int8, n, 2)
+    _dev(state, torch.int8, "state")
+    _check(lib().sq_selective_scan_int8(C.byref(p), B, T, x.data_ptr(), _ld(x), dt.data_ptr(), _ld(dt),
+                                        BC.data_ptr(), _ld(BC), z.data_ptr(), _ld(z), state.data_ptr(),
+                                        int(bool(state_in)), y.data_ptr(), _ld(y), _stream()))
+    return y

@@ -1,0 +1,163 @@
+"""Synthetic random-init quantized models at the BASELINE shapes (no checkpoints exist
+offline; BASELINE.json `data: synthetic`).
+
+* ``random_qblock``  — host QBlock with analytic scales (parity tests at full shapes).
+* ``device_qblock`` / ``synthetic_lm`` — weights generated directly in HBM (random int4
+  bytes are valid nibble pairs), for the bench: a 56-layer 8B-shaped model is built in
+  seconds without a host round trip.
+Scales are chosen so every activation site uses most of its int8 range.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .ssm_block import DeviceBlock, Dims, QBlock, QLinear
+from .tensor import make_rng
+
+U_STD_CODES = 127.0 / 4.0     # N(0,1) inputs quantized with s = 4/127
+
+
+def _slice_scales(d: Dims):
+    s = np.float32(4.0 / 127)
+    return s
+
+
+def _analytic_qlinear(r, n, k, kind, group, out_std, in_code_std):
+    group = min(group, k)
+    if kind == "w8":
+        codes = r.integers(-127, 128, (n, k)).astype(np.int8)
+        rms = np.sqrt((codes.astype(np.float64) ** 2).mean(axis=1))
+        s_ch = (out_std / (np.sqrt(k) * in_code_std * rms)).astype(np.float32)
+        return QLinear("w8", codes, s_ch=s_ch, sg=np.ones((n, 1), np.int8), group=k)
+    codes = r.integers(-8, 8, (n, k)).astype(np.int8)
+    if kind == "w4a8":
+        sg = r.integers(1, 16, (n, k // group)).astype(np.int8)
+        w8 = codes.astype(np.float64).reshape(n, k // group, group) * sg[:, :, None]
+        rms = np.sqrt((w8 ** 2).reshape(n, k).mean(axis=1))
+        s_ch = (out_std / (np.sqrt(k) * in_code_std * rms)).astype(np.float32)
+        return QLinear("w4a8", codes, s_ch=s_ch, sg=sg, group=group)
+    s_group = r.uniform(0.5, 1.5, (n, k // group)).astype(np.float32) * np.float32(out_std / (np.sqrt(k) * 4.6))
+    return QLinear("w4a16", codes, s_group=s_group.astype(np.float32), group=group)
+
+
+def random_qblock(d: Dims, profile: str, seed: int = 0) -> QBlock:
+    r = make_rng(seed, 11, 0)
+    kind = {"W8A8": "w8", "W4A8": "w4a8", "W4A16": "w4a16"}[profile]
+    di = d.d_inner
+    s = np.float32(4.0 / 127)
+    inp = _analytic_qlinear(r, d.in_proj_out, d.d_model, kind, 128, 1.0, U_STD_CODES)
+    out = _analytic_qlinear(r, d.d_model, di, kind, 128, 0.1, 127.0 / 4.0)
+    C = d.conv_dim
+    K = d.conv_kernel
+    conv_w = (r.standard_normal((C, K)) * 0.5 / np.sqrt(K)).astype(np.float32)
+    conv_b = (r.standard_normal(C) * 0.05).astype(np.float32)
+    nd = d.n_heads if d.variant == "mamba2" else di
+    dtv = r.uniform(1e-3, 1e-1, nd)
+    dt_bias = (dtv + np.log(-np.expm1(-dtv))).astype(np.float32)
+    if d.variant == "mamba2":
+        a_log = np.log(r.uniform(1, 16, d.n_heads)).astype(np.float32)
+    else:
+        a_log = np.log(np.tile(np.arange(1, d.d_state + 1, dtype=np.float32), (di, 1))).astype(np.float32)
+    dpar = np.ones(nd, np.float32)
+    norm = (1.0 + 0.1 * r.standard_normal(di)).astype(np.float32)
+    hb = di & -di
+    s_y = np.float32(4.5 * np.sqrt(hb) / 127)
+    qb = QBlock(d, profile, inp, out, conv_w, conv_b, a_log, dpar, dt_bias, norm,
+                head_group=(np.arange(d.n_heads) // max(1, d.n_heads // d.n_state_groups)).astype(np.int32)
+                if d.variant == "mamba2" else None,
+                s_u=s, s_y=s_y)
+    if profile == "W4A16":
+        return qb
+    qb.in_out_scale = np.full(d.in_proj_out, s, np.float32)
+    qb.conv_in_scale = np.full(C, s, np.float32)
+    qb.conv_out_scale = (r.uniform(0.5, 1.0, C) * 2.0 / 127).astype(np.float32)
+    if d.variant == "mamba2":
+        gn = d.n_state_groups * d.d_state
+        qb.conv_out_scale[di:di + gn] = np.repeat(qb.conv_out_scale[di:di + gn:d.d_state], d.d_state)
+        qb.conv_out_scale[di + gn:] = np.repeat(qb.conv_out_scale[di + gn::d.d_state], d.d_state)
+        rows = d.n_heads * d.head_dim
+    else:
+        rows = di
+        R, N = d.dt_rank, d.d_state
+        qb.x_proj = _analytic_qlinear(r, R + 2 * N, di, "w8" if kind == "w8" else "w4a8", 128, 1.0, 64.0)
+        qb.dt_proj = _analytic_qlinear(r, di, R, "w8" if kind == "w8" else "w4a8", 32, 1.0, U_STD_CODES)
+        qb.xproj_out_scale = np.full(R + 2 * N, s, np.float32)
+        qb.s_dt = s
+    qb.state_scale = (r.uniform(0.5, 1.0, rows) * 0.5 / 127).astype(np.float32)
+    return qb
+
+
+@dataclass
+class DeviceQL:
+    """A projection whose kernel-layout weights are already in HBM."""
+    kind: str
+    shape: tuple
+    group: int
+    device_w: torch.Tensor
+    sg: object = None
+    s_ch: object = None
+    s_group: object = None
+
+
+def _device_ql(g: torch.Generator, n, k, kind, dev, group=128, in_code_std=U_STD_CODES, out_std=1.0):
+    group = min(group, k)
+    if kind == "w8":
+        w = torch.randint(-127, 128, (n, k), generator=g, device=dev, dtype=torch.int8)
+        s_ch = np.full(n, out_std / (np.sqrt(k) * in_code_std * 73.3), np.float32)
+        return DeviceQL("w8", (n, k), k, w, s_ch=s_ch)
+    w = torch.randint(0, 256, (n * k // 2,), generator=g, device=dev, dtype=torch.uint8)
+    if kind == "w4a8":
+        sg = torch.randint(1, 16, (n, k // group), generator=g, device=dev, dtype=torch.int8)
+        s_ch = np.full(n, out_std / (np.sqrt(k) * in_code_std * 4.6 * 9.0), np.float32)
+        return DeviceQL("w4a8", (n, k), group, w, sg=sg, s_ch=s_ch)
+    s_group = torch.full((n, k // group), out_std / (np.sqrt(k) * 4.6), device=dev, dtype=torch.float32)
+    return DeviceQL("w4a16", (n, k), group, w, s_group=s_group)
+
+
+def device_qblock(d: Dims, profile: str, seed: int, dev) -> DeviceBlock:
+    """A DeviceBlock whose big projections are generated in HBM; small tensors on host."""
+    kind = {"W8A8": "w8", "W4A8": "w4a8", "W4A16": "w4a16"}[profile]
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    small = random_qblock(Dims(d.variant, 32, d.d_inner, d.d_state, d.n_heads, d.head_dim, d.n_state_groups,
+                               d.conv_kernel, d.dt_rank), profile, seed)
+    small.dims = d
+    small.in_proj = _device_ql(g, d.in_proj_out, d.d_model, kind, dev)
+    small.out_proj = _device_ql(g, d.d_model, d.d_inner, kind, dev, in_code_std=127.0 / 4, out_std=0.1)
+    if profile != "W4A16":
+        small.in_out_scale = np.full(d.in_proj_out, np.float32(4.0 / 127), np.float32)
+        if d.variant == "mamba1":
+            R, N = d.dt_rank, d.d_state
+            k2 = "w8" if kind == "w8" else "w4a8"
+            small.x_proj = _device_ql(g, R + 2 * N, d.d_inner, k2, dev)
+            small.dt_proj = _device_ql(g, d.d_inner, R, k2, dev, group=32)
+    return DeviceBlock(small, dev)
+
+
+@dataclass
+class SynthHost:
+    dims: Dims
+    profiles: list
+    emb_codes: object
+    emb_scale: object
+    layer_norms: list
+    blocks: list
+    final_norm: object
+    head: object
+    s_head: float
+
+
+def synthetic_lm(d: Dims, n_layers: int, profile: str, vocab: int, dev="cuda", seed: int = 0, head_kind="w4a8"):
+    from .model import QuantizedMambaLM
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed + 1000)
+    emb = torch.randint(-127, 128, (vocab, d.d_model), generator=g, device=dev, dtype=torch.int8)
+    es = torch.full((vocab,), 1.0 / 127, device=dev)
+    blocks = [device_qblock(d, profile, seed + l, dev) for l in range(n_layers)]
+    head = _device_ql(g, vocab, d.d_model, head_kind, dev)
+    host = SynthHost(d, [profile] * n_layers, emb, es, [np.ones(d.d_model, np.float32)] * n_layers, blocks,
+                     np.ones(d.d_model, np.float32), head, np.float32(4.0 / 127))
+    return QuantizedMambaLM(host, dev)

@@ -1,0 +1,207 @@
+"""GPU parity: every C-ABI kernel vs the CPU oracle on the same seeded inputs.
+
+Bars (north_star): int32 accumulators, weight codes and packing bit-exact; requantised
+int8 activations / cached state within 1 quantization step (mismatch fractions
+reported and bounded); float outputs within the stated relative tolerance.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import hadamard as ohad
+from oracle import qblock as oq
+from oracle import ssm_block as osb
+from oracle.quantizer import quantize_codes
+from oracle.tensor_core import int_gemm, pack_u4, unpack_u4
+
+pytestmark = pytest.mark.gpu
+
+
+def _ops():
+    from paper_2503_22879_b200 import ops
+    return ops
+
+
+def _rng(*s):
+    from oracle.tensor_core import make_rng
+    return make_rng(1234, *s)
+
+
+def code_diff(a, b):
+    d = np.abs(np.asarray(a, np.int32) - np.asarray(b, np.int32))
+    return int(d.max(initial=0)), float((d > 0).mean()) if d.size else 0.0
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (64, 18560 // 8, 4096), (37, 300, 160), (256, 1024, 512)])
+def test_gemm_w8a8_exact(cuda, M, N, K):
+    ops = _ops()
+    r = _rng(1, M, N)
+    a = r.integers(-128, 128, (M, K)).astype(np.int8)
+    w = r.integers(-127, 128, (N, K)).astype(np.int8)
+    alpha = r.uniform(1e-4, 1e-2, N).astype(np.float32)
+    cs = r.uniform(0.05, 0.2, N).astype(np.float32)
+    ta, tw, tal, tcs = (torch.as_tensor(x, device=cuda) for x in (a, w, alpha, cs))
+    acc = int_gemm(a, w.T)
+    got = ops.gemm_w8a8(ta, tw, tal, ops.EPI_I32).cpu().numpy()
+    assert np.array_equal(got, acc), "int32 accumulators must be bit-exact"
+    y = (acc.astype(np.float32) * alpha[None]).astype(np.float32)
+    gy = ops.gemm_w8a8(ta, tw, tal, ops.EPI_F32).cpu().numpy()
+    assert np.array_equal(gy, y)
+    q = quantize_codes(y, cs[None], 8)
+    gq = ops.gemm_w8a8(ta, tw, tal, ops.EPI_QUANT, col_scale=tcs).cpu().numpy()
+    assert np.array_equal(gq, q)
+    res = r.standard_normal((M, N)).astype(np.float32)
+    tres = torch.as_tensor(res, device=cuda)
+    ops.gemm_w8a8(ta, tw, tal, ops.EPI_RESID, out=tres)
+    assert np.array_equal(tres.cpu().numpy(), (res + y).astype(np.float32))
+
+
+@pytest.mark.parametrize("M,N,K,group", [(64, 384, 4096, 128), (3, 256, 256, 32), (16, 130, 8192, 128)])
+def test_gemm_w4a8_exact(cuda, M, N, K, group):
+    ops = _ops()
+    from paper_2503_22879_b200.ssm_block import pack_u4_host
+    r = _rng(2, M, N)
+    a = r.integers(-128, 128, (M, K)).astype(np.int8)
+    codes = r.integers(-8, 8, (N, K)).astype(np.int8)
+    sg = r.integers(1, 16, (N, K // group)).astype(np.int8)
+    alpha = r.uniform(1e-4, 1e-2, N).astype(np.float32)
+    ql = oq.QLinear("w4a8", codes, s_ch=alpha, sg=sg, group=group)
+    acc = int_gemm(a, ql.int8_weight().T)
+    packed = pack_u4_host(codes)
+    assert np.array_equal(packed, pack_u4(codes)), "product packing == oracle packing"
+    tw = ops.repack_w4(torch.as_tensor(packed, device=cuda), N, K)
+    assert np.array_equal(ops.unpack_w4(tw, N, K).cpu().numpy(), packed)
+    ta = torch.as_tensor(a, device=cuda)
+    tsg = torch.as_tensor(sg, device=cuda)
+    tal = torch.as_tensor(alpha, device=cuda)
+    got = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_I32).cpu().numpy()
+    assert np.array_equal(got, acc)
+    gy = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_F32).cpu().numpy()
+    assert np.array_equal(gy, (acc.astype(np.float32) * alpha[None]).astype(np.float32))
+
+
+@pytest.mark.parametrize("M,N,K,group", [(1, 18560 // 4, 4096, 128), (3, 512, 8192, 128), (16, 200, 160, 32)])
+def test_gemv_w4a16(cuda, M, N, K, group):
+    ops = _ops()
+    from paper_2503_22879_b200.ssm_block import pack_u4_host
+    r = _rng(3, M, N)
+    x = r.standard_normal((M, K)).astype(np.float32)
+    codes = r.integers(-8, 8, (N, K)).astype(np.int8)
+    sgrp = r.uniform(1e-3, 1e-2, (N, K // group)).astype(np.float32)
+    ql = oq.QLinear("w4a16", codes, s_group=sgrp, group=group)
+    ref = oq.qlinear_a16(x, ql)
+    tw = ops.repack_w4(torch.as_tensor(pack_u4_host(codes), device=cuda), N, K)
+    got = ops.gemv_w4a16(torch.as_tensor(x, device=cuda), tw, torch.as_tensor(sgrp, device=cuda), group, N)
+    got = got.cpu().numpy()
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max() + 1e-6
+
+
+@pytest.mark.parametrize("M,D", [(5, 256), (64, 4096), (3, 2560)])
+def test_rmsnorm_quant(cuda, M, D):
+    ops = _ops()
+    r = _rng(4, M, D)
+    x = (r.standard_normal((M, D)) * np.exp(r.uniform(-2, 2, D))).astype(np.float32)
+    g = (1 + 0.1 * r.standard_normal(D)).astype(np.float32)
+    s = np.float32(np.abs(osb.rmsnorm(x, g)).max() / 127)
+    ref = quantize_codes(osb.rmsnorm(x, g), s, 8)
+    got = ops.rmsnorm_quant(torch.as_tensor(x, device=cuda), torch.as_tensor(g, device=cuda), 1e-5, s).cpu().numpy()
+    mx, frac = code_diff(got, ref)
+    assert mx <= 1 and frac < 1e-3
+
+
+@pytest.mark.parametrize("M,D,had", [(4, 512, True), (64, 8192, True), (8, 5120, True), (8, 512, False)])
+def test_gate_norm_had_quant(cuda, M, D, had):
+    ops = _ops()
+    r = _rng(5, M, D)
+    y = (r.standard_normal((M, D)) * np.exp(r.uniform(-1, 1, D))).astype(np.float32)
+    g = (1 + 0.1 * r.standard_normal(D)).astype(np.float32)
+    rn = osb.rmsnorm(y, g)
+    t = ohad.fwht_blocked(rn) if had else rn
+    s = np.float32(np.abs(t).max() / 127)
+    ref = quantize_codes(t, s, 8)
+    got = ops.gate_norm_had_quant(torch.as_tensor(y, device=cuda), torch.as_tensor(g, device=cuda), 1e-5, s,
+                                  had).cpu().numpy()
+    mx, frac = code_diff(got, ref)
+    assert mx <= 1 and frac < 1e-3
+
+
+def test_conv1d_prefill_and_update(cuda):
+    ops = _ops()
+    r = _rng(6)
+    B, T, C, K = 3, 150, 384, 4
+    x = r.integers(-128, 128, (B * T, C)).astype(np.int8)
+    w = (r.standard_normal((C, K)) * 0.3).astype(np.float32)
+    b = (r.standard_normal(C) * 0.05).astype(np.float32)
+    s_in = r.uniform(0.01, 0.05, C).astype(np.float32)
+    s_out = r.uniform(0.01, 0.05, C).astype(np.float32)
+    qb = oq.QBlock(None, "W8A8", None, None, w, b, None, None, None, None, conv_in_scale=s_in, conv_out_scale=s_out)
+    qb.dims = osb.Dims("mamba2", 8, 8, 8, 1, 8, 1, K)
+    cache0 = r.integers(-128, 128, (B, C, K - 1)).astype(np.int8)
+    refs, caches = [], []
+    for bi in range(B):
+        o, c = oq._conv_a8(x[bi * T:(bi + 1) * T], qb, cache0[bi])
+        refs.append(o)
+        caches.append(c)
+    ref = np.concatenate(refs)
+    t = lambda a: torch.as_tensor(a, device=cuda)
+    tcache = t(np.ascontiguousarray(cache0.transpose(0, 2, 1)))
+    got = ops.conv1d_int8(t(x), t(w), t(b), t(s_in), t(s_out), B, T, tcache, True).cpu().numpy()
+    mx, frac = code_diff(got, ref)
+    assert mx <= 1 and frac < 1e-3
+    assert np.array_equal(tcache.cpu().numpy(), np.stack(caches).transpose(0, 2, 1))
+    # decode update: one more token per sequence
+    xn = r.integers(-128, 128, (B, C)).astype(np.int8)
+    refn = np.concatenate([oq._conv_a8(xn[bi:bi + 1], qb, caches[bi])[0] for bi in range(B)])
+    gotn = ops.conv1d_update_int8(t(xn), t(w), t(b), t(s_in), t(s_out), tcache).cpu().numpy()
+    mx, frac = code_diff(gotn, refn)
+    assert mx <= 1 and frac < 1e-2
+
+
+def _tiny_block(profile, variant="mamba2", seed=0):
+    from oracle import pipeline as opl
+    if variant == "mamba2":
+        d = osb.Dims("mamba2", 256, 512, 64, 8, 64, 2, 4)
+    else:
+        d = osb.Dims("mamba1", 256, 512, 16, 1, 512, 1, 4, dt_rank=32)
+    fm = opl.cmd_gen_toy(d, 1, seed=seed)
+    toks = opl.calib_tokens(512, 2, 64, seed)
+    stats = opl.collect_stats(fm, toks)
+    qb = opl.quantize_block(fm.blocks[0], stats[0], profile)
+    u = osb.rmsnorm(fm.embedding[toks[0]], fm.layer_norms[0])
+    return d, qb, u
+
+
+@pytest.mark.parametrize("profile,variant", [("W8A8", "mamba2"), ("W4A8", "mamba2"), ("W4A16", "mamba2"),
+                                             ("W8A8", "mamba1"), ("W4A8", "mamba1")])
+def test_block_forward_quantized(cuda, profile, variant):
+    from paper_2503_22879_b200.ssm_block import block_forward_quantized, DeviceBlock
+    d, qb, u = _tiny_block(profile, variant)
+    tr = {}
+    ref, rst = oq.block_forward_quantized(u, qb, trace=tr)
+    blk = DeviceBlock(qb, cuda)
+    out, st = block_forward_quantized(torch.as_tensor(u, device=cuda), blk)
+    out = out.cpu().numpy()
+    rel = np.abs(out - ref).max() / np.abs(ref).max()
+    assert rel < (2e-2 if qb.a8 else 1e-3), rel
+    if qb.a8:
+        h = st.h.cpu().numpy().reshape(rst.h.shape)
+        mx, frac = code_diff(h, rst.h)
+        assert mx <= 1 and frac < 2e-2
+        cc = st.conv_cache.cpu().numpy()[0].T
+        assert np.array_equal(cc, rst.conv)
+
+
+@pytest.mark.parametrize("profile", ["W8A8", "W4A8", "W4A16"])
+def test_decode_matches_oracle_steps(cuda, profile):
+    """Prefill 48 tokens then 16 single-token decode steps (int8 cached state)."""
+    from paper_2503_22879_b200.ssm_block import block_forward_quantized, DeviceBlock
+    d, qb, u = _tiny_block(profile)
+    blk = DeviceBlock(qb, cuda)
+    _, ost = oq.block_forward_quantized(u[:48], qb)
+    _, gst = block_forward_quantized(torch.as_tensor(u[:48], device=cuda), blk)
+    worst = 0.0
+    for t in range(48, 64):
+        ro, ost = oq.block_forward_quantized(u[t:t + 1], qb, ost)
+        go, gst = block_forward_quantized(torch.as_tensor(u[t:t + 1], device=cuda), blk, state=gst)
+        worst = max(worst, np.abs(go.cpu().numpy() - ro).max() / np.abs(ro).max())
+    assert worst < 5e-2, worst
