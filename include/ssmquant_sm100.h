@@ -64,6 +64,10 @@ const char* sq_last_error(void);
 /* 1 if the current device is sm_100 (B200-class) and the kernels can run. */
 int sq_device_supported(void);
 
+/* Select the A8 GEMM implementation: 0 = legacy mma.sync, 1 = tcgen05 with the W4 operand
+ * expanded into TMEM (default), 2 = tcgen05 with the W4 operand expanded into shared memory. */
+int sq_set_gemm_mode(int mode);
+
 /* ---- weights ---------------------------------------------------------------------- */
 /* u4packed [N x K/2] (low nibble = even k) + int8 sg [N x K/group] -> kernel layout
  * `dst` (sq_w4_bytes(N,K) bytes).  sg may be NULL (all ones; W4A16 layout). */

@@ -69,8 +69,13 @@ __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* __restri
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int gk = k0 + i * 32;
-        rw[i] = (gn < N && gk < K) ? *reinterpret_cast<const int4*>(w + (int64_t)gn * (K / 2) + gk / 2)
-                                   : make_int4(0, 0, 0, 0);
+        int64_t off;
+        if (K % 128 == 0) {   // tiled kernel layout (sq_repack_w4): [tile][kb][chunk][row][16B]
+          off = ((((int64_t)(gn >> 7) * (K >> 7) + (gk >> 7)) * 4 + ((gk & 127) >> 5)) * 128 + (gn & 127)) * 16;
+        } else {
+          off = (int64_t)gn * (K / 2) + gk / 2;
+        }
+        rw[i] = (gn < N && gk < K) ? *reinterpret_cast<const int4*>(w + off) : make_int4(0, 0, 0, 0);
       }
     } else {
 #pragma unroll

@@ -2,6 +2,14 @@
 #include "common.cuh"
 
 namespace sq {
+extern int g_tc_w4_mode;
+static int g_gemm_mode = 1;   // 0: mma.sync only, 1: tcgen05 (TS for W4), 2: tcgen05 (SS for W4)
+int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg, int group, bool w4,
+               const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
+               cudaStream_t st);
+int64_t w4_layout_bytes(int N, int K);
+int repack_w4(const uint8_t* src, int N, int K, uint8_t* dst, cudaStream_t st);
+int unpack_w4(const uint8_t* src, int N, int K, uint8_t* dst, cudaStream_t st);
 int gemm_a8_mma(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg, int group, bool w4,
                 const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
                 cudaStream_t st);
@@ -21,21 +29,25 @@ static int check_gemm(const char* name, const void* a, int64_t lda, int M, int N
 
 using namespace sq;
 
-extern "C" int64_t sq_w4_bytes(int N, int K) { return (int64_t)N * K / 2; }
+extern "C" int64_t sq_w4_bytes(int N, int K) { return w4_layout_bytes(N, K); }
 
-// Layout v1: row-major u4packed (identity).  Kept behind the repack API so the kernel
-// layout can change without touching callers; sq_unpack_w4 proves the round trip.
+// Kernel layout (K % 128 == 0): [n_tile][k_block][chunk][row][16 B] so a warp's 32 weight
+// rows load 512 contiguous bytes per instruction; otherwise row-major u4packed.
+// sq_unpack_w4 inverts it (bit-exact round trip, tested).
 extern "C" int sq_repack_w4(const uint8_t* u4packed, int N, int K, uint8_t* dst, void* stream) {
   SQ_REQUIRE(N > 0 && K > 0 && K % 32 == 0, SQ_ERR_SHAPE, "sq_repack_w4: K must be a multiple of 32");
-  cudaError_t e = cudaMemcpyAsync(dst, u4packed, (size_t)N * K / 2, cudaMemcpyDeviceToDevice, as_stream(stream));
-  SQ_REQUIRE(e == cudaSuccess, SQ_ERR_CUDA, "sq_repack_w4: %s", cudaGetErrorString(e));
-  return SQ_OK;
+  return repack_w4(u4packed, N, K, dst, as_stream(stream));
 }
 
 extern "C" int sq_unpack_w4(const uint8_t* src, int N, int K, uint8_t* u4packed, void* stream) {
   SQ_REQUIRE(N > 0 && K > 0 && K % 32 == 0, SQ_ERR_SHAPE, "sq_unpack_w4: K must be a multiple of 32");
-  cudaError_t e = cudaMemcpyAsync(u4packed, src, (size_t)N * K / 2, cudaMemcpyDeviceToDevice, as_stream(stream));
-  SQ_REQUIRE(e == cudaSuccess, SQ_ERR_CUDA, "sq_unpack_w4: %s", cudaGetErrorString(e));
+  return unpack_w4(src, N, K, u4packed, as_stream(stream));
+}
+
+extern "C" int sq_set_gemm_mode(int mode) {
+  SQ_REQUIRE(mode >= 0 && mode <= 2, SQ_ERR_ARG, "sq_set_gemm_mode: mode must be 0, 1 or 2");
+  g_gemm_mode = mode;
+  g_tc_w4_mode = mode == 2 ? 2 : 1;
   return SQ_OK;
 }
 
@@ -44,6 +56,11 @@ extern "C" int sq_gemm_w8a8(const int8_t* a, int64_t lda, const int8_t* w, const
   int rc = check_gemm("sq_gemm_w8a8", a, lda, M, N, K, epi, ldo, col_scale);
   if (rc) return rc;
   if (M == 0) return SQ_OK;
+  if (g_gemm_mode != 0) {
+    rc = gemm_a8_tc(a, lda, reinterpret_cast<const uint8_t*>(w), nullptr, K, false, alpha, M, N, K, epi, out, ldo,
+                    col_scale, as_stream(stream));
+    if (rc != SQ_ERR_ARG) return rc;
+  }
   return gemm_a8_mma(a, lda, reinterpret_cast<const uint8_t*>(w), nullptr, K, false, alpha, M, N, K, epi, out, ldo,
                      col_scale, as_stream(stream));
 }
@@ -56,5 +73,9 @@ extern "C" int sq_gemm_w4a8(const int8_t* a, int64_t lda, const uint8_t* w4, con
   SQ_REQUIRE(group % 32 == 0 && K % group == 0 && sg != nullptr, SQ_ERR_LAYOUT,
              "sq_gemm_w4a8: group (%d) must be a multiple of 32 dividing K", group);
   if (M == 0) return SQ_OK;
+  if (g_gemm_mode != 0) {
+    rc = gemm_a8_tc(a, lda, w4, sg, group, true, alpha, M, N, K, epi, out, ldo, col_scale, as_stream(stream));
+    if (rc != SQ_ERR_ARG) return rc;
+  }
   return gemm_a8_mma(a, lda, w4, sg, group, true, alpha, M, N, K, epi, out, ldo, col_scale, as_stream(stream));
 }

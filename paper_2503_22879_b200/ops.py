@@ -277,3 +277,8 @@ def selective_scan_int8(p, B, T, x, dt, BC, z, state, state_in, y):
                                         BC.data_ptr(), _ld(BC), z.data_ptr(), _ld(z), state.data_ptr(),
                                         int(bool(state_in)), y.data_ptr(), _ld(y), _stream()))
     return y
+
+
+def set_gemm_mode(mode: int):
+    """0: legacy mma.sync GEMM, 1: tcgen05 (W4 operand expanded into TMEM), 2: tcgen05 (into smem)."""
+    _check(lib().sq_set_gemm_mode(int(mode)))

@@ -32,8 +32,20 @@ def code_diff(a, b):
     return int(d.max(initial=0)), float((d > 0).mean()) if d.size else 0.0
 
 
-@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (64, 18560 // 8, 4096), (37, 300, 160), (256, 1024, 512)])
-def test_gemm_w8a8_exact(cuda, M, N, K):
+GEMM_MODES = [0, 1, 2]
+
+
+@pytest.fixture(params=GEMM_MODES, ids=["mma_sync", "tc_tmem", "tc_smem"])
+def gemm_mode(request, cuda):
+    ops = _ops()
+    ops.set_gemm_mode(request.param)
+    yield request.param
+    ops.set_gemm_mode(1)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (64, 18560 // 8, 4096), (37, 300, 160), (256, 1024, 512),
+                                   (64, 4096, 8192), (200, 2560, 5120)])
+def test_gemm_w8a8_exact(cuda, gemm_mode, M, N, K):
     ops = _ops()
     r = _rng(1, M, N)
     a = r.integers(-128, 128, (M, K)).astype(np.int8)
@@ -56,8 +68,9 @@ def test_gemm_w8a8_exact(cuda, M, N, K):
     assert np.array_equal(tres.cpu().numpy(), (res + y).astype(np.float32))
 
 
-@pytest.mark.parametrize("M,N,K,group", [(64, 384, 4096, 128), (3, 256, 256, 32), (16, 130, 8192, 128)])
-def test_gemm_w4a8_exact(cuda, M, N, K, group):
+@pytest.mark.parametrize("M,N,K,group", [(64, 384, 4096, 128), (3, 256, 256, 32), (16, 130, 8192, 128),
+                                         (64, 4096, 8192, 128), (64, 18560, 4096, 128), (300, 640, 1024, 128)])
+def test_gemm_w4a8_exact(cuda, gemm_mode, M, N, K, group):
     ops = _ops()
     from paper_2503_22879_b200.ssm_block import pack_u4_host
     r = _rng(2, M, N)

@@ -56,26 +56,38 @@ def test_generate_graph_equals_eager_and_oracle(cuda):
     assert agree >= 0.75, (g[0], ref)
 
 
+def _to_oracle(pqb):
+    od = osb.Dims(**vars(pqb.dims))
+    return oq.QBlock(od, pqb.profile, oq.QLinear(**vars(pqb.in_proj)), oq.QLinear(**vars(pqb.out_proj)),
+                     pqb.conv_weight, pqb.conv_bias, pqb.a_log, pqb.d_param, pqb.dt_bias, pqb.norm_weight,
+                     pqb.head_group, s_u=pqb.s_u, in_out_scale=pqb.in_out_scale, conv_in_scale=pqb.conv_in_scale,
+                     conv_out_scale=pqb.conv_out_scale, state_scale=pqb.state_scale, s_y=pqb.s_y)
+
+
 def test_mamba2_8b_layer_decode_b64(cuda):
     """One Mamba2-8B-shaped W4A8 layer, decode b=64 from a random int8 state (C3 shapes)."""
     from paper_2503_22879_b200.ssm_block import DeviceBlock, SsmState
     from paper_2503_22879_b200 import synth
     d = osb.Dims("mamba2", 4096, 8192, 128, 128, 64, 8, 4)
-    qb = synth.random_qblock(d, "W4A8", seed=3)
+    pqb = synth.random_qblock(d, "W4A8", seed=3)
+    qb = _to_oracle(pqb)
     B = 64
     r = np.random.default_rng(0)
     u = (r.standard_normal((B, d.d_model))).astype(np.float32)
     h0 = r.integers(-100, 100, (B, d.n_heads, d.head_dim, d.d_state)).astype(np.int8)
     c0 = r.integers(-100, 100, (B, d.conv_dim, 3)).astype(np.int8)
-    blk = DeviceBlock(qb, cuda)
+    blk = DeviceBlock(pqb, cuda)
     st = SsmState(torch.as_tensor(h0, device=cuda), torch.as_tensor(np.ascontiguousarray(c0.transpose(0, 2, 1)),
                                                                      device=cuda))
     from paper_2503_22879_b200 import ops
     codes = ops.quantize_f32(torch.as_tensor(u, device=cuda), blk.s_u)
     out = blk.forward_codes(codes, B, 1, st, True).cpu().numpy()
-    for i in (0, 17, 63):
-        ro, rs = oq.block_forward_quantized(u[i:i + 1], qb, oq.QState(h0[i], c0[i]))
-        rel = np.abs(out[i] - ro[0]).max() / np.abs(ro).max()
-        assert rel < 2e-2, (i, rel)
-        hd = np.abs(st.h[i].cpu().numpy().astype(np.int32) - rs.h.astype(np.int32))
-        assert hd.max() <= 1 and (hd > 0).mean() < 1e-3
+    ro, rh, rc = oq.decode_step_batched(u, qb, h0, c0)
+    rel = np.abs(out - ro).max() / np.abs(ro).max()
+    assert rel < 2e-2, rel
+    hd = np.abs(st.h.cpu().numpy().astype(np.int32) - rh.astype(np.int32))
+    assert hd.max() <= 1 and (hd > 0).mean() < 1e-3
+    assert np.array_equal(st.conv_cache.cpu().numpy().transpose(0, 2, 1), rc)
+    for i in (0, 63):      # the batched oracle equals the per-sequence oracle
+        ro1, rs1 = oq.block_forward_quantized(u[i:i + 1], qb, oq.QState(h0[i], c0[i]))
+        assert np.array_equal(ro1[0], ro[i]) and np.array_equal(rs1.h, rh[i])
