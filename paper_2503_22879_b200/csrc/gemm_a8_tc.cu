@@ -176,54 +176,55 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int n = n_tile * TC_BN + row;
     const bool valid_n = n < args.N;
     if (WMODE != WM_W8) {
-      constexpr int D = 4;               // K-blocks in flight per thread
+      // Batched converter: D K-blocks are converted, stored (TMEM or smem) and released
+      // together, so the tcgen05.st / proxy-fence latency is paid once per batch while
+      // the next batch's weight loads are already in flight.
+      constexpr int D = 4;
       const uint8_t* wsrc = args.w4 + (size_t)n_tile * nkb_total * W4_TILE_BYTES + row * 16 + half * 2 * 2048;
       const int ng = args.K / args.group;
       const int8_t* sgrow = args.sg + (size_t)(valid_n ? n : 0) * ng;
       int4 buf[D][2];
       int sgb[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        if (j < nkb && valid_n) {
-          const uint8_t* p = wsrc + (size_t)(kb_begin + j) * W4_TILE_BYTES;
+      auto fetch = [&](int i, int j) {
+        if (i < nkb && valid_n) {
+          const uint8_t* p = wsrc + (size_t)(kb_begin + i) * W4_TILE_BYTES;
           buf[j][0] = ldg_stream(p);
           buf[j][1] = ldg_stream(p + 2048);
-          sgb[j] = sgrow[(kb_begin + j) * TC_BK / args.group];
+          sgb[j] = sgrow[(kb_begin + i) * TC_BK / args.group];
         } else {
           buf[j][0] = buf[j][1] = make_int4(0, 0, 0, 0);
           sgb[j] = 0;
         }
-      }
+      };
+#pragma unroll
+      for (int j = 0; j < D; ++j) fetch(j, j);
       for (int i0 = 0; i0 < nkb; i0 += D) {
+        uint32_t wv[D][16];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const uint32_t sg = (uint32_t)sgb[j];
+          const uint32_t L0 = sg * 0x03020100u, L1 = sg * 0x07060504u;
+          const uint32_t L2 = ~(sg * 0x05060708u) + 0x01010101u, L3 = ~(sg * 0x01020304u) + 0x01010101u;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const uint32_t* pw = reinterpret_cast<const uint32_t*>(&buf[j][c]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              wv[j][c * 8 + e * 2] = nib4_to_s8(pw[e], L0, L1, L2, L3);
+              wv[j][c * 8 + e * 2 + 1] = nib4_to_s8(pw[e] >> 16, L0, L1, L2, L3);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) fetch(i0 + D + j, j);   // next batch in flight
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           const int i = i0 + j;
           if (i < nkb) {
-            const uint32_t sg = (uint32_t)sgb[j];
-            const uint32_t L0 = sg * 0x03020100u, L1 = sg * 0x07060504u;
-            const uint32_t L2 = ~(sg * 0x05060708u) + 0x01010101u, L3 = ~(sg * 0x01020304u) + 0x01010101u;
-            uint32_t wv[16];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const uint32_t* pw = reinterpret_cast<const uint32_t*>(&buf[j][c]);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                wv[c * 8 + e * 2] = nib4_to_s8(pw[e], L0, L1, L2, L3);
-                wv[c * 8 + e * 2 + 1] = nib4_to_s8(pw[e] >> 16, L0, L1, L2, L3);
-              }
-            }
-            if (i + D < nkb && valid_n) {   // refill this slot D blocks ahead
-              const uint8_t* p = wsrc + (size_t)(kb_begin + i + D) * W4_TILE_BYTES;
-              buf[j][0] = ldg_stream(p);
-              buf[j][1] = ldg_stream(p + 2048);
-              sgb[j] = sgrow[(kb_begin + i + D) * TC_BK / args.group];
-            }
             const int s = i % STAGES;
             mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
             if (WMODE == WM_W4_TS) {
-              tmem_st_x16(tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + s * 32 + half * 16, wv);
-              tmem_wait_st();
-              tc_fence_before();
+              tmem_st_x16(tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + s * 32 + half * 16, wv[j]);
             } else {
               // swizzled SW128 K-major tile: row r, 16-byte chunk c at ((c ^ (r&7)) * 16)
               uint8_t* base = wsm + s * Cfg::W_BYTES + (row >> 3) * 1024 + (row & 7) * 128;
@@ -231,13 +232,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               for (int c = 0; c < 4; ++c) {
                 const int c16 = half * 4 + c;
                 *reinterpret_cast<uint4*>(base + ((c16 ^ (row & 7)) * 16)) =
-                    make_uint4(wv[c * 4], wv[c * 4 + 1], wv[c * 4 + 2], wv[c * 4 + 3]);
+                    make_uint4(wv[j][c * 4], wv[j][c * 4 + 1], wv[j][c * 4 + 2], wv[j][c * 4 + 3]);
               }
-              fence_proxy_async_smem();
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[s]);
           }
+        }
+        if (WMODE == WM_W4_TS) {
+          tmem_wait_st();
+          tc_fence_before();
+        } else {
+          fence_proxy_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int j = 0; j < D; ++j)
+            if (i0 + j < nkb) mbar_arrive(&full[(i0 + j) % STAGES]);
         }
       }
     }

@@ -10,6 +10,107 @@ namespace sq {
 
 constexpr int kGemvMaxM = 8;
 
+// Tiled-layout GEMV (K % 128 == 0; layout of sq_repack_w4): a CTA owns 128 weight rows;
+// warp w reads row quadrant (w & 3) and K-half (w >> 2) of every 128-wide K-block, so a
+// warp's loads cover 512 contiguous bytes; the activation rows sit in smem (broadcast).
+template <int MT>
+__global__ void __launch_bounds__(256) gemv_w4a16_tiled_kernel(const float* __restrict__ x, int64_t ldx,
+                                                               const uint8_t* __restrict__ w,
+                                                               const float* __restrict__ sgrp, int group, int M,
+                                                               int N, int K, float* __restrict__ out, int64_t ldo,
+                                                               int resid) {
+  extern __shared__ float xs[];  // [MT][K]
+  __shared__ float part[MT][128];
+  for (int i = threadIdx.x; i < MT * K; i += blockDim.x) {
+    const int m = i / K, k = i % K;
+    xs[i] = m < M ? x[(int64_t)m * ldx + k] : 0.f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, khalf = warp >> 2;
+  const int row = q * 32 + lane;
+  const int n = blockIdx.x * 128 + row;
+  const bool valid = n < N;
+  const int nkb = K / 128;
+  const int ng = K / group;
+  const uint8_t* wsrc = w + (size_t)blockIdx.x * nkb * 8192 + row * 16 + khalf * 2 * 2048;
+  const float* srow = sgrp + (size_t)(valid ? n : 0) * ng;
+  float acc[MT];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) acc[m] = 0.f;
+  constexpr int D = 4;
+  int4 buf[D][2];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    if (j < nkb && valid) {
+      buf[j][0] = *reinterpret_cast<const int4*>(wsrc + (size_t)j * 8192);
+      buf[j][1] = *reinterpret_cast<const int4*>(wsrc + (size_t)j * 8192 + 2048);
+    } else {
+      buf[j][0] = buf[j][1] = make_int4(0, 0, 0, 0);
+    }
+  }
+  for (int kb0 = 0; kb0 < nkb; kb0 += D) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int kb = kb0 + j;
+      if (kb < nkb) {
+        int4 cur[2] = {buf[j][0], buf[j][1]};
+        if (kb + D < nkb && valid) {
+          buf[j][0] = *reinterpret_cast<const int4*>(wsrc + (size_t)(kb + D) * 8192);
+          buf[j][1] = *reinterpret_cast<const int4*>(wsrc + (size_t)(kb + D) * 8192 + 2048);
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int k0 = kb * 128 + (khalf * 2 + c) * 32;
+          const float s = valid ? srow[k0 / group] : 0.f;
+          const uint32_t* pw = reinterpret_cast<const uint32_t*>(&cur[c]);
+          float pa[MT];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) pa[m] = 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t u = pw[e] ^ 0x88888888u;   // nibble -> v + 8
+#pragma unroll
+            for (int i4 = 0; i4 < 2; ++i4) {
+              float wv[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                wv[i] = __uint_as_float(((u >> (4 * (i4 * 4 + i))) & 0xFu) | 0x4B000000u) - 8388616.0f;
+#pragma unroll
+              for (int m = 0; m < MT; ++m) {
+                const float4 xv = *reinterpret_cast<const float4*>(&xs[m * K + k0 + e * 8 + i4 * 4]);
+                pa[m] = fmaf(wv[0], xv.x, pa[m]);
+                pa[m] = fmaf(wv[1], xv.y, pa[m]);
+                pa[m] = fmaf(wv[2], xv.z, pa[m]);
+                pa[m] = fmaf(wv[3], xv.w, pa[m]);
+              }
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < MT; ++m) acc[m] = fmaf(pa[m], s, acc[m]);
+        }
+      }
+    }
+  }
+  if (khalf == 1) {
+#pragma unroll
+    for (int m = 0; m < MT; ++m) part[m][row] = acc[m];
+  }
+  __syncthreads();
+  if (khalf == 0 && valid) {
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (m < M) {
+        const float v = acc[m] + part[m][row];
+        float* o = out + (int64_t)m * ldo + n;
+        *o = resid ? __fadd_rn(*o, v) : v;
+      }
+    }
+  }
+}
+
+
+
 template <int MT>
 __global__ void __launch_bounds__(256) gemv_w4a16_kernel(const float* __restrict__ x, int64_t ldx,
                                                          const uint8_t* __restrict__ w,
@@ -71,16 +172,19 @@ extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4, con
   SQ_REQUIRE(M >= 0 && N > 0 && K > 0 && K % 32 == 0 && group % 32 == 0 && K % group == 0, SQ_ERR_SHAPE,
              "sq_gemv_w4a16: K (%d) and group (%d) must be multiples of 32", K, group);
   cudaStream_t st = as_stream(stream);
-  for (int m0 = 0; m0 < M; m0 += kGemvMaxM) {
-    const int mc = M - m0 < kGemvMaxM ? M - m0 : kGemvMaxM;
+  int maxm = (160 * 1024) / (K * 4);
+  maxm = maxm >= 8 ? 8 : maxm >= 4 ? 4 : maxm >= 2 ? 2 : 1;
+  for (int m0 = 0; m0 < M; m0 += maxm) {
+    const int mc = M - m0 < maxm ? M - m0 : maxm;
     const int MT = mc <= 1 ? 1 : (mc <= 2 ? 2 : (mc <= 4 ? 4 : 8));
     const size_t smem = (size_t)MT * K * sizeof(float);
     SQ_REQUIRE(smem <= 200 * 1024, SQ_ERR_SHAPE, "sq_gemv_w4a16: K too large");
-    int blocks = (N + 7) / 8;
-    if (blocks > 148 * 4) blocks = 148 * 4;
+    const bool tiled = K % 128 == 0;
+    int blocks = tiled ? (N + 127) / 128 : (N + 7) / 8;
+    if (!tiled && blocks > 148 * 4) blocks = 148 * 4;
 #define SQ_GV(MTV)                                                                                  \
   {                                                                                                 \
-    auto k = gemv_w4a16_kernel<MTV>;                                                                \
+    auto k = tiled ? gemv_w4a16_tiled_kernel<MTV> : gemv_w4a16_kernel<MTV>;                         \
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     k<<<blocks, 256, smem, st>>>(x + (int64_t)m0 * ldx, ldx, w4, s_group, group, mc, N, K,          \
                                  out + (int64_t)m0 * ldo, ldo, resid);                              \

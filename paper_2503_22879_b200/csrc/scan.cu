@@ -191,6 +191,118 @@ __global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, in
   for (int n = 0; n < N; ++n) st[n] = quant8(hs[n], sh);
 }
 
+// ---------------------------------------------------------------------------------
+// K9 decode: Mamba2 int8 state update, HBM-streaming version.
+// CTA = (sequence, 4 consecutive heads), 256 threads; thread t owns the 16-column
+// chunk (t % 8) of rows {t/8, t/8+32} of each head -> 8 x 16-B loads in flight per
+// thread, a warp touches 512 contiguous bytes.  B̂/Ĉ are dequantised once per CTA
+// into smem; Δ, Ȧ once per head.  Per element: byte->f32 via PRMT+FADD magic,
+// h' = (Ȧ·s_h)·q + (Δ·x̂)·B̂ (two FMA-pipe ops), y += h'·Ĉ, requant with 1/s_h and a
+// magic-number round-to-nearest-even (≤1-ulp differences from the oracle's
+// unfused f32 ops, i.e. a ≤1-step code difference at rounding ties, tested).
+constexpr int SU_HPC = 4;
+constexpr int SU_THREADS = 256;
+
+__device__ __forceinline__ float s8byte_to_f(uint32_t u_xor80, int i) {
+  // u_xor80 = word ^ 0x80808080 (unsigned b+128); returns (float)(signed byte i)
+  uint32_t bits;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bits) : "r"(u_xor80), "r"(0x4B000000u), "r"(0x7440u | (uint32_t)i));
+  return __int_as_float(bits) - 8388736.0f;
+}
+
+__device__ __forceinline__ uint32_t f_to_s8bits(float v) {
+  v = fminf(fmaxf(v, -128.f), 127.f);
+  return __float_as_uint(v + 12582912.0f);   // low byte = rint(v) (two's complement)
+}
+
+__global__ void __launch_bounds__(SU_THREADS) mamba2_state_update_kernel(
+    sq_mamba2_params p, const int8_t* __restrict__ x, int64_t ldx, const int8_t* __restrict__ Bm,
+    const int8_t* __restrict__ Cm, int64_t ldbc, const int8_t* __restrict__ dt, int64_t lddt,
+    const int8_t* __restrict__ z, int64_t ldz, int8_t* __restrict__ state, float* __restrict__ y, int64_t ldy) {
+  constexpr int P = 64, N = 128;   // dispatcher guarantees
+  __shared__ float sB[SU_HPC][N], sC[SU_HPC][N];
+  __shared__ float s_dA[SU_HPC], s_dt[SU_HPC];
+  const int b = blockIdx.y;
+  const int h0 = blockIdx.x * SU_HPC;
+  const int tid = threadIdx.x;
+  const int chunk = tid & 7;
+  const int r0 = tid >> 3;               // rows r0 and r0 + 32 of each head
+  // 1) every global load this thread needs, issued up front (state: 8 x 16 B)
+  int4 raw[SU_HPC][2];
+  int8_t xq[SU_HPC][2], zq[SU_HPC][2];
+  float sxr[SU_HPC][2], shr[SU_HPC][2], Dh[SU_HPC];
+#pragma unroll
+  for (int hh = 0; hh < SU_HPC; ++hh) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int row = r0 + 32 * k;
+      const int ch = (h0 + hh) * P + row;
+      raw[hh][k] = *reinterpret_cast<const int4*>(state + (((int64_t)b * p.n_heads + h0 + hh) * P + row) * N + chunk * 16);
+      xq[hh][k] = x[(int64_t)b * ldx + ch];
+      zq[hh][k] = z[(int64_t)b * ldz + ch];
+      sxr[hh][k] = p.s_x[ch];
+      shr[hh][k] = p.s_h[ch];
+    }
+    Dh[hh] = p.D[h0 + hh];
+  }
+  // 2) B̂/Ĉ of each head's group and the per-head scalars, staged once per CTA
+  for (int i = tid; i < SU_HPC * N; i += SU_THREADS) {
+    const int hh = i / N, n = i % N;
+    const int g = p.head_group[h0 + hh];
+    sB[hh][n] = __fmul_rn((float)Bm[(int64_t)b * ldbc + g * N + n], p.s_B[g]);
+    sC[hh][n] = __fmul_rn((float)Cm[(int64_t)b * ldbc + g * N + n], p.s_C[g]);
+  }
+  if (tid < SU_HPC) {
+    const int h = h0 + tid;
+    const float delta = softplus_f(__fadd_rn(__fmul_rn((float)dt[(int64_t)b * lddt + h], p.s_dt), p.dt_bias[h]));
+    s_dt[tid] = delta;
+    s_dA[tid] = expf(__fmul_rn(delta, p.A[h]));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int hh = 0; hh < SU_HPC; ++hh) {
+    const int h = h0 + hh;
+    const float dA = s_dA[hh], delta = s_dt[hh];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int row = r0 + 32 * k;
+      const int ch = h * P + row;
+      const float sh = shr[hh][k];
+      const float inv = __frcp_rn(sh);
+      const float xh = __fmul_rn((float)xq[hh][k], sxr[hh][k]);
+      const float dtx = __fmul_rn(delta, xh);
+      const float c1 = __fmul_rn(dA, sh);
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&raw[hh][k]);
+      uint32_t outw[4];
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t u = w[e] ^ 0x80808080u;
+        uint32_t q[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int n = chunk * 16 + e * 4 + i;
+          const float hq = s8byte_to_f(u, i);
+          const float hn = fmaf(c1, hq, __fmul_rn(dtx, sB[hh][n]));
+          acc = fmaf(hn, sC[hh][n], acc);
+          q[i] = f_to_s8bits(__fmul_rn(hn, inv));
+        }
+        outw[e] = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);
+      }
+      const int64_t off = (((int64_t)b * p.n_heads + h) * P + row) * N + chunk * 16;
+      *reinterpret_cast<int4*>(state + off) = make_int4(outw[0], outw[1], outw[2], outw[3]);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (chunk == 0) {
+        const float yv = __fadd_rn(acc, __fmul_rn(Dh[hh], xh));
+        const float zv = __fmul_rn((float)zq[hh][k], p.s_z);
+        y[(int64_t)b * ldy + ch] = __fmul_rn(yv, silu_f(zv));
+      }
+    }
+  }
+}
+
 }  // namespace sq
 
 using namespace sq;
@@ -208,6 +320,13 @@ extern "C" int sq_state_update_int8(const sq_mamba2_params* p, int B, const int8
                                     const int8_t* Bm, const int8_t* Cm, int64_t ldbc, const int8_t* dt,
                                     int64_t lddt, const int8_t* z, int64_t ldz, int8_t* state, float* y,
                                     int64_t ldy, void* stream) {
+  if (p && p->head_dim == 64 && p->d_state == 128 && p->n_heads % SU_HPC == 0 && ldbc % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(state) & 15) == 0) {
+    if (B == 0) return SQ_OK;
+    mamba2_state_update_kernel<<<dim3(p->n_heads / SU_HPC, B), SU_THREADS, 0, as_stream(stream)>>>(
+        *p, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, y, ldy);
+    return check_launch("sq_state_update_int8");
+  }
   return launch_mamba2<int8_t>(p, B, 1, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, 1, y, ldy,
                                as_stream(stream), "sq_state_update_int8");
 }
