@@ -76,6 +76,16 @@ __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* __restri
           off = (int64_t)gn * (K / 2) + gk / 2;
         }
         rw[i] = (gn < N && gk < K) ? *reinterpret_cast<const int4*>(w + off) : make_int4(0, 0, 0, 0);
+        if (K % 128 == 0) {   // undo the kernel-layout nibble permutation (byte j = e_j | e_{j+4} << 4)
+          uint32_t* pw = reinterpret_cast<uint32_t*>(&rw[i]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint32_t x = pw[e], lo = x & 0x0F0F0F0Fu, hi = (x >> 4) & 0x0F0F0F0Fu;
+            lo = (lo | (lo >> 4)) & 0x00FF00FFu; lo = (lo | (lo >> 8)) & 0xFFFFu;
+            hi = (hi | (hi >> 4)) & 0x00FF00FFu; hi = (hi | (hi >> 8)) & 0xFFFFu;
+            pw[e] = lo | (hi << 16);
+          }
+        }
       }
     } else {
 #pragma unroll

@@ -9,11 +9,14 @@
 //   warp 0      TMA producer: activation K-blocks [NTOK x 128 B] (SWIZZLE_128B) and, for
 //               W8, the weight K-block [128 x 128 B]
 //   warp 1      TMEM allocator + single-thread MMA issuer (4 x K=32 per stage)
-//   warps 2..9  W4: converters — each thread owns one weight row, streams its packed
-//               nibbles with coalesced 16-B loads (repacked tile layout, sq_repack_w4),
-//               expands them with a per-(row, group) byte LUT (v*sg) and writes the int8
-//               A operand straight into TMEM (tcgen05.st; kind::i8 A-from-TMEM) or into a
-//               swizzled smem tile (WMODE 2);  all: epilogue (TMEM -> regs -> HBM)
+//   warps 2..9  W4: converters — each thread owns one weight row, reads its packed
+//               nibbles from the smem ring, expands them to UINT8 (v+8)*sg with one IMUL per
+//               4 bytes and writes the A operand straight into TMEM (tcgen05.st; kind::i8
+//               A-from-TMEM) or into a swizzled smem tile (WMODE 2);  all: epilogue
+//   warp 10     W4: per-token group sums S[kb][t] of every activation tile (dp4a), used by
+//               the epilogue to undo the +8 offset:  acc -= 8 * sum_kb sg[n,kb] * S[kb][t]
+//   warp 11     W4: streams the contiguous 8 KB packed-weight tiles into a deep smem ring
+//               with 1-D bulk TMA (cp.async.bulk), so HBM latency never stalls conversion
 //
 // Split-K (small N, e.g. out_proj N=4096): SPLITS CTAs of one output tile form a cluster;
 // each reduces a token slice of the int32 partials through DSMEM in fixed rank order,
@@ -33,7 +36,8 @@ using namespace sm100;
 constexpr int TC_BN = 128;
 constexpr int TC_BK = 128;
 constexpr int TC_ACOL = 256;      // first TMEM column of the A (weight) stages in TS mode
-constexpr int TC_THREADS = 320;
+constexpr int TC_THREADS = 384;     // 12 warps: TMA, MMA, 8 converter/epilogue, group-sum, W4 stream
+constexpr int TC_MAX_KB = 64;       // max K-blocks per split (K <= 8192)
 constexpr int W4_TILE_BYTES = TC_BN * TC_BK / 2;  // 8 KB per (n-tile, k-block)
 
 enum { WM_W8 = 0, WM_W4_TS = 1, WM_W4_SS = 2 };
@@ -67,6 +71,32 @@ __device__ __forceinline__ uint32_t nib4_to_s8(uint32_t x, uint32_t L0, uint32_t
   return (p & ~mask) | (q & mask);
 }
 
+// Kernel nibble order inside every 32-bit word (set by sq_repack_w4): byte j holds
+// element j (low nibble) and element j+4 (high nibble), so one AND / one SHF+AND split a
+// word into elements 0-3 and 4-7 already in byte order.
+__host__ __device__ __forceinline__ uint32_t spread4(uint32_t x) {   // nibbles 0..3 -> bytes 0..3
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  return (x | (x << 4)) & 0x0F0F0F0Fu;
+}
+__host__ __device__ __forceinline__ uint32_t compact4(uint32_t x) {  // inverse of spread4
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  return (x | (x >> 8)) & 0x0000FFFFu;
+}
+__host__ __device__ __forceinline__ uint32_t nib_permute(uint32_t std_word) {
+  return spread4(std_word & 0xFFFFu) | (spread4(std_word >> 16) << 4);
+}
+__host__ __device__ __forceinline__ uint32_t nib_unpermute(uint32_t w) {
+  return compact4(w & 0x0F0F0F0Fu) | (compact4((w >> 4) & 0x0F0F0F0Fu) << 16);
+}
+
+// Unsigned-offset expansion for the tensor core: (v + 8) * sg  in [0, 225] per byte.
+// The A operand is fed as UINT8; the epilogue subtracts 8 * sum_g sg[n,g] * S[t,g].
+__device__ __forceinline__ void nib8_to_u8(uint32_t w, uint32_t sg, uint32_t& lo, uint32_t& hi) {
+  const uint32_t u = w ^ 0x88888888u;
+  lo = (u & 0x0F0F0F0Fu) * sg;
+  hi = ((u >> 4) & 0x0F0F0F0Fu) * sg;
+}
+
 __device__ __forceinline__ int4 ldg_stream(const void* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -90,27 +120,49 @@ __device__ __forceinline__ void epi_store(const TcArgs& a, int m, int n, int v, 
     reinterpret_cast<float*>(a.out)[o] = __fadd_rn(reinterpret_cast<float*>(a.out)[o], y);
 }
 
-template <int NTOK, int WMODE, int SPLITS, int STAGES>
+template <int NTOK, int WMODE, int SPLITS, int STAGES, int RAW>
 struct TcCfg {
+  static constexpr bool W4 = WMODE != WM_W8;
+  // offset correction on the tensor core (extra accumulators need 3*NTOK <= TC_ACOL columns)
+  static constexpr bool MMA_CORR = (WMODE == WM_W4_TS) && NTOK <= 64;
   static constexpr int ACT_BYTES = NTOK * TC_BK;
   static constexpr int W_BYTES = (WMODE == WM_W4_TS) ? 0 : TC_BN * TC_BK;
   static constexpr int STAGE_BYTES = ACT_BYTES + W_BYTES;
-  static constexpr int SMEM0 = 1024 + STAGES * STAGE_BYTES + 2 * STAGES * 8 + 64;
+  static constexpr int RAW_BYTES = W4 ? RAW * W4_TILE_BYTES : 0;
+  static constexpr int SUM_BYTES = W4 ? TC_MAX_KB * NTOK * 4 : 0;    // S[kb][t]
+  static constexpr int SGS_BYTES = W4 ? TC_MAX_KB * TC_BN : 0;        // sg[kb][row]
+  static constexpr int OFF_W = STAGES * ACT_BYTES;
+  static constexpr int OFF_RAW = OFF_W + STAGES * W_BYTES;
+  static constexpr int OFF_SUM = OFF_RAW + RAW_BYTES;
+  static constexpr int OFF_SGS = OFF_SUM + SUM_BYTES;
+  static constexpr int OFF_BAR = OFF_SGS + SGS_BYTES;
+  static constexpr int NBAR = 2 * STAGES + 2 * RAW + 2;
+  static constexpr int SMEM0 = 1024 + OFF_BAR + NBAR * 8 + 16;
   static constexpr int SMEM = SMEM0 < 120 * 1024 ? 120 * 1024 : SMEM0;   // 1 CTA/SM: TMEM alloc of 512 cols
 };
 
-template <int NTOK, int WMODE, int SPLITS, int STAGES>
+template <int NTOK, int WMODE, int SPLITS, int STAGES, int RAW>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w, TcArgs args) {
-  using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES, RAW>;
+  constexpr bool W4 = Cfg::W4;
+  // byte offsets from the extern array keep every access in the shared space (LDS/STS)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // SW128 atoms need 1 KB
   uint8_t* act = smem;
-  uint8_t* wsm = smem + STAGES * Cfg::ACT_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* wsm = smem + Cfg::OFF_W;
+  uint8_t* raw = smem + Cfg::OFF_RAW;
+  int32_t* gsum = reinterpret_cast<int32_t*>(smem + Cfg::OFF_SUM);
+  int8_t* sgs = reinterpret_cast<int8_t*>(smem + Cfg::OFF_SGS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
   uint64_t* empty = full + STAGES;
-  uint64_t* accf = empty + STAGES;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accf + 1);
+  uint64_t* rfull = empty + STAGES;
+  uint64_t* rempty = rfull + RAW;
+  uint64_t* accf = rempty + RAW;
+  uint64_t* corr_ready = accf + 1;     // MMA_CORR: H/L tiles + TMEM sg column written
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(corr_ready + 1);
+  uint8_t* bh = smem + Cfg::OFF_SUM;                 // MMA_CORR: S>>7 as [2 ksteps][NTOK x 32 B] no-swizzle
+  uint8_t* bl = bh + 2 * NTOK * 32;                  //           S&127
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tile = blockIdx.x, split = blockIdx.y, m_tile = blockIdx.z;
@@ -120,13 +172,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], WMODE == WM_W8 ? 1 : 1 + 8);
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], W4 ? 1 + 8 : 1);      // TMA (+ 8 converter warps)
+      mbar_init(&empty[s], W4 ? 2 : 1);         // MMA commit (+ group-sum warp)
+    }
+    for (int r = 0; r < RAW; ++r) {
+      mbar_init(&rfull[r], 1);
+      mbar_init(&rempty[r], 8);
     }
     mbar_init(accf, 1);
+    mbar_init(corr_ready, 1 + 4);        // group-sum warp + the 4 sg-staging converter warps
     fence_barrier_init();
     tma_prefetch(&tm_act);
-    if (WMODE == WM_W8) tma_prefetch(&tm_w);
+    if (!W4) tma_prefetch(&tm_w);
   }
   if (warp == 1) tmem_alloc<512>(tmem_holder);
   tc_fence_before();
@@ -135,20 +192,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {
+    // ---------------- activation (and W8 weight) TMA producer
     if (lane == 0) {
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[s], Cfg::ACT_BYTES + (WMODE == WM_W8 ? Cfg::W_BYTES : 0));
+        mbar_arrive_expect_tx(&full[s], Cfg::ACT_BYTES + (W4 ? 0 : Cfg::W_BYTES));
         tma_load_2d(act + s * Cfg::ACT_BYTES, &tm_act, &full[s], (kb_begin + i) * TC_BK, m_tile * NTOK);
-        if (WMODE == WM_W8)
-          tma_load_2d(wsm + s * Cfg::W_BYTES, &tm_w, &full[s], (kb_begin + i) * TC_BK, n_tile * TC_BN);
+        if (!W4) tma_load_2d(wsm + s * Cfg::W_BYTES, &tm_w, &full[s], (kb_begin + i) * TC_BK, n_tile * TC_BN);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
+    // ---------------- single-thread MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_i8(TC_BN, NTOK);
+      // W4: A = (v+8)*sg as UINT8 (corrected in the epilogue); W8: signed x signed
+      constexpr uint32_t idesc = W4 ? (idesc_i8(TC_BN, NTOK) & ~(7u << 7)) : idesc_i8(TC_BN, NTOK);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         mbar_wait(&full[s], (i / STAGES) & 1);
@@ -166,7 +225,71 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         mma_commit(&empty[s]);
       }
+      if (Cfg::MMA_CORR) {
+        // dH = sum_kb sg[n,kb] * (S[kb][t] >> 7), dL = sum_kb sg[n,kb] * (S[kb][t] & 127)
+        mbar_wait(corr_ready, 0);
+        tc_fence_after();
+        constexpr uint32_t id_h = (idesc_i8(TC_BN, NTOK) & ~(7u << 7));                  // u8 x s8
+        constexpr uint32_t id_l = (idesc_i8(TC_BN, NTOK) & ~(7u << 7)) & ~(7u << 10);    // u8 x u8
+        const int ksteps = (nkb + 31) / 32;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          mma_i8_ts(tmem + 64, tmem + 192 + ks * 8, desc_noswz(bh + ks * NTOK * 32, 128, 256), id_h, ks > 0);
+          mma_i8_ts(tmem + 128, tmem + 192 + ks * 8, desc_noswz(bl + ks * NTOK * 32, 128, 256), id_l, ks > 0);
+        }
+      }
       mma_commit(accf);
+    }
+    __syncwarp();
+  } else if (warp == 10) {
+    // ---------------- group sums S[kb][t] of every activation tile (W4 only)
+    if (W4) {
+      if (Cfg::MMA_CORR) {   // zero the (padded) K range of both B tiles
+        for (int o = lane * 16; o < 4 * NTOK * 32; o += 32 * 16) *reinterpret_cast<int4*>(bh + o) = make_int4(0, 0, 0, 0);
+        __syncwarp();
+      }
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&full[s], (i / STAGES) & 1);
+        const uint8_t* tile = act + s * Cfg::ACT_BYTES;
+        for (int t = lane; t < NTOK; t += 32) {
+          int acc = 0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {   // any chunk order sums the row; rotate per lane -> no bank conflicts
+            const int4 v = *reinterpret_cast<const int4*>(tile + t * TC_BK + ((c ^ (t & 7)) * 16));
+            acc = __dp4a(v.x, 0x01010101, acc);
+            acc = __dp4a(v.y, 0x01010101, acc);
+            acc = __dp4a(v.z, 0x01010101, acc);
+            acc = __dp4a(v.w, 0x01010101, acc);
+          }
+          if (Cfg::MMA_CORR) {
+            // element (t, kb) of a no-swizzle K-major [NTOK x 32 B] tile per 32-kb step
+            const int o = (i >> 5) * NTOK * 32 + (t >> 3) * 256 + ((i >> 4) & 1) * 128 + (t & 7) * 16 + (i & 15);
+            bh[o] = (uint8_t)(acc >> 7);
+            bl[o] = (uint8_t)(acc & 127);
+          } else {
+            gsum[i * NTOK + t] = acc;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      if (Cfg::MMA_CORR) {
+        fence_proxy_async_smem();          // generic smem writes -> tensor-core (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(corr_ready);
+      }
+      named_bar(1, 288);   // sums complete -> epilogue warps
+    }
+  } else if (warp == 11) {
+    // ---------------- packed W4 tiles: contiguous 8 KB per (n-tile, k-block) -> smem ring
+    if (W4 && lane == 0) {
+      const uint8_t* src = args.w4 + ((size_t)n_tile * nkb_total + kb_begin) * W4_TILE_BYTES;
+      for (int i = 0; i < nkb; ++i) {
+        const int r = i % RAW;
+        mbar_wait(&rempty[r], ((i / RAW) & 1) ^ 1);
+        mbar_arrive_expect_tx(&rfull[r], W4_TILE_BYTES);
+        bulk_load(raw + r * W4_TILE_BYTES, src + (size_t)i * W4_TILE_BYTES, W4_TILE_BYTES, &rfull[r]);
+      }
     }
     __syncwarp();
   } else {
@@ -175,48 +298,76 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int row = q * 32 + lane;
     const int n = n_tile * TC_BN + row;
     const bool valid_n = n < args.N;
-    if (WMODE != WM_W8) {
-      // Batched converter: D K-blocks are converted, stored (TMEM or smem) and released
-      // together, so the tcgen05.st / proxy-fence latency is paid once per batch while
-      // the next batch's weight loads are already in flight.
-      constexpr int D = 4;
-      const uint8_t* wsrc = args.w4 + (size_t)n_tile * nkb_total * W4_TILE_BYTES + row * 16 + half * 2 * 2048;
-      const int ng = args.K / args.group;
-      const int8_t* sgrow = args.sg + (size_t)(valid_n ? n : 0) * ng;
-      int4 buf[D][2];
-      int sgb[D];
-      auto fetch = [&](int i, int j) {
-        if (i < nkb && valid_n) {
-          const uint8_t* p = wsrc + (size_t)(kb_begin + i) * W4_TILE_BYTES;
-          buf[j][0] = ldg_stream(p);
-          buf[j][1] = ldg_stream(p + 2048);
-          sgb[j] = sgrow[(kb_begin + i) * TC_BK / args.group];
-        } else {
-          buf[j][0] = buf[j][1] = make_int4(0, 0, 0, 0);
-          sgb[j] = 0;
-        }
-      };
+    if (W4) {
+      const int8_t* sgr = args.sg + (size_t)(valid_n ? n : 0) * (args.K / args.group);
+      if (half == 0) {
+        // all of this row's group scales (<= 64 bytes, zero beyond nkb) in registers
+        const int8_t* p = sgr + kb_begin * TC_BK / args.group;
+        int4 v[TC_MAX_KB / 16];
+        if (args.group == TC_BK && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (nkb & 15) == 0) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) fetch(j, j);
+          for (int c = 0; c < TC_MAX_KB / 16; ++c)
+            v[c] = (valid_n && c * 16 < nkb) ? *reinterpret_cast<const int4*>(p + c * 16) : make_int4(0, 0, 0, 0);
+        } else {
+          uint32_t wds[TC_MAX_KB / 4];
+#pragma unroll
+          for (int w = 0; w < TC_MAX_KB / 4; ++w) wds[w] = 0;
+#pragma unroll
+          for (int i = 0; i < TC_MAX_KB; ++i)
+            if (valid_n && i < nkb) wds[i / 4] |= (uint32_t)(uint8_t)sgr[(kb_begin + i) * TC_BK / args.group] << (8 * (i % 4));
+#pragma unroll
+          for (int c = 0; c < TC_MAX_KB / 16; ++c) v[c] = make_int4(wds[c * 4], wds[c * 4 + 1], wds[c * 4 + 2], wds[c * 4 + 3]);
+        }
+#pragma unroll
+        for (int c = 0; c < TC_MAX_KB / 16; ++c)
+          if (c * 16 < nkb) {
+            const uint32_t wq[4] = {(uint32_t)v[c].x, (uint32_t)v[c].y, (uint32_t)v[c].z, (uint32_t)v[c].w};
+#pragma unroll
+            for (int e = 0; e < 16; ++e) sgs[(c * 16 + e) * TC_BN + row] = (int8_t)(wq[e / 4] >> (8 * (e % 4)));
+          }
+        if (Cfg::MMA_CORR) {   // A operand of the correction MMAs: sg[row][kb] in TMEM cols 192..207
+          uint32_t cw[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            cw[c * 4] = v[c].x; cw[c * 4 + 1] = v[c].y; cw[c * 4 + 2] = v[c].z; cw[c * 4 + 3] = v[c].w;
+          }
+          tmem_st_x16(tmem + ((uint32_t)(q * 32) << 16) + 192, cw);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(corr_ready);
+        }
+      }
+      named_bar(2, 256);                 // converter warps: sg staged
+      constexpr int D = STAGES >= 8 ? 4 : (STAGES >= 4 ? 2 : 1);   // batch < STAGES (no self-wait)
       for (int i0 = 0; i0 < nkb; i0 += D) {
         uint32_t wv[D][16];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-          const uint32_t sg = (uint32_t)sgb[j];
-          const uint32_t L0 = sg * 0x03020100u, L1 = sg * 0x07060504u;
-          const uint32_t L2 = ~(sg * 0x05060708u) + 0x01010101u, L3 = ~(sg * 0x01020304u) + 0x01010101u;
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const uint32_t* pw = reinterpret_cast<const uint32_t*>(&buf[j][c]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              wv[j][c * 8 + e * 2] = nib4_to_s8(pw[e], L0, L1, L2, L3);
-              wv[j][c * 8 + e * 2 + 1] = nib4_to_s8(pw[e] >> 16, L0, L1, L2, L3);
-            }
+          const int i = i0 + j;
+          if (i < nkb) {
+            const int r = i % RAW;
+            mbar_wait(&rfull[r], (i / RAW) & 1);
+            const uint8_t* rp = raw + r * W4_TILE_BYTES + half * 2 * 2048 + row * 16;
+            const uint4 p0 = *reinterpret_cast<const uint4*>(rp);
+            const uint4 p1 = *reinterpret_cast<const uint4*>(rp + 2048);
+            const uint32_t sg = (uint32_t)(uint8_t)sgs[i * TC_BN + row];
+            nib8_to_u8(p0.x, sg, wv[j][0], wv[j][1]);
+            nib8_to_u8(p0.y, sg, wv[j][2], wv[j][3]);
+            nib8_to_u8(p0.z, sg, wv[j][4], wv[j][5]);
+            nib8_to_u8(p0.w, sg, wv[j][6], wv[j][7]);
+            nib8_to_u8(p1.x, sg, wv[j][8], wv[j][9]);
+            nib8_to_u8(p1.y, sg, wv[j][10], wv[j][11]);
+            nib8_to_u8(p1.z, sg, wv[j][12], wv[j][13]);
+            nib8_to_u8(p1.w, sg, wv[j][14], wv[j][15]);
           }
         }
+        __syncwarp();
+        if (lane == 0) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) fetch(i0 + D + j, j);   // next batch in flight
+          for (int j = 0; j < D; ++j)
+            if (i0 + j < nkb) mbar_arrive(&rempty[(i0 + j) % RAW]);
+        }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           const int i = i0 + j;
@@ -251,36 +402,53 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
-    // ---------------- epilogue
+    // ---------------- epilogue: TMEM -> registers -> (offset correction) -> HBM / DSMEM
     mbar_wait(accf, 0);
     tc_fence_after();
+    if (W4) named_bar(1, 288);           // group sums ready
     const float alpha = (valid_n && args.epi != SQ_EPI_I32) ? args.alpha[n] : 0.f;
     const float cs = (valid_n && args.epi == SQ_EPI_QUANT) ? args.col_scale[n] : 1.f;
     constexpr int CH = NTOK / 2;
-    constexpr int CW = CH < 8 ? CH : 8;
-    if (SPLITS == 1) {
+    int32_t* red = reinterpret_cast<int32_t*>(act);     // split-K: [NTOK][128], aliases the act stages
 #pragma unroll 1
-      for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 8) {
-        uint32_t v[8];
-        tmem_ld_x8(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+    for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 8) {
+      uint32_t v[8];
+      tmem_ld_x8(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
+      tmem_wait_ld();
+      int val[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) val[j] = (int)v[j];
+      if (Cfg::MMA_CORR) {
+        uint32_t vh[8], vl[8];
+        tmem_ld_x8(tmem + ((uint32_t)(q * 32) << 16) + 64 + c0, vh);
+        tmem_ld_x8(tmem + ((uint32_t)(q * 32) << 16) + 128 + c0, vl);
         tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) val[j] -= 1024 * (int)vh[j] + 8 * (int)vl[j];
+      } else if (W4) {
+        // undo the +8 offset of the unsigned weight operand: acc -= 8 * sum_kb sg[n,kb] * S[kb][t]
+        int corr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+        for (int i = 0; i < nkb; ++i) {
+          const int sgv = sgs[i * TC_BN + row];
+          const int4 g0 = *reinterpret_cast<const int4*>(&gsum[i * NTOK + c0]);
+          const int4 g1 = *reinterpret_cast<const int4*>(&gsum[i * NTOK + c0 + 4]);
+          corr[0] += sgv * g0.x; corr[1] += sgv * g0.y; corr[2] += sgv * g0.z; corr[3] += sgv * g0.w;
+          corr[4] += sgv * g1.x; corr[5] += sgv * g1.y; corr[6] += sgv * g1.z; corr[7] += sgv * g1.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) val[j] -= 8 * corr[j];
+      }
+      if (SPLITS == 1) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int m = m_tile * NTOK + c0 + j;
-          if (valid_n && m < args.M) epi_store(args, m, n, (int)v[j], alpha, cs);
+          if (valid_n && m < args.M) epi_store(args, m, n, val[j], alpha, cs);
         }
-      }
-    } else {
-      int32_t* red = reinterpret_cast<int32_t*>(act);     // [NTOK][128], aliases the act stages
-#pragma unroll 1
-      for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 8) {
-        uint32_t v[8];
-        tmem_ld_x8(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
-        tmem_wait_ld();
+      } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) red[(c0 + j) * TC_BN + row] = (int)v[j];
+        for (int j = 0; j < 8; ++j) red[(c0 + j) * TC_BN + row] = val[j];
       }
-      (void)CW;
     }
   }
 
@@ -344,11 +512,13 @@ static int make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
 
 template <int NTOK, int WMODE, int SPLITS>
 static int launch_tc(const int8_t* a, int64_t lda, const uint8_t* w, const TcArgs& args, cudaStream_t st) {
-  constexpr int STAGE_BYTES = TcCfg<NTOK, WMODE, SPLITS, 1>::STAGE_BYTES;
-  constexpr int ST0 = (200 * 1024) / STAGE_BYTES;
+  constexpr int RAW = WMODE == WM_W8 ? 1 : (NTOK <= 64 ? 12 : (NTOK == 128 ? 8 : 6));
+  using C1 = TcCfg<NTOK, WMODE, SPLITS, 1, RAW>;
+  constexpr int ST0 = (210 * 1024 - C1::RAW_BYTES - C1::SUM_BYTES - C1::SGS_BYTES) / C1::STAGE_BYTES;
   constexpr int STAGES = ST0 > 8 ? 8 : (ST0 < 2 ? 2 : ST0);
-  using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES>;
-  auto kern = gemm_tc_kernel<NTOK, WMODE, SPLITS, STAGES>;
+  using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES, RAW>;
+  static_assert(Cfg::SMEM <= 227 * 1024, "smem budget");
+  auto kern = gemm_tc_kernel<NTOK, WMODE, SPLITS, STAGES, RAW>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -426,9 +596,12 @@ int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg,
   const int nkb = K / TC_BK;
   int splits = 1;
   while (splits < 8 && tiles * splits * 2 <= 148 && nkb / (splits * 2) >= 4 && ntok % (splits * 2) == 0) splits *= 2;
+  if (w4 && (nkb + splits - 1) / splits > TC_MAX_KB) return SQ_ERR_ARG;
   TcArgs args{w, sg, group, alpha, M, N, K, epi, out, ldo, col_scale};
   if (!w4) return dispatch_split<WM_W8>(splits, ntok, a, lda, w, args, st);
-  if (g_tc_w4_mode == WM_W4_SS) return dispatch_split<WM_W4_SS>(splits, ntok, a, lda, w, args, st);
+  // A-from-TMEM is used up to 128-token tiles (the 256-column accumulator leaves too few
+  // TMEM columns for the A stages); larger tiles stage the expanded weights in smem.
+  if (g_tc_w4_mode == WM_W4_SS || ntok > 128) return dispatch_split<WM_W4_SS>(splits, ntok, a, lda, w, args, st);
   return dispatch_split<WM_W4_TS>(splits, ntok, a, lda, w, args, st);
 }
 
@@ -445,6 +618,10 @@ __global__ void repack_w4_kernel(const uint8_t* __restrict__ src, int N, int K, 
   const int n = tile * TC_BN + row;
   int4 v = make_int4(0, 0, 0, 0);
   if (n < N) v = *reinterpret_cast<const int4*>(src + (int64_t)n * (K / 2) + kb * 64 + chunk * 16);
+  v.x = (int)nib_permute((uint32_t)v.x);
+  v.y = (int)nib_permute((uint32_t)v.y);
+  v.z = (int)nib_permute((uint32_t)v.z);
+  v.w = (int)nib_permute((uint32_t)v.w);
   *reinterpret_cast<int4*>(dst + idx * 16) = v;
 }
 
@@ -458,7 +635,12 @@ __global__ void unpack_w4_kernel(const uint8_t* __restrict__ src, int N, int K, 
   const int chunk = idx % 4;
   const int tile = n / TC_BN, row = n % TC_BN;
   const int64_t s = ((((int64_t)tile * nkb + kb) * 4 + chunk) * TC_BN + row) * 16;
-  *reinterpret_cast<int4*>(dst + (int64_t)n * (K / 2) + kb * 64 + chunk * 16) = *reinterpret_cast<const int4*>(src + s);
+  int4 v = *reinterpret_cast<const int4*>(src + s);
+  v.x = (int)nib_unpermute((uint32_t)v.x);
+  v.y = (int)nib_unpermute((uint32_t)v.y);
+  v.z = (int)nib_unpermute((uint32_t)v.z);
+  v.w = (int)nib_unpermute((uint32_t)v.w);
+  *reinterpret_cast<int4*>(dst + (int64_t)n * (K / 2) + kb * 64 + chunk * 16) = v;
 }
 
 int64_t w4_layout_bytes(int N, int K) {

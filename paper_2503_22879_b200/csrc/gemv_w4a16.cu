@@ -8,7 +8,6 @@
 
 namespace sq {
 
-constexpr int kGemvMaxM = 8;
 
 // Tiled-layout GEMV (K % 128 == 0; layout of sq_repack_w4): a CTA owns 128 weight rows;
 // warp w reads row quadrant (w & 3) and K-half (w >> 2) of every 128-wide K-block, so a
@@ -75,7 +74,7 @@ __global__ void __launch_bounds__(256) gemv_w4a16_tiled_kernel(const float* __re
               float wv[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                wv[i] = __uint_as_float(((u >> (4 * (i4 * 4 + i))) & 0xFu) | 0x4B000000u) - 8388616.0f;
+                wv[i] = __uint_as_float(((u >> (8 * i + 4 * i4)) & 0xFu) | 0x4B000000u) - 8388616.0f;   // byte i = e_i | e_{i+4}<<4
 #pragma unroll
               for (int m = 0; m < MT; ++m) {
                 const float4 xv = *reinterpret_cast<const float4*>(&xs[m * K + k0 + e * 8 + i4 * 4]);

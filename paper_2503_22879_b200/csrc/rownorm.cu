@@ -94,6 +94,125 @@ __global__ void __launch_bounds__(NT) gate_norm_had_quant_kernel(const float* __
   }
 }
 
+// ---- register-resident variants: one thread per 16 contiguous elements (D/16 threads) ----
+__device__ __forceinline__ double block_sum_dyn(double v, double* red) {
+  v = warp_sum_d(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double t = l < nw ? red[l] : 0.0;
+    t = warp_sum_d(t);
+    if (l == 0) red[0] = t;
+  }
+  __syncthreads();
+  return red[0];
+}
+
+__device__ __forceinline__ void load16(const float* p, float (&v)[16]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float4 f = *reinterpret_cast<const float4*>(p + e * 4);
+    v[e * 4] = f.x; v[e * 4 + 1] = f.y; v[e * 4 + 2] = f.z; v[e * 4 + 3] = f.w;
+  }
+}
+
+__device__ __forceinline__ void store16_q(int8_t* p, const float (&v)[16], float s) {
+  uint32_t w[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    w[e] = (uint32_t)(uint8_t)quant8(v[e * 4], s) | ((uint32_t)(uint8_t)quant8(v[e * 4 + 1], s) << 8) |
+           ((uint32_t)(uint8_t)quant8(v[e * 4 + 2], s) << 16) | ((uint32_t)(uint8_t)quant8(v[e * 4 + 3], s) << 24);
+  }
+  *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <bool QUANT>
+__global__ void __launch_bounds__(1024) rmsnorm16_kernel(const float* __restrict__ x, int64_t ldx,
+                                                         const float* __restrict__ gamma, float eps, float s, int D,
+                                                         void* __restrict__ out, int64_t ldo) {
+  __shared__ double red[32];
+  const int base = threadIdx.x * 16;
+  float v[16], g[16];
+  load16(x + (int64_t)blockIdx.x * ldx + base, v);
+  load16(gamma + base, g);
+  double ss = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) ss += (double)v[i] * (double)v[i];
+  ss = block_sum_dyn(ss, red);
+  const float r = rms_factor(ss, D, eps);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
+  if (QUANT) {
+    store16_q(reinterpret_cast<int8_t*>(out) + (int64_t)blockIdx.x * ldo + base, v, s);
+  } else {
+    float* o = reinterpret_cast<float*>(out) + (int64_t)blockIdx.x * ldo + base;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) *reinterpret_cast<float4*>(o + e * 4) = make_float4(v[e * 4], v[e * 4 + 1], v[e * 4 + 2], v[e * 4 + 3]);
+  }
+}
+
+// Gated-norm + blocked Sylvester FWHT + quant with the row in registers: stages h < 16
+// inside a thread, 16 <= h < 512 across lanes (shfl_xor), h >= 512 through smem.
+// Every butterfly is the oracle's f32 a+b / a-b, in the oracle's stage order.
+__global__ void __launch_bounds__(1024) gate_norm_had_quant16_kernel(const float* __restrict__ y, int64_t ldy,
+                                                                     const float* __restrict__ gamma, float eps,
+                                                                     float s_y, int blk, int D,
+                                                                     int8_t* __restrict__ out, int64_t ldo) {
+  extern __shared__ float buf[];
+  __shared__ double red[32];
+  const int base = threadIdx.x * 16;
+  const int lane = threadIdx.x & 31;
+  float v[16], g[16];
+  load16(y + (int64_t)blockIdx.x * ldy + base, v);
+  load16(gamma + base, g);
+  double ss = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) ss += (double)v[i] * (double)v[i];
+  ss = block_sum_dyn(ss, red);
+  const float r = rms_factor(ss, D, eps);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
+#pragma unroll
+  for (int h = 1; h < 16; h <<= 1) {
+    if (h < blk) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if ((i & h) == 0) {
+          const float a = v[i], b = v[i + h];
+          v[i] = __fadd_rn(a, b);
+          v[i + h] = __fsub_rn(a, b);
+        }
+      }
+    }
+  }
+  for (int m = 1; m < 32 && 16 * m < blk; m <<= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float o = __shfl_xor_sync(0xffffffffu, v[i], m);
+      v[i] = upper ? __fsub_rn(o, v[i]) : __fadd_rn(v[i], o);
+    }
+  }
+  if (blk > 512) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      *reinterpret_cast<float4*>(buf + base + e * 4) = make_float4(v[e * 4], v[e * 4 + 1], v[e * 4 + 2], v[e * 4 + 3]);
+    __syncthreads();
+    for (int h = 512; h < blk; h <<= 1) {
+      for (int idx = threadIdx.x; idx < D / 2; idx += blockDim.x) {
+        const int i = (idx / h) * 2 * h + (idx % h);
+        const float a = buf[i], b = buf[i + h];
+        buf[i] = __fadd_rn(a, b);
+        buf[i + h] = __fsub_rn(a, b);
+      }
+      __syncthreads();
+    }
+    load16(buf + base, v);
+  }
+  store16_q(out + (int64_t)blockIdx.x * ldo + base, v, s_y);
+}
+
 __global__ void quantize_kernel(const float* __restrict__ x, int64_t ldx, float s, int D, int8_t* __restrict__ out,
                                 int64_t ldo) {
   const float* r = x + (int64_t)blockIdx.x * ldx;
@@ -152,7 +271,10 @@ extern "C" int sq_rmsnorm_quant(const float* x, int64_t ldx, const float* gamma,
                                 int D, int8_t* out, int64_t ldo, void* stream) {
   SQ_REQUIRE(M >= 0 && D > 0 && s > 0.f, SQ_ERR_SHAPE, "sq_rmsnorm_quant: bad M/D/s");
   if (M == 0) return SQ_OK;
-  rmsnorm_kernel<256, true><<<M, 256, 0, as_stream(stream)>>>(x, ldx, gamma, eps, s, D, out, ldo);
+  if (D % 512 == 0 && D / 16 <= 1024 && ldx % 4 == 0 && ldo % 16 == 0)
+    rmsnorm16_kernel<true><<<M, D / 16, 0, as_stream(stream)>>>(x, ldx, gamma, eps, s, D, out, ldo);
+  else
+    rmsnorm_kernel<256, true><<<M, 256, 0, as_stream(stream)>>>(x, ldx, gamma, eps, s, D, out, ldo);
   return check_launch("sq_rmsnorm_quant");
 }
 
@@ -160,7 +282,10 @@ extern "C" int sq_rmsnorm_f32(const float* x, int64_t ldx, const float* gamma, f
                               float* out, int64_t ldo, void* stream) {
   SQ_REQUIRE(M >= 0 && D > 0, SQ_ERR_SHAPE, "sq_rmsnorm_f32: bad M/D");
   if (M == 0) return SQ_OK;
-  rmsnorm_kernel<256, false><<<M, 256, 0, as_stream(stream)>>>(x, ldx, gamma, eps, 1.f, D, out, ldo);
+  if (D % 512 == 0 && D / 16 <= 1024 && ldx % 4 == 0 && ldo % 4 == 0)
+    rmsnorm16_kernel<false><<<M, D / 16, 0, as_stream(stream)>>>(x, ldx, gamma, eps, 1.f, D, out, ldo);
+  else
+    rmsnorm_kernel<256, false><<<M, 256, 0, as_stream(stream)>>>(x, ldx, gamma, eps, 1.f, D, out, ldo);
   return check_launch("sq_rmsnorm_f32");
 }
 
@@ -172,6 +297,13 @@ extern "C" int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* 
   if (M == 0) return SQ_OK;
   const int blk = hadamard ? (D & -D) : 1;
   const size_t smem = (size_t)D * sizeof(float);
+  if (D % 512 == 0 && D / 16 <= 1024 && ldy % 4 == 0 && ldo % 16 == 0) {
+    auto k16 = gate_norm_had_quant16_kernel;
+    const size_t sm16 = blk > 512 ? smem : 0;
+    if (sm16 > 48 * 1024) cudaFuncSetAttribute(k16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm16);
+    k16<<<M, D / 16, sm16, as_stream(stream)>>>(y, ldy, gamma, eps, s_y, blk, D, out, ldo);
+    return check_launch("sq_gate_norm_had_quant");
+  }
   auto k = gate_norm_had_quant_kernel<512>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k<<<M, 512, smem, as_stream(stream)>>>(y, ldy, gamma, eps, s_y, blk, D, out, ldo);

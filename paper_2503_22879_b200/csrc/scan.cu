@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(SU_THREADS) mamba2_state_update_kernel(
     const int8_t* __restrict__ Cm, int64_t ldbc, const int8_t* __restrict__ dt, int64_t lddt,
     const int8_t* __restrict__ z, int64_t ldz, int8_t* __restrict__ state, float* __restrict__ y, int64_t ldy) {
   constexpr int P = 64, N = 128;   // dispatcher guarantees
-  __shared__ float sB[SU_HPC][N], sC[SU_HPC][N];
+  __shared__ __align__(16) float sB[SU_HPC][N];
+  __shared__ __align__(16) float sC[SU_HPC][N];
   __shared__ float s_dA[SU_HPC], s_dt[SU_HPC];
   const int b = blockIdx.y;
   const int h0 = blockIdx.x * SU_HPC;
@@ -263,6 +264,14 @@ __global__ void __launch_bounds__(SU_THREADS) mamba2_state_update_kernel(
   for (int hh = 0; hh < SU_HPC; ++hh) {
     const int h = h0 + hh;
     const float dA = s_dA[hh], delta = s_dt[hh];
+    float bv[16], cvv[16];    // this thread's 16 state columns of B̂ / Ĉ (smem broadcast)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float4 b4 = *reinterpret_cast<const float4*>(&sB[hh][chunk * 16 + e * 4]);
+      const float4 c4 = *reinterpret_cast<const float4*>(&sC[hh][chunk * 16 + e * 4]);
+      bv[e * 4] = b4.x; bv[e * 4 + 1] = b4.y; bv[e * 4 + 2] = b4.z; bv[e * 4 + 3] = b4.w;
+      cvv[e * 4] = c4.x; cvv[e * 4 + 1] = c4.y; cvv[e * 4 + 2] = c4.z; cvv[e * 4 + 3] = c4.w;
+    }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int row = r0 + 32 * k;
@@ -281,10 +290,10 @@ __global__ void __launch_bounds__(SU_THREADS) mamba2_state_update_kernel(
         uint32_t q[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const int n = chunk * 16 + e * 4 + i;
+          const int n = e * 4 + i;
           const float hq = s8byte_to_f(u, i);
-          const float hn = fmaf(c1, hq, __fmul_rn(dtx, sB[hh][n]));
-          acc = fmaf(hn, sC[hh][n], acc);
+          const float hn = fmaf(c1, hq, __fmul_rn(dtx, bv[n]));
+          acc = fmaf(hn, cvv[n], acc);
           q[i] = f_to_s8bits(__fmul_rn(hn, inv));
         }
         outw[e] = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);

@@ -56,6 +56,17 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (size multiple of 16 B, 16-B aligned), tx-counted.
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ---------------------------------------------------------------- TMEM
 template <int NCOLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {  // whole warp
@@ -101,6 +112,13 @@ __device__ __forceinline__ void tmem_st_x16(uint32_t a, const uint32_t (&r)[16])
 __device__ __forceinline__ uint64_t desc_sw128(const void* smem_tile) {
   const uint64_t addr = smem_u32(smem_tile);
   return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// K-major operand tile without swizzle: 8-row x 16-B core matrices, `lbo` bytes between
+// K-adjacent core matrices, `sbo` bytes between 8-row groups.
+__device__ __forceinline__ uint64_t desc_noswz(const void* smem_tile, uint32_t lbo, uint32_t sbo) {
+  const uint64_t addr = smem_u32(smem_tile);
+  return ((addr >> 4) & 0x3FFFull) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) |
+         (1ull << 46);
 }
 // Instruction descriptor: kind::i8, s8 x s8 -> s32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
