@@ -601,7 +601,10 @@ int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg,
   if (!w4) return dispatch_split<WM_W8>(splits, ntok, a, lda, w, args, st);
   // A-from-TMEM is used up to 128-token tiles (the 256-column accumulator leaves too few
   // TMEM columns for the A stages); larger tiles stage the expanded weights in smem.
-  if (g_tc_w4_mode == WM_W4_SS || ntok > 128) return dispatch_split<WM_W4_SS>(splits, ntok, a, lda, w, args, st);
+  // SS (weights expanded into smem) is used without split-K only: with split-K at 64-token
+  // tiles it showed a rare wrong-atom race in repeated runs (under investigation).
+  if (ntok > 128) return dispatch_split<WM_W4_SS>(1, ntok, a, lda, w, args, st);
+  if (g_tc_w4_mode == WM_W4_SS && splits == 1) return dispatch_split<WM_W4_SS>(1, ntok, a, lda, w, args, st);
   return dispatch_split<WM_W4_TS>(splits, ntok, a, lda, w, args, st);
 }
 

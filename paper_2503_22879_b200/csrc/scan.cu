@@ -210,6 +210,13 @@ __device__ __forceinline__ float s8byte_to_f(uint32_t u_xor80, int i) {
   return __int_as_float(bits) - 8388736.0f;
 }
 
+__device__ __forceinline__ float s8byte_to_f_raw(uint32_t u_xor80, int i) {
+  // 2^23 + 128 + (signed byte i); subtract 8388736 to get the value
+  uint32_t bits;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(bits) : "r"(u_xor80), "r"(0x4B000000u), "r"(0x7440u | (uint32_t)i));
+  return __int_as_float(bits);
+}
+
 __device__ __forceinline__ uint32_t f_to_s8bits(float v) {
   v = fminf(fmaxf(v, -128.f), 127.f);
   return __float_as_uint(v + 12582912.0f);   // low byte = rint(v) (two's complement)
@@ -277,27 +284,35 @@ __global__ void __launch_bounds__(SU_THREADS) mamba2_state_update_kernel(
       const int row = r0 + 32 * k;
       const int ch = h * P + row;
       const float sh = shr[hh][k];
-      const float inv = __frcp_rn(sh);
       const float xh = __fmul_rn((float)xq[hh][k], sxr[hh][k]);
       const float dtx = __fmul_rn(delta, xh);
-      const float c1 = __fmul_rn(dA, sh);
+      // scaled units t = h'/s_h = Ȧ·q + (Δx̂/s_h)·B̂: the requant is rint(t), and
+      // y = s_h·Σ t·Ĉ.  Pairs of state columns go through packed FFMA2/FMUL2/FADD2.
+      const float rs = __fdiv_rn(dtx, sh);
+      const float2 dA2 = make_float2(dA, dA), rs2 = make_float2(rs, rs);
+      const float2 mg = make_float2(-8388736.0f, -8388736.0f);
       const uint32_t* w = reinterpret_cast<const uint32_t*>(&raw[hh][k]);
       uint32_t outw[4];
-      float acc = 0.f;
+      float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t u = w[e] ^ 0x80808080u;
         uint32_t q[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 4; i += 2) {
           const int n = e * 4 + i;
-          const float hq = s8byte_to_f(u, i);
-          const float hn = fmaf(c1, hq, __fmul_rn(dtx, bv[n]));
-          acc = fmaf(hn, cvv[n], acc);
-          q[i] = f_to_s8bits(__fmul_rn(hn, inv));
+          float2 hq = make_float2(s8byte_to_f_raw(u, i), s8byte_to_f_raw(u, i + 1));
+          hq = __fadd2_rn(hq, mg);
+          const float2 t = __ffma2_rn(dA2, hq, __fmul2_rn(rs2, make_float2(bv[n], bv[n + 1])));
+          acc2 = __ffma2_rn(t, make_float2(cvv[n], cvv[n + 1]), acc2);
+          const float2 cl = make_float2(fminf(fmaxf(t.x, -128.f), 127.f), fminf(fmaxf(t.y, -128.f), 127.f));
+          const float2 rq = __fadd2_rn(cl, make_float2(12582912.0f, 12582912.0f));   // low byte = rint
+          q[i] = __float_as_uint(rq.x);
+          q[i + 1] = __float_as_uint(rq.y);
         }
         outw[e] = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);
       }
+      float acc = __fmul_rn(sh, __fadd_rn(acc2.x, acc2.y));
       const int64_t off = (((int64_t)b * p.n_heads + h) * P + row) * N + chunk * 16;
       *reinterpret_cast<int4*>(state + off) = make_int4(outw[0], outw[1], outw[2], outw[3]);
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -308,6 +323,102 @@ __global__ void __launch_bounds__(SU_THREADS) mamba2_state_update_kernel(
         const float zv = __fmul_rn((float)zq[hh][k], p.s_z);
         y[(int64_t)b * ldy + ch] = __fmul_rn(yv, silu_f(zv));
       }
+    }
+  }
+}
+
+// Barrier-free variant: CTA = (sequence, 2 heads) x 256 threads; thread t owns head
+// t >> 7, state columns [16*(t&7), +16) of rows ((t&127)>>3) + 16k, k = 0..3.  Every
+// thread issues all of its loads (4 x 16-B state pieces, its 16 B̂ / Ĉ codes, per-row and
+// per-head scalars) up front and computes its head's Δ / Ȧ itself — no smem, no
+// __syncthreads, ~64 registers, so 4 CTAs (32 warps) per SM keep HBM busy.
+__global__ void __launch_bounds__(256, 3) mamba2_state_update2_kernel(
+    sq_mamba2_params p, const int8_t* __restrict__ x, int64_t ldx, const int8_t* __restrict__ Bm,
+    const int8_t* __restrict__ Cm, int64_t ldbc, const int8_t* __restrict__ dt, int64_t lddt,
+    const int8_t* __restrict__ z, int64_t ldz, int8_t* __restrict__ state, float* __restrict__ y, int64_t ldy) {
+  constexpr int P = 64, N = 128;
+  const int b = blockIdx.y;
+  const int h = blockIdx.x * 2 + (threadIdx.x >> 7);
+  const int t = threadIdx.x & 127;
+  const int chunk = t & 7;
+  const int r0 = t >> 3;
+  const int g = p.head_group[h];
+  int8_t* st_base = state + (((int64_t)b * p.n_heads + h) * P) * N + chunk * 16;
+  int4 raw[4];
+  int8_t xq[4], zq[4];
+  float sxr[4], shr[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int row = r0 + 16 * k;
+    raw[k] = *reinterpret_cast<const int4*>(st_base + (int64_t)row * N);
+    const int ch = h * P + row;
+    xq[k] = x[(int64_t)b * ldx + ch];
+    zq[k] = z[(int64_t)b * ldz + ch];
+    sxr[k] = p.s_x[ch];
+    shr[k] = p.s_h[ch];
+  }
+  const int4 bq = *reinterpret_cast<const int4*>(Bm + (int64_t)b * ldbc + g * N + chunk * 16);
+  const int4 cq = *reinterpret_cast<const int4*>(Cm + (int64_t)b * ldbc + g * N + chunk * 16);
+  const float sB = p.s_B[g], sC = p.s_C[g];
+  const float delta = softplus_f(__fadd_rn(__fmul_rn((float)dt[(int64_t)b * lddt + h], p.s_dt), p.dt_bias[h]));
+  const float dA = expf(__fmul_rn(delta, p.A[h]));
+  const float Dh = p.D[h];
+  // B̂ / Ĉ for this thread's 16 columns (exact: f32(code) * scale)
+  float2 bv[8], cv[8];
+  {
+    const uint32_t* bw = reinterpret_cast<const uint32_t*>(&bq);
+    const uint32_t* cw = reinterpret_cast<const uint32_t*>(&cq);
+    const float2 mg = make_float2(-8388736.0f, -8388736.0f);
+    const float2 sB2 = make_float2(sB, sB), sC2 = make_float2(sC, sC);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t ub = bw[e] ^ 0x80808080u, uc = cw[e] ^ 0x80808080u;
+#pragma unroll
+      for (int i = 0; i < 4; i += 2) {
+        bv[e * 2 + i / 2] = __fmul2_rn(__fadd2_rn(make_float2(s8byte_to_f_raw(ub, i), s8byte_to_f_raw(ub, i + 1)), mg), sB2);
+        cv[e * 2 + i / 2] = __fmul2_rn(__fadd2_rn(make_float2(s8byte_to_f_raw(uc, i), s8byte_to_f_raw(uc, i + 1)), mg), sC2);
+      }
+    }
+  }
+  const float2 dA2 = make_float2(dA, dA);
+  const float2 mg = make_float2(-8388736.0f, -8388736.0f);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int row = r0 + 16 * k;
+    const float sh = shr[k];
+    const float xh = __fmul_rn((float)xq[k], sxr[k]);
+    const float rs = __fdiv_rn(__fmul_rn(delta, xh), sh);   // t = h'/s_h = Ȧ·q + (Δx̂/s_h)·B̂
+    const float2 rs2 = make_float2(rs, rs);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&raw[k]);
+    uint32_t outw[4];
+    float2 acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t u = w[e] ^ 0x80808080u;
+      uint32_t q[4];
+#pragma unroll
+      for (int i = 0; i < 4; i += 2) {
+        const int n2 = e * 2 + i / 2;
+        const float2 hq = __fadd2_rn(make_float2(s8byte_to_f_raw(u, i), s8byte_to_f_raw(u, i + 1)), mg);
+        const float2 tt = __ffma2_rn(dA2, hq, __fmul2_rn(rs2, bv[n2]));
+        acc2 = __ffma2_rn(tt, cv[n2], acc2);
+        const float2 cl = make_float2(fminf(fmaxf(tt.x, -128.f), 127.f), fminf(fmaxf(tt.y, -128.f), 127.f));
+        const float2 rq = __fadd2_rn(cl, make_float2(12582912.0f, 12582912.0f));   // low byte = rint
+        q[i] = __float_as_uint(rq.x);
+        q[i + 1] = __float_as_uint(rq.y);
+      }
+      outw[e] = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);
+    }
+    *reinterpret_cast<int4*>(st_base + (int64_t)row * N) = make_int4(outw[0], outw[1], outw[2], outw[3]);
+    float acc = __fmul_rn(sh, __fadd_rn(acc2.x, acc2.y));
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if (chunk == 0) {
+      const int ch = h * P + row;
+      const float yv = __fadd_rn(acc, __fmul_rn(Dh, xh));
+      const float zv = __fmul_rn((float)zq[k], p.s_z);
+      y[(int64_t)b * ldy + ch] = __fmul_rn(yv, silu_f(zv));
     }
   }
 }
@@ -332,7 +443,7 @@ extern "C" int sq_state_update_int8(const sq_mamba2_params* p, int B, const int8
   if (p && p->head_dim == 64 && p->d_state == 128 && p->n_heads % SU_HPC == 0 && ldbc % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(state) & 15) == 0) {
     if (B == 0) return SQ_OK;
-    mamba2_state_update_kernel<<<dim3(p->n_heads / SU_HPC, B), SU_THREADS, 0, as_stream(stream)>>>(
+    mamba2_state_update2_kernel<<<dim3(p->n_heads / 2, B), 256, 0, as_stream(stream)>>>(
         *p, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, y, ldy);
     return check_launch("sq_state_update_int8");
   }

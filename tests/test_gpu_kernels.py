@@ -218,3 +218,21 @@ def test_decode_matches_oracle_steps(cuda, profile):
         go, gst = block_forward_quantized(torch.as_tensor(u[t:t + 1], device=cuda), blk, state=gst)
         worst = max(worst, np.abs(go.cpu().numpy() - ro).max() / np.abs(ro).max())
     assert worst < 5e-2, worst
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 4096, 8192), (64, 8192, 4096), (16, 1024, 8192)])
+def test_gemm_w4a8_tc_repeat_deterministic(cuda, M, N, K):
+    """Split-K cluster reduction and async pipelines: 8 launches on fresh data, all exact."""
+    ops = _ops()
+    from paper_2503_22879_b200.ssm_block import pack_u4_host
+    r = _rng(9, M, N)
+    ops.set_gemm_mode(1)
+    for _ in range(8):
+        a = r.integers(-128, 128, (M, K)).astype(np.int8)
+        codes = r.integers(-8, 8, (N, K)).astype(np.int8)
+        sg = r.integers(1, 16, (N, K // 128)).astype(np.int8)
+        ql = oq.QLinear("w4a8", codes, s_ch=np.ones(N, np.float32), sg=sg, group=128)
+        tw = ops.repack_w4(torch.as_tensor(pack_u4_host(codes), device=cuda), N, K)
+        got = ops.gemm_w4a8(torch.as_tensor(a, device=cuda), tw, torch.as_tensor(sg, device=cuda), 128,
+                            torch.ones(N, device=cuda), N, ops.EPI_I32).cpu().numpy()
+        assert np.array_equal(got, int_gemm(a, ql.int8_weight().T))
