@@ -72,6 +72,10 @@ class ScaleLayout:
             raise LayoutError("scales must be > 0")
         if self.kind == "PerTensor":
             return np.broadcast_to(s.reshape(()), shape)
+        if self.kind == "PerGroup" and nd == 2 and ax == 1 and s.size == shape[0] * (-(-shape[1] // self.group_size)):
+            # weight [out × in] with one scale per (row, group)
+            g = np.minimum(np.arange(shape[1]) // self.group_size, s.size // shape[0] - 1)
+            return s.reshape(shape[0], -1)[:, g]
         if self.kind == "PerRow":
             ax = 0
         if self.kind in ("PerChannel", "PerRow"):
