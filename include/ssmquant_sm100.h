@@ -149,6 +149,35 @@ int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T,
                     const float* dt, int64_t lddt, const float* z, int64_t ldz,
                     float* state, int state_in, float* y, int64_t ldy, void* stream);
 
+/* Mamba2 decode step (K5 decode + K9 + K6), the SSM half of a block for one token per
+ * sequence, from the in_proj requant codes zx[b] = z | x | B | C | dt:
+ *   conv-cache stepping + SiLU + requant of x, B, C  (ssm_block.causal_conv1d with cache,
+ *   SPEC.md:281-289; same int8 math as sq_conv1d_update_int8), dequantised with the
+ *   clustered x / per-group B,C scales into the f32 workspace `ws` together with the
+ *   per-channel scan scalars,
+ *   int8 SSM state update h' = exp(dt*A) h + dt*x*B, y = C.h' + D*x, y*SiLU(z)
+ *   (selective_scan T=1) -> y,
+ *   RMSNorm over d_inner + Sylvester FWHT + quant with s_y -> yq.
+ * Three launches on `stream`.  State and conv cache are updated in place; ws
+ * (sq_mamba2_decode_ws_bytes) and y [B x d_inner] f32 are caller-owned (y holds the gated
+ * SSM output). */
+typedef struct {
+  sq_mamba2_params ssm;
+  int conv_kernel;
+  const float* conv_w;      /* [conv_dim x conv_kernel]                              */
+  const float* conv_b;      /* [conv_dim]                                            */
+  const float* conv_s_in;   /* [conv_dim] scales of the in_proj x|B|C codes          */
+  const float* conv_s_out;  /* [conv_dim] clustered x scales | per-group B, C scales */
+  const float* norm_w;      /* [d_inner]                                             */
+  float eps, s_y;
+  int hadamard;
+} sq_mamba2_decode_params;
+
+int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, int B);
+int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
+                               int8_t* conv_cache /*[B x (Kc-1) x conv_dim]*/, int8_t* state,
+                               void* ws, float* y, int64_t ldy, int8_t* yq, int64_t ldyq, void* stream);
+
 typedef struct {
   int d_inner, d_state;
   const float* A;              /* [d_inner x N]                                        */

@@ -263,7 +263,7 @@ def block_step_batched(u, qb: QBlock, states: list):
     return np.concatenate(outs, axis=0), new
 
 
-def decode_step_batched(u, qb: QBlock, h_codes, conv_codes):
+def decode_step_batched(u, qb: QBlock, h_codes, conv_codes, trace=None):
     """Mamba2 A8 decode step for b independent sequences at once (same math as
     ``block_forward_quantized`` with T=1; vectorised over the batch for the CPU
     baseline).  u [b×d_model]; h_codes [b×nh×P×N] int8; conv_codes [b×C×(K-1)] int8.
@@ -301,4 +301,6 @@ def decode_step_batched(u, qb: QBlock, h_codes, conv_codes):
     r = rmsnorm(y, qb.norm_weight)
     yq = had.hadamard_quantize(r, had.HadamardPlan(di, "none", qb.s_y), 8) if qb.hadamard else quantize_codes(r, qb.s_y, 8)
     out, _ = qlinear_a8(yq, qb.out_proj, qb.s_y)
+    if trace is not None:
+        trace.update(in_codes=codes, conv_codes=cq, y=y, y_q=yq)
     return out, quantize_codes(h, ss, 8), np.ascontiguousarray(win[:, :, 1:]).astype(np.int8)

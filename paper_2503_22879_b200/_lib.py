@@ -26,6 +26,11 @@ class Mamba2Params(C.Structure):
                 ("s_dt", _flt), ("s_z", _flt), ("s_x", _vp), ("s_B", _vp), ("s_C", _vp), ("s_h", _vp)]
 
 
+class Mamba2DecodeParams(C.Structure):
+    _fields_ = [("ssm", Mamba2Params), ("conv_kernel", _int), ("conv_w", _vp), ("conv_b", _vp), ("conv_s_in", _vp),
+                ("conv_s_out", _vp), ("norm_w", _vp), ("eps", _flt), ("s_y", _flt), ("hadamard", _int)]
+
+
 class Mamba1Params(C.Structure):
     _fields_ = [("d_inner", _int), ("d_state", _int), ("A", _vp), ("D", _vp), ("dt_bias", _vp),
                 ("s_dt", _flt), ("s_z", _flt), ("s_B", _flt), ("s_C", _flt), ("s_x", _vp), ("s_h", _vp)]
@@ -58,6 +63,9 @@ _SIGS = {
                          _vp, _int, _vp, _i64, _vp], _int),
     "sq_selective_scan_int8": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                                 _vp, _int, _vp, _i64, _vp], _int),
+    "sq_mamba2_decode_ws_bytes": ([C.POINTER(Mamba2DecodeParams), _int], _i64),
+    "sq_mamba2_decode_step_int8": ([C.POINTER(Mamba2DecodeParams), _int, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp,
+                                    _i64, _vp], _int),
     "sq_gate_norm_had_quant": ([_vp, _i64, _vp, _flt, _flt, _int, _int, _int, _vp, _i64, _vp], _int),
 }
 

@@ -76,6 +76,9 @@ class QuantizedMambaLM:
               "y": e((M, d.d_inner), torch.float32), "yq": e((M, d.d_inner), torch.int8),
               "hq": e((M, d.d_model), torch.int8), "logits": e((M, self.vocab), torch.float32),
               "tok": e((M,), torch.int32)}
+        fused = [b for b in self.blocks if getattr(b, "fused_decode", False)]
+        if fused:
+            ws["dws"] = e((ops.mamba2_decode_ws_bytes(fused[0].decode_params, M),), torch.uint8)
         if any(not b.a8 for b in self.blocks):
             ws.update(uf=e((M, d.d_model), torch.float32), zxf=e((M, d.in_proj_out), torch.float32),
                       convf=e((M, d.conv_dim), torch.float32), r=e((M, d.d_inner), torch.float32))

@@ -232,6 +232,44 @@ def mamba2_params(n_heads, head_dim, d_state, n_groups, head_group, A, D, dt_bia
                              _opt(s_C), _opt(s_h))
 
 
+def mamba2_decode_params(ssm: _lib.Mamba2Params, conv_w, conv_b, conv_s_in, conv_s_out, norm_w, eps, s_y,
+                         hadamard=True) -> _lib.Mamba2DecodeParams:
+    return _lib.Mamba2DecodeParams(ssm, int(conv_w.shape[1]), conv_w.data_ptr(), conv_b.data_ptr(),
+                                   conv_s_in.data_ptr(), conv_s_out.data_ptr(), norm_w.data_ptr(), float(eps),
+                                   float(s_y), int(bool(hadamard)))
+
+
+def mamba2_decode_ws_bytes(p, B) -> int:
+    return int(lib().sq_mamba2_decode_ws_bytes(C.byref(p), B))
+
+
+def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=None):
+    """Mamba2 decode step, SSM half of a block (conv update + int8 state update + gated
+    norm + FWHT + quant).  zx int8 [B x in_proj_out] (z|x|B|C|dt codes); conv_cache int8
+    [B x (K-1) x conv_dim]; state int8 [B x nh x P x N] (both updated in place).  Returns
+    yq int8 [B x d_inner]; ``y`` (f32 [B x d_inner], gated SSM output) and ``ws`` (uint8,
+    mamba2_decode_ws_bytes) are workspaces, allocated when not given."""
+    _dev(zx, torch.int8, "zx", 2)
+    _dev(conv_cache, torch.int8, "conv_cache")
+    _dev(state, torch.int8, "state")
+    di = p.ssm.n_heads * p.ssm.head_dim
+    if yq is None:
+        yq = torch.empty((B, di), dtype=torch.int8, device=zx.device)
+    if y is None:
+        y = torch.empty((B, di), dtype=torch.float32, device=zx.device)
+    nbytes = mamba2_decode_ws_bytes(p, B)
+    if ws is None:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=zx.device)
+    if ws.numel() * ws.element_size() < nbytes:
+        raise ShapeError(f"decode workspace needs {nbytes} bytes")
+    _dev(yq, torch.int8, "yq", 2)
+    _dev(y, torch.float32, "y", 2)
+    _check(lib().sq_mamba2_decode_step_int8(C.byref(p), B, zx.data_ptr(), _ld(zx), conv_cache.data_ptr(),
+                                            state.data_ptr(), ws.data_ptr(), y.data_ptr(), _ld(y), yq.data_ptr(),
+                                            _ld(yq), _stream()))
+    return yq
+
+
 def mamba1_params(d_inner, d_state, A, D, dt_bias, s_dt, s_z, s_B, s_C, s_x, s_h) -> _lib.Mamba1Params:
     return _lib.Mamba1Params(d_inner, d_state, A.data_ptr(), D.data_ptr(), dt_bias.data_ptr(), float(s_dt),
                              float(s_z), float(s_B), float(s_C), s_x.data_ptr(), s_h.data_ptr())

@@ -217,6 +217,8 @@ class DeviceBlock:
         self.profile = qb.profile
         self.a8 = qb.profile in ("W8A8", "W4A8")
         self.hadamard = bool(getattr(qb, "hadamard", True))
+        self.fused_decode = (qb.profile in ("W8A8", "W4A8") and d.variant == "mamba2" and d.head_dim == 64
+                             and d.d_state in (64, 128))
         f = lambda a: _t(np.asarray(a, np.float32), torch.float32, dev)
         self.s_u = np.float32(qb.s_u)
         self.s_y = np.float32(qb.s_y)
@@ -246,6 +248,9 @@ class DeviceBlock:
                 self.params = ops.mamba2_params(d.n_heads, d.head_dim, d.d_state, d.n_state_groups, self.head_group,
                                                 self.A, self.D, self.dt_bias, ios[2 * di + 2 * gn], ios[0],
                                                 self.s_x, self.s_B, self.s_C, self.state_scale)
+                self.decode_params = ops.mamba2_decode_params(self.params, self.conv_w, self.conv_b,
+                                                              self.conv_in_scale, self.conv_out_scale, self.norm_w,
+                                                              EPS_NORM, self.s_y, self.hadamard)
             else:
                 R, N = d.dt_rank, d.d_state
                 ios = np.asarray(qb.in_out_scale, np.float32)
@@ -295,6 +300,13 @@ class DeviceBlock:
         if d.variant == "mamba2":
             gn = d.n_state_groups * d.d_state
             xbc = zx[:, di:2 * di + 2 * gn]
+            if T == 1 and state_in and self.fused_decode:
+                # conv update + int8 state update + gated norm + FWHT + quant (sq_mamba2_decode_step_int8)
+                yq = ops.mamba2_decode_step_int8(self.decode_params, B, zx, state.conv_cache, state.h, ws.get("yq"),
+                                                 y, ws.get("dws"))
+                if resid is not None:
+                    return self.out_proj.a8(yq, ops.EPI_RESID, resid)
+                return self.out_proj.a8(yq, ops.EPI_F32, ws.get("out"))
             if T == 1 and state_in:
                 cv = ops.conv1d_update_int8(xbc, self.conv_w, self.conv_b, self.conv_in_scale, self.conv_out_scale,
                                             state.conv_cache, ws.get("conv"))

@@ -22,6 +22,9 @@ cv = ops.conv1d_update_int8(zx[:, di:2 * di + 2 * gn], blk.conv_w, blk.conv_b, b
                             st.conv_cache)
 y = torch.empty((B, di), device=dev)
 for _ in range(3):
+    if which in ("all", "fused"):
+        cc = st.conv_cache
+        ops.mamba2_decode_step_int8(blk.decode_params, B, zx, cc, st.h, y=y)
     if which in ("all", "state"):
         ops.state_update_int8(blk.params, B, cv[:, :di], cv[:, di:di + gn], cv[:, di + gn:], zx[:, 2 * di + 2 * gn:],
                               zx[:, :di], st.h, y)

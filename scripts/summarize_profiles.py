@@ -30,7 +30,7 @@ def launches(tag, src="launches.csv", name="launches"):
         if len(r) <= vi:
             continue
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         k = r[ki].split("(")[0][:70]
         agg[k][0] += 1
         agg[k][1] += v
