@@ -76,9 +76,10 @@ int sq_repack_w4(const uint8_t* u4packed, int N, int K, uint8_t* dst, void* stre
 int sq_unpack_w4(const uint8_t* src, int N, int K, uint8_t* u4packed, void* stream);
 
 /* ---- model glue --------------------------------------------------------------------- */
-/* out[m,:] = clamp(rint((x[m,:] * rsqrt(mean x^2 + eps)) * gamma / s)) */
+/* out[m,:] = clamp(rint((x[m,:] * rsqrt(mean x^2 + eps)) * gamma / s));  gsum (optional)
+ * receives the sums of the output codes over every 128-wide block, int32 [M x D/128]. */
 int sq_rmsnorm_quant(const float* x, int64_t ldx, const float* gamma, float eps, float s,
-                     int M, int D, int8_t* out, int64_t ldo, void* stream);
+                     int M, int D, int8_t* out, int64_t ldo, int32_t* gsum, int64_t ldg, void* stream);
 /* out[m,:] = x[m,:] * rsqrt(mean x^2 + eps) * gamma (f32) */
 int sq_rmsnorm_f32(const float* x, int64_t ldx, const float* gamma, float eps,
                    int M, int D, float* out, int64_t ldo, void* stream);
@@ -94,10 +95,14 @@ int sq_argmax_f32(const float* logits, int64_t ld, int M, int N, int32_t* tok, v
 int sq_gemm_w8a8(const int8_t* a, int64_t lda, const int8_t* w /*[N x K]*/, const float* alpha,
                  int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
                  void* stream);
+/* a_gsum (optional, NULL = computed in the kernel): sums of the activation codes over every
+ * 128-wide K block, int32 [M x K/128] with row stride ld_gsum, as emitted by
+ * sq_rmsnorm_quant / sq_mamba2_decode_step_int8 for the tensor (the W4 operand is fed to
+ * the tensor core as (v+8)*sg and these sums undo the offset). */
 int sq_gemm_w4a8(const int8_t* a, int64_t lda, const uint8_t* w4 /*repacked*/,
                  const int8_t* sg /*[N x K/group]*/, int group, const float* alpha,
                  int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
-                 void* stream);
+                 const int32_t* a_gsum, int64_t ld_gsum, void* stream);
 /* y[m,n] (+)= sum_g s_group[n,g] * sum_{k in g} w4[n,k] * half(x[m,k]);  resid!=0 adds in place */
 int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4 /*repacked*/,
                   const float* s_group /*[N x K/group]*/, int group, int M, int N, int K,
@@ -176,7 +181,8 @@ typedef struct {
 int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, int B);
 int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
                                int8_t* conv_cache /*[B x (Kc-1) x conv_dim]*/, int8_t* state,
-                               void* ws, float* y, int64_t ldy, int8_t* yq, int64_t ldyq, void* stream);
+                               void* ws, float* y, int64_t ldy, int8_t* yq, int64_t ldyq,
+                               int32_t* yq_gsum /*optional [B x d_inner/128]*/, int64_t ldg, void* stream);
 
 typedef struct {
   int d_inner, d_state;

@@ -44,13 +44,13 @@ _SIGS = {
     "sq_w4_bytes": ([_int, _int], _i64),
     "sq_repack_w4": ([_vp, _int, _int, _vp, _vp], _int),
     "sq_unpack_w4": ([_vp, _int, _int, _vp, _vp], _int),
-    "sq_rmsnorm_quant": ([_vp, _i64, _vp, _flt, _flt, _int, _int, _vp, _i64, _vp], _int),
+    "sq_rmsnorm_quant": ([_vp, _i64, _vp, _flt, _flt, _int, _int, _vp, _i64, _vp, _i64, _vp], _int),
     "sq_rmsnorm_f32": ([_vp, _i64, _vp, _flt, _int, _int, _vp, _i64, _vp], _int),
     "sq_quantize_f32": ([_vp, _i64, _flt, _int, _int, _vp, _i64, _vp], _int),
     "sq_embed_int8": ([_vp, _vp, _vp, _int, _int, _vp, _vp], _int),
     "sq_argmax_f32": ([_vp, _i64, _int, _int, _vp, _vp], _int),
     "sq_gemm_w8a8": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp], _int),
-    "sq_gemm_w4a8": ([_vp, _i64, _vp, _vp, _int, _vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp], _int),
+    "sq_gemm_w4a8": ([_vp, _i64, _vp, _vp, _int, _vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp, _i64, _vp], _int),
     "sq_gemv_w4a16": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _int, _vp], _int),
     "sq_conv1d_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _i64, _vp], _int),
     "sq_conv1d_update_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _vp, _vp, _i64, _vp], _int),
@@ -65,7 +65,7 @@ _SIGS = {
                                 _vp, _int, _vp, _i64, _vp], _int),
     "sq_mamba2_decode_ws_bytes": ([C.POINTER(Mamba2DecodeParams), _int], _i64),
     "sq_mamba2_decode_step_int8": ([C.POINTER(Mamba2DecodeParams), _int, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp,
-                                    _i64, _vp], _int),
+                                    _i64, _vp, _i64, _vp], _int),
     "sq_gate_norm_had_quant": ([_vp, _i64, _vp, _flt, _flt, _int, _int, _int, _vp, _i64, _vp], _int),
 }
 

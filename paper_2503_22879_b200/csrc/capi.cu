@@ -1,6 +1,7 @@
 // C-ABI plumbing: version, thread-local last error, device check.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -22,6 +23,14 @@ int check_launch(const char* what) {
     return SQ_ERR_CUDA;
   }
   return SQ_OK;
+}
+
+bool pdl_enabled(int cls) {
+  static const int mask = [] {
+    const char* e = getenv("SQ_PDL");
+    return e ? atoi(e) : 16;   // default: GEMMs only (measured best, scripts/bench_pdl.sh)
+  }();
+  return (mask & cls) != 0;
 }
 
 }  // namespace sq

@@ -16,7 +16,9 @@
 //                            packed f32x2 FMAs; the requant is a magic-number rint (FADD2) +
 //                            cvt.pack.sat, exact because |Δx̂/s_h·B̂| is clamped to 2^21
 //                            (saturation keeps the sign); y = s_h·Σ t·Ĉ + D·x̂, gated by SiLU(ẑ).
-//  K6   norm_had_kernel      one thread-block cluster per sequence (CL <= 8 CTAs of <= 1024
+//  K6   norm_had8192_kernel  d_inner = 8192: one CTA per row, FWHT in three register phases
+//                            joined by two swizzled smem transposes;
+//       norm_had_kernel      other widths: one thread-block cluster per sequence (CL <= 8 CTAs of <= 1024
 //                            channels): Σy² reduced across the cluster in f64 (rank order),
 //                            r·γ, Sylvester FWHT stages in the oracle's order — in registers,
 //                            shuffles, smem, and across CTAs through DSMEM for Hadamard
@@ -24,6 +26,8 @@
 // Numerics vs the oracle (oracle/qblock.py decode_step_batched): conv codes op-for-op; state
 // codes and yq within one quantization step (fused FMA / scaled-unit update, f32 y sum);
 // tested with mismatch fractions in tests/test_gpu_decode.py.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -82,7 +86,7 @@ __device__ __forceinline__ int8_t conv_step(const sq_mamba2_decode_params& P, in
 // Four consecutive channels c..c+3 with Kc = 4: every load issued up front (3 cache
 // words, the new codes, 4x4 taps, bias / scales as float4), same per-channel op order.
 __device__ __forceinline__ void conv4_step(const sq_mamba2_decode_params& P, int c, int C,
-                                           int8_t* __restrict__ cache_b, const int8_t* __restrict__ xnew,
+                                           int8_t* __restrict__ cache_b, const int8_t* xnew,
                                            int8_t (&code)[4]) {
   const uint32_t w0 = *reinterpret_cast<const uint32_t*>(cache_b + c);
   const uint32_t w1 = *reinterpret_cast<const uint32_t*>(cache_b + C + c);
@@ -107,7 +111,8 @@ __device__ __forceinline__ void conv4_step(const sq_mamba2_decode_params& P, int
       const float q = (float)(int8_t)(win[j] >> (8 * e));
       acc = __fadd_rn(acc, __fmul_rn(fget(taps[e], j), __fmul_rn(q, s_in)));
     }
-    code[e] = quant8(silu_f(acc), fget(so, e));
+    const float so_e = fget(so, e);
+    code[e] = quant8_inv(silu_fast(acc), so_e, __frcp_rn(so_e));
   }
 }
 
@@ -129,13 +134,15 @@ __device__ __forceinline__ int bc_swz(int n, int N) {
 
 // ------------------------------------------------------------------ K5d: conv + scan operands
 __global__ void __launch_bounds__(256) prep_kernel(const sq_mamba2_decode_params P, int C, int di, int GN,
-                                                  const int8_t* __restrict__ zx, int64_t ldzx,
+                                                  const int8_t* zx, int64_t ldzx,
                                                   int8_t* __restrict__ cache, float* __restrict__ ws, int B,
                                                   int vec) {
   const sq_mamba2_params& S = P.ssm;
   const int N = S.d_state, nh = S.n_heads;
   const int b = blockIdx.y;
   const int Kc = P.conv_kernel;
+  pdl_trigger();
+  pdl_wait();
   const int8_t* zrow = zx + (int64_t)b * ldzx;
   int8_t* cache_b = cache + (int64_t)b * (Kc - 1) * C;
   float* rows_b = ws + (int64_t)b * nh * DS_ROWF;
@@ -160,8 +167,8 @@ __global__ void __launch_bounds__(256) prep_kernel(const sq_mamba2_decode_params
       const float xh = __fmul_rn((float)q[e], so);
       const float sh = S.s_h[c + e];
       rf[p] = xh;
-      rf[DS_P + p] = fminf(fmaxf(__fdiv_rn(__fmul_rn(delta, xh), sh), -rsmax), rsmax);
-      rf[2 * DS_P + p] = silu_f(__fmul_rn((float)zrow[c + e], S.s_z));
+      rf[DS_P + p] = fminf(fmaxf(__fmul_rn(__fmul_rn(delta, xh), __frcp_rn(sh)), -rsmax), rsmax);
+      rf[2 * DS_P + p] = silu_fast(__fmul_rn((float)zrow[c + e], S.s_z));
       rf[3 * DS_P + p] = sh;
       if (p == 0) {
         rf[4 * DS_P] = expf(__fmul_rn(delta, S.A[h]));
@@ -208,6 +215,7 @@ __global__ void __launch_bounds__(SR_THREADS, 2) state_ring_kernel(const sq_mamb
   const int nh = S.n_heads, GN = S.n_groups * N;
   const int ntiles_all = B * nh;
   const int ntiles = (ntiles_all - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  pdl_trigger();
   if (tid == 0) {
     for (int i = 0; i < SR_NSLOT; ++i) {
       mbar_init(&full[i], 1);
@@ -216,6 +224,7 @@ __global__ void __launch_bounds__(SR_THREADS, 2) state_ring_kernel(const sq_mamb
     fence_barrier_init();
   }
   __syncthreads();
+  pdl_wait();   // prep outputs (ws) and the state: produced / last written by earlier grids
   const float* bc_all = ws + ds_rows_floats(B, nh);
   if (warp == SR_CONSUMERS) {
     // ---------------- producer: state tile + row scalars + B̂|Ĉ of the head's group
@@ -239,14 +248,17 @@ __global__ void __launch_bounds__(SR_THREADS, 2) state_ring_kernel(const sq_mamb
   const int chunk = tid & 7, rq = tid >> 3;
   const float2 MG = make_float2(-8388736.0f, -8388736.0f);
   const float2 RM = make_float2(12582912.0f, 12582912.0f);
+  const int gstep = gridDim.x;
+  const int db = gstep / nh, dh = gstep % nh;   // tile t -> (b, h) advanced incrementally
+  int b = blockIdx.x / nh, h = blockIdx.x % nh;
+  const uint32_t full0 = smem_u32(full);
   for (int i = 0; i < ntiles; ++i) {
-    const int t = blockIdx.x + i * gridDim.x;
-    const int b = t / nh, h = t % nh;
+    const int t = b * nh + h;
     const int slot = i % SR_NSLOT;
     const uint8_t* sl = smem + slot * Cfg::SLOT;
     const float* rf = reinterpret_cast<const float*>(sl + Cfg::TILE);
     const float* bcs = reinterpret_cast<const float*>(sl + Cfg::TILE + Cfg::ROWB);
-    mbar_wait(&full[slot], (i / SR_NSLOT) & 1);
+    mbar_wait_addr(full0 + slot * 8, (i / SR_NSLOT) & 1);
     float2 bv[CPT / 2], cv[CPT / 2];
 #pragma unroll
     for (int e = 0; e < CPT / 4; ++e) {
@@ -305,13 +317,19 @@ __global__ void __launch_bounds__(SR_THREADS, 2) state_ring_kernel(const sq_mamb
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
+    h += dh;
+    b += db;
+    if (h >= nh) {
+      h -= nh;
+      ++b;
+    }
   }
 }
 
 // ------------------------------------------------------------------ K6: norm + FWHT + quant
 // cluster of `cl` CTAs per sequence, CTA r owns channels [r*CH, (r+1)*CH), E = CH/256 each thread
 __global__ void __launch_bounds__(256) norm_had_kernel(const sq_mamba2_decode_params P, int di, int CH, int cl,
-                                                      int blk, const float* __restrict__ y, int64_t ldy,
+                                                      int blk, const float* y, int64_t ldy,
                                                       int8_t* __restrict__ yq, int64_t ldyq) {
   __shared__ __align__(16) float ys[DS_MAXCH];
   __shared__ double red[9];
@@ -320,6 +338,8 @@ __global__ void __launch_bounds__(256) norm_had_kernel(const sq_mamba2_decode_pa
   const int b = blockIdx.y;
   const int c0 = rank * CH;
   const int E = CH / 256;
+  pdl_trigger();
+  pdl_wait();
   float v[4];
   double ss = 0.0;
   const float* yr = y + (int64_t)b * ldy + c0 + tid * E;
@@ -457,6 +477,133 @@ __global__ void __launch_bounds__(256) norm_had_kernel(const sq_mamba2_decode_pa
   if (cl > 1) cluster_sync();   // peers may still be reading this CTA's smem
 }
 
+// ------------------------------------------------------------------ K6 (d_inner = 8192): one CTA per row
+// 256 threads x 32 values.  The 13 Sylvester stages run in three register phases, bits
+// [0,5) on each thread's contiguous 32 values, bits [5,10) and [10,13) after two swizzled
+// smem transposes (chunk q of 4 floats stored at q ^ ((q >> 3) & 7): conflict-free for the
+// contiguous, stride-32 and stride-1024 access patterns).  Same butterflies, same order as
+// the oracle; the RMS sum is f64.
+__device__ __forceinline__ int had_swz(int i) {   // float index -> swizzled float index
+  const int q = i >> 2;
+  return ((q ^ ((q >> 3) & 7)) << 2) | (i & 3);
+}
+
+__global__ void __launch_bounds__(256) norm_had8192_kernel(const sq_mamba2_decode_params P, const float* y,
+                                                          int64_t ldy, int8_t* __restrict__ yq, int64_t ldyq,
+                                                          int32_t* __restrict__ gsum, int64_t ldg) {
+  constexpr int D = 8192;
+  __shared__ __align__(16) float buf[D];
+  __shared__ double red[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int b = blockIdx.x;
+  float v[32];
+  const float4* src = reinterpret_cast<const float4*>(y + (int64_t)b * ldy + t * 32);
+  const float4* gam = reinterpret_cast<const float4*>(P.norm_w + t * 32);
+  float4 gm[8];
+  pdl_trigger();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) gm[j] = __ldg(gam + j);
+  pdl_wait();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 q = src[j];
+    v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+  }
+  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int e = 0; e < 32; ++e) s4[e & 3] += (double)v[e] * (double)v[e];
+  double ss = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  ss = warp_sum_d(ss);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  double tot = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float isy = __frcp_rn(P.s_y);
+  const float ms = (float)(tot / (double)D);
+  const float rf = __fdiv_rn(1.0f, sqrtf(__fadd_rn(ms, P.eps)));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 g = gm[j];
+    v[4 * j] = __fmul_rn(__fmul_rn(v[4 * j], rf), g.x);
+    v[4 * j + 1] = __fmul_rn(__fmul_rn(v[4 * j + 1], rf), g.y);
+    v[4 * j + 2] = __fmul_rn(__fmul_rn(v[4 * j + 2], rf), g.z);
+    v[4 * j + 3] = __fmul_rn(__fmul_rn(v[4 * j + 3], rf), g.w);
+  }
+  int8_t* out = yq + (int64_t)b * ldyq;
+  if (!P.hadamard) {
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      w[j] = (uint32_t)(uint8_t)quant8_inv(v[4 * j], P.s_y, isy) | ((uint32_t)(uint8_t)quant8_inv(v[4 * j + 1], P.s_y, isy) << 8) |
+             ((uint32_t)(uint8_t)quant8_inv(v[4 * j + 2], P.s_y, isy) << 16) | ((uint32_t)(uint8_t)quant8_inv(v[4 * j + 3], P.s_y, isy) << 24);
+    *reinterpret_cast<uint4*>(out + t * 32) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(out + t * 32 + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+    return;
+  }
+  // phase A: bits 0..4 (contiguous values of this thread)
+#pragma unroll
+  for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if ((e & h) == 0) {
+        const float x0 = v[e], x1 = v[e + h];
+        v[e] = __fadd_rn(x0, x1);
+        v[e + h] = __fsub_rn(x0, x1);
+      }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(buf + had_swz(t * 32 + 4 * j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  __syncthreads();
+  // phase B: bits 5..9; thread holds i = (t_hi << 10) | (k << 5) | t_lo
+  const int tlo = t & 31, thi = t >> 5;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = buf[had_swz((thi << 10) | (k << 5) | tlo)];
+#pragma unroll
+  for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if ((e & h) == 0) {
+        const float x0 = v[e], x1 = v[e + h];
+        v[e] = __fadd_rn(x0, x1);
+        v[e + h] = __fsub_rn(x0, x1);
+      }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) buf[had_swz((thi << 10) | (k << 5) | tlo)] = v[k];
+  __syncthreads();
+  // phase C: bits 10..12; thread holds i = (m << 10) | (t << 2) | j
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const float4 q = *reinterpret_cast<const float4*>(buf + had_swz((m << 10) | (t << 2)));
+    v[4 * m] = q.x; v[4 * m + 1] = q.y; v[4 * m + 2] = q.z; v[4 * m + 3] = q.w;
+  }
+#pragma unroll
+  for (int h = 1; h < 8; h <<= 1)
+#pragma unroll
+    for (int m = 0; m < 8; ++m)
+      if ((m & h) == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float x0 = v[4 * m + j], x1 = v[4 * (m + h) + j];
+          v[4 * m + j] = __fadd_rn(x0, x1);
+          v[4 * (m + h) + j] = __fsub_rn(x0, x1);
+        }
+      }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int8_t q0 = quant8_inv(v[4 * m], P.s_y, isy), q1 = quant8_inv(v[4 * m + 1], P.s_y, isy);
+    const int8_t q2 = quant8_inv(v[4 * m + 2], P.s_y, isy), q3 = quant8_inv(v[4 * m + 3], P.s_y, isy);
+    *reinterpret_cast<uint32_t*>(out + ((m << 10) | (t << 2))) =
+        (uint32_t)(uint8_t)q0 | ((uint32_t)(uint8_t)q1 << 8) | ((uint32_t)(uint8_t)q2 << 16) | ((uint32_t)(uint8_t)q3 << 24);
+    if (gsum) {   // 128-wide block (m << 3) | warp holds exactly this warp's 32 x 4 codes
+      int cs = (int)q0 + q1 + q2 + q3;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
+      if (lane == 0) gsum[(int64_t)b * ldg + ((m << 3) | warp)] = cs;
+    }
+  }
+}
+
 }  // namespace sq
 
 using namespace sq;
@@ -468,7 +615,7 @@ extern "C" int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, i
 
 extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
                                           int8_t* conv_cache, int8_t* state, void* ws, float* y, int64_t ldy,
-                                          int8_t* yq, int64_t ldyq, void* stream) {
+                                          int8_t* yq, int64_t ldyq, int32_t* yq_gsum, int64_t ldg, void* stream) {
   SQ_REQUIRE(p && B >= 0 && ws && y && yq, SQ_ERR_ARG, "sq_mamba2_decode_step_int8: bad args");
   const sq_mamba2_params& S = p->ssm;
   SQ_REQUIRE(S.head_dim == DS_P, SQ_ERR_SHAPE, "sq_mamba2_decode_step_int8: head_dim must be 64 (got %d)", S.head_dim);
@@ -496,10 +643,17 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
   if (B == 0) return SQ_OK;
   cudaStream_t st = as_stream(stream);
   float* wsf = reinterpret_cast<float*>(ws);
+  // SQ_DECODE_STAGES (profiling only): bitmask of the launches to issue, 1 prep | 2 state | 4 norm
+  static const int stages = [] {
+    const char* e = getenv("SQ_DECODE_STAGES");
+    return e ? atoi(e) : 7;
+  }();
   const int vec = p->conv_kernel == 4 && C % 4 == 0 && ldzx % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(zx) & 3) == 0 && (reinterpret_cast<uintptr_t>(conv_cache) & 3) == 0;
   const int per_blk = vec ? 1024 : 256;
-  prep_kernel<<<dim3((C + per_blk - 1) / per_blk, B), 256, 0, st>>>(*p, C, di, GN, zx, ldzx, conv_cache, wsf, B, vec);
+  if (stages & 1)
+    launch_k(PDL_PREP, prep_kernel, dim3((C + per_blk - 1) / per_blk, B), dim3(256), 0, st, *p, C, di, GN, zx, ldzx, conv_cache,
+             wsf, B, vec);
   auto ring = [&](auto kern, int smem) {
     static int grid_cache[2] = {0, 0};
     int& g = grid_cache[smem == SrCfg<128>::SMEM ? 1 : 0];
@@ -513,27 +667,47 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
       g = sms * per_sm;
     }
     const int tiles = B * S.n_heads;
-    kern<<<tiles < g ? tiles : g, SR_THREADS, smem, st>>>(S, B, wsf, state, y, ldy);
+    launch_k(PDL_RING, kern, dim3(tiles < g ? tiles : g), dim3(SR_THREADS), smem, st, S, B, (const float*)wsf, state, y, ldy);
   };
-  if (S.d_state == 128)
-    ring(state_ring_kernel<128>, SrCfg<128>::SMEM);
-  else
-    ring(state_ring_kernel<64>, SrCfg<64>::SMEM);
+  if (stages & 2) {
+    if (S.d_state == 128)
+      ring(state_ring_kernel<128>, SrCfg<128>::SMEM);
+    else
+      ring(state_ring_kernel<64>, SrCfg<64>::SMEM);
+  }
+  if (!(stages & 4)) return check_launch("sq_mamba2_decode_step_int8");
+  SQ_REQUIRE(!yq_gsum || (di % 128 == 0 && ldg >= di / 128), SQ_ERR_SHAPE, "sq_mamba2_decode_step_int8: ldg");
+  if (di == 8192 && ldy % 4 == 0 && ldyq % 16 == 0) {
+    launch_k(PDL_NORM, norm_had8192_kernel, dim3(B), dim3(256), 0, st, *p, (const float*)y, ldy, yq, ldyq,
+             p->hadamard ? yq_gsum : nullptr, ldg);
+    if (yq_gsum && !p->hadamard) return launch_group_sum(yq, ldyq, B, di, yq_gsum, ldg, st);
+    return check_launch("sq_mamba2_decode_step_int8");
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cl, B, 1);
   cfg.blockDim = dim3(256);
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cl;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (cl > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cl;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled(PDL_NORM)) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = cl > 1 ? 1 : 0;
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, norm_had_kernel, *p, di, CH, cl, blk, (const float*)y, ldy, yq, ldyq);
   if (e != cudaSuccess) {
     set_error("sq_mamba2_decode_step_int8 launch: %s", cudaGetErrorString(e));
     return SQ_ERR_CUDA;
   }
+  if (yq_gsum) return launch_group_sum(yq, ldyq, B, di, yq_gsum, ldg, st);
   return check_launch("sq_mamba2_decode_step_int8");
 }

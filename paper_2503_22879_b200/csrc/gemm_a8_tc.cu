@@ -25,6 +25,7 @@
 // Epilogue per (n, t): y = f32(acc) * alpha[n] -> I32 | F32 | int8 requant | residual add.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -52,6 +53,9 @@ struct TcArgs {
   void* out;
   int64_t ldo;
   const float* col_scale;
+  const int32_t* gsum;   // optional precomputed activation sums per 128-K block [M x K/128]
+  int64_t ldg;
+  int dbg;   // profiling only (SQ_GEMM_DBG): 1 = skip the group-sum arithmetic, 2 = CTA timeline
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -105,7 +109,7 @@ __device__ __forceinline__ int4 ldg_stream(const void* p) {
   return r;
 }
 
-__device__ __forceinline__ void epi_store(const TcArgs& a, int m, int n, int v, float alpha, float cs) {
+__device__ __forceinline__ void epi_store(const TcArgs& a, int m, int n, int v, float alpha, float cs, float ics) {
   const int64_t o = (int64_t)m * a.ldo + n;
   if (a.epi == SQ_EPI_I32) {
     reinterpret_cast<int32_t*>(a.out)[o] = v;
@@ -115,7 +119,7 @@ __device__ __forceinline__ void epi_store(const TcArgs& a, int m, int n, int v, 
   if (a.epi == SQ_EPI_F32)
     reinterpret_cast<float*>(a.out)[o] = y;
   else if (a.epi == SQ_EPI_QUANT)
-    reinterpret_cast<int8_t*>(a.out)[o] = quant8(y, cs);
+    reinterpret_cast<int8_t*>(a.out)[o] = quant8_inv(y, cs, ics);
   else
     reinterpret_cast<float*>(a.out)[o] = __fadd_rn(reinterpret_cast<float*>(a.out)[o], y);
 }
@@ -137,7 +141,8 @@ struct TcCfg {
   static constexpr int OFF_SGS = OFF_SUM + SUM_BYTES;
   static constexpr int OFF_BAR = OFF_SGS + SGS_BYTES;
   static constexpr int NBAR = 2 * STAGES + 2 * RAW + 2;
-  static constexpr int SMEM0 = 1024 + OFF_BAR + NBAR * 8 + 16;
+  static constexpr int OFF_EPI = OFF_BAR + NBAR * 8 + 16;   // alpha[128], col_scale[128]
+  static constexpr int SMEM0 = 1024 + OFF_EPI + 2 * TC_BN * 4;
   static constexpr int SMEM = SMEM0 < 120 * 1024 ? 120 * 1024 : SMEM0;   // 1 CTA/SM: TMEM alloc of 512 cols
 };
 
@@ -166,14 +171,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tile = blockIdx.x, split = blockIdx.y, m_tile = blockIdx.z;
+  const bool tl = (args.dbg & 2) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && split == 0;
+  const uint64_t t_entry = tl ? gtimer() : 0;
+  uint64_t t_raw0 = 0, t_rawl = 0, t_conv_done = 0, t_acc = 0, t_epi0 = 0, t_epi1 = 0, t_ld0 = 0, t_loop = 0;
   const int nkb_total = args.K / TC_BK;
   const int kb_begin = split * nkb_total / SPLITS;
   const int nkb = (split + 1) * nkb_total / SPLITS - kb_begin;
 
+  pdl_trigger();
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], W4 ? 1 + 8 : 1);      // TMA (+ 8 converter warps)
-      mbar_init(&empty[s], W4 ? 2 : 1);         // MMA commit (+ group-sum warp)
+      mbar_init(&empty[s], (W4 && !args.gsum) ? 2 : 1);   // MMA commit (+ group-sum warp)
     }
     for (int r = 0; r < RAW; ++r) {
       mbar_init(&rfull[r], 1);
@@ -193,6 +202,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == 0) {
     // ---------------- activation (and W8 weight) TMA producer
+    pdl_wait();   // activations come from the previous grid
     if (lane == 0) {
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
@@ -247,11 +257,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int o = lane * 16; o < 4 * NTOK * 32; o += 32 * 16) *reinterpret_cast<int4*>(bh + o) = make_int4(0, 0, 0, 0);
         __syncwarp();
       }
-      for (int i = 0; i < nkb; ++i) {
+      pdl_wait();
+      if (args.gsum) {
+        // sums precomputed by the producer of the activations: just stage them
+        for (int idx = lane; idx < NTOK * nkb; idx += 32) {
+          const int t = idx / nkb, i = idx % nkb;
+          const int m = m_tile * NTOK + t;
+          const int acc = m < args.M ? args.gsum[(int64_t)m * args.ldg + kb_begin + i] : 0;
+          if (Cfg::MMA_CORR) {
+            const int o = (i >> 5) * NTOK * 32 + (t >> 3) * 256 + ((i >> 4) & 1) * 128 + (t & 7) * 16 + (i & 15);
+            bh[o] = (uint8_t)(acc >> 7);
+            bl[o] = (uint8_t)(acc & 127);
+          } else {
+            gsum[i * NTOK + t] = acc;
+          }
+        }
+        __syncwarp();
+      }
+      for (int i = 0; i < nkb && !args.gsum; ++i) {
         const int s = i % STAGES;
         mbar_wait(&full[s], (i / STAGES) & 1);
         const uint8_t* tile = act + s * Cfg::ACT_BYTES;
-        for (int t = lane; t < NTOK; t += 32) {
+        for (int t = lane; t < NTOK && !(args.dbg & 1); t += 32) {
           int acc = 0;
 #pragma unroll
           for (int c = 0; c < 8; ++c) {   // any chunk order sums the row; rotate per lane -> no bank conflicts
@@ -298,6 +325,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int row = q * 32 + lane;
     const int n = n_tile * TC_BN + row;
     const bool valid_n = n < args.N;
+    // epilogue scales fetched now, so their latency hides behind the main loop
+    float* s_alpha = reinterpret_cast<float*>(smem + Cfg::OFF_EPI);
+    float* s_cs = s_alpha + TC_BN;
+    if (half == 0) {
+      s_alpha[row] = (valid_n && args.epi != SQ_EPI_I32) ? args.alpha[n] : 0.f;
+      s_cs[row] = (valid_n && args.epi == SQ_EPI_QUANT) ? args.col_scale[n] : 1.f;
+    }
     if (W4) {
       const int8_t* sgr = args.sg + (size_t)(valid_n ? n : 0) * (args.K / args.group);
       if (half == 0) {
@@ -348,10 +382,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (i < nkb) {
             const int r = i % RAW;
             mbar_wait(&rfull[r], (i / RAW) & 1);
+            if (tl && warp == 2 && i == 0) t_raw0 = gtimer();
+            if (tl && warp == 2 && i == nkb - 1) t_rawl = gtimer();
             const uint8_t* rp = raw + r * W4_TILE_BYTES + half * 2 * 2048 + row * 16;
             const uint4 p0 = *reinterpret_cast<const uint4*>(rp);
             const uint4 p1 = *reinterpret_cast<const uint4*>(rp + 2048);
             const uint32_t sg = (uint32_t)(uint8_t)sgs[i * TC_BN + row];
+            if (args.dbg & 8) {   // profiling: skip the nibble expansion
+              wv[j][0] = p0.x; wv[j][1] = p0.y; wv[j][2] = p0.z; wv[j][3] = p0.w;
+              wv[j][4] = p1.x; wv[j][5] = p1.y; wv[j][6] = p1.z; wv[j][7] = p1.w;
+              wv[j][8] = p0.x; wv[j][9] = p0.y; wv[j][10] = p0.z; wv[j][11] = p0.w;
+              wv[j][12] = p1.x; wv[j][13] = p1.y; wv[j][14] = p1.z; wv[j][15] = p1.w;
+              continue;
+            }
             nib8_to_u8(p0.x, sg, wv[j][0], wv[j][1]);
             nib8_to_u8(p0.y, sg, wv[j][2], wv[j][3]);
             nib8_to_u8(p0.z, sg, wv[j][4], wv[j][5]);
@@ -375,7 +418,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int s = i % STAGES;
             mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
             if (WMODE == WM_W4_TS) {
-              tmem_st_x16(tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + s * 32 + half * 16, wv[j]);
+              if (!(args.dbg & 4)) tmem_st_x16(tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + s * 32 + half * 16, wv[j]);
             } else {
               // swizzled SW128 K-major tile: row r, 16-byte chunk c at ((c ^ (r&7)) * 16)
               uint8_t* base = wsm + s * Cfg::W_BYTES + (row >> 3) * 1024 + (row & 7) * 128;
@@ -403,11 +446,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
     // ---------------- epilogue: TMEM -> registers -> (offset correction) -> HBM / DSMEM
+    if (tl && warp == 2) t_conv_done = gtimer();
     mbar_wait(accf, 0);
     tc_fence_after();
+    if (tl && warp == 2) t_acc = gtimer();
     if (W4) named_bar(1, 288);           // group sums ready
-    const float alpha = (valid_n && args.epi != SQ_EPI_I32) ? args.alpha[n] : 0.f;
-    const float cs = (valid_n && args.epi == SQ_EPI_QUANT) ? args.col_scale[n] : 1.f;
+    if (tl && warp == 2) t_epi0 = gtimer();
+    pdl_wait();                          // outputs / residual belong to earlier grids too
+    named_bar(3, 256);                   // s_alpha / s_cs (stored at kernel start) visible
+    const float alpha = s_alpha[row], cs = s_cs[row];
+    const float ics = __frcp_rn(cs);
     constexpr int CH = NTOK / 2;
     int32_t* red = reinterpret_cast<int32_t*>(act);     // split-K: [NTOK][128], aliases the act stages
 #pragma unroll 1
@@ -415,6 +463,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       uint32_t v[8];
       tmem_ld_x8(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
       tmem_wait_ld();
+      if (tl && warp == 2 && c0 == half * CH) t_ld0 = gtimer();
       int val[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) val[j] = (int)v[j];
@@ -440,43 +489,113 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int j = 0; j < 8; ++j) val[j] -= 8 * corr[j];
       }
       if (SPLITS == 1) {
+        // stage [NTOK][TC_BN] in smem (aliases the activation stages: every MMA has completed)
+        if (args.epi == SQ_EPI_QUANT && (args.dbg & 16)) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int m = m_tile * NTOK + c0 + j;
-          if (valid_n && m < args.M) epi_store(args, m, n, val[j], alpha, cs);
+          for (int j = 0; j < 8; ++j) act[(c0 + j) * TC_BN + row] = (uint8_t)val[j];
+        } else if (args.epi == SQ_EPI_QUANT) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            act[(c0 + j) * TC_BN + row] = (uint8_t)quant8_inv(__fmul_rn((float)val[j], alpha), cs, ics);
+        } else {
+          uint32_t* st32 = reinterpret_cast<uint32_t*>(act);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st32[(c0 + j) * TC_BN + row] =
+                args.epi == SQ_EPI_I32 ? (uint32_t)val[j] : __float_as_uint(__fmul_rn((float)val[j], alpha));
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) red[(c0 + j) * TC_BN + row] = val[j];
       }
     }
+    if (tl && warp == 2) t_loop = gtimer();
+    if (SPLITS == 1) {
+      // coalesced 16-B stores of the staged tile (residual epilogue: 16-B read-add-write)
+      named_bar(3, 256);
+      const int et = threadIdx.x - 64;
+      const int esz = args.epi == SQ_EPI_QUANT ? 1 : 4;
+      const int per16 = 16 / esz;
+      const int chunks = TC_BN / per16;
+      for (int idx = et; idx < NTOK * chunks; idx += 256) {
+        const int t = idx / chunks, c = idx % chunks;
+        const int m = m_tile * NTOK + t;
+        const int n0 = n_tile * TC_BN + c * per16;
+        if (m >= args.M || n0 >= args.N) continue;
+        const uint8_t* src = act + (t * TC_BN + c * per16) * esz;
+        uint8_t* dst = reinterpret_cast<uint8_t*>(args.out) + ((int64_t)m * args.ldo + n0) * esz;
+        const int nv = min(per16, args.N - n0);
+        if (nv == per16 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          uint4 v = *reinterpret_cast<const uint4*>(src);
+          if (args.epi == SQ_EPI_RESID) {
+            const float4 o = *reinterpret_cast<const float4*>(dst);
+            v.x = __float_as_uint(__fadd_rn(o.x, __uint_as_float(v.x)));
+            v.y = __float_as_uint(__fadd_rn(o.y, __uint_as_float(v.y)));
+            v.z = __float_as_uint(__fadd_rn(o.z, __uint_as_float(v.z)));
+            v.w = __float_as_uint(__fadd_rn(o.w, __uint_as_float(v.w)));
+          }
+          *reinterpret_cast<uint4*>(dst) = v;
+        } else {
+          for (int e = 0; e < nv; ++e) {
+            if (esz == 1) {
+              dst[e] = src[e];
+            } else {
+              const uint32_t v = reinterpret_cast<const uint32_t*>(src)[e];
+              float* d = reinterpret_cast<float*>(dst) + e;
+              if (args.epi == SQ_EPI_RESID) *d = __fadd_rn(*d, __uint_as_float(v));
+              else *reinterpret_cast<uint32_t*>(d) = v;
+            }
+          }
+        }
+      }
+    }
   }
 
+  if (tl && warp == 2) t_epi1 = gtimer();
   if (SPLITS > 1) {
+    pdl_wait();
     __syncwarp();
     cluster_sync();
     const uint32_t rank = cluster_rank();
     constexpr int TPR = NTOK / SPLITS;   // tokens reduced by this CTA
     int32_t* red = reinterpret_cast<int32_t*>(act);
     const uint32_t red_addr = smem_u32(red);
-    for (int idx = threadIdx.x; idx < TPR * TC_BN; idx += TC_THREADS) {
-      const int t = rank * TPR + idx / TC_BN;
-      const int r = idx % TC_BN;
-      const int nn = n_tile * TC_BN + r;
-      const int m = m_tile * NTOK + t;
-      int sum = 0;
+    // 4 consecutive output channels per thread: one 16-B DSMEM load per peer, all in flight
+    for (int idx = threadIdx.x; idx < TPR * (TC_BN / 4); idx += TC_THREADS) {
+      const int t = rank * TPR + idx / (TC_BN / 4);
+      const int r = (idx % (TC_BN / 4)) * 4;
+      int4 part[SPLITS];
 #pragma unroll
-      for (int j = 0; j < SPLITS; ++j) sum += ld_dsmem_s32(map_peer(red_addr + (t * TC_BN + r) * 4, j));
-      if (nn < args.N && m < args.M) {
-        const float al = args.epi != SQ_EPI_I32 ? args.alpha[nn] : 0.f;
-        const float cs = args.epi == SQ_EPI_QUANT ? args.col_scale[nn] : 1.f;
-        epi_store(args, m, nn, sum, al, cs);
+      for (int j = 0; j < SPLITS; ++j) part[j] = ld_dsmem_v4s32(map_peer(red_addr + (t * TC_BN + r) * 4, j));
+      int sum[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < SPLITS; ++j) {   // fixed rank order: deterministic (and exact: int32)
+        sum[0] += part[j].x; sum[1] += part[j].y; sum[2] += part[j].z; sum[3] += part[j].w;
+      }
+      const int m = m_tile * NTOK + t;
+      if (m >= args.M) continue;
+#pragma unroll
+      const float* s_alpha = reinterpret_cast<const float*>(smem + Cfg::OFF_EPI);
+      for (int e = 0; e < 4; ++e) {
+        const int nn = n_tile * TC_BN + r + e;
+        if (nn < args.N) {
+          const float cs = s_alpha[TC_BN + r + e];
+          epi_store(args, m, nn, sum[e], s_alpha[r + e], cs, __frcp_rn(cs));
+        }
       }
     }
     cluster_sync();
   }
   tc_fence_before();
   __syncthreads();
+  if (tl && warp == 2)
+    printf("gemm cta %d N=%d K=%d: raw0 %.2f rawlast %.2f conv_done %.2f acc %.2f epi0 %.2f epi1 %.2f end %.2f us\n",
+           blockIdx.x, args.N, args.K, (t_raw0 - t_entry) * 1e-3, (t_rawl - t_entry) * 1e-3,
+           (t_conv_done - t_entry) * 1e-3, (t_acc - t_entry) * 1e-3, (t_epi0 - t_entry) * 1e-3,
+           (t_epi1 - t_entry) * 1e-3, (gtimer() - t_entry) * 1e-3);
+  if (tl && warp == 2)
+    printf("gemm cta %d: first tmem ld %.2f  loop end %.2f us\n", blockIdx.x, (t_ld0 - t_entry) * 1e-3,
+           (t_loop - t_entry) * 1e-3);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -543,13 +662,22 @@ static int launch_tc(const int8_t* a, int64_t lda, const uint8_t* w, const TcArg
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = SPLITS;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (SPLITS > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 1;
+    at[na].val.clusterDim.y = SPLITS;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled(PDL_GEMM)) {   // weights stream in while the previous grid drains (see common.cuh)
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = SPLITS > 1 ? 1 : 0;
+  cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm_act, tm_w, args);
   if (e != cudaSuccess) {
     set_error("gemm_tc launch: %s", cudaGetErrorString(e));
@@ -586,7 +714,7 @@ int g_tc_w4_mode = WM_W4_TS;   // sq_set_gemm_mode() switches TS/SS for A/B meas
 // Returns SQ_ERR_ARG when the shape is not eligible (caller falls back to mma.sync).
 int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg, int group, bool w4,
                const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
-               cudaStream_t st) {
+               const int32_t* a_gsum, int64_t ld_gsum, cudaStream_t st) {
   if (K % TC_BK != 0 || (w4 && group % TC_BK != 0) || lda % 16 != 0 || (reinterpret_cast<uintptr_t>(a) & 15) ||
       (!w4 && (reinterpret_cast<uintptr_t>(w) & 15)))
     return SQ_ERR_ARG;
@@ -597,7 +725,11 @@ int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg,
   int splits = 1;
   while (splits < 8 && tiles * splits * 2 <= 148 && nkb / (splits * 2) >= 4 && ntok % (splits * 2) == 0) splits *= 2;
   if (w4 && (nkb + splits - 1) / splits > TC_MAX_KB) return SQ_ERR_ARG;
-  TcArgs args{w, sg, group, alpha, M, N, K, epi, out, ldo, col_scale};
+  static const int dbg = [] {
+    const char* e = getenv("SQ_GEMM_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  TcArgs args{w, sg, group, alpha, M, N, K, epi, out, ldo, col_scale, w4 ? a_gsum : nullptr, ld_gsum, dbg};
   if (!w4) return dispatch_split<WM_W8>(splits, ntok, a, lda, w, args, st);
   // A-from-TMEM is used up to 128-token tiles (the 256-column accumulator leaves too few
   // TMEM columns for the A stages); larger tiles stage the expanded weights in smem.

@@ -6,7 +6,7 @@ extern int g_tc_w4_mode;
 static int g_gemm_mode = 1;   // 0: mma.sync only, 1: tcgen05 (TS for W4), 2: tcgen05 (SS for W4)
 int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg, int group, bool w4,
                const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
-               cudaStream_t st);
+               const int32_t* a_gsum, int64_t ld_gsum, cudaStream_t st);
 int64_t w4_layout_bytes(int N, int K);
 int repack_w4(const uint8_t* src, int N, int K, uint8_t* dst, cudaStream_t st);
 int unpack_w4(const uint8_t* src, int N, int K, uint8_t* dst, cudaStream_t st);
@@ -58,7 +58,7 @@ extern "C" int sq_gemm_w8a8(const int8_t* a, int64_t lda, const int8_t* w, const
   if (M == 0) return SQ_OK;
   if (g_gemm_mode != 0) {
     rc = gemm_a8_tc(a, lda, reinterpret_cast<const uint8_t*>(w), nullptr, K, false, alpha, M, N, K, epi, out, ldo,
-                    col_scale, as_stream(stream));
+                    col_scale, nullptr, 0, as_stream(stream));
     if (rc != SQ_ERR_ARG) return rc;
   }
   return gemm_a8_mma(a, lda, reinterpret_cast<const uint8_t*>(w), nullptr, K, false, alpha, M, N, K, epi, out, ldo,
@@ -67,14 +67,16 @@ extern "C" int sq_gemm_w8a8(const int8_t* a, int64_t lda, const int8_t* w, const
 
 extern "C" int sq_gemm_w4a8(const int8_t* a, int64_t lda, const uint8_t* w4, const int8_t* sg, int group,
                             const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo,
-                            const float* col_scale, void* stream) {
+                            const float* col_scale, const int32_t* a_gsum, int64_t ld_gsum, void* stream) {
   int rc = check_gemm("sq_gemm_w4a8", a, lda, M, N, K, epi, ldo, col_scale);
   if (rc) return rc;
   SQ_REQUIRE(group % 32 == 0 && K % group == 0 && sg != nullptr, SQ_ERR_LAYOUT,
              "sq_gemm_w4a8: group (%d) must be a multiple of 32 dividing K", group);
   if (M == 0) return SQ_OK;
   if (g_gemm_mode != 0) {
-    rc = gemm_a8_tc(a, lda, w4, sg, group, true, alpha, M, N, K, epi, out, ldo, col_scale, as_stream(stream));
+    SQ_REQUIRE(!a_gsum || ld_gsum >= K / 128, SQ_ERR_LAYOUT, "sq_gemm_w4a8: ld_gsum < K/128");
+    rc = gemm_a8_tc(a, lda, w4, sg, group, true, alpha, M, N, K, epi, out, ldo, col_scale, a_gsum, ld_gsum,
+                    as_stream(stream));
     if (rc != SQ_ERR_ARG) return rc;
   }
   return gemm_a8_mma(a, lda, w4, sg, group, true, alpha, M, N, K, epi, out, ldo, col_scale, as_stream(stream));

@@ -34,10 +34,12 @@ __device__ __forceinline__ float rms_factor(double ss, int D, float eps) {
 }
 
 template <int NT, bool QUANT>
-__global__ void __launch_bounds__(NT) rmsnorm_kernel(const float* __restrict__ x, int64_t ldx,
+__global__ void __launch_bounds__(NT) rmsnorm_kernel(const float* x, int64_t ldx,
                                                      const float* __restrict__ gamma, float eps, float s,
                                                      int D, void* __restrict__ out, int64_t ldo) {
   __shared__ double red[NT / 32];
+  pdl_trigger();
+  pdl_wait();
   const float* xr = x + (int64_t)blockIdx.x * ldx;
   double ss = 0.0;
   for (int i = threadIdx.x; i < D; i += NT) {
@@ -128,14 +130,17 @@ __device__ __forceinline__ void store16_q(int8_t* p, const float (&v)[16], float
 }
 
 template <bool QUANT>
-__global__ void __launch_bounds__(1024) rmsnorm16_kernel(const float* __restrict__ x, int64_t ldx,
+__global__ void __launch_bounds__(1024) rmsnorm16_kernel(const float* x, int64_t ldx,
                                                          const float* __restrict__ gamma, float eps, float s, int D,
-                                                         void* __restrict__ out, int64_t ldo) {
+                                                         void* __restrict__ out, int64_t ldo,
+                                                         int32_t* __restrict__ gsum, int64_t ldg) {
   __shared__ double red[32];
   const int base = threadIdx.x * 16;
   float v[16], g[16];
-  load16(x + (int64_t)blockIdx.x * ldx + base, v);
+  pdl_trigger();
   load16(gamma + base, g);
+  pdl_wait();
+  load16(x + (int64_t)blockIdx.x * ldx + base, v);
   double ss = 0.0;
 #pragma unroll
   for (int i = 0; i < 16; ++i) ss += (double)v[i] * (double)v[i];
@@ -145,6 +150,16 @@ __global__ void __launch_bounds__(1024) rmsnorm16_kernel(const float* __restrict
   for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
   if (QUANT) {
     store16_q(reinterpret_cast<int8_t*>(out) + (int64_t)blockIdx.x * ldo + base, v, s);
+    if (gsum) {   // sums of the codes over each 128-wide block (8 threads)
+      const float is = __frcp_rn(s);
+      int cs = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cs += quant8_inv(v[i], s, is);
+      cs += __shfl_xor_sync(0xffffffffu, cs, 1);
+      cs += __shfl_xor_sync(0xffffffffu, cs, 2);
+      cs += __shfl_xor_sync(0xffffffffu, cs, 4);
+      if ((threadIdx.x & 7) == 0) gsum[(int64_t)blockIdx.x * ldg + (base >> 7)] = cs;
+    }
   } else {
     float* o = reinterpret_cast<float*>(out) + (int64_t)blockIdx.x * ldo + base;
 #pragma unroll
@@ -213,15 +228,19 @@ __global__ void __launch_bounds__(1024) gate_norm_had_quant16_kernel(const float
   store16_q(out + (int64_t)blockIdx.x * ldo + base, v, s_y);
 }
 
-__global__ void quantize_kernel(const float* __restrict__ x, int64_t ldx, float s, int D, int8_t* __restrict__ out,
+__global__ void quantize_kernel(const float* x, int64_t ldx, float s, int D, int8_t* __restrict__ out,
                                 int64_t ldo) {
+  pdl_trigger();
+  pdl_wait();
   const float* r = x + (int64_t)blockIdx.x * ldx;
   int8_t* o = out + (int64_t)blockIdx.x * ldo;
   for (int i = threadIdx.x; i < D; i += blockDim.x) o[i] = quant8(r[i], s);
 }
 
 __global__ void embed_kernel(const int8_t* __restrict__ codes, const float* __restrict__ rs,
-                             const int32_t* __restrict__ tok, int D, float* __restrict__ h) {
+                             const int32_t* tok, int D, float* __restrict__ h) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x;
   const int t = tok[m];
   const float s = rs[t];
@@ -230,10 +249,12 @@ __global__ void embed_kernel(const int8_t* __restrict__ codes, const float* __re
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lg, int64_t ld, int N,
+__global__ void __launch_bounds__(NT) argmax_kernel(const float* lg, int64_t ld, int N,
                                                     int32_t* __restrict__ tok) {
   __shared__ float bv[NT / 32];
   __shared__ int bi[NT / 32];
+  pdl_trigger();
+  pdl_wait();
   const float* r = lg + (int64_t)blockIdx.x * ld;
   float best = -INFINITY;
   int bidx = 0x7fffffff;
@@ -267,14 +288,43 @@ __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lg
 
 using namespace sq;
 
-extern "C" int sq_rmsnorm_quant(const float* x, int64_t ldx, const float* gamma, float eps, float s, int M,
-                                int D, int8_t* out, int64_t ldo, void* stream) {
-  SQ_REQUIRE(M >= 0 && D > 0 && s > 0.f, SQ_ERR_SHAPE, "sq_rmsnorm_quant: bad M/D/s");
+namespace sq {
+__global__ void group_sum_kernel(const int8_t* codes, int64_t ld, int K, int32_t* __restrict__ gsum,
+                                 int64_t ldg) {
+  // one warp per 128-wide block: 32 lanes x 4 codes
+  pdl_trigger();
+  pdl_wait();
+  const int m = blockIdx.y;
+  const int g = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= K / 128) return;
+  const int lane = threadIdx.x & 31;
+  int acc = __dp4a(*reinterpret_cast<const int*>(codes + (int64_t)m * ld + g * 128 + lane * 4), 0x01010101, 0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) gsum[(int64_t)m * ldg + g] = acc;
+}
+
+int launch_group_sum(const int8_t* codes, int64_t ld, int M, int K, int32_t* gsum, int64_t ldg, cudaStream_t st) {
+  SQ_REQUIRE(K % 128 == 0 && ld % 4 == 0, SQ_ERR_SHAPE, "group sums need K %% 128 == 0 and 4-byte aligned rows");
   if (M == 0) return SQ_OK;
-  if (D % 512 == 0 && D / 16 <= 1024 && ldx % 4 == 0 && ldo % 16 == 0)
-    rmsnorm16_kernel<true><<<M, D / 16, 0, as_stream(stream)>>>(x, ldx, gamma, eps, s, D, out, ldo);
-  else
-    rmsnorm_kernel<256, true><<<M, 256, 0, as_stream(stream)>>>(x, ldx, gamma, eps, s, D, out, ldo);
+  launch_k(PDL_ROW, group_sum_kernel, dim3((K / 128 + 7) / 8, M), dim3(256), 0, st, codes, ld, K, gsum, ldg);
+  return check_launch("group_sum");
+}
+}  // namespace sq
+
+extern "C" int sq_rmsnorm_quant(const float* x, int64_t ldx, const float* gamma, float eps, float s, int M,
+                                int D, int8_t* out, int64_t ldo, int32_t* gsum, int64_t ldg, void* stream) {
+  SQ_REQUIRE(M >= 0 && D > 0 && s > 0.f, SQ_ERR_SHAPE, "sq_rmsnorm_quant: bad M/D/s");
+  SQ_REQUIRE(!gsum || (D % 128 == 0 && ldg >= D / 128), SQ_ERR_SHAPE, "sq_rmsnorm_quant: gsum needs D %% 128 == 0");
+  if (M == 0) return SQ_OK;
+  if (D % 512 == 0 && D / 16 <= 1024 && ldx % 4 == 0 && ldo % 16 == 0) {
+    launch_k(PDL_ROW, rmsnorm16_kernel<true>, dim3(M), dim3(D / 16), 0, as_stream(stream), x, ldx, gamma, eps, s, D,
+             (void*)out, ldo, gsum, ldg);
+  } else {
+    launch_k(PDL_ROW, rmsnorm_kernel<256, true>, dim3(M), dim3(256), 0, as_stream(stream), x, ldx, gamma, eps, s, D,
+             (void*)out, ldo);
+    if (gsum) return launch_group_sum(out, ldo, M, D, gsum, ldg, as_stream(stream));
+  }
   return check_launch("sq_rmsnorm_quant");
 }
 
@@ -283,9 +333,11 @@ extern "C" int sq_rmsnorm_f32(const float* x, int64_t ldx, const float* gamma, f
   SQ_REQUIRE(M >= 0 && D > 0, SQ_ERR_SHAPE, "sq_rmsnorm_f32: bad M/D");
   if (M == 0) return SQ_OK;
   if (D % 512 == 0 && D / 16 <= 1024 && ldx % 4 == 0 && ldo % 4 == 0)
-    rmsnorm16_kernel<false><<<M, D / 16, 0, as_stream(stream)>>>(x, ldx, gamma, eps, 1.f, D, out, ldo);
+    launch_k(PDL_ROW, rmsnorm16_kernel<false>, dim3(M), dim3(D / 16), 0, as_stream(stream), x, ldx, gamma, eps, 1.f, D,
+             (void*)out, ldo, (int32_t*)nullptr, (int64_t)0);
   else
-    rmsnorm_kernel<256, false><<<M, 256, 0, as_stream(stream)>>>(x, ldx, gamma, eps, 1.f, D, out, ldo);
+    launch_k(PDL_ROW, rmsnorm_kernel<256, false>, dim3(M), dim3(256), 0, as_stream(stream), x, ldx, gamma, eps, 1.f, D,
+             (void*)out, ldo);
   return check_launch("sq_rmsnorm_f32");
 }
 
@@ -314,7 +366,7 @@ extern "C" int sq_quantize_f32(const float* x, int64_t ldx, float s, int M, int 
                                void* stream) {
   SQ_REQUIRE(M >= 0 && D > 0 && s > 0.f, SQ_ERR_SHAPE, "sq_quantize_f32: bad shape/scale");
   if (M == 0) return SQ_OK;
-  quantize_kernel<<<M, 256, 0, as_stream(stream)>>>(x, ldx, s, D, out, ldo);
+  launch_k(PDL_ROW, quantize_kernel, dim3(M), dim3(256), 0, as_stream(stream), x, ldx, s, D, out, ldo);
   return check_launch("sq_quantize_f32");
 }
 
@@ -322,13 +374,13 @@ extern "C" int sq_embed_int8(const int8_t* codes, const float* row_scale, const 
                              float* h, void* stream) {
   SQ_REQUIRE(M >= 0 && D > 0, SQ_ERR_SHAPE, "sq_embed_int8: bad shape");
   if (M == 0) return SQ_OK;
-  embed_kernel<<<M, 256, 0, as_stream(stream)>>>(codes, row_scale, tok, D, h);
+  launch_k(PDL_ROW, embed_kernel, dim3(M), dim3(256), 0, as_stream(stream), codes, row_scale, tok, D, h);
   return check_launch("sq_embed_int8");
 }
 
 extern "C" int sq_argmax_f32(const float* logits, int64_t ld, int M, int N, int32_t* tok, void* stream) {
   SQ_REQUIRE(M >= 0 && N > 0, SQ_ERR_SHAPE, "sq_argmax_f32: bad shape");
   if (M == 0) return SQ_OK;
-  argmax_kernel<1024><<<M, 1024, 0, as_stream(stream)>>>(logits, ld, N, tok);
+  launch_k(PDL_ROW, argmax_kernel<1024>, dim3(M), dim3(1024), 0, as_stream(stream), logits, ld, N, tok);
   return check_launch("sq_argmax_f32");
 }

@@ -78,14 +78,26 @@ def unpack_w4(w: torch.Tensor, N: int, K: int) -> torch.Tensor:
 
 
 # ------------------------------------------------------------------ row ops
-def rmsnorm_quant(x, gamma, eps, s, out=None):
+def _gs(gsum, M, K):
+    """Optional int32 [M x K/128] activation block sums (see sq_gemm_w4a8)."""
+    if gsum is None:
+        return 0, 0
+    _dev(gsum, torch.int32, "gsum", 2)
+    if gsum.shape[0] < M or gsum.shape[1] < K // 128:
+        raise ShapeError(f"gsum must be at least [{M} x {K // 128}]")
+    return gsum.data_ptr(), _ld(gsum)
+
+
+def rmsnorm_quant(x, gamma, eps, s, out=None, gsum=None):
+    """Pre-norm + per-tensor quant; ``gsum`` (optional) receives the 128-block code sums."""
     _dev(x, torch.float32, "x", 2)
     _dev(gamma, torch.float32, "gamma", 1)
     M, D = x.shape
     out = torch.empty((M, D), dtype=torch.int8, device=x.device) if out is None else out
     _dev(out, torch.int8, "out", 2)
+    gp, gl = _gs(gsum, M, D)
     _check(lib().sq_rmsnorm_quant(x.data_ptr(), _ld(x), gamma.data_ptr(), float(eps), float(s), M, D,
-                                  out.data_ptr(), _ld(out), _stream()))
+                                  out.data_ptr(), _ld(out), gp, gl, _stream()))
     return out
 
 
@@ -165,7 +177,7 @@ def gemm_w8a8(a, w, alpha, epi=EPI_F32, out=None, col_scale=None):
     return out
 
 
-def gemm_w4a8(a, w4, sg, group, alpha, N, epi=EPI_F32, out=None, col_scale=None):
+def gemm_w4a8(a, w4, sg, group, alpha, N, epi=EPI_F32, out=None, col_scale=None, gsum=None):
     _dev(a, torch.int8, "a", 2)
     _dev(w4, torch.uint8, "w4")
     _dev(sg, torch.int8, "sg", 2)
@@ -173,8 +185,9 @@ def gemm_w4a8(a, w4, sg, group, alpha, N, epi=EPI_F32, out=None, col_scale=None)
     if sg.shape != (N, K // group):
         raise LayoutError(f"sg must be [{N} x {K // group}]")
     out = _gemm_out(a, N, epi, out)
+    gp, gl = _gs(gsum, M, K)
     _check(lib().sq_gemm_w4a8(a.data_ptr(), _ld(a), w4.data_ptr(), sg.data_ptr(), group, alpha.data_ptr(), M, N, K,
-                              epi, out.data_ptr(), _ld(out), _opt(col_scale), _stream()))
+                              epi, out.data_ptr(), _ld(out), _opt(col_scale), gp, gl, _stream()))
     return out
 
 
@@ -243,7 +256,7 @@ def mamba2_decode_ws_bytes(p, B) -> int:
     return int(lib().sq_mamba2_decode_ws_bytes(C.byref(p), B))
 
 
-def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=None):
+def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=None, gsum=None):
     """Mamba2 decode step, SSM half of a block (conv update + int8 state update + gated
     norm + FWHT + quant).  zx int8 [B x in_proj_out] (z|x|B|C|dt codes); conv_cache int8
     [B x (K-1) x conv_dim]; state int8 [B x nh x P x N] (both updated in place).  Returns
@@ -264,9 +277,10 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
         raise ShapeError(f"decode workspace needs {nbytes} bytes")
     _dev(yq, torch.int8, "yq", 2)
     _dev(y, torch.float32, "y", 2)
+    gp, gl = _gs(gsum, B, di)
     _check(lib().sq_mamba2_decode_step_int8(C.byref(p), B, zx.data_ptr(), _ld(zx), conv_cache.data_ptr(),
                                             state.data_ptr(), ws.data_ptr(), y.data_ptr(), _ld(y), yq.data_ptr(),
-                                            _ld(yq), _stream()))
+                                            _ld(yq), gp, gl, _stream()))
     return yq
 
 

@@ -186,11 +186,12 @@ class DeviceLinear:
         dev = self.w.device
         self.alpha = _t((self.s_ch * np.float32(s_a)).astype(np.float32), torch.float32, dev)
 
-    def a8(self, a_codes, epi, out=None, col_scale=None):
+    def a8(self, a_codes, epi, out=None, col_scale=None, gsum=None):
+        """``gsum``: optional int32 128-block sums of ``a_codes`` (W4A8 offset correction)."""
         if self.kind == "w8":
             return ops.gemm_w8a8(a_codes, self.w, self.alpha, epi, out, col_scale)
         if self.kind == "w4a8":
-            return ops.gemm_w4a8(a_codes, self.w, self.sg, self.group, self.alpha, self.N, epi, out, col_scale)
+            return ops.gemm_w4a8(a_codes, self.w, self.sg, self.group, self.alpha, self.N, epi, out, col_scale, gsum)
         raise ShapeError("A8 GEMM on a W4A16 projection")
 
     def a16(self, x, out=None, resid=False):
@@ -286,14 +287,14 @@ class DeviceBlock:
         return n
 
     # ------------------------------------------------------------------ forward
-    def forward_codes(self, u_codes, B, T, state: SsmState, state_in: bool, resid=None, ws=None):
+    def forward_codes(self, u_codes, B, T, state: SsmState, state_in: bool, resid=None, ws=None, u_gsum=None):
         """A8 block on int8 input codes [B*T × d_model].  If ``resid`` is given the out_proj
         epilogue adds into it (residual stream) and it is returned; else returns f32 out."""
         d = self.dims
         di = d.d_inner
         M = B * T
         ws = ws if ws is not None else {}
-        zx = self.in_proj.a8(u_codes, ops.EPI_QUANT, ws.get("zx"), self.in_out_scale)
+        zx = self.in_proj.a8(u_codes, ops.EPI_QUANT, ws.get("zx"), self.in_out_scale, u_gsum)
         y = ws.get("y")
         if y is None:
             y = torch.empty((M, di), dtype=torch.float32, device=u_codes.device)
@@ -302,11 +303,12 @@ class DeviceBlock:
             xbc = zx[:, di:2 * di + 2 * gn]
             if T == 1 and state_in and self.fused_decode:
                 # conv update + int8 state update + gated norm + FWHT + quant (sq_mamba2_decode_step_int8)
+                ygs = ws.get("yq_gs")
                 yq = ops.mamba2_decode_step_int8(self.decode_params, B, zx, state.conv_cache, state.h, ws.get("yq"),
-                                                 y, ws.get("dws"))
+                                                 y, ws.get("dws"), ygs)
                 if resid is not None:
-                    return self.out_proj.a8(yq, ops.EPI_RESID, resid)
-                return self.out_proj.a8(yq, ops.EPI_F32, ws.get("out"))
+                    return self.out_proj.a8(yq, ops.EPI_RESID, resid, gsum=ygs)
+                return self.out_proj.a8(yq, ops.EPI_F32, ws.get("out"), gsum=ygs)
             if T == 1 and state_in:
                 cv = ops.conv1d_update_int8(xbc, self.conv_w, self.conv_b, self.conv_in_scale, self.conv_out_scale,
                                             state.conv_cache, ws.get("conv"))

@@ -68,6 +68,13 @@ res["state_update_int8 (old)"] = timeit(lambda: ops.state_update_int8(blk.params
 res["gate_norm_had_quant (old)"] = timeit(lambda: ops.gate_norm_had_quant(y, blk.norm_w, 1e-5, blk.s_y, True, yq))
 res["in_proj W4A8"] = timeit(lambda: blk.in_proj.a8(u, ops.EPI_QUANT, zx, blk.in_out_scale))
 res["out_proj W4A8"] = timeit(lambda: blk.out_proj.a8(yq, ops.EPI_F32, None))
+ugs = u.view(B, -1, 128).sum(-1, dtype=torch.int32)
+ygs = yq.view(B, -1, 128).sum(-1, dtype=torch.int32)
+res["in_proj W4A8 +gsum"] = timeit(lambda: blk.in_proj.a8(u, ops.EPI_QUANT, zx, blk.in_out_scale, ugs))
+res["out_proj W4A8 +gsum"] = timeit(lambda: blk.out_proj.a8(yq, ops.EPI_F32, None, gsum=ygs))
+tiny_x = torch.zeros((1, 16), device=dev)
+tiny_q = torch.empty((1, 16), dtype=torch.int8, device=dev)
+res["launch floor (1x16 quantize)"] = timeit(lambda: ops.quantize_f32(tiny_x, 0.1, tiny_q), reps=50)
 h2 = torch.empty_like(st.h)
 res["copy state 67MB (torch)"] = timeit(lambda: h2.copy_(st.h))
 big_a = torch.empty(1 << 30, dtype=torch.uint8, device=dev)

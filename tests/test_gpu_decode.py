@@ -63,8 +63,10 @@ def test_fused_decode_step(cuda, shape, permute):
     st = torch.as_tensor(h0, device=cuda)
     cc = torch.as_tensor(np.ascontiguousarray(c0.transpose(0, 2, 1)), device=cuda)
     y = torch.empty((B, d.d_inner), dtype=torch.float32, device=cuda)
-    yq = ops.mamba2_decode_step_int8(blk.decode_params, B, zx, cc, st, y=y)
+    gs = torch.zeros((B, d.d_inner // 128), dtype=torch.int32, device=cuda)
+    yq = ops.mamba2_decode_step_int8(blk.decode_params, B, zx, cc, st, y=y, gsum=gs)
     torch.cuda.synchronize()
+    assert np.array_equal(gs.cpu().numpy(), yq.cpu().numpy().astype(np.int32).reshape(B, -1, 128).sum(-1))
     assert np.array_equal(cc.cpu().numpy().transpose(0, 2, 1), rc), "conv cache must be bit-exact"
     mx, frac = _diff(st.cpu().numpy(), rh)
     assert mx <= 1 and frac < 1e-3, (mx, frac)

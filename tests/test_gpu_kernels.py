@@ -91,6 +91,10 @@ def test_gemm_w4a8_exact(cuda, gemm_mode, M, N, K, group):
     assert np.array_equal(got, acc)
     gy = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_F32).cpu().numpy()
     assert np.array_equal(gy, (acc.astype(np.float32) * alpha[None]).astype(np.float32))
+    if K % 128 == 0:   # activation block sums supplied by the producer instead of computed in-kernel
+        gs = torch.as_tensor(a.astype(np.int32).reshape(M, K // 128, 128).sum(-1).astype(np.int32), device=cuda)
+        got2 = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_I32, gsum=gs).cpu().numpy()
+        assert np.array_equal(got2, acc)
 
 
 @pytest.mark.parametrize("M,N,K,group", [(1, 18560 // 4, 4096, 128), (3, 512, 8192, 128), (16, 200, 160, 32)])
@@ -117,9 +121,13 @@ def test_rmsnorm_quant(cuda, M, D):
     g = (1 + 0.1 * r.standard_normal(D)).astype(np.float32)
     s = np.float32(np.abs(osb.rmsnorm(x, g)).max() / 127)
     ref = quantize_codes(osb.rmsnorm(x, g), s, 8)
-    got = ops.rmsnorm_quant(torch.as_tensor(x, device=cuda), torch.as_tensor(g, device=cuda), 1e-5, s).cpu().numpy()
+    gs = torch.zeros((M, D // 128), dtype=torch.int32, device=cuda) if D % 128 == 0 else None
+    got = ops.rmsnorm_quant(torch.as_tensor(x, device=cuda), torch.as_tensor(g, device=cuda), 1e-5, s,
+                            gsum=gs).cpu().numpy()
     mx, frac = code_diff(got, ref)
     assert mx <= 1 and frac < 1e-3
+    if gs is not None:   # block sums of exactly the codes written
+        assert np.array_equal(gs.cpu().numpy(), got.astype(np.int32).reshape(M, -1, 128).sum(-1))
 
 
 @pytest.mark.parametrize("M,D,had", [(4, 512, True), (64, 8192, True), (8, 5120, True), (8, 512, False)])
