@@ -96,6 +96,24 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(kernel_name):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/*_prof_ring.txt, scripts/summarize_profiles.py), or None."""
+    import glob
+    import re
+    if not kernel_name.startswith("state_ring"):
+        return None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*prof_ring*.txt")))
+    if not files:
+        return None
+    txt = open(files[-1]).read()
+    m = re.search(r"dram__bytes_read.sum=([0-9.]+) (\w+); dram__bytes_write.sum=([0-9.]+) (\w+)", txt)
+    if not m:
+        return None
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    return float(m.group(1)) * unit.get(m.group(2), 1) + float(m.group(3)) * unit.get(m.group(4), 1)
+
+
 def dist_init():
     import torch
     import torch.distributed as dist
@@ -240,26 +258,35 @@ def run_decode(args, wl, world, rank, local):
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
 
-    # dominant kernel (state update) timed live on its own stream with CUDA events
+    # dominant kernel: the int8 SSM state update (K9, state_ring_kernel) of the decode step,
+    # timed live with CUDA events on the launch stream, cycling through all layers' states
+    # (67 MB each at b=64, so every launch streams from HBM, not L2)
     blk = lm.blocks[0]
     di, gn = d.d_inner, d.n_state_groups * d.d_state
-    dom_name = "state_update_int8" if blk.a8 else "ssd_scan_f32"
-    zx, cv, y = ws["zx"], ws["conv"], ws["y"]
-    reps = 50
+    reps = 2 * len(lm.blocks)
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sts = [s for s in states]
-    if blk.a8:
+    if blk.a8 and getattr(blk, "fused_decode", False):
+        dom_name = "state_ring_kernel (K9 int8 state update, decode)"
+        ops.set_decode_stages(2)
+
         def dom(i):
             b_ = lm.blocks[i % len(lm.blocks)]
-            ops.state_update_int8(b_.params, B, cv[:, :di], cv[:, di:di + gn], cv[:, di + gn:],
-                                  zx[:, 2 * di + 2 * gn:], zx[:, :di], sts[i % len(sts)].h, y)
-        dom_bytes = B * d.n_heads * d.head_dim * d.d_state * 2 + B * (d.conv_dim + d.in_proj_out) + B * di * 4
+            s_ = states[i % len(states)]
+            ops.mamba2_decode_step_int8(b_.decode_params, B, ws["zx"], s_.conv_cache, s_.h, ws["yq"], ws["y"],
+                                        ws["dws"])
+        tiles = B * d.n_heads
+        dom_bytes = (2 * tiles * d.head_dim * d.d_state          # int8 state read + write
+                     + B * di * 4                                # y (f32) write
+                     + tiles * (4 * d.head_dim + 4) * 4          # per-row scan operands
+                     + tiles * 2 * d.d_state * 4)                # B̂ | Ĉ of the head's group
     else:
+        dom_name = "ssd_scan_f32 (W4A16 fp32 state update, decode)"
+
         def dom(i):
             b_ = lm.blocks[i % len(lm.blocks)]
             zf, cf = ws["zxf"], ws["convf"]
             ops.ssd_scan_f32(b_.params, B, 1, cf[:, :di], cf[:, di:di + gn], cf[:, di + gn:],
-                             zf[:, 2 * di + 2 * gn:], zf[:, :di], sts[i % len(sts)].h, True, y)
+                             zf[:, 2 * di + 2 * gn:], zf[:, :di], states[i % len(states)].h, True, ws["y"])
         dom_bytes = B * d.n_heads * d.head_dim * d.d_state * 8
     for i in range(5):
         dom(i)
@@ -269,6 +296,7 @@ def run_decode(args, wl, world, rank, local):
         dom(i)
     k1.record(st)
     torch.cuda.synchronize()
+    ops.set_decode_stages(7)
     dom_ms = k0.elapsed_time(k1) / reps
     hbm, bf16, pk_kind = peaks()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
@@ -295,8 +323,9 @@ def run_decode(args, wl, world, rank, local):
                            "step_bytes": step_bytes,
                            "step_hbm_frac": step_bytes / (ms / 1e3) / 1e9 / hbm},
                 "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm,
-                             "unit": "GB/s", "frac": achieved / hbm, "traffic": None, "peak_kind": pk_kind,
-                             "algorithmic_bytes_per_launch": dom_bytes, "launch_ms": dom_ms},
+                             "unit": "GB/s", "frac": achieved / hbm, "traffic": ncu_traffic(dom_name),
+                             "peak_kind": pk_kind, "algorithmic_bytes_per_launch": dom_bytes,
+                             "launch_ms": dom_ms},
                 "cpu_baseline": res,
                 "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": B * 4,
                         "d2h_bytes_per_step": B * 4},

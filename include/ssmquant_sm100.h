@@ -179,6 +179,9 @@ typedef struct {
 } sq_mamba2_decode_params;
 
 int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, int B);
+/* Profiling control: which of the three decode-step launches sq_mamba2_decode_step_int8
+ * issues (bitmask 1 conv+operands | 2 state update | 4 norm+FWHT+quant; default 7). */
+int sq_set_decode_stages(int mask);
 int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
                                int8_t* conv_cache /*[B x (Kc-1) x conv_dim]*/, int8_t* state,
                                void* ws, float* y, int64_t ldy, int8_t* yq, int64_t ldyq,

@@ -35,6 +35,11 @@ namespace sq {
 using namespace sm100;
 
 constexpr int DS_P = 64;
+// profiling control (sq_set_decode_stages): bitmask of the launches issued, 1 prep | 2 state | 4 norm
+static int g_decode_stages = [] {
+  const char* e = getenv("SQ_DECODE_STAGES");
+  return e ? atoi(e) : 7;
+}();
 constexpr int DS_MAXCH = 1024;   // channels per norm CTA
 constexpr int ST_THREADS = 256;
 constexpr int ST_HEADS = 4;      // heads per state CTA
@@ -643,11 +648,7 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
   if (B == 0) return SQ_OK;
   cudaStream_t st = as_stream(stream);
   float* wsf = reinterpret_cast<float*>(ws);
-  // SQ_DECODE_STAGES (profiling only): bitmask of the launches to issue, 1 prep | 2 state | 4 norm
-  static const int stages = [] {
-    const char* e = getenv("SQ_DECODE_STAGES");
-    return e ? atoi(e) : 7;
-  }();
+  const int stages = g_decode_stages;
   const int vec = p->conv_kernel == 4 && C % 4 == 0 && ldzx % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(zx) & 3) == 0 && (reinterpret_cast<uintptr_t>(conv_cache) & 3) == 0;
   const int per_blk = vec ? 1024 : 256;
@@ -710,4 +711,10 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
   }
   if (yq_gsum) return launch_group_sum(yq, ldyq, B, di, yq_gsum, ldg, st);
   return check_launch("sq_mamba2_decode_step_int8");
+}
+
+extern "C" int sq_set_decode_stages(int mask) {
+  SQ_REQUIRE(mask >= 0 && mask <= 7, SQ_ERR_ARG, "sq_set_decode_stages: mask must be in [0, 7]");
+  sq::g_decode_stages = mask;
+  return SQ_OK;
 }

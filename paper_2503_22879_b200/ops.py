@@ -331,6 +331,11 @@ def selective_scan_int8(p, B, T, x, dt, BC, z, state, state_in, y):
     return y
 
 
+def set_decode_stages(mask: int):
+    """Profiling control: launches issued by mamba2_decode_step_int8 (1 conv | 2 state | 4 norm)."""
+    _check(lib().sq_set_decode_stages(int(mask)))
+
+
 def set_gemm_mode(mode: int):
     """0: legacy mma.sync GEMM, 1: tcgen05 (W4 operand expanded into TMEM), 2: tcgen05 (into smem)."""
     _check(lib().sq_set_gemm_mode(int(mode)))

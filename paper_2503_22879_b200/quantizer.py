@@ -1,0 +1,177 @@
+"""quantizer — SPEC `[MODULE] quantizer`: symmetric uniform quantization
+(Eq. 1) with the scale layouts the kernels consume.
+
+Host-side (offline) code.  Arithmetic is float32 with true IEEE division and
+round-half-to-even, done with torch on any device, so weight codes are
+bit-identical to the CPU reference contract (tests/test_host_api.py checks them against the
+oracle).  The online activation quantizers live in the kernels (sq_quantize_f32,
+sq_rmsnorm_quant, GEMM requant epilogues).
+
+Weight formats (LEDGER G11):
+* ``quantize_weight_w8``   PerChannel(axis=0) 8-bit          — W8A8 (int32 over all of K)
+* ``quantize_weight_w4``   PerGroup(axis=1, 128) 4-bit float — W4A16 (SPEC literal)
+* ``quantize_weight_w4a8`` progressive PerGroup: scale[n,g] = s_ch[n]·sg[n,g] with integer
+  sg ∈ [1,15], so w8 = w4·sg is exact int8 and the A8 GEMM accumulates in int32 over K.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .errors import LayoutError, ShapeError
+
+__all__ = ["ScaleLayout", "QTensor", "compute_scale", "quantize", "dequantize", "fuse_scales",
+           "quantize_weight_w8", "quantize_weight_w4", "quantize_weight_w4a8", "qrange"]
+
+
+def qrange(bits: int):
+    return -(1 << (bits - 1)), (1 << (bits - 1)) - 1
+
+
+def _f32(x):
+    return x.to(torch.float32) if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, np.float32))
+
+
+def compute_scale(x_slice, bits: int, clip_percentile=None) -> float:
+    """max|x| / (2^(b-1) - 1); 1.0 for an all-zero (or empty) slice."""
+    if bits not in (4, 8):
+        raise ValueError("bits must be 4 or 8")
+    a = _f32(x_slice).abs().reshape(-1)
+    if not bool(torch.isfinite(a).all()):
+        raise ValueError("non-finite input")
+    if a.numel() == 0:
+        return np.float32(1.0)
+    if clip_percentile is not None:
+        m = np.float32(np.percentile(a.double().cpu().numpy(), clip_percentile))
+    else:
+        m = np.float32(a.max().item())
+    if m == 0:
+        return np.float32(1.0)
+    return np.float32(m / np.float32(qrange(bits)[1]))
+
+
+def _codes(x: torch.Tensor, s: torch.Tensor, bits: int) -> torch.Tensor:
+    lo, hi = qrange(bits)
+    return torch.round(x / s).clamp_(lo, hi).to(torch.int8)   # torch.round: half-to-even
+
+
+@dataclass
+class ScaleLayout:
+    """SPEC.md:96-101.  kind ∈ {PerTensor, PerChannel, PerGroup, PerRow, Clustered,
+    PerStateGroup}; ``scales`` f32.  Clustered carries ``cell_of`` (index -> cell)."""
+    kind: str
+    scales: object
+    axis: int = -1
+    group_size: int = 0
+    bounds: tuple = ()
+    cell_of: object = None
+
+    def expand(self, shape) -> torch.Tensor:
+        s = _f32(self.scales).reshape(-1)
+        shape = tuple(shape)
+        nd = len(shape)
+        if bool((s <= 0).any()):
+            raise LayoutError("scales must be > 0")
+        if self.kind == "PerTensor":
+            if s.numel() != 1:
+                raise LayoutError("PerTensor needs one scale")
+            return s.reshape(()).expand(shape)
+        ax = 0 if self.kind == "PerRow" else self.axis % nd
+        n = shape[ax]
+        if self.kind == "PerGroup" and nd == 2 and ax == 1 and s.numel() == shape[0] * -(-n // self.group_size):
+            g = torch.clamp(torch.arange(n) // self.group_size, max=s.numel() // shape[0] - 1)
+            return s.reshape(shape[0], -1)[:, g]
+        if self.kind in ("PerChannel", "PerRow"):
+            idx = torch.arange(n)
+        elif self.kind == "PerGroup":
+            idx = torch.clamp(torch.arange(n) // self.group_size, max=s.numel() - 1)
+        elif self.kind == "PerStateGroup":
+            idx = torch.searchsorted(torch.as_tensor(self.bounds), torch.arange(n), right=True) - 1
+        elif self.kind == "Clustered":
+            idx = torch.as_tensor(np.asarray(self.cell_of), dtype=torch.long)
+        else:
+            raise LayoutError(f"unknown layout kind {self.kind}")
+        if idx.numel() != n or int(idx.max()) >= s.numel():
+            raise LayoutError("layout does not cover tensor")
+        view = [1] * nd
+        view[ax] = n
+        return s[idx].reshape(view).expand(shape)
+
+
+@dataclass
+class QTensor:
+    """integer payload (4-bit values kept unpacked as int8) + layout."""
+    shape: tuple
+    bits: int
+    payload: torch.Tensor
+    layout: ScaleLayout
+    extra: dict = field(default_factory=dict)
+
+
+def quantize(x, layout: ScaleLayout, bits: int) -> QTensor:
+    """clamp(round_half_even(x / s))."""
+    x = _f32(x)
+    return QTensor(tuple(x.shape), bits, _codes(x, layout.expand(x.shape), bits), layout)
+
+
+def dequantize(q: QTensor) -> torch.Tensor:
+    """x̂ = q · s."""
+    return q.payload.to(torch.float32) * q.layout.expand(q.shape)
+
+
+def fuse_scales(s_x, s_w, s_y) -> np.float32:
+    """s_fused = s_x / s_y; s_w rides in the weight scale."""
+    if s_x <= 0 or s_w <= 0 or s_y <= 0:
+        raise ValueError("scales must be > 0")
+    return np.float32(np.float32(s_x) / np.float32(s_y))
+
+
+def _group_absmax_scale(wg: torch.Tensor, bits: int) -> torch.Tensor:
+    """compute_scale over the last axis of every group, vectorised (zero group -> 1.0)."""
+    m = wg.abs().amax(dim=-1)
+    s = m / np.float32(qrange(bits)[1])
+    return torch.where(m == 0, torch.ones_like(s), s)
+
+
+def quantize_weight_w8(w) -> QTensor:
+    """PerChannel(axis=0) 8-bit weights (W8A8, LEDGER G11)."""
+    w = _f32(w)
+    if w.dim() != 2:
+        raise ShapeError("weights are [out x in]")
+    s = _group_absmax_scale(w, 8)
+    codes = _codes(w, s[:, None], 8)
+    return QTensor(tuple(w.shape), 8, codes, ScaleLayout("PerChannel", s, axis=0),
+                   extra={"s_ch": s, "sg": torch.ones((w.shape[0], 1), dtype=torch.int8), "group": w.shape[1]})
+
+
+def quantize_weight_w4(w, group: int = 128) -> QTensor:
+    """PerGroup(axis=1, group) 4-bit weights with float scales (W4A16)."""
+    w = _f32(w)
+    n, k = w.shape
+    if k % group:
+        raise ShapeError("K must be a multiple of the group size")
+    wg = w.reshape(n, k // group, group)
+    s = _group_absmax_scale(wg, 4)
+    codes = _codes(wg, s[:, :, None], 4).reshape(n, k)
+    return QTensor((n, k), 4, codes, ScaleLayout("PerGroup", s.reshape(-1), axis=1, group_size=group),
+                   extra={"s_group": s, "group": group})
+
+
+def quantize_weight_w4a8(w, group: int = 128) -> QTensor:
+    """Progressive per-group 4-bit weights for the A8 GEMM (LEDGER G11b):
+    s_gf = max|w_g|/7, s_ch = max_g s_gf / 15, sg = clamp(ceil(s_gf/s_ch), 1, 15),
+    codes = clamp(rint(w / (s_ch·sg)))."""
+    w = _f32(w)
+    n, k = w.shape
+    if k % group:
+        raise ShapeError("K must be a multiple of the group size")
+    wg = w.reshape(n, k // group, group)
+    s_gf = _group_absmax_scale(wg, 4)
+    s_ch = s_gf.amax(dim=1) / np.float32(15.0)
+    sg = torch.clamp(torch.ceil(s_gf / s_ch[:, None]), 1, 15).to(torch.int8)
+    scale = s_ch[:, None] * sg.to(torch.float32)
+    codes = _codes(wg, scale[:, :, None], 4).reshape(n, k)
+    return QTensor((n, k), 4, codes, ScaleLayout("PerGroup", scale.reshape(-1), axis=1, group_size=group),
+                   extra={"s_ch": s_ch, "sg": sg, "group": group})
