@@ -91,3 +91,22 @@ def test_mamba2_8b_layer_decode_b64(cuda):
     for i in (0, 63):      # the batched oracle equals the per-sequence oracle
         ro1, rs1 = oq.block_forward_quantized(u[i:i + 1], qb, oq.QState(h0[i], c0[i]))
         assert np.array_equal(ro1[0], ro[i]) and np.array_equal(rs1.h, rh[i])
+
+
+def test_product_quantize_pipeline_on_gpu(cuda):
+    """The product's own host pipeline (gen-toy -> calibrate on the GPU -> quantize) feeding the
+    GPU model: logits within 1e-2 of the oracle pipeline's quantized model."""
+    from paper_2503_22879_b200 import cli
+    from paper_2503_22879_b200.model import QuantizedMambaLM
+    from paper_2503_22879_b200.ssm_block import Dims
+    dims = ("mamba2", 256, 512, 64, 8, 64, 2, 4)
+    fm = cli.cmd_gen_toy(Dims(*dims), 2, seed=0)
+    toks = cli.calib_tokens(512, 2, 64)
+    qm = cli.cmd_quantize(fm, toks, "W4A8", device="cuda")
+    ofm = opl.cmd_gen_toy(osb.Dims(*dims), 2, seed=0)
+    oqm = opl.cmd_quantize(ofm, toks, "W4A8")
+    ref, _ = opl.quant_forward(oqm, toks[0, :32])
+    lm = QuantizedMambaLM(qm, cuda)
+    lg, _ = lm.prefill(torch.as_tensor(toks[:1, :32], device=cuda), all_logits=True)
+    rel = np.abs(lg.cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert rel < 1e-2, rel

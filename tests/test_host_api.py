@@ -1,0 +1,179 @@
+"""CPU: the product's host-side (offline) API against the test oracle — SURVEY §8 a13-a15.
+
+Weight codes, u4 packing, ClusterMaps, reorder permutations and every scale table must be
+bit-exact (north_star); the float calibration forward (torch) agrees with the oracle's
+within float tolerance, and fed the same statistics the whole quantize pipeline produces
+identical quantized models.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import calibrate as ocal
+from oracle import hadamard as ohad
+from oracle import pipeline as opl
+from oracle import quantizer as oqz
+from oracle import reorder as oro
+from oracle import tensor_core as otc
+from oracle.ssm_block import Dims as ODims
+from paper_2503_22879_b200 import archive, calibrate, cli, hadamard, quantizer, reorder
+from paper_2503_22879_b200.ssm_block import Dims
+
+TINY2 = ("mamba2", 64, 128, 16, 8, 16, 2, 4)
+TINY1 = ("mamba1", 64, 128, 16, 1, 128, 1, 4, 8)
+
+
+def _np(t):
+    return t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+def test_weight_quantizers_bit_exact():
+    r = otc.make_rng(31)
+    w = (r.standard_normal((24, 256)) * np.exp(r.uniform(-3, 3, (1, 256)))).astype(np.float32)
+    w[3, :128] = 0.0                                        # a zero group -> scale 1.0
+    a, b = oqz.quantize_weight_w8(w), quantizer.quantize_weight_w8(w)
+    assert np.array_equal(a.payload, _np(b.payload)) and np.array_equal(a.extra["s_ch"], _np(b.extra["s_ch"]))
+    a, b = oqz.quantize_weight_w4_group(w, 128), quantizer.quantize_weight_w4(w, 128)
+    assert np.array_equal(a.payload, _np(b.payload)) and np.array_equal(a.extra["s_group"], _np(b.extra["s_group"]))
+    a, b = oqz.quantize_weight_w4a8(w, 128), quantizer.quantize_weight_w4a8(w, 128)
+    assert np.array_equal(a.payload, _np(b.payload))
+    assert np.array_equal(a.extra["sg"], _np(b.extra["sg"])) and np.array_equal(a.extra["s_ch"], _np(b.extra["s_ch"]))
+
+
+def test_quantize_layouts_and_spec_examples():
+    x = np.array([2.54, -1.27, 0.0], np.float32)
+    assert np.isclose(quantizer.compute_scale(x, 8), 0.02)
+    assert _np(quantizer.quantize(x, quantizer.ScaleLayout("PerTensor", np.float32(0.02)), 8).payload).tolist() == \
+        [127, -64, 0]
+    r = otc.make_rng(32)
+    v = r.standard_normal((6, 40)).astype(np.float32)
+    s = r.uniform(0.01, 0.1, 5).astype(np.float32)
+    for lay_o, lay_p in [
+        (oqz.ScaleLayout("PerGroup", s, axis=1, group_size=8), quantizer.ScaleLayout("PerGroup", s, axis=1, group_size=8)),
+        (oqz.ScaleLayout("PerStateGroup", s, axis=1, bounds=(0, 8, 16, 24, 32, 40)),
+         quantizer.ScaleLayout("PerStateGroup", s, axis=1, bounds=(0, 8, 16, 24, 32, 40))),
+    ]:
+        assert np.array_equal(oqz.quantize(v, lay_o, 8).payload, _np(quantizer.quantize(v, lay_p, 8).payload))
+    assert quantizer.fuse_scales(0.02, 1.0, 0.04) == np.float32(0.5)
+
+
+def test_hadamard_bit_exact():
+    r = otc.make_rng(33)
+    v = r.standard_normal((3, 5120)).astype(np.float32)
+    assert np.array_equal(ohad.fwht_blocked(v), _np(hadamard.fwht_blocked(v)))
+    v = r.standard_normal((2, 64)).astype(np.float32)
+    assert np.array_equal(ohad.fwht(v, ohad.HadamardPlan(64)), _np(hadamard.fwht(v, hadamard.HadamardPlan(64))))
+    w = r.standard_normal((16, 40)).astype(np.float32)
+    assert np.array_equal(ohad.fuse_hadamard_out_proj(w, 40, 1), _np(hadamard.fuse_hadamard_out_proj(w, 40, 1)))
+    assert np.array_equal(ohad.fuse_hadamard_in_proj(w), _np(hadamard.fuse_hadamard_in_proj(w)))
+    y = r.standard_normal((4, 128)).astype(np.float32)
+    assert np.array_equal(ohad.hadamard_quantize(y, ohad.HadamardPlan(128, "none", 0.3), 8),
+                          _np(hadamard.hadamard_quantize(y, hadamard.HadamardPlan(128, "none", 0.3), 8)))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sort_and_cluster_bit_exact(seed):
+    r = otc.make_rng(34, seed)
+    nh, P = [(8, 16), (16, 64), (4, 8), (80, 64), (128, 64), (1, 512)][seed]
+    mx = (np.exp(r.uniform(-3, 3, (nh, P))) * np.exp(r.uniform(-2, 2, (nh, 1)))).astype(np.float32)
+    a = ocal.sort_and_cluster(ocal.CalibStats(mx.reshape(-1), 1), nh, P, 4, 4, seed)
+    b = calibrate.sort_and_cluster(calibrate.CalibStats(mx.reshape(-1), 1), nh, P, 4, 4, seed)
+    for f in ("head_perm", "channel_perm", "head_group_bounds", "channel_group_bounds", "scales"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert np.array_equal(a.cell_of_new(), b.cell_of_new())
+    X = r.standard_normal((30, 5))
+    assert np.array_equal(ocal.kmeans(X, 4, seed), calibrate.kmeans(X, 4, seed))
+
+
+def test_state_group_scales_and_reorder_bit_exact():
+    r = otc.make_rng(35)
+    nh, P, G, N = 8, 16, 2, 16
+    mx = np.exp(r.uniform(-3, 3, nh * P)).astype(np.float32)
+    sb = np.exp(r.uniform(-3, 3, G * N)).astype(np.float32)
+    hh = np.exp(r.uniform(-2, 2, nh * P)).astype(np.float32)
+    ocm = ocal.sort_and_cluster(ocal.CalibStats(mx, 1), nh, P)
+    pcm = calibrate.sort_and_cluster(calibrate.CalibStats(mx, 1), nh, P)
+    a = ocal.build_state_group_scales(ocal.CalibStats(sb, 1), ocal.CalibStats(sb * 2, 1), G, N, ocal.CalibStats(hh, 1), ocm)
+    b = calibrate.build_state_group_scales(calibrate.CalibStats(sb, 1), calibrate.CalibStats(sb * 2, 1), G, N,
+                                           calibrate.CalibStats(hh, 1), pcm)
+    for f in ("boundaries", "scales_B", "scales_C", "scales_state"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    d = Dims(*TINY2)
+    ob = opl.gen_block(ODims(*TINY2), 3, 0)
+    pb = cli.gen_block(d, 3, 0)
+    opl_plan = oro.build_reorder_plan(ocm, ob.dims)
+    p_plan = reorder.build_reorder_plan(pcm, d)
+    assert np.array_equal(opl_plan.pi, p_plan.pi)
+    o2, p2 = oro.apply_reorder(ob, opl_plan), reorder.apply_reorder(pb, p_plan)
+    for f in ("in_proj", "conv_weight", "conv_bias", "a_log", "d_param", "dt_bias", "norm_weight", "out_proj",
+              "head_group"):
+        assert np.array_equal(getattr(o2, f), getattr(p2, f)), f
+    with pytest.raises(Exception):
+        reorder.apply_reorder(p2, p_plan)
+
+
+@pytest.mark.parametrize("dims", [TINY2, TINY1], ids=["mamba2", "mamba1"])
+def test_gen_toy_and_calibration(dims):
+    od, d = ODims(*dims), Dims(*dims)
+    fo, fp = opl.cmd_gen_toy(od, 2, seed=4, vocab=64), cli.cmd_gen_toy(d, 2, seed=4, vocab=64)
+    assert np.array_equal(fo.embedding, fp.embedding) and np.array_equal(fo.head, fp.head)
+    for a, b in zip(fo.blocks, fp.blocks):
+        for f in ("in_proj", "conv_weight", "a_log", "dt_bias", "out_proj", "x_proj", "dt_proj"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)) if getattr(a, f) is not None else getattr(b, f) is None
+    toks = opl.calib_tokens(64, 2, 24)
+    so = opl.collect_stats(fo, toks)
+    sp = calibrate.collect_stats(fp, toks, device="cpu")          # torch float forward
+    for lo, lp in zip(so, sp):
+        assert lo.keys() == lp.keys()
+        for k in lo:
+            a, b = lo[k].channel_max, lp[k].channel_max
+            assert np.allclose(a, b, rtol=2e-4, atol=1e-6 * np.abs(a).max()), k
+
+
+@pytest.mark.parametrize("profile", ["W8A8", "W4A8", "W4A16"])
+@pytest.mark.parametrize("dims", [TINY2, TINY1], ids=["mamba2", "mamba1"])
+def test_quantize_pipeline_bit_exact(profile, dims):
+    """Same float model + same calibration statistics -> identical quantized model."""
+    od, d = ODims(*dims), Dims(*dims)
+    fo, fp = opl.cmd_gen_toy(od, 2, seed=5, vocab=64), cli.cmd_gen_toy(d, 2, seed=5, vocab=64)
+    toks = opl.calib_tokens(64, 2, 24)
+    stats = opl.collect_stats(fo, toks)
+    pstats = [{k: calibrate.CalibStats(v.channel_max, v.sample_count, v.values) for k, v in s.items()}
+              for s in stats]
+    qo = opl.cmd_quantize(fo, toks, profile)
+    qp = cli.cmd_quantize(fp, toks, profile, stats=pstats)
+    assert np.array_equal(qo.emb_codes, qp.emb_codes) and np.array_equal(qo.emb_scale, qp.emb_scale)
+    assert qo.s_head == qp.s_head and np.array_equal(qo.head.codes, qp.head.codes)
+    for a, b in zip(qo.blocks, qp.blocks):
+        for lin in ("in_proj", "out_proj", "x_proj", "dt_proj"):
+            la, lb = getattr(a, lin), getattr(b, lin)
+            if la is None:
+                assert lb is None
+                continue
+            for f in ("codes", "s_ch", "sg", "s_group"):
+                fa, fb = getattr(la, f), getattr(lb, f)
+                assert (fa is None and fb is None) or np.array_equal(np.asarray(fa), np.asarray(fb)), (lin, f)
+        for f in ("s_u", "s_y", "s_dt", "in_out_scale", "conv_in_scale", "conv_out_scale", "state_scale",
+                  "xproj_out_scale", "head_group", "conv_weight", "norm_weight"):
+            fa, fb = getattr(a, f), getattr(b, f)
+            assert (fa is None and fb is None) or np.array_equal(np.asarray(fa), np.asarray(fb)), f
+
+
+def test_archive_roundtrip_and_cli(tmp_path):
+    p = str(tmp_path / "a.bin")
+    archive.archive_write({"w": np.ones((2, 2), np.float32), "q": ("u4packed", np.array([3, -2, -8, 7])),
+                           "m": {"x": 1}}, p)
+    back = archive.archive_read(p)
+    assert back["q"].tolist() == [3, -2, -8, 7] and back["m"] == {"x": 1}
+    assert np.array_equal(archive.pack_u4([3, -2]), otc.pack_u4([3, -2]))               # 0xE3
+    fm_path, q_path = str(tmp_path / "toy.bin"), str(tmp_path / "q.bin")
+    assert cli.main(["gen-toy", "--dims", "mamba2,64,128,16,8,16,2,4", "--blocks", "1", "--vocab", "64",
+                     "--out", fm_path]) == 0
+    fm = archive.read_float_model(fm_path)
+    ref = cli.cmd_gen_toy(Dims(*TINY2), 1, 0, 64)
+    assert np.array_equal(fm.blocks[0].in_proj, ref.blocks[0].in_proj)
+    assert cli.main(["quantize", "--model", fm_path, "--profile", "W4A8", "--samples", "1", "--seq-len", "8",
+                     "--out", q_path]) == 0
+    info = archive.inspect(q_path)
+    assert info["blocks.0.in_proj.codes"][-1] == "int8" and "blocks.0.state_scale" in info
+    assert cli.main(["quantize", "--model", str(tmp_path / "missing.bin"), "--out", q_path]) == 1
