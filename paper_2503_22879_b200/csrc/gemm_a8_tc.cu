@@ -494,9 +494,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) act[(c0 + j) * TC_BN + row] = (uint8_t)val[j];
         } else if (args.epi == SQ_EPI_QUANT) {
+          float yv[8];
+          int8_t qv[8];
+          bool tie = false;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            act[(c0 + j) * TC_BN + row] = (uint8_t)quant8_inv(__fmul_rn((float)val[j], alpha), cs, ics);
+          for (int j = 0; j < 8; ++j) {
+            yv[j] = __fmul_rn((float)val[j], alpha);
+            qv[j] = quant8_fast(yv[j], ics, tie);
+          }
+          if (tie) {   // rare: a value within 1e-4 of a rounding tie -> exact division
+#pragma unroll
+            for (int j = 0; j < 8; ++j) qv[j] = quant8(yv[j], cs);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) act[(c0 + j) * TC_BN + row] = (uint8_t)qv[j];
         } else {
           uint32_t* st32 = reinterpret_cast<uint32_t*>(act);
 #pragma unroll

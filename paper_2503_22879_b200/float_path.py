@@ -18,6 +18,8 @@ EPS_NORM = 1e-5
 
 
 def _t(a, dev, dt=torch.float32):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dt)
     return torch.as_tensor(np.asarray(a)).to(device=dev, dtype=dt)
 
 
