@@ -431,7 +431,14 @@ extern "C" int sq_ssd_scan_int8(const sq_mamba2_params* p, int B, int T, const i
                                 const int8_t* Bm, const int8_t* Cm, int64_t ldbc, const int8_t* dt, int64_t lddt,
                                 const int8_t* z, int64_t ldz, int8_t* state, int state_in, float* y, int64_t ldy,
                                 int chunk, void* stream) {
-  (void)chunk;
+  (void)chunk;   // the tensor-core path uses 64-token chunks
+  SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_ssd_scan_int8: bad args");
+  if (B == 0 || T == 0) return SQ_OK;
+  if (T > 1) {   // chunked SSD on the tensor cores (ssd_chunk.cu); other shapes: sequential scan
+    const int rc = launch_ssd_chunk(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
+                                    as_stream(stream));
+    if (rc != SQ_ERR_ARG) return rc;
+  }
   return launch_mamba2<int8_t>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
                                as_stream(stream), "sq_ssd_scan_int8");
 }

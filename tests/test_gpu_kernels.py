@@ -244,3 +244,54 @@ def test_gemm_w4a8_tc_repeat_deterministic(cuda, M, N, K):
         got = ops.gemm_w4a8(torch.as_tensor(a, device=cuda), tw, torch.as_tensor(sg, device=cuda), 128,
                             torch.ones(N, device=cuda), N, ops.EPI_I32).cpu().numpy()
         assert np.array_equal(got, int_gemm(a, ql.int8_weight().T))
+
+
+@pytest.mark.parametrize("B,T,nh,G,N,seed", [(2, 300, 80, 1, 128, 0), (1, 64, 8, 2, 64, 1), (3, 129, 16, 4, 128, 2)])
+def test_ssd_chunk_scan_vs_oracle(cuda, B, T, nh, G, N, seed):
+    """Tensor-core chunked SSD (sq_ssd_scan_int8, T > 1) vs the oracle's sequential f32 scan on
+    the same int8 codes: y rel-err <= 5e-3, final int8 state within one step (mismatch < 2e-2),
+    with and without an incoming state (chunked prefill continuation)."""
+    ops = _ops()
+    from paper_2503_22879_b200.ssm_block import SsmState  # noqa: F401
+    r = _rng(12, seed)
+    P = 64
+    di, gn = nh * P, G * N
+    hg = (np.arange(nh) // (nh // G)).astype(np.int32)
+    A = (-np.exp(r.uniform(0, 2.7, nh))).astype(np.float32)
+    D = np.ones(nh, np.float32)
+    dtb = (np.log(np.expm1(r.uniform(1e-3, 1e-1, nh)))).astype(np.float32)
+    s_x = r.uniform(0.005, 0.02, di).astype(np.float32)
+    s_B = r.uniform(0.005, 0.02, G).astype(np.float32)
+    s_C = r.uniform(0.005, 0.02, G).astype(np.float32)
+    s_h = r.uniform(0.002, 0.01, di).astype(np.float32)
+    s_dt, s_z = np.float32(0.03), np.float32(0.03)
+    xq = r.integers(-128, 128, (B * T, di)).astype(np.int8)
+    Bq = r.integers(-128, 128, (B * T, gn)).astype(np.int8)
+    Cq = r.integers(-128, 128, (B * T, gn)).astype(np.int8)
+    dq = r.integers(-128, 128, (B * T, nh)).astype(np.int8)
+    zq = r.integers(-128, 128, (B * T, di)).astype(np.int8)
+    h0 = r.integers(-100, 100, (B, nh, P, N)).astype(np.int8)
+    t = lambda a: torch.as_tensor(a, device=cuda)
+    tens = dict(hg=t(hg), A=t(A), D=t(D), dtb=t(dtb), s_x=t(s_x), s_B=t(s_B), s_C=t(s_C), s_h=t(s_h))
+    prm = ops.mamba2_params(nh, P, N, G, tens["hg"], tens["A"], tens["D"], tens["dtb"], s_dt, s_z, tens["s_x"],
+                            tens["s_B"], tens["s_C"], tens["s_h"])
+    for state_in in (False, True):
+        st = t(h0.copy())
+        y = torch.empty((B * T, di), dtype=torch.float32, device=cuda)
+        ops.ssd_scan_int8(prm, B, T, t(xq), t(Bq), t(Cq), t(dq), t(zq), st, state_in, y)
+        y = y.cpu().numpy()
+        st = st.cpu().numpy()
+        for bi in range(B):
+            sl = slice(bi * T, (bi + 1) * T)
+            x = (xq[sl].astype(np.float32) * s_x).reshape(T, nh, P)
+            Bh = (Bq[sl].astype(np.float32).reshape(T, G, N) * s_B[None, :, None]).astype(np.float32)
+            Ch = (Cq[sl].astype(np.float32).reshape(T, G, N) * s_C[None, :, None]).astype(np.float32)
+            dA, dt = osb.discretize((dq[sl].astype(np.float32) * s_dt).astype(np.float32), dtb, A)
+            z = (zq[sl].astype(np.float32) * s_z).reshape(T, nh, P)
+            hin = (h0[bi].astype(np.float32) * s_h.reshape(nh, P)[:, :, None]) if state_in else None
+            ry, rh = osb.selective_scan(x, dA, dt, Bh, Ch, D, z, hin, hg)
+            rel = np.abs(y[sl] - ry.reshape(T, di)).max() / np.abs(ry).max()
+            assert rel <= 5e-3, (state_in, bi, rel)
+            rq = quantize_codes(rh, s_h.reshape(nh, P)[:, :, None], 8)
+            mx, frac = code_diff(st[bi], rq)
+            assert mx <= 1 and frac < 2e-2, (state_in, bi, mx, frac)
