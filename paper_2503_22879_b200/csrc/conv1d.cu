@@ -64,6 +64,88 @@ __global__ void conv1d_prefill_kernel(const TIn* __restrict__ x, int64_t ldx, co
   }
 }
 
+// int8 prefill, 4 channels per thread (one 32-bit load/store per token row, a warp moves
+// 128 contiguous bytes), kSeg4 tokens per thread in sub-blocks of 8 rows whose loads are
+// issued before any math.  Same op order as the scalar kernel; SiLU with a rounded
+// reciprocal and the division-free quantizer with its exact tie fallback, as in the decode
+// prep kernel (decode_ssm.cu conv4_step).
+constexpr int kSeg4 = 32;
+template <int KC>
+__global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __restrict__ x, int64_t ldx,
+                                                              const float* __restrict__ w,
+                                                              const float* __restrict__ bias,
+                                                              const float* __restrict__ s_in,
+                                                              const float* __restrict__ s_out, int T, int C,
+                                                              const int8_t* __restrict__ cache, int cache_in,
+                                                              int8_t* __restrict__ out, int64_t ldo) {
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int b = blockIdx.z;
+  if (c0 >= C) return;
+  const int t0 = blockIdx.y * kSeg4;
+  const int t1 = min(T, t0 + kSeg4);
+  float wc[4][KC], si[4], so[4], iso[4], bc[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+#pragma unroll
+    for (int j = 0; j < KC; ++j) wc[e][j] = j < KC ? w[(c0 + e) * KC + j] : 0.f;
+    si[e] = s_in[c0 + e];
+    so[e] = s_out[c0 + e];
+    iso[e] = __frcp_rn(so[e]);
+    bc[e] = bias[c0 + e];
+  }
+  // win[e][j]: dequantised input at token t-KC+1+j; slot KC-1 is the newest.
+  float win[4][KC];
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+#pragma unroll
+    for (int j = 0; j < KC; ++j) win[e][j] = 0.f;
+#pragma unroll
+  for (int j = 1; j < KC; ++j) {   // tokens t0-KC+j, j = 1..KC-1 -> slots KC-KC+j-1
+    const int t = t0 - KC + j;
+    uint32_t u = 0;
+    if (t >= 0)
+      u = *reinterpret_cast<const uint32_t*>(x + ((int64_t)b * T + t) * ldx + c0);
+    else if (cache_in)
+      u = *reinterpret_cast<const uint32_t*>(cache + ((int64_t)b * (KC - 1) + (KC - 1 + t)) * C + c0);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+#pragma unroll
+      for (int k = 0; k < KC - 1; ++k) win[e][k] = win[e][k + 1];
+      win[e][KC - 1] = __fmul_rn((float)(int8_t)(u >> (8 * e)), si[e]);
+    }
+  }
+  for (int tb = t0; tb < t1; tb += 8) {
+    uint32_t u[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      u[i] = tb + i < t1 ? __ldg(reinterpret_cast<const uint32_t*>(x + ((int64_t)b * T + tb + i) * ldx + c0)) : 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (tb + i >= t1) break;
+      uint32_t packed = 0;
+      bool tie = false;
+      float sv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+#pragma unroll
+        for (int k = 0; k < KC - 1; ++k) win[e][k] = win[e][k + 1];
+        win[e][KC - 1] = __fmul_rn((float)(int8_t)(u[i] >> (8 * e)), si[e]);
+        float acc = bc[e];
+#pragma unroll
+        for (int j = 0; j < KC; ++j) acc = __fadd_rn(acc, __fmul_rn(wc[e][j], win[e][KC - KC + j]));
+        sv[e] = silu_fast(acc);
+        packed |= (uint32_t)(uint8_t)quant8_fast(sv[e], iso[e], tie) << (8 * e);
+      }
+      if (tie) {
+        packed = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) packed |= (uint32_t)(uint8_t)quant8(sv[e], so[e]) << (8 * e);
+      }
+      *reinterpret_cast<uint32_t*>(out + ((int64_t)b * T + tb + i) * ldo + c0) = packed;
+    }
+  }
+}
+
 // Final cache window = last Kc-1 entries of (old cache ++ x).  Separate launch so the
 // prefill kernel's reads of the old cache never race with these writes.
 template <typename T_>
@@ -112,9 +194,14 @@ extern "C" int sq_conv1d_int8(const int8_t* x, int64_t ldx, const float* w, cons
              "sq_conv1d_int8: bad shape (Kc=%d)", Kc);
   if (B == 0 || T == 0) return SQ_OK;
   cudaStream_t st = as_stream(stream);
-  dim3 g((C + 127) / 128, (T + kSeg - 1) / kSeg, B);
-  conv1d_prefill_kernel<int8_t, int8_t, true><<<g, 128, 0, st>>>(x, ldx, w, bias, s_in, s_out, B, T, C, Kc, cache,
-                                                                 cache_in, out, ldo);
+  if (Kc == 4 && C % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0 && ((uintptr_t)x & 3) == 0 && ((uintptr_t)out & 3) == 0) {
+    dim3 g((C / 4 + 127) / 128, (T + kSeg4 - 1) / kSeg4, B);
+    conv1d_prefill4_kernel<4><<<g, 128, 0, st>>>(x, ldx, w, bias, s_in, s_out, T, C, cache, cache_in, out, ldo);
+  } else {
+    dim3 g((C + 127) / 128, (T + kSeg - 1) / kSeg, B);
+    conv1d_prefill_kernel<int8_t, int8_t, true><<<g, 128, 0, st>>>(x, ldx, w, bias, s_in, s_out, B, T, C, Kc, cache,
+                                                                   cache_in, out, ldo);
+  }
   if (Kc > 1) conv1d_cache_kernel<int8_t><<<dim3((C + 127) / 128, B), 128, 0, st>>>(x, ldx, B, T, C, Kc, cache, cache_in);
   return check_launch("sq_conv1d_int8");
 }

@@ -119,13 +119,30 @@ __device__ __forceinline__ void load16(const float* p, float (&v)[16]) {
   }
 }
 
-__device__ __forceinline__ void store16_q(int8_t* p, const float (&v)[16], float s) {
-  uint32_t w[4];
+// 16 codes packed little-endian into 4 words: division-free quantizer, and the exact
+// quant8 only when some value sits within 1e-4 of a rounding tie (bit-identical codes).
+__device__ __forceinline__ void quant16(const float (&v)[16], float s, uint32_t (&w)[4]) {
+  const float is = __frcp_rn(s);
+  bool tie = false;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    w[e] = (uint32_t)(uint8_t)quant8(v[e * 4], s) | ((uint32_t)(uint8_t)quant8(v[e * 4 + 1], s) << 8) |
-           ((uint32_t)(uint8_t)quant8(v[e * 4 + 2], s) << 16) | ((uint32_t)(uint8_t)quant8(v[e * 4 + 3], s) << 24);
+    w[e] = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[e] |= (uint32_t)(uint8_t)quant8_fast(v[e * 4 + k], is, tie) << (8 * k);
   }
+  if (tie) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      w[e] = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[e] |= (uint32_t)(uint8_t)quant8(v[e * 4 + k], s) << (8 * k);
+    }
+  }
+}
+
+__device__ __forceinline__ void store16_q(int8_t* p, const float (&v)[16], float s) {
+  uint32_t w[4];
+  quant16(v, s, w);
   *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
@@ -149,12 +166,14 @@ __global__ void __launch_bounds__(1024) rmsnorm16_kernel(const float* x, int64_t
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
   if (QUANT) {
-    store16_q(reinterpret_cast<int8_t*>(out) + (int64_t)blockIdx.x * ldo + base, v, s);
+    uint32_t w[4];
+    quant16(v, s, w);
+    *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(out) + (int64_t)blockIdx.x * ldo + base) =
+        make_uint4(w[0], w[1], w[2], w[3]);
     if (gsum) {   // sums of the codes over each 128-wide block (8 threads)
-      const float is = __frcp_rn(s);
       int cs = 0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) cs += quant8_inv(v[i], s, is);
+      for (int e = 0; e < 4; ++e) cs = __dp4a((int)w[e], 0x01010101, cs);
       cs += __shfl_xor_sync(0xffffffffu, cs, 1);
       cs += __shfl_xor_sync(0xffffffffu, cs, 2);
       cs += __shfl_xor_sync(0xffffffffu, cs, 4);

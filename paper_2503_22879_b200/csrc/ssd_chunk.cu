@@ -1,21 +1,29 @@
 // K7: int8 SSD chunk scan for Mamba2 prefill on the tensor cores (ssm_block.ssd_chunked,
 // SPEC.md:308-316; "8-bit SSD"; Table 3 shapes PAPER.md:254).
 //
-// One CTA per (sequence, head), 4 warps, chunks of Q = 64 tokens processed in order with the
-// head's state H [P=64 x N] resident in the MMA accumulator registers across chunks:
+// One CTA per (sequence, head), 4 warps, chunks of Q = 64 tokens processed in order.  Warp w
+// owns the state rows p = 16w .. 16w+15: its slice of H [P=64 x N] stays in MMA accumulator
+// registers across chunks, and it produces the transposed outputs Yᵀ[p, t] for those rows:
 //
-//   CB[t,s]  = Ĉ_t · B̂_s                       int8 x int8 -> int32 (m16n8k32), exact
-//   W[t,s]   = CB · s_B s_C · exp(cs_t - cs_s) · Δ_s   (s <= t)     f32 -> fp16, kept in
-//              registers: the CB accumulator fragments are reused as the A operand
-//   Y_diag   = W · Xcodes                      fp16 x fp16 (x codes exact) -> f32, × s_x[p]
-//   Y_off    = exp(cs_t) s_C · (Ccodes · Hᵀ)   fp16 (H rounded to fp16) -> f32
-//   y        = (Y_diag + Y_off + D x̂) · SiLU(ẑ)
-//   H        = exp(cs_Q) H + Σ_s (e^{cs_Q-cs_s} Δ_s s_x[p] s_B x_s[p]) B_s
+//   CB[t,s]  = Ĉ_t · B̂_s                        int8 x int8 -> int32 (m16n8k32), exact; warp w
+//                                                computes rows t = 16w.., all s
+//   W[t,s]   = CB s_B s_C e^{cs_t - cs_s} Δ_s  (s <= t)   -> fp16, shared with all warps
+//   Y_diagᵀ  = X̂ᵀ · Wᵀ                          fp16 (x codes exact) -> f32, × s_x[p]
+//   Y_offᵀ   = H · Ĉᵀ                           fp16 (H rounded to fp16; the accumulator
+//                                                fragments are reused as the A operand)
+//                                                -> f32, × e^{cs_t} s_C
+//   y[t,p]   = (Y_diag + Y_off + D x̂) · SiLU(ẑ)   (SiLU from a 256-entry table of the z codes)
+//   H        = e^{cs_Q} H + Σ_s (e^{cs_Q-cs_s} Δ_s s_x[p] s_B x_s[p]) B_s
 //              the float weights are split fp16 hi + lo, so the state update keeps ~f32
 //              precision (two m16n8k16 MMAs per step) and the int8 state codes written at
 //              the end stay within one step of the sequential f32 recurrence.
-// cs = cumulative Δ·A inside the chunk (f32).  Legacy warp-level mma.sync; the operands are
-// staged in padded (bank-conflict-free) shared memory and converted to fp16 on the fly.
+// cs = cumulative Δ·A inside the chunk (f32).
+//
+// Data movement: the next chunk's int8 codes are fetched with cp.async into a second raw
+// buffer while the current chunk computes; the current chunk's x / B / C codes are widened
+// once to fp16 tiles (exact, byte-permute + one HSUB2 per pair) and every fp16 fragment is
+// read with ldmatrix (.trans where the reduction runs over tokens).  All padded strides are
+// bank-conflict-free for the 8-row ldmatrix phases.  Legacy warp-level mma.sync.
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -26,47 +34,78 @@ constexpr int SC_Q = 64;       // chunk length
 constexpr int SC_P = 64;       // head_dim
 constexpr int SC_THREADS = 128;
 
-__device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+__device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ void mma_i8(int (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+__device__ __forceinline__ void mma_i8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
       : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t h2(float lo, float hi) {   // pack two f32 as fp16x2 (lo in low half)
   const __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
 }
-__device__ __forceinline__ uint32_t s8pair_h2(const int8_t* p) {   // two consecutive int8 -> fp16x2 (exact)
-  return h2((float)p[0], (float)p[1]);
+__device__ __forceinline__ float2 f2(uint32_t v) { return __half22float2(*reinterpret_cast<const __half2*>(&v)); }
+// four int8 codes -> two fp16x2 (exact): bytes biased to unsigned, placed under the fp16
+// exponent of 1024 (0x64xx = 1024 + byte), then 1152 = 1024 + 128 subtracted.
+__device__ __forceinline__ void s8x4_h2x2(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  const uint32_t u = w ^ 0x80808080u;
+  uint32_t a = __byte_perm(u, 0x64646464u, 0x4140), b = __byte_perm(u, 0x64646464u, 0x4342);
+  const __half2 bias = __halves2half2(__ushort_as_half(0x6480), __ushort_as_half(0x6480));
+  const __half2 ha = __hsub2(*reinterpret_cast<__half2*>(&a), bias);
+  const __half2 hb = __hsub2(*reinterpret_cast<__half2*>(&b), bias);
+  lo = *reinterpret_cast<const uint32_t*>(&ha);
+  hi = *reinterpret_cast<const uint32_t*>(&hb);
 }
 
 template <int N>
 struct ScSmem {
-  static constexpr int CP = N + 16;       // padded row bytes of C / B codes [t][n]
-  static constexpr int TP = SC_Q + 8;     // padded row bytes of transposed codes [*][s]
-  int8_t Cs[SC_Q][CP];                    // C codes [t][n]
-  int8_t Bs[SC_Q][CP];                    // B codes [s][n]
-  int8_t BT[N][TP];                       // B codes [n][s]
-  int8_t XT[SC_P][TP];                    // x codes [p][s]
-  int8_t Zs[SC_Q][SC_P + 16];             // z codes [t][p]
-  __half Hs[SC_P][N + 8];                 // H (fp16 copy) [p][n]
-  float cs[SC_Q], dlt[SC_Q], wgt[SC_Q];
-  float sxs[SC_P];                        // clustered x scales of the head's channels
-  float gz[SC_Q][SC_P + 1];               // SiLU(ẑ) [t][p]
+  static constexpr int RP = N + 16;       // raw int8 row bytes of B / C codes (conflict-free m16n8k32 loads)
+  static constexpr int HP = N + 8;        // fp16 row elements of B / C tiles (conflict-free ldmatrix)
+  static constexpr int XP = SC_P + 8;     // fp16 row elements of X / W tiles
+  struct Raw {
+    int8_t B[SC_Q][RP];                   // B codes [s][n]
+    int8_t C[SC_Q][RP];                   // C codes [t][n]
+    int8_t X[SC_Q][SC_P];                 // x codes [s][p]
+    int8_t Z[SC_Q][SC_P + 16];            // z codes [t][p]
+  };
+  Raw raw[2];                             // cp.async double buffer (chunk c and c+1)
+  __half Xh[SC_Q][XP];                    // x codes [s][p] as fp16
+  __half Bh[SC_Q][HP];                    // B codes [s][n] as fp16
+  __half Ch[SC_Q][HP];                    // C codes [t][n] as fp16
+  __half Wh[SC_Q][XP];                    // W [t][s] fp16
+  float cs[SC_Q], dlt[SC_Q], wgt[SC_Q], et[SC_Q];
+  float lut[256];                         // SiLU(z_code s_z), indexed by code + 128
 };
 
 template <int N>
-__global__ void __launch_bounds__(SC_THREADS) ssd_chunk_kernel(sq_mamba2_params p, int T, const int8_t* x, int64_t ldx,
-                                                              const int8_t* Bm, const int8_t* Cm, int64_t ldbc,
-                                                              const int8_t* dt, int64_t lddt, const int8_t* z,
-                                                              int64_t ldz, int8_t* __restrict__ state, int state_in,
-                                                              float* __restrict__ y, int64_t ldy) {
+__global__ void __launch_bounds__(SC_THREADS, 2)
+    ssd_chunk_kernel(sq_mamba2_params p, int T, const int8_t* x, int64_t ldx, const int8_t* Bm, const int8_t* Cm,
+                     int64_t ldbc, const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
+                     int8_t* __restrict__ state, int state_in, float* __restrict__ y, int64_t ldy) {
   using S = ScSmem<N>;
   constexpr int NT = N / 8;               // n-tiles of the state (8 columns each)
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -79,6 +118,28 @@ __global__ void __launch_bounds__(SC_THREADS) ssd_chunk_kernel(sq_mamba2_params 
   const float sB = p.s_B[grp], sC = p.s_C[grp];
   const float sBC = __fmul_rn(sB, sC);
   const int ch0 = h * SC_P;
+  const int64_t tok0 = (int64_t)b * T;
+
+  // async fetch of one chunk's codes into raw buffer `buf` (rows past T zero-filled)
+  auto fetch = [&](int c0, int buf) {
+    typename S::Raw& R = sm.raw[buf];
+    const int Qc = min(SC_Q, T - c0);
+    for (int i = tid; i < SC_Q * (N / 16); i += SC_THREADS) {
+      const int r = i / (N / 16), c16 = (i % (N / 16)) * 16;
+      const int64_t tok = tok0 + c0 + min(r, Qc - 1);
+      cp_async16(&R.B[r][c16], Bm + tok * ldbc + grp * N + c16, r < Qc);
+      cp_async16(&R.C[r][c16], Cm + tok * ldbc + grp * N + c16, r < Qc);
+    }
+    for (int i = tid; i < SC_Q * (SC_P / 16); i += SC_THREADS) {
+      const int r = i / (SC_P / 16), c16 = (i % (SC_P / 16)) * 16;
+      const int64_t tok = tok0 + c0 + min(r, Qc - 1);
+      cp_async16(&R.X[r][c16], x + tok * ldx + ch0 + c16, r < Qc);
+      cp_async16(&R.Z[r][c16], z + tok * ldz + ch0 + c16, r < Qc);
+    }
+    cp_async_commit();
+  };
+  fetch(0, 0);
+
   // this warp's 16 state rows p = 16*warp + {g4, g4+8}; H fragments over all N columns
   const int pr0 = 16 * warp + g4, pr1 = pr0 + 8;
   const float sx0 = p.s_x[ch0 + pr0], sx1 = p.s_x[ch0 + pr1];
@@ -97,52 +158,55 @@ __global__ void __launch_bounds__(SC_THREADS) ssd_chunk_kernel(sq_mamba2_params 
       H[j][0] = H[j][1] = H[j][2] = H[j][3] = 0.f;
     }
   }
-  // per-thread y rows t = 16*warp + {g4, g4+8}; columns p = 8*j + 2*t4 (+1)
-  const int tr0 = 16 * warp + g4, tr1 = tr0 + 8;
-  if (tid < SC_P) sm.sxs[tid] = p.s_x[ch0 + tid];
+  for (int i = tid; i < 256; i += SC_THREADS) sm.lut[i] = silu_fast(__fmul_rn((float)(i - 128), p.s_z));
+  const float f0 = __fmul_rn(sx0, sB), f1 = __fmul_rn(sx1, sB);
+  // per-token Δ code of this thread's token (tid < 64), prefetched one chunk ahead
+  int8_t dcode = (tid < SC_Q && tid < T) ? dt[(tok0 + tid) * lddt + h] : 0;
 
-  for (int c0 = 0; c0 < T; c0 += SC_Q) {
+  int buf = 0;
+  for (int c0 = 0; c0 < T; c0 += SC_Q, buf ^= 1) {
     const int Qc = min(SC_Q, T - c0);
-    // ---------------- stage the chunk's codes
-    __syncthreads();   // previous chunk done with smem
-    for (int i = tid; i < SC_Q * (N / 16); i += SC_THREADS) {
-      const int r = i / (N / 16), c16 = (i % (N / 16)) * 16;
-      int4 bv = make_int4(0, 0, 0, 0), cv = make_int4(0, 0, 0, 0);
-      if (r < Qc) {
-        const int64_t tok = (int64_t)b * T + c0 + r;
-        bv = *reinterpret_cast<const int4*>(Bm + tok * ldbc + grp * N + c16);
-        cv = *reinterpret_cast<const int4*>(Cm + tok * ldbc + grp * N + c16);
-      }
-      *reinterpret_cast<int4*>(&sm.Bs[r][c16]) = bv;
-      *reinterpret_cast<int4*>(&sm.Cs[r][c16]) = cv;
-      const int8_t* bb = reinterpret_cast<const int8_t*>(&bv);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) sm.BT[c16 + e][r] = bb[e];
-    }
-    for (int i = tid; i < SC_Q * (SC_P / 16); i += SC_THREADS) {
-      const int r = i / (SC_P / 16), c16 = (i % (SC_P / 16)) * 16;
-      int4 xv = make_int4(0, 0, 0, 0), zv = make_int4(0, 0, 0, 0);
-      if (r < Qc) {
-        const int64_t tok = (int64_t)b * T + c0 + r;
-        xv = *reinterpret_cast<const int4*>(x + tok * ldx + ch0 + c16);
-        zv = *reinterpret_cast<const int4*>(z + tok * ldz + ch0 + c16);
-      }
-      *reinterpret_cast<int4*>(&sm.Zs[r][c16]) = zv;
-      const int8_t* xb = reinterpret_cast<const int8_t*>(&xv);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) sm.XT[c16 + e][r] = xb[e];
-    }
+    cp_async_wait_all();
+    __syncthreads();   // raw[buf] landed for every thread; previous chunk fully consumed
+    if (c0 + SC_Q < T) fetch(c0 + SC_Q, buf ^ 1);
+    const typename S::Raw& R = sm.raw[buf];
     if (tid < SC_Q) {
       float dA_log = 0.f, dl = 0.f;
       if (tid < Qc) {
-        const float draw = __fadd_rn(__fmul_rn((float)dt[((int64_t)b * T + c0 + tid) * lddt + h], p.s_dt), dtb);
+        const float draw = __fadd_rn(__fmul_rn((float)dcode, p.s_dt), dtb);
         dl = softplus_f(draw);
         dA_log = __fmul_rn(dl, A);
       }
       sm.dlt[tid] = dl;
       sm.cs[tid] = dA_log;
+      const int tn = c0 + SC_Q + tid;
+      dcode = tn < T ? dt[(tok0 + tn) * lddt + h] : 0;
     }
-    __syncthreads();
+    // widen this chunk's x / B / C codes to fp16 tiles
+    for (int i = tid; i < SC_Q * (N / 16); i += SC_THREADS) {
+      const int r = i / (N / 16), c16 = (i % (N / 16)) * 16;
+      const uint4 bv = *reinterpret_cast<const uint4*>(&R.B[r][c16]);
+      const uint4 cv = *reinterpret_cast<const uint4*>(&R.C[r][c16]);
+      uint4 o0, o1;
+      s8x4_h2x2(bv.x, o0.x, o0.y); s8x4_h2x2(bv.y, o0.z, o0.w);
+      s8x4_h2x2(bv.z, o1.x, o1.y); s8x4_h2x2(bv.w, o1.z, o1.w);
+      *reinterpret_cast<uint4*>(&sm.Bh[r][c16]) = o0;
+      *reinterpret_cast<uint4*>(&sm.Bh[r][c16 + 8]) = o1;
+      s8x4_h2x2(cv.x, o0.x, o0.y); s8x4_h2x2(cv.y, o0.z, o0.w);
+      s8x4_h2x2(cv.z, o1.x, o1.y); s8x4_h2x2(cv.w, o1.z, o1.w);
+      *reinterpret_cast<uint4*>(&sm.Ch[r][c16]) = o0;
+      *reinterpret_cast<uint4*>(&sm.Ch[r][c16 + 8]) = o1;
+    }
+    for (int i = tid; i < SC_Q * (SC_P / 16); i += SC_THREADS) {
+      const int r = i / (SC_P / 16), c16 = (i % (SC_P / 16)) * 16;
+      const uint4 xv = *reinterpret_cast<const uint4*>(&R.X[r][c16]);
+      uint4 o0, o1;
+      s8x4_h2x2(xv.x, o0.x, o0.y); s8x4_h2x2(xv.y, o0.z, o0.w);
+      s8x4_h2x2(xv.z, o1.x, o1.y); s8x4_h2x2(xv.w, o1.z, o1.w);
+      *reinterpret_cast<uint4*>(&sm.Xh[r][c16]) = o0;
+      *reinterpret_cast<uint4*>(&sm.Xh[r][c16 + 8]) = o1;
+    }
+    __syncthreads();   // dlt / cs / fp16 tiles visible
     if (warp == 0) {   // inclusive prefix sum of Δ·A over the chunk (sequential order, f32)
       float v0 = sm.cs[lane], v1 = sm.cs[lane + 32];
 #pragma unroll
@@ -156,111 +220,111 @@ __global__ void __launch_bounds__(SC_THREADS) ssd_chunk_kernel(sq_mamba2_params 
       v1 += __shfl_sync(0xffffffffu, v0, 31);
       sm.cs[lane] = v0;
       sm.cs[lane + 32] = v1;
-      // state-update weights e^{cs_Q - cs_s} Δ_s (padded tokens have Δ = 0)
+      // state-update weights e^{cs_Q - cs_s} Δ_s (padded tokens have Δ = 0); Y_off column
+      // scales e^{cs_t} s_C
       const float csQ = __shfl_sync(0xffffffffu, v1, 31);
       sm.wgt[lane] = __fmul_rn(expf(__fsub_rn(csQ, v0)), sm.dlt[lane]);
       sm.wgt[lane + 32] = __fmul_rn(expf(__fsub_rn(csQ, v1)), sm.dlt[lane + 32]);
+      sm.et[lane] = __fmul_rn(__expf(v0), sC);
+      sm.et[lane + 32] = __fmul_rn(__expf(v1), sC);
     }
-    // SiLU(ẑ) table and H (fp16) for Y_off, written from the register-resident state
-    for (int i = tid; i < SC_Q * SC_P; i += SC_THREADS) {
-      const int t = i / SC_P, pp = i % SC_P;
-      sm.gz[t][pp] = silu_fast(__fmul_rn((float)sm.Zs[t][pp], p.s_z));
-    }
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int n = 8 * j + 2 * t4;
-      *reinterpret_cast<__half2*>(&sm.Hs[pr0][n]) = __floats2half2_rn(H[j][0], H[j][1]);
-      *reinterpret_cast<__half2*>(&sm.Hs[pr1][n]) = __floats2half2_rn(H[j][2], H[j][3]);
-    }
-    __syncthreads();
-    const float csQ = sm.cs[SC_Q - 1];   // padded tokens carry Δ = 0
-
-    // ---------------- CB = C · Bᵀ (int8, exact), rows t of this warp, all s
+    // ---------------- CB = C · Bᵀ (int8, exact), rows t = 16*warp + {g4, g4+8}, all s
+    const int tr0 = 16 * warp + g4, tr1 = tr0 + 8;
     int cb[SC_Q / 8][4];
 #pragma unroll
     for (int j = 0; j < SC_Q / 8; ++j) cb[j][0] = cb[j][1] = cb[j][2] = cb[j][3] = 0;
 #pragma unroll
     for (int kk = 0; kk < N / 32; ++kk) {
       uint32_t a[4];
-      a[0] = *reinterpret_cast<const uint32_t*>(&sm.Cs[tr0][32 * kk + 4 * t4]);
-      a[1] = *reinterpret_cast<const uint32_t*>(&sm.Cs[tr1][32 * kk + 4 * t4]);
-      a[2] = *reinterpret_cast<const uint32_t*>(&sm.Cs[tr0][32 * kk + 16 + 4 * t4]);
-      a[3] = *reinterpret_cast<const uint32_t*>(&sm.Cs[tr1][32 * kk + 16 + 4 * t4]);
+      a[0] = *reinterpret_cast<const uint32_t*>(&R.C[tr0][32 * kk + 4 * t4]);
+      a[1] = *reinterpret_cast<const uint32_t*>(&R.C[tr1][32 * kk + 4 * t4]);
+      a[2] = *reinterpret_cast<const uint32_t*>(&R.C[tr0][32 * kk + 16 + 4 * t4]);
+      a[3] = *reinterpret_cast<const uint32_t*>(&R.C[tr1][32 * kk + 16 + 4 * t4]);
+#pragma unroll
+      for (int j = 0; j < SC_Q / 8; ++j)
+        mma_i8(cb[j], a, *reinterpret_cast<const uint32_t*>(&R.B[8 * j + g4][32 * kk + 4 * t4]),
+               *reinterpret_cast<const uint32_t*>(&R.B[8 * j + g4][32 * kk + 16 + 4 * t4]));
+    }
+    __syncthreads();   // cs / wgt / et visible
+    // ---------------- W = CB s_B s_C e^{cs_t - cs_s} Δ_s (causal) -> fp16 tile [t][s]
+    {
+      const float cst0 = sm.cs[tr0], cst1 = sm.cs[tr1];
 #pragma unroll
       for (int j = 0; j < SC_Q / 8; ++j) {
-        uint32_t bf[2];
-        bf[0] = *reinterpret_cast<const uint32_t*>(&sm.Bs[8 * j + g4][32 * kk + 4 * t4]);
-        bf[1] = *reinterpret_cast<const uint32_t*>(&sm.Bs[8 * j + g4][32 * kk + 16 + 4 * t4]);
-        mma_i8(cb[j], a, bf);
+        const int s0 = 8 * j + 2 * t4, s1 = s0 + 1;
+        const float css0 = sm.cs[s0], css1 = sm.cs[s1], d0 = sm.dlt[s0], d1 = sm.dlt[s1];
+        const float w00 = s0 <= tr0 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][0], sBC), __expf(cst0 - css0)), d0) : 0.f;
+        const float w01 = s1 <= tr0 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][1], sBC), __expf(cst0 - css1)), d1) : 0.f;
+        const float w10 = s0 <= tr1 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][2], sBC), __expf(cst1 - css0)), d0) : 0.f;
+        const float w11 = s1 <= tr1 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][3], sBC), __expf(cst1 - css1)), d1) : 0.f;
+        *reinterpret_cast<uint32_t*>(&sm.Wh[tr0][s0]) = h2(w00, w01);
+        *reinterpret_cast<uint32_t*>(&sm.Wh[tr1][s0]) = h2(w10, w11);
       }
     }
-    // ---------------- W = CB s_B s_C e^{cs_t - cs_s} Δ_s (causal) -> fp16 A fragments
-    const float cst0 = sm.cs[tr0], cst1 = sm.cs[tr1];
-    uint32_t wa[SC_Q / 16][4];
+    // X̂ᵀ A fragments (rows p of this warp, k = s), reused by Y_diag, the D term and the H update
+    uint32_t xa[SC_Q / 16][4];
+    {
+      const int mi = lane >> 3, r = lane & 7;
+#pragma unroll
+      for (int kk = 0; kk < SC_Q / 16; ++kk)
+        ldsm_x4_t(xa[kk], &sm.Xh[16 * kk + (mi >> 1) * 8 + r][16 * warp + (mi & 1) * 8]);
+    }
+    __syncthreads();   // W visible
+    // ---------------- Yᵀ = X̂ᵀ Wᵀ  and  H Ĉᵀ   (f32 accumulators, rows p, cols t)
+    float yd[SC_Q / 8][4], yo[SC_Q / 8][4];
 #pragma unroll
     for (int j = 0; j < SC_Q / 8; ++j) {
-      const int s0 = 8 * j + 2 * t4, s1 = s0 + 1;
-      const float css0 = sm.cs[s0], css1 = sm.cs[s1], d0 = sm.dlt[s0], d1 = sm.dlt[s1];
-      const float w00 = s0 <= tr0 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][0], sBC), expf(cst0 - css0)), d0) : 0.f;
-      const float w01 = s1 <= tr0 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][1], sBC), expf(cst0 - css1)), d1) : 0.f;
-      const float w10 = s0 <= tr1 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][2], sBC), expf(cst1 - css0)), d0) : 0.f;
-      const float w11 = s1 <= tr1 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][3], sBC), expf(cst1 - css1)), d1) : 0.f;
-      // C-fragment of n-tile j -> A-fragment of k-step j/2 (cols 16kk + {2t4, 2t4+8})
-      wa[j >> 1][(j & 1) * 2 + 0] = h2(w00, w01);
-      wa[j >> 1][(j & 1) * 2 + 1] = h2(w10, w11);
-    }
-    // ---------------- Y = W · X  +  C · Hᵀ  (f32 accumulators, rows t, cols p)
-    float yd[SC_P / 8][4], yo[SC_P / 8][4];
-#pragma unroll
-    for (int j = 0; j < SC_P / 8; ++j) {
       yd[j][0] = yd[j][1] = yd[j][2] = yd[j][3] = 0.f;
       yo[j][0] = yo[j][1] = yo[j][2] = yo[j][3] = 0.f;
     }
-#pragma unroll
-    for (int kk = 0; kk < SC_Q / 16; ++kk) {
-#pragma unroll
-      for (int j = 0; j < SC_P / 8; ++j) {
-        uint32_t bf[2];
-        bf[0] = s8pair_h2(&sm.XT[8 * j + g4][16 * kk + 2 * t4]);
-        bf[1] = s8pair_h2(&sm.XT[8 * j + g4][16 * kk + 8 + 2 * t4]);
-        mma_f16(yd[j], wa[kk], bf);
-      }
-    }
-#pragma unroll
-    for (int kk = 0; kk < N / 16; ++kk) {
-      uint32_t a[4];
-      a[0] = s8pair_h2(&sm.Cs[tr0][16 * kk + 2 * t4]);
-      a[1] = s8pair_h2(&sm.Cs[tr1][16 * kk + 2 * t4]);
-      a[2] = s8pair_h2(&sm.Cs[tr0][16 * kk + 8 + 2 * t4]);
-      a[3] = s8pair_h2(&sm.Cs[tr1][16 * kk + 8 + 2 * t4]);
-#pragma unroll
-      for (int j = 0; j < SC_P / 8; ++j) {
-        uint32_t bf[2];
-        bf[0] = *reinterpret_cast<const uint32_t*>(&sm.Hs[8 * j + g4][16 * kk + 2 * t4]);
-        bf[1] = *reinterpret_cast<const uint32_t*>(&sm.Hs[8 * j + g4][16 * kk + 8 + 2 * t4]);
-        mma_f16(yo[j], a, bf);
-      }
-    }
     {
-      const float e0 = __fmul_rn(expf(cst0), sC), e1 = __fmul_rn(expf(cst1), sC);
+      const int mi = lane >> 3, r = lane & 7;
 #pragma unroll
-      for (int j = 0; j < SC_P / 8; ++j) {
+      for (int kk = 0; kk < SC_Q / 16; ++kk) {
+#pragma unroll
+        for (int j = 0; j < SC_Q / 8; j += 2) {
+          uint32_t bw[4];   // b0,b1 of t-tile j, then of t-tile j+1
+          ldsm_x4(bw, &sm.Wh[8 * (j + (mi >> 1)) + r][16 * kk + (mi & 1) * 8]);
+          mma_f16(yd[j], xa[kk], bw[0], bw[1]);
+          mma_f16(yd[j + 1], xa[kk], bw[2], bw[3]);
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < N / 16; ++kk) {
+        const uint32_t ha[4] = {h2(H[2 * kk][0], H[2 * kk][1]), h2(H[2 * kk][2], H[2 * kk][3]),
+                                h2(H[2 * kk + 1][0], H[2 * kk + 1][1]), h2(H[2 * kk + 1][2], H[2 * kk + 1][3])};
+#pragma unroll
+        for (int j = 0; j < SC_Q / 8; j += 2) {
+          uint32_t bc[4];
+          ldsm_x4(bc, &sm.Ch[8 * (j + (mi >> 1)) + r][16 * kk + (mi & 1) * 8]);
+          mma_f16(yo[j], ha, bc[0], bc[1]);
+          mma_f16(yo[j + 1], ha, bc[2], bc[3]);
+        }
+      }
+    }
+    // ---------------- epilogue: y[t][p] for p in {pr0, pr1}, t = 8j + 2t4 (+1)
+    {
+#pragma unroll
+      for (int j = 0; j < SC_Q / 8; ++j) {
+        // x codes at (p, t) from the X̂ᵀ fragments: t-tile j = k-step j/2, half j&1
+        const float2 xc0 = f2(xa[j >> 1][(j & 1) * 2]), xc1 = f2(xa[j >> 1][(j & 1) * 2 + 1]);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int t = q < 2 ? tr0 : tr1;
-          const int pp = 8 * j + 2 * t4 + (q & 1);
+          const int t = 8 * j + 2 * t4 + (q & 1);
+          const int pp = q < 2 ? pr0 : pr1;
           if (t < Qc) {
-            const float sxp = sm.sxs[pp];
-            const float xh = __fmul_rn((float)sm.XT[pp][t], sxp);
-            const float yv = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][q], sxp), __fmul_rn(yo[j][q], q < 2 ? e0 : e1)),
+            const float sxp = q < 2 ? sx0 : sx1;
+            const float xcode = q == 0 ? xc0.x : q == 1 ? xc0.y : q == 2 ? xc1.x : xc1.y;
+            const float xh = __fmul_rn(xcode, sxp);
+            const float yv = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][q], sxp), __fmul_rn(yo[j][q], sm.et[t])),
                                        __fmul_rn(Dh, xh));
-            y[((int64_t)b * T + c0 + t) * ldy + ch0 + pp] = __fmul_rn(yv, sm.gz[t][pp]);
+            y[(tok0 + c0 + t) * ldy + ch0 + pp] = __fmul_rn(yv, sm.lut[(int)R.Z[t][pp] + 128]);
           }
         }
       }
     }
     // ---------------- H = e^{cs_Q} H + Σ_s w_s s_x s_B x_s ⊗ B_s   (fp16 hi + lo split of the weights)
-    const float eQ = expf(csQ);
+    const float eQ = expf(sm.cs[SC_Q - 1]);   // padded tokens carry Δ = 0
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       H[j][0] = __fmul_rn(H[j][0], eQ);
@@ -268,36 +332,37 @@ __global__ void __launch_bounds__(SC_THREADS) ssd_chunk_kernel(sq_mamba2_params 
       H[j][2] = __fmul_rn(H[j][2], eQ);
       H[j][3] = __fmul_rn(H[j][3], eQ);
     }
-    const float f0 = __fmul_rn(sx0, sB), f1 = __fmul_rn(sx1, sB);
+    {
+      const int mi = lane >> 3, r = lane & 7;
 #pragma unroll
-    for (int kk = 0; kk < SC_Q / 16; ++kk) {
-      uint32_t ahi[4], alo[4];
+      for (int kk = 0; kk < SC_Q / 16; ++kk) {
+        uint32_t ahi[4], alo[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int pp = (q & 1) ? pr1 : pr0;
-        const int s = 16 * kk + ((q & 2) ? 8 : 0) + 2 * t4;
-        const float fr = (q & 1) ? f1 : f0;
-        const float v0 = __fmul_rn(__fmul_rn(sm.wgt[s], (float)sm.XT[pp][s]), fr);
-        const float v1 = __fmul_rn(__fmul_rn(sm.wgt[s + 1], (float)sm.XT[pp][s + 1]), fr);
-        const __half2 hi = __floats2half2_rn(v0, v1);
-        const float2 hf = __half22float2(hi);
-        const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
-        ahi[q] = *reinterpret_cast<const uint32_t*>(&hi);
-        alo[q] = *reinterpret_cast<const uint32_t*>(&lo);
-      }
-      // fragment order: a0 (row g, k 2t), a1 (row g+8, k 2t), a2 (row g, k 2t+8), a3 (row g+8, k 2t+8)
-      const uint32_t A_hi[4] = {ahi[0], ahi[1], ahi[2], ahi[3]};
-      const uint32_t A_lo[4] = {alo[0], alo[1], alo[2], alo[3]};
+        for (int q = 0; q < 4; ++q) {   // a0 (row g, k 2t), a1 (row g+8, k 2t), a2 (row g, k 2t+8), a3 (row g+8, k 2t+8)
+          const int s = 16 * kk + ((q & 2) ? 8 : 0) + 2 * t4;
+          const float fr = (q & 1) ? f1 : f0;
+          const float2 xc = f2(xa[kk][q]);
+          const float v0 = __fmul_rn(__fmul_rn(sm.wgt[s], xc.x), fr);
+          const float v1 = __fmul_rn(__fmul_rn(sm.wgt[s + 1], xc.y), fr);
+          const __half2 hi = __floats2half2_rn(v0, v1);
+          const float2 hf = __half22float2(hi);
+          const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+          ahi[q] = *reinterpret_cast<const uint32_t*>(&hi);
+          alo[q] = *reinterpret_cast<const uint32_t*>(&lo);
+        }
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        uint32_t bf[2];
-        bf[0] = s8pair_h2(&sm.BT[8 * j + g4][16 * kk + 2 * t4]);
-        bf[1] = s8pair_h2(&sm.BT[8 * j + g4][16 * kk + 8 + 2 * t4]);
-        mma_f16(H[j], A_hi, bf);
-        mma_f16(H[j], A_lo, bf);
+        for (int j = 0; j < NT; j += 2) {
+          uint32_t bb[4];   // b0,b1 of n-tile j, then of n-tile j+1 (stored [s][n] -> .trans)
+          ldsm_x4_t(bb, &sm.Bh[16 * kk + (mi & 1) * 8 + r][8 * (j + (mi >> 1))]);
+          mma_f16(H[j], ahi, bb[0], bb[1]);
+          mma_f16(H[j], alo, bb[0], bb[1]);
+          mma_f16(H[j + 1], ahi, bb[2], bb[3]);
+          mma_f16(H[j + 1], alo, bb[2], bb[3]);
+        }
       }
     }
   }
+  cp_async_wait_all();
   // ---------------- final state -> int8 codes (ClusterMap-cell scales)
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
@@ -309,6 +374,21 @@ __global__ void __launch_bounds__(SC_THREADS) ssd_chunk_kernel(sq_mamba2_params 
   }
 }
 
+template <int N>
+static int launch_n(const sq_mamba2_params* p, int B, int T, const int8_t* x, int64_t ldx, const int8_t* Bm,
+                    const int8_t* Cm, int64_t ldbc, const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
+                    int8_t* state, int state_in, float* y, int64_t ldy, cudaStream_t st) {
+  const int smem = sizeof(ScSmem<N>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ssd_chunk_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  ssd_chunk_kernel<N><<<dim3(p->n_heads, B), SC_THREADS, smem, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz,
+                                                                    state, state_in, y, ldy);
+  return SQ_OK;
+}
+
 int launch_ssd_chunk(const sq_mamba2_params* p, int B, int T, const int8_t* x, int64_t ldx, const int8_t* Bm,
                      const int8_t* Cm, int64_t ldbc, const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
                      int8_t* state, int state_in, float* y, int64_t ldy, cudaStream_t st) {
@@ -317,26 +397,10 @@ int launch_ssd_chunk(const sq_mamba2_params* p, int B, int T, const int8_t* x, i
       (reinterpret_cast<uintptr_t>(Bm) & 15) || (reinterpret_cast<uintptr_t>(Cm) & 15) ||
       (reinterpret_cast<uintptr_t>(z) & 15))
     return SQ_ERR_ARG;
-  dim3 grid(p->n_heads, B);
-  if (p->d_state == 128) {
-    const int smem = sizeof(ScSmem<128>);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(ssd_chunk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
-    ssd_chunk_kernel<128><<<grid, SC_THREADS, smem, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state,
-                                                          state_in, y, ldy);
-  } else {
-    const int smem = sizeof(ScSmem<64>);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(ssd_chunk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
-    ssd_chunk_kernel<64><<<grid, SC_THREADS, smem, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state,
-                                                         state_in, y, ldy);
-  }
+  if (p->d_state == 128)
+    launch_n<128>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy, st);
+  else
+    launch_n<64>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy, st);
   return check_launch("sq_ssd_scan_int8 (chunked)");
 }
 
