@@ -38,6 +38,10 @@ __device__ __forceinline__ float silu_fast(float v) {
   return __fmul_rn(v, __frcp_rn(__fadd_rn(1.0f, expf(-v))));
 }
 
+// SiLU with the hardware exp2 / reciprocal approximations (a few ulp from silu_f); for
+// values that are requantized right away, where it moves a code only at a rounding tie.
+__device__ __forceinline__ float silu_approx(float v) { return __fdividef(v, 1.0f + __expf(-v)); }
+
 // quant8(v, s) without the IEEE division or FRND on the common path: t = v * (1/s) is
 // clamped to [-129, 128] and rounded half-to-even with the 1.5 * 2^23 magic add; t lies
 // within a few ulp of v/s, so unless t sits within 1e-4 of a rounding tie (|t - v/s| <= 4e-5 for |t| <= 129) (detected, and

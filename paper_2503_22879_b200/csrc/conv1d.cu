@@ -66,9 +66,9 @@ __global__ void conv1d_prefill_kernel(const TIn* __restrict__ x, int64_t ldx, co
 
 // int8 prefill, 4 channels per thread (one 32-bit load/store per token row, a warp moves
 // 128 contiguous bytes), kSeg4 tokens per thread in sub-blocks of 8 rows whose loads are
-// issued before any math.  Same op order as the scalar kernel; SiLU with a rounded
-// reciprocal and the division-free quantizer with its exact tie fallback, as in the decode
-// prep kernel (decode_ssm.cu conv4_step).
+// issued before any math.  Same op order as the scalar kernel; SiLU from the hardware
+// exp2 / reciprocal approximations and the division-free quantizer with its exact tie
+// fallback (codes move only at rounding ties).
 constexpr int kSeg4 = 32;
 template <int KC>
 __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __restrict__ x, int64_t ldx,
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __re
         float acc = bc[e];
 #pragma unroll
         for (int j = 0; j < KC; ++j) acc = __fadd_rn(acc, __fmul_rn(wc[e][j], win[e][KC - KC + j]));
-        sv[e] = silu_fast(acc);
+        sv[e] = silu_approx(acc);
         packed |= (uint32_t)(uint8_t)quant8_fast(sv[e], iso[e], tie) << (8 * e);
       }
       if (tie) {

@@ -220,29 +220,30 @@ __global__ void __launch_bounds__(1024) gate_norm_had_quant16_kernel(const float
       }
     }
   }
+  // cross-thread stages: the lower element gets a + b, the upper b' - a' — one FMA with
+  // sign ±1 (fma(-1, v, o) = RN(o - v), fma(1, v, o) = RN(v + o): the same rounding)
   for (int m = 1; m < 32 && 16 * m < blk; m <<= 1) {
-    const bool upper = (lane & m) != 0;
+    const float sg = (lane & m) ? -1.f : 1.f;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float o = __shfl_xor_sync(0xffffffffu, v[i], m);
-      v[i] = upper ? __fsub_rn(o, v[i]) : __fadd_rn(v[i], o);
-    }
+    for (int i = 0; i < 16; ++i) v[i] = __fmaf_rn(sg, v[i], __shfl_xor_sync(0xffffffffu, v[i], m));
   }
-  if (blk > 512) {
+  // stages h >= 512 pair thread t with thread t ^ (h / 16) through shared memory
+  for (int m = 32; 16 * m < blk; m <<= 1) {
+    __syncthreads();   // previous stage's reads done
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       *reinterpret_cast<float4*>(buf + base + e * 4) = make_float4(v[e * 4], v[e * 4 + 1], v[e * 4 + 2], v[e * 4 + 3]);
     __syncthreads();
-    for (int h = 512; h < blk; h <<= 1) {
-      for (int idx = threadIdx.x; idx < D / 2; idx += blockDim.x) {
-        const int i = (idx / h) * 2 * h + (idx % h);
-        const float a = buf[i], b = buf[i + h];
-        buf[i] = __fadd_rn(a, b);
-        buf[i + h] = __fsub_rn(a, b);
-      }
-      __syncthreads();
+    const float sg = (threadIdx.x & m) ? -1.f : 1.f;
+    const float* o = buf + (int)((threadIdx.x ^ m) * 16);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float4 f = *reinterpret_cast<const float4*>(o + e * 4);
+      v[e * 4] = __fmaf_rn(sg, v[e * 4], f.x);
+      v[e * 4 + 1] = __fmaf_rn(sg, v[e * 4 + 1], f.y);
+      v[e * 4 + 2] = __fmaf_rn(sg, v[e * 4 + 2], f.z);
+      v[e * 4 + 3] = __fmaf_rn(sg, v[e * 4 + 3], f.w);
     }
-    load16(buf + base, v);
   }
   store16_q(out + (int64_t)blockIdx.x * ldo + base, v, s_y);
 }

@@ -35,13 +35,13 @@ constexpr int SC_P = 64;       // head_dim
 constexpr int SC_THREADS = 128;
 
 __device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 __device__ __forceinline__ void mma_i8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
       : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -93,10 +93,15 @@ struct ScSmem {
     int8_t Z[SC_Q][SC_P + 16];            // z codes [t][p]
   };
   Raw raw[2];                             // cp.async double buffer (chunk c and c+1)
-  __half Xh[SC_Q][XP];                    // x codes [s][p] as fp16
   __half Bh[SC_Q][HP];                    // B codes [s][n] as fp16
   __half Ch[SC_Q][HP];                    // C codes [t][n] as fp16
-  __half Wh[SC_Q][XP];                    // W [t][s] fp16
+  union {
+    struct {
+      __half Xh[SC_Q][XP];                // x codes [s][p] as fp16
+      __half Wh[SC_Q][XP];                // W [t][s] fp16
+    };
+    float Ys[SC_Q][SC_P + 4];             // pre-gate outputs [t][p], after the Y MMAs
+  };
   float cs[SC_Q], dlt[SC_Q], wgt[SC_Q], et[SC_Q];
   float lut[256];                         // SiLU(z_code s_z), indexed by code + 128
 };
@@ -161,7 +166,8 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
   for (int i = tid; i < 256; i += SC_THREADS) sm.lut[i] = silu_fast(__fmul_rn((float)(i - 128), p.s_z));
   const float f0 = __fmul_rn(sx0, sB), f1 = __fmul_rn(sx1, sB);
   // per-token Δ code of this thread's token (tid < 64), prefetched one chunk ahead
-  int8_t dcode = (tid < SC_Q && tid < T) ? dt[(tok0 + tid) * lddt + h] : 0;
+  // (addresses clamped instead of predicated: no select waits on the load; rows past Qc get Δ = 0)
+  int8_t dcode = tid < SC_Q ? dt[(tok0 + min(tid, T - 1)) * lddt + h] : 0;
 
   int buf = 0;
   for (int c0 = 0; c0 < T; c0 += SC_Q, buf ^= 1) {
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
       sm.dlt[tid] = dl;
       sm.cs[tid] = dA_log;
       const int tn = c0 + SC_Q + tid;
-      dcode = tn < T ? dt[(tok0 + tn) * lddt + h] : 0;
+      dcode = dt[(tok0 + min(tn, T - 1)) * lddt + h];
     }
     // widen this chunk's x / B / C codes to fp16 tiles
     for (int i = tid; i < SC_Q * (N / 16); i += SC_THREADS) {
@@ -242,8 +248,9 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
       a[3] = *reinterpret_cast<const uint32_t*>(&R.C[tr1][32 * kk + 16 + 4 * t4]);
 #pragma unroll
       for (int j = 0; j < SC_Q / 8; ++j)
-        mma_i8(cb[j], a, *reinterpret_cast<const uint32_t*>(&R.B[8 * j + g4][32 * kk + 4 * t4]),
-               *reinterpret_cast<const uint32_t*>(&R.B[8 * j + g4][32 * kk + 16 + 4 * t4]));
+        if (j <= 2 * warp + 1)   // s-tiles past this warp's last row are causally masked
+          mma_i8(cb[j], a, *reinterpret_cast<const uint32_t*>(&R.B[8 * j + g4][32 * kk + 4 * t4]),
+                 *reinterpret_cast<const uint32_t*>(&R.B[8 * j + g4][32 * kk + 16 + 4 * t4]));
     }
     __syncthreads();   // cs / wgt / et visible
     // ---------------- W = CB s_B s_C e^{cs_t - cs_s} Δ_s (causal) -> fp16 tile [t][s]
@@ -252,13 +259,22 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
 #pragma unroll
       for (int j = 0; j < SC_Q / 8; ++j) {
         const int s0 = 8 * j + 2 * t4, s1 = s0 + 1;
-        const float css0 = sm.cs[s0], css1 = sm.cs[s1], d0 = sm.dlt[s0], d1 = sm.dlt[s1];
-        const float w00 = s0 <= tr0 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][0], sBC), __expf(cst0 - css0)), d0) : 0.f;
-        const float w01 = s1 <= tr0 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][1], sBC), __expf(cst0 - css1)), d1) : 0.f;
-        const float w10 = s0 <= tr1 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][2], sBC), __expf(cst1 - css0)), d0) : 0.f;
-        const float w11 = s1 <= tr1 ? __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][3], sBC), __expf(cst1 - css1)), d1) : 0.f;
-        *reinterpret_cast<uint32_t*>(&sm.Wh[tr0][s0]) = h2(w00, w01);
-        *reinterpret_cast<uint32_t*>(&sm.Wh[tr1][s0]) = h2(w10, w11);
+        uint32_t wv0 = 0, wv1 = 0;
+        if (j <= 2 * warp + 1) {
+          const float css0 = sm.cs[s0], css1 = sm.cs[s1], d0 = sm.dlt[s0], d1 = sm.dlt[s1];
+          float w00 = __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][0], sBC), __expf(cst0 - css0)), d0);
+          float w01 = __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][1], sBC), __expf(cst0 - css1)), d1);
+          float w10 = __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][2], sBC), __expf(cst1 - css0)), d0);
+          float w11 = __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][3], sBC), __expf(cst1 - css1)), d1);
+          w00 = s0 <= tr0 ? w00 : 0.f;
+          w01 = s1 <= tr0 ? w01 : 0.f;
+          w10 = s0 <= tr1 ? w10 : 0.f;
+          w11 = s1 <= tr1 ? w11 : 0.f;
+          wv0 = h2(w00, w01);
+          wv1 = h2(w10, w11);
+        }
+        *reinterpret_cast<uint32_t*>(&sm.Wh[tr0][s0]) = wv0;
+        *reinterpret_cast<uint32_t*>(&sm.Wh[tr1][s0]) = wv1;
       }
     }
     // X̂ᵀ A fragments (rows p of this warp, k = s), reused by Y_diag, the D term and the H update
@@ -283,6 +299,7 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
       for (int kk = 0; kk < SC_Q / 16; ++kk) {
 #pragma unroll
         for (int j = 0; j < SC_Q / 8; j += 2) {
+          if (kk > j / 2) continue;   // W[t][s] = 0 for s > t: t-tiles j, j+1 need s < 8j + 16
           uint32_t bw[4];   // b0,b1 of t-tile j, then of t-tile j+1
           ldsm_x4(bw, &sm.Wh[8 * (j + (mi >> 1)) + r][16 * kk + (mi & 1) * 8]);
           mma_f16(yd[j], xa[kk], bw[0], bw[1]);
@@ -302,24 +319,35 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
         }
       }
     }
-    // ---------------- epilogue: y[t][p] for p in {pr0, pr1}, t = 8j + 2t4 (+1)
+    // ---------------- epilogue: pre-gate y staged as [t][p] in smem (over the X / W tiles),
+    // then SiLU(ẑ) gating and coalesced 16-byte stores
+    __syncthreads();   // every warp done reading Xh / Wh
+#pragma unroll
+    for (int j = 0; j < SC_Q / 8; ++j) {
+      // x codes at (p, t) from the X̂ᵀ fragments: t-tile j = k-step j/2, half j&1
+      const float2 xc0 = f2(xa[j >> 1][(j & 1) * 2]), xc1 = f2(xa[j >> 1][(j & 1) * 2 + 1]);
+      const int t = 8 * j + 2 * t4;
+      const float e0 = sm.et[t], e1 = sm.et[t + 1];
+      sm.Ys[t][pr0] = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][0], sx0), __fmul_rn(yo[j][0], e0)), __fmul_rn(Dh, __fmul_rn(xc0.x, sx0)));
+      sm.Ys[t + 1][pr0] = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][1], sx0), __fmul_rn(yo[j][1], e1)), __fmul_rn(Dh, __fmul_rn(xc0.y, sx0)));
+      sm.Ys[t][pr1] = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][2], sx1), __fmul_rn(yo[j][2], e0)), __fmul_rn(Dh, __fmul_rn(xc1.x, sx1)));
+      sm.Ys[t + 1][pr1] = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][3], sx1), __fmul_rn(yo[j][3], e1)), __fmul_rn(Dh, __fmul_rn(xc1.y, sx1)));
+    }
+    __syncthreads();
     {
+      const int p4 = (tid & 15) * 4;
 #pragma unroll
-      for (int j = 0; j < SC_Q / 8; ++j) {
-        // x codes at (p, t) from the X̂ᵀ fragments: t-tile j = k-step j/2, half j&1
-        const float2 xc0 = f2(xa[j >> 1][(j & 1) * 2]), xc1 = f2(xa[j >> 1][(j & 1) * 2 + 1]);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int t = 8 * j + 2 * t4 + (q & 1);
-          const int pp = q < 2 ? pr0 : pr1;
-          if (t < Qc) {
-            const float sxp = q < 2 ? sx0 : sx1;
-            const float xcode = q == 0 ? xc0.x : q == 1 ? xc0.y : q == 2 ? xc1.x : xc1.y;
-            const float xh = __fmul_rn(xcode, sxp);
-            const float yv = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][q], sxp), __fmul_rn(yo[j][q], sm.et[t])),
-                                       __fmul_rn(Dh, xh));
-            y[(tok0 + c0 + t) * ldy + ch0 + pp] = __fmul_rn(yv, sm.lut[(int)R.Z[t][pp] + 128]);
-          }
+      for (int i = 0; i < SC_Q / 8; ++i) {
+        const int t = (tid >> 4) + 8 * i;
+        if (t < Qc) {
+          const float4 v = *reinterpret_cast<const float4*>(&sm.Ys[t][p4]);
+          const uint32_t zc = *reinterpret_cast<const uint32_t*>(&R.Z[t][p4]);
+          float4 o;
+          o.x = __fmul_rn(v.x, sm.lut[(int)(int8_t)(zc) + 128]);
+          o.y = __fmul_rn(v.y, sm.lut[(int)(int8_t)(zc >> 8) + 128]);
+          o.z = __fmul_rn(v.z, sm.lut[(int)(int8_t)(zc >> 16) + 128]);
+          o.w = __fmul_rn(v.w, sm.lut[(int)(int8_t)(zc >> 24) + 128]);
+          *reinterpret_cast<float4*>(y + (tok0 + c0 + t) * ldy + ch0 + p4) = o;
         }
       }
     }
@@ -350,13 +378,19 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
           ahi[q] = *reinterpret_cast<const uint32_t*>(&hi);
           alo[q] = *reinterpret_cast<const uint32_t*>(&lo);
         }
+        // hi pass over every n-tile, then lo pass: dependent MMAs on one H tile are NT apart
 #pragma unroll
         for (int j = 0; j < NT; j += 2) {
           uint32_t bb[4];   // b0,b1 of n-tile j, then of n-tile j+1 (stored [s][n] -> .trans)
           ldsm_x4_t(bb, &sm.Bh[16 * kk + (mi & 1) * 8 + r][8 * (j + (mi >> 1))]);
           mma_f16(H[j], ahi, bb[0], bb[1]);
-          mma_f16(H[j], alo, bb[0], bb[1]);
           mma_f16(H[j + 1], ahi, bb[2], bb[3]);
+        }
+#pragma unroll
+        for (int j = 0; j < NT; j += 2) {
+          uint32_t bb[4];
+          ldsm_x4_t(bb, &sm.Bh[16 * kk + (mi & 1) * 8 + r][8 * (j + (mi >> 1))]);
+          mma_f16(H[j], alo, bb[0], bb[1]);
           mma_f16(H[j + 1], alo, bb[2], bb[3]);
         }
       }
