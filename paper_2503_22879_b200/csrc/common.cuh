@@ -57,11 +57,14 @@ __device__ __forceinline__ int8_t quant8_inv(float v, float s, float inv_s) {
 // Branch-free first pass of quant8_inv: returns the code from v * (1/s) and flags (tie=true)
 // values within 1e-4 of a rounding tie, which the caller recomputes with quant8 (exact), so
 // the codes stay bit-identical to quant8 while the common path has no division or branch.
+// Clamping t to [-128, 127] before rounding equals rounding then clamping (integer bounds,
+// monotone rint), so no integer clamp is needed; a clamped t is never flagged as a tie, and
+// near ±127.5 / -128.5 both roundings clamp to the same code.
 __device__ __forceinline__ int8_t quant8_fast(float v, float inv_s, bool& tie) {
-  const float t = fminf(fmaxf(__fmul_rn(v, inv_s), -129.f), 128.f);
+  const float t = fminf(fmaxf(__fmul_rn(v, inv_s), -128.f), 127.f);
   const float r = __fadd_rn(t, 12582912.0f);
   tie |= fabsf(__fsub_rn(t, __fsub_rn(r, 12582912.0f))) > 0.4999f;
-  return (int8_t)max(-128, min(127, __float_as_int(r) - 0x4B400000));
+  return (int8_t)(__float_as_int(r) - 0x4B400000);
 }
 
 // LEDGER G14: log1p(exp(x)), identity above 20.

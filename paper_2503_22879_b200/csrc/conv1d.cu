@@ -70,6 +70,33 @@ __global__ void conv1d_prefill_kernel(const TIn* __restrict__ x, int64_t ldx, co
 // exp2 / reciprocal approximations and the division-free quantizer with its exact tie
 // fallback (codes move only at rounding ties).
 constexpr int kSeg4 = 32;
+// 4 int8 codes -> 2 x float2 (exact): each byte, biased to unsigned, becomes the low mantissa
+// byte of 2^23 (PRMT), then 2^23 + 128 is subtracted with one packed add.
+__device__ __forceinline__ void s8x4_f2x2(uint32_t u, float2& a, float2& b) {
+  const uint32_t v = u ^ 0x80808080u;
+  const float2 bias = make_float2(-8388736.0f, -8388736.0f);
+  a = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540)),
+                             __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541))), bias);
+  b = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7542)),
+                             __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7543))), bias);
+}
+__device__ __forceinline__ float ex2_approx(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+// SiLU of a channel pair with packed f32x2 math around the two MUFU ops (silu_approx form)
+__device__ __forceinline__ float2 silu2_approx(float2 v) {
+  const float2 t = __fmul2_rn(v, make_float2(-1.4426950408889634f, -1.4426950408889634f));
+  const float2 d = __fadd2_rn(make_float2(ex2_approx(t.x), ex2_approx(t.y)), make_float2(1.f, 1.f));
+  return __fmul2_rn(v, make_float2(rcp_approx(d.x), rcp_approx(d.y)));
+}
+
 template <int KC>
 __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __restrict__ x, int64_t ldx,
                                                               const float* __restrict__ w,
@@ -83,37 +110,44 @@ __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __re
   if (c0 >= C) return;
   const int t0 = blockIdx.y * kSeg4;
   const int t1 = min(T, t0 + kSeg4);
-  float wc[4][KC], si[4], so[4], iso[4], bc[4];
+  // channel pairs (c0, c0+1) and (c0+2, c0+3) as float2 lanes
+  float2 wc[2][KC], si[2], iso[2], bc[2];
+  float so[4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int pr = 0; pr < 2; ++pr) {
+    const int ca = c0 + 2 * pr, cb = ca + 1;
 #pragma unroll
-    for (int j = 0; j < KC; ++j) wc[e][j] = j < KC ? w[(c0 + e) * KC + j] : 0.f;
-    si[e] = s_in[c0 + e];
-    so[e] = s_out[c0 + e];
-    iso[e] = __frcp_rn(so[e]);
-    bc[e] = bias[c0 + e];
+    for (int j = 0; j < KC; ++j) wc[pr][j] = make_float2(w[ca * KC + j], w[cb * KC + j]);
+    si[pr] = make_float2(s_in[ca], s_in[cb]);
+    so[2 * pr] = s_out[ca];
+    so[2 * pr + 1] = s_out[cb];
+    iso[pr] = make_float2(__frcp_rn(so[2 * pr]), __frcp_rn(so[2 * pr + 1]));
+    bc[pr] = make_float2(bias[ca], bias[cb]);
   }
-  // win[e][j]: dequantised input at token t-KC+1+j; slot KC-1 is the newest.
-  float win[4][KC];
+  // win[pr][j]: dequantised input at token t-KC+1+j; slot KC-1 is the newest.
+  float2 win[2][KC];
 #pragma unroll
-  for (int e = 0; e < 4; ++e)
+  for (int pr = 0; pr < 2; ++pr)
 #pragma unroll
-    for (int j = 0; j < KC; ++j) win[e][j] = 0.f;
+    for (int j = 0; j < KC; ++j) win[pr][j] = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int j = 1; j < KC; ++j) {   // tokens t0-KC+j, j = 1..KC-1 -> slots KC-KC+j-1
+  for (int j = 1; j < KC; ++j) {   // tokens t0-KC+j, j = 1..KC-1
     const int t = t0 - KC + j;
     uint32_t u = 0;
     if (t >= 0)
       u = *reinterpret_cast<const uint32_t*>(x + ((int64_t)b * T + t) * ldx + c0);
     else if (cache_in)
       u = *reinterpret_cast<const uint32_t*>(cache + ((int64_t)b * (KC - 1) + (KC - 1 + t)) * C + c0);
+    float2 q[2];
+    s8x4_f2x2(u, q[0], q[1]);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int pr = 0; pr < 2; ++pr) {
 #pragma unroll
-      for (int k = 0; k < KC - 1; ++k) win[e][k] = win[e][k + 1];
-      win[e][KC - 1] = __fmul_rn((float)(int8_t)(u >> (8 * e)), si[e]);
+      for (int k = 0; k < KC - 1; ++k) win[pr][k] = win[pr][k + 1];
+      win[pr][KC - 1] = __fmul2_rn(q[pr], si[pr]);
     }
   }
+  const float2 RM = make_float2(12582912.0f, 12582912.0f), NRM = make_float2(-12582912.0f, -12582912.0f);
   for (int tb = t0; tb < t1; tb += 8) {
     uint32_t u[8];
 #pragma unroll
@@ -122,24 +156,32 @@ __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __re
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if (tb + i >= t1) break;
+      float2 q[2], sv[2];
+      s8x4_f2x2(u[i], q[0], q[1]);
       uint32_t packed = 0;
       bool tie = false;
-      float sv[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int pr = 0; pr < 2; ++pr) {
 #pragma unroll
-        for (int k = 0; k < KC - 1; ++k) win[e][k] = win[e][k + 1];
-        win[e][KC - 1] = __fmul_rn((float)(int8_t)(u[i] >> (8 * e)), si[e]);
-        float acc = bc[e];
+        for (int k = 0; k < KC - 1; ++k) win[pr][k] = win[pr][k + 1];
+        win[pr][KC - 1] = __fmul2_rn(q[pr], si[pr]);
+        float2 acc = bc[pr];
 #pragma unroll
-        for (int j = 0; j < KC; ++j) acc = __fadd_rn(acc, __fmul_rn(wc[e][j], win[e][KC - KC + j]));
-        sv[e] = silu_approx(acc);
-        packed |= (uint32_t)(uint8_t)quant8_fast(sv[e], iso[e], tie) << (8 * e);
+        for (int j = 0; j < KC; ++j) acc = __fadd2_rn(acc, __fmul2_rn(wc[pr][j], win[pr][j]));
+        sv[pr] = silu2_approx(acc);
+        // quant8_fast on the pair: t = v / s (by reciprocal), magic-number rint, tie flag
+        float2 t = __fmul2_rn(sv[pr], iso[pr]);
+        t.x = fminf(fmaxf(t.x, -128.f), 127.f);   // clamp-then-round == round-then-clamp (quant8_fast)
+        t.y = fminf(fmaxf(t.y, -128.f), 127.f);
+        const float2 r = __fadd2_rn(t, RM);
+        const float2 d = __ffma2_rn(__fadd2_rn(r, NRM), make_float2(-1.f, -1.f), t);   // t - rint(t)
+        tie |= fabsf(d.x) > 0.4999f || fabsf(d.y) > 0.4999f;
+        // code bytes = low bytes of the rint bit patterns (0x4B400000 has a zero low byte)
+        packed |= (__byte_perm(__float_as_uint(r.x), __float_as_uint(r.y), 0x0040) & 0xFFFFu) << (16 * pr);
       }
       if (tie) {
-        packed = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) packed |= (uint32_t)(uint8_t)quant8(sv[e], so[e]) << (8 * e);
+        packed = (uint32_t)(uint8_t)quant8(sv[0].x, so[0]) | ((uint32_t)(uint8_t)quant8(sv[0].y, so[1]) << 8) |
+                 ((uint32_t)(uint8_t)quant8(sv[1].x, so[2]) << 16) | ((uint32_t)(uint8_t)quant8(sv[1].y, so[3]) << 24);
       }
       *reinterpret_cast<uint32_t*>(out + ((int64_t)b * T + tb + i) * ldo + c0) = packed;
     }

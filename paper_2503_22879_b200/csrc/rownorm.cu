@@ -97,18 +97,16 @@ __global__ void __launch_bounds__(NT) gate_norm_had_quant_kernel(const float* __
 }
 
 // ---- register-resident variants: one thread per 16 contiguous elements (D/16 threads) ----
+// Block sum with one barrier: every thread adds the per-warp partials in warp order (a fixed,
+// deterministic order).  Callers alternate `red` between two buffers on consecutive rows.
 __device__ __forceinline__ double block_sum_dyn(double v, double* red) {
   v = warp_sum_d(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
   if (l == 0) red[w] = v;
   __syncthreads();
-  if (w == 0) {
-    double t = l < nw ? red[l] : 0.0;
-    t = warp_sum_d(t);
-    if (l == 0) red[0] = t;
-  }
-  __syncthreads();
-  return red[0];
+  double t = 0.0;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  return t;
 }
 
 __device__ __forceinline__ void load16(const float* p, float (&v)[16]) {
@@ -146,106 +144,145 @@ __device__ __forceinline__ void store16_q(int8_t* p, const float (&v)[16], float
   *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// Row loops: a CTA walks rows blockIdx.x, blockIdx.x + gridDim.x, … and loads the next row
+// into registers before working on the current one, so HBM latency overlaps the reduction
+// and transform; the reduction scratch alternates between two buffers per row.
 template <bool QUANT>
-__global__ void __launch_bounds__(1024) rmsnorm16_kernel(const float* x, int64_t ldx,
+__global__ void __launch_bounds__(512) rmsnorm16_kernel(const float* x, int64_t ldx,
                                                          const float* __restrict__ gamma, float eps, float s, int D,
-                                                         void* __restrict__ out, int64_t ldo,
+                                                         int M, void* __restrict__ out, int64_t ldo,
                                                          int32_t* __restrict__ gsum, int64_t ldg) {
-  __shared__ double red[32];
+  __shared__ double red[2][32];
   const int base = threadIdx.x * 16;
   float v[16], g[16];
   pdl_trigger();
   load16(gamma + base, g);
   pdl_wait();
-  load16(x + (int64_t)blockIdx.x * ldx + base, v);
-  double ss = 0.0;
+  int row = blockIdx.x;
+  load16(x + (int64_t)row * ldx + base, v);
+  for (int it = 0; row < M; row += gridDim.x, ++it) {
+    float vn[16];
+    const int nrow = row + gridDim.x;
+    if (nrow < M) load16(x + (int64_t)nrow * ldx + base, vn);
+    double ss = 0.0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) ss += (double)v[i] * (double)v[i];
-  ss = block_sum_dyn(ss, red);
-  const float r = rms_factor(ss, D, eps);
+    for (int i = 0; i < 16; ++i) ss += (double)v[i] * (double)v[i];
+    ss = block_sum_dyn(ss, red[it & 1]);
+    const float r = rms_factor(ss, D, eps);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
-  if (QUANT) {
-    uint32_t w[4];
-    quant16(v, s, w);
-    *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(out) + (int64_t)blockIdx.x * ldo + base) =
-        make_uint4(w[0], w[1], w[2], w[3]);
-    if (gsum) {   // sums of the codes over each 128-wide block (8 threads)
-      int cs = 0;
+    for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
+    if (QUANT) {
+      uint32_t w[4];
+      quant16(v, s, w);
+      *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(out) + (int64_t)row * ldo + base) =
+          make_uint4(w[0], w[1], w[2], w[3]);
+      if (gsum) {   // sums of the codes over each 128-wide block (8 threads)
+        int cs = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) cs = __dp4a((int)w[e], 0x01010101, cs);
-      cs += __shfl_xor_sync(0xffffffffu, cs, 1);
-      cs += __shfl_xor_sync(0xffffffffu, cs, 2);
-      cs += __shfl_xor_sync(0xffffffffu, cs, 4);
-      if ((threadIdx.x & 7) == 0) gsum[(int64_t)blockIdx.x * ldg + (base >> 7)] = cs;
+        for (int e = 0; e < 4; ++e) cs = __dp4a((int)w[e], 0x01010101, cs);
+        cs += __shfl_xor_sync(0xffffffffu, cs, 1);
+        cs += __shfl_xor_sync(0xffffffffu, cs, 2);
+        cs += __shfl_xor_sync(0xffffffffu, cs, 4);
+        if ((threadIdx.x & 7) == 0) gsum[(int64_t)row * ldg + (base >> 7)] = cs;
+      }
+    } else {
+      float* o = reinterpret_cast<float*>(out) + (int64_t)row * ldo + base;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) *reinterpret_cast<float4*>(o + e * 4) = make_float4(v[e * 4], v[e * 4 + 1], v[e * 4 + 2], v[e * 4 + 3]);
     }
-  } else {
-    float* o = reinterpret_cast<float*>(out) + (int64_t)blockIdx.x * ldo + base;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) *reinterpret_cast<float4*>(o + e * 4) = make_float4(v[e * 4], v[e * 4 + 1], v[e * 4 + 2], v[e * 4 + 3]);
+    for (int i = 0; i < 16; ++i) v[i] = vn[i];
   }
 }
 
 // Gated-norm + blocked Sylvester FWHT + quant with the row in registers: stages h < 16
 // inside a thread, 16 <= h < 512 across lanes (shfl_xor), h >= 512 through smem.
 // Every butterfly is the oracle's f32 a+b / a-b, in the oracle's stage order.
-__global__ void __launch_bounds__(1024) gate_norm_had_quant16_kernel(const float* __restrict__ y, int64_t ldy,
+__global__ void __launch_bounds__(512) gate_norm_had_quant16_kernel(const float* __restrict__ y, int64_t ldy,
                                                                      const float* __restrict__ gamma, float eps,
-                                                                     float s_y, int blk, int D,
+                                                                     float s_y, int blk, int D, int M,
                                                                      int8_t* __restrict__ out, int64_t ldo) {
   extern __shared__ float buf[];
-  __shared__ double red[32];
+  __shared__ double red[2][32];
   const int base = threadIdx.x * 16;
   const int lane = threadIdx.x & 31;
-  float v[16], g[16];
-  load16(y + (int64_t)blockIdx.x * ldy + base, v);
-  load16(gamma + base, g);
-  double ss = 0.0;
+  float v[16];
+  int row = blockIdx.x;
+  load16(y + (int64_t)row * ldy + base, v);
+  int stage = 0;   // partner-stage counter: the exchange buffer alternates halves
+  for (int it = 0; row < M; row += gridDim.x, ++it) {
+    float vn[16];
+    const int nrow = row + gridDim.x;
+    if (nrow < M) load16(y + (int64_t)nrow * ldy + base, vn);
+    double ss = 0.0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) ss += (double)v[i] * (double)v[i];
-  ss = block_sum_dyn(ss, red);
-  const float r = rms_factor(ss, D, eps);
+    for (int i = 0; i < 16; ++i) ss += (double)v[i] * (double)v[i];
+    ss = block_sum_dyn(ss, red[it & 1]);
+    const float r = rms_factor(ss, D, eps);
+    {
+      float g[16];
+      load16(gamma + base, g);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
+      for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
+    }
 #pragma unroll
-  for (int h = 1; h < 16; h <<= 1) {
-    if (h < blk) {
+    for (int h = 1; h < 16; h <<= 1) {
+      if (h < blk) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        if ((i & h) == 0) {
-          const float a = v[i], b = v[i + h];
-          v[i] = __fadd_rn(a, b);
-          v[i + h] = __fsub_rn(a, b);
+        for (int i = 0; i < 16; ++i) {
+          if ((i & h) == 0) {
+            const float a = v[i], b = v[i + h];
+            v[i] = __fadd_rn(a, b);
+            v[i + h] = __fsub_rn(a, b);
+          }
         }
       }
     }
-  }
-  // cross-thread stages: the lower element gets a + b, the upper b' - a' — one FMA with
-  // sign ±1 (fma(-1, v, o) = RN(o - v), fma(1, v, o) = RN(v + o): the same rounding)
-  for (int m = 1; m < 32 && 16 * m < blk; m <<= 1) {
-    const float sg = (lane & m) ? -1.f : 1.f;
+    // cross-thread stages: the lower element gets a + b, the upper b' - a' — one FMA with
+    // sign ±1 (fma(-1, v, o) = RN(o - v), fma(1, v, o) = RN(v + o): the same rounding)
+    for (int m = 1; m < 32 && 16 * m < blk; m <<= 1) {
+      const float sg = (lane & m) ? -1.f : 1.f;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __fmaf_rn(sg, v[i], __shfl_xor_sync(0xffffffffu, v[i], m));
-  }
-  // stages h >= 512 pair thread t with thread t ^ (h / 16) through shared memory
-  for (int m = 32; 16 * m < blk; m <<= 1) {
-    __syncthreads();   // previous stage's reads done
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      *reinterpret_cast<float4*>(buf + base + e * 4) = make_float4(v[e * 4], v[e * 4 + 1], v[e * 4 + 2], v[e * 4 + 3]);
-    __syncthreads();
-    const float sg = (threadIdx.x & m) ? -1.f : 1.f;
-    const float* o = buf + (int)((threadIdx.x ^ m) * 16);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float4 f = *reinterpret_cast<const float4*>(o + e * 4);
-      v[e * 4] = __fmaf_rn(sg, v[e * 4], f.x);
-      v[e * 4 + 1] = __fmaf_rn(sg, v[e * 4 + 1], f.y);
-      v[e * 4 + 2] = __fmaf_rn(sg, v[e * 4 + 2], f.z);
-      v[e * 4 + 3] = __fmaf_rn(sg, v[e * 4 + 3], f.w);
+      for (int i = 0; i < 16; ++i) v[i] = __fmaf_rn(sg, v[i], __shfl_xor_sync(0xffffffffu, v[i], m));
     }
+    // stages h >= 512 pair thread t with thread t ^ (h / 16) through shared memory
+    // (two exchange buffers: a stage's writes go to the half the previous stage did not read,
+    //  whose readers all passed that stage's barrier, so one barrier per stage suffices)
+    for (int m = 32; 16 * m < blk; m <<= 1, ++stage) {
+      float* xb = buf + (stage & 1) * D;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        *reinterpret_cast<float4*>(xb + base + e * 4) = make_float4(v[e * 4], v[e * 4 + 1], v[e * 4 + 2], v[e * 4 + 3]);
+      __syncthreads();
+      const float sg = (threadIdx.x & m) ? -1.f : 1.f;
+      const float* o = xb + (int)((threadIdx.x ^ m) * 16);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 f = *reinterpret_cast<const float4*>(o + e * 4);
+        v[e * 4] = __fmaf_rn(sg, v[e * 4], f.x);
+        v[e * 4 + 1] = __fmaf_rn(sg, v[e * 4 + 1], f.y);
+        v[e * 4 + 2] = __fmaf_rn(sg, v[e * 4 + 2], f.z);
+        v[e * 4 + 3] = __fmaf_rn(sg, v[e * 4 + 3], f.w);
+      }
+    }
+    store16_q(out + (int64_t)row * ldo + base, v, s_y);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = vn[i];
   }
-  store16_q(out + (int64_t)blockIdx.x * ldo + base, v, s_y);
+}
+
+// CTAs for a row loop: every resident slot, but never more CTAs than rows.
+template <typename K>
+static int row_grid(K kern, int threads, size_t smem, int M) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  return max(1, min(M, sms * max(per_sm, 1)));
 }
 
 __global__ void quantize_kernel(const float* x, int64_t ldx, float s, int D, int8_t* __restrict__ out,
@@ -337,9 +374,9 @@ extern "C" int sq_rmsnorm_quant(const float* x, int64_t ldx, const float* gamma,
   SQ_REQUIRE(M >= 0 && D > 0 && s > 0.f, SQ_ERR_SHAPE, "sq_rmsnorm_quant: bad M/D/s");
   SQ_REQUIRE(!gsum || (D % 128 == 0 && ldg >= D / 128), SQ_ERR_SHAPE, "sq_rmsnorm_quant: gsum needs D %% 128 == 0");
   if (M == 0) return SQ_OK;
-  if (D % 512 == 0 && D / 16 <= 1024 && ldx % 4 == 0 && ldo % 16 == 0) {
-    launch_k(PDL_ROW, rmsnorm16_kernel<true>, dim3(M), dim3(D / 16), 0, as_stream(stream), x, ldx, gamma, eps, s, D,
-             (void*)out, ldo, gsum, ldg);
+  if (D % 512 == 0 && D / 16 <= 512 && ldx % 4 == 0 && ldo % 16 == 0) {
+    launch_k(PDL_ROW, rmsnorm16_kernel<true>, dim3(row_grid(rmsnorm16_kernel<true>, D / 16, 0, M)), dim3(D / 16), 0,
+             as_stream(stream), x, ldx, gamma, eps, s, D, M, (void*)out, ldo, gsum, ldg);
   } else {
     launch_k(PDL_ROW, rmsnorm_kernel<256, true>, dim3(M), dim3(256), 0, as_stream(stream), x, ldx, gamma, eps, s, D,
              (void*)out, ldo);
@@ -352,9 +389,9 @@ extern "C" int sq_rmsnorm_f32(const float* x, int64_t ldx, const float* gamma, f
                               float* out, int64_t ldo, void* stream) {
   SQ_REQUIRE(M >= 0 && D > 0, SQ_ERR_SHAPE, "sq_rmsnorm_f32: bad M/D");
   if (M == 0) return SQ_OK;
-  if (D % 512 == 0 && D / 16 <= 1024 && ldx % 4 == 0 && ldo % 4 == 0)
-    launch_k(PDL_ROW, rmsnorm16_kernel<false>, dim3(M), dim3(D / 16), 0, as_stream(stream), x, ldx, gamma, eps, 1.f, D,
-             (void*)out, ldo, (int32_t*)nullptr, (int64_t)0);
+  if (D % 512 == 0 && D / 16 <= 512 && ldx % 4 == 0 && ldo % 4 == 0)
+    launch_k(PDL_ROW, rmsnorm16_kernel<false>, dim3(row_grid(rmsnorm16_kernel<false>, D / 16, 0, M)), dim3(D / 16), 0,
+             as_stream(stream), x, ldx, gamma, eps, 1.f, D, M, (void*)out, ldo, (int32_t*)nullptr, (int64_t)0);
   else
     launch_k(PDL_ROW, rmsnorm_kernel<256, false>, dim3(M), dim3(256), 0, as_stream(stream), x, ldx, gamma, eps, 1.f, D,
              (void*)out, ldo);
@@ -369,11 +406,12 @@ extern "C" int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* 
   if (M == 0) return SQ_OK;
   const int blk = hadamard ? (D & -D) : 1;
   const size_t smem = (size_t)D * sizeof(float);
-  if (D % 512 == 0 && D / 16 <= 1024 && ldy % 4 == 0 && ldo % 16 == 0) {
+  if (D % 512 == 0 && D / 16 <= 512 && ldy % 4 == 0 && ldo % 16 == 0) {
     auto k16 = gate_norm_had_quant16_kernel;
-    const size_t sm16 = blk > 512 ? smem : 0;
+    const size_t sm16 = blk > 512 ? 2 * smem : 0;
     if (sm16 > 48 * 1024) cudaFuncSetAttribute(k16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm16);
-    k16<<<M, D / 16, sm16, as_stream(stream)>>>(y, ldy, gamma, eps, s_y, blk, D, out, ldo);
+    k16<<<row_grid(k16, D / 16, sm16, M), D / 16, sm16, as_stream(stream)>>>(y, ldy, gamma, eps, s_y, blk, D, M, out,
+                                                                             ldo);
     return check_launch("sq_gate_norm_had_quant");
   }
   auto k = gate_norm_had_quant_kernel<512>;
