@@ -67,6 +67,51 @@ __device__ __forceinline__ int8_t quant8_fast(float v, float inv_s, bool& tie) {
   return (int8_t)(__float_as_int(r) - 0x4B400000);
 }
 
+// 4 int8 codes -> 2 x float2 (exact): each byte, biased to unsigned, becomes the low mantissa
+// byte of 2^23 (PRMT), then 2^23 + 128 is subtracted with one packed add.
+__device__ __forceinline__ void s8x4_f2x2(uint32_t u, float2& a, float2& b) {
+  const uint32_t v = u ^ 0x80808080u;
+  const float2 bias = make_float2(-8388736.0f, -8388736.0f);
+  a = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540)),
+                             __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541))), bias);
+  b = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7542)),
+                             __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7543))), bias);
+}
+__device__ __forceinline__ float ex2_approx(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float rcp_approx(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+// SiLU of a channel pair with packed f32x2 math around the two MUFU ops (silu_approx form)
+__device__ __forceinline__ float2 silu2_approx(float2 v) {
+  const float2 t = __fmul2_rn(v, make_float2(-1.4426950408889634f, -1.4426950408889634f));
+  const float2 d = __fadd2_rn(make_float2(ex2_approx(t.x), ex2_approx(t.y)), make_float2(1.f, 1.f));
+  return __fmul2_rn(v, make_float2(rcp_approx(d.x), rcp_approx(d.y)));
+}
+
+// quant8_fast on four values held as two float2 (packed multiply / magic-number rint);
+// returns the packed little-endian codes and ORs the tie flag (see quant8_fast).
+__device__ __forceinline__ uint32_t quant8x4_fast(float2 v0, float2 v1, float2 inv0, float2 inv1, bool& tie) {
+  const float2 RM = make_float2(12582912.0f, 12582912.0f), NRM = make_float2(-12582912.0f, -12582912.0f);
+  const float2 M1 = make_float2(-1.f, -1.f);
+  float2 t0 = __fmul2_rn(v0, inv0), t1 = __fmul2_rn(v1, inv1);
+  t0.x = fminf(fmaxf(t0.x, -128.f), 127.f);
+  t0.y = fminf(fmaxf(t0.y, -128.f), 127.f);
+  t1.x = fminf(fmaxf(t1.x, -128.f), 127.f);
+  t1.y = fminf(fmaxf(t1.y, -128.f), 127.f);
+  const float2 r0 = __fadd2_rn(t0, RM), r1 = __fadd2_rn(t1, RM);
+  const float2 d0 = __ffma2_rn(__fadd2_rn(r0, NRM), M1, t0), d1 = __ffma2_rn(__fadd2_rn(r1, NRM), M1, t1);
+  tie |= fmaxf(fmaxf(fabsf(d0.x), fabsf(d0.y)), fmaxf(fabsf(d1.x), fabsf(d1.y))) > 0.4999f;
+  // code bytes = low bytes of the rint bit patterns (0x4B400000 has a zero low byte)
+  return __byte_perm(__byte_perm(__float_as_uint(r0.x), __float_as_uint(r0.y), 0x0040),
+                     __byte_perm(__float_as_uint(r1.x), __float_as_uint(r1.y), 0x0040), 0x5410);
+}
+
 // LEDGER G14: log1p(exp(x)), identity above 20.
 __device__ __forceinline__ float softplus_f(float v) {
   return v > 20.f ? v : log1pf(expf(v));

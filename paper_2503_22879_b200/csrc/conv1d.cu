@@ -70,33 +70,6 @@ __global__ void conv1d_prefill_kernel(const TIn* __restrict__ x, int64_t ldx, co
 // exp2 / reciprocal approximations and the division-free quantizer with its exact tie
 // fallback (codes move only at rounding ties).
 constexpr int kSeg4 = 32;
-// 4 int8 codes -> 2 x float2 (exact): each byte, biased to unsigned, becomes the low mantissa
-// byte of 2^23 (PRMT), then 2^23 + 128 is subtracted with one packed add.
-__device__ __forceinline__ void s8x4_f2x2(uint32_t u, float2& a, float2& b) {
-  const uint32_t v = u ^ 0x80808080u;
-  const float2 bias = make_float2(-8388736.0f, -8388736.0f);
-  a = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7540)),
-                             __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7541))), bias);
-  b = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(v, 0x4B000000u, 0x7542)),
-                             __uint_as_float(__byte_perm(v, 0x4B000000u, 0x7543))), bias);
-}
-__device__ __forceinline__ float ex2_approx(float v) {
-  float r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
-  return r;
-}
-__device__ __forceinline__ float rcp_approx(float v) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
-  return r;
-}
-// SiLU of a channel pair with packed f32x2 math around the two MUFU ops (silu_approx form)
-__device__ __forceinline__ float2 silu2_approx(float2 v) {
-  const float2 t = __fmul2_rn(v, make_float2(-1.4426950408889634f, -1.4426950408889634f));
-  const float2 d = __fadd2_rn(make_float2(ex2_approx(t.x), ex2_approx(t.y)), make_float2(1.f, 1.f));
-  return __fmul2_rn(v, make_float2(rcp_approx(d.x), rcp_approx(d.y)));
-}
-
 template <int KC>
 __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __restrict__ x, int64_t ldx,
                                                               const float* __restrict__ w,

@@ -89,10 +89,11 @@ __device__ __forceinline__ int8_t conv_step(const sq_mamba2_decode_params& P, in
 }
 
 // Four consecutive channels c..c+3 with Kc = 4: every load issued up front (3 cache
-// words, the new codes, 4x4 taps, bias / scales as float4), same per-channel op order.
-__device__ __forceinline__ void conv4_step(const sq_mamba2_decode_params& P, int c, int C,
-                                           int8_t* __restrict__ cache_b, const int8_t* xnew,
-                                           int8_t (&code)[4]) {
+// words, the new codes, 4x4 taps, bias / scales as float4), the same per-channel op order
+// (acc = b + Σ_j w_j·(q_j·s_in), IEEE RN each) computed as packed f32x2 pairs, SiLU from the
+// MUFU exp2 / reciprocal, and the division-free quantizer with its exact tie fallback.
+__device__ __forceinline__ uint32_t conv4_step(const sq_mamba2_decode_params& P, int c, int C,
+                                               int8_t* __restrict__ cache_b, const int8_t* xnew) {
   const uint32_t w0 = *reinterpret_cast<const uint32_t*>(cache_b + c);
   const uint32_t w1 = *reinterpret_cast<const uint32_t*>(cache_b + C + c);
   const uint32_t w2 = *reinterpret_cast<const uint32_t*>(cache_b + 2 * C + c);
@@ -105,20 +106,28 @@ __device__ __forceinline__ void conv4_step(const sq_mamba2_decode_params& P, int
   *reinterpret_cast<uint32_t*>(cache_b + c) = w1;
   *reinterpret_cast<uint32_t*>(cache_b + C + c) = w2;
   *reinterpret_cast<uint32_t*>(cache_b + 2 * C + c) = w3;
-  const float4 taps[4] = {t0, t1, t2, t3};
+  // taps of channel pairs (c, c+1) and (c+2, c+3), tap j
+  const float2 wa[4] = {make_float2(t0.x, t1.x), make_float2(t0.y, t1.y), make_float2(t0.z, t1.z), make_float2(t0.w, t1.w)};
+  const float2 wb[4] = {make_float2(t2.x, t3.x), make_float2(t2.y, t3.y), make_float2(t2.z, t3.z), make_float2(t2.w, t3.w)};
   const uint32_t win[4] = {w0, w1, w2, w3};
+  const float2 sia = make_float2(si.x, si.y), sib = make_float2(si.z, si.w);
+  float2 acca = make_float2(bi.x, bi.y), accb = make_float2(bi.z, bi.w);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const float s_in = fget(si, e);
-    float acc = fget(bi, e);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float q = (float)(int8_t)(win[j] >> (8 * e));
-      acc = __fadd_rn(acc, __fmul_rn(fget(taps[e], j), __fmul_rn(q, s_in)));
-    }
-    const float so_e = fget(so, e);
-    code[e] = quant8_inv(silu_fast(acc), so_e, __frcp_rn(so_e));
+  for (int j = 0; j < 4; ++j) {
+    float2 qa, qb;
+    s8x4_f2x2(win[j], qa, qb);
+    acca = __fadd2_rn(acca, __fmul2_rn(wa[j], __fmul2_rn(qa, sia)));
+    accb = __fadd2_rn(accb, __fmul2_rn(wb[j], __fmul2_rn(qb, sib)));
   }
+  const float2 va = silu2_approx(acca), vb = silu2_approx(accb);
+  bool tie = false;
+  // reciprocal estimates are within ~1 ulp: quant8_fast's tie window (1e-4 of a step) covers it
+  uint32_t code = quant8x4_fast(va, vb, make_float2(rcp_approx(so.x), rcp_approx(so.y)),
+                                make_float2(rcp_approx(so.z), rcp_approx(so.w)), tie);
+  if (tie)
+    code = (uint32_t)(uint8_t)quant8(va.x, so.x) | ((uint32_t)(uint8_t)quant8(va.y, so.y) << 8) |
+           ((uint32_t)(uint8_t)quant8(vb.x, so.z) << 16) | ((uint32_t)(uint8_t)quant8(vb.y, so.w) << 24);
+  return code;
 }
 
 
@@ -155,39 +164,65 @@ __global__ void __launch_bounds__(256) prep_kernel(const sq_mamba2_decode_params
   const int step = vec ? 4 : 1;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * step;
   if (c >= C) return;
-  int8_t q[4];
-  if (vec) {
-    conv4_step(P, c, C, cache_b, zrow + di + c, q);
-  } else {
-    q[0] = conv_step(P, Kc, c, C, cache_b, zrow[di + c]);
-  }
-  if (c < di) {   // x channels: the scan's per-row operands
-    const int h = c / DS_P;
-    const float delta = softplus_f(__fadd_rn(__fmul_rn((float)zrow[2 * di + 2 * GN + h], S.s_dt), S.dt_bias[h]));
-    const float rsmax = 2097152.0f / (128.0f * S.s_B[S.head_group[h]]);   // |rs·B̂| <= 2^21
-    float* rf = rows_b + (int64_t)h * DS_ROWF;
-    for (int e = 0; e < step; ++e) {
-      const int p = (c + e) % DS_P;
-      const float so = P.conv_s_out[c + e];
-      const float xh = __fmul_rn((float)q[e], so);
-      const float sh = S.s_h[c + e];
-      rf[p] = xh;
-      rf[DS_P + p] = fminf(fmaxf(__fmul_rn(__fmul_rn(delta, xh), __frcp_rn(sh)), -rsmax), rsmax);
-      rf[2 * DS_P + p] = silu_fast(__fmul_rn((float)zrow[c + e], S.s_z));
-      rf[3 * DS_P + p] = sh;
+  if (vec) {   // four consecutive channels, one head (x) or one group run of B / C
+    const uint32_t code = conv4_step(P, c, C, cache_b, zrow + di + c);
+    const float4 so = __ldg(reinterpret_cast<const float4*>(P.conv_s_out + c));
+    const float4 v = make_float4(__fmul_rn((float)(int8_t)code, so.x), __fmul_rn((float)(int8_t)(code >> 8), so.y),
+                                 __fmul_rn((float)(int8_t)(code >> 16), so.z), __fmul_rn((float)(int8_t)(code >> 24), so.w));
+    if (c < di) {   // x channels: the scan's per-row operands
+      const int h = c / DS_P, p = c % DS_P;
+      const float delta = softplus_f(__fadd_rn(__fmul_rn((float)zrow[2 * di + 2 * GN + h], S.s_dt), S.dt_bias[h]));
+      const float rsmax = 2097152.0f / (128.0f * S.s_B[S.head_group[h]]);   // |rs·B̂| <= 2^21
+      float* rf = rows_b + (int64_t)h * DS_ROWF;
+      const float4 sh = __ldg(reinterpret_cast<const float4*>(S.s_h + c));
+      const uint32_t zc = *reinterpret_cast<const uint32_t*>(zrow + c);
+      auto rs = [&](float xh, float s) {
+        return fminf(fmaxf(__fmul_rn(__fmul_rn(delta, xh), __frcp_rn(s)), -rsmax), rsmax);
+      };
+      const float2 za = silu2_approx(__fmul2_rn(make_float2((float)(int8_t)zc, (float)(int8_t)(zc >> 8)),
+                                                make_float2(S.s_z, S.s_z)));
+      const float2 zb = silu2_approx(__fmul2_rn(make_float2((float)(int8_t)(zc >> 16), (float)(int8_t)(zc >> 24)),
+                                                make_float2(S.s_z, S.s_z)));
+      *reinterpret_cast<float4*>(rf + p) = v;
+      *reinterpret_cast<float4*>(rf + DS_P + p) = make_float4(rs(v.x, sh.x), rs(v.y, sh.y), rs(v.z, sh.z), rs(v.w, sh.w));
+      *reinterpret_cast<float4*>(rf + 2 * DS_P + p) = make_float4(za.x, za.y, zb.x, zb.y);
+      *reinterpret_cast<float4*>(rf + 3 * DS_P + p) = sh;
       if (p == 0) {
         rf[4 * DS_P] = expf(__fmul_rn(delta, S.A[h]));
         rf[4 * DS_P + 1] = S.D[h];
       }
-    }
-  } else {        // B | C channels
-    for (int e = 0; e < step; ++e) {
-      const int j = c + e - di;
+    } else {        // B | C channels: four consecutive n of one group land contiguously
+      const int j = c - di;
       const int isC = j >= GN ? 1 : 0;
       const int jj = j - isC * GN;
       const int g = jj / N, n = jj % N;
-      bc_b[(int64_t)g * 2 * N + isC * N + bc_swz(n, N)] = __fmul_rn((float)q[e], P.conv_s_out[c + e]);
+      *reinterpret_cast<float4*>(bc_b + (int64_t)g * 2 * N + isC * N + bc_swz(n, N)) = v;
     }
+    return;
+  }
+  const int8_t q = conv_step(P, Kc, c, C, cache_b, zrow[di + c]);
+  if (c < di) {
+    const int h = c / DS_P;
+    const float delta = softplus_f(__fadd_rn(__fmul_rn((float)zrow[2 * di + 2 * GN + h], S.s_dt), S.dt_bias[h]));
+    const float rsmax = 2097152.0f / (128.0f * S.s_B[S.head_group[h]]);
+    float* rf = rows_b + (int64_t)h * DS_ROWF;
+    const int p = c % DS_P;
+    const float xh = __fmul_rn((float)q, P.conv_s_out[c]);
+    const float sh = S.s_h[c];
+    rf[p] = xh;
+    rf[DS_P + p] = fminf(fmaxf(__fmul_rn(__fmul_rn(delta, xh), __frcp_rn(sh)), -rsmax), rsmax);
+    rf[2 * DS_P + p] = silu_approx(__fmul_rn((float)zrow[c], S.s_z));
+    rf[3 * DS_P + p] = sh;
+    if (p == 0) {
+      rf[4 * DS_P] = expf(__fmul_rn(delta, S.A[h]));
+      rf[4 * DS_P + 1] = S.D[h];
+    }
+  } else {
+    const int j = c - di;
+    const int isC = j >= GN ? 1 : 0;
+    const int jj = j - isC * GN;
+    const int g = jj / N, n = jj % N;
+    bc_b[(int64_t)g * 2 * N + isC * N + bc_swz(n, N)] = __fmul_rn((float)q, P.conv_s_out[c]);
   }
 }
 
