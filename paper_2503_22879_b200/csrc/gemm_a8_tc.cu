@@ -40,6 +40,13 @@ constexpr int TC_ACOL = 256;      // first TMEM column of the A (weight) stages 
 constexpr int TC_THREADS = 384;     // 12 warps: TMA, MMA, 8 converter/epilogue, group-sum, W4 stream
 constexpr int TC_MAX_KB = 64;       // max K-blocks per split (K <= 8192)
 constexpr int W4_TILE_BYTES = TC_BN * TC_BK / 2;  // 8 KB per (n-tile, k-block)
+// packed-weight ring depth for small token tiles: the HBM stream needs ~150 KB in flight per
+// SM to approach peak (Little's law at the loaded latency), so the ring takes most of smem
+// and the activation stages (L2-resident, shared by every CTA) shrink to what remains.
+#ifndef SQ_RAW64
+#define SQ_RAW64 12
+#endif
+constexpr int g_raw64 = SQ_RAW64;
 
 enum { WM_W8 = 0, WM_W4_TS = 1, WM_W4_SS = 2 };
 
@@ -150,6 +157,10 @@ template <int NTOK, int WMODE, int SPLITS, int STAGES, int RAW>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w, TcArgs args) {
   using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES, RAW>;
+  // converter batch: D k-blocks per raw-ring barrier and per TMEM-stage wait (D < STAGES, no self-wait)
+  constexpr int D = STAGES >= 8 ? 4 : (STAGES >= 4 ? 2 : 1);
+  constexpr int RB = RAW / D;   // raw-ring batch slots
+  static_assert(WMODE == WM_W8 || RAW % D == 0, "raw ring must hold whole converter batches");
   constexpr bool W4 = Cfg::W4;
   // byte offsets from the extern array keep every access in the shared space (LDS/STS)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -174,6 +185,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const bool tl = (args.dbg & 2) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && split == 0;
   const uint64_t t_entry = tl ? gtimer() : 0;
   uint64_t t_raw0 = 0, t_rawl = 0, t_conv_done = 0, t_acc = 0, t_epi0 = 0, t_epi1 = 0, t_ld0 = 0, t_loop = 0;
+  long long c_raw = 0, c_emp = 0, c_stw = 0, c_full = 0;   // timeline: SM cycles spent waiting
+  long long c_b0 = 0, c_b1 = 0, c_b2 = 0;                  // timeline: convert / store / signal phases
   const int nkb_total = args.K / TC_BK;
   const int kb_begin = split * nkb_total / SPLITS;
   const int nkb = (split + 1) * nkb_total / SPLITS - kb_begin;
@@ -184,7 +197,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&full[s], W4 ? 1 + 8 : 1);      // TMA (+ 8 converter warps)
       mbar_init(&empty[s], (W4 && !args.gsum) ? 2 : 1);   // MMA commit (+ group-sum warp)
     }
-    for (int r = 0; r < RAW; ++r) {
+    for (int r = 0; r < RB; ++r) {
       mbar_init(&rfull[r], 1);
       mbar_init(&rempty[r], 8);
     }
@@ -220,7 +233,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       constexpr uint32_t idesc = W4 ? (idesc_i8(TC_BN, NTOK) & ~(7u << 7)) : idesc_i8(TC_BN, NTOK);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
+        const long long c0 = tl ? clock64() : 0;
         mbar_wait(&full[s], (i / STAGES) & 1);
+        if (tl) c_full += clock64() - c0;
         tc_fence_after();
         const uint64_t bdesc = desc_sw128(act + s * Cfg::ACT_BYTES);
 #pragma unroll
@@ -311,11 +326,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- packed W4 tiles: contiguous 8 KB per (n-tile, k-block) -> smem ring
     if (W4 && lane == 0) {
       const uint8_t* src = args.w4 + ((size_t)n_tile * nkb_total + kb_begin) * W4_TILE_BYTES;
-      for (int i = 0; i < nkb; ++i) {
-        const int r = i % RAW;
-        mbar_wait(&rempty[r], ((i / RAW) & 1) ^ 1);
-        mbar_arrive_expect_tx(&rfull[r], W4_TILE_BYTES);
-        bulk_load(raw + r * W4_TILE_BYTES, src + (size_t)i * W4_TILE_BYTES, W4_TILE_BYTES, &rfull[r]);
+      for (int bi = 0; bi * D < nkb; ++bi) {   // one barrier per converter batch of D tiles
+        const int r = bi % RB;
+        mbar_wait(&rempty[r], ((bi / RB) & 1) ^ 1);
+        const int n = min(D, nkb - bi * D);
+        mbar_arrive_expect_tx(&rfull[r], n * W4_TILE_BYTES);
+        for (int t = 0; t < n; ++t)
+          bulk_load(raw + (r * D + t) * W4_TILE_BYTES, src + (size_t)(bi * D + t) * W4_TILE_BYTES, W4_TILE_BYTES,
+                    &rfull[r]);
       }
     }
     __syncwarp();
@@ -373,50 +391,67 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
       named_bar(2, 256);                 // converter warps: sg staged
-      constexpr int D = STAGES >= 8 ? 4 : (STAGES >= 4 ? 2 : 1);   // batch < STAGES (no self-wait)
       for (int i0 = 0; i0 < nkb; i0 += D) {
+        const int rb = (i0 / D) % RB, nb = min(D, nkb - i0);
+        const long long cb0 = tl ? clock64() : 0;
+        // (1) the batch's tiles landed; (2) every smem read of the batch issued together; (3)
+        // the expansion of D tiles interleaved — no barrier wait sits between a load and the
+        // next tile's load, so the LDS / IMUL latencies overlap across the batch.
         uint32_t wv[D][16];
+        {
+          const long long c0 = tl ? clock64() : 0;
+          mbar_wait(&rfull[rb], ((i0 / D) / RB) & 1);
+          if (tl) c_raw += clock64() - c0;
+          if (tl && warp == 2 && i0 == 0) t_raw0 = gtimer();
+          if (tl && warp == 2 && i0 + D >= nkb) t_rawl = gtimer();
+        }
+        uint4 p0[D], p1[D];
+        uint32_t sgv[D];
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-          const int i = i0 + j;
-          if (i < nkb) {
-            const int r = i % RAW;
-            mbar_wait(&rfull[r], (i / RAW) & 1);
-            if (tl && warp == 2 && i == 0) t_raw0 = gtimer();
-            if (tl && warp == 2 && i == nkb - 1) t_rawl = gtimer();
-            const uint8_t* rp = raw + r * W4_TILE_BYTES + half * 2 * 2048 + row * 16;
-            const uint4 p0 = *reinterpret_cast<const uint4*>(rp);
-            const uint4 p1 = *reinterpret_cast<const uint4*>(rp + 2048);
-            const uint32_t sg = (uint32_t)(uint8_t)sgs[i * TC_BN + row];
-            if (args.dbg & 8) {   // profiling: skip the nibble expansion
-              wv[j][0] = p0.x; wv[j][1] = p0.y; wv[j][2] = p0.z; wv[j][3] = p0.w;
-              wv[j][4] = p1.x; wv[j][5] = p1.y; wv[j][6] = p1.z; wv[j][7] = p1.w;
-              wv[j][8] = p0.x; wv[j][9] = p0.y; wv[j][10] = p0.z; wv[j][11] = p0.w;
-              wv[j][12] = p1.x; wv[j][13] = p1.y; wv[j][14] = p1.z; wv[j][15] = p1.w;
-              continue;
-            }
-            nib8_to_u8(p0.x, sg, wv[j][0], wv[j][1]);
-            nib8_to_u8(p0.y, sg, wv[j][2], wv[j][3]);
-            nib8_to_u8(p0.z, sg, wv[j][4], wv[j][5]);
-            nib8_to_u8(p0.w, sg, wv[j][6], wv[j][7]);
-            nib8_to_u8(p1.x, sg, wv[j][8], wv[j][9]);
-            nib8_to_u8(p1.y, sg, wv[j][10], wv[j][11]);
-            nib8_to_u8(p1.z, sg, wv[j][12], wv[j][13]);
-            nib8_to_u8(p1.w, sg, wv[j][14], wv[j][15]);
+          const int i = min(i0 + j, nkb - 1);
+          const uint8_t* rp = raw + (rb * D + (i - i0)) * W4_TILE_BYTES + half * 2 * 2048 + row * 16;
+          p0[j] = *reinterpret_cast<const uint4*>(rp);
+          p1[j] = *reinterpret_cast<const uint4*>(rp + 2048);
+          sgv[j] = (uint32_t)(uint8_t)sgs[i * TC_BN + row];
+        }
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          if (args.dbg & 8) {   // profiling: skip the nibble expansion
+            wv[j][0] = p0[j].x; wv[j][1] = p0[j].y; wv[j][2] = p0[j].z; wv[j][3] = p0[j].w;
+            wv[j][4] = p1[j].x; wv[j][5] = p1[j].y; wv[j][6] = p1[j].z; wv[j][7] = p1[j].w;
+            wv[j][8] = p0[j].x; wv[j][9] = p0[j].y; wv[j][10] = p0[j].z; wv[j][11] = p0[j].w;
+            wv[j][12] = p1[j].x; wv[j][13] = p1[j].y; wv[j][14] = p1[j].z; wv[j][15] = p1[j].w;
+            continue;
           }
+          nib8_to_u8(p0[j].x, sgv[j], wv[j][0], wv[j][1]);
+          nib8_to_u8(p0[j].y, sgv[j], wv[j][2], wv[j][3]);
+          nib8_to_u8(p0[j].z, sgv[j], wv[j][4], wv[j][5]);
+          nib8_to_u8(p0[j].w, sgv[j], wv[j][6], wv[j][7]);
+          nib8_to_u8(p1[j].x, sgv[j], wv[j][8], wv[j][9]);
+          nib8_to_u8(p1[j].y, sgv[j], wv[j][10], wv[j][11]);
+          nib8_to_u8(p1[j].z, sgv[j], wv[j][12], wv[j][13]);
+          nib8_to_u8(p1[j].w, sgv[j], wv[j][14], wv[j][15]);
         }
         __syncwarp();
         if (lane == 0) {
-#pragma unroll
-          for (int j = 0; j < D; ++j)
-            if (i0 + j < nkb) mbar_arrive(&rempty[(i0 + j) % RAW]);
+          mbar_arrive(&rempty[rb]);
+        }
+        const long long cb1 = tl ? clock64() : 0;
+        {
+          // the batch's stages are free once the MMA read their previous contents; MMAs and
+          // their commits complete in issue order, so the batch's last stage implies the rest
+          // (the barriers are never more than one phase ahead: the MMA waits on our arrivals)
+          const int il = i0 + nb - 1;
+          const long long c0 = tl ? clock64() : 0;
+          mbar_wait(&empty[il % STAGES], ((il / STAGES) & 1) ^ 1);
+          if (tl) c_emp += clock64() - c0;
         }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           const int i = i0 + j;
           if (i < nkb) {
             const int s = i % STAGES;
-            mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
             if (WMODE == WM_W4_TS) {
               if (!(args.dbg & 4)) tmem_st_x16(tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + s * 32 + half * 16, wv[j]);
             } else {
@@ -431,8 +466,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           }
         }
+        const long long cb2 = tl ? clock64() : 0;
         if (WMODE == WM_W4_TS) {
+          const long long c0 = tl ? clock64() : 0;
           tmem_wait_st();
+          if (tl) c_stw += clock64() - c0;
           tc_fence_before();
         } else {
           fence_proxy_async_smem();
@@ -442,6 +480,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < D; ++j)
             if (i0 + j < nkb) mbar_arrive(&full[(i0 + j) % STAGES]);
+        }
+        if (tl) {
+          const long long cb3 = clock64();
+          c_b0 += cb1 - cb0;
+          c_b1 += cb2 - cb1;
+          c_b2 += cb3 - cb2;
         }
       }
     }
@@ -607,6 +651,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (tl && warp == 2)
     printf("gemm cta %d: first tmem ld %.2f  loop end %.2f us\n", blockIdx.x, (t_ld0 - t_entry) * 1e-3,
            (t_loop - t_entry) * 1e-3);
+  if (tl && warp == 2 && lane == 0)
+    printf("gemm cta %d waits (cycles): converter rfull %lld empty %lld wait_st %lld | phases convert %lld store %lld "
+           "signal %lld\n", blockIdx.x, c_raw, c_emp, c_stw, c_b0, c_b1, c_b2);
+  if (tl && warp == 1 && lane == 0)
+    printf("gemm cta %d waits (cycles): mma full %lld\n", blockIdx.x, c_full);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -642,7 +691,7 @@ static int make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
 
 template <int NTOK, int WMODE, int SPLITS>
 static int launch_tc(const int8_t* a, int64_t lda, const uint8_t* w, const TcArgs& args, cudaStream_t st) {
-  constexpr int RAW = WMODE == WM_W8 ? 1 : (NTOK <= 64 ? 12 : (NTOK == 128 ? 8 : 6));
+  constexpr int RAW = WMODE == WM_W8 ? 1 : (NTOK <= 64 ? g_raw64 : (NTOK == 128 ? 8 : 6));
   using C1 = TcCfg<NTOK, WMODE, SPLITS, 1, RAW>;
   constexpr int ST0 = (210 * 1024 - C1::RAW_BYTES - C1::SUM_BYTES - C1::SGS_BYTES) / C1::STAGE_BYTES;
   constexpr int STAGES = ST0 > 8 ? 8 : (ST0 < 2 ? 2 : ST0);

@@ -115,6 +115,14 @@ __device__ __forceinline__ void tmem_ld_x16(uint32_t a, uint32_t (&r)[16]) {
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(a));
 }
+template <int NC>
+__device__ __forceinline__ void tmem_ld_n(uint32_t a, uint32_t (&r)[NC]) {
+  static_assert(NC == 8 || NC == 16, "tmem_ld_n: 8 or 16 columns");
+  if constexpr (NC == 8)
+    tmem_ld_x8(a, r);
+  else
+    tmem_ld_x16(a, r);
+}
 __device__ __forceinline__ void tmem_st_x16(uint32_t a, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(a),
