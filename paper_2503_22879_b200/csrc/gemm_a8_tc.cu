@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (lane == 0) {
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
-        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        mbar_wait_lazy(&empty[s], ((i / STAGES) & 1) ^ 1);   // polling would steal converter issue slots
         mbar_arrive_expect_tx(&full[s], Cfg::ACT_BYTES + (W4 ? 0 : Cfg::W_BYTES));
         tma_load_2d(act + s * Cfg::ACT_BYTES, &tm_act, &full[s], (kb_begin + i) * TC_BK, m_tile * NTOK);
         if (!W4) tma_load_2d(wsm + s * Cfg::W_BYTES, &tm_w, &full[s], (kb_begin + i) * TC_BK, n_tile * TC_BN);
@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int ks = 0; ks < TC_BK / 32; ++ks) {
           const uint32_t acc = (i > 0 || ks > 0) ? 1u : 0u;
+          if (args.dbg & 32) continue;   // profiling: no main-loop MMAs (commit only)
           if (WMODE == WM_W4_TS) {
             mma_i8_ts(tmem, tmem + TC_ACOL + s * 32 + ks * 8, bdesc + 2 * ks, idesc, acc);
           } else {
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint8_t* src = args.w4 + ((size_t)n_tile * nkb_total + kb_begin) * W4_TILE_BYTES;
       for (int bi = 0; bi * D < nkb; ++bi) {   // one barrier per converter batch of D tiles
         const int r = bi % RB;
-        mbar_wait(&rempty[r], ((bi / RB) & 1) ^ 1);
+        mbar_wait_lazy(&rempty[r], ((bi / RB) & 1) ^ 1);
         const int n = min(D, nkb - bi * D);
         mbar_arrive_expect_tx(&rfull[r], n * W4_TILE_BYTES);
         for (int t = 0; t < n; ++t)
@@ -417,13 +418,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-          if (args.dbg & 8) {   // profiling: skip the nibble expansion
-            wv[j][0] = p0[j].x; wv[j][1] = p0[j].y; wv[j][2] = p0[j].z; wv[j][3] = p0[j].w;
-            wv[j][4] = p1[j].x; wv[j][5] = p1[j].y; wv[j][6] = p1[j].z; wv[j][7] = p1[j].w;
-            wv[j][8] = p0[j].x; wv[j][9] = p0[j].y; wv[j][10] = p0[j].z; wv[j][11] = p0[j].w;
-            wv[j][12] = p1[j].x; wv[j][13] = p1[j].y; wv[j][14] = p1[j].z; wv[j][15] = p1[j].w;
-            continue;
-          }
           nib8_to_u8(p0[j].x, sgv[j], wv[j][0], wv[j][1]);
           nib8_to_u8(p0[j].y, sgv[j], wv[j][2], wv[j][3]);
           nib8_to_u8(p0[j].z, sgv[j], wv[j][4], wv[j][5]);
@@ -433,6 +427,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           nib8_to_u8(p1[j].z, sgv[j], wv[j][12], wv[j][13]);
           nib8_to_u8(p1[j].w, sgv[j], wv[j][14], wv[j][15]);
         }
+        // generic-proxy reads of the raw slot are ordered before the bulk copy (async proxy)
+        // that will refill it
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&rempty[rb]);
@@ -793,8 +790,7 @@ int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg,
   if (!w4) return dispatch_split<WM_W8>(splits, ntok, a, lda, w, args, st);
   // A-from-TMEM is used up to 128-token tiles (the 256-column accumulator leaves too few
   // TMEM columns for the A stages); larger tiles stage the expanded weights in smem.
-  // SS (weights expanded into smem) is used without split-K only: with split-K at 64-token
-  // tiles it showed a rare wrong-atom race in repeated runs (under investigation).
+  // SS (weights expanded into smem) is used without split-K only.
   if (ntok > 128) return dispatch_split<WM_W4_SS>(1, ntok, a, lda, w, args, st);
   if (g_tc_w4_mode == WM_W4_SS && splits == 1) return dispatch_split<WM_W4_SS>(1, ntok, a, lda, w, args, st);
   return dispatch_split<WM_W4_TS>(splits, ntok, a, lda, w, args, st);

@@ -68,6 +68,15 @@ def test_gemm_w8a8_exact(cuda, gemm_mode, M, N, K):
     assert np.array_equal(tres.cpu().numpy(), (res + y).astype(np.float32))
 
 
+def _same(got, want, what):
+    """Exact equality with a diagnostic of where the results differ."""
+    d = got != want
+    if d.any():
+        r, c = np.nonzero(d)
+        raise AssertionError(f"{what}: {d.sum()} of {d.size} differ; rows {np.unique(r)[:10]} (x{len(np.unique(r))}), "
+                             f"col tiles {np.unique(c // 128)}; first got {got[r[0], c[0]]} want {want[r[0], c[0]]}")
+
+
 @pytest.mark.parametrize("M,N,K,group", [(64, 384, 4096, 128), (3, 256, 256, 32), (16, 130, 8192, 128),
                                          (64, 4096, 8192, 128), (64, 18560, 4096, 128), (300, 640, 1024, 128)])
 def test_gemm_w4a8_exact(cuda, gemm_mode, M, N, K, group):
@@ -88,13 +97,13 @@ def test_gemm_w4a8_exact(cuda, gemm_mode, M, N, K, group):
     tsg = torch.as_tensor(sg, device=cuda)
     tal = torch.as_tensor(alpha, device=cuda)
     got = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_I32).cpu().numpy()
-    assert np.array_equal(got, acc)
+    _same(got, acc, "I32")
     gy = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_F32).cpu().numpy()
-    assert np.array_equal(gy, (acc.astype(np.float32) * alpha[None]).astype(np.float32))
+    _same(gy, (acc.astype(np.float32) * alpha[None]).astype(np.float32), "F32")
     if K % 128 == 0:   # activation block sums supplied by the producer instead of computed in-kernel
         gs = torch.as_tensor(a.astype(np.int32).reshape(M, K // 128, 128).sum(-1).astype(np.int32), device=cuda)
         got2 = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_I32, gsum=gs).cpu().numpy()
-        assert np.array_equal(got2, acc)
+        _same(got2, acc, "I32+gsum")
 
 
 @pytest.mark.parametrize("M,N,K,group", [(1, 18560 // 4, 4096, 128), (3, 512, 8192, 128), (16, 200, 160, 32)])
