@@ -355,6 +355,7 @@ __global__ void __launch_bounds__(SR_THREADS, 2) state_ring_kernel(const sq_mamb
         y[(int64_t)b * ldy + h * DS_P + R] =
             __fmul_rn(__fadd_rn(__fmul_rn(rf[3 * DS_P + R], acc), __fmul_rn(Dh, rf[R])), rf[2 * DS_P + R]);
     }
+    fence_proxy_async_smem();   // our generic reads of the slot precede the next bulk copy into it
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
     h += dh;

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             gsum[i * NTOK + t] = acc;
           }
         }
+        fence_proxy_async_smem();   // generic reads of the stage precede the next TMA write into it
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
