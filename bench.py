@@ -172,11 +172,46 @@ def cpu_decode_sample(dims, profile, batch, layers_sample=2, seed=0):
     return dt
 
 
+def cpu_prefill_sample(dims, profile, tokens, seed=0):
+    """Time the oracle (numpy port) prefill of one full-width layer over `tokens` tokens of one
+    sequence (chunked SSD path); returns seconds per token per layer."""
+    from oracle import qblock as oq
+    from oracle.ssm_block import Dims as ODims
+    from paper_2503_22879_b200 import synth
+    from paper_2503_22879_b200.ssm_block import Dims
+    d = Dims(*dims)
+    od = ODims(*dims)
+    qb = synth.random_qblock(d, profile, seed)
+    oqb = oq.QBlock(od, qb.profile, oq.QLinear(**vars(qb.in_proj)), oq.QLinear(**vars(qb.out_proj)),
+                    qb.conv_weight, qb.conv_bias, qb.a_log, qb.d_param, qb.dt_bias, qb.norm_weight, qb.head_group,
+                    s_u=qb.s_u, in_out_scale=qb.in_out_scale, conv_in_scale=qb.conv_in_scale,
+                    conv_out_scale=qb.conv_out_scale, state_scale=qb.state_scale, s_y=qb.s_y)
+    u = np.random.default_rng(seed).standard_normal((tokens, d.d_model)).astype(np.float32)
+    t0 = time.perf_counter()
+    oq.block_forward_quantized(u, oqb)
+    return (time.perf_counter() - t0) / tokens
+
+
 def run_reference_arm(args, wl, world, rank):
     if rank != 0:
         return
     import multiprocessing
     cores = multiprocessing.cpu_count()
+    if args.workload.startswith("prefill"):
+        ntok = 128
+        cpu_prefill_sample(wl["dims"], wl["profile"], 16)
+        spts = [cpu_prefill_sample(wl["dims"], wl["profile"], ntok) for _ in range(args.steps)]
+        val = 1.0 / (float(np.mean(spts)) * wl["layers"])
+        line = {"impl": "reference", "metric": "prefill tok/s", "value": val, "unit": "tok/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wl["batch"] * wl["seq"] / val,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+                "data": "synthetic", "config": {"workload": args.workload, "desc": wl["desc"]},
+                "cpu_baseline": {"value": val, "unit": "tok/s", "cores": cores, "kind": "port",
+                                 "sample": f"one full-width layer over {ntok} tokens per timed step, x{wl['layers']} "
+                                           f"layers (extrapolated); numpy oracle, exact-int f64 BLAS"},
+                "e2e": {"value": val, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     b = wl["batch"] * world
     per_layer = []
     for _ in range(max(1, args.warmup and 1)):
@@ -266,6 +301,35 @@ def run_prefill(args, wl, world, rank, local):
     ops_per = 2.0 * M * d.in_proj_out * d.d_model
     achieved = ops_per / (gemm_ms / 1e3) / 1e12
     hbm, bf16, pk_kind = peaks()
+    # the step's largest kernel: the chunked int8 SSD scan (HBM-bound in principle: int8 codes
+    # in, f32 y + int8 state out), timed live on the layer's own inputs
+    di, gn, nh = d.d_inner, d.n_state_groups * d.d_state, d.n_heads
+    cv, zx = ws["conv"], ws["zx"]
+    st_tmp = torch.empty((B, nh, d.head_dim, d.d_state), dtype=torch.int8, device=dev)
+
+    def ssd():
+        ops.ssd_scan_int8(blk.params, B, T, cv[:, :di], cv[:, di:di + gn], cv[:, di + gn:], zx[:, 2 * di + 2 * gn:],
+                          zx[:, :di], st_tmp, False, ws["y"])
+    for _ in range(2):
+        ssd()
+    torch.cuda.synchronize()
+    k0.record(st)
+    for _ in range(5):
+        ssd()
+    k1.record(st)
+    torch.cuda.synchronize()
+    ssd_ms = k0.elapsed_time(k1) / 5
+    ssd_bytes = M * (di + 2 * gn + di + nh + 4 * di) + st_tmp.numel()
+    ssd_gbs = ssd_bytes / (ssd_ms / 1e3) / 1e9
+    launches_per_step = 7 * len(lm.blocks) + 3   # per layer: norm, in_proj, conv (2), scan, gated norm, out_proj
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import multiprocessing
+        ntok = 256
+        spt = cpu_prefill_sample(wl["dims"], wl["profile"], ntok)
+        cpu = {"value": 1.0 / (spt * wl["layers"]), "unit": "tok/s", "cores": multiprocessing.cpu_count(),
+               "kind": "port", "sample": f"one full-width layer over {ntok} tokens of one sequence (chunked SSD), "
+                                         f"x{wl['layers']} layers (extrapolated); numpy oracle, exact-int f64 BLAS"}
     if rank == 0:
         line = {"metric": "prefill tok/s", "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -274,14 +338,18 @@ def run_prefill(args, wl, world, rank, local):
                            "global_batch": B * world, "seq_len": T, "layers": wl["layers"],
                            "parallelism": f"dp{world} (batch-shard replicas, no collective)",
                            "l2": "activations 16384 x 10576 int8 per layer exceed L2; no flush"},
-                "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (in_proj W8A8, tcgen05 kind::i8)",
-                             "achieved": achieved, "peak": bf16 * 2, "unit": "TOP/s", "frac": achieved / (bf16 * 2),
-                             "traffic": None, "peak_kind": pk_kind + " (int8 = 2 x measured bf16 dense)",
-                             "algorithmic_ops_per_launch": ops_per, "launch_ms": gemm_ms},
-                "cpu_baseline": None,
+                "roofline": {"bound": "hbm", "kernel": "ssd_chunk_kernel (chunked int8 SSD scan, mma.sync)",
+                             "achieved": ssd_gbs, "peak": hbm, "unit": "GB/s", "frac": ssd_gbs / hbm,
+                             "traffic": None, "peak_kind": pk_kind,
+                             "algorithmic_bytes_per_launch": ssd_bytes, "launch_ms": ssd_ms},
+                "roofline_gemm": {"bound": "tensor", "kernel": "gemm_tc_kernel (in_proj W8A8, tcgen05 kind::i8)",
+                                  "achieved": achieved, "peak": bf16 * 2, "unit": "TOP/s", "frac": achieved / (bf16 * 2),
+                                  "traffic": None, "peak_kind": pk_kind + " (int8 = 2 x measured bf16 dense)",
+                                  "algorithmic_ops_per_launch": ops_per, "launch_ms": gemm_ms},
+                "cpu_baseline": cpu,
                 "e2e": {"value": world * B * T / (e2e_ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": B * T * 4,
                         "d2h_bytes_per_step": B * lm.vocab * 4},
-                "gpu_launches": None, "clocks": clk.summary()}
+                "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
 
 

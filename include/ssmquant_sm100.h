@@ -204,6 +204,14 @@ int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T,
                            const int8_t* BC, int64_t ldbc, const int8_t* z, int64_t ldz,
                            int8_t* state, int state_in, float* y, int64_t ldy, void* stream);
 
+/* Mamba1 W4A16 scan on floats: x / dt_raw / z [B*T x d], B|C rows [B*T x 2N] (stride ldbc,
+ * C at +N), state f32 [B x d x N].  Replaces the reference's float selective_scan for the
+ * Mamba1 W4A16 profile. */
+int sq_selective_scan_f32(const sq_mamba1_params* p, int B, int T,
+                          const float* x, int64_t ldx, const float* dt, int64_t lddt,
+                          const float* BC, int64_t ldbc, const float* z, int64_t ldz,
+                          float* state, int state_in, float* y, int64_t ldy, void* stream);
+
 /* ---- gated-norm + Hadamard + quant ------------------------------------------------ */
 /* out[m,:] = clamp(rint(H_blk (y*rsqrt(mean y^2+eps)*gamma) / s_y)); hadamard=0 skips H. */
 int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* gamma, float eps, float s_y,

@@ -63,6 +63,8 @@ _SIGS = {
                          _vp, _int, _vp, _i64, _vp], _int),
     "sq_selective_scan_int8": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                                 _vp, _int, _vp, _i64, _vp], _int),
+    "sq_selective_scan_f32": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
+                                _vp, _int, _vp, _i64, _vp], _int),
     "sq_mamba2_decode_ws_bytes": ([C.POINTER(Mamba2DecodeParams), _int], _i64),
     "sq_set_decode_stages": ([_int], _int),
     "sq_mamba2_decode_step_int8": ([C.POINTER(Mamba2DecodeParams), _int, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp,

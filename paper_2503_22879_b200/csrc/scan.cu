@@ -191,6 +191,47 @@ __global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, in
   for (int n = 0; n < N; ++n) st[n] = quant8(hs[n], sh);
 }
 
+// Mamba1 W4A16 (float) scan: the same recurrence on f32 operands and an f32 state
+// (oracle/ssm_block.py selective_scan, Mamba1 branch).  dt is the raw
+// dt_proj output; B|C come from the x_proj output row (C at +N).
+template <int N>
+__global__ void __launch_bounds__(128) mamba1_scan_f32_kernel(sq_mamba1_params p, int B, int T,
+                                                             const float* __restrict__ x, int64_t ldx,
+                                                             const float* __restrict__ dt, int64_t lddt,
+                                                             const float* __restrict__ BC, int64_t ldbc,
+                                                             const float* __restrict__ z, int64_t ldz,
+                                                             float* __restrict__ state, int state_in,
+                                                             float* __restrict__ y, int64_t ldy) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (c >= p.d_inner) return;
+  const float Dc = p.D[c], dtb = p.dt_bias[c];
+  float A[N], hs[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) A[n] = p.A[c * N + n];
+  float* st = state + ((int64_t)b * p.d_inner + c) * N;
+#pragma unroll
+  for (int n = 0; n < N; ++n) hs[n] = state_in ? st[n] : 0.f;
+  for (int t = 0; t < T; ++t) {
+    const int64_t tok = (int64_t)b * T + t;
+    const float delta = softplus_f(__fadd_rn(dt[tok * lddt + c], dtb));
+    const float xv = x[tok * ldx + c];
+    const float dtx = __fmul_rn(delta, xv);
+    const float* bc = BC + tok * ldbc;
+    float acc = 0.f;
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const float dA = expf(__fmul_rn(delta, A[n]));
+      hs[n] = __fadd_rn(__fmul_rn(dA, hs[n]), __fmul_rn(dtx, bc[n]));
+      acc = fmaf(hs[n], bc[N + n], acc);
+    }
+    const float yv = __fadd_rn(acc, __fmul_rn(Dc, xv));
+    y[tok * ldy + c] = __fmul_rn(yv, silu_f(z[tok * ldz + c]));
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) st[n] = hs[n];
+}
+
 // ---------------------------------------------------------------------------------
 // K9 decode: Mamba2 int8 state update, HBM-streaming version.
 // CTA = (sequence, 4 consecutive heads), 256 threads; thread t owns the 16-column
@@ -477,4 +518,16 @@ extern "C" int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T, c
   mamba1_scan_kernel<16><<<grid, 128, 0, as_stream(stream)>>>(*p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz, state,
                                                               state_in, y, ldy);
   return check_launch("sq_selective_scan_int8");
+}
+
+extern "C" int sq_selective_scan_f32(const sq_mamba1_params* p, int B, int T, const float* x, int64_t ldx,
+                                     const float* dt, int64_t lddt, const float* BC, int64_t ldbc, const float* z,
+                                     int64_t ldz, float* state, int state_in, float* y, int64_t ldy, void* stream) {
+  SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_selective_scan_f32: bad args");
+  SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan_f32: d_state must be 16 (got %d)", p->d_state);
+  if (B == 0 || T == 0) return SQ_OK;
+  dim3 grid((p->d_inner + 127) / 128, B);
+  mamba1_scan_f32_kernel<16><<<grid, 128, 0, as_stream(stream)>>>(*p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz,
+                                                                  state, state_in, y, ldy);
+  return check_launch("sq_selective_scan_f32");
 }

@@ -32,7 +32,7 @@ namespace sq {
 
 constexpr int SC_Q = 64;       // chunk length
 constexpr int SC_P = 64;       // head_dim
-constexpr int SC_THREADS = 128;
+constexpr int SC_THREADS = 256;   // 8 warps: (row group w = warp & 3) x (state half nh = warp >> 2)
 
 __device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm(
@@ -112,18 +112,21 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
                      int64_t ldbc, const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
                      int8_t* __restrict__ state, int state_in, float* __restrict__ y, int64_t ldy) {
   using S = ScSmem<N>;
-  constexpr int NT = N / 8;               // n-tiles of the state (8 columns each)
+  constexpr int NTH = N / 16;             // n-tiles (8 columns) of this warp's state half
   extern __shared__ __align__(16) uint8_t smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
   const int h = blockIdx.x, b = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int w = warp & 3, nh = warp >> 2;    // rows p (and t for C·Bᵀ) 16w..16w+15; state columns half nh
   const int g4 = lane >> 2, t4 = lane & 3;   // fragment row / column-pair indices
+  const int mi = lane >> 3, r8 = lane & 7;   // ldmatrix: matrix index / row within it
   const int grp = p.head_group[h];
   const float A = p.A[h], Dh = p.D[h], dtb = p.dt_bias[h];
   const float sB = p.s_B[grp], sC = p.s_C[grp];
   const float sBC = __fmul_rn(sB, sC);
   const int ch0 = h * SC_P;
   const int64_t tok0 = (int64_t)b * T;
+  const int n0 = nh * (N / 2);               // first state column of this warp
 
   // async fetch of one chunk's codes into raw buffer `buf` (rows past T zero-filled)
   auto fetch = [&](int c0, int buf) {
@@ -145,15 +148,14 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
   };
   fetch(0, 0);
 
-  // this warp's 16 state rows p = 16*warp + {g4, g4+8}; H fragments over all N columns
-  const int pr0 = 16 * warp + g4, pr1 = pr0 + 8;
+  const int pr0 = 16 * w + g4, pr1 = pr0 + 8;
   const float sx0 = p.s_x[ch0 + pr0], sx1 = p.s_x[ch0 + pr1];
   const float sh0 = p.s_h[ch0 + pr0], sh1 = p.s_h[ch0 + pr1];
-  float H[NT][4];
+  float H[NTH][4];   // this warp's slice: rows pr0 / pr1, columns n0 + 8j + 2t4 (+1)
   int8_t* st = state + ((int64_t)b * p.n_heads + h) * SC_P * N;
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    const int n = 8 * j + 2 * t4;
+  for (int j = 0; j < NTH; ++j) {
+    const int n = n0 + 8 * j + 2 * t4;
     if (state_in) {
       H[j][0] = __fmul_rn((float)st[pr0 * N + n], sh0);
       H[j][1] = __fmul_rn((float)st[pr0 * N + n + 1], sh0);
@@ -185,32 +187,26 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
       }
       sm.dlt[tid] = dl;
       sm.cs[tid] = dA_log;
-      const int tn = c0 + SC_Q + tid;
-      dcode = dt[(tok0 + min(tn, T - 1)) * lddt + h];
+      dcode = dt[(tok0 + min(c0 + SC_Q + tid, T - 1)) * lddt + h];
     }
-    // widen this chunk's x / B / C codes to fp16 tiles
-    for (int i = tid; i < SC_Q * (N / 16); i += SC_THREADS) {
-      const int r = i / (N / 16), c16 = (i % (N / 16)) * 16;
-      const uint4 bv = *reinterpret_cast<const uint4*>(&R.B[r][c16]);
-      const uint4 cv = *reinterpret_cast<const uint4*>(&R.C[r][c16]);
-      uint4 o0, o1;
-      s8x4_h2x2(bv.x, o0.x, o0.y); s8x4_h2x2(bv.y, o0.z, o0.w);
-      s8x4_h2x2(bv.z, o1.x, o1.y); s8x4_h2x2(bv.w, o1.z, o1.w);
-      *reinterpret_cast<uint4*>(&sm.Bh[r][c16]) = o0;
-      *reinterpret_cast<uint4*>(&sm.Bh[r][c16 + 8]) = o1;
-      s8x4_h2x2(cv.x, o0.x, o0.y); s8x4_h2x2(cv.y, o0.z, o0.w);
-      s8x4_h2x2(cv.z, o1.x, o1.y); s8x4_h2x2(cv.w, o1.z, o1.w);
-      *reinterpret_cast<uint4*>(&sm.Ch[r][c16]) = o0;
-      *reinterpret_cast<uint4*>(&sm.Ch[r][c16 + 8]) = o1;
+    // widen this chunk's x / B / C codes to fp16 tiles: 8 codes (8 B) -> 8 halves (16 B) per
+    // thread, consecutive threads on consecutive 16 B (conflict-free stores)
+    for (int i = tid; i < SC_Q * (N / 8); i += SC_THREADS) {
+      const int r = i / (N / 8), c8 = (i % (N / 8)) * 8;
+      const uint2 bv = *reinterpret_cast<const uint2*>(&R.B[r][c8]);
+      const uint2 cv = *reinterpret_cast<const uint2*>(&R.C[r][c8]);
+      uint4 o;
+      s8x4_h2x2(bv.x, o.x, o.y); s8x4_h2x2(bv.y, o.z, o.w);
+      *reinterpret_cast<uint4*>(&sm.Bh[r][c8]) = o;
+      s8x4_h2x2(cv.x, o.x, o.y); s8x4_h2x2(cv.y, o.z, o.w);
+      *reinterpret_cast<uint4*>(&sm.Ch[r][c8]) = o;
     }
-    for (int i = tid; i < SC_Q * (SC_P / 16); i += SC_THREADS) {
-      const int r = i / (SC_P / 16), c16 = (i % (SC_P / 16)) * 16;
-      const uint4 xv = *reinterpret_cast<const uint4*>(&R.X[r][c16]);
-      uint4 o0, o1;
-      s8x4_h2x2(xv.x, o0.x, o0.y); s8x4_h2x2(xv.y, o0.z, o0.w);
-      s8x4_h2x2(xv.z, o1.x, o1.y); s8x4_h2x2(xv.w, o1.z, o1.w);
-      *reinterpret_cast<uint4*>(&sm.Xh[r][c16]) = o0;
-      *reinterpret_cast<uint4*>(&sm.Xh[r][c16 + 8]) = o1;
+    for (int i = tid; i < SC_Q * (SC_P / 8); i += SC_THREADS) {
+      const int r = i / (SC_P / 8), c8 = (i % (SC_P / 8)) * 8;
+      const uint2 xv = *reinterpret_cast<const uint2*>(&R.X[r][c8]);
+      uint4 o;
+      s8x4_h2x2(xv.x, o.x, o.y); s8x4_h2x2(xv.y, o.z, o.w);
+      *reinterpret_cast<uint4*>(&sm.Xh[r][c8]) = o;
     }
     __syncthreads();   // dlt / cs / fp16 tiles visible
     if (warp == 0) {   // inclusive prefix sum of Δ·A over the chunk (sequential order, f32)
@@ -234,11 +230,11 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
       sm.et[lane] = __fmul_rn(__expf(v0), sC);
       sm.et[lane + 32] = __fmul_rn(__expf(v1), sC);
     }
-    // ---------------- CB = C · Bᵀ (int8, exact), rows t = 16*warp + {g4, g4+8}, all s
-    const int tr0 = 16 * warp + g4, tr1 = tr0 + 8;
-    int cb[SC_Q / 8][4];
+    // ---------------- CB = C · Bᵀ (int8, exact): rows t = 16w + {g4, g4+8}, s-tiles 4nh..4nh+3
+    const int tr0 = 16 * w + g4, tr1 = tr0 + 8;
+    int cb[4][4];
 #pragma unroll
-    for (int j = 0; j < SC_Q / 8; ++j) cb[j][0] = cb[j][1] = cb[j][2] = cb[j][3] = 0;
+    for (int j = 0; j < 4; ++j) cb[j][0] = cb[j][1] = cb[j][2] = cb[j][3] = 0;
 #pragma unroll
     for (int kk = 0; kk < N / 32; ++kk) {
       uint32_t a[4];
@@ -247,20 +243,23 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
       a[2] = *reinterpret_cast<const uint32_t*>(&R.C[tr0][32 * kk + 16 + 4 * t4]);
       a[3] = *reinterpret_cast<const uint32_t*>(&R.C[tr1][32 * kk + 16 + 4 * t4]);
 #pragma unroll
-      for (int j = 0; j < SC_Q / 8; ++j)
-        if (j <= 2 * warp + 1)   // s-tiles past this warp's last row are causally masked
-          mma_i8(cb[j], a, *reinterpret_cast<const uint32_t*>(&R.B[8 * j + g4][32 * kk + 4 * t4]),
-                 *reinterpret_cast<const uint32_t*>(&R.B[8 * j + g4][32 * kk + 16 + 4 * t4]));
+      for (int j = 0; j < 4; ++j) {
+        const int jg = 4 * nh + j;
+        if (jg <= 2 * w + 1)   // s-tiles past this warp's last row are causally masked
+          mma_i8(cb[j], a, *reinterpret_cast<const uint32_t*>(&R.B[8 * jg + g4][32 * kk + 4 * t4]),
+                 *reinterpret_cast<const uint32_t*>(&R.B[8 * jg + g4][32 * kk + 16 + 4 * t4]));
+      }
     }
     __syncthreads();   // cs / wgt / et visible
     // ---------------- W = CB s_B s_C e^{cs_t - cs_s} Δ_s (causal) -> fp16 tile [t][s]
     {
       const float cst0 = sm.cs[tr0], cst1 = sm.cs[tr1];
 #pragma unroll
-      for (int j = 0; j < SC_Q / 8; ++j) {
-        const int s0 = 8 * j + 2 * t4, s1 = s0 + 1;
+      for (int j = 0; j < 4; ++j) {
+        const int jg = 4 * nh + j;
+        const int s0 = 8 * jg + 2 * t4, s1 = s0 + 1;
         uint32_t wv0 = 0, wv1 = 0;
-        if (j <= 2 * warp + 1) {
+        if (jg <= 2 * w + 1) {
           const float css0 = sm.cs[s0], css1 = sm.cs[s1], d0 = sm.dlt[s0], d1 = sm.dlt[s1];
           float w00 = __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][0], sBC), __expf(cst0 - css0)), d0);
           float w01 = __fmul_rn(__fmul_rn(__fmul_rn((float)cb[j][1], sBC), __expf(cst0 - css1)), d1);
@@ -277,68 +276,97 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
         *reinterpret_cast<uint32_t*>(&sm.Wh[tr1][s0]) = wv1;
       }
     }
-    // X̂ᵀ A fragments (rows p of this warp, k = s), reused by Y_diag, the D term and the H update
+    // X̂ᵀ A fragments (rows p of this warp's group, k = s): Y_diag, the D term and the H update
     uint32_t xa[SC_Q / 16][4];
-    {
-      const int mi = lane >> 3, r = lane & 7;
 #pragma unroll
-      for (int kk = 0; kk < SC_Q / 16; ++kk)
-        ldsm_x4_t(xa[kk], &sm.Xh[16 * kk + (mi >> 1) * 8 + r][16 * warp + (mi & 1) * 8]);
-    }
+    for (int kk = 0; kk < SC_Q / 16; ++kk)
+      ldsm_x4_t(xa[kk], &sm.Xh[16 * kk + (mi >> 1) * 8 + r8][16 * w + (mi & 1) * 8]);
     __syncthreads();   // W visible
-    // ---------------- Yᵀ = X̂ᵀ Wᵀ  and  H Ĉᵀ   (f32 accumulators, rows p, cols t)
-    float yd[SC_Q / 8][4], yo[SC_Q / 8][4];
+    // ---------------- Yᵀ: Y_diag for t-tiles 4nh..4nh+3, Y_off partial over this warp's n half
+    float yd[4][4], yo[SC_Q / 8][4];
 #pragma unroll
-    for (int j = 0; j < SC_Q / 8; ++j) {
-      yd[j][0] = yd[j][1] = yd[j][2] = yd[j][3] = 0.f;
-      yo[j][0] = yo[j][1] = yo[j][2] = yo[j][3] = 0.f;
-    }
-    {
-      const int mi = lane >> 3, r = lane & 7;
+    for (int j = 0; j < 4; ++j) yd[j][0] = yd[j][1] = yd[j][2] = yd[j][3] = 0.f;
 #pragma unroll
-      for (int kk = 0; kk < SC_Q / 16; ++kk) {
+    for (int j = 0; j < SC_Q / 8; ++j) yo[j][0] = yo[j][1] = yo[j][2] = yo[j][3] = 0.f;
 #pragma unroll
-        for (int j = 0; j < SC_Q / 8; j += 2) {
-          if (kk > j / 2) continue;   // W[t][s] = 0 for s > t: t-tiles j, j+1 need s < 8j + 16
-          uint32_t bw[4];   // b0,b1 of t-tile j, then of t-tile j+1
-          ldsm_x4(bw, &sm.Wh[8 * (j + (mi >> 1)) + r][16 * kk + (mi & 1) * 8]);
-          mma_f16(yd[j], xa[kk], bw[0], bw[1]);
-          mma_f16(yd[j + 1], xa[kk], bw[2], bw[3]);
-        }
-      }
+    for (int kk = 0; kk < SC_Q / 16; ++kk) {
 #pragma unroll
-      for (int kk = 0; kk < N / 16; ++kk) {
-        const uint32_t ha[4] = {h2(H[2 * kk][0], H[2 * kk][1]), h2(H[2 * kk][2], H[2 * kk][3]),
-                                h2(H[2 * kk + 1][0], H[2 * kk + 1][1]), h2(H[2 * kk + 1][2], H[2 * kk + 1][3])};
-#pragma unroll
-        for (int j = 0; j < SC_Q / 8; j += 2) {
-          uint32_t bc[4];
-          ldsm_x4(bc, &sm.Ch[8 * (j + (mi >> 1)) + r][16 * kk + (mi & 1) * 8]);
-          mma_f16(yo[j], ha, bc[0], bc[1]);
-          mma_f16(yo[j + 1], ha, bc[2], bc[3]);
-        }
+      for (int j = 0; j < 4; j += 2) {
+        const int jg = 4 * nh + j;
+        if (kk > jg / 2) continue;   // W[t][s] = 0 for s > t: t-tiles jg, jg+1 need s < 8jg + 16
+        uint32_t bw[4];   // b0,b1 of t-tile jg, then of t-tile jg+1
+        ldsm_x4(bw, &sm.Wh[8 * (jg + (mi >> 1)) + r8][16 * kk + (mi & 1) * 8]);
+        mma_f16(yd[j], xa[kk], bw[0], bw[1]);
+        mma_f16(yd[j + 1], xa[kk], bw[2], bw[3]);
       }
     }
-    // ---------------- epilogue: pre-gate y staged as [t][p] in smem (over the X / W tiles),
-    // then SiLU(ẑ) gating and coalesced 16-byte stores
+#pragma unroll
+    for (int kk = 0; kk < NTH / 2; ++kk) {
+      const uint32_t ha[4] = {h2(H[2 * kk][0], H[2 * kk][1]), h2(H[2 * kk][2], H[2 * kk][3]),
+                              h2(H[2 * kk + 1][0], H[2 * kk + 1][1]), h2(H[2 * kk + 1][2], H[2 * kk + 1][3])};
+#pragma unroll
+      for (int j = 0; j < SC_Q / 8; j += 2) {
+        uint32_t bc[4];
+        ldsm_x4(bc, &sm.Ch[8 * (j + (mi >> 1)) + r8][n0 + 16 * kk + (mi & 1) * 8]);
+        mma_f16(yo[j], ha, bc[0], bc[1]);
+        mma_f16(yo[j + 1], ha, bc[2], bc[3]);
+      }
+    }
+    // ---------------- epilogue: y[t][p] assembled in smem (over the X / W tiles) in a fixed
+    // order — (Y_diag·s_x + (Y_off[n half 0] + Y_off[n half 1])·e^{cs_t} s_C) + D x̂ — then
+    // SiLU(ẑ) gating and coalesced 16-byte stores
     __syncthreads();   // every warp done reading Xh / Wh
+    if (nh == 1) {
 #pragma unroll
-    for (int j = 0; j < SC_Q / 8; ++j) {
+      for (int j = 0; j < SC_Q / 8; ++j) {
+        const int t = 8 * j + 2 * t4;
+        sm.Ys[t][pr0] = yo[j][0];
+        sm.Ys[t + 1][pr0] = yo[j][1];
+        sm.Ys[t][pr1] = yo[j][2];
+        sm.Ys[t + 1][pr1] = yo[j][3];
+      }
+    }
+    __syncthreads();
+    auto finish = [&](int j, int jl, float o0, float o1, float o2, float o3) {
       // x codes at (p, t) from the X̂ᵀ fragments: t-tile j = k-step j/2, half j&1
       const float2 xc0 = f2(xa[j >> 1][(j & 1) * 2]), xc1 = f2(xa[j >> 1][(j & 1) * 2 + 1]);
       const int t = 8 * j + 2 * t4;
       const float e0 = sm.et[t], e1 = sm.et[t + 1];
-      sm.Ys[t][pr0] = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][0], sx0), __fmul_rn(yo[j][0], e0)), __fmul_rn(Dh, __fmul_rn(xc0.x, sx0)));
-      sm.Ys[t + 1][pr0] = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][1], sx0), __fmul_rn(yo[j][1], e1)), __fmul_rn(Dh, __fmul_rn(xc0.y, sx0)));
-      sm.Ys[t][pr1] = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][2], sx1), __fmul_rn(yo[j][2], e0)), __fmul_rn(Dh, __fmul_rn(xc1.x, sx1)));
-      sm.Ys[t + 1][pr1] = __fadd_rn(__fadd_rn(__fmul_rn(yd[j][3], sx1), __fmul_rn(yo[j][3], e1)), __fmul_rn(Dh, __fmul_rn(xc1.y, sx1)));
+      sm.Ys[t][pr0] = __fadd_rn(__fadd_rn(__fmul_rn(yd[jl][0], sx0), __fmul_rn(o0, e0)), __fmul_rn(Dh, __fmul_rn(xc0.x, sx0)));
+      sm.Ys[t + 1][pr0] = __fadd_rn(__fadd_rn(__fmul_rn(yd[jl][1], sx0), __fmul_rn(o1, e1)), __fmul_rn(Dh, __fmul_rn(xc0.y, sx0)));
+      sm.Ys[t][pr1] = __fadd_rn(__fadd_rn(__fmul_rn(yd[jl][2], sx1), __fmul_rn(o2, e0)), __fmul_rn(Dh, __fmul_rn(xc1.x, sx1)));
+      sm.Ys[t + 1][pr1] = __fadd_rn(__fadd_rn(__fmul_rn(yd[jl][3], sx1), __fmul_rn(o3, e1)), __fmul_rn(Dh, __fmul_rn(xc1.y, sx1)));
+    };
+    if (nh == 0) {
+#pragma unroll
+      for (int j = 0; j < SC_Q / 8; ++j) {
+        const int t = 8 * j + 2 * t4;
+        const float o0 = __fadd_rn(yo[j][0], sm.Ys[t][pr0]), o1 = __fadd_rn(yo[j][1], sm.Ys[t + 1][pr0]);
+        const float o2 = __fadd_rn(yo[j][2], sm.Ys[t][pr1]), o3 = __fadd_rn(yo[j][3], sm.Ys[t + 1][pr1]);
+        if (j < 4) {
+          finish(j, j, o0, o1, o2, o3);
+        } else {   // the other half's t-tiles: leave the summed Y_off for it
+          sm.Ys[t][pr0] = o0;
+          sm.Ys[t + 1][pr0] = o1;
+          sm.Ys[t][pr1] = o2;
+          sm.Ys[t + 1][pr1] = o3;
+        }
+      }
+    }
+    __syncthreads();
+    if (nh == 1) {
+#pragma unroll
+      for (int j = 4; j < SC_Q / 8; ++j) {
+        const int t = 8 * j + 2 * t4;
+        finish(j, j - 4, sm.Ys[t][pr0], sm.Ys[t + 1][pr0], sm.Ys[t][pr1], sm.Ys[t + 1][pr1]);
+      }
     }
     __syncthreads();
     {
       const int p4 = (tid & 15) * 4;
 #pragma unroll
-      for (int i = 0; i < SC_Q / 8; ++i) {
-        const int t = (tid >> 4) + 8 * i;
+      for (int i = 0; i < SC_Q / 16; ++i) {
+        const int t = (tid >> 4) + 16 * i;
         if (t < Qc) {
           const float4 v = *reinterpret_cast<const float4*>(&sm.Ys[t][p4]);
           const uint32_t zc = *reinterpret_cast<const uint32_t*>(&R.Z[t][p4]);
@@ -354,53 +382,50 @@ __global__ void __launch_bounds__(SC_THREADS, 2)
     // ---------------- H = e^{cs_Q} H + Σ_s w_s s_x s_B x_s ⊗ B_s   (fp16 hi + lo split of the weights)
     const float eQ = expf(sm.cs[SC_Q - 1]);   // padded tokens carry Δ = 0
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
+    for (int j = 0; j < NTH; ++j) {
       H[j][0] = __fmul_rn(H[j][0], eQ);
       H[j][1] = __fmul_rn(H[j][1], eQ);
       H[j][2] = __fmul_rn(H[j][2], eQ);
       H[j][3] = __fmul_rn(H[j][3], eQ);
     }
-    {
-      const int mi = lane >> 3, r = lane & 7;
 #pragma unroll
-      for (int kk = 0; kk < SC_Q / 16; ++kk) {
-        uint32_t ahi[4], alo[4];
+    for (int kk = 0; kk < SC_Q / 16; ++kk) {
+      uint32_t ahi[4], alo[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {   // a0 (row g, k 2t), a1 (row g+8, k 2t), a2 (row g, k 2t+8), a3 (row g+8, k 2t+8)
-          const int s = 16 * kk + ((q & 2) ? 8 : 0) + 2 * t4;
-          const float fr = (q & 1) ? f1 : f0;
-          const float2 xc = f2(xa[kk][q]);
-          const float v0 = __fmul_rn(__fmul_rn(sm.wgt[s], xc.x), fr);
-          const float v1 = __fmul_rn(__fmul_rn(sm.wgt[s + 1], xc.y), fr);
-          const __half2 hi = __floats2half2_rn(v0, v1);
-          const float2 hf = __half22float2(hi);
-          const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
-          ahi[q] = *reinterpret_cast<const uint32_t*>(&hi);
-          alo[q] = *reinterpret_cast<const uint32_t*>(&lo);
-        }
-        // hi pass over every n-tile, then lo pass: dependent MMAs on one H tile are NT apart
+      for (int q = 0; q < 4; ++q) {   // a0 (row g, k 2t), a1 (row g+8, k 2t), a2 (row g, k 2t+8), a3 (row g+8, k 2t+8)
+        const int s = 16 * kk + ((q & 2) ? 8 : 0) + 2 * t4;
+        const float fr = (q & 1) ? f1 : f0;
+        const float2 xc = f2(xa[kk][q]);
+        const float v0 = __fmul_rn(__fmul_rn(sm.wgt[s], xc.x), fr);
+        const float v1 = __fmul_rn(__fmul_rn(sm.wgt[s + 1], xc.y), fr);
+        const __half2 hi = __floats2half2_rn(v0, v1);
+        const float2 hf = __half22float2(hi);
+        const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+        ahi[q] = *reinterpret_cast<const uint32_t*>(&hi);
+        alo[q] = *reinterpret_cast<const uint32_t*>(&lo);
+      }
+      // hi pass over this half's n-tiles, then lo pass: dependent MMAs on one H tile are NTH apart
 #pragma unroll
-        for (int j = 0; j < NT; j += 2) {
-          uint32_t bb[4];   // b0,b1 of n-tile j, then of n-tile j+1 (stored [s][n] -> .trans)
-          ldsm_x4_t(bb, &sm.Bh[16 * kk + (mi & 1) * 8 + r][8 * (j + (mi >> 1))]);
-          mma_f16(H[j], ahi, bb[0], bb[1]);
-          mma_f16(H[j + 1], ahi, bb[2], bb[3]);
-        }
+      for (int j = 0; j < NTH; j += 2) {
+        uint32_t bb[4];   // b0,b1 of n-tile j, then of n-tile j+1 (stored [s][n] -> .trans)
+        ldsm_x4_t(bb, &sm.Bh[16 * kk + (mi & 1) * 8 + r8][n0 + 8 * (j + (mi >> 1))]);
+        mma_f16(H[j], ahi, bb[0], bb[1]);
+        mma_f16(H[j + 1], ahi, bb[2], bb[3]);
+      }
 #pragma unroll
-        for (int j = 0; j < NT; j += 2) {
-          uint32_t bb[4];
-          ldsm_x4_t(bb, &sm.Bh[16 * kk + (mi & 1) * 8 + r][8 * (j + (mi >> 1))]);
-          mma_f16(H[j], alo, bb[0], bb[1]);
-          mma_f16(H[j + 1], alo, bb[2], bb[3]);
-        }
+      for (int j = 0; j < NTH; j += 2) {
+        uint32_t bb[4];
+        ldsm_x4_t(bb, &sm.Bh[16 * kk + (mi & 1) * 8 + r8][n0 + 8 * (j + (mi >> 1))]);
+        mma_f16(H[j], alo, bb[0], bb[1]);
+        mma_f16(H[j + 1], alo, bb[2], bb[3]);
       }
     }
   }
   cp_async_wait_all();
   // ---------------- final state -> int8 codes (ClusterMap-cell scales)
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    const int n = 8 * j + 2 * t4;
+  for (int j = 0; j < NTH; ++j) {
+    const int n = n0 + 8 * j + 2 * t4;
     st[pr0 * N + n] = quant8(H[j][0], sh0);
     st[pr0 * N + n + 1] = quant8(H[j][1], sh0);
     st[pr1 * N + n] = quant8(H[j][2], sh1);

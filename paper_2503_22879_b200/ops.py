@@ -331,6 +331,17 @@ def selective_scan_int8(p, B, T, x, dt, BC, z, state, state_in, y):
     return y
 
 
+def selective_scan_f32(p, B, T, x, dt, BC, z, state, state_in, y):
+    """Mamba1 W4A16 scan (float operands, f32 state)."""
+    for n, t in (("x", x), ("dt", dt), ("BC", BC), ("z", z), ("y", y)):
+        _dev(t, torch.float32, n, 2)
+    _dev(state, torch.float32, "state")
+    _check(lib().sq_selective_scan_f32(C.byref(p), B, T, x.data_ptr(), _ld(x), dt.data_ptr(), _ld(dt),
+                                       BC.data_ptr(), _ld(BC), z.data_ptr(), _ld(z), state.data_ptr(),
+                                       int(bool(state_in)), y.data_ptr(), _ld(y), _stream()))
+    return y
+
+
 def set_decode_stages(mask: int):
     """Profiling control: launches issued by mamba2_decode_step_int8 (1 conv | 2 state | 4 norm)."""
     _check(lib().sq_set_decode_stages(int(mask)))

@@ -268,7 +268,13 @@ class DeviceBlock:
                 self.params = ops.mamba2_params(d.n_heads, d.head_dim, d.d_state, d.n_state_groups,
                                                 self.head_group, self.A, self.D, self.dt_bias)
             else:
-                raise NotImplementedError("W4A16 Mamba1 blocks are not on the GPU path yet")
+                # float operands: the scan kernel takes raw dt_proj outputs and x_proj B|C rows
+                self.x_proj = DeviceLinear(qb.x_proj, dev)
+                self.dt_proj = DeviceLinear(qb.dt_proj, dev)
+                ones = f(np.ones(d.d_inner, np.float32))
+                self._ones = ones
+                self.params = ops.mamba1_params(d.d_inner, d.d_state, self.A, self.D, self.dt_bias, 1.0, 1.0, 1.0,
+                                                1.0, ones, ones)
 
     # ------------------------------------------------------------------ state
     def new_state(self, batch: int, dev="cuda"):
@@ -282,7 +288,7 @@ class DeviceBlock:
     @property
     def weight_bytes(self):
         n = self.in_proj.nbytes + self.out_proj.nbytes
-        if self.dims.variant == "mamba1" and self.a8:
+        if self.dims.variant == "mamba1":
             n += self.x_proj.nbytes + self.dt_proj.nbytes
         return n
 
@@ -340,9 +346,23 @@ class DeviceBlock:
         """W4A16 float path on f32 input u [B*T × d_model]."""
         d = self.dims
         di = d.d_inner
-        gn = d.n_state_groups * d.d_state
         ws = ws if ws is not None else {}
         zx = self.in_proj.a16(u, ws.get("zxf"))
+        if d.variant == "mamba1":   # in_proj rows z | x; x_proj rows Δ_low | B | C (LEDGER G4)
+            R = d.dt_rank
+            cv = ops.conv1d_f32(zx[:, di:], self.conv_w, self.conv_b, B, T, state.conv_cache, state_in,
+                                ws.get("convf"))
+            xd = self.x_proj.a16(cv)
+            dtr = self.dt_proj.a16(xd[:, :R])
+            y = ws.get("y")
+            if y is None:
+                y = torch.empty((B * T, di), dtype=torch.float32, device=u.device)
+            ops.selective_scan_f32(self.params, B, T, cv, dtr, xd[:, R:], zx[:, :di], state.h, state_in, y)
+            r = ops.rmsnorm_f32(y, self.norm_w, EPS_NORM, ws.get("r"))
+            if resid is not None:
+                return self.out_proj.a16(r, resid, resid=True)
+            return self.out_proj.a16(r, ws.get("out"))
+        gn = d.n_state_groups * d.d_state
         xbc = zx[:, di:2 * di + 2 * gn]
         cv = ops.conv1d_f32(xbc, self.conv_w, self.conv_b, B, T, state.conv_cache, state_in, ws.get("convf"))
         y = ws.get("y")

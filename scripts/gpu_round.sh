@@ -17,4 +17,12 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm
   -o gpurun_out/prof_gemm -f python scripts/prof_kernels.py gemm > gpurun_out/ncu_gemm.log 2>&1
 timeout 300 python scripts/bench_decode_kernels.py > gpurun_out/bdk.log 2>&1
 bash scripts/bench_stages.sh > gpurun_out/stages.log 2>&1
+# prefill (configs[1]): bench line, launch list, per-kernel timing, ncu of the chunk scan / conv / norm / GEMM
+timeout 900 python bench.py --workload prefill27b --steps 3 > gpurun_out/bench_prefill.json 2> gpurun_out/bench_prefill.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+  --log-file gpurun_out/launches_prefill.csv python bench.py --workload prefill27b --steps 1 --warmup 3 \
+  --no-cpu-baseline > gpurun_out/ncu_launch_pf.log 2>&1
+timeout 300 python scripts/prof_prefill.py all 5 > gpurun_out/prefill_kernels.txt 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssd_chunk|conv1d_prefill|gate_norm" -c 3 \
+  -o gpurun_out/prof_prefill -f python scripts/prof_prefill.py all 1 > gpurun_out/ncu_pf.log 2>&1
 echo done

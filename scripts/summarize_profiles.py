@@ -84,4 +84,13 @@ if __name__ == "__main__":
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
     launches(tag)
+    launches(tag, "launches_prefill.csv", "launches_prefill")
     ncu_reports(tag)
+    for src, dst in (("bench.json", "bench.json"), ("bench_ref.json", "bench_ref.json"),
+                     ("bench_prefill.json", "bench_prefill.json"), ("pytest_gpu.log", "pytest_gpu.txt"),
+                     ("bdk.log", "decode_kernels.txt"), ("stages.log", "decode_stages.txt"),
+                     ("prefill_kernels.txt", "prefill_kernels.txt"), ("smoke.log", "smoke.txt")):
+        p = os.path.join(OUT, src)
+        if os.path.exists(p):
+            open(os.path.join(PROF, f"{tag}_{dst}"), "w").write(open(p).read())
+            print(f"copied profiles/{tag}_{dst}")

@@ -202,7 +202,7 @@ def _tiny_block(profile, variant="mamba2", seed=0):
 
 
 @pytest.mark.parametrize("profile,variant", [("W8A8", "mamba2"), ("W4A8", "mamba2"), ("W4A16", "mamba2"),
-                                             ("W8A8", "mamba1"), ("W4A8", "mamba1")])
+                                             ("W8A8", "mamba1"), ("W4A8", "mamba1"), ("W4A16", "mamba1")])
 def test_block_forward_quantized(cuda, profile, variant):
     from paper_2503_22879_b200.ssm_block import block_forward_quantized, DeviceBlock
     d, qb, u = _tiny_block(profile, variant)
@@ -219,13 +219,19 @@ def test_block_forward_quantized(cuda, profile, variant):
         assert mx <= 1 and frac < 2e-2
         cc = st.conv_cache.cpu().numpy()[0].T
         assert np.array_equal(cc, rst.conv)
+    else:   # float state and conv cache
+        h = st.h.cpu().numpy().reshape(rst.h.shape)
+        assert np.abs(h - rst.h).max() <= 1e-3 * np.abs(rst.h).max() + 1e-6
+        cc = st.conv_cache.cpu().numpy()[0].T   # conv inputs = in_proj outputs (GEMV vs BLAS order)
+        assert np.abs(cc - rst.conv).max() <= 1e-4 * np.abs(rst.conv).max()
 
 
-@pytest.mark.parametrize("profile", ["W8A8", "W4A8", "W4A16"])
-def test_decode_matches_oracle_steps(cuda, profile):
-    """Prefill 48 tokens then 16 single-token decode steps (int8 cached state)."""
+@pytest.mark.parametrize("profile,variant", [("W8A8", "mamba2"), ("W4A8", "mamba2"), ("W4A16", "mamba2"),
+                                             ("W4A16", "mamba1")])
+def test_decode_matches_oracle_steps(cuda, profile, variant):
+    """Prefill 48 tokens then 16 single-token decode steps (cached state)."""
     from paper_2503_22879_b200.ssm_block import block_forward_quantized, DeviceBlock
-    d, qb, u = _tiny_block(profile)
+    d, qb, u = _tiny_block(profile, variant)
     blk = DeviceBlock(qb, cuda)
     _, ost = oq.block_forward_quantized(u[:48], qb)
     _, gst = block_forward_quantized(torch.as_tensor(u[:48], device=cuda), blk)

@@ -21,7 +21,7 @@ def _tiny_model(profile, n_layers=2, variant="mamba2"):
 
 
 @pytest.mark.parametrize("profile,variant", [("W8A8", "mamba2"), ("W4A8", "mamba2"), ("W4A16", "mamba2"),
-                                             ("W8A8", "mamba1")])
+                                             ("W8A8", "mamba1"), ("W4A16", "mamba1")])
 def test_model_prefill_logits(cuda, profile, variant):
     from paper_2503_22879_b200.model import QuantizedMambaLM
     fm, toks, qm = _tiny_model(profile, variant=variant)
