@@ -88,30 +88,30 @@ __device__ __forceinline__ int8_t conv_step(const sq_mamba2_decode_params& P, in
   return quant8(silu_f(acc), P.conv_s_out[c]);
 }
 
-// Four consecutive channels c..c+3 with Kc = 4: every load issued up front (3 cache
-// words, the new codes, 4x4 taps, bias / scales as float4), the same per-channel op order
-// (acc = b + Σ_j w_j·(q_j·s_in), IEEE RN each) computed as packed f32x2 pairs, SiLU from the
-// MUFU exp2 / reciprocal, and the division-free quantizer with its exact tie fallback.
-__device__ __forceinline__ uint32_t conv4_step(const sq_mamba2_decode_params& P, int c, int C,
-                                               int8_t* __restrict__ cache_b, const int8_t* xnew) {
-  const uint32_t w0 = *reinterpret_cast<const uint32_t*>(cache_b + c);
-  const uint32_t w1 = *reinterpret_cast<const uint32_t*>(cache_b + C + c);
-  const uint32_t w2 = *reinterpret_cast<const uint32_t*>(cache_b + 2 * C + c);
-  const uint32_t w3 = *reinterpret_cast<const uint32_t*>(xnew);
+// Four consecutive channels c..c+3 with Kc = 4.  The layer's constants (taps, bias, scales)
+// are loaded before the grid-dependency wait; the codes after it.  Same per-channel op order
+// as the oracle (acc = b + Σ_j w_j·(q_j·s_in), IEEE RN each) computed as packed f32x2 pairs,
+// SiLU from the MUFU exp2 / reciprocal, and the division-free quantizer with its exact tie
+// fallback.
+struct Conv4Params {
+  float4 t0, t1, t2, t3, bi, si, so;
+};
+__device__ __forceinline__ Conv4Params conv4_params(const sq_mamba2_decode_params& P, int c) {
   const float4* wt = reinterpret_cast<const float4*>(P.conv_w + (int64_t)c * 4);
-  const float4 t0 = __ldg(wt), t1 = __ldg(wt + 1), t2 = __ldg(wt + 2), t3 = __ldg(wt + 3);
-  const float4 bi = __ldg(reinterpret_cast<const float4*>(P.conv_b + c));
-  const float4 si = __ldg(reinterpret_cast<const float4*>(P.conv_s_in + c));
-  const float4 so = __ldg(reinterpret_cast<const float4*>(P.conv_s_out + c));
-  *reinterpret_cast<uint32_t*>(cache_b + c) = w1;
-  *reinterpret_cast<uint32_t*>(cache_b + C + c) = w2;
-  *reinterpret_cast<uint32_t*>(cache_b + 2 * C + c) = w3;
+  return {__ldg(wt), __ldg(wt + 1), __ldg(wt + 2), __ldg(wt + 3),
+          __ldg(reinterpret_cast<const float4*>(P.conv_b + c)), __ldg(reinterpret_cast<const float4*>(P.conv_s_in + c)),
+          __ldg(reinterpret_cast<const float4*>(P.conv_s_out + c))};
+}
+__device__ __forceinline__ uint32_t conv4_compute(const Conv4Params& k, uint32_t w0, uint32_t w1, uint32_t w2,
+                                                  uint32_t w3) {
   // taps of channel pairs (c, c+1) and (c+2, c+3), tap j
-  const float2 wa[4] = {make_float2(t0.x, t1.x), make_float2(t0.y, t1.y), make_float2(t0.z, t1.z), make_float2(t0.w, t1.w)};
-  const float2 wb[4] = {make_float2(t2.x, t3.x), make_float2(t2.y, t3.y), make_float2(t2.z, t3.z), make_float2(t2.w, t3.w)};
+  const float2 wa[4] = {make_float2(k.t0.x, k.t1.x), make_float2(k.t0.y, k.t1.y), make_float2(k.t0.z, k.t1.z),
+                        make_float2(k.t0.w, k.t1.w)};
+  const float2 wb[4] = {make_float2(k.t2.x, k.t3.x), make_float2(k.t2.y, k.t3.y), make_float2(k.t2.z, k.t3.z),
+                        make_float2(k.t2.w, k.t3.w)};
   const uint32_t win[4] = {w0, w1, w2, w3};
-  const float2 sia = make_float2(si.x, si.y), sib = make_float2(si.z, si.w);
-  float2 acca = make_float2(bi.x, bi.y), accb = make_float2(bi.z, bi.w);
+  const float2 sia = make_float2(k.si.x, k.si.y), sib = make_float2(k.si.z, k.si.w);
+  float2 acca = make_float2(k.bi.x, k.bi.y), accb = make_float2(k.bi.z, k.bi.w);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     float2 qa, qb;
@@ -122,11 +122,11 @@ __device__ __forceinline__ uint32_t conv4_step(const sq_mamba2_decode_params& P,
   const float2 va = silu2_approx(acca), vb = silu2_approx(accb);
   bool tie = false;
   // reciprocal estimates are within ~1 ulp: quant8_fast's tie window (1e-4 of a step) covers it
-  uint32_t code = quant8x4_fast(va, vb, make_float2(rcp_approx(so.x), rcp_approx(so.y)),
-                                make_float2(rcp_approx(so.z), rcp_approx(so.w)), tie);
+  uint32_t code = quant8x4_fast(va, vb, make_float2(rcp_approx(k.so.x), rcp_approx(k.so.y)),
+                                make_float2(rcp_approx(k.so.z), rcp_approx(k.so.w)), tie);
   if (tie)
-    code = (uint32_t)(uint8_t)quant8(va.x, so.x) | ((uint32_t)(uint8_t)quant8(va.y, so.y) << 8) |
-           ((uint32_t)(uint8_t)quant8(vb.x, so.z) << 16) | ((uint32_t)(uint8_t)quant8(vb.y, so.w) << 24);
+    code = (uint32_t)(uint8_t)quant8(va.x, k.so.x) | ((uint32_t)(uint8_t)quant8(va.y, k.so.y) << 8) |
+           ((uint32_t)(uint8_t)quant8(vb.x, k.so.z) << 16) | ((uint32_t)(uint8_t)quant8(vb.y, k.so.w) << 24);
   return code;
 }
 
@@ -156,26 +156,45 @@ __global__ void __launch_bounds__(256) prep_kernel(const sq_mamba2_decode_params
   const int b = blockIdx.y;
   const int Kc = P.conv_kernel;
   pdl_trigger();
-  pdl_wait();
   const int8_t* zrow = zx + (int64_t)b * ldzx;
   int8_t* cache_b = cache + (int64_t)b * (Kc - 1) * C;
   float* rows_b = ws + (int64_t)b * nh * DS_ROWF;
   float* bc_b = ws + ds_rows_floats(B, nh) + (int64_t)b * 2 * GN;
   const int step = vec ? 4 : 1;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * step;
-  if (c >= C) return;
-  if (vec) {   // four consecutive channels, one head (x) or one group run of B / C
-    const uint32_t code = conv4_step(P, c, C, cache_b, zrow + di + c);
-    const float4 so = __ldg(reinterpret_cast<const float4*>(P.conv_s_out + c));
+  if (vec && c < C) {   // four consecutive channels, one head (x) or one group run of B / C
+    // layer constants first (no grid in the chain writes them), then wait for the codes
+    const Conv4Params kp = conv4_params(P, c);
+    const bool isx = c < di;
+    const int h = isx ? c / DS_P : 0;
+    float4 sh = make_float4(0.f, 0.f, 0.f, 0.f);
+    float dtb = 0.f, Ah = 0.f, Dh = 0.f, sBg = 1.f;
+    if (isx) {
+      sh = __ldg(reinterpret_cast<const float4*>(S.s_h + c));
+      dtb = S.dt_bias[h];
+      Ah = S.A[h];
+      Dh = S.D[h];
+      sBg = S.s_B[S.head_group[h]];
+    }
+    pdl_wait();
+    const uint32_t w0 = *reinterpret_cast<const uint32_t*>(cache_b + c);
+    const uint32_t w1 = *reinterpret_cast<const uint32_t*>(cache_b + C + c);
+    const uint32_t w2 = *reinterpret_cast<const uint32_t*>(cache_b + 2 * C + c);
+    const uint32_t w3 = *reinterpret_cast<const uint32_t*>(zrow + di + c);
+    const uint32_t zc = isx ? *reinterpret_cast<const uint32_t*>(zrow + c) : 0u;
+    const int8_t dcode = isx ? zrow[2 * di + 2 * GN + h] : (int8_t)0;
+    *reinterpret_cast<uint32_t*>(cache_b + c) = w1;
+    *reinterpret_cast<uint32_t*>(cache_b + C + c) = w2;
+    *reinterpret_cast<uint32_t*>(cache_b + 2 * C + c) = w3;
+    const uint32_t code = conv4_compute(kp, w0, w1, w2, w3);
+    const float4 so = kp.so;
     const float4 v = make_float4(__fmul_rn((float)(int8_t)code, so.x), __fmul_rn((float)(int8_t)(code >> 8), so.y),
                                  __fmul_rn((float)(int8_t)(code >> 16), so.z), __fmul_rn((float)(int8_t)(code >> 24), so.w));
-    if (c < di) {   // x channels: the scan's per-row operands
-      const int h = c / DS_P, p = c % DS_P;
-      const float delta = softplus_f(__fadd_rn(__fmul_rn((float)zrow[2 * di + 2 * GN + h], S.s_dt), S.dt_bias[h]));
-      const float rsmax = 2097152.0f / (128.0f * S.s_B[S.head_group[h]]);   // |rs·B̂| <= 2^21
+    if (isx) {   // x channels: the scan's per-row operands
+      const int p = c % DS_P;
+      const float delta = softplus_f(__fadd_rn(__fmul_rn((float)dcode, S.s_dt), dtb));
+      const float rsmax = 2097152.0f / (128.0f * sBg);   // |rs·B̂| <= 2^21
       float* rf = rows_b + (int64_t)h * DS_ROWF;
-      const float4 sh = __ldg(reinterpret_cast<const float4*>(S.s_h + c));
-      const uint32_t zc = *reinterpret_cast<const uint32_t*>(zrow + c);
       auto rs = [&](float xh, float s) {
         return fminf(fmaxf(__fmul_rn(__fmul_rn(delta, xh), __frcp_rn(s)), -rsmax), rsmax);
       };
@@ -188,8 +207,8 @@ __global__ void __launch_bounds__(256) prep_kernel(const sq_mamba2_decode_params
       *reinterpret_cast<float4*>(rf + 2 * DS_P + p) = make_float4(za.x, za.y, zb.x, zb.y);
       *reinterpret_cast<float4*>(rf + 3 * DS_P + p) = sh;
       if (p == 0) {
-        rf[4 * DS_P] = expf(__fmul_rn(delta, S.A[h]));
-        rf[4 * DS_P + 1] = S.D[h];
+        rf[4 * DS_P] = expf(__fmul_rn(delta, Ah));
+        rf[4 * DS_P + 1] = Dh;
       }
     } else {        // B | C channels: four consecutive n of one group land contiguously
       const int j = c - di;
@@ -200,6 +219,8 @@ __global__ void __launch_bounds__(256) prep_kernel(const sq_mamba2_decode_params
     }
     return;
   }
+  pdl_wait();
+  if (c >= C) return;
   const int8_t q = conv_step(P, Kc, c, C, cache_b, zrow[di + c]);
   if (c < di) {
     const int h = c / DS_P;
