@@ -550,6 +550,36 @@ __device__ __forceinline__ int had_swz(int i) {   // float index -> swizzled flo
   return ((q ^ ((q >> 3) & 7)) << 2) | (i & 3);
 }
 
+// One Sylvester stage of stride h (h >= 2) over 32 register values with packed f32x2 ops:
+// lanes (e, e+1) and (e+h, e+h+1) butterfly together; a - b as fma(b, -1, a) rounds like
+// the oracle's f32 subtraction.
+template <int H>
+__device__ __forceinline__ void had_stage32(float (&v)[32]) {
+  const float2 M1 = make_float2(-1.f, -1.f);
+#pragma unroll
+  for (int e = 0; e < 32; e += 2)
+    if ((e & H) == 0) {
+      const float2 a = make_float2(v[e], v[e + 1]), b = make_float2(v[e + H], v[e + H + 1]);
+      const float2 s = __fadd2_rn(a, b), d = __ffma2_rn(b, M1, a);
+      v[e] = s.x; v[e + 1] = s.y; v[e + H] = d.x; v[e + H + 1] = d.y;
+    }
+}
+__device__ __forceinline__ void had_stage32_h1(float (&v)[32]) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    const float x0 = v[e], x1 = v[e + 1];
+    v[e] = __fadd_rn(x0, x1);
+    v[e + 1] = __fsub_rn(x0, x1);
+  }
+}
+__device__ __forceinline__ void had_5stages(float (&v)[32]) {
+  had_stage32_h1(v);
+  had_stage32<2>(v);
+  had_stage32<4>(v);
+  had_stage32<8>(v);
+  had_stage32<16>(v);
+}
+
 __global__ void __launch_bounds__(256) norm_had8192_kernel(const sq_mamba2_decode_params P, const float* y,
                                                           int64_t ldy, int8_t* __restrict__ yq, int64_t ldyq,
                                                           int32_t* __restrict__ gsum, int64_t ldg) {
@@ -604,15 +634,7 @@ __global__ void __launch_bounds__(256) norm_had8192_kernel(const sq_mamba2_decod
     return;
   }
   // phase A: bits 0..4 (contiguous values of this thread)
-#pragma unroll
-  for (int h = 1; h < 32; h <<= 1)
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if ((e & h) == 0) {
-        const float x0 = v[e], x1 = v[e + h];
-        v[e] = __fadd_rn(x0, x1);
-        v[e + h] = __fsub_rn(x0, x1);
-      }
+  had_5stages(v);
 #pragma unroll
   for (int j = 0; j < 8; ++j)
     *reinterpret_cast<float4*>(buf + had_swz(t * 32 + 4 * j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -621,15 +643,7 @@ __global__ void __launch_bounds__(256) norm_had8192_kernel(const sq_mamba2_decod
   const int tlo = t & 31, thi = t >> 5;
 #pragma unroll
   for (int k = 0; k < 32; ++k) v[k] = buf[had_swz((thi << 10) | (k << 5) | tlo)];
-#pragma unroll
-  for (int h = 1; h < 32; h <<= 1)
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if ((e & h) == 0) {
-        const float x0 = v[e], x1 = v[e + h];
-        v[e] = __fadd_rn(x0, x1);
-        v[e + h] = __fsub_rn(x0, x1);
-      }
+  had_5stages(v);
 #pragma unroll
   for (int k = 0; k < 32; ++k) buf[had_swz((thi << 10) | (k << 5) | tlo)] = v[k];
   __syncthreads();
@@ -639,26 +653,23 @@ __global__ void __launch_bounds__(256) norm_had8192_kernel(const sq_mamba2_decod
     const float4 q = *reinterpret_cast<const float4*>(buf + had_swz((m << 10) | (t << 2)));
     v[4 * m] = q.x; v[4 * m + 1] = q.y; v[4 * m + 2] = q.z; v[4 * m + 3] = q.w;
   }
-#pragma unroll
-  for (int h = 1; h < 8; h <<= 1)
-#pragma unroll
-    for (int m = 0; m < 8; ++m)
-      if ((m & h) == 0) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float x0 = v[4 * m + j], x1 = v[4 * (m + h) + j];
-          v[4 * m + j] = __fadd_rn(x0, x1);
-          v[4 * (m + h) + j] = __fsub_rn(x0, x1);
-        }
-      }
+  // stages h = 4, 8, 16 in units of the 4-value groups (value index 4m + j): packed pairs
+  had_stage32<4>(v);
+  had_stage32<8>(v);
+  had_stage32<16>(v);
+  const float2 is2 = make_float2(isy, isy);
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
-    const int8_t q0 = quant8_inv(v[4 * m], P.s_y, isy), q1 = quant8_inv(v[4 * m + 1], P.s_y, isy);
-    const int8_t q2 = quant8_inv(v[4 * m + 2], P.s_y, isy), q3 = quant8_inv(v[4 * m + 3], P.s_y, isy);
-    *reinterpret_cast<uint32_t*>(out + ((m << 10) | (t << 2))) =
-        (uint32_t)(uint8_t)q0 | ((uint32_t)(uint8_t)q1 << 8) | ((uint32_t)(uint8_t)q2 << 16) | ((uint32_t)(uint8_t)q3 << 24);
+    bool tie = false;
+    uint32_t code = quant8x4_fast(make_float2(v[4 * m], v[4 * m + 1]), make_float2(v[4 * m + 2], v[4 * m + 3]), is2,
+                                  is2, tie);
+    if (tie)   // rare: a value within 1e-4 of a rounding tie -> exact division
+      code = (uint32_t)(uint8_t)quant8(v[4 * m], P.s_y) | ((uint32_t)(uint8_t)quant8(v[4 * m + 1], P.s_y) << 8) |
+             ((uint32_t)(uint8_t)quant8(v[4 * m + 2], P.s_y) << 16) |
+             ((uint32_t)(uint8_t)quant8(v[4 * m + 3], P.s_y) << 24);
+    *reinterpret_cast<uint32_t*>(out + ((m << 10) | (t << 2))) = code;
     if (gsum) {   // 128-wide block (m << 3) | warp holds exactly this warp's 32 x 4 codes
-      int cs = (int)q0 + q1 + q2 + q3;
+      int cs = __dp4a((int)code, 0x01010101, 0);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(0xffffffffu, cs, o);
       if (lane == 0) gsum[(int64_t)b * ldg + ((m << 3) | warp)] = cs;
