@@ -627,10 +627,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       const int m = m_tile * NTOK + t;
       if (m >= args.M) continue;
-#pragma unroll
       const float* s_alpha = reinterpret_cast<const float*>(smem + Cfg::OFF_EPI);
+      const int n0 = n_tile * TC_BN + r;
+      const int64_t o = (int64_t)m * args.ldo + n0;
+      if ((args.epi == SQ_EPI_F32 || args.epi == SQ_EPI_RESID) && n0 + 3 < args.N &&
+          (reinterpret_cast<uintptr_t>(reinterpret_cast<float*>(args.out) + o) & 15) == 0) {
+        // four contiguous channels: one 16-B store (16-B read-add-write for the residual)
+        const float4 al = *reinterpret_cast<const float4*>(s_alpha + r);
+        float4 yv = make_float4(__fmul_rn((float)sum[0], al.x), __fmul_rn((float)sum[1], al.y),
+                                __fmul_rn((float)sum[2], al.z), __fmul_rn((float)sum[3], al.w));
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + o);
+        if (args.epi == SQ_EPI_RESID) {
+          const float4 h = *dst;
+          yv = make_float4(__fadd_rn(h.x, yv.x), __fadd_rn(h.y, yv.y), __fadd_rn(h.z, yv.z), __fadd_rn(h.w, yv.w));
+        }
+        *dst = yv;
+        continue;
+      }
+#pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int nn = n_tile * TC_BN + r + e;
+        const int nn = n0 + e;
         if (nn < args.N) {
           const float cs = s_alpha[TC_BN + r + e];
           epi_store(args, m, nn, sum[e], s_alpha[r + e], cs, __frcp_rn(cs));
