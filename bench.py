@@ -38,6 +38,13 @@ WORKLOADS = {
     "decode8b_w4a16": dict(dims=("mamba2", 4096, 8192, 128, 128, 64, 8, 4), layers=56, vocab=256000,
                            profile="W4A16", batch=1,
                            desc="Mamba2-8B-shaped W4A16 decode, batch 1, fp32 state, 56 layers + W4A8 head"),
+    # configs[4]: Mamba1-2.8B W8A8, the paper's TTFT protocol (b=1, 1024-token prefill) and decode
+    "m1prefill28b": dict(dims=("mamba1", 2560, 5120, 16, 1, 5120, 1, 4, 160), layers=64, vocab=50288,
+                         profile="W8A8", batch=1, seq=1024, model="Mamba1-2.8B-shaped",
+                         desc="Mamba1-2.8B-shaped W8A8 prefill, batch 1 x 1024 tokens, 64 layers, last-token head"),
+    "m1decode28b": dict(dims=("mamba1", 2560, 5120, 16, 1, 5120, 1, 4, 160), layers=64, vocab=50288,
+                        profile="W8A8", batch=1, model="Mamba1-2.8B-shaped",
+                        desc="Mamba1-2.8B-shaped W8A8 decode, batch 1, int8 state, 64 layers + W4A8 head"),
 }
 
 
@@ -118,31 +125,18 @@ def ncu_traffic(kernel_name):
 
 
 def dist_init():
-    import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return world, rank, local
+    from paper_2503_22879_b200 import dist as pdist
+    return pdist.init("nccl")
 
 
 def max_over_ranks(v, world):
-    if world == 1:
-        return v
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2503_22879_b200 import dist as pdist
+    return pdist.max_over_ranks(v, world)
 
 
 def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    from paper_2503_22879_b200 import dist as pdist
+    pdist.barrier(world)
 
 
 # ------------------------------------------------------------------ CPU baseline (oracle)
@@ -197,7 +191,7 @@ def run_reference_arm(args, wl, world, rank):
         return
     import multiprocessing
     cores = multiprocessing.cpu_count()
-    if args.workload.startswith("prefill"):
+    if "seq" in wl:   # prefill workloads
         ntok = 128
         cpu_prefill_sample(wl["dims"], wl["profile"], 16)
         spts = [cpu_prefill_sample(wl["dims"], wl["profile"], ntok) for _ in range(args.steps)]
@@ -302,7 +296,11 @@ def run_prefill(args, wl, world, rank, local):
     achieved = ops_per / (gemm_ms / 1e3) / 1e12
     hbm, bf16, pk_kind = peaks()
     # the step's largest kernel: the chunked int8 SSD scan (HBM-bound in principle: int8 codes
-    # in, f32 y + int8 state out), timed live on the layer's own inputs
+    # in, f32 y + int8 state out), timed live on the layer's own inputs (Mamba2); Mamba1's
+    # largest kernel is the in_proj GEMM itself
+    if d.variant == "mamba1":
+        return _prefill_line(args, wl, world, rank, d, B, T, value, ms, e2e_ms, lm, clk, achieved, bf16, pk_kind,
+                             ops_per, gemm_ms)
     di, gn, nh = d.d_inner, d.n_state_groups * d.d_state, d.n_heads
     cv, zx = ws["conv"], ws["zx"]
     st_tmp = torch.empty((B, nh, d.head_dim, d.d_state), dtype=torch.int8, device=dev)
@@ -350,6 +348,35 @@ def run_prefill(args, wl, world, rank, local):
                 "e2e": {"value": world * B * T / (e2e_ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": B * T * 4,
                         "d2h_bytes_per_step": B * lm.vocab * 4},
                 "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
+def _prefill_line(args, wl, world, rank, d, B, T, value, ms, e2e_ms, lm, clk, achieved, bf16, pk_kind, ops_per,
+                  gemm_ms):
+    """Mamba1 prefill line: the in_proj W8A8 GEMM is the dominant kernel."""
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import multiprocessing
+        ntok = 128
+        spt = cpu_prefill_sample(wl["dims"], wl["profile"], ntok)
+        cpu = {"value": 1.0 / (spt * wl["layers"]), "unit": "tok/s", "cores": multiprocessing.cpu_count(),
+               "kind": "port", "sample": f"one full-width layer over {ntok} tokens of one sequence, "
+                                         f"x{wl['layers']} layers (extrapolated); numpy oracle, exact-int f64 BLAS"}
+    if rank == 0:
+        line = {"metric": "prefill tok/s", "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+                "config": {"workload": args.workload, "desc": wl["desc"], "model": wl.get("model", ""),
+                           "global_batch": B * world, "seq_len": T, "layers": wl["layers"],
+                           "parallelism": f"dp{world} (batch-shard replicas, no collective)"},
+                "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (in_proj W8A8, tcgen05 kind::i8)",
+                             "achieved": achieved, "peak": bf16 * 2, "unit": "TOP/s", "frac": achieved / (bf16 * 2),
+                             "traffic": None, "peak_kind": pk_kind + " (int8 = 2 x measured bf16 dense)",
+                             "algorithmic_ops_per_launch": ops_per, "launch_ms": gemm_ms},
+                "cpu_baseline": cpu,
+                "e2e": {"value": world * B * T / (e2e_ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": B * T * 4,
+                        "d2h_bytes_per_step": B * lm.vocab * 4},
+                "gpu_launches": None, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
 
 
@@ -424,7 +451,14 @@ def run_decode(args, wl, world, rank, local):
     di, gn = d.d_inner, d.n_state_groups * d.d_state
     reps = 2 * len(lm.blocks)
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if blk.a8 and getattr(blk, "fused_decode", False):
+    if d.variant == "mamba1":
+        dom_name = "gemm_tc_kernel / gemm_a8_mma (in_proj W8A8, decode weight stream)"
+
+        def dom(i):
+            b_ = lm.blocks[i % len(lm.blocks)]
+            b_.in_proj.a8(ws["u"][:B], ops.EPI_QUANT, ws["zx"][:B], b_.in_out_scale)
+        dom_bytes = d.in_proj_out * d.d_model + B * (d.d_model + d.in_proj_out)
+    elif blk.a8 and getattr(blk, "fused_decode", False):
         dom_name = "state_ring_kernel (K9 int8 state update, decode)"
         ops.set_decode_stages(2)
 
@@ -464,7 +498,8 @@ def run_decode(args, wl, world, rank, local):
                                          s.conv_cache.numel() * s.conv_cache.element_size() * 2 for s in states)
     res = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        t = cpu_decode_sample(wl["dims"], wl["profile"], B, layers_sample=2) if blk.a8 else None
+        t = (cpu_decode_sample(wl["dims"], wl["profile"], B, layers_sample=2)
+             if blk.a8 and d.variant == "mamba2" else None)
         if t is not None:
             import multiprocessing
             res = {"value": B / (t * wl["layers"]), "unit": "tok/s", "cores": multiprocessing.cpu_count(),
@@ -475,7 +510,7 @@ def run_decode(args, wl, world, rank, local):
         line = {"metric": "decode tok/s", "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "int8" if blk.a8 else "f32", "data": "synthetic",
-                "config": {"workload": args.workload, "desc": wl["desc"], "model": "Mamba2-8B-shaped",
+                "config": {"workload": args.workload, "desc": wl["desc"], "model": wl.get("model", "Mamba2-8B-shaped"),
                            "global_batch": B * world, "seq_len": 1, "layers": wl["layers"], "vocab": wl["vocab"],
                            "parallelism": f"dp{world} (batch-shard replicas, no collective)",
                            "l2": "inputs larger than L2 (weights+state stream every step), no flush",
@@ -511,7 +546,7 @@ def main():
         run_reference_arm(args, wl, world, rank)
         return
     world, rank, local = dist_init()
-    if args.workload.startswith("prefill"):
+    if "seq" in wl:   # prefill workloads
         run_prefill(args, wl, world, rank, local)
     else:
         run_decode(args, wl, world, rank, local)

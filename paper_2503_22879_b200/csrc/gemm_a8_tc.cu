@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t t_raw0 = 0, t_rawl = 0, t_conv_done = 0, t_acc = 0, t_epi0 = 0, t_epi1 = 0, t_ld0 = 0, t_loop = 0;
   long long c_raw = 0, c_emp = 0, c_stw = 0, c_full = 0;   // timeline: SM cycles spent waiting
   long long c_b0 = 0, c_b1 = 0, c_b2 = 0;                  // timeline: convert / store / signal phases
+  uint64_t t_mloop = 0, t_mcorr = 0;                       // timeline: MMA warp issue progress
   const int nkb_total = args.K / TC_BK;
   const int kb_begin = split * nkb_total / SPLITS;
   const int nkb = (split + 1) * nkb_total / SPLITS - kb_begin;
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         mma_commit(&empty[s]);
       }
+      t_mloop = tl ? gtimer() : 0;
       if (Cfg::MMA_CORR) {
         // dH = sum_kb sg[n,kb] * (S[kb][t] >> 7), dL = sum_kb sg[n,kb] * (S[kb][t] & 127)
         mbar_wait(corr_ready, 0);
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
       mma_commit(accf);
+      t_mcorr = tl ? gtimer() : 0;
     }
     __syncwarp();
   } else if (warp == 10) {
@@ -669,7 +672,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     printf("gemm cta %d waits (cycles): converter rfull %lld empty %lld wait_st %lld | phases convert %lld store %lld "
            "signal %lld\n", blockIdx.x, c_raw, c_emp, c_stw, c_b0, c_b1, c_b2);
   if (tl && warp == 1 && lane == 0)
-    printf("gemm cta %d waits (cycles): mma full %lld\n", blockIdx.x, c_full);
+    printf("gemm cta %d waits (cycles): mma full %lld | main-loop MMAs issued %.2f us, correction issued %.2f us\n",
+           blockIdx.x, c_full, (t_mloop - t_entry) * 1e-3, (t_mcorr - t_entry) * 1e-3);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);

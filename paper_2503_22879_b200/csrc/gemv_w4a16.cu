@@ -110,6 +110,104 @@ __global__ void __launch_bounds__(256) gemv_w4a16_tiled_kernel(const float* __re
 
 
 
+// Quadrant-split tiled GEMV (K % 128 == 0): a CTA owns one 32-row quadrant of a 128-row
+// weight tile (4 CTAs per tile, so small-N projections still fill the GPU); its 8 warps take
+// the (k-block, 32-wide chunk) pieces round-robin, lane = row, so each warp load is 512
+// contiguous bytes.  Nibbles become floats with a byte-permute into 2^23 + v + 8 and one
+// packed subtract; products accumulate in packed f32x2 pairs (short dependency chains); the
+// 8 warps' partial row sums are added in fixed warp order (deterministic).
+template <int MT>
+__global__ void __launch_bounds__(256) gemv_w4a16_q_kernel(const float* __restrict__ x, int64_t ldx,
+                                                           const uint8_t* __restrict__ w,
+                                                           const float* __restrict__ sgrp, int group, int M, int N,
+                                                           int K, float* __restrict__ out, int64_t ldo, int resid) {
+  extern __shared__ __align__(16) float xs[];  // [MT][K]
+  __shared__ float part[8][MT][32];
+  const int tile = blockIdx.x >> 2, q = blockIdx.x & 3;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = tile * 128 + q * 32 + lane;
+  const bool valid = n < N;
+  const int nkb = K / 128, ng = K / group;
+  const uint8_t* wt = w + (size_t)tile * nkb * 8192 + (q * 32 + lane) * 16;   // + kb*8192 + chunk*2048
+  const float* srow = sgrp + (size_t)(valid ? n : 0) * ng;
+  const int npieces = nkb * 4;
+  // first weight loads before the activation staging (independent of it)
+  constexpr int D = 4;
+  int4 buf[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const int pc = warp + 8 * j;
+    buf[j] = pc < npieces ? __ldg(reinterpret_cast<const int4*>(wt + (size_t)(pc >> 2) * 8192 + (pc & 3) * 2048))
+                          : make_int4(0, 0, 0, 0);
+  }
+  for (int i = threadIdx.x * 4; i < MT * K; i += blockDim.x * 4) {
+    const int m = i / K, k = i % K;
+    *reinterpret_cast<float4*>(xs + i) = m < M ? *reinterpret_cast<const float4*>(x + (int64_t)m * ldx + k)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  float acc[MT];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) acc[m] = 0.f;
+  const float2 MB = make_float2(-8388616.0f, -8388616.0f);   // 2^23 + 8
+  for (int p0 = warp; p0 < npieces; p0 += 8 * D) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int pc = p0 + 8 * j;
+      if (pc >= npieces) break;
+      const int4 cur = buf[j];
+      const int pn = pc + 8 * D;
+      if (pn < npieces) buf[j] = __ldg(reinterpret_cast<const int4*>(wt + (size_t)(pn >> 2) * 8192 + (pn & 3) * 2048));
+      const int k0 = (pc >> 2) * 128 + (pc & 3) * 32;
+      const float s = valid ? srow[k0 / group] : 0.f;
+      const uint32_t pw[4] = {(uint32_t)cur.x, (uint32_t)cur.y, (uint32_t)cur.z, (uint32_t)cur.w};
+      float2 pa[MT][2];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) pa[m][0] = pa[m][1] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t u = pw[e] ^ 0x88888888u;                       // nibble v -> v + 8
+        const uint32_t lo = u & 0x0F0F0F0Fu, hi = (u >> 4) & 0x0F0F0F0Fu;   // elements 0-3 / 4-7
+        const float2 w01 = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7440)),
+                                                  __uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7441))), MB);
+        const float2 w23 = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7442)),
+                                                  __uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7443))), MB);
+        const float2 w45 = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7440)),
+                                                  __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7441))), MB);
+        const float2 w67 = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7442)),
+                                                  __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7443))), MB);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const float4 xa = *reinterpret_cast<const float4*>(&xs[m * K + k0 + e * 8]);
+          const float4 xb = *reinterpret_cast<const float4*>(&xs[m * K + k0 + e * 8 + 4]);
+          pa[m][0] = __ffma2_rn(w01, make_float2(xa.x, xa.y), pa[m][0]);
+          pa[m][1] = __ffma2_rn(w23, make_float2(xa.z, xa.w), pa[m][1]);
+          pa[m][0] = __ffma2_rn(w45, make_float2(xb.x, xb.y), pa[m][0]);
+          pa[m][1] = __ffma2_rn(w67, make_float2(xb.z, xb.w), pa[m][1]);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+        acc[m] = fmaf(__fadd_rn(__fadd_rn(pa[m][0].x, pa[m][0].y), __fadd_rn(pa[m][1].x, pa[m][1].y)), s, acc[m]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < MT; ++m) part[warp][m][lane] = acc[m];
+  __syncthreads();
+  if (warp == 0 && valid) {
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (m < M) {
+        float v = 0.f;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; ++w8) v = __fadd_rn(v, part[w8][m][lane]);
+        float* o = out + (int64_t)m * ldo + n;
+        *o = resid ? __fadd_rn(*o, v) : v;
+      }
+    }
+  }
+}
+
 template <int MT>
 __global__ void __launch_bounds__(256) gemv_w4a16_kernel(const float* __restrict__ x, int64_t ldx,
                                                          const uint8_t* __restrict__ w,
@@ -178,12 +276,13 @@ extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4, con
     const int MT = mc <= 1 ? 1 : (mc <= 2 ? 2 : (mc <= 4 ? 4 : 8));
     const size_t smem = (size_t)MT * K * sizeof(float);
     SQ_REQUIRE(smem <= 200 * 1024, SQ_ERR_SHAPE, "sq_gemv_w4a16: K too large");
-    const bool tiled = K % 128 == 0;
-    int blocks = tiled ? (N + 127) / 128 : (N + 7) / 8;
+    const bool tiled = K % 128 == 0;   // kernel layout of sq_repack_w4
+    const bool quad = tiled && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    int blocks = quad ? 4 * ((N + 127) / 128) : tiled ? (N + 127) / 128 : (N + 7) / 8;
     if (!tiled && blocks > 148 * 4) blocks = 148 * 4;
 #define SQ_GV(MTV)                                                                                  \
   {                                                                                                 \
-    auto k = tiled ? gemv_w4a16_tiled_kernel<MTV> : gemv_w4a16_kernel<MTV>;                         \
+    auto k = quad ? gemv_w4a16_q_kernel<MTV> : tiled ? gemv_w4a16_tiled_kernel<MTV> : gemv_w4a16_kernel<MTV>; \
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     k<<<blocks, 256, smem, st>>>(x + (int64_t)m0 * ldx, ldx, w4, s_group, group, mc, N, K,          \
                                  out + (int64_t)m0 * ldo, ldo, resid);                              \
