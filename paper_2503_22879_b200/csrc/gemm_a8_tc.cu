@@ -150,11 +150,14 @@ struct TcCfg {
   static constexpr int NBAR = 2 * STAGES + 2 * RAW + 2;
   static constexpr int OFF_EPI = OFF_BAR + NBAR * 8 + 16;   // alpha[128], col_scale[128]
   static constexpr int SMEM0 = 1024 + OFF_EPI + 2 * TC_BN * 4;
-  static constexpr int SMEM = SMEM0 < 120 * 1024 ? 120 * 1024 : SMEM0;   // 1 CTA/SM: TMEM alloc of 512 cols
+  // W4: 1 CTA/SM (TMEM alloc of 512 cols: accumulators + A stages).  W8: accumulators only
+  // (<= 256 cols), two CTAs per SM so one CTA's epilogue overlaps the other's main loop.
+  static constexpr int TMEM_COLS = W4 ? 512 : 256;
+  static constexpr int SMEM = (W4 && SMEM0 < 120 * 1024) ? 120 * 1024 : SMEM0;
 };
 
 template <int NTOK, int WMODE, int SPLITS, int STAGES, int RAW>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TC_THREADS, WMODE == WM_W8 ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w, TcArgs args) {
   using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES, RAW>;
   // converter batch: D k-blocks per raw-ring barrier and per TMEM-stage wait (D < STAGES, no self-wait)
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tma_prefetch(&tm_act);
     if (!W4) tma_prefetch(&tm_w);
   }
-  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -503,8 +506,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const float ics = __frcp_rn(cs);
     constexpr int CH = NTOK / 2;
     int32_t* red = reinterpret_cast<int32_t*>(act);     // split-K: [NTOK][128], aliases the act stages
+    // staging the whole fp32 tile can exceed the stage area when two CTAs share an SM (W8):
+    // then the token halves are staged and stored one after the other
+    const int esz = args.epi == SQ_EPI_QUANT ? 1 : 4;
+    const int npass = (SPLITS == 1 && NTOK * TC_BN * esz > Cfg::OFF_SUM) ? 2 : 1;
+    static_assert(SPLITS > 1 || NTOK * TC_BN * 2 <= Cfg::OFF_SUM, "half a fp32 tile must fit the stage area");
+    // (W4 tiles wider than 128 tokens run without split-K: gemm_a8_tc dispatch)
+    static_assert(SPLITS == 1 || (W4 && NTOK > 128) || NTOK * TC_BN * 4 <= Cfg::OFF_SUM,
+                  "split-K reduction tile must fit the stage area");
+    for (int pass = 0; pass < npass; ++pass) {
+    const int tbase = npass == 2 ? pass * CH : 0;        // first token of this pass's staging buffer
+    const int tcount = npass == 2 ? CH : NTOK;
 #pragma unroll 1
-    for (int c0 = half * CH; c0 < (half + 1) * CH; c0 += 8) {
+    for (int c0 = half * CH; c0 < (half + 1) * CH && (npass == 1 || half == pass); c0 += 8) {
       uint32_t v[8];
       tmem_ld_x8(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
       tmem_wait_ld();
@@ -537,7 +551,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // stage [NTOK][TC_BN] in smem (aliases the activation stages: every MMA has completed)
         if (args.epi == SQ_EPI_QUANT && (args.dbg & 16)) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) act[(c0 + j) * TC_BN + row] = (uint8_t)val[j];
+          for (int j = 0; j < 8; ++j) act[(c0 + j - tbase) * TC_BN + row] = (uint8_t)val[j];
         } else if (args.epi == SQ_EPI_QUANT) {
           float yv[8];
           int8_t qv[8];
@@ -552,12 +566,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int j = 0; j < 8; ++j) qv[j] = quant8(yv[j], cs);
           }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) act[(c0 + j) * TC_BN + row] = (uint8_t)qv[j];
+          for (int j = 0; j < 8; ++j) act[(c0 + j - tbase) * TC_BN + row] = (uint8_t)qv[j];
         } else {
           uint32_t* st32 = reinterpret_cast<uint32_t*>(act);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            st32[(c0 + j) * TC_BN + row] =
+            st32[(c0 + j - tbase) * TC_BN + row] =
                 args.epi == SQ_EPI_I32 ? (uint32_t)val[j] : __float_as_uint(__fmul_rn((float)val[j], alpha));
         }
       } else {
@@ -570,15 +584,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // coalesced 16-B stores of the staged tile (residual epilogue: 16-B read-add-write)
       named_bar(3, 256);
       const int et = threadIdx.x - 64;
-      const int esz = args.epi == SQ_EPI_QUANT ? 1 : 4;
       const int per16 = 16 / esz;
       const int chunks = TC_BN / per16;
-      for (int idx = et; idx < NTOK * chunks; idx += 256) {
-        const int t = idx / chunks, c = idx % chunks;
+      for (int idx = et; idx < tcount * chunks; idx += 256) {
+        const int ts = idx / chunks, c = idx % chunks;
+        const int t = tbase + ts;
         const int m = m_tile * NTOK + t;
         const int n0 = n_tile * TC_BN + c * per16;
         if (m >= args.M || n0 >= args.N) continue;
-        const uint8_t* src = act + (t * TC_BN + c * per16) * esz;
+        const uint8_t* src = act + (ts * TC_BN + c * per16) * esz;
         uint8_t* dst = reinterpret_cast<uint8_t*>(args.out) + ((int64_t)m * args.ldo + n0) * esz;
         const int nv = min(per16, args.N - n0);
         if (nv == per16 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
@@ -604,6 +618,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
       }
+    }
+      if (npass == 2 && pass == 0) named_bar(3, 256);   // staging buffer reused by the next pass
     }
   }
 
@@ -676,7 +692,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
            blockIdx.x, c_full, (t_mloop - t_entry) * 1e-3, (t_mcorr - t_entry) * 1e-3);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<Cfg::TMEM_COLS>(tmem);
   }
 }
 
@@ -711,7 +727,10 @@ template <int NTOK, int WMODE, int SPLITS>
 static int launch_tc(const int8_t* a, int64_t lda, const uint8_t* w, const TcArgs& args, cudaStream_t st) {
   constexpr int RAW = WMODE == WM_W8 ? 1 : (NTOK <= 64 ? g_raw64 : (NTOK == 128 ? 8 : 6));
   using C1 = TcCfg<NTOK, WMODE, SPLITS, 1, RAW>;
-  constexpr int ST0 = (210 * 1024 - C1::RAW_BYTES - C1::SUM_BYTES - C1::SGS_BYTES) / C1::STAGE_BYTES;
+  // W8 targets two CTAs per SM (~105 KB each); W4 one CTA with the raw ring
+  // (split-K keeps the one-CTA budget: its int32 reduction tile [NTOK][128] needs the room)
+  constexpr int BUDGET = (WMODE == WM_W8 && SPLITS == 1) ? 104 * 1024 : 210 * 1024;
+  constexpr int ST0 = (BUDGET - C1::RAW_BYTES - C1::SUM_BYTES - C1::SGS_BYTES) / C1::STAGE_BYTES;
   constexpr int STAGES = ST0 > 8 ? 8 : (ST0 < 2 ? 2 : ST0);
   using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES, RAW>;
   static_assert(Cfg::SMEM <= 227 * 1024, "smem budget");

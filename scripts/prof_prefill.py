@@ -51,3 +51,19 @@ for r in range(reps):
 for k, v in tm.items():
     if v:
         print(f"{k}: last {v[-1]:.1f} us  min {min(v):.1f} us")
+if which in ("gemm",):
+    u = torch.randint(-100, 100, (M, d.d_model), generator=g, dtype=torch.int8, device=dev)
+    yq = torch.randint(-100, 100, (M, di), generator=g, dtype=torch.int8, device=dev)
+    h = torch.zeros((M, d.d_model), device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for r_ in range(reps):
+        e0.record()
+        blk.in_proj.a8(u, ops.EPI_QUANT, zx, blk.in_out_scale)
+        e1.record()
+        torch.cuda.synchronize()
+        t_in = e0.elapsed_time(e1) * 1e3
+        e0.record()
+        blk.out_proj.a8(yq, ops.EPI_RESID, h)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"in_proj {t_in:.1f} us  out_proj {e0.elapsed_time(e1) * 1e3:.1f} us")
