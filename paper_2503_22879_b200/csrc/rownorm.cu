@@ -121,13 +121,11 @@ __device__ __forceinline__ void load16(const float* p, float (&v)[16]) {
 // quant8 only when some value sits within 1e-4 of a rounding tie (bit-identical codes).
 __device__ __forceinline__ void quant16(const float (&v)[16], float s, uint32_t (&w)[4]) {
   const float is = __frcp_rn(s);
+  const float2 is2 = make_float2(is, is);
   bool tie = false;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    w[e] = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) w[e] |= (uint32_t)(uint8_t)quant8_fast(v[e * 4 + k], is, tie) << (8 * k);
-  }
+  for (int e = 0; e < 4; ++e)
+    w[e] = quant8x4_fast(make_float2(v[e * 4], v[e * 4 + 1]), make_float2(v[e * 4 + 2], v[e * 4 + 3]), is2, is2, tie);
   if (tie) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -222,28 +220,50 @@ __global__ void __launch_bounds__(512) gate_norm_had_quant16_kernel(const float*
     {
       float g[16];
       load16(gamma + base, g);
+      const float2 r2 = make_float2(r, r);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __fmul_rn(__fmul_rn(v[i], r), g[i]);
+      for (int i = 0; i < 16; i += 2) {
+        const float2 t = __fmul2_rn(__fmul2_rn(make_float2(v[i], v[i + 1]), r2), make_float2(g[i], g[i + 1]));
+        v[i] = t.x;
+        v[i + 1] = t.y;
+      }
+    }
+    // in-thread stages: h = 1 scalar; h >= 2 as packed pairs (a - b as fma(b, -1, a))
+    if (blk > 1) {
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) {
+        const float a = v[i], b = v[i + 1];
+        v[i] = __fadd_rn(a, b);
+        v[i + 1] = __fsub_rn(a, b);
+      }
     }
 #pragma unroll
-    for (int h = 1; h < 16; h <<= 1) {
+    for (int h = 2; h < 16; h <<= 1) {
       if (h < blk) {
+        const float2 M1 = make_float2(-1.f, -1.f);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < 16; i += 2) {
           if ((i & h) == 0) {
-            const float a = v[i], b = v[i + h];
-            v[i] = __fadd_rn(a, b);
-            v[i + h] = __fsub_rn(a, b);
+            const float2 a = make_float2(v[i], v[i + 1]), b = make_float2(v[i + h], v[i + h + 1]);
+            const float2 sm = __fadd2_rn(a, b), df = __ffma2_rn(b, M1, a);
+            v[i] = sm.x; v[i + 1] = sm.y; v[i + h] = df.x; v[i + h + 1] = df.y;
           }
         }
       }
     }
     // cross-thread stages: the lower element gets a + b, the upper b' - a' — one FMA with
-    // sign ±1 (fma(-1, v, o) = RN(o - v), fma(1, v, o) = RN(v + o): the same rounding)
+    // sign ±1 (fma(-1, v, o) = RN(o - v), fma(1, v, o) = RN(v + o): the same rounding),
+    // two elements per packed FMA
     for (int m = 1; m < 32 && 16 * m < blk; m <<= 1) {
       const float sg = (lane & m) ? -1.f : 1.f;
+      const float2 sg2 = make_float2(sg, sg);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __fmaf_rn(sg, v[i], __shfl_xor_sync(0xffffffffu, v[i], m));
+      for (int i = 0; i < 16; i += 2) {
+        const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[i], m), __shfl_xor_sync(0xffffffffu, v[i + 1], m));
+        const float2 t = __ffma2_rn(sg2, make_float2(v[i], v[i + 1]), o);
+        v[i] = t.x;
+        v[i + 1] = t.y;
+      }
     }
     // stages h >= 512 pair thread t with thread t ^ (h / 16) through shared memory
     // (two exchange buffers: a stage's writes go to the half the previous stage did not read,
@@ -255,14 +275,14 @@ __global__ void __launch_bounds__(512) gate_norm_had_quant16_kernel(const float*
         *reinterpret_cast<float4*>(xb + base + e * 4) = make_float4(v[e * 4], v[e * 4 + 1], v[e * 4 + 2], v[e * 4 + 3]);
       __syncthreads();
       const float sg = (threadIdx.x & m) ? -1.f : 1.f;
+      const float2 sg2 = make_float2(sg, sg);
       const float* o = xb + (int)((threadIdx.x ^ m) * 16);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float4 f = *reinterpret_cast<const float4*>(o + e * 4);
-        v[e * 4] = __fmaf_rn(sg, v[e * 4], f.x);
-        v[e * 4 + 1] = __fmaf_rn(sg, v[e * 4 + 1], f.y);
-        v[e * 4 + 2] = __fmaf_rn(sg, v[e * 4 + 2], f.z);
-        v[e * 4 + 3] = __fmaf_rn(sg, v[e * 4 + 3], f.w);
+        const float2 t0 = __ffma2_rn(sg2, make_float2(v[e * 4], v[e * 4 + 1]), make_float2(f.x, f.y));
+        const float2 t1 = __ffma2_rn(sg2, make_float2(v[e * 4 + 2], v[e * 4 + 3]), make_float2(f.z, f.w));
+        v[e * 4] = t0.x; v[e * 4 + 1] = t0.y; v[e * 4 + 2] = t1.x; v[e * 4 + 3] = t1.y;
       }
     }
     store16_q(out + (int64_t)row * ldo + base, v, s_y);
