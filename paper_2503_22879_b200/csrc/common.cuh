@@ -134,6 +134,9 @@ int launch_group_sum(const int8_t* codes, int64_t ld, int M, int K, int32_t* gsu
 int launch_ssd_chunk(const sq_mamba2_params* p, int B, int T, const int8_t* x, int64_t ldx, const int8_t* Bm,
                      const int8_t* Cm, int64_t ldbc, const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
                      int8_t* state, int state_in, float* y, int64_t ldy, cudaStream_t st);
+int launch_ssd_chunk_tc(const sq_mamba2_params* p, int B, int T, const int8_t* x, int64_t ldx, const int8_t* Bm,
+                     const int8_t* Cm, int64_t ldbc, const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
+                     int8_t* state, int state_in, float* y, int64_t ldy, cudaStream_t st);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -13,6 +13,8 @@
 //   h[p,n] = Ȧ·h[p,n] + (Δ·x̂[p])·B̂[n]   (unfused f32, oracle order)
 //   y[p]   = Σ_n h[p,n]·Ĉ[n] + D[h]·x̂[p];  y ← y·silu(ẑ[p])
 // The cached state is requantised once per call: q = rint(h / s_h[h,p]).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sq {
@@ -475,7 +477,17 @@ extern "C" int sq_ssd_scan_int8(const sq_mamba2_params* p, int B, int T, const i
   (void)chunk;   // the tensor-core path uses 64-token chunks
   SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_ssd_scan_int8: bad args");
   if (B == 0 || T == 0) return SQ_OK;
-  if (T > 1) {   // chunked SSD on the tensor cores (ssd_chunk.cu); other shapes: sequential scan
+  if (T > 1) {   // chunked SSD on the tensor cores (ssd_chunk_tc.cu tcgen05, ssd_chunk.cu mma.sync);
+                  // other shapes: sequential scan
+    static const int tc = [] {
+      const char* e = getenv("SQ_SSD_TC");
+      return e ? atoi(e) : 0;
+    }();
+    if (tc) {
+      const int rc = launch_ssd_chunk_tc(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
+                                         as_stream(stream));
+      if (rc != SQ_ERR_ARG) return rc;
+    }
     const int rc = launch_ssd_chunk(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
                                     as_stream(stream));
     if (rc != SQ_ERR_ARG) return rc;
