@@ -1,7 +1,8 @@
 // K7 on the 5th-gen tensor cores: int8 SSD chunk scan for Mamba2 prefill with tcgen05.mma
 // (ssm_block.ssd_chunked; "8-bit SSD").
 //
-// One CTA (4 warps, thread = TMEM lane) per (sequence, head), chunks of Q = 128 tokens.
+// One CTA (8 warps: a TMEM lane row per thread pair, column halves split between the pair)
+// per (sequence, head), chunks of Q = 128 tokens.
 // Every product runs as a 128-row tcgen05.mma with its operands in SW128 K-major shared
 // memory tiles and its accumulator in TMEM:
 //
@@ -29,7 +30,7 @@ using namespace sm100;
 constexpr int TQ = 128;   // chunk length
 constexpr int TP = 64;    // head_dim
 constexpr int TN = 128;   // d_state
-constexpr int TC_SSD_THREADS = 128;
+constexpr int TC_SSD_THREADS = 256;   // 8 warps: TMEM lane quadrant (warp & 3) x column half (warp >> 2)
 
 // byte offset of element (row r, byte b) in a SW128 K-major tile of 128-byte rows
 __device__ __forceinline__ int sw128(int r, int b) { return r * 128 + ((((b >> 4) ^ (r & 7))) << 4) + (b & 15); }
@@ -67,8 +68,9 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 struct TcSsdSmem {
   static constexpr int RAWC = 0;                 // C codes [t][n] int8 SW128      16 KB
   static constexpr int RAWB = RAWC + 16384;      // B codes [s][n] int8 SW128      16 KB
-  static constexpr int RAWX = RAWB + 16384;      // x codes [s][p] int8, 2 buffers 2 x 8 KB
-  static constexpr int RAWZ = RAWX + 16384;      // z codes [t][p] int8, 2 buffers 2 x 8 KB
+  static constexpr int XR = 80;                  // x code row pitch (64 B + 16: conflict-free row reads)
+  static constexpr int RAWX = RAWB + 16384;      // x codes [s][p] int8, 2 buffers 2 x 10 KB
+  static constexpr int RAWZ = RAWX + 2 * 128 * XR;   // z codes [t][p] int8, 2 buffers 2 x 8 KB
   static constexpr int CF = RAWZ + 16384;        // C fp16 [t][n] (2 K-blocks), later W [t][s]   32 KB
   static constexpr int BTF = CF + 32768;         // Bᵀ fp16 [n][s] (2 K-blocks), later y staging 32 KB
   static constexpr int XTF = BTF + 32768;        // Xᵀ fp16 [p][s] (2 K-blocks)                   16 KB
@@ -105,7 +107,9 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
   const float sBC = __fmul_rn(sB, sC);
   const int ch0 = h * TP;
   const int64_t tok0 = (int64_t)b * T;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;   // this warp's TMEM lane quadrant
+  const int q4 = warp & 3, hw = warp >> 2;
+  const int row = q4 * 32 + lane;                            // TMEM lane (t, n) of this thread
+  const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;      // this warp's TMEM lane quadrant
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     for (int i = tid; i < TQ * (TP / 16); i += TC_SSD_THREADS) {
       const int r = i / (TP / 16), c16 = (i % (TP / 16)) * 16;
       const int64_t tok = tok0 + c0 + min(r, Qc - 1);
-      cpa16(sbase + L::RAWX + buf * 8192 + r * TP + c16, x + tok * ldx + ch0 + c16, r < Qc);
+      cpa16(sbase + L::RAWX + buf * 128 * L::XR + r * L::XR + c16, x + tok * ldx + ch0 + c16, r < Qc);
       cpa16(sbase + L::RAWZ + buf * 8192 + r * TP + c16, z + tok * ldz + ch0 + c16, r < Qc);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -143,10 +147,10 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
 
   // initial state: thread n (lane) holds Hᵀ[n][0..63] = code · s_h[p]
   {
-    const int n = tid;
+    const int n = row;
     int8_t* st = state + ((int64_t)b * p.n_heads + h) * TP * N;
 #pragma unroll
-    for (int c = 0; c < TP; c += 16) {
+    for (int c = hw * 32; c < hw * 32 + 32; c += 16) {
       uint32_t v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j)
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     }
     tmem_wait_st();
   }
-  int8_t dcode = dt[(tok0 + min(tid, T - 1)) * lddt + h];   // prefetched one chunk ahead
+  int8_t dcode = tid < TQ ? dt[(tok0 + min(tid, T - 1)) * lddt + h] : 0;   // prefetched one chunk ahead
   const uint64_t dCF = desc_sw128(sm + L::CF), dBT = desc_sw128(sm + L::BTF), dXT = desc_sw128(sm + L::XTF);
   const uint64_t dHF = desc_sw128(sm + L::HF), dAL = desc_sw128(sm + L::AWL);
   const uint64_t dRC = desc_sw128(sm + L::RAWC), dRB = desc_sw128(sm + L::RAWB);
@@ -168,10 +172,10 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     const int Qc = min(TQ, T - c0);
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();   // this chunk's codes landed; the previous chunk is fully consumed
-    const int8_t* rx = reinterpret_cast<const int8_t*>(sm + L::RAWX + buf * 8192);
+    const int8_t* rx = reinterpret_cast<const int8_t*>(sm + L::RAWX + buf * 128 * L::XR);
     const int8_t* rz = reinterpret_cast<const int8_t*>(sm + L::RAWZ + buf * 8192);
     // ---- P1: Δ, fp16 operand tiles, H (fp16) for Y_off
-    {
+    if (tid < TQ) {
       float dl = 0.f, dA = 0.f;
       if (tid < Qc) {
         dl = softplus_f(__fadd_rn(__fmul_rn((float)dcode, p.s_dt), dtb));
@@ -181,10 +185,10 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
       s_cs[tid] = dA;
       dcode = dt[(tok0 + min(c0 + TQ + tid, T - 1)) * lddt + h];
     }
-    {   // C fp16 row t = tid (K = n: two 64-wide blocks)
-      const int t = tid;
+    {   // C fp16 row t (K = n: two 64-wide blocks), this thread's column half
+      const int t = row;
 #pragma unroll
-      for (int c16 = 0; c16 < N / 16; ++c16) {
+      for (int c16 = hw * (N / 32); c16 < (hw + 1) * (N / 32); ++c16) {
         const uint4 w = *reinterpret_cast<const uint4*>(sm + L::RAWC + sw128(t, c16 * 16));
         uint4 o0, o1;
         s8x4_h2x2_t(w.x, o0.x, o0.y); s8x4_h2x2_t(w.y, o0.z, o0.w);
@@ -194,10 +198,10 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
         *reinterpret_cast<uint4*>(sm + L::CF + blk * TQ * 128 + sw128(t, b0 + 16)) = o1;
       }
     }
-    {   // Bᵀ fp16 row n = tid (K = s), from the B tile's column n
-      const int n = tid;
+    {   // Bᵀ fp16 row n (K = s), from the B tile's column n; this thread's s half
+      const int n = row;
 #pragma unroll 2
-      for (int s8 = 0; s8 < TQ; s8 += 8) {
+      for (int s8 = hw * 64; s8 < hw * 64 + 64; s8 += 8) {
         float f[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) f[j] = (float)*reinterpret_cast<const int8_t*>(sm + L::RAWB + sw128(s8 + j, n));
@@ -205,21 +209,21 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
         *reinterpret_cast<uint4*>(sm + L::BTF + (s8 >> 6) * N * 128 + sw128(n, (s8 & 63) * 2)) = o;
       }
     }
-    {   // Xᵀ fp16 row p (K = s): thread (p, s half)
-      const int pp = tid & 63, sh = (tid >> 6) * 64;
+    {   // Xᵀ fp16 row p (K = s): thread (p, s quarter)
+      const int pp = tid & 63, sh = (tid >> 6) * 32;
 #pragma unroll 2
-      for (int s8 = sh; s8 < sh + 64; s8 += 8) {
+      for (int s8 = sh; s8 < sh + 32; s8 += 8) {
         float f[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) f[j] = (float)rx[(s8 + j) * TP + pp];
+        for (int j = 0; j < 8; ++j) f[j] = (float)rx[(s8 + j) * L::XR + pp];
         const uint4 o = make_uint4(pack_h2(f[0], f[1]), pack_h2(f[2], f[3]), pack_h2(f[4], f[5]), pack_h2(f[6], f[7]));
         *reinterpret_cast<uint4*>(sm + L::XTF + (s8 >> 6) * TP * 128 + sw128(pp, (s8 & 63) * 2)) = o;
       }
     }
-    {   // H fp16 [p][n]: thread n writes column n
-      const int n = tid;
+    {   // H fp16 [p][n]: thread n writes column n, its p half
+      const int n = row;
 #pragma unroll
-      for (int c = 0; c < TP; c += 16) {
+      for (int c = hw * 32; c < hw * 32 + 32; c += 16) {
         uint32_t v[16];
         tmem_ld_x16(T_H + lane_off + c, v);
         tmem_wait_ld();
@@ -268,14 +272,20 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     if (c0 + TQ < T) fetch(c0 + TQ, buf ^ 1);   // B / C tiles are free once CB has completed
     // ---- P3: W (from CB) and the state-update weights Aw (hi / lo)
     {
-      const int t = tid;
+      const int t = row;
       const float cst = s_cs[t];
 #pragma unroll 1
-      for (int c = 0; c < TQ; c += 16) {
+      for (int c = hw * 64; c < hw * 64 + 64; c += 16) {
+        uint32_t o[8];
+        const int blk = c >> 6, b0 = (c & 63) * 2;
+        if (c > 32 * q4 + 31) {   // s > t for every row of this warp: causally zero
+          *reinterpret_cast<uint4*>(sm + L::CF + blk * TQ * 128 + sw128(t, b0)) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(sm + L::CF + blk * TQ * 128 + sw128(t, b0 + 16)) = make_uint4(0, 0, 0, 0);
+          continue;
+        }
         uint32_t v[16];
         tmem_ld_x16(T_CB + lane_off + c, v);
         tmem_wait_ld();
-        uint32_t o[8];
 #pragma unroll
         for (int j = 0; j < 16; j += 2) {
           float wv[2];
@@ -287,21 +297,20 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
           }
           o[j >> 1] = pack_h2(wv[0], wv[1]);
         }
-        const int blk = c >> 6, b0 = (c & 63) * 2;
         *reinterpret_cast<uint4*>(sm + L::CF + blk * TQ * 128 + sw128(t, b0)) = make_uint4(o[0], o[1], o[2], o[3]);
         *reinterpret_cast<uint4*>(sm + L::CF + blk * TQ * 128 + sw128(t, b0 + 16)) = make_uint4(o[4], o[5], o[6], o[7]);
       }
     }
-    {   // Aw[p][s] = w_s x_s[p] s_x[p] s_B, split fp16 hi + lo: thread (p, s half)
-      const int pp = tid & 63, sh = (tid >> 6) * 64;
+    {   // Aw[p][s] = w_s x_s[p] s_x[p] s_B, split fp16 hi + lo: thread (p, s quarter)
+      const int pp = tid & 63, sh = (tid >> 6) * 32;
       const float fr = __fmul_rn(s_sx[pp], sB);
 #pragma unroll 2
-      for (int s8 = sh; s8 < sh + 64; s8 += 8) {
+      for (int s8 = sh; s8 < sh + 32; s8 += 8) {
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int j = 0; j < 8; j += 2) {
-          const float v0 = __fmul_rn(__fmul_rn(s_wgt[s8 + j], (float)rx[(s8 + j) * TP + pp]), fr);
-          const float v1 = __fmul_rn(__fmul_rn(s_wgt[s8 + j + 1], (float)rx[(s8 + j + 1) * TP + pp]), fr);
+          const float v0 = __fmul_rn(__fmul_rn(s_wgt[s8 + j], (float)rx[(s8 + j) * L::XR + pp]), fr);
+          const float v1 = __fmul_rn(__fmul_rn(s_wgt[s8 + j + 1], (float)rx[(s8 + j + 1) * L::XR + pp]), fr);
           const __half2 hh = __floats2half2_rn(v0, v1);
           const float2 hf = __half22float2(hh);
           hi[j >> 1] = *reinterpret_cast<const uint32_t*>(&hh);
@@ -331,19 +340,21 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     // ---- P5: outputs (staged over the Bᵀ tile) and the state update in TMEM
     float* ys = reinterpret_cast<float*>(sm + L::BTF);   // [128][64 + 4]
     {
-      const int t = tid;
+      const int t = row;
       const float et = s_et[t];
 #pragma unroll 1
-      for (int c = 0; c < TP; c += 16) {
+      for (int c = hw * 32; c < hw * 32 + 32; c += 16) {
         uint32_t vd[16], vo[16];
         tmem_ld_x16(T_YD + lane_off + c, vd);
         tmem_ld_x16(T_YO + lane_off + c, vo);
+        const uint4 xq = *reinterpret_cast<const uint4*>(rx + t * L::XR + c);   // this row's 16 x codes
+        const int8_t* xb = reinterpret_cast<const int8_t*>(&xq);
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int pp = c + j;
           const float sxp = s_sx[pp];
-          const float xh = __fmul_rn((float)rx[t * TP + pp], sxp);
+          const float xh = __fmul_rn((float)xb[j], sxp);
           ys[t * (TP + 4) + pp] = __fadd_rn(__fadd_rn(__fmul_rn(__uint_as_float(vd[j]), sxp),
                                                       __fmul_rn(__uint_as_float(vo[j]), et)),
                                             __fmul_rn(Dh, xh));
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     {
       const float eQ = expf(s_cs[TQ - 1]);   // padded tokens carry Δ = 0
 #pragma unroll
-      for (int c = 0; c < TP; c += 16) {
+      for (int c = hw * 32; c < hw * 32 + 32; c += 16) {
         uint32_t vh[16], vd[16];
         tmem_ld_x16(T_H + lane_off + c, vh);
         tmem_ld_x16(T_DH + lane_off + c, vd);
@@ -369,8 +380,8 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     {
       const int p4 = (tid & 15) * 4;
 #pragma unroll 4
-      for (int i = 0; i < TQ / 8; ++i) {
-        const int t = (tid >> 4) + 8 * i;
+      for (int i = 0; i < TQ / 16; ++i) {
+        const int t = (tid >> 4) + 16 * i;
         if (t < Qc) {
           const float4 v = *reinterpret_cast<const float4*>(&ys[t * (TP + 4) + p4]);
           const uint32_t zc = *reinterpret_cast<const uint32_t*>(rz + t * TP + p4);
@@ -388,11 +399,11 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   // ---- final state -> int8 codes [p][n] (ClusterMap-cell scales)
   {
-    const int n = tid;
+    const int n = row;
     int8_t* st = state + ((int64_t)b * p.n_heads + h) * TP * N;
     tc_fence_after();
 #pragma unroll
-    for (int c = 0; c < TP; c += 16) {
+    for (int c = hw * 32; c < hw * 32 + 32; c += 16) {
       uint32_t v[16];
       tmem_ld_x16(T_H + lane_off + c, v);
       tmem_wait_ld();
