@@ -67,6 +67,9 @@ int sq_device_supported(void);
 /* Select the A8 GEMM implementation: 0 = legacy mma.sync, 1 = tcgen05 with the W4 operand
  * expanded into TMEM (default), 2 = tcgen05 with the W4 operand expanded into shared memory. */
 int sq_set_gemm_mode(int mode);
+/* Mamba2 chunked-scan engine for prefill: 0 = warp-level mma.sync (64-token chunks, default),
+ * 1 = tcgen05 with TMEM accumulators and the f32 state in TMEM (128-token chunks, d_state 128). */
+int sq_set_ssd_mode(int mode);
 
 /* ---- weights ---------------------------------------------------------------------- */
 /* u4packed [N x K/2] (low nibble = even k) + int8 sg [N x K/group] -> kernel layout

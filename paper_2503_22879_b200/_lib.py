@@ -41,6 +41,7 @@ _SIGS = {
     "sq_last_error": ([], C.c_char_p),
     "sq_device_supported": ([], _int),
     "sq_set_gemm_mode": ([_int], _int),
+    "sq_set_ssd_mode": ([_int], _int),
     "sq_w4_bytes": ([_int, _int], _i64),
     "sq_repack_w4": ([_vp, _int, _int, _vp, _vp], _int),
     "sq_unpack_w4": ([_vp, _int, _int, _vp, _vp], _int),

@@ -18,6 +18,11 @@
 #include "common.cuh"
 
 namespace sq {
+// chunk-scan engine (sq_set_ssd_mode); SQ_SSD_TC=1 in the environment selects tcgen05 at load
+int g_ssd_mode = [] {
+  const char* e = getenv("SQ_SSD_TC");
+  return e ? atoi(e) : 0;
+}();
 
 template <typename TQ>
 struct Deq;
@@ -479,11 +484,7 @@ extern "C" int sq_ssd_scan_int8(const sq_mamba2_params* p, int B, int T, const i
   if (B == 0 || T == 0) return SQ_OK;
   if (T > 1) {   // chunked SSD on the tensor cores (ssd_chunk_tc.cu tcgen05, ssd_chunk.cu mma.sync);
                   // other shapes: sequential scan
-    static const int tc = [] {
-      const char* e = getenv("SQ_SSD_TC");
-      return e ? atoi(e) : 0;
-    }();
-    if (tc) {
+    if (g_ssd_mode == 1) {
       const int rc = launch_ssd_chunk_tc(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
                                          as_stream(stream));
       if (rc != SQ_ERR_ARG) return rc;
@@ -494,6 +495,12 @@ extern "C" int sq_ssd_scan_int8(const sq_mamba2_params* p, int B, int T, const i
   }
   return launch_mamba2<int8_t>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
                                as_stream(stream), "sq_ssd_scan_int8");
+}
+
+extern "C" int sq_set_ssd_mode(int mode) {
+  SQ_REQUIRE(mode == 0 || mode == 1, SQ_ERR_ARG, "sq_set_ssd_mode: mode must be 0 or 1");
+  g_ssd_mode = mode;
+  return SQ_OK;
 }
 
 extern "C" int sq_state_update_int8(const sq_mamba2_params* p, int B, const int8_t* x, int64_t ldx,

@@ -66,10 +66,10 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 
 // shared memory map (bytes; SW128 tiles 1024-aligned)
 struct TcSsdSmem {
-  static constexpr int RAWC = 0;                 // C codes [t][n] int8 SW128      16 KB
-  static constexpr int RAWB = RAWC + 16384;      // B codes [s][n] int8 SW128      16 KB
+  static constexpr int RAWC = 0;                 // C codes [t][n] int8 SW128, buffer k at +k*32 KB
+  static constexpr int RAWB = RAWC + 16384;      // B codes [s][n] int8 SW128, buffer k at +k*32 KB
   static constexpr int XR = 80;                  // x code row pitch (64 B + 16: conflict-free row reads)
-  static constexpr int RAWX = RAWB + 16384;      // x codes [s][p] int8, 2 buffers 2 x 10 KB
+  static constexpr int RAWX = RAWC + 65536;      // x codes [s][p] int8, 2 buffers 2 x 10 KB
   static constexpr int RAWZ = RAWX + 2 * 128 * XR;   // z codes [t][p] int8, 2 buffers 2 x 8 KB
   static constexpr int CF = RAWZ + 16384;        // C fp16 [t][n] (2 K-blocks), later W [t][s]   32 KB
   static constexpr int BTF = CF + 32768;         // Bᵀ fp16 [n][s] (2 K-blocks), later y staging 32 KB
@@ -132,8 +132,8 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     for (int i = tid; i < TQ * (N / 16); i += TC_SSD_THREADS) {
       const int r = i / (N / 16), c16 = i % (N / 16);
       const int64_t tok = tok0 + c0 + min(r, Qc - 1);
-      cpa16(sbase + L::RAWB + sw128(r, c16 * 16), Bm + tok * ldbc + grp * N + c16 * 16, r < Qc);
-      cpa16(sbase + L::RAWC + sw128(r, c16 * 16), Cm + tok * ldbc + grp * N + c16 * 16, r < Qc);
+      cpa16(sbase + L::RAWB + buf * 32768 + sw128(r, c16 * 16), Bm + tok * ldbc + grp * N + c16 * 16, r < Qc);
+      cpa16(sbase + L::RAWC + buf * 32768 + sw128(r, c16 * 16), Cm + tok * ldbc + grp * N + c16 * 16, r < Qc);
     }
     for (int i = tid; i < TQ * (TP / 16); i += TC_SSD_THREADS) {
       const int r = i / (TP / 16), c16 = (i % (TP / 16)) * 16;
@@ -172,6 +172,8 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     const int Qc = min(TQ, T - c0);
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();   // this chunk's codes landed; the previous chunk is fully consumed
+    if (c0 + TQ < T) fetch(c0 + TQ, buf ^ 1);   // a whole chunk of compute hides the next loads
+    const int rbc = buf * 32768;
     const int8_t* rx = reinterpret_cast<const int8_t*>(sm + L::RAWX + buf * 128 * L::XR);
     const int8_t* rz = reinterpret_cast<const int8_t*>(sm + L::RAWZ + buf * 8192);
     // ---- P1: Δ, fp16 operand tiles, H (fp16) for Y_off
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
       const int t = row;
 #pragma unroll
       for (int c16 = hw * (N / 32); c16 < (hw + 1) * (N / 32); ++c16) {
-        const uint4 w = *reinterpret_cast<const uint4*>(sm + L::RAWC + sw128(t, c16 * 16));
+        const uint4 w = *reinterpret_cast<const uint4*>(sm + L::RAWC + rbc + sw128(t, c16 * 16));
         uint4 o0, o1;
         s8x4_h2x2_t(w.x, o0.x, o0.y); s8x4_h2x2_t(w.y, o0.z, o0.w);
         s8x4_h2x2_t(w.z, o1.x, o1.y); s8x4_h2x2_t(w.w, o1.z, o1.w);
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
       for (int s8 = hw * 64; s8 < hw * 64 + 64; s8 += 8) {
         float f[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) f[j] = (float)*reinterpret_cast<const int8_t*>(sm + L::RAWB + sw128(s8 + j, n));
+        for (int j = 0; j < 8; ++j) f[j] = (float)*reinterpret_cast<const int8_t*>(sm + L::RAWB + rbc + sw128(s8 + j, n));
         const uint4 o = make_uint4(pack_h2(f[0], f[1]), pack_h2(f[2], f[3]), pack_h2(f[4], f[5]), pack_h2(f[6], f[7]));
         *reinterpret_cast<uint4*>(sm + L::BTF + (s8 >> 6) * N * 128 + sw128(n, (s8 & 63) * 2)) = o;
       }
@@ -240,7 +242,8 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll
-      for (int ks = 0; ks < N / 32; ++ks) mma_i8_ss(T_CB, dRC + 2 * ks, dRB + 2 * ks, ID_I8, ks > 0);
+      for (int ks = 0; ks < N / 32; ++ks)
+        mma_i8_ss(T_CB, dRC + (rbc >> 4) + 2 * ks, dRB + (rbc >> 4) + 2 * ks, ID_I8, ks > 0);
 #pragma unroll
       for (int ks = 0; ks < N / 16; ++ks) mma_f16_ss(T_YO, kdesc(dCF, TQ, ks), kdesc(dHF, TP, ks), ID_64, ks > 0);
       mma_commit(&bar[0]);
@@ -269,7 +272,6 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     __syncthreads();   // cs / wgt / et visible
     mbar_wait(&bar[0], ph);
     tc_fence_after();
-    if (c0 + TQ < T) fetch(c0 + TQ, buf ^ 1);   // B / C tiles are free once CB has completed
     // ---- P3: W (from CB) and the state-update weights Aw (hi / lo)
     {
       const int t = row;
@@ -350,15 +352,18 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
         const uint4 xq = *reinterpret_cast<const uint4*>(rx + t * L::XR + c);   // this row's 16 x codes
         const int8_t* xb = reinterpret_cast<const int8_t*>(&xq);
         tmem_wait_ld();
+        float yv[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int pp = c + j;
           const float sxp = s_sx[pp];
           const float xh = __fmul_rn((float)xb[j], sxp);
-          ys[t * (TP + 4) + pp] = __fadd_rn(__fadd_rn(__fmul_rn(__uint_as_float(vd[j]), sxp),
-                                                      __fmul_rn(__uint_as_float(vo[j]), et)),
-                                            __fmul_rn(Dh, xh));
+          yv[j] = __fadd_rn(__fadd_rn(__fmul_rn(__uint_as_float(vd[j]), sxp), __fmul_rn(__uint_as_float(vo[j]), et)),
+                            __fmul_rn(Dh, xh));
         }
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)   // 16-B stores: a quarter-warp covers all 32 banks (row pitch 68 floats)
+          *reinterpret_cast<float4*>(&ys[t * (TP + 4) + c + j]) = make_float4(yv[j], yv[j + 1], yv[j + 2], yv[j + 3]);
       }
     }
     {

@@ -347,6 +347,11 @@ def set_decode_stages(mask: int):
     _check(lib().sq_set_decode_stages(int(mask)))
 
 
+def set_ssd_mode(mode: int):
+    """Mamba2 prefill chunk scan: 0 = mma.sync (64-token chunks), 1 = tcgen05 / TMEM (128-token chunks)."""
+    _check(lib().sq_set_ssd_mode(int(mode)))
+
+
 def set_gemm_mode(mode: int):
     """0: legacy mma.sync GEMM, 1: tcgen05 (W4 operand expanded into TMEM), 2: tcgen05 (into smem)."""
     _check(lib().sq_set_gemm_mode(int(mode)))

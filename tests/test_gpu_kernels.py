@@ -261,8 +261,16 @@ def test_gemm_w4a8_tc_repeat_deterministic(cuda, M, N, K):
         assert np.array_equal(got, int_gemm(a, ql.int8_weight().T))
 
 
+@pytest.fixture(params=[0, 1], ids=["mma_sync", "tcgen05"])
+def ssd_mode(request, cuda):
+    ops = _ops()
+    ops.set_ssd_mode(request.param)
+    yield request.param
+    ops.set_ssd_mode(0)
+
+
 @pytest.mark.parametrize("B,T,nh,G,N,seed", [(2, 300, 80, 1, 128, 0), (1, 64, 8, 2, 64, 1), (3, 129, 16, 4, 128, 2)])
-def test_ssd_chunk_scan_vs_oracle(cuda, B, T, nh, G, N, seed):
+def test_ssd_chunk_scan_vs_oracle(cuda, ssd_mode, B, T, nh, G, N, seed):
     """Tensor-core chunked SSD (sq_ssd_scan_int8, T > 1) vs the oracle's sequential f32 scan on
     the same int8 codes: y rel-err <= 5e-3, final int8 state within one step (mismatch < 2e-2),
     with and without an incoming state (chunked prefill continuation)."""
