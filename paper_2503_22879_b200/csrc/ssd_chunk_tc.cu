@@ -46,6 +46,13 @@ __device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uin
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// MN-major SW128 operand: 128-byte rows along M/N (64 fp16), 8-row (along K) swizzle atoms
+// 1024 B apart (SBO); `lbo` bytes between 64-wide M/N blocks.  A K-step of 16 advances 2048 B.
+__device__ __forceinline__ uint64_t desc_mn(const void* tile, uint32_t lbo) {
+  const uint64_t addr = smem_u32(tile);
+  return ((addr >> 4) & 0x3FFFull) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) | (64ull << 32) | (1ull << 46) |
+         (2ull << 61);
+}
 __device__ __forceinline__ void cpa16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
@@ -72,9 +79,9 @@ struct TcSsdSmem {
   static constexpr int RAWX = RAWC + 65536;      // x codes [s][p] int8, 2 buffers 2 x 10 KB
   static constexpr int RAWZ = RAWX + 2 * 128 * XR;   // z codes [t][p] int8, 2 buffers 2 x 8 KB
   static constexpr int CF = RAWZ + 16384;        // C fp16 [t][n] (2 K-blocks), later W [t][s]   32 KB
-  static constexpr int BTF = CF + 32768;         // Bᵀ fp16 [n][s] (2 K-blocks), later y staging 32 KB
-  static constexpr int XTF = BTF + 32768;        // Xᵀ fp16 [p][s] (2 K-blocks)                   16 KB
-  static constexpr int HF = XTF + 16384;         // H fp16 [p][n] (2 K-blocks), later Aw hi       16 KB
+  static constexpr int BTF = CF + 32768;         // B fp16 [s][n] MN-major (2 n-blocks), later y staging 32 KB
+  static constexpr int XTF = BTF + 32768;        // x fp16 [s][p] MN-major                        16 KB
+  static constexpr int HF = XTF + 16384;         // H fp16 [n][p] MN-major, later Aw hi [p][s]    16 KB
   static constexpr int AWL = HF + 16384;         // Aw lo fp16 [p][s] (2 K-blocks)                16 KB
   static constexpr int SMALL = AWL + 16384;      // cs, dlt, wgt, et [128] f32; lut [256]; sx [64]
   static constexpr int BAR = SMALL + 4 * 512 + 1024 + 256;
@@ -160,10 +167,13 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     tmem_wait_st();
   }
   int8_t dcode = tid < TQ ? dt[(tok0 + min(tid, T - 1)) * lddt + h] : 0;   // prefetched one chunk ahead
-  const uint64_t dCF = desc_sw128(sm + L::CF), dBT = desc_sw128(sm + L::BTF), dXT = desc_sw128(sm + L::XTF);
-  const uint64_t dHF = desc_sw128(sm + L::HF), dAL = desc_sw128(sm + L::AWL);
+  const uint64_t dCF = desc_sw128(sm + L::CF), dHF = desc_sw128(sm + L::HF), dAL = desc_sw128(sm + L::AWL);
+  const uint64_t dBN = desc_mn(sm + L::BTF, TQ * 128), dXN = desc_mn(sm + L::XTF, TQ * 128);
+  const uint64_t dHN = desc_mn(sm + L::HF, N * 128);
   const uint64_t dRC = desc_sw128(sm + L::RAWC), dRB = desc_sw128(sm + L::RAWB);
-  constexpr uint32_t ID_I8 = idesc_i8(128, 128), ID_64 = idesc_f16f32(128, 64);
+  constexpr uint32_t ID_I8 = idesc_i8(128, 128);
+  constexpr uint32_t ID_BMN = idesc_f16f32(128, 64) | (1u << 16);   // A K-major, B MN-major
+  constexpr uint32_t ID_AMN = idesc_f16f32(128, 64) | (1u << 15);   // A MN-major, B K-major
   // descriptor of K-step ks (16 fp16 = 32 B) of a two-block fp16 tile with `rows` rows
   auto kdesc = [](uint64_t d0, int rows, int ks) { return d0 + (uint64_t)((ks >> 2) * rows * 128 >> 4) + 2 * (ks & 3); };
 
@@ -200,39 +210,46 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
         *reinterpret_cast<uint4*>(sm + L::CF + blk * TQ * 128 + sw128(t, b0 + 16)) = o1;
       }
     }
-    {   // Bᵀ fp16 row n (K = s), from the B tile's column n; this thread's s half
-      const int n = row;
-#pragma unroll 2
-      for (int s8 = hw * 64; s8 < hw * 64 + 64; s8 += 8) {
-        float f[8];
+    {   // B fp16 [s][n] (MN-major: n-blocks of 64), row s = row, this thread's n half
+      const int sr = row;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) f[j] = (float)*reinterpret_cast<const int8_t*>(sm + L::RAWB + rbc + sw128(s8 + j, n));
-        const uint4 o = make_uint4(pack_h2(f[0], f[1]), pack_h2(f[2], f[3]), pack_h2(f[4], f[5]), pack_h2(f[6], f[7]));
-        *reinterpret_cast<uint4*>(sm + L::BTF + (s8 >> 6) * N * 128 + sw128(n, (s8 & 63) * 2)) = o;
+      for (int c16 = hw * (N / 32); c16 < (hw + 1) * (N / 32); ++c16) {
+        const uint4 w = *reinterpret_cast<const uint4*>(sm + L::RAWB + rbc + sw128(sr, c16 * 16));
+        uint4 o0, o1;
+        s8x4_h2x2_t(w.x, o0.x, o0.y); s8x4_h2x2_t(w.y, o0.z, o0.w);
+        s8x4_h2x2_t(w.z, o1.x, o1.y); s8x4_h2x2_t(w.w, o1.z, o1.w);
+        const int blk = c16 >> 2, b0 = (c16 & 3) * 32;
+        *reinterpret_cast<uint4*>(sm + L::BTF + blk * TQ * 128 + sw128(sr, b0)) = o0;
+        *reinterpret_cast<uint4*>(sm + L::BTF + blk * TQ * 128 + sw128(sr, b0 + 16)) = o1;
       }
     }
-    {   // Xᵀ fp16 row p (K = s): thread (p, s quarter)
-      const int pp = tid & 63, sh = (tid >> 6) * 32;
-#pragma unroll 2
-      for (int s8 = sh; s8 < sh + 32; s8 += 8) {
-        float f[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) f[j] = (float)rx[(s8 + j) * L::XR + pp];
-        const uint4 o = make_uint4(pack_h2(f[0], f[1]), pack_h2(f[2], f[3]), pack_h2(f[4], f[5]), pack_h2(f[6], f[7]));
-        *reinterpret_cast<uint4*>(sm + L::XTF + (s8 >> 6) * TP * 128 + sw128(pp, (s8 & 63) * 2)) = o;
-      }
+    {   // x fp16 [s][p] (MN-major): row s = row, this thread's 32 codes
+      const int sr = row;
+      const uint4 w0 = *reinterpret_cast<const uint4*>(rx + sr * L::XR + hw * 32);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(rx + sr * L::XR + hw * 32 + 16);
+      uint4 o0, o1, o2, o3;
+      s8x4_h2x2_t(w0.x, o0.x, o0.y); s8x4_h2x2_t(w0.y, o0.z, o0.w);
+      s8x4_h2x2_t(w0.z, o1.x, o1.y); s8x4_h2x2_t(w0.w, o1.z, o1.w);
+      s8x4_h2x2_t(w1.x, o2.x, o2.y); s8x4_h2x2_t(w1.y, o2.z, o2.w);
+      s8x4_h2x2_t(w1.z, o3.x, o3.y); s8x4_h2x2_t(w1.w, o3.z, o3.w);
+      const int b0 = hw * 64;
+      *reinterpret_cast<uint4*>(sm + L::XTF + sw128(sr, b0)) = o0;
+      *reinterpret_cast<uint4*>(sm + L::XTF + sw128(sr, b0 + 16)) = o1;
+      *reinterpret_cast<uint4*>(sm + L::XTF + sw128(sr, b0 + 32)) = o2;
+      *reinterpret_cast<uint4*>(sm + L::XTF + sw128(sr, b0 + 48)) = o3;
     }
-    {   // H fp16 [p][n]: thread n writes column n, its p half
+    {   // H fp16 [n][p] (MN-major): thread n writes its own row, its p half
       const int n = row;
 #pragma unroll
       for (int c = hw * 32; c < hw * 32 + 32; c += 16) {
         uint32_t v[16];
         tmem_ld_x16(T_H + lane_off + c, v);
         tmem_wait_ld();
+        uint32_t hv[8];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          *reinterpret_cast<__half*>(sm + L::HF + (n >> 6) * TP * 128 + sw128(c + j, (n & 63) * 2)) =
-              __float2half_rn(__uint_as_float(v[j]));
+        for (int j = 0; j < 8; ++j) hv[j] = pack_h2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        *reinterpret_cast<uint4*>(sm + L::HF + sw128(n, c * 2)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+        *reinterpret_cast<uint4*>(sm + L::HF + sw128(n, c * 2 + 16)) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
       }
     }
     fence_proxy_async_smem();
@@ -245,7 +262,7 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
       for (int ks = 0; ks < N / 32; ++ks)
         mma_i8_ss(T_CB, dRC + (rbc >> 4) + 2 * ks, dRB + (rbc >> 4) + 2 * ks, ID_I8, ks > 0);
 #pragma unroll
-      for (int ks = 0; ks < N / 16; ++ks) mma_f16_ss(T_YO, kdesc(dCF, TQ, ks), kdesc(dHF, TP, ks), ID_64, ks > 0);
+      for (int ks = 0; ks < N / 16; ++ks) mma_f16_ss(T_YO, kdesc(dCF, TQ, ks), dHN + 128 * ks, ID_BMN, ks > 0);
       mma_commit(&bar[0]);
     }
     if (warp == 1) {   // inclusive prefix of Δ·A over 128 tokens (4 per lane, in order)
@@ -330,11 +347,11 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll
-      for (int ks = 0; ks < TQ / 16; ++ks) mma_f16_ss(T_YD, kdesc(dCF, TQ, ks), kdesc(dXT, TP, ks), ID_64, ks > 0);
+      for (int ks = 0; ks < TQ / 16; ++ks) mma_f16_ss(T_YD, kdesc(dCF, TQ, ks), dXN + 128 * ks, ID_BMN, ks > 0);
 #pragma unroll
-      for (int ks = 0; ks < TQ / 16; ++ks) mma_f16_ss(T_DH, kdesc(dBT, N, ks), kdesc(dHF, TP, ks), ID_64, ks > 0);
+      for (int ks = 0; ks < TQ / 16; ++ks) mma_f16_ss(T_DH, dBN + 128 * ks, kdesc(dHF, TP, ks), ID_AMN, ks > 0);
 #pragma unroll
-      for (int ks = 0; ks < TQ / 16; ++ks) mma_f16_ss(T_DH, kdesc(dBT, N, ks), kdesc(dAL, TP, ks), ID_64, 1);
+      for (int ks = 0; ks < TQ / 16; ++ks) mma_f16_ss(T_DH, dBN + 128 * ks, kdesc(dAL, TP, ks), ID_AMN, 1);
       mma_commit(&bar[1]);
     }
     mbar_wait(&bar[1], ph);
