@@ -22,7 +22,13 @@ timeout 900 python bench.py --workload prefill27b --steps 3 > gpurun_out/bench_p
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
   --log-file gpurun_out/launches_prefill.csv python bench.py --workload prefill27b --steps 1 --warmup 3 \
   --no-cpu-baseline > gpurun_out/ncu_launch_pf.log 2>&1
-timeout 300 python scripts/prof_prefill.py all 5 > gpurun_out/prefill_kernels.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ssd_chunk|conv1d_prefill|gate_norm" -c 3 \
   -o gpurun_out/prof_prefill -f python scripts/prof_prefill.py all 1 > gpurun_out/ncu_pf.log 2>&1
+SQ_SSD_TC=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:ssd_chunk_tc -c 1 \
+  -o gpurun_out/prof_ssdtc -f python scripts/prof_prefill.py ssd 1 > gpurun_out/ncu_st.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -c 2 \
+  -o gpurun_out/prof_pgemm -f python scripts/prof_prefill.py gemm 1 > gpurun_out/ncu_pg.log 2>&1
+(timeout 300 python scripts/prof_prefill.py all 3; SQ_SSD_TC=1 timeout 300 python scripts/prof_prefill.py ssd 3 | sed 's/^ssd/ssd_tcgen05/'; \
+  timeout 300 python scripts/prof_prefill.py gemm 3) > gpurun_out/prefill_kernels.txt 2>&1
+for w in decode8b_w4a16 m1prefill28b m1decode28b; do timeout 600 python bench.py --workload $w --steps 5; done > gpurun_out/bench_other.json 2>/dev/null
 echo done

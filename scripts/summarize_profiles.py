@@ -89,7 +89,8 @@ if __name__ == "__main__":
     for src, dst in (("bench.json", "bench.json"), ("bench_ref.json", "bench_ref.json"),
                      ("bench_prefill.json", "bench_prefill.json"), ("pytest_gpu.log", "pytest_gpu.txt"),
                      ("bdk.log", "decode_kernels.txt"), ("stages.log", "decode_stages.txt"),
-                     ("prefill_kernels.txt", "prefill_kernels.txt"), ("smoke.log", "smoke.txt")):
+                     ("prefill_kernels.txt", "prefill_kernels.txt"), ("smoke.log", "smoke.txt"),
+                     ("bench_other.json", "bench_other.json")):
         p = os.path.join(OUT, src)
         if os.path.exists(p):
             open(os.path.join(PROF, f"{tag}_{dst}"), "w").write(open(p).read())
