@@ -106,18 +106,23 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def ncu_traffic(kernel_name):
-    """dram read+write bytes per launch of the dominant kernel from the committed ncu
-    --set full summary (profiles/*_prof_ring.txt, scripts/summarize_profiles.py), or None."""
+def ncu_traffic(kernel_name, pattern=None):
+    """dram read+write bytes per launch of `kernel_name` from the newest committed ncu --set full
+    summary (profiles/*.txt written by scripts/summarize_profiles.py), or None."""
     import glob
     import re
-    if not kernel_name.startswith("state_ring"):
-        return None
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*prof_ring*.txt")))
+    if pattern is None:
+        pattern = "*prof_ring*.txt" if kernel_name.startswith("state_ring") else "*prof_prefill*.txt"
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern)))
     if not files:
         return None
     txt = open(files[-1]).read()
-    m = re.search(r"dram__bytes_read.sum=([0-9.]+) (\w+); dram__bytes_write.sum=([0-9.]+) (\w+)", txt)
+    key = kernel_name.split()[0]
+    ids = [m.group(1) for m in re.finditer(r"## ID (\d+): (?:void )?(\S+)", txt) if m.group(2).startswith(key)]
+    if not ids:
+        return None
+    m = re.search(r"## raw ID %s: dram__bytes_read.sum=([0-9.]+) (\w+); dram__bytes_write.sum=([0-9.]+) (\w+)" % ids[0],
+                  txt)
     if not m:
         return None
     unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -166,6 +171,17 @@ def cpu_decode_sample(dims, profile, batch, layers_sample=2, seed=0):
     return dt
 
 
+def _oracle_qblock(qb, od):
+    """The oracle's QBlock for a synthetic product QBlock (Mamba2 or Mamba1 fields)."""
+    from oracle import qblock as oq
+    ql = lambda q: None if q is None else oq.QLinear(**vars(q))   # noqa: E731
+    return oq.QBlock(od, qb.profile, ql(qb.in_proj), ql(qb.out_proj), qb.conv_weight, qb.conv_bias, qb.a_log,
+                     qb.d_param, qb.dt_bias, qb.norm_weight, qb.head_group, x_proj=ql(getattr(qb, "x_proj", None)),
+                     dt_proj=ql(getattr(qb, "dt_proj", None)), s_u=qb.s_u, in_out_scale=qb.in_out_scale,
+                     conv_in_scale=qb.conv_in_scale, conv_out_scale=qb.conv_out_scale, state_scale=qb.state_scale,
+                     s_y=qb.s_y, xproj_out_scale=getattr(qb, "xproj_out_scale", None), s_dt=getattr(qb, "s_dt", 1.0))
+
+
 def cpu_prefill_sample(dims, profile, tokens, seed=0):
     """Time the oracle (numpy port) prefill of one full-width layer over `tokens` tokens of one
     sequence (chunked SSD path); returns seconds per token per layer."""
@@ -176,10 +192,7 @@ def cpu_prefill_sample(dims, profile, tokens, seed=0):
     d = Dims(*dims)
     od = ODims(*dims)
     qb = synth.random_qblock(d, profile, seed)
-    oqb = oq.QBlock(od, qb.profile, oq.QLinear(**vars(qb.in_proj)), oq.QLinear(**vars(qb.out_proj)),
-                    qb.conv_weight, qb.conv_bias, qb.a_log, qb.d_param, qb.dt_bias, qb.norm_weight, qb.head_group,
-                    s_u=qb.s_u, in_out_scale=qb.in_out_scale, conv_in_scale=qb.conv_in_scale,
-                    conv_out_scale=qb.conv_out_scale, state_scale=qb.state_scale, s_y=qb.s_y)
+    oqb = _oracle_qblock(qb, od)
     u = np.random.default_rng(seed).standard_normal((tokens, d.d_model)).astype(np.float32)
     t0 = time.perf_counter()
     oq.block_forward_quantized(u, oqb)
@@ -338,7 +351,7 @@ def run_prefill(args, wl, world, rank, local):
                            "l2": "activations 16384 x 10576 int8 per layer exceed L2; no flush"},
                 "roofline": {"bound": "hbm", "kernel": "ssd_chunk_kernel (chunked int8 SSD scan, mma.sync)",
                              "achieved": ssd_gbs, "peak": hbm, "unit": "GB/s", "frac": ssd_gbs / hbm,
-                             "traffic": None, "peak_kind": pk_kind,
+                             "traffic": ncu_traffic("ssd_chunk_kernel<128>"), "peak_kind": pk_kind,
                              "algorithmic_bytes_per_launch": ssd_bytes, "launch_ms": ssd_ms},
                 "roofline_gemm": {"bound": "tensor", "kernel": "gemm_tc_kernel (in_proj W8A8, tcgen05 kind::i8)",
                                   "achieved": achieved, "peak": bf16 * 2, "unit": "TOP/s", "frac": achieved / (bf16 * 2),

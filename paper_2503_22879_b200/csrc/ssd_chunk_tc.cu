@@ -84,7 +84,7 @@ struct TcSsdSmem {
   static constexpr int HF = XTF + 16384;         // H fp16 [n][p] MN-major, later Aw hi [p][s]    16 KB
   static constexpr int AWL = HF + 16384;         // Aw lo fp16 [p][s] (2 K-blocks)                16 KB
   static constexpr int SMALL = AWL + 16384;      // cs, dlt, wgt, et [128] f32; lut [256]; sx [64]
-  static constexpr int BAR = SMALL + 4 * 512 + 1024 + 256;
+  static constexpr int BAR = SMALL + 4 * 512 + 1024 + 256 + 1024;   // + cs·log2e, s_B s_C Δ [128] each
   static constexpr int BYTES = BAR + 64;
   static constexpr int ALLOC = BYTES + 1024;     // + alignment slack
 };
@@ -104,6 +104,8 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
   float* s_et = s_wgt + TQ;
   float* s_lut = s_et + TQ;            // 256
   float* s_sx = s_lut + 256;           // 64
+  float* s_cs2 = s_sx + 64;            // cs · log2(e)  [128]
+  float* s_db = s_cs2 + TQ;            // s_B s_C Δ     [128]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);   // [0] MMA group 1, [1] MMA group 2
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 4);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -282,6 +284,8 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
       for (int j = 0; j < 4; ++j) {
         const int t = 4 * lane + j;
         s_cs[t] = vv[j];
+        s_cs2[t] = __fmul_rn(vv[j], 1.4426950408889634f);
+        s_db[t] = __fmul_rn(sBC, s_dlt[t]);
         s_wgt[t] = __fmul_rn(expf(__fsub_rn(csQ, vv[j])), s_dlt[t]);
         s_et[t] = __fmul_rn(__expf(vv[j]), sC);
       }
@@ -292,7 +296,8 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
     // ---- P3: W (from CB) and the state-update weights Aw (hi / lo)
     {
       const int t = row;
-      const float cst = s_cs[t];
+      const float2 cst2 = make_float2(s_cs2[t], s_cs2[t]);
+      const float2 M1 = make_float2(-1.f, -1.f);
 #pragma unroll 1
       for (int c = hw * 64; c < hw * 64 + 64; c += 16) {
         uint32_t o[8];
@@ -306,15 +311,13 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
         tmem_ld_x16(T_CB + lane_off + c, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          float wv[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int s = c + j + e;
-            const float wt = __fmul_rn(__fmul_rn(__fmul_rn((float)(int)v[j + e], sBC), __expf(cst - s_cs[s])), s_dlt[s]);
-            wv[e] = s <= t ? wt : 0.f;
-          }
-          o[j >> 1] = pack_h2(wv[0], wv[1]);
+        for (int j = 0; j < 16; j += 2) {   // W pair (s, s+1) = CB · 2^{(cs_t - cs_s) log2 e} · s_B s_C Δ_s, packed f32x2
+          const int s = c + j;
+          const float2 d = __ffma2_rn(*reinterpret_cast<const float2*>(&s_cs2[s]), M1, cst2);
+          const float2 e2 = make_float2(ex2_approx(d.x), ex2_approx(d.y));
+          const float2 w2 = __fmul2_rn(__fmul2_rn(make_float2((float)(int)v[j], (float)(int)v[j + 1]), e2),
+                                       *reinterpret_cast<const float2*>(&s_db[s]));
+          o[j >> 1] = pack_h2(s <= t ? w2.x : 0.f, s + 1 <= t ? w2.y : 0.f);
         }
         *reinterpret_cast<uint4*>(sm + L::CF + blk * TQ * 128 + sw128(t, b0)) = make_uint4(o[0], o[1], o[2], o[3]);
         *reinterpret_cast<uint4*>(sm + L::CF + blk * TQ * 128 + sw128(t, b0 + 16)) = make_uint4(o[4], o[5], o[6], o[7]);
@@ -326,14 +329,16 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
 #pragma unroll 2
       for (int s8 = sh; s8 < sh + 32; s8 += 8) {
         uint32_t hi[4], lo[4];
+        const float2 fr2 = make_float2(fr, fr);
 #pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-          const float v0 = __fmul_rn(__fmul_rn(s_wgt[s8 + j], (float)rx[(s8 + j) * L::XR + pp]), fr);
-          const float v1 = __fmul_rn(__fmul_rn(s_wgt[s8 + j + 1], (float)rx[(s8 + j + 1) * L::XR + pp]), fr);
-          const __half2 hh = __floats2half2_rn(v0, v1);
+        for (int j = 0; j < 8; j += 2) {   // packed pairs (s, s+1)
+          const float2 xv = make_float2((float)rx[(s8 + j) * L::XR + pp], (float)rx[(s8 + j + 1) * L::XR + pp]);
+          const float2 v2 = __fmul2_rn(__fmul2_rn(*reinterpret_cast<const float2*>(&s_wgt[s8 + j]), xv), fr2);
+          const __half2 hh = __floats2half2_rn(v2.x, v2.y);
           const float2 hf = __half22float2(hh);
           hi[j >> 1] = *reinterpret_cast<const uint32_t*>(&hh);
-          lo[j >> 1] = pack_h2(v0 - hf.x, v1 - hf.y);
+          const float2 rem = __ffma2_rn(hf, make_float2(-1.f, -1.f), v2);
+          lo[j >> 1] = pack_h2(rem.x, rem.y);
         }
         const int off = (s8 >> 6) * TP * 128 + sw128(pp, (s8 & 63) * 2);
         *reinterpret_cast<uint4*>(sm + L::HF + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);   // HF reused as Aw hi
@@ -370,13 +375,16 @@ __global__ void __launch_bounds__(TC_SSD_THREADS, 1)
         const int8_t* xb = reinterpret_cast<const int8_t*>(&xq);
         tmem_wait_ld();
         float yv[16];
+        const float2 et2 = make_float2(et, et), Dh2 = make_float2(Dh, Dh);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int pp = c + j;
-          const float sxp = s_sx[pp];
-          const float xh = __fmul_rn((float)xb[j], sxp);
-          yv[j] = __fadd_rn(__fadd_rn(__fmul_rn(__uint_as_float(vd[j]), sxp), __fmul_rn(__uint_as_float(vo[j]), et)),
-                            __fmul_rn(Dh, xh));
+        for (int j = 0; j < 16; j += 2) {   // (Y_diag s_x + Y_off e_t) + D x̂, packed over p pairs
+          const float2 sx2 = *reinterpret_cast<const float2*>(&s_sx[c + j]);
+          const float2 xh = __fmul2_rn(make_float2((float)xb[j], (float)xb[j + 1]), sx2);
+          const float2 a = __fmul2_rn(make_float2(__uint_as_float(vd[j]), __uint_as_float(vd[j + 1])), sx2);
+          const float2 bo = __fmul2_rn(make_float2(__uint_as_float(vo[j]), __uint_as_float(vo[j + 1])), et2);
+          const float2 r2 = __fadd2_rn(__fadd2_rn(a, bo), __fmul2_rn(Dh2, xh));
+          yv[j] = r2.x;
+          yv[j + 1] = r2.y;
         }
 #pragma unroll
         for (int j = 0; j < 16; j += 4)   // 16-B stores: a quarter-warp covers all 32 banks (row pitch 68 floats)
