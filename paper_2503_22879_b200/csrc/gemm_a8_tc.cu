@@ -62,7 +62,7 @@ struct TcArgs {
   const float* col_scale;
   const int32_t* gsum;   // optional precomputed activation sums per 128-K block [M x K/128]
   int64_t ldg;
-  int dbg;   // profiling only (SQ_GEMM_DBG): 1 = skip the group-sum arithmetic, 2 = CTA timeline
+  int dbg;   // profiling only (SQ_GEMM_DBG): 1 = skip the group-sum arithmetic, 2 = CTA timeline, 64 = time 512 back-to-back MMAs first
 };
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -235,6 +235,21 @@ __global__ void __launch_bounds__(TC_THREADS, WMODE == WM_W8 ? 2 : 1)
     if (lane == 0) {
       // W4: A = (v+8)*sg as UINT8 (corrected in the epilogue); W8: signed x signed
       constexpr uint32_t idesc = W4 ? (idesc_i8(TC_BN, NTOK) & ~(7u << 7)) : idesc_i8(TC_BN, NTOK);
+      if ((args.dbg & 64) && blockIdx.x == 0 && split == 0) {
+        // profiling (scripts/mma_rate.sh): issue rate of back-to-back MMAs on garbage operands
+        // (the main loop's first MMA overwrites the accumulator, so results stay correct)
+        const long long c0 = clock64();
+        for (int r = 0; r < 512; ++r) {
+          const int s = (r / 4) % STAGES, ks = r % 4;
+          if (WMODE == WM_W4_TS)
+            mma_i8_ts(tmem, tmem + TC_ACOL + s * 32 + ks * 8, desc_sw128(act + s * Cfg::ACT_BYTES) + 2 * ks, idesc, 1u);
+          else
+            mma_i8_ss(tmem, desc_sw128(wsm + s * Cfg::W_BYTES) + 2 * ks, desc_sw128(act + s * Cfg::ACT_BYTES) + 2 * ks,
+                      idesc, 1u);
+        }
+        printf("gemm mma-rate N=%d NTOK=%d mode=%d: %.1f cycles per MMA issue (512 MMAs)\n", args.N, NTOK, WMODE,
+               (clock64() - c0) / 512.0);
+      }
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         const long long c0 = tl ? clock64() : 0;
