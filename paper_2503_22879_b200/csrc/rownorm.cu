@@ -7,6 +7,8 @@
 // f64 sum order moves the f32 mean across a rounding boundary (≤1 step, rare).
 // The FWHT runs the oracle's butterfly stages h = 1, 2, 4, … with identical f32
 // a+b / a-b, so the transform itself is bit-identical.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sq {
@@ -291,6 +293,129 @@ __global__ void __launch_bounds__(512) gate_norm_had_quant16_kernel(const float*
   }
 }
 
+// Gated-norm + I_q ⊗ H_1024 + quant (D = q·1024: Mamba2-2.7B / Mamba1-2.8B d_inner 5120, G9).
+// One warp per 1024-point Hadamard block, one CTA (D/1024 warps) per row in a row loop with
+// the next row prefetched.  Global loads and stores are fully coalesced (lane l moves the
+// 16 B at l·16 of every 512 B); a per-warp shared tile of 32 rows × 36 floats (conflict-free
+// for both float4 row access and scalar column access) redistributes the block so that lane l
+// first holds elements l·32 + i (stages h = 1..16 in registers), then elements i·32 + l (stages
+// h = 32..512 in registers).  No shuffles; the only CTA barrier is the row's Σy².
+// Same f32 butterflies in the oracle's stage order as gate_norm_had_quant16_kernel.
+constexpr int N1K_LD = 36;                       // tile row stride (floats)
+constexpr int N1K_WARP_FLOATS = 2 * 32 * N1K_LD + 256;   // data tile, γ tile, 1 KB of codes
+
+__device__ __forceinline__ int n1k_off(int p) { return (p >> 5) * N1K_LD + (p & 31); }   // element p -> tile
+
+__global__ void __launch_bounds__(512) gate_norm_had1k_kernel(const float* __restrict__ y, int64_t ldy,
+                                                               const float* __restrict__ gamma, float eps, float s_y,
+                                                               int D, int M, int8_t* __restrict__ out, int64_t ldo) {
+  extern __shared__ float tsm[];
+  __shared__ double red[2][16];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float* s = tsm + warp * N1K_WARP_FLOATS;
+  float* gs = s + 32 * N1K_LD;
+  uint8_t* qb = reinterpret_cast<uint8_t*>(gs + 32 * N1K_LD);
+  const int blk0 = warp * 1024;
+  // γ of this block, once, in the tile layout
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int p = e * 128 + lane * 4;
+    *reinterpret_cast<float4*>(gs + n1k_off(p)) = __ldg(reinterpret_cast<const float4*>(gamma + blk0 + p));
+  }
+  float4 cur[8];
+  int row = blockIdx.x;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) cur[e] = *reinterpret_cast<const float4*>(y + (int64_t)row * ldy + blk0 + e * 128 + lane * 4);
+  for (int it = 0; row < M; row += gridDim.x, ++it) {
+    // coalesced rows -> tile
+#pragma unroll
+    for (int e = 0; e < 8; ++e) *reinterpret_cast<float4*>(s + n1k_off(e * 128 + lane * 4)) = cur[e];
+    const int nrow = row + gridDim.x;
+    if (nrow < M) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        cur[e] = *reinterpret_cast<const float4*>(y + (int64_t)nrow * ldy + blk0 + e * 128 + lane * 4);
+    }
+    __syncwarp();
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 f = *reinterpret_cast<const float4*>(s + lane * N1K_LD + k * 4);
+      v[k * 4] = f.x; v[k * 4 + 1] = f.y; v[k * 4 + 2] = f.z; v[k * 4 + 3] = f.w;
+    }
+    double ss = 0.0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) ss += (double)v[i] * (double)v[i];
+    ss = warp_sum_d(ss);
+    if (lane == 0) red[it & 1][warp] = ss;
+    __syncthreads();
+    double tot = 0.0;
+    for (int w = 0; w < nw; ++w) tot += red[it & 1][w];   // fixed warp order: deterministic
+    const float r = rms_factor(tot, D, eps);
+    const float2 r2 = make_float2(r, r);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 g = *reinterpret_cast<const float4*>(gs + lane * N1K_LD + k * 4);
+      const float2 t0 = __fmul2_rn(__fmul2_rn(make_float2(v[k * 4], v[k * 4 + 1]), r2), make_float2(g.x, g.y));
+      const float2 t1 = __fmul2_rn(__fmul2_rn(make_float2(v[k * 4 + 2], v[k * 4 + 3]), r2), make_float2(g.z, g.w));
+      v[k * 4] = t0.x; v[k * 4 + 1] = t0.y; v[k * 4 + 2] = t1.x; v[k * 4 + 3] = t1.y;
+    }
+    // stages h = 1..16 (element bits 0..4 = register index)
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if ((i & h) == 0) {
+          const float a = v[i], b = v[i + h];
+          v[i] = __fadd_rn(a, b);
+          v[i + h] = __fsub_rn(a, b);
+        }
+    }
+    __syncwarp();   // every lane has read its row of the tile
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      *reinterpret_cast<float4*>(s + lane * N1K_LD + k * 4) = make_float4(v[k * 4], v[k * 4 + 1], v[k * 4 + 2], v[k * 4 + 3]);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = s[i * N1K_LD + lane];   // lane l: elements i·32 + l
+    // stages h = 32..512 (element bits 5..9 = register index)
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if ((i & h) == 0) {
+          const float a = v[i], b = v[i + h];
+          v[i] = __fadd_rn(a, b);
+          v[i + h] = __fsub_rn(a, b);
+        }
+    }
+    const float is = __frcp_rn(s_y);
+    const float2 is2 = make_float2(is, is);
+    bool tie = false;
+    uint32_t w[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      w[e] = quant8x4_fast(make_float2(v[e * 4], v[e * 4 + 1]), make_float2(v[e * 4 + 2], v[e * 4 + 3]), is2, is2, tie);
+    if (tie) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        w[e] = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[e] |= (uint32_t)(uint8_t)quant8(v[e * 4 + k], s_y) << (8 * k);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) qb[i * 32 + lane] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+    __syncwarp();
+    int8_t* o = out + (int64_t)row * ldo + blk0;
+    *reinterpret_cast<uint4*>(o + lane * 16) = *reinterpret_cast<const uint4*>(qb + lane * 16);
+    *reinterpret_cast<uint4*>(o + 512 + lane * 16) = *reinterpret_cast<const uint4*>(qb + 512 + lane * 16);
+    // the next row's first tile write follows these reads in program order of every lane
+    // only after the __syncwarp below
+    __syncwarp();
+  }
+}
+
 // CTAs for a row loop: every resident slot, but never more CTAs than rows.
 template <typename K>
 static int row_grid(K kern, int threads, size_t smem, int M) {
@@ -418,6 +543,9 @@ extern "C" int sq_rmsnorm_f32(const float* x, int64_t ldx, const float* gamma, f
   return check_launch("sq_rmsnorm_f32");
 }
 
+// profiling A/B (SQ_NORM_LEGACY=1): route D = q·1024 rows through gate_norm_had_quant16_kernel
+static const bool g_norm_legacy = getenv("SQ_NORM_LEGACY") != nullptr;
+
 extern "C" int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* gamma, float eps, float s_y,
                                       int hadamard, int M, int D, int8_t* out, int64_t ldo, void* stream) {
   SQ_REQUIRE(M >= 0 && D > 0 && D % 4 == 0 && D <= 16384 && ldy % 4 == 0 && ldo % 4 == 0, SQ_ERR_SHAPE,
@@ -426,6 +554,14 @@ extern "C" int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* 
   if (M == 0) return SQ_OK;
   const int blk = hadamard ? (D & -D) : 1;
   const size_t smem = (size_t)D * sizeof(float);
+  if (blk == 1024 && D / 1024 <= 16 && ldy % 4 == 0 && ldo % 16 == 0 && !g_norm_legacy) {
+    auto k1 = gate_norm_had1k_kernel;
+    const int nthr = D / 32;
+    const size_t sm1 = (size_t)(D / 1024) * N1K_WARP_FLOATS * sizeof(float);
+    if (sm1 > 48 * 1024) cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    k1<<<row_grid(k1, nthr, sm1, M), nthr, sm1, as_stream(stream)>>>(y, ldy, gamma, eps, s_y, D, M, out, ldo);
+    return check_launch("sq_gate_norm_had_quant");
+  }
   if (D % 512 == 0 && D / 16 <= 512 && ldy % 4 == 0 && ldo % 16 == 0) {
     auto k16 = gate_norm_had_quant16_kernel;
     const size_t sm16 = blk > 512 ? 2 * smem : 0;

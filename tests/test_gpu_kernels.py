@@ -139,7 +139,8 @@ def test_rmsnorm_quant(cuda, M, D):
         assert np.array_equal(gs.cpu().numpy(), got.astype(np.int32).reshape(M, -1, 128).sum(-1))
 
 
-@pytest.mark.parametrize("M,D,had", [(4, 512, True), (64, 8192, True), (8, 5120, True), (8, 512, False)])
+@pytest.mark.parametrize("M,D,had", [(4, 512, True), (64, 8192, True), (8, 5120, True), (8, 512, False),
+                                     (300, 5120, True), (45, 3072, True)])
 def test_gate_norm_had_quant(cuda, M, D, had):
     ops = _ops()
     r = _rng(5, M, D)
