@@ -601,7 +601,45 @@ __global__ void __launch_bounds__(TC_THREADS, WMODE == WM_W8 ? 2 : 1)
       const int et = threadIdx.x - 64;
       const int per16 = 16 / esz;
       const int chunks = TC_BN / per16;
-      for (int idx = et; idx < tcount * chunks; idx += 256) {
+      // residual epilogue: the read-add-write is done in batches of RU items whose residual
+      // loads are all issued before any add/store (a store may alias a later load as far as
+      // the compiler knows, so an item-at-a-time loop pays one HBM latency per item)
+      constexpr int RU = 4;
+      int idx0 = et;
+      if (args.epi == SQ_EPI_RESID) {
+        for (; idx0 + 256 * (RU - 1) < tcount * chunks; idx0 += 256 * RU) {
+          float4 o[RU];
+          float* d[RU];
+          bool fast[RU];
+#pragma unroll
+          for (int u = 0; u < RU; ++u) {
+            const int idx = idx0 + 256 * u;
+            const int ts = idx / chunks, c = idx % chunks;
+            const int m = m_tile * NTOK + tbase + ts;
+            const int n0 = n_tile * TC_BN + c * per16;
+            d[u] = reinterpret_cast<float*>(args.out) + (int64_t)m * args.ldo + n0;
+            fast[u] = m < args.M && n0 + per16 <= args.N && (reinterpret_cast<uintptr_t>(d[u]) & 15) == 0;
+            o[u] = fast[u] ? *reinterpret_cast<const float4*>(d[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < RU; ++u) {
+            const int idx = idx0 + 256 * u;
+            const int ts = idx / chunks, c = idx % chunks;
+            const float* src = reinterpret_cast<const float*>(act) + ts * TC_BN + c * per16;
+            if (fast[u]) {
+              const float4 v = *reinterpret_cast<const float4*>(src);
+              *reinterpret_cast<float4*>(d[u]) = make_float4(__fadd_rn(o[u].x, v.x), __fadd_rn(o[u].y, v.y),
+                                                             __fadd_rn(o[u].z, v.z), __fadd_rn(o[u].w, v.w));
+            } else {
+              const int m = m_tile * NTOK + tbase + ts;
+              const int n0 = n_tile * TC_BN + c * per16;
+              if (m >= args.M || n0 >= args.N) continue;
+              for (int e = 0; e < min(per16, args.N - n0); ++e) d[u][e] = __fadd_rn(d[u][e], src[e]);
+            }
+          }
+        }
+      }
+      for (int idx = idx0; idx < tcount * chunks; idx += 256) {
         const int ts = idx / chunks, c = idx % chunks;
         const int t = tbase + ts;
         const int m = m_tile * NTOK + t;
@@ -831,7 +869,12 @@ int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg,
       (!w4 && (reinterpret_cast<uintptr_t>(w) & 15)))
     return SQ_ERR_ARG;
   if (!get_encoder()) return SQ_ERR_ARG;
-  const int ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+  static const int ntok_force = [] {   // profiling: SQ_GEMM_NTOK forces the token tile
+    const char* e = getenv("SQ_GEMM_NTOK");
+    return e ? atoi(e) : 0;
+  }();
+  int ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+  if (ntok_force) ntok = ntok_force;
   const int tiles = ((N + TC_BN - 1) / TC_BN) * ((M + ntok - 1) / ntok);
   const int nkb = K / TC_BK;
   int splits = 1;
