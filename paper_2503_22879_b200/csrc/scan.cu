@@ -127,6 +127,88 @@ __global__ void __launch_bounds__(256) mamba2_scan_kernel(sq_mamba2_params p, in
   store_state<TQ, NPT>(st, sh, hs);
 }
 
+// W4A16 float path, coalesced: CTA = (head, sequence, 32-row block), warp = 8 state rows,
+// lane = CPL consecutive state columns, so every state load / store instruction of a warp
+// moves one whole contiguous row (N·4 bytes) and B / C of the lane's columns sit in CPL
+// registers for all rows.  The per-element update is mamba2_scan_kernel's (identical f32 ops,
+// bit-identical state); only y's column sum runs in a different order (lane partials, then a
+// warp butterfly).
+template <int CPL>
+__global__ void __launch_bounds__(128) mamba2_scan_f32_rows_kernel(sq_mamba2_params p, int T, const float* x,
+                                                                   int64_t ldx, const float* Bm, const float* Cm,
+                                                                   int64_t ldbc, const float* dt, int64_t lddt,
+                                                                   const float* z, int64_t ldz,
+                                                                   float* __restrict__ state, int state_in,
+                                                                   float* __restrict__ y, int64_t ldy) {
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = p.head_dim, N = p.d_state;   // N == 32 * CPL
+  const int r0 = blockIdx.z * 32 + warp * 8;
+  const int g = p.head_group[h];
+  const float A = p.A[h], Dh = p.D[h], dtb = p.dt_bias[h];
+  float* st = state + (((int64_t)b * p.n_heads + h) * P + r0) * N + lane * CPL;
+  float hs[8][CPL];
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2) {
+      if (state_in) {
+        const float2 v = *reinterpret_cast<const float2*>(st + r * N + i);
+        hs[r][i] = v.x;
+        hs[r][i + 1] = v.y;
+      } else {
+        hs[r][i] = hs[r][i + 1] = 0.f;
+      }
+    }
+  for (int t = 0; t < T; ++t) {
+    const int64_t tok = (int64_t)b * T + t;
+    const float delta = softplus_f(__fadd_rn(dt[tok * lddt + h], dtb));
+    const float dA = expf(__fmul_rn(delta, A));
+    float bv[CPL], cv[CPL], xr[8];
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2) {
+      const float2 b2 = *reinterpret_cast<const float2*>(Bm + tok * ldbc + g * N + lane * CPL + i);
+      const float2 c2 = *reinterpret_cast<const float2*>(Cm + tok * ldbc + g * N + lane * CPL + i);
+      bv[i] = b2.x; bv[i + 1] = b2.y;
+      cv[i] = c2.x; cv[i + 1] = c2.y;
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) xr[r] = x[tok * ldx + h * P + r0 + r];
+    float acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float dtx = __fmul_rn(delta, xr[r]);
+      acc[r] = 0.f;
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        hs[r][i] = __fadd_rn(__fmul_rn(dA, hs[r][i]), __fmul_rn(dtx, bv[i]));
+        acc[r] = fmaf(hs[r][i], cv[i], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+    if (lane < 8) {
+      float a = acc[0], xv = xr[0];
+#pragma unroll
+      for (int r = 1; r < 8; ++r)
+        if (lane == r) {
+          a = acc[r];
+          xv = xr[r];
+        }
+      const float yv = __fadd_rn(a, __fmul_rn(Dh, xv));
+      const int ch = h * P + r0 + lane;
+      y[tok * ldy + ch] = __fmul_rn(yv, silu_f(z[tok * ldz + ch]));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2)
+      *reinterpret_cast<float2*>(st + r * N + i) = make_float2(hs[r][i], hs[r][i + 1]);
+}
+
 template <typename TQ>
 static int launch_mamba2(const sq_mamba2_params* p, int B, int T, const TQ* x, int64_t ldx, const TQ* Bm,
                          const TQ* Cm, int64_t ldbc, const TQ* dt, int64_t lddt, const TQ* z, int64_t ldz,
@@ -522,6 +604,20 @@ extern "C" int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T, const fl
                                const float* Bm, const float* Cm, int64_t ldbc, const float* dt, int64_t lddt,
                                const float* z, int64_t ldz, float* state, int state_in, float* y, int64_t ldy,
                                void* stream) {
+  static const bool legacy = getenv("SQ_SCAN_LEGACY") != nullptr;   // profiling A/B
+  if (p && B > 0 && T > 0 && !legacy && p->head_dim % 32 == 0 && (p->d_state == 64 || p->d_state == 128 || p->d_state == 256) &&
+      p->n_heads % p->n_groups == 0 && ldbc % 2 == 0 && (reinterpret_cast<uintptr_t>(Bm) & 7) == 0 &&
+      (reinterpret_cast<uintptr_t>(Cm) & 7) == 0 && (reinterpret_cast<uintptr_t>(state) & 7) == 0) {
+    const dim3 grid(p->n_heads, B, p->head_dim / 32);
+    cudaStream_t st = as_stream(stream);
+    if (p->d_state == 64)
+      mamba2_scan_f32_rows_kernel<2><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+    else if (p->d_state == 128)
+      mamba2_scan_f32_rows_kernel<4><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+    else
+      mamba2_scan_f32_rows_kernel<8><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+    return check_launch("sq_ssd_scan_f32");
+  }
   return launch_mamba2<float>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
                               as_stream(stream), "sq_ssd_scan_f32");
 }

@@ -319,3 +319,42 @@ def test_ssd_chunk_scan_vs_oracle(cuda, ssd_mode, B, T, nh, G, N, seed):
             rq = quantize_codes(rh, s_h.reshape(nh, P)[:, :, None], 8)
             mx, frac = code_diff(st[bi], rq)
             assert mx <= 1 and frac < 2e-2, (state_in, bi, mx, frac)
+
+
+@pytest.mark.parametrize("B,T,nh,G,N", [(1, 1, 128, 8, 128), (2, 5, 16, 2, 64), (1, 16, 32, 4, 128), (2, 3, 8, 1, 256)])
+def test_ssd_scan_f32_vs_oracle(cuda, B, T, nh, G, N):
+    """W4A16 float scan (sq_ssd_scan_f32: decode T=1 at the Mamba2-8B head shape, short prompts)
+    vs the oracle's sequential f32 selective scan: y rel-err <= 1e-4; the state is the same
+    element-wise f32 recurrence (rel <= 1e-5: exp / log1p ulps), with and without an incoming state."""
+    ops = _ops()
+    r = _rng(13, B * 1000 + T, nh * 1000 + N)
+    P = 64
+    di, gn = nh * P, G * N
+    hg = (np.arange(nh) // (nh // G)).astype(np.int32)
+    A = (-np.exp(r.uniform(0, 2.7, nh))).astype(np.float32)
+    D = r.uniform(0.5, 1.5, nh).astype(np.float32)
+    dtb = (np.log(np.expm1(r.uniform(1e-3, 1e-1, nh)))).astype(np.float32)
+    x = r.standard_normal((B * T, di)).astype(np.float32)
+    Bm = r.standard_normal((B * T, gn)).astype(np.float32)
+    Cm = r.standard_normal((B * T, gn)).astype(np.float32)
+    dr = (r.standard_normal((B * T, nh)) * 0.5).astype(np.float32)
+    z = r.standard_normal((B * T, di)).astype(np.float32)
+    h0 = (r.standard_normal((B, nh, P, N)) * 0.3).astype(np.float32)
+    t = lambda a: torch.as_tensor(a, device=cuda)
+    tens = dict(hg=t(hg), A=t(A), D=t(D), dtb=t(dtb))
+    prm = ops.mamba2_params(nh, P, N, G, tens["hg"], tens["A"], tens["D"], tens["dtb"])
+    for state_in in (False, True):
+        st = t(h0.copy())
+        y = torch.empty((B * T, di), dtype=torch.float32, device=cuda)
+        ops.ssd_scan_f32(prm, B, T, t(x), t(Bm), t(Cm), t(dr), t(z), st, state_in, y)
+        y, st = y.cpu().numpy(), st.cpu().numpy()
+        for bi in range(B):
+            sl = slice(bi * T, (bi + 1) * T)
+            dA, dt = osb.discretize(dr[sl], dtb, A)
+            ry, rh = osb.selective_scan(x[sl].reshape(T, nh, P), dA, dt, Bm[sl].reshape(T, G, N),
+                                        Cm[sl].reshape(T, G, N), D, z[sl].reshape(T, nh, P),
+                                        h0[bi] if state_in else None, hg)
+            rel = np.abs(y[sl] - ry.reshape(T, di)).max() / np.abs(ry).max()
+            assert rel <= 1e-4, (state_in, bi, rel)
+            hrel = np.abs(st[bi] - rh).max() / np.abs(rh).max()
+            assert hrel <= 1e-5, (state_in, bi, hrel)
