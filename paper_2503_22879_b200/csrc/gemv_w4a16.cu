@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) gemv_w4a16_tiled_kernel(const float* __re
 // contiguous bytes.  Nibbles become floats with a byte-permute into 2^23 + v + 8 and one
 // packed subtract; products accumulate in packed f32x2 pairs (short dependency chains); the
 // 8 warps' partial row sums are added in fixed warp order (deterministic).
-template <int MT>
+template <int MT, int D>
 __global__ void __launch_bounds__(256) gemv_w4a16_q_kernel(const float* __restrict__ x, int64_t ldx,
                                                            const uint8_t* __restrict__ w,
                                                            const float* __restrict__ sgrp, int group, int M, int N,
@@ -131,19 +131,32 @@ __global__ void __launch_bounds__(256) gemv_w4a16_q_kernel(const float* __restri
   const uint8_t* wt = w + (size_t)tile * nkb * 8192 + (q * 32 + lane) * 16;   // + kb*8192 + chunk*2048
   const float* srow = sgrp + (size_t)(valid ? n : 0) * ng;
   const int npieces = nkb * 4;
-  // first weight loads before the activation staging (independent of it)
-  constexpr int D = 4;
+  // first weight loads before the activation staging (independent of it); D pieces of 512 B
+  // in flight per warp (HBM latency × per-SM bandwidth needs tens of KB in flight per SM)
   int4 buf[D];
+  float sbuf[D];   // group scale of each in-flight piece, fetched with its weights
 #pragma unroll
   for (int j = 0; j < D; ++j) {
     const int pc = warp + 8 * j;
     buf[j] = pc < npieces ? __ldg(reinterpret_cast<const int4*>(wt + (size_t)(pc >> 2) * 8192 + (pc & 3) * 2048))
                           : make_int4(0, 0, 0, 0);
+    sbuf[j] = (pc < npieces && valid) ? __ldg(srow + ((pc >> 2) * 128 + (pc & 3) * 32) / group) : 0.f;
   }
-  for (int i = threadIdx.x * 4; i < MT * K; i += blockDim.x * 4) {
-    const int m = i / K, k = i % K;
-    *reinterpret_cast<float4*>(xs + i) = m < M ? *reinterpret_cast<const float4*>(x + (int64_t)m * ldx + k)
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+  // activation staging: batches of 8 loads issued before their smem stores
+  for (int i0 = threadIdx.x * 4; i0 < MT * K; i0 += blockDim.x * 4 * 8) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x * 4;
+      const int m = i / K, k = i % K;
+      v[u] = (i < MT * K && m < M) ? *reinterpret_cast<const float4*>(x + (int64_t)m * ldx + k)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x * 4;
+      if (i < MT * K) *reinterpret_cast<float4*>(xs + i) = v[u];
+    }
   }
   __syncthreads();
   float acc[MT];
@@ -156,10 +169,13 @@ __global__ void __launch_bounds__(256) gemv_w4a16_q_kernel(const float* __restri
       const int pc = p0 + 8 * j;
       if (pc >= npieces) break;
       const int4 cur = buf[j];
+      const float s = sbuf[j];
       const int pn = pc + 8 * D;
-      if (pn < npieces) buf[j] = __ldg(reinterpret_cast<const int4*>(wt + (size_t)(pn >> 2) * 8192 + (pn & 3) * 2048));
+      if (pn < npieces) {
+        buf[j] = __ldg(reinterpret_cast<const int4*>(wt + (size_t)(pn >> 2) * 8192 + (pn & 3) * 2048));
+        sbuf[j] = valid ? __ldg(srow + ((pn >> 2) * 128 + (pn & 3) * 32) / group) : 0.f;
+      }
       const int k0 = (pc >> 2) * 128 + (pc & 3) * 32;
-      const float s = valid ? srow[k0 / group] : 0.f;
       const uint32_t pw[4] = {(uint32_t)cur.x, (uint32_t)cur.y, (uint32_t)cur.z, (uint32_t)cur.w};
       float2 pa[MT][2];
 #pragma unroll
@@ -280,9 +296,12 @@ extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4, con
     const bool quad = tiled && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     int blocks = quad ? 4 * ((N + 127) / 128) : tiled ? (N + 127) / 128 : (N + 7) / 8;
     if (!tiled && blocks > 148 * 4) blocks = 148 * 4;
+    // few CTAs (small N, e.g. out_proj): each must keep more weight bytes in flight
+    const bool deep = MT <= 2 && blocks <= 2 * 148;
 #define SQ_GV(MTV)                                                                                  \
   {                                                                                                 \
-    auto k = quad ? gemv_w4a16_q_kernel<MTV> : tiled ? gemv_w4a16_tiled_kernel<MTV> : gemv_w4a16_kernel<MTV>; \
+    auto k = quad ? (deep ? gemv_w4a16_q_kernel<MTV, 16> : gemv_w4a16_q_kernel<MTV, 8>)               \
+                  : tiled ? gemv_w4a16_tiled_kernel<MTV> : gemv_w4a16_kernel<MTV>;                    \
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     k<<<blocks, 256, smem, st>>>(x + (int64_t)m0 * ldx, ldx, w4, s_group, group, mc, N, K,          \
                                  out + (int64_t)m0 * ldo, ldo, resid);                              \
