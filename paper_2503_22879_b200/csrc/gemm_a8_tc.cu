@@ -782,7 +782,9 @@ static int launch_tc(const int8_t* a, int64_t lda, const uint8_t* w, const TcArg
   using C1 = TcCfg<NTOK, WMODE, SPLITS, 1, RAW>;
   // W8 targets two CTAs per SM (~105 KB each); W4 one CTA with the raw ring
   // (split-K keeps the one-CTA budget: its int32 reduction tile [NTOK][128] needs the room)
-  constexpr int BUDGET = (WMODE == WM_W8 && SPLITS == 1) ? 104 * 1024 : 210 * 1024;
+  // (W8 split-K with small token tiles: the [NTOK][128] int32 reduction tile is small, so it
+  //  keeps the two-CTA budget and small-batch projections spread over twice the CTAs)
+  constexpr int BUDGET = (WMODE == WM_W8 && (SPLITS == 1 || NTOK <= 32)) ? 104 * 1024 : 210 * 1024;
   constexpr int ST0 = (BUDGET - C1::RAW_BYTES - C1::SUM_BYTES - C1::SGS_BYTES) / C1::STAGE_BYTES;
   constexpr int STAGES = ST0 > 8 ? 8 : (ST0 < 2 ? 2 : ST0);
   using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES, RAW>;
@@ -878,7 +880,8 @@ int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg,
   const int tiles = ((N + TC_BN - 1) / TC_BN) * ((M + ntok - 1) / ntok);
   const int nkb = K / TC_BK;
   int splits = 1;
-  while (splits < 8 && tiles * splits * 2 <= 148 && nkb / (splits * 2) >= 4 && ntok % (splits * 2) == 0) splits *= 2;
+  const int slots = (!w4 && ntok <= 32) ? 2 * 148 : 148;   // resident CTAs (see launch_tc BUDGET)
+  while (splits < 8 && tiles * splits * 2 <= slots && nkb / (splits * 2) >= 4 && ntok % (splits * 2) == 0) splits *= 2;
   if (w4 && (nkb + splits - 1) / splits > TC_MAX_KB) return SQ_ERR_ARG;
   static const int dbg = [] {
     const char* e = getenv("SQ_GEMM_DBG");
