@@ -28,7 +28,7 @@ int check_launch(const char* what) {
 bool pdl_enabled(int cls) {
   static const int mask = [] {
     const char* e = getenv("SQ_PDL");
-    return e ? atoi(e) : 22;   // default: GEMMs, decode prep and state ring (measured best, scripts/bench_pdl.sh)
+    return e ? atoi(e) : 54;   // default: GEMMs, decode prep, state ring, b=1 chain (scripts/bench_pdl.sh)
   }();
   return (mask & cls) != 0;
 }

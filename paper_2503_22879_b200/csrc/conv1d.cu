@@ -16,11 +16,12 @@ constexpr int kMaxK = 8;
 constexpr int kSeg = 64;   // tokens per thread in the prefill kernel
 
 template <typename TIn, typename TOut, bool Q>
-__global__ void conv1d_prefill_kernel(const TIn* __restrict__ x, int64_t ldx, const float* __restrict__ w,
+__global__ void conv1d_prefill_kernel(const TIn* x, int64_t ldx, const float* __restrict__ w,
                                       const float* __restrict__ bias, const float* __restrict__ s_in,
                                       const float* __restrict__ s_out, int B, int T, int C, int Kc,
-                                      const TIn* __restrict__ cache, int cache_in, TOut* __restrict__ out,
-                                      int64_t ldo) {
+                                      const TIn* cache, int cache_in, TOut* out, int64_t ldo) {
+  pdl_trigger();
+  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int seg = blockIdx.y;
   const int b = blockIdx.z;
@@ -164,8 +165,10 @@ __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __re
 // Final cache window = last Kc-1 entries of (old cache ++ x).  Separate launch so the
 // prefill kernel's reads of the old cache never race with these writes.
 template <typename T_>
-__global__ void conv1d_cache_kernel(const T_* __restrict__ x, int64_t ldx, int B, int T, int C, int Kc,
-                                    T_* __restrict__ cache, int cache_in) {
+__global__ void conv1d_cache_kernel(const T_* x, int64_t ldx, int B, int T, int C, int Kc, T_* cache,
+                                    int cache_in) {
+  pdl_trigger();
+  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (c >= C) return;
@@ -180,10 +183,12 @@ __global__ void conv1d_cache_kernel(const T_* __restrict__ x, int64_t ldx, int B
   for (int j = 0; j < Kc - 1; ++j) cache[((int64_t)b * (Kc - 1) + j) * C + c] = nv[j];
 }
 
-__global__ void conv1d_update_kernel(const int8_t* __restrict__ x, int64_t ldx, const float* __restrict__ w,
+__global__ void conv1d_update_kernel(const int8_t* x, int64_t ldx, const float* __restrict__ w,
                                      const float* __restrict__ bias, const float* __restrict__ s_in,
-                                     const float* __restrict__ s_out, int B, int C, int Kc,
-                                     int8_t* __restrict__ cache, int8_t* __restrict__ out, int64_t ldo) {
+                                     const float* __restrict__ s_out, int B, int C, int Kc, int8_t* cache,
+                                     int8_t* out, int64_t ldo) {
+  pdl_trigger();
+  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (c >= C) return;
@@ -214,10 +219,10 @@ extern "C" int sq_conv1d_int8(const int8_t* x, int64_t ldx, const float* w, cons
     conv1d_prefill4_kernel<4><<<g, 128, 0, st>>>(x, ldx, w, bias, s_in, s_out, T, C, cache, cache_in, out, ldo);
   } else {
     dim3 g((C + 127) / 128, (T + kSeg - 1) / kSeg, B);
-    conv1d_prefill_kernel<int8_t, int8_t, true><<<g, 128, 0, st>>>(x, ldx, w, bias, s_in, s_out, B, T, C, Kc, cache,
+    launch_k(PDL_SMALL, conv1d_prefill_kernel<int8_t, int8_t, true>, g, dim3(128), 0, st, x, ldx, w, bias, s_in, s_out, B, T, C, Kc, cache,
                                                                    cache_in, out, ldo);
   }
-  if (Kc > 1) conv1d_cache_kernel<int8_t><<<dim3((C + 127) / 128, B), 128, 0, st>>>(x, ldx, B, T, C, Kc, cache, cache_in);
+  if (Kc > 1) launch_k(PDL_SMALL, conv1d_cache_kernel<int8_t>, dim3((C + 127) / 128, B), dim3(128), 0, st, x, ldx, B, T, C, Kc, cache, cache_in);
   return check_launch("sq_conv1d_int8");
 }
 
@@ -227,9 +232,9 @@ extern "C" int sq_conv1d_f32(const float* x, int64_t ldx, const float* w, const 
   if (B == 0 || T == 0) return SQ_OK;
   cudaStream_t st = as_stream(stream);
   dim3 g((C + 127) / 128, (T + kSeg - 1) / kSeg, B);
-  conv1d_prefill_kernel<float, float, false><<<g, 128, 0, st>>>(x, ldx, w, bias, nullptr, nullptr, B, T, C, Kc, cache,
+  launch_k(PDL_SMALL, conv1d_prefill_kernel<float, float, false>, g, dim3(128), 0, st, x, ldx, w, bias, (const float*)nullptr, (const float*)nullptr, B, T, C, Kc, cache,
                                                                 cache_in, out, ldo);
-  if (Kc > 1) conv1d_cache_kernel<float><<<dim3((C + 127) / 128, B), 128, 0, st>>>(x, ldx, B, T, C, Kc, cache, cache_in);
+  if (Kc > 1) launch_k(PDL_SMALL, conv1d_cache_kernel<float>, dim3((C + 127) / 128, B), dim3(128), 0, st, x, ldx, B, T, C, Kc, cache, cache_in);
   return check_launch("sq_conv1d_f32");
 }
 
@@ -238,7 +243,7 @@ extern "C" int sq_conv1d_update_int8(const int8_t* x, int64_t ldx, const float* 
                                      int8_t* out, int64_t ldo, void* stream) {
   SQ_REQUIRE(B >= 0 && C > 0 && Kc >= 1 && Kc <= kMaxK, SQ_ERR_SHAPE, "sq_conv1d_update_int8: bad shape");
   if (B == 0) return SQ_OK;
-  conv1d_update_kernel<<<dim3((C + 127) / 128, B), 128, 0, as_stream(stream)>>>(x, ldx, w, bias, s_in, s_out, B, C,
+  launch_k(PDL_SMALL8, conv1d_update_kernel, dim3((C + 127) / 128, B), dim3(128), 0, as_stream(stream), x, ldx, w, bias, s_in, s_out, B, C,
                                                                                  Kc, cache, out, ldo);
   return check_launch("sq_conv1d_update_int8");
 }

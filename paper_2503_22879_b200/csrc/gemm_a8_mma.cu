@@ -32,12 +32,14 @@ __device__ __forceinline__ void mma_s8(int (&c)[4], const uint32_t (&a)[4], cons
 }
 
 template <bool W4>
-__global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* __restrict__ a, int64_t lda,
+__global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* a, int64_t lda,
                                                           const uint8_t* __restrict__ w,
                                                           const int8_t* __restrict__ sg, int group,
                                                           const float* __restrict__ alpha, int M, int N, int K,
-                                                          int epi, void* __restrict__ out, int64_t ldo,
+                                                          int epi, void* out, int64_t ldo,
                                                           const float* __restrict__ col_scale) {
+  pdl_trigger();
+  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   __shared__ __align__(16) int8_t As[BM][PADK];
   __shared__ __align__(16) int8_t Ws[BN][PADK];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -188,9 +190,11 @@ int gemm_a8_mma(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg
                 cudaStream_t st) {
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
   if (w4)
-    gemm_a8_mma_kernel<true><<<grid, 128, 0, st>>>(a, lda, w, sg, group, alpha, M, N, K, epi, out, ldo, col_scale);
+    launch_k(PDL_SMALL8, gemm_a8_mma_kernel<true>, grid, dim3(128), 0, st, a, lda, w, sg, group, alpha, M, N, K, epi, out,
+             ldo, col_scale);
   else
-    gemm_a8_mma_kernel<false><<<grid, 128, 0, st>>>(a, lda, w, sg, group, alpha, M, N, K, epi, out, ldo, col_scale);
+    launch_k(PDL_SMALL8, gemm_a8_mma_kernel<false>, grid, dim3(128), 0, st, a, lda, w, sg, group, alpha, M, N, K, epi,
+             out, ldo, col_scale);
   return check_launch("gemm_a8_mma");
 }
 

@@ -117,10 +117,11 @@ __global__ void __launch_bounds__(256) gemv_w4a16_tiled_kernel(const float* __re
 // packed subtract; products accumulate in packed f32x2 pairs (short dependency chains); the
 // 8 warps' partial row sums are added in fixed warp order (deterministic).
 template <int MT, int D>
-__global__ void __launch_bounds__(256) gemv_w4a16_q_kernel(const float* __restrict__ x, int64_t ldx,
+__global__ void __launch_bounds__(256) gemv_w4a16_q_kernel(const float* x, int64_t ldx,
                                                            const uint8_t* __restrict__ w,
                                                            const float* __restrict__ sgrp, int group, int M, int N,
-                                                           int K, float* __restrict__ out, int64_t ldo, int resid) {
+                                                           int K, float* out, int64_t ldo, int resid) {
+  pdl_trigger();
   extern __shared__ __align__(16) float xs[];  // [MT][K]
   __shared__ float part[8][MT][32];
   const int tile = blockIdx.x >> 2, q = blockIdx.x & 3;
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(256) gemv_w4a16_q_kernel(const float* __restri
                           : make_int4(0, 0, 0, 0);
     sbuf[j] = (pc < npieces && valid) ? __ldg(srow + ((pc >> 2) * 128 + (pc & 3) * 32) / group) : 0.f;
   }
+  pdl_wait();   // weights and scales above are read-only; x / out come from earlier grids
   // activation staging: batches of 8 loads issued before their smem stores
   for (int i0 = threadIdx.x * 4; i0 < MT * K; i0 += blockDim.x * 4 * 8) {
     float4 v[8];
@@ -303,8 +305,12 @@ extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4, con
     auto k = quad ? (deep ? gemv_w4a16_q_kernel<MTV, 16> : gemv_w4a16_q_kernel<MTV, 8>)               \
                   : tiled ? gemv_w4a16_tiled_kernel<MTV> : gemv_w4a16_kernel<MTV>;                    \
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k<<<blocks, 256, smem, st>>>(x + (int64_t)m0 * ldx, ldx, w4, s_group, group, mc, N, K,          \
-                                 out + (int64_t)m0 * ldo, ldo, resid);                              \
+    if (quad)                                                                                       \
+      launch_k(PDL_SMALL, k, dim3(blocks), dim3(256), smem, st, x + (int64_t)m0 * ldx, ldx, w4, s_group, \
+               group, mc, N, K, out + (int64_t)m0 * ldo, ldo, resid);                               \
+    else                                                                                            \
+      k<<<blocks, 256, smem, st>>>(x + (int64_t)m0 * ldx, ldx, w4, s_group, group, mc, N, K,        \
+                                   out + (int64_t)m0 * ldo, ldo, resid);                            \
   }
     if (MT == 1) SQ_GV(1) else if (MT == 2) SQ_GV(2) else if (MT == 4) SQ_GV(4) else SQ_GV(8)
 #undef SQ_GV

@@ -306,9 +306,9 @@ constexpr int N1K_WARP_FLOATS = 2 * 32 * N1K_LD + 256;   // data tile, γ tile, 
 
 __device__ __forceinline__ int n1k_off(int p) { return (p >> 5) * N1K_LD + (p & 31); }   // element p -> tile
 
-__global__ void __launch_bounds__(512) gate_norm_had1k_kernel(const float* __restrict__ y, int64_t ldy,
+__global__ void __launch_bounds__(512) gate_norm_had1k_kernel(const float* y, int64_t ldy,
                                                                const float* __restrict__ gamma, float eps, float s_y,
-                                                               int D, int M, int8_t* __restrict__ out, int64_t ldo) {
+                                                               int D, int M, int8_t* out, int64_t ldo) {
   extern __shared__ float tsm[];
   __shared__ double red[2][16];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -316,12 +316,14 @@ __global__ void __launch_bounds__(512) gate_norm_had1k_kernel(const float* __res
   float* gs = s + 32 * N1K_LD;
   uint8_t* qb = reinterpret_cast<uint8_t*>(gs + 32 * N1K_LD);
   const int blk0 = warp * 1024;
-  // γ of this block, once, in the tile layout
+  pdl_trigger();
+  // γ of this block, once, in the tile layout (a weight: read before the grid dependency wait)
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int p = e * 128 + lane * 4;
     *reinterpret_cast<float4*>(gs + n1k_off(p)) = __ldg(reinterpret_cast<const float4*>(gamma + blk0 + p));
   }
+  pdl_wait();   // y comes from the previous grid (launched with PDL_SMALL)
   float4 cur[8];
   int row = blockIdx.x;
 #pragma unroll
@@ -559,7 +561,8 @@ extern "C" int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* 
     const int nthr = D / 32;
     const size_t sm1 = (size_t)(D / 1024) * N1K_WARP_FLOATS * sizeof(float);
     if (sm1 > 48 * 1024) cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-    k1<<<row_grid(k1, nthr, sm1, M), nthr, sm1, as_stream(stream)>>>(y, ldy, gamma, eps, s_y, D, M, out, ldo);
+    launch_k(PDL_SMALL8, k1, dim3(row_grid(k1, nthr, sm1, M)), dim3(nthr), sm1, as_stream(stream), y, ldy, gamma, eps, s_y,
+             D, M, out, ldo);
     return check_launch("sq_gate_norm_had_quant");
   }
   if (D % 512 == 0 && D / 16 <= 512 && ldy % 4 == 0 && ldo % 16 == 0) {

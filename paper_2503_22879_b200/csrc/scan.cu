@@ -137,9 +137,10 @@ template <int CPL>
 __global__ void __launch_bounds__(128) mamba2_scan_f32_rows_kernel(sq_mamba2_params p, int T, const float* x,
                                                                    int64_t ldx, const float* Bm, const float* Cm,
                                                                    int64_t ldbc, const float* dt, int64_t lddt,
-                                                                   const float* z, int64_t ldz,
-                                                                   float* __restrict__ state, int state_in,
-                                                                   float* __restrict__ y, int64_t ldy) {
+                                                                   const float* z, int64_t ldz, float* state,
+                                                                   int state_in, float* y, int64_t ldy) {
+  pdl_trigger();
+  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int h = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = p.head_dim, N = p.d_state;   // N == 32 * CPL
@@ -235,13 +236,13 @@ static int launch_mamba2(const sq_mamba2_params* p, int B, int T, const TQ* x, i
 
 // Mamba1: one thread per (sequence, channel); N state columns in registers.
 template <int N>
-__global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, int B, int T,
-                                                         const int8_t* __restrict__ x, int64_t ldx,
-                                                         const int8_t* __restrict__ dt, int64_t lddt,
-                                                         const int8_t* __restrict__ BC, int64_t ldbc,
-                                                         const int8_t* __restrict__ z, int64_t ldz,
-                                                         int8_t* __restrict__ state, int state_in,
-                                                         float* __restrict__ y, int64_t ldy) {
+__global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, int B, int T, const int8_t* x,
+                                                         int64_t ldx, const int8_t* dt, int64_t lddt,
+                                                         const int8_t* BC, int64_t ldbc, const int8_t* z,
+                                                         int64_t ldz, int8_t* state, int state_in, float* y,
+                                                         int64_t ldy) {
+  pdl_trigger();
+  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (c >= p.d_inner) return;
@@ -284,13 +285,13 @@ __global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, in
 // (oracle/ssm_block.py selective_scan, Mamba1 branch).  dt is the raw
 // dt_proj output; B|C come from the x_proj output row (C at +N).
 template <int N>
-__global__ void __launch_bounds__(128) mamba1_scan_f32_kernel(sq_mamba1_params p, int B, int T,
-                                                             const float* __restrict__ x, int64_t ldx,
-                                                             const float* __restrict__ dt, int64_t lddt,
-                                                             const float* __restrict__ BC, int64_t ldbc,
-                                                             const float* __restrict__ z, int64_t ldz,
-                                                             float* __restrict__ state, int state_in,
-                                                             float* __restrict__ y, int64_t ldy) {
+__global__ void __launch_bounds__(128) mamba1_scan_f32_kernel(sq_mamba1_params p, int B, int T, const float* x,
+                                                             int64_t ldx, const float* dt, int64_t lddt,
+                                                             const float* BC, int64_t ldbc, const float* z,
+                                                             int64_t ldz, float* state, int state_in, float* y,
+                                                             int64_t ldy) {
+  pdl_trigger();
+  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (c >= p.d_inner) return;
@@ -611,11 +612,11 @@ extern "C" int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T, const fl
     const dim3 grid(p->n_heads, B, p->head_dim / 32);
     cudaStream_t st = as_stream(stream);
     if (p->d_state == 64)
-      mamba2_scan_f32_rows_kernel<2><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<2>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
     else if (p->d_state == 128)
-      mamba2_scan_f32_rows_kernel<4><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<4>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
     else
-      mamba2_scan_f32_rows_kernel<8><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<8>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
     return check_launch("sq_ssd_scan_f32");
   }
   return launch_mamba2<float>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
@@ -630,7 +631,7 @@ extern "C" int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T, c
   SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan_int8: d_state must be 16 (got %d)", p->d_state);
   if (B == 0 || T == 0) return SQ_OK;
   dim3 grid((p->d_inner + 127) / 128, B);
-  mamba1_scan_kernel<16><<<grid, 128, 0, as_stream(stream)>>>(*p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz, state,
+  launch_k(PDL_SMALL8, mamba1_scan_kernel<16>, grid, dim3(128), 0, as_stream(stream), *p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz, state,
                                                               state_in, y, ldy);
   return check_launch("sq_selective_scan_int8");
 }
@@ -642,7 +643,7 @@ extern "C" int sq_selective_scan_f32(const sq_mamba1_params* p, int B, int T, co
   SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan_f32: d_state must be 16 (got %d)", p->d_state);
   if (B == 0 || T == 0) return SQ_OK;
   dim3 grid((p->d_inner + 127) / 128, B);
-  mamba1_scan_f32_kernel<16><<<grid, 128, 0, as_stream(stream)>>>(*p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz,
+  launch_k(PDL_SMALL, mamba1_scan_f32_kernel<16>, grid, dim3(128), 0, as_stream(stream), *p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz,
                                                                   state, state_in, y, ldy);
   return check_launch("sq_selective_scan_f32");
 }
