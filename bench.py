@@ -486,14 +486,14 @@ def run_decode(args, wl, world, rank, local):
                      + tiles * (4 * d.head_dim + 4) * 4          # per-row scan operands
                      + tiles * 2 * d.d_state * 4)                # B̂ | Ĉ of the head's group
     else:
-        dom_name = "ssd_scan_f32 (W4A16 fp32 state update, decode)"
+        # W4A16: the in_proj GEMV streams the most bytes of the step (61% of the launch list)
+        dom_name = "gemv_w4a16_q_kernel (in_proj W4A16, decode weight stream)"
 
         def dom(i):
             b_ = lm.blocks[i % len(lm.blocks)]
-            zf, cf = ws["zxf"], ws["convf"]
-            ops.ssd_scan_f32(b_.params, B, 1, cf[:, :di], cf[:, di:di + gn], cf[:, di + gn:],
-                             zf[:, 2 * di + 2 * gn:], zf[:, :di], states[i % len(states)].h, True, ws["y"])
-        dom_bytes = B * d.n_heads * d.head_dim * d.d_state * 8
+            b_.in_proj.a16(ws["uf"][:B], ws["zxf"][:B])
+        n_out = d.in_proj_out
+        dom_bytes = n_out * d.d_model // 2 + n_out * (d.d_model // 128) * 4 + B * (d.d_model + n_out) * 4
     for i in range(5):
         dom(i)
     torch.cuda.synchronize()
