@@ -140,7 +140,7 @@ def test_rmsnorm_quant(cuda, M, D):
 
 
 @pytest.mark.parametrize("M,D,had", [(4, 512, True), (64, 8192, True), (8, 5120, True), (8, 512, False),
-                                     (300, 5120, True), (45, 3072, True)])
+                                     (300, 5120, True), (45, 3072, True), (1, 1024, True), (5, 15360, True)])
 def test_gate_norm_had_quant(cuda, M, D, had):
     ops = _ops()
     r = _rng(5, M, D)
