@@ -98,7 +98,7 @@ class QuantizedMambaLM:
         for l, blk in enumerate(self.blocks):
             st = states[l]
             if blk.a8:
-                ugs = ws.get("u_gs")
+                ugs = ws.get("u_gs") if blk.profile == "W4A8" else None   # block sums feed W4A8 only
                 ops.rmsnorm_quant(h, self.layer_norms[l], EPS_NORM, blk.s_u, ws["u"], ugs)
                 blk.forward_codes(ws["u"], B, T, st, state_in, resid=h, ws=ws, u_gsum=ugs)
             else:

@@ -309,7 +309,7 @@ class DeviceBlock:
             xbc = zx[:, di:2 * di + 2 * gn]
             if T == 1 and state_in and self.fused_decode:
                 # conv update + int8 state update + gated norm + FWHT + quant (sq_mamba2_decode_step_int8)
-                ygs = ws.get("yq_gs")
+                ygs = ws.get("yq_gs") if self.profile == "W4A8" else None   # block sums feed W4A8 only
                 yq = ops.mamba2_decode_step_int8(self.decode_params, B, zx, state.conv_cache, state.h, ws.get("yq"),
                                                  y, ws.get("dws"), ygs)
                 if resid is not None:
