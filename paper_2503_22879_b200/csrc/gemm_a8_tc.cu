@@ -473,6 +473,13 @@ __global__ void __launch_bounds__(TC_THREADS, WMODE == WM_W8 ? 2 : 1)
             const int s = i % STAGES;
             if (WMODE == WM_W4_TS) {
               if (!(args.dbg & 4)) tmem_st_x16(tmem + ((uint32_t)(q * 32) << 16) + TC_ACOL + s * 32 + half * 16, wv[j]);
+              // publish each stage as soon as it is in TMEM, so the MMA issuer starts on the
+              // batch's first k-block while the later ones are still being stored (shorter MMA
+              // tail after the last batch); the wait covers only this warp's stores
+              tmem_wait_st();
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&full[s]);
             } else {
               // swizzled SW128 K-major tile: row r, 16-byte chunk c at ((c ^ (r&7)) * 16)
               uint8_t* base = wsm + s * Cfg::W_BYTES + (row >> 3) * 1024 + (row & 7) * 128;
@@ -486,19 +493,14 @@ __global__ void __launch_bounds__(TC_THREADS, WMODE == WM_W8 ? 2 : 1)
           }
         }
         const long long cb2 = tl ? clock64() : 0;
-        if (WMODE == WM_W4_TS) {
-          const long long c0 = tl ? clock64() : 0;
-          tmem_wait_st();
-          if (tl) c_stw += clock64() - c0;
-          tc_fence_before();
-        } else {
+        if (WMODE != WM_W4_TS) {
           fence_proxy_async_smem();
-        }
-        __syncwarp();
-        if (lane == 0) {
+          __syncwarp();
+          if (lane == 0) {
 #pragma unroll
-          for (int j = 0; j < D; ++j)
-            if (i0 + j < nkb) mbar_arrive(&full[(i0 + j) % STAGES]);
+            for (int j = 0; j < D; ++j)
+              if (i0 + j < nkb) mbar_arrive(&full[(i0 + j) % STAGES]);
+          }
         }
         if (tl) {
           const long long cb3 = clock64();
