@@ -161,7 +161,10 @@ __global__ void __launch_bounds__(TC_THREADS, WMODE == WM_W8 ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w, TcArgs args) {
   using Cfg = TcCfg<NTOK, WMODE, SPLITS, STAGES, RAW>;
   // converter batch: D k-blocks per raw-ring barrier and per TMEM-stage wait (D < STAGES, no self-wait)
-  constexpr int D = STAGES >= 8 ? 4 : (STAGES >= 4 ? 2 : 1);
+#ifndef SQ_CONV_D
+#define SQ_CONV_D 2
+#endif
+  constexpr int D = STAGES >= 8 ? SQ_CONV_D : (STAGES >= 4 ? 2 : 1);
   constexpr int RB = RAW / D;   // raw-ring batch slots
   static_assert(WMODE == WM_W8 || RAW % D == 0, "raw ring must hold whole converter batches");
   constexpr bool W4 = Cfg::W4;
