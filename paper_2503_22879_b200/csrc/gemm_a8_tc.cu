@@ -40,11 +40,11 @@ constexpr int TC_ACOL = 256;      // first TMEM column of the A (weight) stages 
 constexpr int TC_THREADS = 384;     // 12 warps: TMA, MMA, 8 converter/epilogue, group-sum, W4 stream
 constexpr int TC_MAX_KB = 64;       // max K-blocks per split (K <= 8192)
 constexpr int W4_TILE_BYTES = TC_BN * TC_BK / 2;  // 8 KB per (n-tile, k-block)
-// packed-weight ring depth for small token tiles: the HBM stream needs ~150 KB in flight per
-// SM to approach peak (Little's law at the loaded latency), so the ring takes most of smem
-// and the activation stages (L2-resident, shared by every CTA) shrink to what remains.
+// packed-weight ring depth for small token tiles (8 KB slots).  Same-box A/B of the decode step
+// with 2-k-block converter batches (scripts/ab_lib.sh): 6 / 8 / 10 / 12 / 14 / 16 slots ->
+// 15.38k / 15.43k / 15.31k / 15.17k / 14.83k / 13.80k tok/s, so 64 KB in flight per SM wins.
 #ifndef SQ_RAW64
-#define SQ_RAW64 12
+#define SQ_RAW64 8
 #endif
 constexpr int g_raw64 = SQ_RAW64;
 
