@@ -250,7 +250,10 @@ __global__ void __launch_bounds__(256) prep_kernel(const sq_mamba2_decode_params
 // ------------------------------------------------------------------ K9: streaming state update
 constexpr int SR_CONSUMERS = 8;
 constexpr int SR_THREADS = (SR_CONSUMERS + 1) * 32;
-constexpr int SR_NSLOT = 8;
+#ifndef SQ_SR_NSLOT
+#define SQ_SR_NSLOT 8
+#endif
+constexpr int SR_NSLOT = SQ_SR_NSLOT;   // state-tile ring depth per CTA (two per SM); same-box sweep 6 / 8 / 10 -> 15.19k / 15.52k / 15.13k tok/s
 template <int N>
 struct SrCfg {
   static constexpr int TILE = DS_P * N;
