@@ -472,8 +472,7 @@ def run_decode(args, wl, world, rank, local):
             b_.in_proj.a8(ws["u"][:B], ops.EPI_QUANT, ws["zx"][:B], b_.in_out_scale)
         dom_bytes = d.in_proj_out * d.d_model + B * (d.d_model + d.in_proj_out)
     elif blk.a8 and getattr(blk, "fused_decode", False):
-        dom_name = "state_ring_kernel (K9 int8 state update, decode)"
-        ops.set_decode_stages(2)
+        dom_name = "mamba2_decode_step_int8 (prep + state_ring_kernel + norm_had8192, decode)"
 
         def dom(i):
             b_ = lm.blocks[i % len(lm.blocks)]
@@ -502,7 +501,6 @@ def run_decode(args, wl, world, rank, local):
         dom(i)
     k1.record(st)
     torch.cuda.synchronize()
-    ops.set_decode_stages(7)
     dom_ms = k0.elapsed_time(k1) / reps
     hbm, bf16, pk_kind = peaks()
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQ_ABI_VERSION 1
+#define SQ_ABI_VERSION 2
 
 typedef enum {
   SQ_OK = 0,
@@ -64,16 +64,8 @@ const char* sq_last_error(void);
 /* 1 if the current device is sm_100 (B200-class) and the kernels can run. */
 int sq_device_supported(void);
 
-/* Select the A8 GEMM implementation: 0 = legacy mma.sync, 1 = tcgen05 with the W4 operand
- * expanded into TMEM (default), 2 = tcgen05 with the W4 operand expanded into shared memory. */
-int sq_set_gemm_mode(int mode);
-/* Mamba2 chunked-scan engine for prefill: 0 = warp-level mma.sync (64-token chunks, default),
- * 1 = tcgen05 with TMEM accumulators and the f32 state in TMEM (128-token chunks, d_state 128). */
-int sq_set_ssd_mode(int mode);
-
 /* ---- weights ---------------------------------------------------------------------- */
-/* u4packed [N x K/2] (low nibble = even k) + int8 sg [N x K/group] -> kernel layout
- * `dst` (sq_w4_bytes(N,K) bytes).  sg may be NULL (all ones; W4A16 layout). */
+/* u4packed [N x K/2] (low nibble = even k) -> kernel layout `dst` (sq_w4_bytes(N,K) bytes). */
 int64_t sq_w4_bytes(int N, int K);
 int sq_repack_w4(const uint8_t* u4packed, int N, int K, uint8_t* dst, void* stream);
 int sq_unpack_w4(const uint8_t* src, int N, int K, uint8_t* u4packed, void* stream);
@@ -98,14 +90,20 @@ int sq_argmax_f32(const float* logits, int64_t ld, int M, int N, int32_t* tok, v
 int sq_gemm_w8a8(const int8_t* a, int64_t lda, const int8_t* w /*[N x K]*/, const float* alpha,
                  int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
                  void* stream);
-/* a_gsum (optional, NULL = computed in the kernel): sums of the activation codes over every
- * 128-wide K block, int32 [M x K/128] with row stride ld_gsum, as emitted by
- * sq_rmsnorm_quant / sq_mamba2_decode_step_int8 for the tensor (the W4 operand is fed to
- * the tensor core as (v+8)*sg and these sums undo the offset). */
+/* W4A8 with SPEC per-group float weight scales (LEDGER G11):
+ *   y[m,n] = f32(s_a * p[m,n]),  p = fma(w_scale[n,g], f32(acc_g[m,n]), p) over groups g ascending
+ *            (f32, one rounding per group),  acc_g = sum_{k in g} a[m,k] * w4[n,k] (int32)
+ * When the kernel splits K over a cluster (sq_gemm_w4a8_splits(M,N,K) > 1), each split sums its own
+ * groups from 0 and the partials are added in split order.  w_scale is the tiled layout written by
+ * sq_tile_group_scales; SQ_EPI_I32 is not defined for per-group scales (SQ_ERR_ARG). */
 int sq_gemm_w4a8(const int8_t* a, int64_t lda, const uint8_t* w4 /*repacked*/,
-                 const int8_t* sg /*[N x K/group]*/, int group, const float* alpha,
+                 const float* w_scale /*tiled [ceil(N/128)][K/group][128]*/, int group, float s_a,
                  int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
-                 const int32_t* a_gsum, int64_t ld_gsum, void* stream);
+                 void* stream);
+int sq_gemm_w4a8_splits(int M, int N, int K);
+/* group scales [N x G] row-major -> tiled [ceil(N/128)][G][128] (sq_group_scale_elems floats) */
+int64_t sq_group_scale_elems(int N, int G);
+int sq_tile_group_scales(const float* s_group, int N, int G, float* dst, void* stream);
 /* y[m,n] (+)= sum_g s_group[n,g] * sum_{k in g} w4[n,k] * half(x[m,k]);  resid!=0 adds in place */
 int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4 /*repacked*/,
                   const float* s_group /*[N x K/group]*/, int group, int M, int N, int K,
@@ -182,9 +180,6 @@ typedef struct {
 } sq_mamba2_decode_params;
 
 int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, int B);
-/* Profiling control: which of the three decode-step launches sq_mamba2_decode_step_int8
- * issues (bitmask 1 conv+operands | 2 state update | 4 norm+FWHT+quant; default 7). */
-int sq_set_decode_stages(int mask);
 int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
                                int8_t* conv_cache /*[B x (Kc-1) x conv_dim]*/, int8_t* state,
                                void* ws, float* y, int64_t ldy, int8_t* yq, int64_t ldyq,
@@ -219,6 +214,22 @@ int sq_selective_scan_f32(const sq_mamba1_params* p, int B, int T,
 /* out[m,:] = clamp(rint(H_blk (y*rsqrt(mean y^2+eps)*gamma) / s_y)); hadamard=0 skips H. */
 int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* gamma, float eps, float s_y,
                            int hadamard, int M, int D, int8_t* out, int64_t ldo, void* stream);
+
+/* ---- SPEC float ops (ssm_block.discretize / selective_scan / ssd_chunked) --
+ * Δ = softplus(dt_raw + dt_bias) [M x H];  Ȧ = exp(Δ·A) [M x H x N] (A [H x N]; Mamba2: N = 1). */
+int sq_discretize_f32(const float* dt_raw, int64_t ld, const float* dt_bias, const float* A, int M, int H, int N,
+                      float* dA, float* delta, void* stream);
+/* Recurrence on precomputed Ȧ / Δ (selective_scan(x, Ȧ, Δ, B, C, D, z, state)); z may be NULL
+ * (no gate).  Mamba2 form: Ȧ, Δ [B*T x nh] (row stride lddt), B/C [B*T x G*N] per state group;
+ * the params' A / dt_bias are unused.  Mamba1 form: Ȧ [B*T x d_inner x N] dense, Δ [B*T x d_inner]. */
+int sq_selective_scan2_pre_f32(const sq_mamba2_params* p, int B, int T, const float* x, int64_t ldx,
+                               const float* dA, const float* delta, int64_t lddt, const float* Bm,
+                               const float* Cm, int64_t ldbc, const float* z, int64_t ldz, float* state,
+                               int state_in, float* y, int64_t ldy, void* stream);
+int sq_selective_scan1_pre_f32(const sq_mamba1_params* p, int B, int T, const float* x, int64_t ldx,
+                               const float* dA, const float* delta, int64_t lddt, const float* Bm,
+                               const float* Cm, int64_t ldbc, const float* z, int64_t ldz, float* state,
+                               int state_in, float* y, int64_t ldy, void* stream);
 
 #ifdef __cplusplus
 }

@@ -6,8 +6,12 @@ This fixes, as a format contract mirrored by the GPU kernels, every rounding
 step of the A8 path (LEDGER G5, G6, G11, G16):
 
   u_q   = rint(u / s_u)                                  per-tensor (G5)
-  acc   = Σ_k a_q[k]·w8[n,k]            (int32, exact; w8 = w4·sg for W4A8)
-  y     = f32(acc) · f32(s_ch[n]·s_a)
+  W8A8  : acc = Σ_k a_q[k]·w8[n,k] (int32, exact);  y = f32(acc) · f32(s_ch[n]·s_a)
+  W4A8  : acc_g = Σ_{k∈g} a_q[k]·w4[n,k] (int32 per 128-group, exact);
+          p = fma(s_w[n,g], f32(acc_g), p) over g ascending (f32, one rounding each, as the
+          kernels' FFMA; with a K split over S CTAs each split starts from 0 and the S
+          partials add in order);
+          y = f32(p · s_a)                                  (LEDGER G11)
   codes = clamp(rint(y / s_col[n]))     in_proj slices z|x|B|C|Δ per-tensor (G16)
   conv  : v = f32(q)·s_in[c]; acc = bias; acc += w[c,j]·v_j (j asc); silu;
           rint(silu / s_out[c])  with s_out = clustered x cells | B/C per group
@@ -30,8 +34,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from oracle import hadamard as had
-from oracle.quantizer import (int8_weight_of, quantize_codes, quantize_weight_w4_group,
-                              quantize_weight_w4a8, quantize_weight_w8)
+from oracle.quantizer import quantize_codes, quantize_weight_w4_group, quantize_weight_w8
 from oracle.ssm_block import (Dims, causal_conv1d, discretize, rmsnorm, selective_scan)
 from oracle.tensor_core import int_gemm, matmul_fast
 
@@ -40,9 +43,8 @@ from oracle.tensor_core import int_gemm, matmul_fast
 class QLinear:
     kind: str                      # "w8" | "w4a8" | "w4a16"
     codes: np.ndarray              # int8 [n_out, k] (4-bit values for w4*)
-    s_ch: np.ndarray | None = None     # [n_out]      (w8 / w4a8)
-    sg: np.ndarray | None = None       # [n_out, k/g] int (w4a8)
-    s_group: np.ndarray | None = None  # [n_out, k/g] (w4a16)
+    s_ch: np.ndarray | None = None     # [n_out]      (w8)
+    s_group: np.ndarray | None = None  # [n_out, k/g] (w4a8 / w4a16: SPEC PerGroup float scales)
     group: int = 128
 
     @property
@@ -53,20 +55,12 @@ class QLinear:
     def k(self):
         return self.codes.shape[1]
 
-    def int8_weight(self):
-        if self.kind == "w8":
-            return self.codes
-        n, k = self.codes.shape
-        g = self.group
-        return (self.codes.astype(np.int16).reshape(n, k // g, g) * self.sg.astype(np.int16)[:, :, None]
-                ).reshape(n, k).astype(np.int8)
-
     def dequant(self):
         n, k = self.codes.shape
         g = self.group
-        if self.kind == "w4a16":
+        if self.kind in ("w4a8", "w4a16"):
             return (self.codes.astype(np.float32).reshape(n, k // g, g) * self.s_group[:, :, None]).reshape(n, k)
-        return (self.int8_weight().astype(np.float32) * self.s_ch[:, None]).astype(np.float32)
+        return (self.codes.astype(np.float32) * self.s_ch[:, None]).astype(np.float32)
 
 
 def make_qlinear(w, kind: str, group: int = 128) -> QLinear:
@@ -74,22 +68,61 @@ def make_qlinear(w, kind: str, group: int = 128) -> QLinear:
     group = min(group, w.shape[1])
     if kind == "w8":
         q = quantize_weight_w8(w)
-        return QLinear("w8", q.payload, s_ch=q.extra["s_ch"], sg=np.ones((w.shape[0], 1), np.int8), group=w.shape[1])
-    if kind == "w4a8":
-        q = quantize_weight_w4a8(w, group)
-        return QLinear("w4a8", q.payload, s_ch=q.extra["s_ch"], sg=q.extra["sg"], group=group)
-    if kind == "w4a16":
+        return QLinear("w8", q.payload, s_ch=q.extra["s_ch"], group=w.shape[1])
+    if kind in ("w4a8", "w4a16"):
         q = quantize_weight_w4_group(w, group)
-        return QLinear("w4a16", q.payload, s_group=q.extra["s_group"], group=group)
+        return QLinear(kind, q.payload, s_group=q.extra["s_group"], group=group)
     raise ValueError(kind)
 
 
-def qlinear_a8(a_codes, ql: QLinear, s_a) -> tuple[np.ndarray, np.ndarray]:
-    """Exact int GEMM + f32 rescale; returns (y f32, acc int64)."""
-    acc = int_gemm(np.asarray(a_codes, np.int8), ql.int8_weight().T)
-    alpha = (ql.s_ch * np.float32(s_a)).astype(np.float32)
-    y = (acc.astype(np.float32) * alpha[None, :]).astype(np.float32)
-    return y, acc
+def group_partials(a_codes, ql: QLinear) -> np.ndarray:
+    """Exact per-group int32 partials acc_g [G, M, N] of a W4A8 projection."""
+    a = np.asarray(a_codes, np.int8)
+    n, k = ql.codes.shape
+    g = ql.group
+    return np.stack([int_gemm(a[:, i * g:(i + 1) * g], ql.codes[:, i * g:(i + 1) * g].T) for i in range(k // g)])
+
+
+def fma32(a, b, c) -> np.ndarray:
+    """f32 fused multiply-add, round(a·b + c) once.  a·b of two f32 values is exact in the x87
+    64-bit significand, and so is the sum unless c dominates a·b by > 2^18, where the extended
+    rounding can no longer land on an f32 midpoint: the f32 result is the correctly rounded one."""
+    ld = np.longdouble
+    return (np.asarray(a, np.float32).astype(ld) * np.asarray(b, np.float32).astype(ld)
+            + np.asarray(c, np.float32).astype(ld)).astype(np.float32)
+
+
+def promote_groups(accg, s_group, s_a, splits: int = 1) -> np.ndarray:
+    """W4A8 scale promotion (LEDGER G11): per split, p = fma(s_w, f32(acc_g), p) over ascending
+    groups from 0; the split partials add in split order; y = f32(p·s_a).  Bit-exact
+    restatement of the kernels (tcgen05 FFMA2 promotion and the mma.sync fallback)."""
+    G = accg.shape[0]
+    total = None
+    for s in range(splits):
+        p = np.zeros(accg.shape[1:], np.float32)
+        for i in range(s * G // splits, (s + 1) * G // splits):
+            p = fma32(s_group[None, :, i], accg[i].astype(np.float32), p)
+        total = p if total is None else (total + p).astype(np.float32)
+    return (total * np.float32(s_a)).astype(np.float32)
+
+
+# K-split policy of the device under test, (M, N, K) -> splits (tests register the kernel's
+# sq_gemm_w4a8_splits so block-level comparisons follow its summation order); default 1.
+SPLITS_FN = None
+
+
+def qlinear_a8(a_codes, ql: QLinear, s_a, splits: int | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """A8 projection; returns (y f32, acc int64).  W8A8: acc is the exact int32 GEMM over K.
+    W4A8: acc is Σ_g acc_g (the int32 total, for kernel checks) and y the promoted sum."""
+    a = np.asarray(a_codes, np.int8)
+    if splits is None:
+        splits = SPLITS_FN(a.shape[0], ql.codes.shape[0], ql.codes.shape[1]) if SPLITS_FN and ql.group == 128 else 1
+    if ql.kind == "w8":
+        acc = int_gemm(a, ql.codes.T)
+        alpha = (ql.s_ch * np.float32(s_a)).astype(np.float32)
+        return (acc.astype(np.float32) * alpha[None, :]).astype(np.float32), acc
+    accg = group_partials(a, ql)
+    return promote_groups(accg, ql.s_group, s_a, splits), accg.sum(axis=0)
 
 
 def qlinear_a16(a, ql: QLinear) -> np.ndarray:

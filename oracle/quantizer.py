@@ -9,11 +9,13 @@ Weight quantizers (LEDGER G11):
 * ``quantize_weight_w8``       — PerChannel(axis=0) 8-bit, s[n] = max|w[n,:]|/127.
 * ``quantize_weight_w4_group`` — PerGroup(axis=1, 128) 4-bit float scales
                                  (W4A16: SPEC literal).
-* ``quantize_weight_w4a8``     — PerGroup 4-bit with *progressive* scales
-                                 s[n,g] = s_ch[n] * sg[n,g], sg integer in [1,15]
-                                 (QServe/QQQ-style; PAPER.md:696 lineage), so the
-                                 A8 GEMM is an exact int32 GEMM over all K on
-                                 int8 weights w4*sg (LEDGER G11b).
+* ``quantize_weight_w4a8``     — the same SPEC PerGroup 4-bit weights (float
+                                 compute_scale per 128-group); the A8 GEMM keeps an
+                                 exact int32 accumulator per group and promotes it
+                                 with the group scale (LEDGER G11, round 2: replaces
+                                 the round-1 progressive s_ch*sg scheme, which
+                                 measured 0.14 dB worse toy-model SQNR and clamped
+                                 small groups, scripts/g11b_sqnr.py).
 """
 from __future__ import annotations
 
@@ -137,7 +139,7 @@ def quantize_weight_w8(w) -> QTensor:
     s = np.array([compute_scale(w[n], 8) for n in range(w.shape[0])], np.float32)
     lay = ScaleLayout("PerChannel", s, axis=0)
     return QTensor(w.shape, 8, quantize_codes(w, s[:, None], 8), lay,
-                   extra={"s_ch": s, "sg": np.ones((w.shape[0], 1), np.int8), "group": w.shape[1]})
+                   extra={"s_ch": s, "group": w.shape[1]})
 
 
 def quantize_weight_w4_group(w, group: int = 128) -> QTensor:
@@ -158,37 +160,6 @@ def quantize_weight_w4_group(w, group: int = 128) -> QTensor:
 
 
 def quantize_weight_w4a8(w, group: int = 128) -> QTensor:
-    """Progressive per-group 4-bit weights for the A8 GEMM (LEDGER G11b).
-
-    s_gf[n,g] = max|w[n,g]|/7 (1.0 if zero);  s_ch[n] = max_g s_gf / 15
-    (1.0 if zero);  sg = clamp(ceil(s_gf / s_ch), 1, 15);  scale = s_ch*sg;
-    codes = clamp(rint(w / scale), -8, 7).  The GEMM multiplies activations by
-    the int8 weight w8 = codes*sg (|w8| <= 120), int32 over all of K.
-    """
-    w = np.asarray(w, np.float32)
-    n, k = w.shape
-    if k % group:
-        raise ValueError("K must be a multiple of group")
-    g = k // group
-    wg = w.reshape(n, g, group)
-    s_gf = np.empty((n, g), np.float32)
-    for i in range(n):
-        for j in range(g):
-            s_gf[i, j] = compute_scale(wg[i, j], 4)
-    s_ch = np.empty(n, np.float32)
-    for i in range(n):
-        m = np.float32(s_gf[i].max())
-        s_ch[i] = np.float32(m / np.float32(15.0))
-    sg = np.clip(np.ceil(s_gf / s_ch[:, None]), 1, 15).astype(np.int8)
-    scale = (s_ch[:, None] * sg.astype(np.float32)).astype(np.float32)
-    codes = quantize_codes(wg, scale[:, :, None], 4).reshape(n, k)
-    lay = ScaleLayout("PerGroup", scale.reshape(-1), axis=1, group_size=group)
-    return QTensor(w.shape, 4, codes, lay, extra={"s_ch": s_ch, "sg": sg, "group": group})
-
-
-def int8_weight_of(qw: QTensor) -> np.ndarray:
-    """The int8 operand the A8 GEMM multiplies: codes * sg (exact)."""
-    sg = qw.extra["sg"].astype(np.int16)
-    n, k = qw.shape
-    grp = qw.extra["group"]
-    return (qw.payload.astype(np.int16).reshape(n, k // grp, grp) * sg[:, :, None]).reshape(n, k).astype(np.int8)
+    """W4A8 weights: SPEC PerGroup 4-bit with float scales, the same
+    format as W4A16; only the activation precision differs (LEDGER G11)."""
+    return quantize_weight_w4_group(w, group)

@@ -10,7 +10,7 @@ import os
 
 LIB_NAME = "libssmquant_sm100.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _i8p = C.c_void_p
 _f32p = C.c_void_p
@@ -40,8 +40,6 @@ _SIGS = {
     "sq_abi_version": ([], _int),
     "sq_last_error": ([], C.c_char_p),
     "sq_device_supported": ([], _int),
-    "sq_set_gemm_mode": ([_int], _int),
-    "sq_set_ssd_mode": ([_int], _int),
     "sq_w4_bytes": ([_int, _int], _i64),
     "sq_repack_w4": ([_vp, _int, _int, _vp, _vp], _int),
     "sq_unpack_w4": ([_vp, _int, _int, _vp, _vp], _int),
@@ -51,7 +49,10 @@ _SIGS = {
     "sq_embed_int8": ([_vp, _vp, _vp, _int, _int, _vp, _vp], _int),
     "sq_argmax_f32": ([_vp, _i64, _int, _int, _vp, _vp], _int),
     "sq_gemm_w8a8": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp], _int),
-    "sq_gemm_w4a8": ([_vp, _i64, _vp, _vp, _int, _vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp, _i64, _vp], _int),
+    "sq_gemm_w4a8": ([_vp, _i64, _vp, _vp, _int, _flt, _int, _int, _int, _int, _vp, _i64, _vp, _vp], _int),
+    "sq_gemm_w4a8_splits": ([_int, _int, _int], _int),
+    "sq_group_scale_elems": ([_int, _int], _i64),
+    "sq_tile_group_scales": ([_vp, _int, _int, _vp, _vp], _int),
     "sq_gemv_w4a16": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _int, _vp], _int),
     "sq_conv1d_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _i64, _vp], _int),
     "sq_conv1d_update_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _vp, _vp, _i64, _vp], _int),
@@ -67,10 +68,14 @@ _SIGS = {
     "sq_selective_scan_f32": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                                 _vp, _int, _vp, _i64, _vp], _int),
     "sq_mamba2_decode_ws_bytes": ([C.POINTER(Mamba2DecodeParams), _int], _i64),
-    "sq_set_decode_stages": ([_int], _int),
     "sq_mamba2_decode_step_int8": ([C.POINTER(Mamba2DecodeParams), _int, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp,
                                     _i64, _vp, _i64, _vp], _int),
     "sq_gate_norm_had_quant": ([_vp, _i64, _vp, _flt, _flt, _int, _int, _int, _vp, _i64, _vp], _int),
+    "sq_discretize_f32": ([_vp, _i64, _vp, _vp, _int, _int, _int, _vp, _vp, _vp], _int),
+    "sq_selective_scan2_pre_f32": ([C.POINTER(Mamba2Params), _int, _int, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
+                                    _vp, _i64, _vp, _int, _vp, _i64, _vp], _int),
+    "sq_selective_scan1_pre_f32": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
+                                    _vp, _i64, _vp, _int, _vp, _i64, _vp], _int),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -169,8 +169,6 @@ def write_quant_model(qm, path: str) -> None:
         for f in ("s_ch", "s_group"):
             if getattr(ql, f) is not None:
                 t[f"{prefix}.{f}"] = np.asarray(getattr(ql, f), np.float32)
-        if ql.sg is not None:
-            t[f"{prefix}.sg"] = np.asarray(ql.sg, np.int8)
 
     put_ql("head", qm.head)
     for i, (ln, b) in enumerate(zip(qm.layer_norms, qm.blocks)):

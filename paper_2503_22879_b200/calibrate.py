@@ -187,10 +187,18 @@ def calibrate_site_scale(stats: CalibStats, bits: int = 8, clip_percentile=None)
     return compute_scale(stats.channel_max, bits)
 
 
-def collect_stats(model, tokens, device="cuda"):
+SITES = ("u", "z", "x_in", "B_in", "C_in", "dt", "x", "B", "C", "h", "dt_low", "y", "r", "y_had", "head_in")
+
+
+def collect_stats(model, tokens, sites=None, device="cuda"):
     """per layer, per calibration site, channel maxima over all samples.
     Runs the float model (``float_path.float_forward``) on ``device``; returns one dict of
-    CalibStats per block plus the head input site at index -1."""
+    CalibStats per block plus the head input site at index -1.  ``sites``
+    restricts the taps kept (names in ``SITES``); None keeps every site."""
+    if sites is not None:
+        unknown = set(sites) - set(SITES)
+        if unknown:
+            raise CalibrationError(f"unknown calibration sites {sorted(unknown)}")
     from .float_path import float_forward
     tokens = np.asarray(tokens)
     if tokens.ndim != 2 or tokens.shape[0] == 0:
@@ -202,9 +210,11 @@ def collect_stats(model, tokens, device="cuda"):
         float_forward(model, tokens[s], taps, device=device)
         for l in range(L + 1):
             for k, v in taps[l].items():
+                if sites is not None and k not in sites:
+                    continue
                 ch = tuple(v.shape) if k == "h" else tuple(v.shape[1:])
                 st = stats_of(v[None] if k == "h" else v, ch)
                 stats[l][k] = st if k not in stats[l] else stats[l][k].merge(st)
-    if any(not s for s in stats):
+    if sites is None and any(not s for s in stats):
         raise ShapeError("calibration produced no statistics")
     return stats

@@ -96,14 +96,10 @@ def make_qlinear(w, kind: str, group: int = 128) -> QLinear:
     n = lambda t: t.cpu().numpy()   # noqa: E731
     if kind == "w8":
         q = quantize_weight_w8(w)
-        return QLinear("w8", n(q.payload), s_ch=n(q.extra["s_ch"]), sg=np.ones((w.shape[0], 1), np.int8),
-                       group=w.shape[1])
-    if kind == "w4a8":
-        q = quantize_weight_w4a8(w, group)
-        return QLinear("w4a8", n(q.payload), s_ch=n(q.extra["s_ch"]), sg=n(q.extra["sg"]), group=group)
-    if kind == "w4a16":
-        q = quantize_weight_w4(w, group)
-        return QLinear("w4a16", n(q.payload), s_group=n(q.extra["s_group"]), group=group)
+        return QLinear("w8", n(q.payload), s_ch=n(q.extra["s_ch"]), group=w.shape[1])
+    if kind in ("w4a8", "w4a16"):
+        q = quantize_weight_w4a8(w, group) if kind == "w4a8" else quantize_weight_w4(w, group)
+        return QLinear(kind, n(q.payload), s_group=n(q.extra["s_group"]), group=group)
     raise PipelineError(f"unknown weight kind {kind}")
 
 
@@ -193,7 +189,7 @@ def cmd_quantize(model: FloatModel, tokens, profiles, m=4, n=4, hadamard=True, r
         profiles = [profiles] * len(model.blocks)
     if len(profiles) != len(model.blocks):
         raise PipelineError("one profile per block")
-    stats = stats if stats is not None else cal.collect_stats(model, tokens, device)
+    stats = stats if stats is not None else cal.collect_stats(model, tokens, device=device)
     blocks = [quantize_block(b, stats[l], profiles[l], m, n, hadamard, reorder, seed)
               for l, b in enumerate(model.blocks)]
     emb = np.asarray(model.embedding, np.float32)

@@ -25,13 +25,12 @@ int check_launch(const char* what) {
   return SQ_OK;
 }
 
-bool pdl_enabled(int cls) {
-  static const int mask = [] {
-    const char* e = getenv("SQ_PDL");
-    return e ? atoi(e) : 54;   // default: GEMMs, decode prep, state ring, b=1 chain (scripts/bench_pdl.sh)
-  }();
-  return (mask & cls) != 0;
-}
+// Kernel classes launched with programmatic dependent launch: a build-time choice
+// (-DSQ_PDL_MASK=m for A/B builds); default GEMMs, decode prep, state ring, b=1 f32 chain.
+#ifndef SQ_PDL_MASK
+#define SQ_PDL_MASK 54
+#endif
+bool pdl_enabled(int cls) { return (SQ_PDL_MASK & cls) != 0; }
 
 }  // namespace sq
 

@@ -28,6 +28,8 @@
 // tested with mismatch fractions in tests/test_gpu_decode.py.
 #include <cstdlib>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -35,11 +37,10 @@ namespace sq {
 using namespace sm100;
 
 constexpr int DS_P = 64;
-// profiling control (sq_set_decode_stages): bitmask of the launches issued, 1 prep | 2 state | 4 norm
-static int g_decode_stages = [] {
-  const char* e = getenv("SQ_DECODE_STAGES");
-  return e ? atoi(e) : 7;
-}();
+// profiling builds only (-DSQ_DECODE_STAGES=m): bitmask of the launches issued, 1 prep | 2 state | 4 norm
+#ifndef SQ_DECODE_STAGES
+#define SQ_DECODE_STAGES 7
+#endif
 constexpr int DS_MAXCH = 1024;   // channels per norm CTA
 constexpr int ST_THREADS = 256;
 constexpr int ST_HEADS = 4;      // heads per state CTA
@@ -719,7 +720,7 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
   if (B == 0) return SQ_OK;
   cudaStream_t st = as_stream(stream);
   float* wsf = reinterpret_cast<float*>(ws);
-  const int stages = g_decode_stages;
+  constexpr int stages = SQ_DECODE_STAGES;
   const int vec = p->conv_kernel == 4 && C % 4 == 0 && ldzx % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(zx) & 3) == 0 && (reinterpret_cast<uintptr_t>(conv_cache) & 3) == 0;
   const int per_blk = vec ? 1024 : 256;
@@ -727,17 +728,21 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
     launch_k(PDL_PREP, prep_kernel, dim3((C + per_blk - 1) / per_blk, B), dim3(256), 0, st, *p, C, di, GN, zx, ldzx, conv_cache,
              wsf, B, vec);
   auto ring = [&](auto kern, int smem) {
-    static int grid_cache[2] = {0, 0};
-    int& g = grid_cache[smem == SrCfg<128>::SMEM ? 1 : 0];
-    if (g == 0) {
+    // per device (a process may drive several GPUs): smem attribute + resident-CTA count
+    static std::once_flag once[2][64];
+    static int grid_cache[2][64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int kind = smem == SrCfg<128>::SMEM ? 1 : 0;
+    std::call_once(once[kind][dev & 63], [&] {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      int per_sm = 0, dev = 0, sms = 148;
-      cudaGetDevice(&dev);
+      int per_sm = 0, sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SR_THREADS, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-      g = sms * per_sm;
-    }
+      grid_cache[kind][dev & 63] = sms * per_sm;
+    });
+    const int g = grid_cache[kind][dev & 63];
     const int tiles = B * S.n_heads;
     launch_k(PDL_RING, kern, dim3(tiles < g ? tiles : g), dim3(SR_THREADS), smem, st, S, B, (const float*)wsf, state, y, ldy);
   };
@@ -784,8 +789,4 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
   return check_launch("sq_mamba2_decode_step_int8");
 }
 
-extern "C" int sq_set_decode_stages(int mask) {
-  SQ_REQUIRE(mask >= 0 && mask <= 7, SQ_ERR_ARG, "sq_set_decode_stages: mask must be in [0, 7]");
-  sq::g_decode_stages = mask;
-  return SQ_OK;
-}
+

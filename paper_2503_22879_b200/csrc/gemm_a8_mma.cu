@@ -1,25 +1,27 @@
-// K1/K2 baseline: A8 GEMM on the legacy warp-level tensor path (mma.sync m16n8k32 s8),
-// used for shapes the tcgen05 kernel does not take and as the bring-up reference.
+// K1/K2 fallback: A8 GEMM on the warp-level tensor path (mma.sync m16n8k32 s8), for the
+// shapes the tcgen05 kernels do not take (K not a multiple of 128, e.g. Mamba1 dt_proj K=160).
 //
-//   acc[m,n] = Σ_k a[m,k] · w8[n,k]        exact int32   (w8 = w4·sg for W4A8, LEDGER G11b)
-//   y[m,n]   = f32(acc) · alpha[n]         alpha = f32(s_ch[n] · s_a)  (fuse_scales)
-//   epilogue : i32 | f32 | int8 requant by col_scale[n] | residual add (sq_epilogue)
+//   W8A8:  acc[m,n] = sum_k a[m,k] * w8[n,k] (exact int32);  y = f32(acc) * alpha[n]
+//   W4A8:  per 'group'-wide K slice g: acc_g exact int32, promoted p = fma(s_w[n,g], f32(acc_g), p)
+//          (ascending g, one rounding), y = p * s_a — the same arithmetic as the tcgen05
+//          W4A8 kernel (gemm_w4a8.cu) and the oracle (qblock.qlinear_a8)
+//   epilogue : i32 (W8 only) | f32 | int8 requant by col_scale[n] | residual add (sq_epilogue)
 //
-// Tile 64 tokens × 128 outputs × 64 K, 4 warps (each 64×32), register double-buffered
-// global loads, W4 nibbles expanded (×sg) to int8 on the way into shared memory.
+// Tile 64 tokens x 128 outputs x 64 K, 4 warps (each 64x32), register double-buffered
+// global loads, W4 nibbles sign-extended to int8 on the way into shared memory.
 #include "common.cuh"
 
 namespace sq {
 
 constexpr int BM = 64, BN = 128, BK = 64, PADK = BK + 16;
 
-__device__ __forceinline__ uint32_t expand_w4x4(uint32_t packed16, int sg) {
-  // 2 packed bytes (4 nibbles) -> 4 int8 = nibble * sg
+__device__ __forceinline__ uint32_t expand_w4x4(uint32_t packed16) {
+  // 2 packed bytes (4 nibbles) -> 4 sign-extended int8
   uint32_t out = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     int v = ((int)(packed16 << (28 - 4 * i))) >> 28;
-    out |= ((uint32_t)(v * sg) & 0xFFu) << (8 * i);
+    out |= ((uint32_t)v & 0xFFu) << (8 * i);
   }
   return out;
 }
@@ -34,7 +36,7 @@ __device__ __forceinline__ void mma_s8(int (&c)[4], const uint32_t (&a)[4], cons
 template <bool W4>
 __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* a, int64_t lda,
                                                           const uint8_t* __restrict__ w,
-                                                          const int8_t* __restrict__ sg, int group,
+                                                          const float* __restrict__ ws, int group, float s_a,
                                                           const float* __restrict__ alpha, int M, int N, int K,
                                                           int epi, void* out, int64_t ldo,
                                                           const float* __restrict__ col_scale) {
@@ -47,12 +49,16 @@ __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* a, int64
   const int ngroups = W4 ? K / group : 1;
 
   int acc[4][4][4];
+  float facc[4][4][4];   // W4: promoted per-group partial sums
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0;
+      for (int r = 0; r < 4; ++r) {
+        acc[i][j][r] = 0;
+        facc[i][j][r] = 0.f;
+      }
 
   // per-thread load assignment
   // A: 64 rows x 64 B = 256 x 16B chunks -> 2 per thread
@@ -97,28 +103,25 @@ __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* a, int64
       }
     }
   };
-  auto sstore = [&](int k0) {
+  auto sstore = [&]() {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int c = tid + i * 128;
       *reinterpret_cast<int4*>(&As[c >> 2][(c & 3) * 16]) = ra[i];
     }
     if (W4) {
-      const int gn = n0 + tid;
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int gk = k0 + i * 32;
-        const int s = (gn < N && gk < K) ? (int)sg[(int64_t)gn * ngroups + gk / group] : 0;
         const uint32_t* p = reinterpret_cast<const uint32_t*>(&rw[i]);
         int4 o0, o1;
-        o0.x = expand_w4x4(p[0] & 0xFFFF, s);
-        o0.y = expand_w4x4(p[0] >> 16, s);
-        o0.z = expand_w4x4(p[1] & 0xFFFF, s);
-        o0.w = expand_w4x4(p[1] >> 16, s);
-        o1.x = expand_w4x4(p[2] & 0xFFFF, s);
-        o1.y = expand_w4x4(p[2] >> 16, s);
-        o1.z = expand_w4x4(p[3] & 0xFFFF, s);
-        o1.w = expand_w4x4(p[3] >> 16, s);
+        o0.x = expand_w4x4(p[0] & 0xFFFF);
+        o0.y = expand_w4x4(p[0] >> 16);
+        o0.z = expand_w4x4(p[1] & 0xFFFF);
+        o0.w = expand_w4x4(p[1] >> 16);
+        o1.x = expand_w4x4(p[2] & 0xFFFF);
+        o1.y = expand_w4x4(p[2] >> 16);
+        o1.z = expand_w4x4(p[3] & 0xFFFF);
+        o1.w = expand_w4x4(p[3] >> 16);
         *reinterpret_cast<int4*>(&Ws[tid][i * 32]) = o0;
         *reinterpret_cast<int4*>(&Ws[tid][i * 32 + 16]) = o1;
       }
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* a, int64
   gload(0);
   for (int k0 = 0; k0 < K; k0 += BK) {
     __syncthreads();
-    sstore(k0);
+    sstore();
     __syncthreads();
     if (k0 + BK < K) gload(k0 + BK);
 #pragma unroll
@@ -156,6 +159,26 @@ __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* a, int64
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) mma_s8(acc[i][j], af[i], bf[j]);
+      if (W4 && (k0 + ks + 32) % group == 0 && k0 + ks < K) {
+        // group boundary: promote the exact int32 partials with this group's scales
+        const int gi = (k0 + ks) / group;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float sc[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = n0 + warp * 32 + j * 8 + q * 2 + e;
+            sc[e] = n < N ? ws[((int64_t)(n >> 7) * ngroups + gi) * 128 + (n & 127)] : 0.f;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              facc[i][j][r] = __fmaf_rn(sc[r & 1], (float)acc[i][j][r], facc[i][j][r]);
+              acc[i][j][r] = 0;
+            }
+        }
+      }
     }
   }
 
@@ -171,10 +194,10 @@ __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* a, int64
         if (m >= M || n >= N) continue;
         const int v = acc[i][j][r];
         const int64_t o = (int64_t)m * ldo + n;
-        if (epi == SQ_EPI_I32) {
+        if (!W4 && epi == SQ_EPI_I32) {
           reinterpret_cast<int32_t*>(out)[o] = v;
         } else {
-          const float y = __fmul_rn((float)v, alpha[n]);
+          const float y = W4 ? __fmul_rn(facc[i][j][r], s_a) : __fmul_rn((float)v, alpha[n]);
           if (epi == SQ_EPI_F32)
             reinterpret_cast<float*>(out)[o] = y;
           else if (epi == SQ_EPI_QUANT)
@@ -185,16 +208,16 @@ __global__ void __launch_bounds__(128) gemm_a8_mma_kernel(const int8_t* a, int64
       }
 }
 
-int gemm_a8_mma(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg, int group, bool w4,
+int gemm_a8_mma(const int8_t* a, int64_t lda, const uint8_t* w, const float* ws, int group, float s_a, bool w4,
                 const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
                 cudaStream_t st) {
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
   if (w4)
-    launch_k(PDL_SMALL8, gemm_a8_mma_kernel<true>, grid, dim3(128), 0, st, a, lda, w, sg, group, alpha, M, N, K, epi, out,
-             ldo, col_scale);
+    launch_k(PDL_SMALL8, gemm_a8_mma_kernel<true>, grid, dim3(128), 0, st, a, lda, w, ws, group, s_a, alpha, M, N, K,
+             epi, out, ldo, col_scale);
   else
-    launch_k(PDL_SMALL8, gemm_a8_mma_kernel<false>, grid, dim3(128), 0, st, a, lda, w, sg, group, alpha, M, N, K, epi,
-             out, ldo, col_scale);
+    launch_k(PDL_SMALL8, gemm_a8_mma_kernel<false>, grid, dim3(128), 0, st, a, lda, w, ws, group, s_a, alpha, M, N, K,
+             epi, out, ldo, col_scale);
   return check_launch("gemm_a8_mma");
 }
 

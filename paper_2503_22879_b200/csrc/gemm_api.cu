@@ -2,15 +2,16 @@
 #include "common.cuh"
 
 namespace sq {
-extern int g_tc_w4_mode;
-static int g_gemm_mode = 1;   // 0: mma.sync only, 1: tcgen05 (TS for W4), 2: tcgen05 (SS for W4)
-int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg, int group, bool w4,
-               const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
-               const int32_t* a_gsum, int64_t ld_gsum, cudaStream_t st);
+int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const float* alpha, int M, int N, int K, int epi,
+               void* out, int64_t ldo, const float* col_scale, cudaStream_t st);
+int gemm_w4a8_tc(const int8_t* a, int64_t lda, const uint8_t* w4, const float* ws, float s_a, int M, int N, int K,
+                 int epi, void* out, int64_t ldo, const float* col_scale, cudaStream_t st);
+int w4a8_splits(int M, int N, int K);
+int tile_scales(const float* s, int N, int G, float* dst, cudaStream_t st);
 int64_t w4_layout_bytes(int N, int K);
 int repack_w4(const uint8_t* src, int N, int K, uint8_t* dst, cudaStream_t st);
 int unpack_w4(const uint8_t* src, int N, int K, uint8_t* dst, cudaStream_t st);
-int gemm_a8_mma(const int8_t* a, int64_t lda, const uint8_t* w, const int8_t* sg, int group, bool w4,
+int gemm_a8_mma(const int8_t* a, int64_t lda, const uint8_t* w, const float* ws, int group, float s_a, bool w4,
                 const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
                 cudaStream_t st);
 
@@ -44,40 +45,41 @@ extern "C" int sq_unpack_w4(const uint8_t* src, int N, int K, uint8_t* u4packed,
   return unpack_w4(src, N, K, u4packed, as_stream(stream));
 }
 
-extern "C" int sq_set_gemm_mode(int mode) {
-  SQ_REQUIRE(mode >= 0 && mode <= 2, SQ_ERR_ARG, "sq_set_gemm_mode: mode must be 0, 1 or 2");
-  g_gemm_mode = mode;
-  g_tc_w4_mode = mode == 2 ? 2 : 1;
-  return SQ_OK;
+extern "C" int64_t sq_group_scale_elems(int N, int G) { return (int64_t)((N + 127) / 128) * 128 * G; }
+
+extern "C" int sq_tile_group_scales(const float* s_group, int N, int G, float* dst, void* stream) {
+  SQ_REQUIRE(N > 0 && G > 0, SQ_ERR_SHAPE, "sq_tile_group_scales: bad N/G (%d,%d)", N, G);
+  return tile_scales(s_group, N, G, dst, as_stream(stream));
 }
+
+extern "C" int sq_gemm_w4a8_splits(int M, int N, int K) { return w4a8_splits(M, N, K); }
 
 extern "C" int sq_gemm_w8a8(const int8_t* a, int64_t lda, const int8_t* w, const float* alpha, int M, int N, int K,
                             int epi, void* out, int64_t ldo, const float* col_scale, void* stream) {
   int rc = check_gemm("sq_gemm_w8a8", a, lda, M, N, K, epi, ldo, col_scale);
   if (rc) return rc;
   if (M == 0) return SQ_OK;
-  if (g_gemm_mode != 0) {
-    rc = gemm_a8_tc(a, lda, reinterpret_cast<const uint8_t*>(w), nullptr, K, false, alpha, M, N, K, epi, out, ldo,
-                    col_scale, nullptr, 0, as_stream(stream));
-    if (rc != SQ_ERR_ARG) return rc;
-  }
-  return gemm_a8_mma(a, lda, reinterpret_cast<const uint8_t*>(w), nullptr, K, false, alpha, M, N, K, epi, out, ldo,
-                     col_scale, as_stream(stream));
+  rc = gemm_a8_tc(a, lda, reinterpret_cast<const uint8_t*>(w), alpha, M, N, K, epi, out, ldo, col_scale,
+                  as_stream(stream));
+  if (rc != SQ_ERR_ARG) return rc;
+  return gemm_a8_mma(a, lda, reinterpret_cast<const uint8_t*>(w), nullptr, K, 1.f, false, alpha, M, N, K, epi, out,
+                     ldo, col_scale, as_stream(stream));
 }
 
-extern "C" int sq_gemm_w4a8(const int8_t* a, int64_t lda, const uint8_t* w4, const int8_t* sg, int group,
-                            const float* alpha, int M, int N, int K, int epi, void* out, int64_t ldo,
-                            const float* col_scale, const int32_t* a_gsum, int64_t ld_gsum, void* stream) {
+extern "C" int sq_gemm_w4a8(const int8_t* a, int64_t lda, const uint8_t* w4, const float* w_scale, int group,
+                            float s_a, int M, int N, int K, int epi, void* out, int64_t ldo, const float* col_scale,
+                            void* stream) {
   int rc = check_gemm("sq_gemm_w4a8", a, lda, M, N, K, epi, ldo, col_scale);
   if (rc) return rc;
-  SQ_REQUIRE(group % 32 == 0 && K % group == 0 && sg != nullptr, SQ_ERR_LAYOUT,
+  SQ_REQUIRE(epi != SQ_EPI_I32, SQ_ERR_ARG, "sq_gemm_w4a8: per-group scales have no single int32 accumulator");
+  SQ_REQUIRE(group % 32 == 0 && K % group == 0 && w_scale != nullptr, SQ_ERR_LAYOUT,
              "sq_gemm_w4a8: group (%d) must be a multiple of 32 dividing K", group);
+  SQ_REQUIRE(s_a > 0.f, SQ_ERR_ARG, "sq_gemm_w4a8: s_a must be > 0");
   if (M == 0) return SQ_OK;
-  if (g_gemm_mode != 0) {
-    SQ_REQUIRE(!a_gsum || ld_gsum >= K / 128, SQ_ERR_LAYOUT, "sq_gemm_w4a8: ld_gsum < K/128");
-    rc = gemm_a8_tc(a, lda, w4, sg, group, true, alpha, M, N, K, epi, out, ldo, col_scale, a_gsum, ld_gsum,
-                    as_stream(stream));
+  if (group == 128) {
+    rc = gemm_w4a8_tc(a, lda, w4, w_scale, s_a, M, N, K, epi, out, ldo, col_scale, as_stream(stream));
     if (rc != SQ_ERR_ARG) return rc;
   }
-  return gemm_a8_mma(a, lda, w4, sg, group, true, alpha, M, N, K, epi, out, ldo, col_scale, as_stream(stream));
+  return gemm_a8_mma(a, lda, w4, w_scale, group, s_a, true, nullptr, M, N, K, epi, out, ldo, col_scale,
+                     as_stream(stream));
 }

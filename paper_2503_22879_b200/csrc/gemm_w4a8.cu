@@ -1,0 +1,516 @@
+// K2: W4A8 projection GEMM with SPEC per-group weight scales, on the 5th-gen tensor cores.
+//
+//   y[m,n] = s_a * sum_g s_w[n,g] * acc_g[m,n],   acc_g = sum_{k in g} a[m,k] * w4[n,k]  (int32, exact)
+//
+// s_w[n,g] = compute_scale(w[n, g*128:(g+1)*128], 4) = max|w_g| / 7: the
+// float per-group scale of the reference quantizer, so an archive quantized the SPEC way runs
+// unchanged (LEDGER G11, round 2; the round-1 progressive integer scales are gone).  Every
+// 128-wide K group is its own tcgen05 accumulation; the group's int32 tile is read back from
+// TMEM and promoted into f32 registers (p = fma(s_w, f32(acc_g), p), one rounding, ascending g),
+// which the oracle restates exactly (oracle/qblock.py promote_groups).
+//
+// Swap-AB decode formulation: the CTA's 128 weight rows are the MMA M side (TMEM lane = output
+// channel), the token tile (16/32/64) is the MMA N side.  Roles (16 warps):
+//   warp 0     activation TMA producer: [NTOK x 128 B] K-blocks, SWIZZLE_128B
+//   warp 1     TMEM allocator + single-thread MMA issuer (4 x K=32 kind::i8 per group)
+//   warp 2     weight stream: contiguous 8 KB packed (n-tile, k-block) tiles by 1-D bulk copy
+//   warps 4-7  converters: nibble v -> int8 16*v with one AND (high nibble) / SHF+AND (low),
+//              stored straight into a TMEM A stage (kind::i8 A-from-TMEM).  The x16 is exact
+//              (|16*v| <= 128) and is undone by s_a/16 in the epilogue (a power of two).
+//   warps 8-15 promotion + epilogue.  Every accumulator buffer is pre-set to 0x4B400000 and the
+//              MMAs accumulate onto it, so the read-back word is the f32 1.5*2^23 + acc exactly
+//              (|acc| <= 2^21): one FADD recovers f32(acc) without an I2F; the warp re-arms the
+//              buffer with one tcgen05.st before releasing it to the MMA issuer.
+// No weight byte is read twice and no scale is rounded: the kernel streams 0.5 B per weight
+// plus 4 B per 128 weights.
+//
+// Split-K (small N, e.g. out_proj): SPLITS CTAs of one output tile form a cluster; each keeps its
+// groups' partial sum (ascending g from 0) and rank r reduces a token slice over the peers in rank
+// order through DSMEM.  sq_gemm_w4a8_splits() reports the split the dispatcher picks so the oracle
+// can reproduce the summation order bit for bit.  Without split-K the kernel is persistent: a CTA
+// walks work units (n-tile, m-tile) and its rings never drain between units, so the next unit's
+// weights stream during the current unit's epilogue.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace sq {
+using namespace sm100;
+
+namespace w4pg {
+constexpr int BN = 128;                 // weight rows per tile (MMA M)
+constexpr int BK = 128;                 // K per group / k-block
+constexpr int THREADS = 512;
+constexpr int TILE_BYTES = BN * BK / 2; // 8 KB packed weights per (n-tile, k-block)
+constexpr int RAW = 8;                  // packed-weight ring slots
+constexpr int AST = 4;                  // activation stages
+constexpr int TST = 8;                  // TMEM A stages (32 columns each)
+constexpr int NACC = 4;                 // accumulator buffers (NTOK columns each)
+constexpr uint32_t MAGIC = 0x4B400000u; // bit pattern of 1.5 * 2^23
+
+template <int NTOK>
+struct Cfg {
+  static constexpr int ACT_BYTES = NTOK * BK;
+  static constexpr int OFF_RAW = 0;
+  static constexpr int OFF_ACT = RAW * TILE_BYTES;
+  static constexpr int OFF_BAR = OFF_ACT + AST * ACT_BYTES;
+  static constexpr int NBAR = 2 * RAW + 2 * AST + 2 * TST + 2 * NACC + 4;
+  static constexpr int OFF_SCL = (OFF_BAR + NBAR * 8 + 16 + 127) & ~127;   // 2 unit slabs of group scales
+  // dynamic smem = SMEM0 + 2 * nkb * 512 (each unit's [nkb][128] f32 scales, one bulk copy)
+  static constexpr int SMEM0 = 1024 + OFF_SCL;
+  static constexpr int ACC_COL = 0;
+  static constexpr int A_COL = NACC * NTOK;
+  static constexpr int COLS_USED = A_COL + TST * 32;
+  static constexpr int TMEM_COLS = COLS_USED <= 256 ? 256 : 512;
+  static constexpr int HALF = NTOK / 2;   // token columns per promotion warp
+  static_assert(NTOK * BN * 4 <= OFF_ACT, "split-K partial tile must fit the weight ring");
+};
+
+struct Args {
+  const uint8_t* w4;       // repacked [n_tile][kb][chunk][row][16 B]
+  const float* ws;         // group scales, tiled [n_tile][G][128]
+  float sa16;              // s_a / 16
+  int M, N, K;
+  int epi;
+  void* out;
+  int64_t ldo;
+  const float* col_scale;
+  int units;               // SPLITS == 1: n_tiles * m_tiles work units
+  int n_tiles;
+};
+
+__device__ __forceinline__ void to_s8x16(uint32_t w, uint32_t& lo, uint32_t& hi) {
+  // byte j of w = element j (low nibble) | element j+4 (high nibble)  (sq_repack_w4 order)
+  hi = w & 0xF0F0F0F0u;          // 16 * v[j+4] as int8
+  lo = (w << 4) & 0xF0F0F0F0u;   // 16 * v[j]
+}
+
+template <int NC>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t addr, uint32_t (&v)[NC]) {
+  if constexpr (NC == 8) {
+    tmem_ld_x8(addr, v);
+  } else if constexpr (NC == 16) {
+    tmem_ld_x16(addr, v);
+  } else {
+    tmem_ld_x32(addr, v);
+  }
+}
+
+template <int NC>
+__device__ __forceinline__ void tmem_arm(uint32_t addr) {   // every column = MAGIC
+  uint32_t c[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i] = MAGIC;
+#pragma unroll
+  for (int i = 0; i < NC; i += 8) tmem_st_x8(addr + i, c);
+}
+
+__device__ __forceinline__ void store_out(const Args& a, int m, int n, float y, float cs) {
+  const int64_t o = (int64_t)m * a.ldo + n;
+  if (a.epi == SQ_EPI_F32)
+    reinterpret_cast<float*>(a.out)[o] = y;
+  else if (a.epi == SQ_EPI_QUANT)
+    reinterpret_cast<int8_t*>(a.out)[o] = quant8_inv(y, cs, __frcp_rn(cs));
+  else
+    reinterpret_cast<float*>(a.out)[o] = __fadd_rn(reinterpret_cast<float*>(a.out)[o], y);
+}
+
+template <int NTOK, int SPLITS>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_w4a8_pg_kernel(const __grid_constant__ CUtensorMap tm_act, Args args) {
+  using C = Cfg<NTOK>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* raw = smem + C::OFF_RAW;
+  uint8_t* act = smem + C::OFF_ACT;
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* rempty = rfull + RAW;
+  uint64_t* afull = rempty + RAW;
+  uint64_t* aempty = afull + AST;
+  uint64_t* tfull = aempty + AST;
+  uint64_t* tempty = tfull + TST;
+  uint64_t* cfull = tempty + TST;
+  uint64_t* cempty = cfull + NACC;
+  uint64_t* sfull = cempty + NACC;      // [2] unit scale slabs
+  uint64_t* sempty = sfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = args.K / BK;
+  // work decomposition: split-K clusters own exactly one unit; otherwise persistent over units
+  const int split = SPLITS > 1 ? (int)blockIdx.x : 0;
+  const int kb0 = split * G / SPLITS;
+  const int nkb = (split + 1) * G / SPLITS - kb0;
+  const int u_first = SPLITS > 1 ? (int)(blockIdx.z * gridDim.y + blockIdx.y) : (int)blockIdx.x;
+  const int u_step = SPLITS > 1 ? args.units : (int)gridDim.x;
+  float* scl = reinterpret_cast<float*>(smem + C::OFF_SCL);   // [2][nkb][128]
+  auto unit_n = [&](int u) { return u % args.n_tiles; };
+  auto unit_m = [&](int u) { return u / args.n_tiles; };
+
+  pdl_trigger();
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < RAW; ++i) { mbar_init(&rfull[i], 1); mbar_init(&rempty[i], 4); }
+    for (int i = 0; i < AST; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1); }
+    for (int i = 0; i < TST; ++i) { mbar_init(&tfull[i], 4); mbar_init(&tempty[i], 1); }
+    for (int i = 0; i < NACC; ++i) { mbar_init(&cfull[i], 1); mbar_init(&cempty[i], 8); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 8); }
+    fence_barrier_init();
+    tma_prefetch(&tm_act);
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  if (warp >= 8) {   // arm both accumulator buffers (this warp's lane quadrant and column half)
+    const int q = warp & 3, h = (warp - 8) >> 2;
+#pragma unroll
+    for (int c = 0; c < NACC; ++c) tmem_arm<C::HALF>(tmem + ((uint32_t)(q * 32) << 16) + C::ACC_COL + c * NTOK + h * C::HALF);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == 0) {
+    // ------------------------------------------------ activation K-blocks (TMA)
+    if (lane == 0) {
+      pdl_wait();   // activations are written by the previous grid
+      int j = 0;
+      for (int u = u_first; u < args.units; u += u_step) {
+        const int m_tile = unit_m(u);
+        for (int i = 0; i < nkb; ++i, ++j) {
+          const int s = j % AST;
+          mbar_wait_lazy(&aempty[s], ((j / AST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&afull[s], C::ACT_BYTES);
+          tma_load_2d(act + s * C::ACT_BYTES, &tm_act, &afull[s], (kb0 + i) * BK, m_tile * NTOK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_i8(BN, NTOK);   // s8 x s8 -> s32
+      int j = 0;
+      for (int u = u_first; u < args.units; u += u_step) {
+        for (int i = 0; i < nkb; ++i, ++j) {
+          const int s = j % AST, t = j % TST, c = j % NACC;
+          mbar_wait(&afull[s], (j / AST) & 1);
+          mbar_wait(&tfull[t], (j / TST) & 1);
+          mbar_wait(&cempty[c], ((j / NACC) & 1) ^ 1);
+          tc_fence_after();
+          const uint64_t bdesc = desc_sw128(act + s * C::ACT_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < BK / 32; ++ks)
+            mma_i8_ts(tmem + C::ACC_COL + c * NTOK, tmem + C::A_COL + t * 32 + ks * 8, bdesc + 2 * ks, idesc, 1u);
+          mma_commit(&aempty[s]);
+          mma_commit(&tempty[t]);
+          mma_commit(&cfull[c]);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------ packed weight stream (static: before PDL wait)
+    if (lane == 0) {
+      int j = 0, ui = 0;
+      for (int u = u_first; u < args.units; u += u_step, ++ui) {
+        // the unit's group scales: one contiguous [nkb][128] f32 slab of the tiled table
+        const int sb = ui & 1;
+        mbar_wait_lazy(&sempty[sb], ((ui >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sfull[sb], nkb * BN * 4);
+        bulk_load(scl + sb * nkb * BN, args.ws + ((size_t)unit_n(u) * G + kb0) * BN, nkb * BN * 4, &sfull[sb]);
+        const uint8_t* src = args.w4 + ((size_t)unit_n(u) * G + kb0) * TILE_BYTES;
+        for (int i = 0; i < nkb; ++i, ++j) {
+          const int r = j % RAW;
+          mbar_wait_lazy(&rempty[r], ((j / RAW) & 1) ^ 1);
+          mbar_arrive_expect_tx(&rfull[r], TILE_BYTES);
+          bulk_load(raw + r * TILE_BYTES, src + (size_t)i * TILE_BYTES, TILE_BYTES, &rfull[r]);
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------ converters: packed nibbles -> TMEM A stage
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + C::A_COL;
+    int j = 0;
+    for (int u = u_first; u < args.units; u += u_step) {
+      for (int i = 0; i < nkb; ++i, ++j) {
+        const int r = j % RAW, t = j % TST;
+        mbar_wait(&rfull[r], (j / RAW) & 1);
+        uint4 p[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) p[c] = *reinterpret_cast<const uint4*>(raw + r * TILE_BYTES + c * 2048 + row * 16);
+        fence_proxy_async_smem();   // generic reads of the slot precede the bulk copy that refills it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[r]);
+        uint32_t wv[32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          to_s8x16(p[c].x, wv[c * 8 + 0], wv[c * 8 + 1]);
+          to_s8x16(p[c].y, wv[c * 8 + 2], wv[c * 8 + 3]);
+          to_s8x16(p[c].z, wv[c * 8 + 4], wv[c * 8 + 5]);
+          to_s8x16(p[c].w, wv[c * 8 + 6], wv[c * 8 + 7]);
+        }
+        mbar_wait(&tempty[t], ((j / TST) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st_x32(lane_base + t * 32, wv);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tfull[t]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------ promotion + epilogue
+    const int q = warp & 3, h = (warp - 8) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t acc_base = tmem + ((uint32_t)(q * 32) << 16) + C::ACC_COL + h * C::HALF;
+    int j = 0, ui = 0;
+    bool waited = false;
+    for (int u = u_first; u < args.units; u += u_step, ++ui) {
+      const int n_tile = unit_n(u), m_tile = unit_m(u);
+      const int n = n_tile * BN + row;
+      const int sb = ui & 1;
+      const float* ssl = scl + sb * nkb * BN + row;
+      float p[C::HALF];
+#pragma unroll
+      for (int e = 0; e < C::HALF; ++e) p[e] = 0.f;
+      mbar_wait(&sfull[sb], (ui >> 1) & 1);
+      for (int i = 0; i < nkb; ++i, ++j) {
+        const int c = j % NACC;
+        const float s0 = ssl[i * BN];
+        mbar_wait(&cfull[c], (j / NACC) & 1);
+        tc_fence_after();
+        uint32_t v[C::HALF];
+        tmem_ld_cols<C::HALF>(acc_base + c * NTOK, v);
+        tmem_wait_ld();
+        tmem_arm<C::HALF>(acc_base + c * NTOK);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cempty[c]);
+        const float2 sv = make_float2(s0, s0), nm = make_float2(-12582912.0f, -12582912.0f);
+#pragma unroll
+        for (int e = 0; e < C::HALF; e += 2) {
+          const float2 f = __fadd2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), nm);
+          const float2 r2 = __ffma2_rn(sv, f, make_float2(p[e], p[e + 1]));
+          p[e] = r2.x;
+          p[e + 1] = r2.y;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[sb]);   // slab read: the stream warp may refill it
+      if (!waited) {
+        pdl_wait();   // outputs / residual belong to earlier grids too
+        waited = true;
+      }
+      const int t0 = m_tile * NTOK + h * C::HALF;
+      if (SPLITS == 1) {
+        if (n < args.N) {
+          const float cs = args.epi == SQ_EPI_QUANT ? args.col_scale[n] : 1.f;
+          if (args.epi == SQ_EPI_RESID) {
+            // residual loads of a chunk are all issued before its stores (a store may alias a
+            // later load as far as the compiler knows)
+            constexpr int RC = C::HALF < 16 ? C::HALF : 16;
+            float* o_ptr = reinterpret_cast<float*>(args.out) + n;
+#pragma unroll
+            for (int e0 = 0; e0 < C::HALF; e0 += RC) {
+              float o[RC];
+#pragma unroll
+              for (int e = 0; e < RC; ++e)
+                o[e] = t0 + e0 + e < args.M ? o_ptr[(int64_t)(t0 + e0 + e) * args.ldo] : 0.f;
+#pragma unroll
+              for (int e = 0; e < RC; ++e)
+                if (t0 + e0 + e < args.M)
+                  o_ptr[(int64_t)(t0 + e0 + e) * args.ldo] = __fadd_rn(o[e], __fmul_rn(p[e0 + e], args.sa16));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < C::HALF; ++e)
+              if (t0 + e < args.M) store_out(args, t0 + e, n, __fmul_rn(p[e], args.sa16), cs);
+          }
+        }
+      } else {
+        float* red = reinterpret_cast<float*>(raw);   // [NTOK][128]; the weight ring is idle now
+#pragma unroll
+        for (int e = 0; e < C::HALF; ++e) red[(h * C::HALF + e) * BN + row] = p[e];
+      }
+    }
+  }
+
+  if (SPLITS > 1) {
+    pdl_wait();
+    __syncwarp();
+    cluster_sync();
+    const uint32_t rank = cluster_rank();
+    constexpr int TPR = NTOK / SPLITS;
+    const int n_tile = unit_n(u_first), m_tile = unit_m(u_first);
+    const uint32_t red_addr = smem_u32(raw);
+    for (int idx = threadIdx.x; idx < TPR * BN; idx += THREADS) {
+      const int tl = rank * TPR + idx / BN, r = idx % BN;
+      const int m = m_tile * NTOK + tl, n = n_tile * BN + r;
+      float part[SPLITS];
+#pragma unroll
+      for (int s = 0; s < SPLITS; ++s) part[s] = ld_dsmem_f32(map_peer(red_addr + (tl * BN + r) * 4, s));
+      float sum = part[0];
+#pragma unroll
+      for (int s = 1; s < SPLITS; ++s) sum = __fadd_rn(sum, part[s]);   // rank order: deterministic
+      if (m < args.M && n < args.N)
+        store_out(args, m, n, __fmul_rn(sum, args.sa16), args.epi == SQ_EPI_QUANT ? args.col_scale[n] : 1.f);
+    }
+    cluster_sync();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static bool encoder() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+static int ntok_for(int M) { return M <= 16 ? 16 : (M <= 32 ? 32 : 64); }
+static int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+}  // namespace w4pg
+
+// Split-K factor the tcgen05 W4A8 kernel uses for (M, N, K); 1 when not eligible.
+int w4a8_splits(int M, int N, int K) {
+  using namespace w4pg;
+  if (K % BK) return 1;
+  const int ntok = ntok_for(M);
+  const int tiles = ((N + BN - 1) / BN) * ((M + ntok - 1) / ntok);
+  const int G = K / BK;
+  int splits = 1;
+  while (splits < 8 && tiles * splits * 2 <= 148 && G / (splits * 2) >= 4 && ntok % (splits * 2) == 0) splits *= 2;
+  return splits;
+}
+
+template <int NTOK, int SPLITS>
+static int launch_w4pg(const CUtensorMap& tm, const w4pg::Args& a, cudaStream_t st) {
+  using namespace w4pg;
+  using C = Cfg<NTOK>;
+  auto kern = gemm_w4a8_pg_kernel<NTOK, SPLITS>;
+  // per-device attribute setup (a process may drive several GPUs)
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev & 63], [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (SPLITS > 1) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  });
+  cudaLaunchConfig_t cfg = {};
+  const int m_tiles = (a.M + NTOK - 1) / NTOK;
+  if (SPLITS > 1)
+    cfg.gridDim = dim3(SPLITS, a.n_tiles, m_tiles);
+  else
+    cfg.gridDim = dim3(std::min(a.units, sm_count()));
+  cfg.blockDim = dim3(THREADS);
+  const int nkb = (a.K / BK + SPLITS - 1) / SPLITS;
+  cfg.dynamicSmemBytes = C::SMEM0 + 2 * nkb * BN * 4;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (SPLITS > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = SPLITS;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled(PDL_GEMM)) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tm, a);
+  if (e != cudaSuccess) {
+    set_error("gemm_w4a8 launch: %s", cudaGetErrorString(e));
+    return SQ_ERR_CUDA;
+  }
+  return check_launch("gemm_w4a8");
+}
+
+template <int NTOK>
+static int dispatch_w4pg_split(int splits, const CUtensorMap& tm, const w4pg::Args& a, cudaStream_t st) {
+  switch (splits) {
+    case 1: return launch_w4pg<NTOK, 1>(tm, a, st);
+    case 2: return launch_w4pg<NTOK, 2>(tm, a, st);
+    case 4: return launch_w4pg<NTOK, 4>(tm, a, st);
+    default: return launch_w4pg<NTOK, 8>(tm, a, st);
+  }
+}
+
+// Returns SQ_ERR_ARG when the shape is not eligible (the caller runs the mma.sync kernel).
+int gemm_w4a8_tc(const int8_t* a, int64_t lda, const uint8_t* w4, const float* ws, float s_a, int M, int N, int K,
+                 int epi, void* out, int64_t ldo, const float* col_scale, cudaStream_t st) {
+  using namespace w4pg;
+  if (K % BK != 0 || lda % 16 != 0 || (reinterpret_cast<uintptr_t>(a) & 15) || epi == SQ_EPI_I32) return SQ_ERR_ARG;
+  if (!encoder()) return SQ_ERR_ARG;
+  const int ntok = ntok_for(M);
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+  cuuint64_t strides[1] = {(cuuint64_t)lda};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)ntok};
+  cuuint32_t es[2] = {1, 1};
+  if (g_encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(a), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    set_error("gemm_w4a8: activation tensor map encode failed");
+    return SQ_ERR_CUDA;
+  }
+  Args args{w4, ws, __builtin_ldexpf(s_a, -4), M, N, K, epi, out, ldo, col_scale, 0, (N + BN - 1) / BN};
+  args.units = args.n_tiles * ((M + ntok - 1) / ntok);
+  const int splits = w4a8_splits(M, N, K);
+  const int nkb = (K / BK + splits - 1) / splits;
+  if (Cfg<64>::SMEM0 + 2 * nkb * BN * 4 > 227 * 1024) return SQ_ERR_ARG;   // scale slabs must fit
+  switch (ntok) {
+    case 16: return dispatch_w4pg_split<16>(splits, tm, args, st);
+    case 32: return dispatch_w4pg_split<32>(splits, tm, args, st);
+    default: return dispatch_w4pg_split<64>(splits, tm, args, st);
+  }
+}
+
+// Group scales [N x G] (row-major, SPEC PerGroup) -> tiled [ceil(N/128)][G][128] (rows >= N: 1.0).
+__global__ void tile_scales_kernel(const float* __restrict__ s, int N, int G, float* __restrict__ dst) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)((N + 127) / 128) * G * 128;
+  if (idx >= total) return;
+  const int r = idx % 128;
+  const int g = (idx / 128) % G;
+  const int tile = idx / (128 * G);
+  const int n = tile * 128 + r;
+  dst[idx] = n < N ? s[(int64_t)n * G + g] : 1.f;
+}
+
+int tile_scales(const float* s, int N, int G, float* dst, cudaStream_t st) {
+  const int64_t total = (int64_t)((N + 127) / 128) * G * 128;
+  tile_scales_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, N, G, dst);
+  return check_launch("sq_tile_group_scales");
+}
+
+}  // namespace sq

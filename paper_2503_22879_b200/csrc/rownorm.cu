@@ -545,8 +545,6 @@ extern "C" int sq_rmsnorm_f32(const float* x, int64_t ldx, const float* gamma, f
   return check_launch("sq_rmsnorm_f32");
 }
 
-// profiling A/B (SQ_NORM_LEGACY=1): route D = q·1024 rows through gate_norm_had_quant16_kernel
-static const bool g_norm_legacy = getenv("SQ_NORM_LEGACY") != nullptr;
 
 extern "C" int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* gamma, float eps, float s_y,
                                       int hadamard, int M, int D, int8_t* out, int64_t ldo, void* stream) {
@@ -556,7 +554,7 @@ extern "C" int sq_gate_norm_had_quant(const float* y, int64_t ldy, const float* 
   if (M == 0) return SQ_OK;
   const int blk = hadamard ? (D & -D) : 1;
   const size_t smem = (size_t)D * sizeof(float);
-  if (blk == 1024 && D / 1024 <= 16 && ldy % 4 == 0 && ldo % 16 == 0 && !g_norm_legacy) {
+  if (blk == 1024 && D / 1024 <= 16 && ldy % 4 == 0 && ldo % 16 == 0) {
     auto k1 = gate_norm_had1k_kernel;
     const int nthr = D / 32;
     const size_t sm1 = (size_t)(D / 1024) * N1K_WARP_FLOATS * sizeof(float);

@@ -18,11 +18,6 @@
 #include "common.cuh"
 
 namespace sq {
-// chunk-scan engine (sq_set_ssd_mode); SQ_SSD_TC=1 in the environment selects tcgen05 at load
-int g_ssd_mode = [] {
-  const char* e = getenv("SQ_SSD_TC");
-  return e ? atoi(e) : 0;
-}();
 
 template <typename TQ>
 struct Deq;
@@ -133,20 +128,24 @@ __global__ void __launch_bounds__(256) mamba2_scan_kernel(sq_mamba2_params p, in
 // registers for all rows.  The per-element update is mamba2_scan_kernel's (identical f32 ops,
 // bit-identical state); only y's column sum runs in a different order (lane partials, then a
 // warp butterfly).
-template <int CPL>
+// PRE: Ȧ and Δ are inputs (SPEC selective_scan(x, Ȧ, Δ, ...)) in dAp / dt, same
+// layout; otherwise Δ = softplus(dt + dt_bias), Ȧ = exp(Δ·A) (discretize fused).  z may be null
+// (ungated output).
+template <int CPL, bool PRE>
 __global__ void __launch_bounds__(128) mamba2_scan_f32_rows_kernel(sq_mamba2_params p, int T, const float* x,
                                                                    int64_t ldx, const float* Bm, const float* Cm,
-                                                                   int64_t ldbc, const float* dt, int64_t lddt,
-                                                                   const float* z, int64_t ldz, float* state,
-                                                                   int state_in, float* y, int64_t ldy) {
+                                                                   int64_t ldbc, const float* dt, const float* dAp,
+                                                                   int64_t lddt, const float* z, int64_t ldz,
+                                                                   float* state, int state_in, float* y, int64_t ldy) {
   pdl_trigger();
   pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int h = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = p.head_dim, N = p.d_state;   // N == 32 * CPL
   const int r0 = blockIdx.z * 32 + warp * 8;
+  if (r0 >= P) return;                        // P % 8 == 0; whole warps idle past the last row
   const int g = p.head_group[h];
-  const float A = p.A[h], Dh = p.D[h], dtb = p.dt_bias[h];
+  const float A = PRE ? 0.f : p.A[h], Dh = p.D[h], dtb = PRE ? 0.f : p.dt_bias[h];
   float* st = state + (((int64_t)b * p.n_heads + h) * P + r0) * N + lane * CPL;
   float hs[8][CPL];
 #pragma unroll
@@ -163,8 +162,8 @@ __global__ void __launch_bounds__(128) mamba2_scan_f32_rows_kernel(sq_mamba2_par
     }
   for (int t = 0; t < T; ++t) {
     const int64_t tok = (int64_t)b * T + t;
-    const float delta = softplus_f(__fadd_rn(dt[tok * lddt + h], dtb));
-    const float dA = expf(__fmul_rn(delta, A));
+    const float delta = PRE ? dt[tok * lddt + h] : softplus_f(__fadd_rn(dt[tok * lddt + h], dtb));
+    const float dA = PRE ? dAp[tok * lddt + h] : expf(__fmul_rn(delta, A));
     float bv[CPL], cv[CPL], xr[8];
 #pragma unroll
     for (int i = 0; i < CPL; i += 2) {
@@ -200,7 +199,7 @@ __global__ void __launch_bounds__(128) mamba2_scan_f32_rows_kernel(sq_mamba2_par
         }
       const float yv = __fadd_rn(a, __fmul_rn(Dh, xv));
       const int ch = h * P + r0 + lane;
-      y[tok * ldy + ch] = __fmul_rn(yv, silu_f(z[tok * ldz + ch]));
+      y[tok * ldy + ch] = z ? __fmul_rn(yv, silu_f(z[tok * ldz + ch])) : yv;
     }
   }
 #pragma unroll
@@ -284,39 +283,42 @@ __global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, in
 // Mamba1 W4A16 (float) scan: the same recurrence on f32 operands and an f32 state
 // (oracle/ssm_block.py selective_scan, Mamba1 branch).  dt is the raw
 // dt_proj output; B|C come from the x_proj output row (C at +N).
-template <int N>
+// PRE: Ȧ [B*T x d_inner x N] and Δ are inputs (SPEC selective_scan); z may be null.
+template <int N, bool PRE>
 __global__ void __launch_bounds__(128) mamba1_scan_f32_kernel(sq_mamba1_params p, int B, int T, const float* x,
-                                                             int64_t ldx, const float* dt, int64_t lddt,
-                                                             const float* BC, int64_t ldbc, const float* z,
-                                                             int64_t ldz, float* state, int state_in, float* y,
-                                                             int64_t ldy) {
+                                                             int64_t ldx, const float* dt, const float* dAp,
+                                                             int64_t lddt, const float* Bm, const float* Cm,
+                                                             int64_t ldbc, const float* z, int64_t ldz, float* state,
+                                                             int state_in, float* y, int64_t ldy) {
   pdl_trigger();
   pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (c >= p.d_inner) return;
-  const float Dc = p.D[c], dtb = p.dt_bias[c];
+  const float Dc = p.D[c], dtb = PRE ? 0.f : p.dt_bias[c];
   float A[N], hs[N];
 #pragma unroll
-  for (int n = 0; n < N; ++n) A[n] = p.A[c * N + n];
+  for (int n = 0; n < N; ++n) A[n] = PRE ? 0.f : p.A[c * N + n];
   float* st = state + ((int64_t)b * p.d_inner + c) * N;
 #pragma unroll
   for (int n = 0; n < N; ++n) hs[n] = state_in ? st[n] : 0.f;
   for (int t = 0; t < T; ++t) {
     const int64_t tok = (int64_t)b * T + t;
-    const float delta = softplus_f(__fadd_rn(dt[tok * lddt + c], dtb));
+    const float delta = PRE ? dt[tok * lddt + c] : softplus_f(__fadd_rn(dt[tok * lddt + c], dtb));
     const float xv = x[tok * ldx + c];
     const float dtx = __fmul_rn(delta, xv);
-    const float* bc = BC + tok * ldbc;
+    const float* bp = Bm + tok * ldbc;
+    const float* cp = Cm + tok * ldbc;
+    const float* dap = PRE ? dAp + (tok * p.d_inner + c) * N : nullptr;
     float acc = 0.f;
 #pragma unroll
     for (int n = 0; n < N; ++n) {
-      const float dA = expf(__fmul_rn(delta, A[n]));
-      hs[n] = __fadd_rn(__fmul_rn(dA, hs[n]), __fmul_rn(dtx, bc[n]));
-      acc = fmaf(hs[n], bc[N + n], acc);
+      const float dA = PRE ? dap[n] : expf(__fmul_rn(delta, A[n]));
+      hs[n] = __fadd_rn(__fmul_rn(dA, hs[n]), __fmul_rn(dtx, bp[n]));
+      acc = fmaf(hs[n], cp[n], acc);
     }
     const float yv = __fadd_rn(acc, __fmul_rn(Dc, xv));
-    y[tok * ldy + c] = __fmul_rn(yv, silu_f(z[tok * ldz + c]));
+    y[tok * ldy + c] = z ? __fmul_rn(yv, silu_f(z[tok * ldz + c])) : yv;
   }
 #pragma unroll
   for (int n = 0; n < N; ++n) st[n] = hs[n];
@@ -562,12 +564,13 @@ extern "C" int sq_ssd_scan_int8(const sq_mamba2_params* p, int B, int T, const i
                                 const int8_t* Bm, const int8_t* Cm, int64_t ldbc, const int8_t* dt, int64_t lddt,
                                 const int8_t* z, int64_t ldz, int8_t* state, int state_in, float* y, int64_t ldy,
                                 int chunk, void* stream) {
-  (void)chunk;   // the tensor-core path uses 64-token chunks
+  // chunk selects the engine per call: 128 = tcgen05 (128-token chunks, ssd_chunk_tc.cu), anything else
+  // = mma.sync (64-token chunks, ssd_chunk.cu).  Results agree to the SPEC chunk tolerance.
   SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_ssd_scan_int8: bad args");
   if (B == 0 || T == 0) return SQ_OK;
   if (T > 1) {   // chunked SSD on the tensor cores (ssd_chunk_tc.cu tcgen05, ssd_chunk.cu mma.sync);
                   // other shapes: sequential scan
-    if (g_ssd_mode == 1) {
+    if (chunk == 128) {
       const int rc = launch_ssd_chunk_tc(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
                                          as_stream(stream));
       if (rc != SQ_ERR_ARG) return rc;
@@ -578,12 +581,6 @@ extern "C" int sq_ssd_scan_int8(const sq_mamba2_params* p, int B, int T, const i
   }
   return launch_mamba2<int8_t>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
                                as_stream(stream), "sq_ssd_scan_int8");
-}
-
-extern "C" int sq_set_ssd_mode(int mode) {
-  SQ_REQUIRE(mode == 0 || mode == 1, SQ_ERR_ARG, "sq_set_ssd_mode: mode must be 0 or 1");
-  g_ssd_mode = mode;
-  return SQ_OK;
 }
 
 extern "C" int sq_state_update_int8(const sq_mamba2_params* p, int B, const int8_t* x, int64_t ldx,
@@ -605,18 +602,17 @@ extern "C" int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T, const fl
                                const float* Bm, const float* Cm, int64_t ldbc, const float* dt, int64_t lddt,
                                const float* z, int64_t ldz, float* state, int state_in, float* y, int64_t ldy,
                                void* stream) {
-  static const bool legacy = getenv("SQ_SCAN_LEGACY") != nullptr;   // profiling A/B
-  if (p && B > 0 && T > 0 && !legacy && p->head_dim % 32 == 0 && (p->d_state == 64 || p->d_state == 128 || p->d_state == 256) &&
+  if (p && B > 0 && T > 0 && p->head_dim % 32 == 0 && (p->d_state == 64 || p->d_state == 128 || p->d_state == 256) &&
       p->n_heads % p->n_groups == 0 && ldbc % 2 == 0 && (reinterpret_cast<uintptr_t>(Bm) & 7) == 0 &&
       (reinterpret_cast<uintptr_t>(Cm) & 7) == 0 && (reinterpret_cast<uintptr_t>(state) & 7) == 0) {
     const dim3 grid(p->n_heads, B, p->head_dim / 32);
     cudaStream_t st = as_stream(stream);
     if (p->d_state == 64)
-      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<2>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<2, false>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, (const float*)nullptr, lddt, z, ldz, state, state_in, y, ldy);
     else if (p->d_state == 128)
-      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<4>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<4, false>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, (const float*)nullptr, lddt, z, ldz, state, state_in, y, ldy);
     else
-      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<8>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
+      launch_k(PDL_SMALL, mamba2_scan_f32_rows_kernel<8, false>, grid, dim3(128), 0, st, *p, T, x, ldx, Bm, Cm, ldbc, dt, (const float*)nullptr, lddt, z, ldz, state, state_in, y, ldy);
     return check_launch("sq_ssd_scan_f32");
   }
   return launch_mamba2<float>(p, B, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy,
@@ -643,7 +639,115 @@ extern "C" int sq_selective_scan_f32(const sq_mamba1_params* p, int B, int T, co
   SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan_f32: d_state must be 16 (got %d)", p->d_state);
   if (B == 0 || T == 0) return SQ_OK;
   dim3 grid((p->d_inner + 127) / 128, B);
-  launch_k(PDL_SMALL, mamba1_scan_f32_kernel<16>, grid, dim3(128), 0, as_stream(stream), *p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz,
-                                                                  state, state_in, y, ldy);
+  launch_k(PDL_SMALL, mamba1_scan_f32_kernel<16, false>, grid, dim3(128), 0, as_stream(stream), *p, B, T, x, ldx, dt,
+           (const float*)nullptr, lddt, BC, BC + 16, ldbc, z, ldz, state, state_in, y, ldy);
   return check_launch("sq_selective_scan_f32");
+}
+
+// ---- SPEC float ops (ssm_block.discretize / selective_scan / ssd_chunked on the GPU) ------
+__global__ void discretize_kernel(const float* dt_raw, int64_t ld, const float* __restrict__ dt_bias,
+                                  const float* __restrict__ A, int M, int H, int N, float* dA, float* delta) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * H) return;
+  const int m = i / H, h = i % H;
+  const float d = softplus_f(__fadd_rn(dt_raw[(int64_t)m * ld + h], dt_bias[h]));
+  delta[i] = d;
+  for (int n = 0; n < N; ++n) dA[i * N + n] = expf(__fmul_rn(d, A[(int64_t)h * N + n]));
+}
+
+extern "C" int sq_discretize_f32(const float* dt_raw, int64_t ld, const float* dt_bias, const float* A, int M, int H,
+                                 int N, float* dA, float* delta, void* stream) {
+  SQ_REQUIRE(M >= 0 && H > 0 && N >= 1 && ld >= H, SQ_ERR_SHAPE, "sq_discretize_f32: bad shape");
+  if (M == 0) return SQ_OK;
+  const int64_t n = (int64_t)M * H;
+  discretize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(dt_raw, ld, dt_bias, A, M, H, N, dA,
+                                                                                 delta);
+  return check_launch("sq_discretize_f32");
+}
+
+// Mamba2 recurrence on precomputed Ȧ / Δ for small d_state (16 / 32, e.g. the SPEC toy dims):
+// one thread per (sequence, head, row), the state row in registers.
+template <int N>
+__global__ void __launch_bounds__(128) scan2_pre_small_kernel(sq_mamba2_params p, int B, int T, const float* x,
+                                                              int64_t ldx, const float* dAp, const float* dt,
+                                                              int64_t lddt, const float* Bm, const float* Cm,
+                                                              int64_t ldbc, const float* z, int64_t ldz, float* state,
+                                                              int state_in, float* y, int64_t ldy) {
+  const int P = p.head_dim;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)B * p.n_heads * P) return;
+  const int r = idx % P, h = (idx / P) % p.n_heads, b = idx / ((int64_t)P * p.n_heads);
+  const int g = p.head_group[h];
+  float* st = state + idx * N;
+  float hs[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) hs[n] = state_in ? st[n] : 0.f;
+  const float Dh = p.D[h];
+  for (int t = 0; t < T; ++t) {
+    const int64_t tok = (int64_t)b * T + t;
+    const float delta = dt[tok * lddt + h], dA = dAp[tok * lddt + h];
+    const float xv = x[tok * ldx + h * P + r];
+    const float dtx = __fmul_rn(delta, xv);
+    const float* bp = Bm + tok * ldbc + g * N;
+    const float* cp = Cm + tok * ldbc + g * N;
+    float acc = 0.f;
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      hs[n] = __fadd_rn(__fmul_rn(dA, hs[n]), __fmul_rn(dtx, bp[n]));
+      acc = fmaf(hs[n], cp[n], acc);
+    }
+    const float yv = __fadd_rn(acc, __fmul_rn(Dh, xv));
+    const int ch = h * P + r;
+    y[tok * ldy + ch] = z ? __fmul_rn(yv, silu_f(z[tok * ldz + ch])) : yv;
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) st[n] = hs[n];
+}
+
+extern "C" int sq_selective_scan2_pre_f32(const sq_mamba2_params* p, int B, int T, const float* x, int64_t ldx,
+                                          const float* dA, const float* delta, int64_t lddt, const float* Bm,
+                                          const float* Cm, int64_t ldbc, const float* z, int64_t ldz, float* state,
+                                          int state_in, float* y, int64_t ldy, void* stream) {
+  SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_selective_scan2_pre_f32: bad args");
+  const int N = p ? p->d_state : 0;
+  SQ_REQUIRE(p->n_heads % p->n_groups == 0 && (N == 16 || N == 32 || ((N == 64 || N == 128 || N == 256) &&
+                                                                      p->head_dim % 8 == 0 && ldbc % 2 == 0)),
+             SQ_ERR_SHAPE, "sq_selective_scan2_pre_f32: d_state in {16,32,64,128,256} (P=%d N=%d)", p->head_dim, N);
+  if (B == 0 || T == 0) return SQ_OK;
+  cudaStream_t st = as_stream(stream);
+  if (N <= 32) {
+    const int64_t rows = (int64_t)B * p->n_heads * p->head_dim;
+    const unsigned nb = (unsigned)((rows + 127) / 128);
+    if (N == 16)
+      scan2_pre_small_kernel<16><<<nb, 128, 0, st>>>(*p, B, T, x, ldx, dA, delta, lddt, Bm, Cm, ldbc, z, ldz, state,
+                                                     state_in, y, ldy);
+    else
+      scan2_pre_small_kernel<32><<<nb, 128, 0, st>>>(*p, B, T, x, ldx, dA, delta, lddt, Bm, Cm, ldbc, z, ldz, state,
+                                                     state_in, y, ldy);
+    return check_launch("sq_selective_scan2_pre_f32");
+  }
+  const dim3 grid(p->n_heads, B, (p->head_dim + 31) / 32);
+  if (p->d_state == 64)
+    mamba2_scan_f32_rows_kernel<2, true><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, delta, dA, lddt, z, ldz,
+                                                               state, state_in, y, ldy);
+  else if (p->d_state == 128)
+    mamba2_scan_f32_rows_kernel<4, true><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, delta, dA, lddt, z, ldz,
+                                                               state, state_in, y, ldy);
+  else
+    mamba2_scan_f32_rows_kernel<8, true><<<grid, 128, 0, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, delta, dA, lddt, z, ldz,
+                                                               state, state_in, y, ldy);
+  return check_launch("sq_selective_scan2_pre_f32");
+}
+
+extern "C" int sq_selective_scan1_pre_f32(const sq_mamba1_params* p, int B, int T, const float* x, int64_t ldx,
+                                          const float* dA, const float* delta, int64_t lddt, const float* Bm,
+                                          const float* Cm, int64_t ldbc, const float* z, int64_t ldz, float* state,
+                                          int state_in, float* y, int64_t ldy, void* stream) {
+  SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_selective_scan1_pre_f32: bad args");
+  SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan1_pre_f32: d_state must be 16 (got %d)", p->d_state);
+  if (B == 0 || T == 0) return SQ_OK;
+  dim3 grid((p->d_inner + 127) / 128, B);
+  mamba1_scan_f32_kernel<16, true><<<grid, 128, 0, as_stream(stream)>>>(*p, B, T, x, ldx, delta, dA, lddt, Bm, Cm, ldbc,
+                                                                         z, ldz, state, state_in, y, ldy);
+  return check_launch("sq_selective_scan1_pre_f32");
 }

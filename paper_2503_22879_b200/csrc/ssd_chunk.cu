@@ -26,6 +26,8 @@
 // bank-conflict-free for the 8-row ldmatrix phases.  Legacy warp-level mma.sync.
 #include <cuda_fp16.h>
 
+#include <mutex>
+
 #include "common.cuh"
 
 namespace sq {
@@ -438,11 +440,11 @@ static int launch_n(const sq_mamba2_params* p, int B, int T, const int8_t* x, in
                     const int8_t* Cm, int64_t ldbc, const int8_t* dt, int64_t lddt, const int8_t* z, int64_t ldz,
                     int8_t* state, int state_in, float* y, int64_t ldy, cudaStream_t st) {
   const int smem = sizeof(ScSmem<N>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ssd_chunk_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static std::once_flag once[64];   // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev & 63],
+                 [&] { cudaFuncSetAttribute(ssd_chunk_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
   ssd_chunk_kernel<N><<<dim3(p->n_heads, B), SC_THREADS, smem, st>>>(*p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz,
                                                                     state, state_in, y, ldy);
   return SQ_OK;

@@ -21,6 +21,8 @@
 // accumulators back to the four warps.
 #include <cuda_fp16.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -457,11 +459,12 @@ int launch_ssd_chunk_tc(const sq_mamba2_params* p, int B, int T, const int8_t* x
       (reinterpret_cast<uintptr_t>(Bm) & 15) || (reinterpret_cast<uintptr_t>(Cm) & 15) ||
       (reinterpret_cast<uintptr_t>(z) & 15) || ldy % 4 || (reinterpret_cast<uintptr_t>(y) & 15))
     return SQ_ERR_ARG;
-  static bool attr = false;
-  if (!attr) {
+  static std::once_flag once[64];   // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev & 63], [] {
     cudaFuncSetAttribute(ssd_chunk_tc_kernel<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSsdSmem::ALLOC);
-    attr = true;
-  }
+  });
   ssd_chunk_tc_kernel<TN><<<dim3(p->n_heads, B), TC_SSD_THREADS, TcSsdSmem::ALLOC, st>>>(
       *p, T, x, ldx, Bm, Cm, ldbc, dt, lddt, z, ldz, state, state_in, y, ldy);
   return check_launch("sq_ssd_scan_int8 (tcgen05 chunks)");

@@ -79,10 +79,6 @@ class QuantizedMambaLM:
         fused = [b for b in self.blocks if getattr(b, "fused_decode", False)]
         if fused:
             ws["dws"] = e((ops.mamba2_decode_ws_bytes(fused[0].decode_params, M),), torch.uint8)
-        if d.d_model % 128 == 0:      # 128-block code sums for the W4A8 offset correction
-            ws["u_gs"] = e((M, d.d_model // 128), torch.int32)
-        if d.d_inner % 128 == 0:
-            ws["yq_gs"] = e((M, d.d_inner // 128), torch.int32)
         if any(not b.a8 for b in self.blocks):
             ws.update(uf=e((M, d.d_model), torch.float32), zxf=e((M, d.in_proj_out), torch.float32),
                       convf=e((M, d.conv_dim), torch.float32), r=e((M, d.d_inner), torch.float32))
@@ -98,9 +94,8 @@ class QuantizedMambaLM:
         for l, blk in enumerate(self.blocks):
             st = states[l]
             if blk.a8:
-                ugs = ws.get("u_gs") if blk.profile == "W4A8" else None   # block sums feed W4A8 only
-                ops.rmsnorm_quant(h, self.layer_norms[l], EPS_NORM, blk.s_u, ws["u"], ugs)
-                blk.forward_codes(ws["u"], B, T, st, state_in, resid=h, ws=ws, u_gsum=ugs)
+                ops.rmsnorm_quant(h, self.layer_norms[l], EPS_NORM, blk.s_u, ws["u"])
+                blk.forward_codes(ws["u"], B, T, st, state_in, resid=h, ws=ws)
             else:
                 ops.rmsnorm_f32(h, self.layer_norms[l], EPS_NORM, ws["uf"])
                 blk.forward_a16(ws["uf"], B, T, st, state_in, resid=h, ws=ws)
@@ -110,10 +105,8 @@ class QuantizedMambaLM:
         else:   # last token of every sequence only
             hs = h.view(B, T, -1)[:, T - 1, :]
             hq, lg = ws["hq"][:B], ws["logits"][:B]
-        hgs = ws.get("u_gs")
-        hgs = hgs[:hq.shape[0]] if hgs is not None else None
-        ops.rmsnorm_quant(hs, self.final_norm, EPS_NORM, self.s_head, hq, hgs)
-        self.head.a8(hq, ops.EPI_F32, lg, gsum=hgs)
+        ops.rmsnorm_quant(hs, self.final_norm, EPS_NORM, self.s_head, hq)
+        self.head.a8(hq, ops.EPI_F32, lg)
         return lg
 
     def prefill(self, tokens: torch.Tensor, states=None, all_logits=False):

@@ -177,17 +177,39 @@ def gemm_w8a8(a, w, alpha, epi=EPI_F32, out=None, col_scale=None):
     return out
 
 
-def gemm_w4a8(a, w4, sg, group, alpha, N, epi=EPI_F32, out=None, col_scale=None, gsum=None):
+def tile_group_scales(s_group):
+    """SPEC PerGroup scales [N x G] f32 -> the W4A8 kernel's tiled layout [ceil(N/128)][G][128]."""
+    _dev(s_group, torch.float32, "s_group", 2)
+    N, G = s_group.shape
+    s = s_group.contiguous()
+    out = torch.empty(int(lib().sq_group_scale_elems(N, G)), dtype=torch.float32, device=s.device)
+    _check(lib().sq_tile_group_scales(s.data_ptr(), N, G, out.data_ptr(), _stream()))
+    return out
+
+
+def gemm_w4a8_splits(M: int, N: int, K: int) -> int:
+    """K split of the W4A8 tensor-core kernel for this shape (its f32 summation order)."""
+    return int(lib().sq_gemm_w4a8_splits(M, N, K))
+
+
+def gemm_w4a8(a, w4, w_scale, group, s_a, N, epi=EPI_F32, out=None, col_scale=None):
+    """W4A8 projection with SPEC per-group scales; ``w_scale`` in the tiled layout of
+    ``tile_group_scales``, ``s_a`` the per-tensor activation scale."""
     _dev(a, torch.int8, "a", 2)
     _dev(w4, torch.uint8, "w4")
-    _dev(sg, torch.int8, "sg", 2)
+    _dev(w_scale, torch.float32, "w_scale")
     M, K = a.shape
-    if sg.shape != (N, K // group):
-        raise LayoutError(f"sg must be [{N} x {K // group}]")
+    if K % group:
+        raise LayoutError(f"group {group} must divide K={K}")
+    if w_scale.numel() != int(lib().sq_group_scale_elems(N, K // group)):
+        raise LayoutError(f"w_scale must hold the tiled [{N} x {K // group}] group scales")
+    if w4.numel() < w4_bytes(N, K):
+        raise ShapeError(f"w4 must hold {w4_bytes(N, K)} bytes")
+    if epi == EPI_QUANT and (col_scale is None or col_scale.numel() < N):
+        raise ShapeError("EPI_QUANT needs col_scale [N]")
     out = _gemm_out(a, N, epi, out)
-    gp, gl = _gs(gsum, M, K)
-    _check(lib().sq_gemm_w4a8(a.data_ptr(), _ld(a), w4.data_ptr(), sg.data_ptr(), group, alpha.data_ptr(), M, N, K,
-                              epi, out.data_ptr(), _ld(out), _opt(col_scale), gp, gl, _stream()))
+    _check(lib().sq_gemm_w4a8(a.data_ptr(), _ld(a), w4.data_ptr(), w_scale.data_ptr(), group, float(s_a), M, N, K,
+                              epi, out.data_ptr(), _ld(out), _opt(col_scale), _stream()))
     return out
 
 
@@ -342,16 +364,53 @@ def selective_scan_f32(p, B, T, x, dt, BC, z, state, state_in, y):
     return y
 
 
-def set_decode_stages(mask: int):
-    """Profiling control: launches issued by mamba2_decode_step_int8 (1 conv | 2 state | 4 norm)."""
-    _check(lib().sq_set_decode_stages(int(mask)))
+# ------------------------------------------------------------------ SPEC float ops
+def discretize_f32(dt_raw, dt_bias, A):
+    """Δ = softplus(Δ_raw + dt_bias), Ȧ = exp(Δ·A) (SPEC.md:290-298).  dt_raw [M×H];
+    A [H] (Mamba2) or [H×N] (Mamba1) → (Ȧ [M×H] or [M×H×N], Δ [M×H])."""
+    _dev(dt_raw, torch.float32, "dt_raw", 2)
+    _dev(dt_bias, torch.float32, "dt_bias", 1)
+    _dev(A, torch.float32, "A")
+    M, H = dt_raw.shape
+    N = 1 if A.dim() == 1 else A.shape[1]
+    if A.shape[0] != H or dt_bias.shape[0] != H:
+        raise ShapeError(f"A / dt_bias must have {H} rows")
+    dA = torch.empty((M, H) if A.dim() == 1 else (M, H, N), dtype=torch.float32, device=dt_raw.device)
+    delta = torch.empty((M, H), dtype=torch.float32, device=dt_raw.device)
+    _check(lib().sq_discretize_f32(dt_raw.data_ptr(), _ld(dt_raw), dt_bias.data_ptr(), A.contiguous().data_ptr(),
+                                   M, H, N, dA.data_ptr(), delta.data_ptr(), _stream()))
+    return dA, delta
 
 
-def set_ssd_mode(mode: int):
-    """Mamba2 prefill chunk scan: 0 = mma.sync (64-token chunks), 1 = tcgen05 / TMEM (128-token chunks)."""
-    _check(lib().sq_set_ssd_mode(int(mode)))
+def selective_scan2_pre_f32(p, B, T, x, dA, delta, Bm, Cm, z, state, state_in, y):
+    """Mamba2 recurrence on precomputed Ȧ / Δ [B·T×nh]; z None = ungated."""
+    for n, t in (("x", x), ("dA", dA), ("delta", delta), ("B", Bm), ("C", Cm), ("y", y)):
+        _dev(t, torch.float32, n, 2)
+    _dev(state, torch.float32, "state")
+    if dA.stride(0) != delta.stride(0) or Bm.stride(0) != Cm.stride(0):
+        raise LayoutError("dA/delta and B/C must share row strides")
+    if state.numel() != B * p.n_heads * p.head_dim * p.d_state:
+        raise ShapeError("state must be [B x nh x P x N]")
+    _check(lib().sq_selective_scan2_pre_f32(C.byref(p), B, T, x.data_ptr(), _ld(x), dA.data_ptr(), delta.data_ptr(),
+                                            _ld(dA), Bm.data_ptr(), Cm.data_ptr(), _ld(Bm), _opt(z),
+                                            0 if z is None else _ld(z), state.data_ptr(), int(bool(state_in)),
+                                            y.data_ptr(), _ld(y), _stream()))
+    return y
 
 
-def set_gemm_mode(mode: int):
-    """0: legacy mma.sync GEMM, 1: tcgen05 (W4 operand expanded into TMEM), 2: tcgen05 (into smem)."""
-    _check(lib().sq_set_gemm_mode(int(mode)))
+def selective_scan1_pre_f32(p, B, T, x, dA, delta, Bm, Cm, z, state, state_in, y):
+    """Mamba1 recurrence on precomputed Ȧ [B·T×d×N] / Δ [B·T×d]; z None = ungated."""
+    for n, t in (("x", x), ("delta", delta), ("B", Bm), ("C", Cm), ("y", y)):
+        _dev(t, torch.float32, n, 2)
+    _dev(dA, torch.float32, "dA", 3)
+    _dev(state, torch.float32, "state")
+    if Bm.stride(0) != Cm.stride(0):
+        raise LayoutError("B and C must share a row stride")
+    if state.numel() != B * p.d_inner * p.d_state:
+        raise ShapeError("state must be [B x d_inner x N]")
+    _check(lib().sq_selective_scan1_pre_f32(C.byref(p), B, T, x.data_ptr(), _ld(x), dA.data_ptr(), delta.data_ptr(),
+                                            _ld(delta), Bm.data_ptr(), Cm.data_ptr(), _ld(Bm), _opt(z),
+                                            0 if z is None else _ld(z), state.data_ptr(), int(bool(state_in)),
+                                            y.data_ptr(), _ld(y), _stream()))
+    return y
+

@@ -10,8 +10,9 @@ sq_rmsnorm_quant, GEMM requant epilogues).
 Weight formats (LEDGER G11):
 * ``quantize_weight_w8``   PerChannel(axis=0) 8-bit          — W8A8 (int32 over all of K)
 * ``quantize_weight_w4``   PerGroup(axis=1, 128) 4-bit float — W4A16 (SPEC literal)
-* ``quantize_weight_w4a8`` progressive PerGroup: scale[n,g] = s_ch[n]·sg[n,g] with integer
-  sg ∈ [1,15], so w8 = w4·sg is exact int8 and the A8 GEMM accumulates in int32 over K.
+* ``quantize_weight_w4a8`` the same SPEC PerGroup 4-bit weights; the A8 GEMM keeps one exact
+  int32 accumulator per group and promotes it with the group's float scale (round 2; the
+  round-1 progressive s_ch·sg scales measured worse SQNR, scripts/g11b_sqnr.py).
 """
 from __future__ import annotations
 
@@ -143,7 +144,7 @@ def quantize_weight_w8(w) -> QTensor:
     s = _group_absmax_scale(w, 8)
     codes = _codes(w, s[:, None], 8)
     return QTensor(tuple(w.shape), 8, codes, ScaleLayout("PerChannel", s, axis=0),
-                   extra={"s_ch": s, "sg": torch.ones((w.shape[0], 1), dtype=torch.int8), "group": w.shape[1]})
+                   extra={"s_ch": s, "group": w.shape[1]})
 
 
 def quantize_weight_w4(w, group: int = 128) -> QTensor:
@@ -160,18 +161,6 @@ def quantize_weight_w4(w, group: int = 128) -> QTensor:
 
 
 def quantize_weight_w4a8(w, group: int = 128) -> QTensor:
-    """Progressive per-group 4-bit weights for the A8 GEMM (LEDGER G11b):
-    s_gf = max|w_g|/7, s_ch = max_g s_gf / 15, sg = clamp(ceil(s_gf/s_ch), 1, 15),
-    codes = clamp(rint(w / (s_ch·sg)))."""
-    w = _f32(w)
-    n, k = w.shape
-    if k % group:
-        raise ShapeError("K must be a multiple of the group size")
-    wg = w.reshape(n, k // group, group)
-    s_gf = _group_absmax_scale(wg, 4)
-    s_ch = s_gf.amax(dim=1) / np.float32(15.0)
-    sg = torch.clamp(torch.ceil(s_gf / s_ch[:, None]), 1, 15).to(torch.int8)
-    scale = s_ch[:, None] * sg.to(torch.float32)
-    codes = _codes(wg, scale[:, :, None], 4).reshape(n, k)
-    return QTensor((n, k), 4, codes, ScaleLayout("PerGroup", scale.reshape(-1), axis=1, group_size=group),
-                   extra={"s_ch": s_ch, "sg": sg, "group": group})
+    """W4A8 weights: SPEC PerGroup 4-bit with float group scales, the
+    W4A16 format; only the activation precision differs (LEDGER G11)."""
+    return quantize_weight_w4(w, group)

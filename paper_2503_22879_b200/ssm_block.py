@@ -90,13 +90,11 @@ class SsmState:
 
 @dataclass
 class QLinear:
-    """A quantized projection.  kind "w8": int8 per-output-channel (s_ch); "w4a8":
-    4-bit codes with progressive group scales s_ch·sg (LEDGER G11b); "w4a16": 4-bit
-    codes with float group scales s_group (SPEC PerGroup)."""
+    """A quantized projection.  kind "w8": int8 per-output-channel (s_ch); "w4a8" / "w4a16":
+    4-bit codes with float group scales s_group (SPEC PerGroup, LEDGER G11)."""
     kind: str
     codes: np.ndarray
     s_ch: np.ndarray | None = None
-    sg: np.ndarray | None = None
     s_group: np.ndarray | None = None
     group: int = 128
 
@@ -169,29 +167,32 @@ class DeviceLinear:
             else:
                 packed = _t(pack_u4_host(ql.codes), torch.uint8, dev)
                 self.w = ops.repack_w4(packed, self.N, self.K)
-        if self.kind == "w4a8":
-            sg = ql.sg
-            self.sg = sg if isinstance(sg, torch.Tensor) else _t(np.asarray(sg).astype(np.int8), torch.int8, dev)
-        if self.kind == "w4a16":
+        if self.kind in ("w4a8", "w4a16"):
             sgr = ql.s_group
             self.s_group = sgr if isinstance(sgr, torch.Tensor) else _t(np.asarray(sgr, np.float32), torch.float32, dev)
-        else:
+            if self.s_group.shape != (self.N, self.K // self.group):
+                raise ShapeError(f"s_group must be [{self.N} x {self.K // self.group}]")
+        if self.kind == "w4a8":
+            self.ws = ops.tile_group_scales(self.s_group)   # kernel layout [N/128][G][128]
+        if self.kind == "w8":
             self.s_ch = np.asarray(ql.s_ch, np.float32)
             self.alpha = None
-            if s_a is not None:
-                self.set_input_scale(s_a)
+        self.s_a = None
+        if s_a is not None:
+            self.set_input_scale(s_a)
 
     def set_input_scale(self, s_a: float):
-        """alpha[n] = f32(s_ch[n] · s_a) (fuse_scales, SPEC.md:137-145)."""
-        dev = self.w.device
-        self.alpha = _t((self.s_ch * np.float32(s_a)).astype(np.float32), torch.float32, dev)
+        """W8: alpha[n] = f32(s_ch[n] · s_a) (fuse_scales); W4A8: s_a scales
+        the promoted per-group sum."""
+        self.s_a = np.float32(s_a)
+        if self.kind == "w8":
+            self.alpha = _t((self.s_ch * np.float32(s_a)).astype(np.float32), torch.float32, self.w.device)
 
-    def a8(self, a_codes, epi, out=None, col_scale=None, gsum=None):
-        """``gsum``: optional int32 128-block sums of ``a_codes`` (W4A8 offset correction)."""
+    def a8(self, a_codes, epi, out=None, col_scale=None):
         if self.kind == "w8":
             return ops.gemm_w8a8(a_codes, self.w, self.alpha, epi, out, col_scale)
         if self.kind == "w4a8":
-            return ops.gemm_w4a8(a_codes, self.w, self.sg, self.group, self.alpha, self.N, epi, out, col_scale, gsum)
+            return ops.gemm_w4a8(a_codes, self.w, self.ws, self.group, self.s_a, self.N, epi, out, col_scale)
         raise ShapeError("A8 GEMM on a W4A16 projection")
 
     def a16(self, x, out=None, resid=False):
@@ -200,9 +201,7 @@ class DeviceLinear:
     @property
     def nbytes(self):
         n = self.w.numel() * self.w.element_size()
-        if self.kind == "w4a8":
-            n += self.sg.numel()
-        if self.kind == "w4a16":
+        if self.kind in ("w4a8", "w4a16"):
             n += self.s_group.numel() * 4
         else:
             n += self.N * 4
@@ -293,14 +292,14 @@ class DeviceBlock:
         return n
 
     # ------------------------------------------------------------------ forward
-    def forward_codes(self, u_codes, B, T, state: SsmState, state_in: bool, resid=None, ws=None, u_gsum=None):
+    def forward_codes(self, u_codes, B, T, state: SsmState, state_in: bool, resid=None, ws=None):
         """A8 block on int8 input codes [B*T × d_model].  If ``resid`` is given the out_proj
         epilogue adds into it (residual stream) and it is returned; else returns f32 out."""
         d = self.dims
         di = d.d_inner
         M = B * T
         ws = ws if ws is not None else {}
-        zx = self.in_proj.a8(u_codes, ops.EPI_QUANT, ws.get("zx"), self.in_out_scale, u_gsum)
+        zx = self.in_proj.a8(u_codes, ops.EPI_QUANT, ws.get("zx"), self.in_out_scale)
         y = ws.get("y")
         if y is None:
             y = torch.empty((M, di), dtype=torch.float32, device=u_codes.device)
@@ -309,12 +308,11 @@ class DeviceBlock:
             xbc = zx[:, di:2 * di + 2 * gn]
             if T == 1 and state_in and self.fused_decode:
                 # conv update + int8 state update + gated norm + FWHT + quant (sq_mamba2_decode_step_int8)
-                ygs = ws.get("yq_gs") if self.profile == "W4A8" else None   # block sums feed W4A8 only
                 yq = ops.mamba2_decode_step_int8(self.decode_params, B, zx, state.conv_cache, state.h, ws.get("yq"),
-                                                 y, ws.get("dws"), ygs)
+                                                 y, ws.get("dws"))
                 if resid is not None:
-                    return self.out_proj.a8(yq, ops.EPI_RESID, resid, gsum=ygs)
-                return self.out_proj.a8(yq, ops.EPI_F32, ws.get("out"), gsum=ygs)
+                    return self.out_proj.a8(yq, ops.EPI_RESID, resid)
+                return self.out_proj.a8(yq, ops.EPI_F32, ws.get("out"))
             if T == 1 and state_in:
                 cv = ops.conv1d_update_int8(xbc, self.conv_w, self.conv_b, self.conv_in_scale, self.conv_out_scale,
                                             state.conv_cache, ws.get("conv"))
@@ -374,6 +372,157 @@ class DeviceBlock:
         if resid is not None:
             return self.out_proj.a16(r, resid, resid=True)
         return self.out_proj.a16(r, ws.get("out"))
+
+
+# ============================================================== SPEC float ops on the GPU
+# SPEC.md:272-325 with the reference's argument order (oracle/ssm_block.py restates them).  Each
+# takes CUDA float32 tensors and runs on the library kernels: sq_conv1d_f32, sq_discretize_f32,
+# sq_selective_scan{2,1}_pre_f32, sq_rmsnorm_f32; the float projections are plain library GEMMs
+# (cuBLAS, float64 accumulation like tensor.matmul, pkg/src/ssmquant/tensor.py:33-54).
+def _f32(a, dev=None):
+    if isinstance(a, torch.Tensor):
+        if not a.is_cuda:
+            raise ShapeError("SPEC ops take CUDA tensors (no CPU fallback)")
+        return a.to(torch.float32)
+    return torch.as_tensor(np.asarray(a, np.float32), device=dev or "cuda")
+
+
+def _gemm_f(a, w):
+    w = _f32(w, a.device)
+    return (a.to(torch.float64) @ w.to(torch.float64).T).to(torch.float32)
+
+
+def project_inputs(u, w: SsmBlockWeights):
+    """Mamba2 → (x, B, C, Δ_raw, z), slices of one in_proj GEMM in the fixed
+    order z | x | B | C | Δ; Mamba1 → (x, None, None, None, z) (B/C/Δ come from
+    x_proj after the conv)."""
+    d = w.dims
+    u = _f32(u)
+    if u.dim() != 2 or u.shape[1] != d.d_model:
+        raise ShapeError(f"u must be [T x {d.d_model}]")
+    zx = _gemm_f(u, w.in_proj)
+    if zx.shape[1] != d.in_proj_out:
+        raise ShapeError(f"in_proj must have {d.in_proj_out} rows")
+    di = d.d_inner
+    z, x = zx[:, :di], zx[:, di:2 * di]
+    if d.variant == "mamba1":
+        return x, None, None, None, z
+    gn = d.n_state_groups * d.d_state
+    return x, zx[:, 2 * di:2 * di + gn], zx[:, 2 * di + gn:2 * di + 2 * gn], zx[:, 2 * di + 2 * gn:], z
+
+
+def causal_conv1d(x, weight, bias, cache=None):
+    """depthwise causal conv + SiLU over x [T×C] (sq_conv1d_f32); ``cache``
+    [C×(K−1)] holds the previous K−1 inputs (None = zeros).  Returns (y, new_cache)."""
+    x = _f32(x)
+    wt, b = _f32(weight, x.device).contiguous(), _f32(bias, x.device).contiguous()
+    T, C_ = x.shape
+    K = wt.shape[1]
+    if wt.shape[0] != C_ or b.shape[0] != C_:
+        raise ShapeError("cache/channel mismatch: weight / bias channels")
+    cc = torch.zeros((1, K - 1, C_), dtype=torch.float32, device=x.device)
+    if cache is not None:
+        cache = _f32(cache, x.device)
+        if tuple(cache.shape) != (C_, K - 1):
+            raise ShapeError("cache/channel mismatch")
+        cc[0] = cache.T
+    y = ops.conv1d_f32(x.contiguous(), wt, b, 1, T, cc, cache is not None)
+    return y, cc[0].T.contiguous()
+
+
+def discretize(dt_raw, dt_bias, A):
+    """SPEC.md:290-298 (sq_discretize_f32): Δ = softplus(Δ_raw + dt_bias), Ȧ = exp(Δ·A).
+    Mamba2: Δ_raw [T×nh], A [nh] → Ȧ [T×nh]; Mamba1: A [d×N] → Ȧ [T×d×N].  Returns (Ȧ, Δ)."""
+    dt_raw = _f32(dt_raw)
+    return ops.discretize_f32(dt_raw, _f32(dt_bias, dt_raw.device).contiguous(), _f32(A, dt_raw.device))
+
+
+def _scan_pre(x, dA, dt, B, C, D, z, state, head_group):
+    x = _f32(x)
+    dev = x.device
+    T = x.shape[0]
+    Dv = _f32(D, dev).contiguous()
+    if x.dim() == 3:        # Mamba2: x [T×nh×P], Ȧ/Δ [T×nh], B/C [T×G×N]
+        _, nh, P = x.shape
+        G, N = B.shape[1], B.shape[2]
+        hg = (torch.as_tensor(np.asarray(head_group), dtype=torch.int32, device=dev) if head_group is not None
+              else (torch.arange(nh, device=dev, dtype=torch.int32) // (nh // G)))
+        zero = torch.zeros(nh, dtype=torch.float32, device=dev)
+        p = ops.mamba2_params(nh, P, N, G, hg, zero, Dv, zero)
+        h = (torch.zeros((1, nh, P, N), dtype=torch.float32, device=dev) if state is None
+             else _f32(state, dev).reshape(1, nh, P, N).clone())
+        y = torch.empty((T, nh * P), dtype=torch.float32, device=dev)
+        zz = None if z is None else _f32(z, dev).reshape(T, nh * P).contiguous()
+        ops.selective_scan2_pre_f32(p, 1, T, x.reshape(T, nh * P).contiguous(), _f32(dA, dev).contiguous(),
+                                    _f32(dt, dev).contiguous(), _f32(B, dev).reshape(T, G * N).contiguous(),
+                                    _f32(C, dev).reshape(T, G * N).contiguous(), zz, h, state is not None, y)
+        _keep = (hg, zero, Dv)   # noqa: F841  (the params struct holds raw pointers)
+        return y.reshape(T, nh, P), h[0]
+    _, d = x.shape          # Mamba1: x [T×d], Ȧ [T×d×N], Δ [T×d], B/C [T×N]
+    N = B.shape[1]
+    zero = torch.zeros(d * N, dtype=torch.float32, device=dev)
+    ones = torch.ones(d, dtype=torch.float32, device=dev)
+    p = ops.mamba1_params(d, N, zero, Dv, zero, 1.0, 1.0, 1.0, 1.0, ones, ones)
+    h = (torch.zeros((1, d, N), dtype=torch.float32, device=dev) if state is None
+         else _f32(state, dev).reshape(1, d, N).clone())
+    y = torch.empty((T, d), dtype=torch.float32, device=dev)
+    zz = None if z is None else _f32(z, dev).contiguous()
+    ops.selective_scan1_pre_f32(p, 1, T, x.contiguous(), _f32(dA, dev).contiguous(), _f32(dt, dev).contiguous(),
+                                _f32(B, dev).contiguous(), _f32(C, dev).contiguous(), zz, h, state is not None, y)
+    _keep = (zero, ones, Dv)   # noqa: F841
+    return y, h.reshape(1, d, N)
+
+
+def selective_scan(x, dA, dt, B, C, D, z=None, state=None, head_group=None):
+    """SPEC.md:299-307, Eq. 2: h_t = Ȧ_t h_{t−1} + (Δ_t x_t) B_t, y_t = C_t·h_t + D x_t, optional
+    gate y·SiLU(z).  Mamba2 when x is [T×nh×P] (B/C [T×G×N] per state group), Mamba1 when x is
+    [T×d] (Ȧ [T×d×N], B/C [T×N]).  Returns (y, h) like the oracle (oracle/ssm_block.py)."""
+    return _scan_pre(x, dA, dt, B, C, D, z, state, head_group)
+
+
+def ssd_chunked(x, dA, dt, B, C, D, z=None, chunk=64, state=None, head_group=None):
+    """SPEC.md:308-316 for float operands.  Mamba2 shapes.  The float path evaluates the same
+    f32 recurrence as ``selective_scan`` (exact, so every chunk size gives the same result,
+    within the SPEC's 1e-4 of the block decomposition); the chunked tensor-core engines serve
+    the int8 path (sq_ssd_scan_int8, ``DeviceBlock.forward_codes``)."""
+    if chunk < 1:
+        raise ValueError("chunk must be >= 1")
+    if _f32(x).dim() != 3:
+        raise ShapeError("ssd_chunked takes Mamba2 operands x [T x nh x P]")
+    return _scan_pre(x, dA, dt, B, C, D, z, state, head_group)
+
+
+def block_forward_float(u, w: SsmBlockWeights, state: SsmState | None = None, chunk=None):
+    """SPEC.md:317-325 on the GPU: project → conv → discretize → scan/SSD → gate → RMSNorm →
+    out_proj for one sequence u [T×d_model].  Returns (out [T×d_model], SsmState) with the
+    state in the SPEC layout (h [nh×P×N] / [1×d×N], conv_cache [C×(K−1)])."""
+    d = w.dims
+    u = _f32(u)
+    dev = u.device
+    x, Bi, Ci, dt_raw, z = project_inputs(u, w)
+    A = -torch.exp(_f32(w.a_log, dev))
+    cache = None if state is None else state.conv_cache
+    h0 = None if state is None else state.h
+    T = u.shape[0]
+    if d.variant == "mamba2":
+        di, gn = d.d_inner, d.n_state_groups * d.d_state
+        co, cache = causal_conv1d(torch.cat([x, Bi, Ci], 1), w.conv_weight, w.conv_bias, cache)
+        dA, dt = discretize(dt_raw, w.dt_bias, A)
+        scan = selective_scan if chunk is None else (lambda *a, **k: ssd_chunked(*a, chunk=chunk, **k))
+        y, h = scan(co[:, :di].reshape(T, d.n_heads, d.head_dim), dA, dt,
+                    co[:, di:di + gn].reshape(T, d.n_state_groups, d.d_state),
+                    co[:, di + gn:].reshape(T, d.n_state_groups, d.d_state), w.d_param,
+                    z=z.reshape(T, d.n_heads, d.head_dim), state=h0, head_group=w.head_group)
+        y = y.reshape(T, di)
+    else:
+        R, N = d.dt_rank, d.d_state
+        xc, cache = causal_conv1d(x, w.conv_weight, w.conv_bias, cache)
+        xd = _gemm_f(xc, w.x_proj)
+        dt_raw = _gemm_f(xd[:, :R].contiguous(), w.dt_proj)
+        dA, dt = discretize(dt_raw, w.dt_bias, A)
+        y, h = selective_scan(xc, dA, dt, xd[:, R:R + N], xd[:, R + N:R + 2 * N], w.d_param, z=z, state=h0)
+    r = ops.rmsnorm_f32(y.contiguous(), _f32(w.norm_weight, dev).contiguous(), EPS_NORM)
+    return _gemm_f(r, w.out_proj), SsmState(h, cache)
 
 
 def block_forward_quantized(u, qw, plan=None, bits_profile=None, state: SsmState | None = None, batch: int = 1):

@@ -25,22 +25,20 @@ def _slice_scales(d: Dims):
     return s
 
 
-def _analytic_qlinear(r, n, k, kind, group, out_std, in_code_std):
+def _analytic_qlinear(r, n, k, kind, group, out_std, in_code_std, s_a=1.0):
+    """Weights whose outputs have std ~out_std (float units) for A8 inputs of code std
+    in_code_std and input scale s_a (the epilogue multiplies by s_a), or float inputs of std 1."""
     group = min(group, k)
     if kind == "w8":
         codes = r.integers(-127, 128, (n, k)).astype(np.int8)
         rms = np.sqrt((codes.astype(np.float64) ** 2).mean(axis=1))
-        s_ch = (out_std / (np.sqrt(k) * in_code_std * rms)).astype(np.float32)
-        return QLinear("w8", codes, s_ch=s_ch, sg=np.ones((n, 1), np.int8), group=k)
+        s_ch = (out_std / (s_a * np.sqrt(k) * in_code_std * rms)).astype(np.float32)
+        return QLinear("w8", codes, s_ch=s_ch, group=k)
     codes = r.integers(-8, 8, (n, k)).astype(np.int8)
-    if kind == "w4a8":
-        sg = r.integers(1, 16, (n, k // group)).astype(np.int8)
-        w8 = codes.astype(np.float64).reshape(n, k // group, group) * sg[:, :, None]
-        rms = np.sqrt((w8 ** 2).reshape(n, k).mean(axis=1))
-        s_ch = (out_std / (np.sqrt(k) * in_code_std * rms)).astype(np.float32)
-        return QLinear("w4a8", codes, s_ch=s_ch, sg=sg, group=group)
-    s_group = r.uniform(0.5, 1.5, (n, k // group)).astype(np.float32) * np.float32(out_std / (np.sqrt(k) * 4.6))
-    return QLinear("w4a16", codes, s_group=s_group.astype(np.float32), group=group)
+    # per-group float scales (SPEC PerGroup); A8 inputs are codes of std in_code_std
+    std_in = in_code_std * s_a if kind == "w4a8" else 1.0
+    s_group = r.uniform(0.5, 1.5, (n, k // group)).astype(np.float32) * np.float32(out_std / (np.sqrt(k) * 4.6 * std_in))
+    return QLinear(kind, codes, s_group=s_group.astype(np.float32), group=group)
 
 
 def random_qblock(d: Dims, profile: str, seed: int = 0) -> QBlock:
@@ -48,8 +46,10 @@ def random_qblock(d: Dims, profile: str, seed: int = 0) -> QBlock:
     kind = {"W8A8": "w8", "W4A8": "w4a8", "W4A16": "w4a16"}[profile]
     di = d.d_inner
     s = np.float32(4.0 / 127)
-    inp = _analytic_qlinear(r, d.in_proj_out, d.d_model, kind, 128, 1.0, U_STD_CODES)
-    out = _analytic_qlinear(r, d.d_model, di, kind, 128, 0.1, 127.0 / 4.0)
+    hb = di & -di
+    s_y = np.float32(4.5 * np.sqrt(hb) / 127)
+    inp = _analytic_qlinear(r, d.in_proj_out, d.d_model, kind, 128, 1.0, U_STD_CODES, s)
+    out = _analytic_qlinear(r, d.d_model, di, kind, 128, 0.1, 127.0 / 4.0, s_y)
     C = d.conv_dim
     K = d.conv_kernel
     conv_w = (r.standard_normal((C, K)) * 0.5 / np.sqrt(K)).astype(np.float32)
@@ -63,8 +63,6 @@ def random_qblock(d: Dims, profile: str, seed: int = 0) -> QBlock:
         a_log = np.log(np.tile(np.arange(1, d.d_state + 1, dtype=np.float32), (di, 1))).astype(np.float32)
     dpar = np.ones(nd, np.float32)
     norm = (1.0 + 0.1 * r.standard_normal(di)).astype(np.float32)
-    hb = di & -di
-    s_y = np.float32(4.5 * np.sqrt(hb) / 127)
     qb = QBlock(d, profile, inp, out, conv_w, conv_b, a_log, dpar, dt_bias, norm,
                 head_group=(np.arange(d.n_heads) // max(1, d.n_heads // d.n_state_groups)).astype(np.int32)
                 if d.variant == "mamba2" else None,
@@ -83,7 +81,7 @@ def random_qblock(d: Dims, profile: str, seed: int = 0) -> QBlock:
         rows = di
         R, N = d.dt_rank, d.d_state
         qb.x_proj = _analytic_qlinear(r, R + 2 * N, di, "w8" if kind == "w8" else "w4a8", 128, 1.0, 64.0)
-        qb.dt_proj = _analytic_qlinear(r, di, R, "w8" if kind == "w8" else "w4a8", 32, 1.0, U_STD_CODES)
+        qb.dt_proj = _analytic_qlinear(r, di, R, "w8" if kind == "w8" else "w4a8", 32, 1.0, U_STD_CODES, s)
         qb.xproj_out_scale = np.full(R + 2 * N, s, np.float32)
         qb.s_dt = s
     qb.state_scale = (r.uniform(0.5, 1.0, rows) * 0.5 / 127).astype(np.float32)
@@ -97,24 +95,21 @@ class DeviceQL:
     shape: tuple
     group: int
     device_w: torch.Tensor
-    sg: object = None
     s_ch: object = None
     s_group: object = None
 
 
-def _device_ql(g: torch.Generator, n, k, kind, dev, group=128, in_code_std=U_STD_CODES, out_std=1.0):
+def _device_ql(g: torch.Generator, n, k, kind, dev, group=128, in_code_std=U_STD_CODES, out_std=1.0, s_a=1.0):
     group = min(group, k)
     if kind == "w8":
         w = torch.randint(-127, 128, (n, k), generator=g, device=dev, dtype=torch.int8)
-        s_ch = np.full(n, out_std / (np.sqrt(k) * in_code_std * 73.3), np.float32)
+        s_ch = np.full(n, out_std / (s_a * np.sqrt(k) * in_code_std * 73.3), np.float32)
         return DeviceQL("w8", (n, k), k, w, s_ch=s_ch)
     w = torch.randint(0, 256, (n * k // 2,), generator=g, device=dev, dtype=torch.uint8)
-    if kind == "w4a8":
-        sg = torch.randint(1, 16, (n, k // group), generator=g, device=dev, dtype=torch.int8)
-        s_ch = np.full(n, out_std / (np.sqrt(k) * in_code_std * 4.6 * 9.0), np.float32)
-        return DeviceQL("w4a8", (n, k), group, w, sg=sg, s_ch=s_ch)
-    s_group = torch.full((n, k // group), out_std / (np.sqrt(k) * 4.6), device=dev, dtype=torch.float32)
-    return DeviceQL("w4a16", (n, k), group, w, s_group=s_group)
+    std_in = in_code_std * s_a if kind == "w4a8" else 1.0
+    s_group = torch.rand((n, k // group), generator=g, device=dev, dtype=torch.float32).add_(0.5).mul_(
+        out_std / (np.sqrt(k) * 4.6 * std_in))
+    return DeviceQL(kind, (n, k), group, w, s_group=s_group)
 
 
 def device_qblock(d: Dims, profile: str, seed: int, dev) -> DeviceBlock:
@@ -125,15 +120,15 @@ def device_qblock(d: Dims, profile: str, seed: int, dev) -> DeviceBlock:
     small = random_qblock(Dims(d.variant, 32, d.d_inner, d.d_state, d.n_heads, d.head_dim, d.n_state_groups,
                                d.conv_kernel, d.dt_rank), profile, seed)
     small.dims = d
-    small.in_proj = _device_ql(g, d.in_proj_out, d.d_model, kind, dev)
-    small.out_proj = _device_ql(g, d.d_model, d.d_inner, kind, dev, in_code_std=127.0 / 4, out_std=0.1)
+    small.in_proj = _device_ql(g, d.in_proj_out, d.d_model, kind, dev, s_a=small.s_u)
+    small.out_proj = _device_ql(g, d.d_model, d.d_inner, kind, dev, in_code_std=127.0 / 4, out_std=0.1, s_a=small.s_y)
     if profile != "W4A16":
         small.in_out_scale = np.full(d.in_proj_out, np.float32(4.0 / 127), np.float32)
         if d.variant == "mamba1":
             R, N = d.dt_rank, d.d_state
             k2 = "w8" if kind == "w8" else "w4a8"
-            small.x_proj = _device_ql(g, R + 2 * N, d.d_inner, k2, dev)
-            small.dt_proj = _device_ql(g, d.d_inner, R, k2, dev, group=32)
+            small.x_proj = _device_ql(g, R + 2 * N, d.d_inner, k2, dev, in_code_std=64.0)
+            small.dt_proj = _device_ql(g, d.d_inner, R, k2, dev, group=32, s_a=small.s_u)
     return DeviceBlock(small, dev)
 
 
@@ -157,7 +152,7 @@ def synthetic_lm(d: Dims, n_layers: int, profile: str, vocab: int, dev="cuda", s
     emb = torch.randint(-127, 128, (vocab, d.d_model), generator=g, device=dev, dtype=torch.int8)
     es = torch.full((vocab,), 1.0 / 127, device=dev)
     blocks = [device_qblock(d, profile, seed + l, dev) for l in range(n_layers)]
-    head = _device_ql(g, vocab, d.d_model, head_kind, dev)
+    head = _device_ql(g, vocab, d.d_model, head_kind, dev, s_a=np.float32(4.0 / 127))
     host = SynthHost(d, [profile] * n_layers, emb, es, [np.ones(d.d_model, np.float32)] * n_layers, blocks,
                      np.ones(d.d_model, np.float32), head, np.float32(4.0 / 127))
     return QuantizedMambaLM(host, dev)

@@ -1,4 +1,5 @@
-"""Time the A8 GEMM modes on the decode/prefill projection shapes (CUDA events)."""
+"""Time the A8 projection GEMMs on the decode / prefill shapes (CUDA events, distinct weight
+buffers per launch so every launch streams its weights from HBM, as in the decode step)."""
 import os
 import sys
 
@@ -13,13 +14,13 @@ SHAPES = [("in_proj 8B b64", 64, 18560, 4096), ("out_proj 8B b64", 64, 4096, 819
 
 
 def timeit(fn, reps=20):
-    for _ in range(3):
-        fn()
+    for i in range(3):
+        fn(i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(reps):
-        fn()
+    for i in range(reps):
+        fn(i)
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
@@ -30,16 +31,15 @@ for name, M, N, K in SHAPES:
     a = torch.randint(-128, 128, (M, K), dtype=torch.int8, device=dev)
     alpha = torch.rand(N, device=dev) * 1e-3
     out = torch.empty((M, N), dtype=torch.float32, device=dev)
-    w4 = torch.randint(0, 256, (ops.w4_bytes(N, K),), dtype=torch.uint8, device=dev)
-    sg = torch.randint(1, 16, (N, K // 128), dtype=torch.int8, device=dev)
-    w8 = torch.randint(-127, 128, (N, K), dtype=torch.int8, device=dev)
-    for mode in (0, 1, 2):
-        ops.set_gemm_mode(mode)
-        t4 = timeit(lambda: ops.gemm_w4a8(a, w4, sg, 128, alpha, N, ops.EPI_F32, out))
-        t8 = timeit(lambda: ops.gemm_w8a8(a, w8, alpha, ops.EPI_F32, out)) if mode != 2 else float("nan")
-        b4 = N * K / 2 + N * K / 128 + M * K + M * N * 4
-        b8 = N * K + M * K + M * N * 4
-        ops_ = 2.0 * M * N * K
-        print(f"{name:24s} mode={mode} W4A8 {t4*1e3:8.1f} us {b4/t4/1e6:7.0f} GB/s {ops_/t4/1e9:7.1f} TOPS | "
-              f"W8A8 {t8*1e3:8.1f} us {b8/t8/1e6:7.0f} GB/s {ops_/t8/1e9:7.1f} TOPS", flush=True)
-ops.set_gemm_mode(1)
+    nbuf = max(1, min(8, int(2e9 // (N * K))))     # rotate weights so they do not sit in L2
+    w4 = [torch.randint(0, 256, (ops.w4_bytes(N, K),), dtype=torch.uint8, device=dev) for _ in range(nbuf)]
+    ws = [ops.tile_group_scales(torch.rand(N, K // 128, device=dev) * 1e-2 + 1e-3) for _ in range(nbuf)]
+    w8 = [torch.randint(-127, 128, (N, K), dtype=torch.int8, device=dev) for _ in range(nbuf)]
+    t4 = timeit(lambda i: ops.gemm_w4a8(a, w4[i % nbuf], ws[i % nbuf], 128, 0.01, N, ops.EPI_F32, out))
+    t8 = timeit(lambda i: ops.gemm_w8a8(a, w8[i % nbuf], alpha, ops.EPI_F32, out))
+    b4 = N * K / 2 + N * K / 128 * 4 + M * K + M * N * 4
+    b8 = N * K + M * K + M * N * 4
+    ops_ = 2.0 * M * N * K
+    print(f"{name:24s} W4A8 {t4*1e3:8.1f} us {b4/t4/1e6:7.0f} GB/s {ops_/t4/1e9:7.1f} TOPS (splits "
+          f"{ops.gemm_w4a8_splits(M, N, K)}) | W8A8 {t8*1e3:8.1f} us {b8/t8/1e6:7.0f} GB/s {ops_/t8/1e9:7.1f} TOPS",
+          flush=True)

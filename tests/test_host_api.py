@@ -36,8 +36,7 @@ def test_weight_quantizers_bit_exact():
     a, b = oqz.quantize_weight_w4_group(w, 128), quantizer.quantize_weight_w4(w, 128)
     assert np.array_equal(a.payload, _np(b.payload)) and np.array_equal(a.extra["s_group"], _np(b.extra["s_group"]))
     a, b = oqz.quantize_weight_w4a8(w, 128), quantizer.quantize_weight_w4a8(w, 128)
-    assert np.array_equal(a.payload, _np(b.payload))
-    assert np.array_equal(a.extra["sg"], _np(b.extra["sg"])) and np.array_equal(a.extra["s_ch"], _np(b.extra["s_ch"]))
+    assert np.array_equal(a.payload, _np(b.payload)) and np.array_equal(a.extra["s_group"], _np(b.extra["s_group"]))
 
 
 def test_quantize_layouts_and_spec_examples():
@@ -150,7 +149,7 @@ def test_quantize_pipeline_bit_exact(profile, dims):
             if la is None:
                 assert lb is None
                 continue
-            for f in ("codes", "s_ch", "sg", "s_group"):
+            for f in ("codes", "s_ch", "s_group"):
                 fa, fb = getattr(la, f), getattr(lb, f)
                 assert (fa is None and fb is None) or np.array_equal(np.asarray(fa), np.asarray(fb)), (lin, f)
         for f in ("s_u", "s_y", "s_dt", "in_out_scale", "conv_in_scale", "conv_out_scale", "state_scale",

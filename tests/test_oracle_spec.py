@@ -162,12 +162,54 @@ def test_weight_quantizers_layouts():
     assert q4.payload.min() >= -8 and q4.payload.max() <= 7
     err = np.abs(qz.dequantize(q4) - w)
     assert (err <= np.repeat(q4.extra["s_group"], 128, axis=1) / 2 * 1.0001).all()
+    qa = qz.quantize_weight_w4a8(w, 128)     # LEDGER G11: W4A8 weights are the SPEC PerGroup format
+    assert np.array_equal(qa.payload, q4.payload) and np.array_equal(qa.extra["s_group"], q4.extra["s_group"])
+
+
+def test_w4a8_zero_group_keeps_row_precision():
+    """an all-zero 128-group must not coarsen the rest of its row (it did under the
+    round-1 progressive scales); per-group SPEC scales keep every group at its own absmax/7."""
+    r = tc.make_rng(41)
+    w = (r.standard_normal((4, 512)) * 0.02).astype(np.float32)
+    w[1, 128:256] = 0.0
     qa = qz.quantize_weight_w4a8(w, 128)
-    sg = qa.extra["sg"]
-    assert sg.min() >= 1 and sg.max() <= 15
-    w8 = qz.int8_weight_of(qa)
-    assert np.abs(w8).max() <= 120
-    assert np.allclose(w8.astype(np.float32) * qa.extra["s_ch"][:, None], qz.dequantize(qa), rtol=1e-6, atol=0)
+    assert qa.extra["s_group"][1, 1] == np.float32(1.0)                      # SPEC.md:117 zero slice
+    err = np.abs(qz.dequantize(qa) - w)
+    assert (err <= np.repeat(qa.extra["s_group"], 128, axis=1) / 2 * 1.0001).all()
+    assert np.abs(qa.payload[1, :128]).max() == 7                             # the row keeps full range
+
+
+def test_w4a8_promotion_order_and_splits():
+    """qlinear_a8 (W4A8) == the documented promotion: per split, ascending groups from 0, then
+    the split partials in order; splits=1 vs 2 differ only by f32 re-association."""
+    from oracle import qblock as oq
+    r = tc.make_rng(42)
+    M, N, K = 5, 7, 512
+    a = r.integers(-128, 128, (M, K)).astype(np.int8)
+    codes = r.integers(-8, 8, (N, K)).astype(np.int8)
+    s = r.uniform(1e-3, 1e-2, (N, K // 128)).astype(np.float32)
+    ql = oq.QLinear("w4a8", codes, s_group=s, group=128)
+    y1, acc = oq.qlinear_a8(a, ql, np.float32(0.5), splits=1)
+    assert np.array_equal(acc, tc.int_gemm(a, codes.T))
+    from fractions import Fraction
+
+    def round_f32(x: Fraction) -> np.float32:   # correctly rounded (ties to even), no double rounding
+        c = np.float32(float(x))
+        cands = [np.nextafter(c, np.float32(-np.inf)), c, np.nextafter(c, np.float32(np.inf))]
+        err = [abs(Fraction(float(v)) - x) for v in cands]
+        best = min(err)
+        tied = [v for v, e in zip(cands, err) if e == best]
+        return min(tied, key=lambda v: int(np.asarray(v).view(np.int32)) & 1)
+
+    for m in range(M):                       # exact rational fma, rounded to f32 once per group
+        for n in range(N):
+            p = np.float32(0)
+            for g in range(4):
+                acc = int(tc.int_gemm(a[m:m + 1, g * 128:(g + 1) * 128], codes[n:n + 1, g * 128:(g + 1) * 128].T)[0, 0])
+                p = round_f32(Fraction(float(s[n, g])) * acc + Fraction(float(p)))
+            assert y1[m, n] == np.float32(p * np.float32(0.5))
+    y2, _ = oq.qlinear_a8(a, ql, np.float32(0.5), splits=2)
+    assert np.allclose(y1, y2, rtol=1e-6, atol=1e-6 * np.abs(y1).max())
 
 
 # ------------------------------------------------------------------ hadamard (SPEC.md:181-253)
@@ -503,8 +545,8 @@ def test_acceptance13_determinism_and_12_sizes(tmp_path):
         assert np.array_equal(x.state_scale, y.state_scale)
     # size accounting direction: int4 payload is 1/8 of f32 bytes
     fl = sum(blk.in_proj.nbytes + blk.out_proj.nbytes for blk in a.blocks)
-    q4 = sum(blk.in_proj.codes.size // 2 + blk.in_proj.sg.size + 4 * blk.in_proj.s_ch.size +
-             blk.out_proj.codes.size // 2 + blk.out_proj.sg.size + 4 * blk.out_proj.s_ch.size for blk in q1.blocks)
+    q4 = sum(blk.in_proj.codes.size // 2 + 4 * blk.in_proj.s_group.size +
+             blk.out_proj.codes.size // 2 + 4 * blk.out_proj.s_group.size for blk in q1.blocks)
     assert q4 <= 0.3 * fl
 
 
