@@ -57,6 +57,34 @@ def peaks():
         return FALLBACK_HBM, FALLBACK_BF16, "fallback"
 
 
+_INT8_PEAK = None
+
+
+def int8_peak_tops(dev) -> float:
+    """Dense INT8 tensor peak measured here: torch._int_mm (cuBLASLt) on 8192^3, best of 10
+    (the driver's MEASURED_PEAKS.json has no INT8 figure)."""
+    global _INT8_PEAK
+    if _INT8_PEAK is None:
+        import torch
+        n = 8192
+        a = torch.randint(-128, 128, (n, n), dtype=torch.int8, device=dev)
+        b = torch.randint(-128, 128, (n, n), dtype=torch.int8, device=dev).t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        _INT8_PEAK = 2.0 * n ** 3 / best / 1e12
+        del a, b
+    return _INT8_PEAK
+
+
 class Clocks:
     """Samples nvidia-smi clocks/throttle reasons during the timed region."""
 
@@ -239,9 +267,10 @@ def run_reference_arm(args, wl, world, rank):
 
 
 # ------------------------------------------------------------------ GPU arm
-def run_prefill(args, wl, world, rank, local):
+def run_prefill(args, wl, world, rank, local, emit=True):
     """configs[1]: one step = prefill of batch x seq tokens through every layer (fresh state,
-    int8 final state written), last-token logits; tokens from pinned host memory for e2e."""
+    int8 final state written), last-token logits; tokens from pinned host memory for e2e.
+    Returns the line (rank 0); prints it when ``emit``."""
     import torch
     from paper_2503_22879_b200 import ops, synth
     from paper_2503_22879_b200.ssm_block import Dims
@@ -308,12 +337,18 @@ def run_prefill(args, wl, world, rank, local):
     ops_per = 2.0 * M * d.in_proj_out * d.d_model
     achieved = ops_per / (gemm_ms / 1e3) / 1e12
     hbm, bf16, pk_kind = peaks()
+    i8peak = int8_peak_tops(dev)
     # the step's largest kernel: the chunked int8 SSD scan (HBM-bound in principle: int8 codes
     # in, f32 y + int8 state out), timed live on the layer's own inputs (Mamba2); Mamba1's
     # largest kernel is the in_proj GEMM itself
+    launches_per_step = ops.LAUNCH_COUNTER[0]
+    ops.LAUNCH_COUNTER[0] = 0
+    step()
+    torch.cuda.synchronize()
+    launches_per_step, ops.LAUNCH_COUNTER[0] = ops.LAUNCH_COUNTER[0], launches_per_step
     if d.variant == "mamba1":
-        return _prefill_line(args, wl, world, rank, d, B, T, value, ms, e2e_ms, lm, clk, achieved, bf16, pk_kind,
-                             ops_per, gemm_ms)
+        return _prefill_line(args, wl, world, rank, d, B, T, value, ms, e2e_ms, lm, clk, achieved, i8peak, pk_kind,
+                             ops_per, gemm_ms, launches_per_step, emit)
     di, gn, nh = d.d_inner, d.n_state_groups * d.d_state, d.n_heads
     cv, zx = ws["conv"], ws["zx"]
     st_tmp = torch.empty((B, nh, d.head_dim, d.d_state), dtype=torch.int8, device=dev)
@@ -332,7 +367,6 @@ def run_prefill(args, wl, world, rank, local):
     ssd_ms = k0.elapsed_time(k1) / 5
     ssd_bytes = M * (di + 2 * gn + di + nh + 4 * di) + st_tmp.numel()
     ssd_gbs = ssd_bytes / (ssd_ms / 1e3) / 1e9
-    launches_per_step = 7 * len(lm.blocks) + 3   # per layer: norm, in_proj, conv (2), scan, gated norm, out_proj
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import multiprocessing
@@ -354,18 +388,22 @@ def run_prefill(args, wl, world, rank, local):
                              "traffic": ncu_traffic("ssd_chunk_kernel<128>"), "peak_kind": pk_kind,
                              "algorithmic_bytes_per_launch": ssd_bytes, "launch_ms": ssd_ms},
                 "roofline_gemm": {"bound": "tensor", "kernel": "gemm_tc_kernel (in_proj W8A8, tcgen05 kind::i8)",
-                                  "achieved": achieved, "peak": bf16 * 2, "unit": "TOP/s", "frac": achieved / (bf16 * 2),
-                                  "traffic": None, "peak_kind": pk_kind + " (int8 = 2 x measured bf16 dense)",
+                                  "achieved": achieved, "peak": i8peak, "unit": "TOP/s", "frac": achieved / i8peak,
+                                  "traffic": None,
+                                  "peak_kind": "measured here: torch._int_mm int8 8192^3 dense (cuBLASLt), best of 10",
                                   "algorithmic_ops_per_launch": ops_per, "launch_ms": gemm_ms},
                 "cpu_baseline": cpu,
                 "e2e": {"value": world * B * T / (e2e_ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": B * T * 4,
                         "d2h_bytes_per_step": B * lm.vocab * 4},
                 "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
-        print(json.dumps(line), flush=True)
+        if emit:
+            print(json.dumps(line), flush=True)
+        return line
+    return None
 
 
-def _prefill_line(args, wl, world, rank, d, B, T, value, ms, e2e_ms, lm, clk, achieved, bf16, pk_kind, ops_per,
-                  gemm_ms):
+def _prefill_line(args, wl, world, rank, d, B, T, value, ms, e2e_ms, lm, clk, achieved, i8peak, pk_kind, ops_per,
+                  gemm_ms, launches_per_step, emit=True):
     """Mamba1 prefill line: the in_proj W8A8 GEMM is the dominant kernel."""
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -383,14 +421,18 @@ def _prefill_line(args, wl, world, rank, d, B, T, value, ms, e2e_ms, lm, clk, ac
                            "global_batch": B * world, "seq_len": T, "layers": wl["layers"],
                            "parallelism": f"dp{world} (batch-shard replicas, no collective)"},
                 "roofline": {"bound": "tensor", "kernel": "gemm_tc_kernel (in_proj W8A8, tcgen05 kind::i8)",
-                             "achieved": achieved, "peak": bf16 * 2, "unit": "TOP/s", "frac": achieved / (bf16 * 2),
-                             "traffic": None, "peak_kind": pk_kind + " (int8 = 2 x measured bf16 dense)",
+                             "achieved": achieved, "peak": i8peak, "unit": "TOP/s", "frac": achieved / i8peak,
+                             "traffic": None,
+                             "peak_kind": "measured here: torch._int_mm int8 8192^3 dense (cuBLASLt), best of 10",
                              "algorithmic_ops_per_launch": ops_per, "launch_ms": gemm_ms},
                 "cpu_baseline": cpu,
                 "e2e": {"value": world * B * T / (e2e_ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": B * T * 4,
                         "d2h_bytes_per_step": B * lm.vocab * 4},
-                "gpu_launches": None, "clocks": clk.summary()}
-        print(json.dumps(line), flush=True)
+                "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
+        if emit:
+            print(json.dumps(line), flush=True)
+        return line
+    return None
 
 
 def run_decode(args, wl, world, rank, local):
@@ -402,7 +444,14 @@ def run_decode(args, wl, world, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     d = Dims(*wl["dims"])
-    B = wl["batch"]
+    from paper_2503_22879_b200 import dist as pdist
+    if args.global_batch:   # strong scaling: a fixed global batch sharded over the ranks
+        lo, hi = pdist.shard_range(args.global_batch, world, rank)
+        B = hi - lo
+        global_batch, scaling = args.global_batch, "strong"
+    else:                   # weak scaling: wl["batch"] sequences per GPU
+        B = wl["batch"]
+        global_batch, scaling = B * world, "weak"
     lm = synth.synthetic_lm(d, wl["layers"], wl["profile"], wl["vocab"], dev, seed=rank)
     states = lm.new_states(B)
     g = torch.Generator(device=dev)
@@ -414,7 +463,6 @@ def run_decode(args, wl, world, rank, local):
                                              dtype=torch.int8))
         else:
             s.h.normal_(0, 0.1, generator=g)
-    ops.LAUNCH_COUNTER[0] = 0
     graph, tok, logits, ws = lm.capture_decode(B, states)
     launches_per_step = ops.LAUNCH_COUNTER[1]
     tok.copy_(torch.randint(0, wl["vocab"], (B,), generator=g, device=dev, dtype=torch.int32))
@@ -437,7 +485,7 @@ def run_decode(args, wl, world, rank, local):
     barrier(world)
     ms = e0.elapsed_time(e1) / args.steps
     ms = max_over_ranks(ms, world)
-    value = world * B / (ms / 1e3)
+    value = global_batch / (ms / 1e3)
 
     # e2e: host tokens in (pinned H2D), step, host tokens out (D2H) every step
     pin_in = torch.randint(0, wl["vocab"], (B,), dtype=torch.int32).pin_memory()
@@ -457,9 +505,9 @@ def run_decode(args, wl, world, rank, local):
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
 
-    # dominant kernel: the int8 SSM state update (K9, state_ring_kernel) of the decode step,
-    # timed live with CUDA events on the launch stream, cycling through all layers' states
-    # (67 MB each at b=64, so every launch streams from HBM, not L2)
+    # dominant kernel class: the int8 SSM half of the decode step (K5d conv update, K9 state update,
+    # K6 gated norm + FWHT + quant), timed live with CUDA events on the launch stream, cycling
+    # through all layers' states (67 MB each at b=64, so every launch streams from HBM, not L2)
     blk = lm.blocks[0]
     di, gn = d.d_inner, d.n_state_groups * d.d_state
     reps = 2 * len(lm.blocks)
@@ -472,18 +520,18 @@ def run_decode(args, wl, world, rank, local):
             b_.in_proj.a8(ws["u"][:B], ops.EPI_QUANT, ws["zx"][:B], b_.in_out_scale)
         dom_bytes = d.in_proj_out * d.d_model + B * (d.d_model + d.in_proj_out)
     elif blk.a8 and getattr(blk, "fused_decode", False):
-        dom_name = "mamba2_decode_step_int8 (prep + state_ring_kernel + norm_had8192, decode)"
+        dom_name = "mamba2_decode_step_int8 (prep_kernel + state_ring_kernel + norm_had8192_kernel, decode)"
 
         def dom(i):
             b_ = lm.blocks[i % len(lm.blocks)]
             s_ = states[i % len(states)]
             ops.mamba2_decode_step_int8(b_.decode_params, B, ws["zx"], s_.conv_cache, s_.h, ws["yq"], ws["y"],
                                         ws["dws"])
-        tiles = B * d.n_heads
-        dom_bytes = (2 * tiles * d.head_dim * d.d_state          # int8 state read + write
-                     + B * di * 4                                # y (f32) write
-                     + tiles * (4 * d.head_dim + 4) * 4          # per-row scan operands
-                     + tiles * 2 * d.d_state * 4)                # B̂ | Ĉ of the head's group
+        # strictly algorithmic bytes (no workspace): int8 state read + write, int8 conv cache read +
+        # write, the in_proj codes read (z|x|B|C|dt), the int8 out_proj input written
+        dom_bytes = (2 * B * d.n_heads * d.head_dim * d.d_state
+                     + 2 * B * (d.conv_kernel - 1) * d.conv_dim
+                     + B * d.in_proj_out + B * di)
     else:
         # W4A16: the in_proj GEMV streams the most bytes of the step (61% of the launch list)
         dom_name = "gemv_w4a16_q_kernel (in_proj W4A16, decode weight stream)"
@@ -517,12 +565,23 @@ def run_decode(args, wl, world, rank, local):
                    "kind": "port",
                    "sample": f"2 full-width layers of one b={B} decode step, x{wl['layers']} layers (extrapolated); "
                              "numpy oracle with exact-int f64 BLAS on all host threads"}
+    prefill = None
+    if args.workload == "decode8b" and not args.no_prefill:
+        # configs[1] (the metric's prefill half) measured in the same run on a Mamba2-2.7B W8A8 model
+        del graph, lm, states, ws, logits, tok
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        pl = run_prefill(args, WORKLOADS["prefill27b"], world, rank, local, emit=False)
+        if pl is not None:
+            prefill = {k: pl[k] for k in ("metric", "value", "unit", "ms_per_step", "config", "roofline",
+                                          "roofline_gemm", "e2e", "gpu_launches", "cpu_baseline", "clocks")}
     if rank == 0:
         line = {"metric": "decode tok/s", "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "int8" if blk.a8 else "f32", "data": "synthetic",
                 "config": {"workload": args.workload, "desc": wl["desc"], "model": wl.get("model", "Mamba2-8B-shaped"),
-                           "global_batch": B * world, "seq_len": 1, "layers": wl["layers"], "vocab": wl["vocab"],
+                           "global_batch": global_batch, "batch_per_gpu": B, "seq_len": 1, "layers": wl["layers"],
+                           "vocab": wl["vocab"],
                            "parallelism": f"dp{world} (batch-shard replicas, no collective)",
                            "l2": "inputs larger than L2 (weights+state stream every step), no flush",
                            "step_bytes": step_bytes,
@@ -532,10 +591,10 @@ def run_decode(args, wl, world, rank, local):
                              "peak_kind": pk_kind, "algorithmic_bytes_per_launch": dom_bytes,
                              "launch_ms": dom_ms},
                 "cpu_baseline": res,
-                "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": B * 4,
+                "e2e": {"value": global_batch / (e2e_ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": B * 4,
                         "d2h_bytes_per_step": B * 4},
                 "gpu_launches": launches_per_step * args.steps,
-                "clocks": clk.summary()}
+                "clocks": clk.summary(), "prefill": prefill}
         print(json.dumps(line), flush=True)
 
 
@@ -547,6 +606,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="decode8b", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="decode8b: skip the configs[1] prefill sub-record")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="decode: shard this many sequences over the ranks (strong scaling); default 64 per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -17,10 +17,9 @@
 //   warps 4-7  converters: nibble v -> int8 16*v with one AND (high nibble) / SHF+AND (low),
 //              stored straight into a TMEM A stage (kind::i8 A-from-TMEM).  The x16 is exact
 //              (|16*v| <= 128) and is undone by s_a/16 in the epilogue (a power of two).
-//   warps 8-15 promotion + epilogue.  Every accumulator buffer is pre-set to 0x4B400000 and the
-//              MMAs accumulate onto it, so the read-back word is the f32 1.5*2^23 + acc exactly
-//              (|acc| <= 2^21): one FADD recovers f32(acc) without an I2F; the warp re-arms the
-//              buffer with one tcgen05.st before releasing it to the MMA issuer.
+//   warps 8-15 promotion + epilogue: tcgen05.ld of the group's int32 tile, then f32(acc) without
+//              an I2F: acc + 0x4B400000 is the bit pattern of the f32 1.5*2^23 + acc (|acc| <= 2^21),
+//              so one IADD and one FADD2 per pair recover it exactly; p = fma(s_w, f32(acc), p).
 // No weight byte is read twice and no scale is rounded: the kernel streams 0.5 B per weight
 // plus 4 B per 128 weights.
 //
@@ -45,10 +44,19 @@ constexpr int BN = 128;                 // weight rows per tile (MMA M)
 constexpr int BK = 128;                 // K per group / k-block
 constexpr int THREADS = 512;
 constexpr int TILE_BYTES = BN * BK / 2; // 8 KB packed weights per (n-tile, k-block)
-constexpr int RAW = 8;                  // packed-weight ring slots
-constexpr int AST = 4;                  // activation stages
-constexpr int TST = 8;                  // TMEM A stages (32 columns each)
-constexpr int NACC = 4;                 // accumulator buffers (NTOK columns each)
+#ifndef SQ_W4_RAW
+#define SQ_W4_RAW 8
+#endif
+constexpr int RAW = SQ_W4_RAW;          // packed-weight ring slots
+// The pipeline advances in steps of two groups (one barrier wait / arrive / commit per step and
+// role instead of per group: the MMA thread's barrier waits and commits, ~100 cycles each, set the
+// group rate otherwise).  Rings, each released by one tcgen05.commit per step: activation stages
+// (AST, 2 K-blocks each), TMEM A stages (TST, 2 x 32 columns each) and accumulator buffers (NACC,
+// 2 x NTOK columns each).
+constexpr int GS = 2;                   // groups per step
+constexpr int AST = 4;                  // activation stages (steps)
+constexpr int TST = 4;                  // TMEM A stages (steps)
+constexpr int NACC = 2;                 // accumulator buffers (steps)
 constexpr uint32_t MAGIC = 0x4B400000u; // bit pattern of 1.5 * 2^23
 
 template <int NTOK>
@@ -56,14 +64,14 @@ struct Cfg {
   static constexpr int ACT_BYTES = NTOK * BK;
   static constexpr int OFF_RAW = 0;
   static constexpr int OFF_ACT = RAW * TILE_BYTES;
-  static constexpr int OFF_BAR = OFF_ACT + AST * ACT_BYTES;
+  static constexpr int OFF_BAR = OFF_ACT + AST * GS * ACT_BYTES;
   static constexpr int NBAR = 2 * RAW + 2 * AST + 2 * TST + 2 * NACC + 4;
   static constexpr int OFF_SCL = (OFF_BAR + NBAR * 8 + 16 + 127) & ~127;   // 2 unit slabs of group scales
   // dynamic smem = SMEM0 + 2 * nkb * 512 (each unit's [nkb][128] f32 scales, one bulk copy)
   static constexpr int SMEM0 = 1024 + OFF_SCL;
   static constexpr int ACC_COL = 0;
-  static constexpr int A_COL = NACC * NTOK;
-  static constexpr int COLS_USED = A_COL + TST * 32;
+  static constexpr int A_COL = NACC * GS * NTOK;
+  static constexpr int COLS_USED = A_COL + TST * GS * 32;
   static constexpr int TMEM_COLS = COLS_USED <= 256 ? 256 : 512;
   static constexpr int HALF = NTOK / 2;   // token columns per promotion warp
   static_assert(NTOK * BN * 4 <= OFF_ACT, "split-K partial tile must fit the weight ring");
@@ -82,6 +90,15 @@ struct Args {
   int n_tiles;
 };
 
+#ifdef SQ_W4_PROBE_TIMELINE
+// profiling builds only: global-timer stamps of CTA 0's pipeline events (scripts/probe_w4.py)
+__device__ unsigned long long g_tl[8][80];
+#define TL(row, idx) \
+  if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (idx) < 80) g_tl[row][idx] = gtimer();
+#else
+#define TL(row, idx)
+#endif
+
 __device__ __forceinline__ void to_s8x16(uint32_t w, uint32_t& lo, uint32_t& hi) {
   // byte j of w = element j (low nibble) | element j+4 (high nibble)  (sq_repack_w4 order)
   hi = w & 0xF0F0F0F0u;          // 16 * v[j+4] as int8
@@ -97,15 +114,6 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t addr, uint32_t (&v)[NC]) {
   } else {
     tmem_ld_x32(addr, v);
   }
-}
-
-template <int NC>
-__device__ __forceinline__ void tmem_arm(uint32_t addr) {   // every column = MAGIC
-  uint32_t c[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) c[i] = MAGIC;
-#pragma unroll
-  for (int i = 0; i < NC; i += 8) tmem_st_x8(addr + i, c);
 }
 
 __device__ __forceinline__ void store_out(const Args& a, int m, int n, float y, float cs) {
@@ -150,12 +158,22 @@ __global__ void __launch_bounds__(THREADS, 1)
   auto unit_n = [&](int u) { return u % args.n_tiles; };
   auto unit_m = [&](int u) { return u / args.n_tiles; };
 
+  if (threadIdx.x == 0) TL(0, 0);
   pdl_trigger();
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < RAW; ++i) { mbar_init(&rfull[i], 1); mbar_init(&rempty[i], 4); }
-    for (int i = 0; i < AST; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 1); }
-    for (int i = 0; i < TST; ++i) { mbar_init(&tfull[i], 4); mbar_init(&tempty[i], 1); }
-    for (int i = 0; i < NACC; ++i) { mbar_init(&cfull[i], 1); mbar_init(&cempty[i], 8); }
+    for (int i = 0; i < AST; ++i) {
+      mbar_init(&afull[i], 1);
+      mbar_init(&aempty[i], 1);
+    }
+    for (int i = 0; i < TST; ++i) {
+      mbar_init(&tfull[i], 4);
+      mbar_init(&tempty[i], 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(&cfull[i], 1);
+      mbar_init(&cempty[i], 8);
+    }
     for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 8); }
     fence_barrier_init();
     tma_prefetch(&tm_act);
@@ -165,28 +183,23 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  if (warp >= 8) {   // arm both accumulator buffers (this warp's lane quadrant and column half)
-    const int q = warp & 3, h = (warp - 8) >> 2;
-#pragma unroll
-    for (int c = 0; c < NACC; ++c) tmem_arm<C::HALF>(tmem + ((uint32_t)(q * 32) << 16) + C::ACC_COL + c * NTOK + h * C::HALF);
-    tmem_wait_st();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
 
+  // step q covers groups 2q, 2q+1 of its unit (the last step of an odd count has one)
+  const int nst = (nkb + GS - 1) / GS;
   if (warp == 0) {
     // ------------------------------------------------ activation K-blocks (TMA)
     if (lane == 0) {
       pdl_wait();   // activations are written by the previous grid
-      int j = 0;
+      int q = 0;
       for (int u = u_first; u < args.units; u += u_step) {
         const int m_tile = unit_m(u);
-        for (int i = 0; i < nkb; ++i, ++j) {
-          const int s = j % AST;
-          mbar_wait_lazy(&aempty[s], ((j / AST) & 1) ^ 1);
-          mbar_arrive_expect_tx(&afull[s], C::ACT_BYTES);
-          tma_load_2d(act + s * C::ACT_BYTES, &tm_act, &afull[s], (kb0 + i) * BK, m_tile * NTOK);
+        for (int k = 0; k < nst; ++k, ++q) {
+          const int s = q % AST, ng = min(GS, nkb - k * GS);
+          mbar_wait_lazy(&aempty[s], ((q / AST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&afull[s], ng * C::ACT_BYTES);
+          for (int g = 0; g < ng; ++g)
+            tma_load_2d(act + (s * GS + g) * C::ACT_BYTES, &tm_act, &afull[s], (kb0 + k * GS + g) * BK,
+                        m_tile * NTOK);
         }
       }
     }
@@ -194,21 +207,30 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_i8(BN, NTOK);   // s8 x s8 -> s32
-      int j = 0;
+      int q = 0;
       for (int u = u_first; u < args.units; u += u_step) {
-        for (int i = 0; i < nkb; ++i, ++j) {
-          const int s = j % AST, t = j % TST, c = j % NACC;
-          mbar_wait(&afull[s], (j / AST) & 1);
-          mbar_wait(&tfull[t], (j / TST) & 1);
-          mbar_wait(&cempty[c], ((j / NACC) & 1) ^ 1);
+        for (int k = 0; k < nst; ++k, ++q) {
+          const int s = q % AST, t = q % TST, c = q % NACC, ng = min(GS, nkb - k * GS);
+          TL(6, q);
+          mbar_wait(&afull[s], (q / AST) & 1);
+          TL(7, q);
+          mbar_wait(&tfull[t], (q / TST) & 1);
+          TL(2, q);
+          mbar_wait(&cempty[c], ((q / NACC) & 1) ^ 1);
+          TL(3, q);
           tc_fence_after();
-          const uint64_t bdesc = desc_sw128(act + s * C::ACT_BYTES);
+          for (int g = 0; g < ng; ++g) {
+            const uint64_t bdesc = desc_sw128(act + (s * GS + g) * C::ACT_BYTES);
 #pragma unroll
-          for (int ks = 0; ks < BK / 32; ++ks)
-            mma_i8_ts(tmem + C::ACC_COL + c * NTOK, tmem + C::A_COL + t * 32 + ks * 8, bdesc + 2 * ks, idesc, 1u);
+            for (int ks = 0; ks < BK / 32; ++ks)
+              mma_i8_ts(tmem + C::ACC_COL + (c * GS + g) * NTOK, tmem + C::A_COL + (t * GS + g) * 32 + ks * 8,
+                        bdesc + 2 * ks, idesc, ks > 0 ? 1u : 0u);   // each group starts its own accumulator
+          }
+          TL(5, q);
           mma_commit(&aempty[s]);
           mma_commit(&tempty[t]);
           mma_commit(&cfull[c]);
+          TL(1, q);
         }
       }
     }
@@ -232,44 +254,58 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp >= 4 && warp < 8) {
-    // ------------------------------------------------ converters: packed nibbles -> TMEM A stage
-    const int q = warp & 3;
-    const int row = q * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + C::A_COL;
-    int j = 0;
+    // ------------------------------------------------ converters: packed nibbles -> TMEM A stages
+    const int qd = warp & 3;
+    const int row = qd * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(qd * 32) << 16) + C::A_COL;
+    int j = 0, q = 0;
     for (int u = u_first; u < args.units; u += u_step) {
-      for (int i = 0; i < nkb; ++i, ++j) {
-        const int r = j % RAW, t = j % TST;
-        mbar_wait(&rfull[r], (j / RAW) & 1);
-        uint4 p[4];
+      for (int k = 0; k < nst; ++k, ++q) {
+        const int t = q % TST, ng = min(GS, nkb - k * GS);
+        uint32_t wv[GS][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) p[c] = *reinterpret_cast<const uint4*>(raw + r * TILE_BYTES + c * 2048 + row * 16);
-        fence_proxy_async_smem();   // generic reads of the slot precede the bulk copy that refills it
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&rempty[r]);
-        uint32_t wv[32];
+        for (int g = 0; g < GS; ++g) {
+          if (g < ng) {
+            const int r = (j + g) % RAW;
+            mbar_wait(&rfull[r], ((j + g) / RAW) & 1);
+
+            uint4 p[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          to_s8x16(p[c].x, wv[c * 8 + 0], wv[c * 8 + 1]);
-          to_s8x16(p[c].y, wv[c * 8 + 2], wv[c * 8 + 3]);
-          to_s8x16(p[c].z, wv[c * 8 + 4], wv[c * 8 + 5]);
-          to_s8x16(p[c].w, wv[c * 8 + 6], wv[c * 8 + 7]);
+            for (int c = 0; c < 4; ++c)
+              p[c] = *reinterpret_cast<const uint4*>(raw + r * TILE_BYTES + c * 2048 + row * 16);
+            fence_proxy_async_smem();   // generic reads of the slot precede the bulk copy that refills it
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rempty[r]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              to_s8x16(p[c].x, wv[g][c * 8 + 0], wv[g][c * 8 + 1]);
+              to_s8x16(p[c].y, wv[g][c * 8 + 2], wv[g][c * 8 + 3]);
+              to_s8x16(p[c].z, wv[g][c * 8 + 4], wv[g][c * 8 + 5]);
+              to_s8x16(p[c].w, wv[g][c * 8 + 6], wv[g][c * 8 + 7]);
+            }
+          }
         }
-        mbar_wait(&tempty[t], ((j / TST) & 1) ^ 1);
+        j += ng;
+        mbar_wait(&tempty[t], ((q / TST) & 1) ^ 1);
         tc_fence_after();
-        tmem_st_x32(lane_base + t * 32, wv);
+#ifndef SQ_W4_PROBE_NOCONV   // profiling builds only: the A stage is left as is
+#pragma unroll
+        for (int g = 0; g < GS; ++g)
+          if (g < ng) tmem_st_x32(lane_base + (t * GS + g) * 32, wv[g]);
         tmem_wait_st();
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tfull[t]);
+        if (warp == 4 && lane == 0) TL(4, q);
       }
     }
   } else if (warp >= 8) {
     // ------------------------------------------------ promotion + epilogue
-    const int q = warp & 3, h = (warp - 8) >> 2;
-    const int row = q * 32 + lane;
-    const uint32_t acc_base = tmem + ((uint32_t)(q * 32) << 16) + C::ACC_COL + h * C::HALF;
-    int j = 0, ui = 0;
+    const int qd = warp & 3, h = (warp - 8) >> 2;
+    const int row = qd * 32 + lane;
+    const uint32_t acc_base = tmem + ((uint32_t)(qd * 32) << 16) + C::ACC_COL + h * C::HALF;
+    int q = 0, ui = 0;
     bool waited = false;
     for (int u = u_first; u < args.units; u += u_step, ++ui) {
       const int n_tile = unit_n(u), m_tile = unit_m(u);
@@ -280,26 +316,41 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int e = 0; e < C::HALF; ++e) p[e] = 0.f;
       mbar_wait(&sfull[sb], (ui >> 1) & 1);
-      for (int i = 0; i < nkb; ++i, ++j) {
-        const int c = j % NACC;
-        const float s0 = ssl[i * BN];
-        mbar_wait(&cfull[c], (j / NACC) & 1);
+      for (int k = 0; k < nst; ++k, ++q) {
+        const int c = q % NACC, ng = min(GS, nkb - k * GS);
+        mbar_wait(&cfull[c], (q / NACC) & 1);
+
         tc_fence_after();
-        uint32_t v[C::HALF];
-        tmem_ld_cols<C::HALF>(acc_base + c * NTOK, v);
-        tmem_wait_ld();
-        tmem_arm<C::HALF>(acc_base + c * NTOK);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&cempty[c]);
-        const float2 sv = make_float2(s0, s0), nm = make_float2(-12582912.0f, -12582912.0f);
+        const float2 nm = make_float2(-12582912.0f, -12582912.0f);
 #pragma unroll
-        for (int e = 0; e < C::HALF; e += 2) {
-          const float2 f = __fadd2_rn(make_float2(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), nm);
-          const float2 r2 = __ffma2_rn(sv, f, make_float2(p[e], p[e + 1]));
-          p[e] = r2.x;
-          p[e + 1] = r2.y;
+        for (int g = 0; g < GS; ++g) {
+          if (g < ng) {
+            uint32_t v[C::HALF];
+#ifndef SQ_W4_PROBE_NOPROMO  // profiling builds only: accumulators not read
+            tmem_ld_cols<C::HALF>(acc_base + (c * GS + g) * NTOK, v);
+            tmem_wait_ld();
+#else
+#pragma unroll
+            for (int e = 0; e < C::HALF; ++e) v[e] = 0u;
+#endif
+            if (g == ng - 1) {   // every accumulator of the step is in registers: release the buffers
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&cempty[c]);
+            }
+            const float s0 = ssl[(k * GS + g) * BN];
+            const float2 sv = make_float2(s0, s0);
+#pragma unroll
+            for (int e = 0; e < C::HALF; e += 2) {
+              // f32(acc) without I2F: the int32 + 0x4B400000 bit pattern is the float 1.5·2^23 + acc
+              // (|acc| <= 2^21)
+              const float2 f = __fadd2_rn(
+                  make_float2(__uint_as_float(v[e] + MAGIC), __uint_as_float(v[e + 1] + MAGIC)), nm);
+              const float2 r2 = __ffma2_rn(sv, f, make_float2(p[e], p[e + 1]));
+              p[e] = r2.x;
+              p[e + 1] = r2.y;
+            }
+          }
         }
       }
       __syncwarp();
@@ -364,6 +415,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     cluster_sync();
   }
+  if (threadIdx.x == 0) TL(0, 1);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -512,5 +564,11 @@ int tile_scales(const float* s, int N, int G, float* dst, cudaStream_t st) {
   tile_scales_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, N, G, dst);
   return check_launch("sq_tile_group_scales");
 }
+
+#ifdef SQ_W4_PROBE_TIMELINE
+extern "C" int sq_probe_w4_timeline(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, w4pg::g_tl, sizeof(w4pg::g_tl)) == cudaSuccess ? 0 : -3;
+}
+#endif
 
 }  // namespace sq

@@ -24,8 +24,9 @@ def lib():
 LAUNCH_COUNTER = [0, 0]   # [kernel launches issued through this module, launches in last captured step]
 
 
-def _check(rc: int):
-    LAUNCH_COUNTER[0] += 1
+def _check(rc: int, launches: int = 1):
+    """Map a C-ABI status onto the errors hierarchy; ``launches`` = kernels the call issued."""
+    LAUNCH_COUNTER[0] += launches
     if rc != 0:
         raise status_error(rc, _lib.last_error())
 
@@ -97,7 +98,8 @@ def rmsnorm_quant(x, gamma, eps, s, out=None, gsum=None):
     _dev(out, torch.int8, "out", 2)
     gp, gl = _gs(gsum, M, D)
     _check(lib().sq_rmsnorm_quant(x.data_ptr(), _ld(x), gamma.data_ptr(), float(eps), float(s), M, D,
-                                  out.data_ptr(), _ld(out), gp, gl, _stream()))
+                                  out.data_ptr(), _ld(out), gp, gl, _stream()),
+           1 + (gsum is not None and D % 16 != 0))
     return out
 
 
@@ -233,7 +235,7 @@ def conv1d_int8(x, w, bias, s_in, s_out, B, T, cache, cache_in=False, out=None):
     out = torch.empty((B * T, C_), dtype=torch.int8, device=x.device) if out is None else out
     _check(lib().sq_conv1d_int8(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), s_in.data_ptr(),
                                 s_out.data_ptr(), B, T, C_, Kc, cache.data_ptr(), int(bool(cache_in)),
-                                out.data_ptr(), _ld(out), _stream()))
+                                out.data_ptr(), _ld(out), _stream()), 1 + (Kc > 1))
     return out
 
 
@@ -254,7 +256,7 @@ def conv1d_f32(x, w, bias, B, T, cache, cache_in=False, out=None):
     C_, Kc = w.shape
     out = torch.empty((B * T, C_), dtype=torch.float32, device=x.device) if out is None else out
     _check(lib().sq_conv1d_f32(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), B, T, C_, Kc, cache.data_ptr(),
-                               int(bool(cache_in)), out.data_ptr(), _ld(out), _stream()))
+                               int(bool(cache_in)), out.data_ptr(), _ld(out), _stream()), 1 + (Kc > 1))
     return out
 
 
@@ -302,7 +304,8 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     gp, gl = _gs(gsum, B, di)
     _check(lib().sq_mamba2_decode_step_int8(C.byref(p), B, zx.data_ptr(), _ld(zx), conv_cache.data_ptr(),
                                             state.data_ptr(), ws.data_ptr(), y.data_ptr(), _ld(y), yq.data_ptr(),
-                                            _ld(yq), gp, gl, _stream()))
+                                            _ld(yq), gp, gl, _stream()),
+           3 + (gsum is not None and not (di == 8192 and p.hadamard)))   # prep, state ring, norm (+ sums)
     return yq
 
 

@@ -14,13 +14,24 @@ SHAPES = [("in_proj 8B b64", 64, 18560, 4096), ("out_proj 8B b64", 64, 4096, 819
 
 
 def timeit(fn, reps=20):
+    """Device time per launch of `reps` back-to-back launches replayed from a CUDA graph (no host
+    launch overhead between them, like the decode step)."""
     for i in range(3):
         fn(i)
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for i in range(reps):
+                fn(i)
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for i in range(reps):
-        fn(i)
+    g.replay()
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps

@@ -239,7 +239,7 @@ def test_block_forward_quantized(cuda, profile, variant):
 
 
 @pytest.mark.parametrize("profile,variant", [("W8A8", "mamba2"), ("W4A8", "mamba2"), ("W4A16", "mamba2"),
-                                             ("W4A16", "mamba1")])
+                                             ("W8A8", "mamba1"), ("W4A8", "mamba1"), ("W4A16", "mamba1")])
 def test_decode_matches_oracle_steps(cuda, profile, variant):
     """Prefill 48 tokens then 16 single-token decode steps (cached state)."""
     from paper_2503_22879_b200.ssm_block import block_forward_quantized, DeviceBlock

@@ -6,6 +6,7 @@ within float tolerance, and fed the same statistics the whole quantize pipeline 
 identical quantized models.
 """
 import numpy as np
+from paper_2503_22879_b200.errors import CalibrationError
 import pytest
 import torch
 
@@ -127,6 +128,14 @@ def test_gen_toy_and_calibration(dims):
         for k in lo:
             a, b = lo[k].channel_max, lp[k].channel_max
             assert np.allclose(a, b, rtol=2e-4, atol=1e-6 * np.abs(a).max()), k
+    # SPEC.md:384 sites argument: only the requested taps are kept, with the same statistics
+    sub = calibrate.collect_stats(fp, toks, sites=["x", "h", "head_in"], device="cpu")
+    assert [set(s) for s in sub] == [{"x", "h"}] * len(fp.blocks) + [{"head_in"}]
+    for full, part in zip(sp, sub):
+        for k in part:
+            assert np.array_equal(full[k].channel_max, part[k].channel_max)
+    with pytest.raises(CalibrationError):
+        calibrate.collect_stats(fp, toks, sites=["nope"], device="cpu")
 
 
 @pytest.mark.parametrize("profile", ["W8A8", "W4A8", "W4A16"])
