@@ -379,7 +379,7 @@ def run_prefill(args, wl, world, rank, local, emit=True):
         line = {"metric": "prefill tok/s", "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-                "config": {"workload": args.workload, "desc": wl["desc"], "model": "Mamba2-2.7B-shaped",
+                "config": {"workload": wl.get("name", args.workload), "desc": wl["desc"], "model": "Mamba2-2.7B-shaped",
                            "global_batch": B * world, "seq_len": T, "layers": wl["layers"],
                            "parallelism": f"dp{world} (batch-shard replicas, no collective)",
                            "l2": "activations 16384 x 10576 int8 per layer exceed L2; no flush"},
@@ -571,7 +571,7 @@ def run_decode(args, wl, world, rank, local):
         del graph, lm, states, ws, logits, tok
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
-        pl = run_prefill(args, WORKLOADS["prefill27b"], world, rank, local, emit=False)
+        pl = run_prefill(args, dict(WORKLOADS["prefill27b"], name="prefill27b"), world, rank, local, emit=False)
         if pl is not None:
             prefill = {k: pl[k] for k in ("metric", "value", "unit", "ms_per_step", "config", "roofline",
                                           "roofline_gemm", "e2e", "gpu_launches", "cpu_baseline", "clocks")}

@@ -54,7 +54,10 @@ constexpr int RAW = SQ_W4_RAW;          // packed-weight ring slots
 // (AST, 2 K-blocks each), TMEM A stages (TST, 2 x 32 columns each) and accumulator buffers (NACC,
 // 2 x NTOK columns each).
 constexpr int GS = 2;                   // groups per step
-constexpr int AST = 4;                  // activation stages (steps)
+#ifndef SQ_W4_AST
+#define SQ_W4_AST 4
+#endif
+constexpr int AST = SQ_W4_AST;          // activation stages (steps)
 constexpr int TST = 4;                  // TMEM A stages (steps)
 constexpr int NACC = 2;                 // accumulator buffers (steps)
 constexpr uint32_t MAGIC = 0x4B400000u; // bit pattern of 1.5 * 2^23
@@ -204,8 +207,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------ MMA issuer (whole warp; one elected lane issues)
+    {
       constexpr uint32_t idesc = idesc_i8(BN, NTOK);   // s8 x s8 -> s32
       int q = 0;
       for (int u = u_first; u < args.units; u += u_step) {
@@ -215,22 +218,25 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(&afull[s], (q / AST) & 1);
           TL(7, q);
           mbar_wait(&tfull[t], (q / TST) & 1);
-          TL(2, q);
           mbar_wait(&cempty[c], ((q / NACC) & 1) ^ 1);
-          TL(3, q);
           tc_fence_after();
-          for (int g = 0; g < ng; ++g) {
-            const uint64_t bdesc = desc_sw128(act + (s * GS + g) * C::ACT_BYTES);
+          if (elect_one()) {
+            // the step's groups accumulate into independent TMEM buffers, K-steps interleaved
 #pragma unroll
             for (int ks = 0; ks < BK / 32; ++ks)
-              mma_i8_ts(tmem + C::ACC_COL + (c * GS + g) * NTOK, tmem + C::A_COL + (t * GS + g) * 32 + ks * 8,
-                        bdesc + 2 * ks, idesc, ks > 0 ? 1u : 0u);   // each group starts its own accumulator
+#pragma unroll
+              for (int g = 0; g < GS; ++g)
+                if (g < ng)
+                  mma_i8_ts(tmem + C::ACC_COL + (c * GS + g) * NTOK, tmem + C::A_COL + (t * GS + g) * 32 + ks * 8,
+                            desc_sw128(act + (s * GS + g) * C::ACT_BYTES) + 2 * ks, idesc,
+                            ks > 0 ? 1u : 0u);   // each group starts its own accumulator
+            TL(5, q);
+            mma_commit(&aempty[s]);
+            mma_commit(&tempty[t]);
+            mma_commit(&cfull[c]);
+            TL(1, q);
           }
-          TL(5, q);
-          mma_commit(&aempty[s]);
-          mma_commit(&tempty[t]);
-          mma_commit(&cfull[c]);
-          TL(1, q);
+          __syncwarp();
         }
       }
     }
@@ -263,29 +269,37 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int k = 0; k < nst; ++k, ++q) {
         const int t = q % TST, ng = min(GS, nkb - k * GS);
         uint32_t wv[GS][32];
+        uint4 p[GS][4];
+        // the step's tiles: every smem read issued before one proxy fence and the slot releases
 #pragma unroll
         for (int g = 0; g < GS; ++g) {
           if (g < ng) {
             const int r = (j + g) % RAW;
             mbar_wait(&rfull[r], ((j + g) / RAW) & 1);
-
-            uint4 p[4];
+            if (warp == 4 && lane == 0 && g == 0) TL(2, q);
 #pragma unroll
             for (int c = 0; c < 4; ++c)
-              p[c] = *reinterpret_cast<const uint4*>(raw + r * TILE_BYTES + c * 2048 + row * 16);
-            fence_proxy_async_smem();   // generic reads of the slot precede the bulk copy that refills it
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&rempty[r]);
+              p[g][c] = *reinterpret_cast<const uint4*>(raw + r * TILE_BYTES + c * 2048 + row * 16);
+          }
+        }
+        fence_proxy_async_smem();   // generic reads of the slots precede the bulk copies that refill them
+        __syncwarp();
+        if (lane == 0)
+          for (int g = 0; g < ng; ++g) mbar_arrive(&rempty[(j + g) % RAW]);
+#pragma unroll
+        for (int g = 0; g < GS; ++g) {
+          if (g < ng) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              to_s8x16(p[c].x, wv[g][c * 8 + 0], wv[g][c * 8 + 1]);
-              to_s8x16(p[c].y, wv[g][c * 8 + 2], wv[g][c * 8 + 3]);
-              to_s8x16(p[c].z, wv[g][c * 8 + 4], wv[g][c * 8 + 5]);
-              to_s8x16(p[c].w, wv[g][c * 8 + 6], wv[g][c * 8 + 7]);
+              to_s8x16(p[g][c].x, wv[g][c * 8 + 0], wv[g][c * 8 + 1]);
+              to_s8x16(p[g][c].y, wv[g][c * 8 + 2], wv[g][c * 8 + 3]);
+              to_s8x16(p[g][c].z, wv[g][c * 8 + 4], wv[g][c * 8 + 5]);
+              to_s8x16(p[g][c].w, wv[g][c * 8 + 6], wv[g][c * 8 + 7]);
             }
           }
         }
         j += ng;
+        if (warp == 4 && lane == 0) TL(3, q);
         mbar_wait(&tempty[t], ((q / TST) & 1) ^ 1);
         tc_fence_after();
 #ifndef SQ_W4_PROBE_NOCONV   // profiling builds only: the A stage is left as is

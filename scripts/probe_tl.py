@@ -27,7 +27,7 @@ for sname, M, N, K in [("in_proj", 64, 18560, 4096), ("out_proj", 64, 4096, 8192
     lib.sq_probe_w4_timeline(buf.ctypes.data_as(ctypes.c_void_p))
     t0 = buf[0, 0]
     rel = (buf.astype(np.int64) - np.int64(t0)) / 1e3
-    names = ["entry/exit", "mma committed", "mma got A", "mma got acc", "conv pub", "mma issued", "mma wait0",
+    names = ["entry/exit", "mma committed", "conv got w0", "conv converted", "conv pub", "mma issued", "mma wait0",
              "mma got act"]
     print(f"== {sname}: exit at {rel[0, 1]:.2f} us")
     G = (K // 128 if sname == "in_proj" else K // 128 // ops.gemm_w4a8_splits(M, N, K)) // 2   # steps
