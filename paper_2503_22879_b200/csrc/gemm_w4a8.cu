@@ -181,11 +181,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     fence_barrier_init();
     tma_prefetch(&tm_act);
   }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
+  __syncthreads();   // barriers ready: the weight stream starts now, before the TMEM allocation
+  uint32_t tmem = 0;
+  if (warp != 2) {   // (the stream warp never touches TMEM)
+    if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
+    tc_fence_before();
+    named_bar(1, THREADS - 32);
+    tc_fence_after();
+    tmem = *tmem_holder;
+  }
 
   // step q covers groups 2q, 2q+1 of its unit (the last step of an odd count has one)
   const int nst = (nkb + GS - 1) / GS;
