@@ -83,6 +83,9 @@ int sq_quantize_f32(const float* x, int64_t ldx, float s, int M, int D, int8_t* 
 /* h[m,:] = codes[tok[m],:] * row_scale[tok[m]] */
 int sq_embed_int8(const int8_t* codes, const float* row_scale, const int32_t* tok, int M, int D,
                   float* h, void* stream);
+/* 4-bit embedding: h[m,:] = v(tok[m],:) * row_scale[tok[m]], v from u4packed rows [V x D/2] */
+int sq_embed_u4(const uint8_t* packed, const float* row_scale, const int32_t* tok, int M, int D,
+                float* h, void* stream);
 /* tok[m] = argmax_n logits[m, n] (lowest index on ties) */
 int sq_argmax_f32(const float* logits, int64_t ld, int M, int N, int32_t* tok, void* stream);
 

@@ -226,7 +226,8 @@ def cmd_quantize(model: FloatModel, tokens, profiles, m=4, n=4, hadamard=True, r
     ec = quantize_codes(model.embedding, es[:, None], emb_bits)
     head = make_qlinear(model.head, "w4a8" if head_bits == 4 else "w8", _gemm_group(model.dims.d_model))
     s_head = cal.calibrate_site_scale(stats[-1]["head_in"])
-    return QuantModel(model.dims, list(profiles), ec, es, model.layer_norms, blocks, model.final_norm, head, s_head)
+    return QuantModel(model.dims, list(profiles), ec, es, model.layer_norms, blocks, model.final_norm, head, s_head,
+                      extra={"emb_bits": emb_bits})
 
 
 def quant_forward(qm: QuantModel, tokens, states=None, trace=None):

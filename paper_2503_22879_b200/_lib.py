@@ -47,6 +47,7 @@ _SIGS = {
     "sq_rmsnorm_f32": ([_vp, _i64, _vp, _flt, _int, _int, _vp, _i64, _vp], _int),
     "sq_quantize_f32": ([_vp, _i64, _flt, _int, _int, _vp, _i64, _vp], _int),
     "sq_embed_int8": ([_vp, _vp, _vp, _int, _int, _vp, _vp], _int),
+    "sq_embed_u4": ([_vp, _vp, _vp, _int, _int, _vp, _vp], _int),
     "sq_argmax_f32": ([_vp, _i64, _int, _int, _vp, _vp], _int),
     "sq_gemm_w8a8": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _vp, _vp], _int),
     "sq_gemm_w4a8": ([_vp, _i64, _vp, _vp, _int, _flt, _int, _int, _int, _int, _vp, _i64, _vp, _vp], _int),

@@ -14,7 +14,8 @@ import numpy as np
 
 from .errors import ArchiveError, ShapeError
 
-__all__ = ["pack_u4", "unpack_u4", "archive_write", "archive_read", "inspect"]
+__all__ = ["pack_u4", "unpack_u4", "archive_write", "archive_read", "inspect", "write_float_model",
+           "read_float_model", "write_quant_model", "read_quant_model"]
 
 
 def pack_u4(vals) -> np.ndarray:
@@ -156,9 +157,13 @@ def read_float_model(path: str):
 
 
 def write_quant_model(qm, path: str) -> None:
+    """Quantized model -> archive (SPEC.md:591 stage 11): u4packed payloads for 4-bit weights and
+    embeddings, f32 scale tables, per-block scalars and the profile as json-meta."""
+    emb_bits = int((getattr(qm, "extra", None) or {}).get("emb_bits", 8))
     t = {"meta": {"kind": "quantized", "dims": vars(qm.dims), "profiles": qm.profiles,
-                  "s_head": float(qm.s_head)},
-         "emb_codes": qm.emb_codes, "emb_scale": qm.emb_scale, "final_norm": qm.final_norm}
+                  "s_head": float(qm.s_head), "emb_bits": emb_bits, "n_blocks": len(qm.blocks)},
+         "emb_codes": ("u4packed", np.asarray(qm.emb_codes)) if emb_bits == 4 else np.asarray(qm.emb_codes, np.int8),
+         "emb_scale": np.asarray(qm.emb_scale, np.float32), "final_norm": np.asarray(qm.final_norm, np.float32)}
 
     def put_ql(prefix, ql):
         t[f"{prefix}.meta"] = {"kind": ql.kind, "group": int(ql.group)}
@@ -184,3 +189,43 @@ def write_quant_model(qm, path: str) -> None:
                                     "hadamard": bool(b.hadamard), "profile": b.profile,
                                     "head_group": None if b.head_group is None else np.asarray(b.head_group).tolist()}
     archive_write(t, path)
+
+
+def read_quant_model(path: str):
+    """Archive written by ``write_quant_model`` -> cli.QuantModel (QuantizedMambaLM loads it and
+    repacks the u4 payloads into the kernel layout once)."""
+    from .cli import QuantModel
+    from .ssm_block import Dims, QBlock, QLinear
+    a = archive_read(path)
+    meta = a.get("meta", {})
+    if meta.get("kind") != "quantized":
+        raise ArchiveError("not a quantized-model archive")
+    d = Dims(**meta["dims"])
+
+    def get_ql(prefix):
+        m = a.get(f"{prefix}.meta")
+        if m is None:
+            return None
+        codes = np.asarray(a[f"{prefix}.codes"], np.int8)
+        return QLinear(m["kind"], codes, s_ch=a.get(f"{prefix}.s_ch"), s_group=a.get(f"{prefix}.s_group"),
+                       group=int(m["group"]))
+
+    n_blocks = int(meta.get("n_blocks", len(meta["profiles"])))
+    blocks, lns = [], []
+    for i in range(n_blocks):
+        g = lambda f: a.get(f"blocks.{i}.{f}")   # noqa: E731
+        sc = g("scalars")
+        hg = sc.get("head_group")
+        qb = QBlock(d, sc["profile"], get_ql(f"blocks.{i}.in_proj"), get_ql(f"blocks.{i}.out_proj"),
+                    g("conv_weight"), g("conv_bias"), g("a_log"), g("d_param"), g("dt_bias"), g("norm_weight"),
+                    None if hg is None else np.asarray(hg, np.int32), get_ql(f"blocks.{i}.x_proj"),
+                    get_ql(f"blocks.{i}.dt_proj"), s_u=np.float32(sc["s_u"]), in_out_scale=g("in_out_scale"),
+                    conv_in_scale=g("conv_in_scale"), conv_out_scale=g("conv_out_scale"),
+                    state_scale=g("state_scale"), s_y=np.float32(sc["s_y"]), xproj_out_scale=g("xproj_out_scale"),
+                    s_dt=np.float32(sc["s_dt"]), hadamard=bool(sc["hadamard"]))
+        blocks.append(qb)
+        lns.append(g("layer_norm"))
+    return QuantModel(d, list(meta["profiles"]), np.asarray(a["emb_codes"], np.int8), a["emb_scale"], lns, blocks,
+                      a["final_norm"], get_ql("head"), np.float32(meta["s_head"]),
+                      extra={"emb_bits": int(meta.get("emb_bits", 8))})
+

@@ -194,10 +194,11 @@ def cmd_quantize(model: FloatModel, tokens, profiles, m=4, n=4, hadamard=True, r
               for l, b in enumerate(model.blocks)]
     emb = np.asarray(model.embedding, np.float32)
     es = np.array([compute_scale(emb[v], emb_bits) for v in range(emb.shape[0])], np.float32)
-    ec = np.clip(np.rint(emb / es[:, None]), -128, 127).astype(np.int8)
+    lo, hi = -(1 << (emb_bits - 1)), (1 << (emb_bits - 1)) - 1
+    ec = np.clip(np.rint(emb / es[:, None]), lo, hi).astype(np.int8)
     head = make_qlinear(model.head, "w4a8" if head_bits == 4 else "w8", _gemm_group(model.dims.d_model))
     return QuantModel(model.dims, list(profiles), ec, es, model.layer_norms, blocks, model.final_norm, head,
-                      cal.calibrate_site_scale(stats[-1]["head_in"]))
+                      cal.calibrate_site_scale(stats[-1]["head_in"]), extra={"emb_bits": emb_bits})
 
 
 # ------------------------------------------------------------------ console script

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_tile = blockIdx.x, split = blockIdx.y, m_tile = blockIdx.z;
-  const int nkb_total = args.K / TC_BK;
+  const int nkb_total = (args.K + TC_BK - 1) / TC_BK;   // a partial last K-block is zero-filled by TMA
   const int kb_begin = split * nkb_total / SPLITS;
   const int nkb = (split + 1) * nkb_total / SPLITS - kb_begin;
 
@@ -457,12 +457,14 @@ static int dispatch_ntok(int ntok, const int8_t* a, int64_t lda, const uint8_t* 
 // Returns SQ_ERR_ARG when the shape is not eligible (caller falls back to mma.sync).
 int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const float* alpha, int M, int N, int K, int epi,
                void* out, int64_t ldo, const float* col_scale, cudaStream_t st) {
-  if (K % TC_BK != 0 || lda % 16 != 0 || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(w) & 15))
+  // K need not be a multiple of 128 (e.g. Mamba1 dt_proj, K = dt_rank = 160): the TMA boxes past K
+  // are zero-filled for both operands, so the padded products add nothing; rows must be 16-B aligned
+  if (K % 16 != 0 || lda % 16 != 0 || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(w) & 15))
     return SQ_ERR_ARG;
   if (!get_encoder()) return SQ_ERR_ARG;
   const int ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
   const int tiles = ((N + TC_BN - 1) / TC_BN) * ((M + ntok - 1) / ntok);
-  const int nkb = K / TC_BK;
+  const int nkb = (K + TC_BK - 1) / TC_BK;
   int splits = 1;
   const int slots = ntok <= 32 ? 2 * 148 : 148;   // resident CTAs (see launch_tc BUDGET)
   while (splits < 8 && tiles * splits * 2 <= slots && nkb / (splits * 2) >= 4 && ntok % (splits * 2) == 0) splits *= 2;

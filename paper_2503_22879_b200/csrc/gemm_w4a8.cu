@@ -318,6 +318,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (warp == 4 && lane == 0) TL(4, q);
       }
     }
+    // split-K: the partial tile reuses the weight ring; order every converter read of it before
+    // the promotion warps' writes (compute-sanitizer racecheck: the mbarrier / tcgen05.commit
+    // chain between them is not a generic-proxy happens-before)
+    if (SPLITS > 1) named_bar(2, 384);
   } else if (warp >= 8) {
     // ------------------------------------------------ promotion + epilogue
     const int qd = warp & 3, h = (warp - 8) >> 2;
@@ -404,6 +408,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       } else {
+        named_bar(2, 384);   // converters are past their last read of the ring
         float* red = reinterpret_cast<float*>(raw);   // [NTOK][128]; the weight ring is idle now
 #pragma unroll
         for (int e = 0; e < C::HALF; ++e) red[(h * C::HALF + e) * BN + row] = p[e];

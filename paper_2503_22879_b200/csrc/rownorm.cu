@@ -452,6 +452,23 @@ __global__ void embed_kernel(const int8_t* __restrict__ codes, const float* __re
     h[(int64_t)m * D + i] = __fmul_rn((float)codes[(int64_t)t * D + i], s);
 }
 
+// 4-bit embedding rows (head-to-toe quantization): u4packed [V x D/2] (low
+// nibble = even index), h[m, d] = v(tok[m], d) * row_scale[tok[m]].
+__global__ void embed_u4_kernel(const uint8_t* __restrict__ packed, const float* __restrict__ rs,
+                                const int32_t* tok, int D, float* __restrict__ h) {
+  pdl_trigger();
+  pdl_wait();
+  const int m = blockIdx.x;
+  const int t = tok[m];
+  const float s = rs[t];
+  const uint8_t* row = packed + (int64_t)t * (D / 2);
+  for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
+    const uint32_t b = row[i];
+    const int lo = ((int)(b << 28)) >> 28, hi = ((int)(b << 24)) >> 28;
+    *reinterpret_cast<float2*>(h + (int64_t)m * D + 2 * i) = make_float2(__fmul_rn((float)lo, s), __fmul_rn((float)hi, s));
+  }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) argmax_kernel(const float* lg, int64_t ld, int N,
                                                     int32_t* __restrict__ tok) {
@@ -591,6 +608,15 @@ extern "C" int sq_embed_int8(const int8_t* codes, const float* row_scale, const 
   if (M == 0) return SQ_OK;
   launch_k(PDL_ROW, embed_kernel, dim3(M), dim3(256), 0, as_stream(stream), codes, row_scale, tok, D, h);
   return check_launch("sq_embed_int8");
+}
+
+extern "C" int sq_embed_u4(const uint8_t* packed, const float* row_scale, const int32_t* tok, int M, int D,
+                           float* h, void* stream) {
+  SQ_REQUIRE(M >= 0 && D > 0 && D % 2 == 0, SQ_ERR_SHAPE, "sq_embed_u4: D must be even");
+  SQ_REQUIRE((reinterpret_cast<uintptr_t>(h) & 7) == 0, SQ_ERR_LAYOUT, "sq_embed_u4: h must be 8-B aligned");
+  if (M == 0) return SQ_OK;
+  launch_k(PDL_ROW, embed_u4_kernel, dim3(M), dim3(256), 0, as_stream(stream), packed, row_scale, tok, D, h);
+  return check_launch("sq_embed_u4");
 }
 
 extern "C" int sq_argmax_f32(const float* logits, int64_t ld, int M, int N, int32_t* tok, void* stream) {

@@ -280,6 +280,125 @@ __global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, in
   for (int n = 0; n < N; ++n) st[n] = quant8(hs[n], sh);
 }
 
+// Mamba1 int8 selective scan, staged (K8): CTA = 32 channels x
+// 4 state quarters (thread = one channel's 4 of the 16 states), so d_inner 5120 runs on 160 CTAs
+// instead of 40 one-channel-per-thread CTAs.  Time is walked in chunks of M1_TC tokens whose
+// operands are staged into shared memory by all 128 threads (cp.async, double-buffered one chunk
+// ahead): the codes are turned once per (token, channel) into Δ = softplus(Δ̂ + dt_bias), Δ·x̂ and
+// SiLU(ẑ), and B̂ | Ĉ once per token, so the sequential recurrence reads only smem.  Per step a
+// thread updates its 4 states (h = Ȧ·h + (Δx̂)·B̂, unfused like the oracle) and the channel's
+// C·h is reduced over the 4 threads with two shuffles.  The final state is requantised once.
+constexpr int M1_TC = 32;
+constexpr int M1_CH = 32;
+struct M1Stage {
+  float dl[M1_TC][M1_CH];      // Δ
+  float dx[M1_TC][M1_CH];      // Δ·x̂
+  float xh[M1_TC][M1_CH];      // x̂ (the D·x skip)
+  float gz[M1_TC][M1_CH];      // SiLU(ẑ)
+  float bc[M1_TC][32];         // B̂[16] | Ĉ[16]
+};
+struct M1Raw {                 // int8 codes of one chunk (cp.async targets)
+  int8_t x[M1_TC][M1_CH], dt[M1_TC][M1_CH], z[M1_TC][M1_CH], bc[M1_TC][32];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int NW>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NW) : "memory"); }
+
+__global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_params p, int B, int T, const int8_t* x,
+                                                                 int64_t ldx, const int8_t* dt, int64_t lddt,
+                                                                 const int8_t* BC, int64_t ldbc, const int8_t* z,
+                                                                 int64_t ldz, int8_t* state, int state_in, float* y,
+                                                                 int64_t ldy) {
+  constexpr int N = 16;
+  __shared__ __align__(16) M1Raw raw[2];
+  __shared__ __align__(16) M1Stage stg;
+  const int tid = threadIdx.x;
+  const int cl = tid >> 2, qt = tid & 3;       // channel within the CTA, state quarter
+  const int c0 = blockIdx.x * M1_CH, c = c0 + cl;
+  const int b = blockIdx.y;
+  pdl_trigger();
+  float A[4], hs[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) A[i] = p.A[c * N + qt * 4 + i];
+  const float sh = p.s_h[c], Dc = p.D[c];
+  // staging role constants: thread -> (token row, 16-B piece) of the raw tiles
+  pdl_wait();   // inputs come from the previous grid
+  int8_t* st = state + ((int64_t)b * p.d_inner + c) * N + qt * 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) hs[i] = state_in ? __fmul_rn((float)st[i], sh) : 0.f;
+  const int nch = (T + M1_TC - 1) / M1_TC;
+  auto issue = [&](int ch) {   // M1_TC rows x (x 2 + dt 2 + z 2 + bc 2) 16-B pieces, 128 threads
+    M1Raw& r = raw[ch & 1];
+#pragma unroll
+    for (int k = 0; k < M1_TC * 8 / 128; ++k) {
+      const int piece = tid + k * 128;
+      const int row = piece >> 3, kind = (piece >> 1) & 3, half = piece & 1;
+      const int t = ch * M1_TC + row;
+      if (t < T) {
+        const int64_t tok = (int64_t)b * T + t;
+        const int8_t* src = kind == 0 ? x + tok * ldx + c0 : kind == 1 ? dt + tok * lddt + c0
+                          : kind == 2 ? z + tok * ldz + c0 : BC + tok * ldbc;
+        int8_t* dst = kind == 0 ? r.x[row] : kind == 1 ? r.dt[row] : kind == 2 ? r.z[row] : r.bc[row];
+        cp_async16(dst + half * 16, src + half * 16);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  for (int ch = 0; ch < nch; ++ch) {
+    const int tn = min(M1_TC, T - ch * M1_TC);
+    if (ch + 1 < nch) {
+      issue(ch + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();   // raw[ch & 1] landed; every thread is done with the previous stage
+    const M1Raw& r = raw[ch & 1];
+    // per (token, channel) operands: M1_TC x 32 items
+    for (int i = tid; i < tn * M1_CH; i += 128) {
+      const int row = i / M1_CH, cc = i % M1_CH, ch_g = c0 + cc;
+      const float delta = softplus_f(__fadd_rn(__fmul_rn((float)r.dt[row][cc], p.s_dt), p.dt_bias[ch_g]));
+      const float xv = __fmul_rn((float)r.x[row][cc], p.s_x[ch_g]);
+      stg.dl[row][cc] = delta;
+      stg.dx[row][cc] = __fmul_rn(delta, xv);
+      stg.xh[row][cc] = xv;
+      stg.gz[row][cc] = silu_f(__fmul_rn((float)r.z[row][cc], p.s_z));
+    }
+    for (int i = tid; i < tn * 32; i += 128) {
+      const int row = i >> 5, n = i & 31;
+      stg.bc[row][n] = __fmul_rn((float)r.bc[row][n], n < N ? p.s_B : p.s_C);
+    }
+    __syncthreads();
+    for (int tt = 0; tt < tn; ++tt) {
+      const float delta = stg.dl[tt][cl], dtx = stg.dx[tt][cl];
+      const float4 bv = *reinterpret_cast<const float4*>(&stg.bc[tt][qt * 4]);
+      const float4 cv = *reinterpret_cast<const float4*>(&stg.bc[tt][N + qt * 4]);
+      const float bb[4] = {bv.x, bv.y, bv.z, bv.w}, cc4[4] = {cv.x, cv.y, cv.z, cv.w};
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float dA = expf(__fmul_rn(delta, A[i]));
+        hs[i] = __fadd_rn(__fmul_rn(dA, hs[i]), __fmul_rn(dtx, bb[i]));
+        acc = fmaf(hs[i], cc4[i], acc);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (qt == 0) {
+        const float yv = __fadd_rn(acc, __fmul_rn(Dc, stg.xh[tt][cl]));
+        y[((int64_t)b * T + ch * M1_TC + tt) * ldy + c] = __fmul_rn(yv, stg.gz[tt][cl]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) st[i] = quant8(hs[i], sh);
+}
+
 // Mamba1 W4A16 (float) scan: the same recurrence on f32 operands and an f32 state
 // (oracle/ssm_block.py selective_scan, Mamba1 branch).  dt is the raw
 // dt_proj output; B|C come from the x_proj output row (C at +N).
@@ -626,6 +745,13 @@ extern "C" int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T, c
   SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_selective_scan_int8: bad args");
   SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan_int8: d_state must be 16 (got %d)", p->d_state);
   if (B == 0 || T == 0) return SQ_OK;
+  if (T > 1 && p->d_inner % M1_CH == 0 && ldx % 16 == 0 && lddt % 16 == 0 && ldz % 16 == 0 && ldbc % 16 == 0 &&
+      !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dt) | reinterpret_cast<uintptr_t>(z) |
+         reinterpret_cast<uintptr_t>(BC)) & 15)) {
+    launch_k(PDL_SMALL8, mamba1_scan_staged_kernel, dim3(p->d_inner / M1_CH, B), dim3(128), 0, as_stream(stream), *p,
+             B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz, state, state_in, y, ldy);
+    return check_launch("sq_selective_scan_int8");
+  }
   dim3 grid((p->d_inner + 127) / 128, B);
   launch_k(PDL_SMALL8, mamba1_scan_kernel<16>, grid, dim3(128), 0, as_stream(stream), *p, B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz, state,
                                                               state_in, y, ldy);

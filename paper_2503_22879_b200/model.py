@@ -2,7 +2,8 @@
 
 Model wrapper (LEDGER G8): pre-norm residual stack
     h = E[tok];  for l: h += block_l(rmsnorm(h, ln_l));  logits = head(rmsnorm(h, ln_f))
-Head-to-toe quantisation: embedding per-row int8, head W4A8 (or W8A8)
+Head-to-toe quantisation: embedding per-row int8 or 4-bit (u4packed rows,
+PAPER.md:315-316), head W4A8 (or W8A8)
 with a per-tensor 8-bit activation scale.  Every op is a kernel of
 libssmquant_sm100.so; the residual stream stays fp32 in HBM.
 
@@ -45,7 +46,14 @@ class QuantizedMambaLM:
                 return a.to(device=dev, dtype=dt)
             return torch.as_tensor(np.asarray(a)).to(device=dev, dtype=dt)
         f = lambda a: t(a, torch.float32)
-        self.emb_codes = t(hm.emb_codes, torch.int8)
+        extra = getattr(hm, "extra", None) or {}
+        self.emb_bits = int(extra.get("emb_bits", 8))
+        if self.emb_bits == 4:   # u4packed rows, half the bytes of the int8 table
+            from .ssm_block import pack_u4_host
+            codes = hm.emb_codes.cpu().numpy() if isinstance(hm.emb_codes, torch.Tensor) else np.asarray(hm.emb_codes)
+            self.emb_codes = torch.as_tensor(pack_u4_host(codes), device=dev)
+        else:
+            self.emb_codes = t(hm.emb_codes, torch.int8)
         self.emb_scale = f(hm.emb_scale)
         self.layer_norms = [f(w) for w in hm.layer_norms]
         self.blocks = [b if isinstance(b, DeviceBlock) else DeviceBlock(b, dev) for b in hm.blocks]
@@ -90,7 +98,10 @@ class QuantizedMambaLM:
     def _run(self, tok, B, T, states, state_in, ws, all_logits):
         """tok int32 [B*T] (b-major) → logits; every launch on the current stream."""
         h = ws["h"]
-        ops.embed_int8(self.emb_codes, self.emb_scale, tok, h)
+        if self.emb_bits == 4:
+            ops.embed_u4(self.emb_codes, self.emb_scale, tok, self.dims.d_model, h)
+        else:
+            ops.embed_int8(self.emb_codes, self.emb_scale, tok, h)
         for l, blk in enumerate(self.blocks):
             st = states[l]
             if blk.a8:

@@ -132,6 +132,19 @@ def embed_int8(codes, row_scale, tok, out=None):
     return out
 
 
+def embed_u4(packed, row_scale, tok, D, out=None):
+    """4-bit embedding rows: ``packed`` uint8 u4packed [V x D/2]."""
+    _dev(packed, torch.uint8, "packed", 2)
+    _dev(tok, torch.int32, "tok", 1)
+    if packed.shape[1] * 2 != D:
+        raise ShapeError(f"packed rows must hold {D} nibbles")
+    M = tok.shape[0]
+    out = torch.empty((M, D), dtype=torch.float32, device=packed.device) if out is None else out
+    _check(lib().sq_embed_u4(packed.data_ptr(), row_scale.data_ptr(), tok.data_ptr(), M, D, out.data_ptr(),
+                             _stream()))
+    return out
+
+
 def argmax(logits, out=None):
     _dev(logits, torch.float32, "logits", 2)
     M, N = logits.shape

@@ -110,3 +110,37 @@ def test_product_quantize_pipeline_on_gpu(cuda):
     lg, _ = lm.prefill(torch.as_tensor(toks[:1, :32], device=cuda), all_logits=True)
     rel = np.abs(lg.cpu().numpy() - ref).max() / np.abs(ref).max()
     assert rel < 1e-2, rel
+
+
+def test_quant_archive_loads_into_gpu_model(cuda, tmp_path):
+    """A quantized artifact (ModelArchive) read back into QuantizedMambaLM gives
+    the same logits as the in-memory quantized model (u4 payloads repacked once on load)."""
+    from paper_2503_22879_b200 import archive, cli
+    from paper_2503_22879_b200.model import QuantizedMambaLM
+    from paper_2503_22879_b200.ssm_block import Dims
+    fm = cli.cmd_gen_toy(Dims("mamba2", 256, 512, 64, 8, 64, 2, 4), 2, seed=3)
+    toks = cli.calib_tokens(512, 2, 32)
+    qm = cli.cmd_quantize(fm, toks, ["W4A8", "W8A8"], device="cuda", emb_bits=4)
+    p = str(tmp_path / "q.bin")
+    archive.write_quant_model(qm, p)
+    x = torch.as_tensor(toks[:1, :24], device=cuda)
+    a, _ = QuantizedMambaLM(qm, cuda).prefill(x, all_logits=True)
+    b, _ = QuantizedMambaLM(archive.read_quant_model(p), cuda).prefill(x, all_logits=True)
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("profile", ["W8A8", "W4A8"])
+def test_4bit_embedding_logits(cuda, profile):
+    """Head-to-toe with 4-bit embedding rows: logits within 1e-2 of the oracle."""
+    from paper_2503_22879_b200.model import QuantizedMambaLM
+    d = osb.Dims("mamba2", 256, 512, 64, 8, 64, 2, 4)
+    fm = opl.cmd_gen_toy(d, 2, seed=0)
+    toks = opl.calib_tokens(512, 2, 64)
+    qm = opl.cmd_quantize(fm, toks, profile, emb_bits=4)
+    assert qm.emb_codes.min() >= -8 and qm.emb_codes.max() <= 7
+    ref, _ = opl.quant_forward(qm, toks[0, :40])
+    lm = QuantizedMambaLM(qm, cuda)
+    assert lm.emb_bits == 4 and lm.emb_codes.dtype == torch.uint8
+    lg, _ = lm.prefill(torch.as_tensor(toks[:1, :40], device=cuda), all_logits=True)
+    rel = np.abs(lg.cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert rel < 1e-2, rel

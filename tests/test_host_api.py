@@ -185,3 +185,40 @@ def test_archive_roundtrip_and_cli(tmp_path):
     info = archive.inspect(q_path)
     assert info["blocks.0.in_proj.codes"][-1] == "int8" and "blocks.0.state_scale" in info
     assert cli.main(["quantize", "--model", str(tmp_path / "missing.bin"), "--out", q_path]) == 1
+
+
+@pytest.mark.parametrize("emb_bits", [8, 4])
+@pytest.mark.parametrize("profile,dims", [("W4A8", TINY2), ("W8A8", TINY1), ("W4A16", TINY2)],
+                         ids=["w4a8-mamba2", "w8a8-mamba1", "w4a16-mamba2"])
+def test_quant_archive_roundtrip(tmp_path, profile, dims, emb_bits):
+    """write_quant_model -> read_quant_model restores every code, scale table and scalar bit for bit
+    (SPEC.md:49-57, 591), including a 4-bit (u4packed) embedding."""
+    fm = cli.cmd_gen_toy(Dims(*dims), 2, seed=7, vocab=64)
+    toks = opl.calib_tokens(64, 1, 16)
+    qm = cli.cmd_quantize(fm, toks, profile, device="cpu", emb_bits=emb_bits)
+    if emb_bits == 4:
+        assert qm.emb_codes.min() >= -8 and qm.emb_codes.max() <= 7
+    p = str(tmp_path / "q.bin")
+    archive.write_quant_model(qm, p)
+    if emb_bits == 4:
+        assert archive.archive_read(p)["emb_codes"].dtype == np.int8
+        assert "u4packed" in open(p, "rb").read(4096).decode("utf-8", "ignore")
+    back = archive.read_quant_model(p)
+    assert back.profiles == qm.profiles and back.extra["emb_bits"] == emb_bits and back.s_head == qm.s_head
+    assert np.array_equal(back.emb_codes, qm.emb_codes) and np.array_equal(back.emb_scale, qm.emb_scale)
+    for a, b in zip([qm.head] + [getattr(x, f) for x in qm.blocks for f in ("in_proj", "out_proj", "x_proj", "dt_proj")],
+                    [back.head] + [getattr(x, f) for x in back.blocks for f in ("in_proj", "out_proj", "x_proj", "dt_proj")]):
+        if a is None:
+            assert b is None
+            continue
+        assert a.kind == b.kind and a.group == b.group and np.array_equal(a.codes, b.codes)
+        for f in ("s_ch", "s_group"):
+            assert (getattr(a, f) is None) == (getattr(b, f) is None)
+            if getattr(a, f) is not None:
+                assert np.array_equal(np.asarray(getattr(a, f)), getattr(b, f))
+    for x, y in zip(qm.blocks, back.blocks):
+        for f in ("conv_weight", "conv_bias", "a_log", "d_param", "dt_bias", "norm_weight", "in_out_scale",
+                  "conv_in_scale", "conv_out_scale", "state_scale", "xproj_out_scale", "head_group"):
+            fa, fb = getattr(x, f), getattr(y, f)
+            assert (fa is None) == (fb is None) and (fa is None or np.array_equal(np.asarray(fa), np.asarray(fb))), f
+        assert (x.s_u, x.s_y, x.s_dt, x.hadamard, x.profile) == (y.s_u, y.s_y, y.s_dt, y.hadamard, y.profile)
