@@ -74,21 +74,22 @@ def fwht(v, plan: HadamardPlan) -> np.ndarray:
     return out
 
 
-def fwht_blocked(v) -> np.ndarray:
-    """Unnormalised I_q ⊗ H_b along the last axis (LEDGER G9)."""
+def fwht_blocked(v, b: int | None = None) -> np.ndarray:
+    """Unnormalised I_q ⊗ H_b along the last axis (LEDGER G9; b defaults to the largest power of
+    two dividing n, a smaller power of two gives the shard-local transform)."""
     v = np.asarray(v, np.float32)
     n = v.shape[-1]
-    b = block_size(n)
+    b = block_size(n) if b is None else b
     r = v.reshape(v.shape[:-1] + (n // b, b))
     return _butterflies(r).reshape(v.shape)
 
 
-def blocked_matrix(n: int) -> np.ndarray:
-    b = block_size(n)
+def blocked_matrix(n: int, b: int | None = None) -> np.ndarray:
+    b = block_size(n) if b is None else b
     return np.kron(np.eye(n // b, dtype=np.int64), hadamard_matrix(b))
 
 
-def fuse_hadamard_out_proj(w_out, n_in: int, n_out: int) -> np.ndarray:
+def fuse_hadamard_out_proj(w_out, n_in: int, n_out: int, block: int | None = None) -> np.ndarray:
     """normalised H_out · W · H_inᵀ (block-diagonal for
     non-power-of-two widths; n_out = 1 leaves the output side unrotated)."""
     w = np.asarray(w_out, np.float64)
@@ -96,7 +97,8 @@ def fuse_hadamard_out_proj(w_out, n_in: int, n_out: int) -> np.ndarray:
     if n_in != d_in or n_out not in (1, d_out):
         from oracle.errors import ShapeError
         raise ShapeError("fuse_hadamard_out_proj dims")
-    hi = blocked_matrix(d_in) / np.sqrt(block_size(d_in))
+    bi = block_size(d_in) if block is None else block
+    hi = blocked_matrix(d_in, bi) / np.sqrt(bi)
     r = w @ hi.T
     if n_out == d_out:
         ho = blocked_matrix(d_out) / np.sqrt(block_size(d_out))
@@ -112,8 +114,8 @@ def fuse_hadamard_in_proj(w_in) -> np.ndarray:
     return (w @ h.T).astype(np.float32)
 
 
-def hadamard_quantize(y, plan: HadamardPlan, bits: int = 8) -> np.ndarray:
+def hadamard_quantize(y, plan: HadamardPlan, bits: int = 8, block: int | None = None) -> np.ndarray:
     """one-pass quantize(fwht(y), s_y) (unnormalised H)."""
     if plan.fused_output_scale is None:
         raise ValueError("missing fused scale")
-    return quantize_codes(fwht_blocked(y), np.float32(plan.fused_output_scale), bits)
+    return quantize_codes(fwht_blocked(y, block), np.float32(plan.fused_output_scale), bits)

@@ -173,8 +173,8 @@ def quantize_block(blk: SsmBlockWeights, st: dict, profile: str, m=4, n=4, hadam
     s_xin = compute_scale(st["x_in"].channel_max, 8)
     out_w = w.out_proj
     if hadamard:
-        b = had.block_size(di)
-        out_w = (had.fuse_hadamard_out_proj(out_w, di, 1) / np.float32(np.sqrt(b))).astype(np.float32)
+        b = d.had_block
+        out_w = (had.fuse_hadamard_out_proj(out_w, di, 1, b) / np.float32(np.sqrt(b))).astype(np.float32)
     s_y = cal.calibrate_site_scale(st["y_had"]) if hadamard else compute_scale(st["r"].channel_max, 8)
     x_cell_scale = cmap.scales.reshape(-1)[cells].astype(np.float32)
     ssg = None

@@ -243,9 +243,9 @@ def block_forward_quantized(u, qb: QBlock, state: QState | None = None, chunk=No
         y, h = selective_scan(xh, dA, dt, Bm, Cm, qb.d_param, zz, h0)
         h_q = quantize_codes(h.reshape(1, di, N), qb.state_scale.reshape(1, di)[:, :, None], 8)
     tr.update(y=y)
-    r = rmsnorm(y, qb.norm_weight)
+    r = rmsnorm(y, qb.norm_weight, groups=d.norm_groups)
     if qb.hadamard:
-        yq = had.hadamard_quantize(r, had.HadamardPlan(di, "none", qb.s_y), 8)
+        yq = had.hadamard_quantize(r, had.HadamardPlan(di, "none", qb.s_y), 8, d.had_block)
     else:
         yq = quantize_codes(r, qb.s_y, 8)
     out, acc_out = qlinear_a8(yq, qb.out_proj, qb.s_y)
@@ -280,7 +280,7 @@ def _block_forward_a16(u, qb: QBlock, st: QState, tr):
         dA, dt = discretize(dt_raw, qb.dt_bias, qb.A)
         y, h = selective_scan(xc, dA, dt, xd[:, R:R + N], xd[:, R + N:], qb.d_param, z,
                               st.h.reshape(di, N))
-    r = rmsnorm(y, qb.norm_weight)
+    r = rmsnorm(y, qb.norm_weight, groups=d.norm_groups)
     out = qlinear_a16(r, qb.out_proj)
     tr.update(in_y=zx, y=y, r=r, out=out)
     return out, QState(np.asarray(h, np.float32).reshape(st.h.shape), cache)
@@ -331,8 +331,9 @@ def decode_step_batched(u, qb: QBlock, h_codes, conv_codes, trace=None):
          + (qb.d_param[None, :, None] * x).astype(np.float32))
     z = (codes[:, :di].astype(np.float32) * qb.in_out_scale[0]).reshape(-1, nh, P)
     y = (y * silu(z)).astype(np.float32).reshape(-1, di)
-    r = rmsnorm(y, qb.norm_weight)
-    yq = had.hadamard_quantize(r, had.HadamardPlan(di, "none", qb.s_y), 8) if qb.hadamard else quantize_codes(r, qb.s_y, 8)
+    r = rmsnorm(y, qb.norm_weight, groups=d.norm_groups)
+    yq = (had.hadamard_quantize(r, had.HadamardPlan(di, "none", qb.s_y), 8, d.had_block) if qb.hadamard
+          else quantize_codes(r, qb.s_y, 8))
     out, _ = qlinear_a8(yq, qb.out_proj, qb.s_y)
     if trace is not None:
         trace.update(in_codes=codes, conv_codes=cq, y=y, y_q=yq)

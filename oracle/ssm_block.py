@@ -34,6 +34,14 @@ class Dims:
     n_state_groups: int
     conv_kernel: int = 4
     dt_rank: int = 0          # Mamba1 only
+    norm_groups: int = 1      # gated RMSNorm groups (1 = full d_inner; LEDGER G13)
+
+    @property
+    def had_block(self):
+        """Online Hadamard block (LEDGER G9): largest power of two dividing d_inner / norm_groups,
+        so no block crosses a norm group (head-shard recipe)."""
+        g = self.d_inner // self.norm_groups
+        return g & (-g)
 
     @property
     def conv_dim(self):
@@ -247,9 +255,16 @@ def ssd_chunked(x, dA, dt, B, C, D, z=None, chunk=64, state=None, head_group=Non
     return y, H.astype(np.float32)
 
 
-def rmsnorm(v, weight, eps=EPS_NORM):
-    """RMS normalisation over the last axis (full d_inner, LEDGER G13)."""
+def rmsnorm(v, weight, eps=EPS_NORM, groups: int = 1):
+    """RMS normalisation over the last axis (full d_inner, LEDGER G13), or over
+    ``groups`` contiguous equal slices of it (the grouped norm of the head-shard recipe)."""
     v = np.asarray(v, np.float32)
+    if groups > 1:
+        n = v.shape[-1]
+        vg = v.reshape(v.shape[:-1] + (groups, n // groups))
+        ms = np.mean(vg.astype(np.float64) ** 2, axis=-1, keepdims=True).astype(np.float32)
+        r = (np.float32(1.0) / np.sqrt(ms + np.float32(eps))).astype(np.float32)
+        return ((vg * r).astype(np.float32).reshape(v.shape) * np.asarray(weight, np.float32)).astype(np.float32)
     ms = np.mean(v.astype(np.float64) ** 2, axis=-1, keepdims=True).astype(np.float32)
     r = (np.float32(1.0) / np.sqrt(ms + np.float32(eps))).astype(np.float32)
     return ((v * r).astype(np.float32) * np.asarray(weight, np.float32)).astype(np.float32)
@@ -290,9 +305,9 @@ def block_forward_float(u, w: SsmBlockWeights, state: SsmState | None = None, ch
         y, h = selective_scan(xc, dA, dt, B, C, w.d_param, z, st.h, hmax=hm)
         if taps is not None:
             taps.update(u=u, z=z, x_in=x, x=xc, dt_low=dt_low, B=B, C=C, dt=dt_raw, h=hm["h"])
-    r = rmsnorm(y, w.norm_weight)
+    r = rmsnorm(y, w.norm_weight, groups=d.norm_groups)
     if taps is not None:
         from oracle.hadamard import fwht_blocked
-        taps.update(y=y, r=r, y_had=fwht_blocked(r))
+        taps.update(y=y, r=r, y_had=fwht_blocked(r, d.had_block))
     out = _gemm(r, w.out_proj, fast)
     return out, SsmState(h, cache)

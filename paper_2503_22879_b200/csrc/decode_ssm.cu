@@ -681,13 +681,368 @@ __global__ void __launch_bounds__(256) norm_had8192_kernel(const sq_mamba2_decod
   }
 }
 
+// ------------------------------------------------------------------ fused decode step (one launch)
+// K5d + K9 + K6 in one persistent kernel (N1 decode: no f32 operand workspace, no y round trip
+// through a separate norm launch).  A CTA walks (sequence, head) tiles round-robin:
+//   warp 8       producer: bulk TMA of the int8 state tile (8 KB) into a NSLOT-deep smem ring
+//   warp 9       x operands of the tile's 64 channels: conv-cache stepping + SiLU + requant to the
+//                clustered x scale (prep_kernel's op order), x̂, Δx̂/s_h, SiLU(ẑ), s_h, Ȧ, D -> slot;
+//                the x channels' cache window is written here (one writer per channel)
+//   warp 10      B̂ | Ĉ of the head's state group (conv + SiLU + requant + dequant, recomputed only
+//                when (sequence, group) changes between consecutive tiles).  The group's cache
+//                window is shared by its heads, so it is rewritten by whichever tile is the last
+//                of the group to read the old window (a per-(sequence, group) counter)
+//   warps 0-7    consumers: the scaled-unit int8 state update of state_ring_kernel, y to HBM/L2
+// A row's gated norm + FWHT + quant runs in the CTA that completes the row's last tile: after each
+// tile the consumers count it on the row counter (after their y stores), and the CTA whose count
+// is the row's nh-th normalises the row in smem -- no CTA ever waits on another, so the grid size
+// is free.  Counters live in the caller's workspace (zeroed once, reset by their last user), so
+// the step is graph-replayable.
+constexpr int FU_CONSUMERS = 8;
+constexpr int FU_THREADS = (FU_CONSUMERS + 3) * 32;
+constexpr int FU_MAXD = 8192;      // d_inner handled by one CTA's gated norm
+template <int N>
+struct FuCfg {
+  static constexpr int TILE = DS_P * N;
+  static constexpr int ROWB = DS_ROWF * 4;
+  static constexpr int BCB = 2 * N * 4;
+  static constexpr int SLOT = TILE + ROWB + BCB;
+  static constexpr int NSLOT = 7;
+  static constexpr int OFF_NORM = NSLOT * SLOT;
+  static constexpr int OFF_BAR = OFF_NORM + FU_MAXD * 4;
+  static constexpr int SMEM = OFF_BAR + 2 * NSLOT * 8 + 16 + 128;
+  static_assert(SLOT % 16 == 0, "slot alignment");
+};
+
+__device__ __forceinline__ int conv1_code(const sq_mamba2_decode_params& P, int c, const int8_t q[4], float& so) {
+  // one channel, Kc = 4: acc = b + Σ_j w_j·(q_j·s_in) in tap order (IEEE RN, the oracle's order)
+  const float4 w = __ldg(reinterpret_cast<const float4*>(P.conv_w) + c);
+  const float si = __ldg(P.conv_s_in + c);
+  float acc = __ldg(P.conv_b + c);
+  acc = __fadd_rn(acc, __fmul_rn(w.x, __fmul_rn((float)q[0], si)));
+  acc = __fadd_rn(acc, __fmul_rn(w.y, __fmul_rn((float)q[1], si)));
+  acc = __fadd_rn(acc, __fmul_rn(w.z, __fmul_rn((float)q[2], si)));
+  acc = __fadd_rn(acc, __fmul_rn(w.w, __fmul_rn((float)q[3], si)));
+  so = __ldg(P.conv_s_out + c);
+  const float v = silu_approx(acc);
+  bool tie = false;
+  int8_t code = quant8_fast(v, rcp_approx(so), tie);
+  if (tie) code = quant8(v, so);
+  return code;
+}
+
+template <int N>
+__global__ void __launch_bounds__(FU_THREADS, 2)
+    mamba2_decode_fused_kernel(const sq_mamba2_decode_params P, int B, const int8_t* zx, int64_t ldzx,
+                               int8_t* conv_cache, int8_t* state, int* cnt, float* y, int64_t ldy, int8_t* yq,
+                               int64_t ldyq) {
+  using Cfg = FuCfg<N>;
+  const sq_mamba2_params& S = P.ssm;
+  constexpr int CPT = N / 8, VW = CPT / 4;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
+  uint64_t* empty = full + Cfg::NSLOT;
+  float* nbuf = reinterpret_cast<float*>(smem + Cfg::OFF_NORM);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nh = S.n_heads, G = S.n_groups, di = nh * DS_P, GN = G * N, C = di + 2 * GN;
+  // tiles are dealt round-robin (tile t = blockIdx.x + i * gridDim.x): each wave of the grid
+  // covers consecutive (sequence, head) tiles, so a row's tiles finish close together and the
+  // gated norm of a row runs in the CTA that completes the row's last tile (no waiting)
+  const int ntiles = B * nh, tstep = gridDim.x;
+  int* s_last = reinterpret_cast<int*>(smem + Cfg::OFF_BAR + 2 * Cfg::NSLOT * 8);
+  int* cnt_bg = cnt;            // [B * G]
+  int* cnt_row = cnt + B * G;   // [B]
+  pdl_trigger();
+  if (tid == 0) {
+    for (int i = 0; i < Cfg::NSLOT; ++i) {
+      mbar_init(&full[i], 3);                // producer (tx) + x-operand warp + B|C warp
+      mbar_init(&empty[i], FU_CONSUMERS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_wait();   // zx from in_proj; state / caches last written by earlier grids
+  if (warp == FU_CONSUMERS) {
+    // ---------------- producer: the int8 state tiles
+    if (lane == 0) {
+      for (int t = blockIdx.x, i = 0; t < ntiles; t += tstep, ++i) {
+        const int slot = i % Cfg::NSLOT;
+        if (i >= Cfg::NSLOT) mbar_wait(&empty[slot], ((i / Cfg::NSLOT) - 1) & 1);
+        mbar_arrive_expect_tx(&full[slot], Cfg::TILE);
+        bulk_load(smem + slot * Cfg::SLOT, state + (int64_t)t * Cfg::TILE, Cfg::TILE, &full[slot]);
+      }
+    }
+    return;
+  }
+  if (warp == FU_CONSUMERS + 1) {
+    // ---------------- x operands of the tile's 64 channels (2 per lane)
+    for (int t = blockIdx.x, i = 0; t < ntiles; t += tstep, ++i) {
+      const int slot = i % Cfg::NSLOT;
+      if (i >= Cfg::NSLOT) mbar_wait(&empty[slot], ((i / Cfg::NSLOT) - 1) & 1);
+      const int b = t / nh, h = t % nh;
+      const int8_t* zrow = zx + (int64_t)b * ldzx;
+      int8_t* cache_b = conv_cache + (int64_t)b * 3 * C;
+      float* rf = reinterpret_cast<float*>(smem + slot * Cfg::SLOT + Cfg::TILE);
+      const int p0 = 2 * lane, c = h * DS_P + p0;
+      const uint16_t c0 = *reinterpret_cast<const uint16_t*>(cache_b + c);
+      const uint16_t c1 = *reinterpret_cast<const uint16_t*>(cache_b + C + c);
+      const uint16_t c2 = *reinterpret_cast<const uint16_t*>(cache_b + 2 * C + c);
+      const uint16_t xn = *reinterpret_cast<const uint16_t*>(zrow + di + c);
+      const uint16_t zc = *reinterpret_cast<const uint16_t*>(zrow + c);
+      const int8_t dcode = zrow[2 * di + 2 * GN + h];
+      const float delta = softplus_f(__fadd_rn(__fmul_rn((float)dcode, S.s_dt), __ldg(S.dt_bias + h)));
+      const float rsmax = 2097152.0f / (128.0f * __ldg(S.s_B + __ldg(S.head_group + h)));
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int8_t q[4] = {(int8_t)(c0 >> (8 * e)), (int8_t)(c1 >> (8 * e)), (int8_t)(c2 >> (8 * e)),
+                             (int8_t)(xn >> (8 * e))};
+        float so;
+        const int code = conv1_code(P, c + e, q, so);
+        const float xh = __fmul_rn((float)code, so);
+        const float sh = __ldg(S.s_h + c + e);
+        rf[p0 + e] = xh;
+        rf[DS_P + p0 + e] = fminf(fmaxf(__fmul_rn(__fmul_rn(delta, xh), __frcp_rn(sh)), -rsmax), rsmax);
+        rf[2 * DS_P + p0 + e] = silu_approx(__fmul_rn((float)(int8_t)(zc >> (8 * e)), S.s_z));
+        rf[3 * DS_P + p0 + e] = sh;
+      }
+      if (lane == 0) {
+        rf[4 * DS_P] = expf(__fmul_rn(delta, __ldg(S.A + h)));
+        rf[4 * DS_P + 1] = __ldg(S.D + h);
+      }
+      // shift the x channels' cache window (this tile is their only reader and writer)
+      *reinterpret_cast<uint16_t*>(cache_b + c) = c1;
+      *reinterpret_cast<uint16_t*>(cache_b + C + c) = c2;
+      *reinterpret_cast<uint16_t*>(cache_b + 2 * C + c) = xn;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[slot]);
+    }
+    return;
+  }
+  if (warp == FU_CONSUMERS + 2) {
+    // ---------------- B̂ | Ĉ of the head's state group (N / 16 channels of B and of C per lane)
+    constexpr int PL = N / 32;
+    float bv[PL], cv[PL];
+    int cur_b = -1, cur_g = -1;
+    for (int t = blockIdx.x, i = 0; t < ntiles; t += tstep, ++i) {
+      const int slot = i % Cfg::NSLOT;
+      if (i >= Cfg::NSLOT) mbar_wait(&empty[slot], ((i / Cfg::NSLOT) - 1) & 1);
+      const int b = t / nh, h = t % nh, g = __ldg(S.head_group + h);
+      int8_t* cache_b = conv_cache + (int64_t)b * 3 * C;
+      int8_t nq[2][PL], o1[2][PL], o2[2][PL];
+      if (b != cur_b || g != cur_g) {
+        const int8_t* zrow = zx + (int64_t)b * ldzx;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int e = 0; e < PL; ++e) {
+            const int cc = di + k * GN + g * N + lane + 32 * e;
+            int8_t q[4] = {cache_b[cc], cache_b[C + cc], cache_b[2 * C + cc], zrow[di + cc]};
+            o1[k][e] = q[1];
+            o2[k][e] = q[2];
+            nq[k][e] = q[3];
+            float so;
+            const int code = conv1_code(P, cc, q, so);
+            (k == 0 ? bv : cv)[e] = __fmul_rn((float)code, so);
+          }
+        cur_b = b;
+        cur_g = g;
+      }
+      float* bcs = reinterpret_cast<float*>(smem + slot * Cfg::SLOT + Cfg::TILE + Cfg::ROWB);
+#pragma unroll
+      for (int e = 0; e < PL; ++e) {
+        bcs[bc_swz(lane + 32 * e, N)] = bv[e];
+        bcs[N + bc_swz(lane + 32 * e, N)] = cv[e];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[slot]);
+      // this tile has read the group's old cache window: the group's last reader rewrites it
+      int heads_g = 0;
+      for (int hh = lane; hh < nh; hh += 32) heads_g += __ldg(S.head_group + hh) == g;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) heads_g += __shfl_xor_sync(0xffffffffu, heads_g, o);
+      int last = 0;
+      if (lane == 0) {
+        __threadfence();
+        last = atomicAdd(&cnt_bg[b * G + g], 1) == heads_g - 1;
+        if (last) cnt_bg[b * G + g] = 0;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        // (the window values are re-read when this tile reused B̂|Ĉ from an earlier tile)
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+          for (int e = 0; e < PL; ++e) {
+            const int cc = di + k * GN + g * N + lane + 32 * e;
+            const int8_t a1 = cache_b[C + cc], a2 = cache_b[2 * C + cc], an = zx[(int64_t)b * ldzx + di + cc];
+            cache_b[cc] = a1;
+            cache_b[C + cc] = a2;
+            cache_b[2 * C + cc] = an;
+          }
+      }
+      (void)nq; (void)o1; (void)o2;
+    }
+    return;
+  }
+  // ---------------- consumers: thread = (row quad rq, column chunk); rows rq and rq + 32
+  const int chunk = tid & 7, rq = tid >> 3;
+  const float2 MG = make_float2(-8388736.0f, -8388736.0f);
+  const float2 RM = make_float2(12582912.0f, 12582912.0f);
+  const uint32_t full0 = smem_u32(full);
+  for (int t = blockIdx.x, i = 0; t < ntiles; t += tstep, ++i) {
+    const int b = t / nh, h = t % nh;
+    const int slot = i % Cfg::NSLOT;
+    const uint8_t* sl = smem + slot * Cfg::SLOT;
+    const float* rf = reinterpret_cast<const float*>(sl + Cfg::TILE);
+    const float* bcs = reinterpret_cast<const float*>(sl + Cfg::TILE + Cfg::ROWB);
+    mbar_wait_addr(full0 + slot * 8, (i / Cfg::NSLOT) & 1);
+    float2 bv[CPT / 2], cv[CPT / 2];
+#pragma unroll
+    for (int e = 0; e < CPT / 4; ++e) {
+      const float4 b4 = *reinterpret_cast<const float4*>(bcs + ((e * 8 + chunk) << 2));
+      const float4 c4 = *reinterpret_cast<const float4*>(bcs + N + ((e * 8 + chunk) << 2));
+      bv[e * 2] = make_float2(b4.x, b4.y);
+      bv[e * 2 + 1] = make_float2(b4.z, b4.w);
+      cv[e * 2] = make_float2(c4.x, c4.y);
+      cv[e * 2 + 1] = make_float2(c4.z, c4.w);
+    }
+    const float dA = rf[4 * DS_P], Dh = rf[4 * DS_P + 1];
+    const float2 dA2 = make_float2(dA, dA);
+    int8_t* st = state + (int64_t)t * Cfg::TILE + chunk * CPT;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int R = rq + 32 * k;
+      const float rs = rf[DS_P + R];
+      const float2 rs2 = make_float2(rs, rs);
+      uint32_t raw[VW];
+      if constexpr (VW == 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(sl + R * N + chunk * CPT);
+        raw[0] = v.x; raw[1] = v.y; raw[2] = v.z; raw[3] = v.w;
+      } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(sl + R * N + chunk * CPT);
+        raw[0] = v.x; raw[1] = v.y;
+      }
+      uint32_t outw[VW];
+      float2 acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        const uint32_t u = raw[e] ^ 0x80808080u;
+        int qi[4];
+#pragma unroll
+        for (int i2 = 0; i2 < 4; i2 += 2) {
+          const int n2 = e * 2 + i2 / 2;
+          const float2 hq = __fadd2_rn(make_float2(s8_raw(u, i2), s8_raw(u, i2 + 1)), MG);
+          const float2 tt = __ffma2_rn(dA2, hq, __fmul2_rn(rs2, bv[n2]));
+          acc2 = __ffma2_rn(tt, cv[n2], acc2);
+          const float2 rr = __fadd2_rn(tt, RM);   // bits = 0x4B400000 + rint(t), |t| < 2^22
+          qi[i2] = __float_as_int(rr.x) - 0x4B400000;
+          qi[i2 + 1] = __float_as_int(rr.y) - 0x4B400000;
+        }
+        outw[e] = pack4_sat(qi[0], qi[1], qi[2], qi[3]);
+      }
+      if constexpr (VW == 4)
+        *reinterpret_cast<uint4*>(st + R * N) = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+      else
+        *reinterpret_cast<uint2*>(st + R * N) = make_uint2(outw[0], outw[1]);
+      float acc = __fadd_rn(acc2.x, acc2.y);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (chunk == 0)
+        y[(int64_t)b * ldy + h * DS_P + R] =
+            __fmul_rn(__fadd_rn(__fmul_rn(rf[3 * DS_P + R], acc), __fmul_rn(Dh, rf[R])), rf[2 * DS_P + R]);
+    }
+    fence_proxy_async_smem();   // our generic reads of the slot precede the next bulk copy into it
+    if (chunk == 0) __threadfence();   // this thread's y stores precede the row count below
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    named_bar(1, FU_CONSUMERS * 32);
+    if (tid == 0) {
+      const int last = atomicAdd(&cnt_row[b], 1) == nh - 1;
+      if (last) {
+        __threadfence();   // acquire: the other tiles' y stores are visible to this CTA
+        cnt_row[b] = 0;    // self-reset for the next launch
+      }
+      *s_last = last;
+    }
+    named_bar(1, FU_CONSUMERS * 32);
+    if (*s_last) {
+      // ---------------- row b is complete (this CTA counted its last head): gated RMSNorm
+      // (f64 sum of squares) + blocked FWHT (Sylvester stages in the oracle's order) + quant
+      const int E = di / (FU_CONSUMERS * 32);      // contiguous values per thread (<= 32)
+      const float* yr = y + (int64_t)b * ldy + tid * E;
+      float v[32];
+      double ss = 0.0;
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < E) {
+          v[e] = __ldcg(yr + e);
+          ss += (double)v[e] * (double)v[e];
+        }
+      ss = warp_sum_d(ss);
+      double* red = reinterpret_cast<double*>(nbuf);   // nbuf is free until the FWHT stage
+      if (lane == 0) red[warp] = ss;
+      named_bar(1, FU_CONSUMERS * 32);
+      double tot = 0.0;
+#pragma unroll
+      for (int w = 0; w < FU_CONSUMERS; ++w) tot += red[w];
+      named_bar(1, FU_CONSUMERS * 32);
+      const float ms = (float)(tot / (double)di);
+      const float rfac = __fdiv_rn(1.0f, sqrtf(__fadd_rn(ms, P.eps)));
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < E) v[e] = __fmul_rn(__fmul_rn(v[e], rfac), __ldg(P.norm_w + tid * E + e));
+      const int hb = P.hadamard ? (di & -di) : 1;
+      for (int hh = 1; hh < E && hh < hb; hh <<= 1)
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e < E && (e & hh) == 0) {
+            const float x0 = v[e], x1 = v[e + hh];
+            v[e] = __fadd_rn(x0, x1);
+            v[e + hh] = __fsub_rn(x0, x1);
+          }
+      if (hb > E) {   // remaining stages across threads, in smem
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e < E) nbuf[tid * E + e] = v[e];
+        named_bar(1, FU_CONSUMERS * 32);
+        for (int hh = E, lg = __ffs(E) - 1; hh < hb; hh <<= 1, ++lg) {
+          for (int idx = tid; idx < di / 2; idx += FU_CONSUMERS * 32) {
+            const int i0 = ((idx >> lg) << (lg + 1)) | (idx & (hh - 1));
+            const float x0 = nbuf[i0], x1 = nbuf[i0 + hh];
+            nbuf[i0] = __fadd_rn(x0, x1);
+            nbuf[i0 + hh] = __fsub_rn(x0, x1);
+          }
+          named_bar(1, FU_CONSUMERS * 32);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e < E) v[e] = nbuf[tid * E + e];
+        named_bar(1, FU_CONSUMERS * 32);   // nbuf reads done before the next row reuses it
+      }
+      int8_t* out = yq + (int64_t)b * ldyq + tid * E;
+#pragma unroll
+      for (int e = 0; e < 32; ++e)
+        if (e < E) out[e] = quant8(v[e], P.s_y);
+    }
+  }
+}
+
 }  // namespace sq
 
 using namespace sq;
 
+// Workspace: [f32 operands of the three-launch path][int32 counters of the fused path: B*G
+// (sequence, group) + B rows].  The counter region must be zero before the first call; the fused
+// kernel leaves it zero (each counter is reset by its last user).
+static int64_t ds_counter_off(int B, const sq_mamba2_params& S) {
+  return ((ds_ws_floats(B, S.n_heads, S.n_groups, S.d_state) * 4 + 255) / 256) * 256;
+}
+
 extern "C" int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, int B) {
   if (!p || B < 0) return -1;
-  return ds_ws_floats(B, p->ssm.n_heads, p->ssm.n_groups, p->ssm.d_state) * 4;
+  return ds_counter_off(B, p->ssm) + (int64_t)(B * p->ssm.n_groups + B) * 4;
 }
 
 extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
@@ -721,6 +1076,38 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
   cudaStream_t st = as_stream(stream);
   float* wsf = reinterpret_cast<float*>(ws);
   constexpr int stages = SQ_DECODE_STAGES;
+  // one fused launch (conv + state update + gated norm + FWHT + quant) when the shape allows
+  const int fe = di / (FU_CONSUMERS * 32);   // values per consumer thread in the row norm (a power of two)
+  const bool fused = stages == 7 && p->conv_kernel == 4 && di <= FU_MAXD && di % (FU_CONSUMERS * 32) == 0 &&
+                     fe <= 32 && (fe & (fe - 1)) == 0 && ldzx % 2 == 0 && !yq_gsum &&
+                     !(reinterpret_cast<uintptr_t>(zx) & 1) && !(reinterpret_cast<uintptr_t>(p->conv_w) & 15);
+  if (fused) {
+    int* cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ds_counter_off(B, S));
+    auto launch = [&](auto kern, int smem) {
+      static std::once_flag once[2][64];
+      static int grid_cache[2][64];
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const int kind = S.d_state == 128 ? 1 : 0;
+      std::call_once(once[kind][dev & 63], [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int per_sm = 0, sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FU_THREADS, smem) != cudaSuccess || per_sm < 1)
+          per_sm = 1;
+        grid_cache[kind][dev & 63] = sms * per_sm;   // one wave of persistent CTAs
+      });
+      const int tiles = B * S.n_heads;
+      const int g = grid_cache[kind][dev & 63];
+      launch_k(PDL_RING, kern, dim3(tiles < g ? tiles : g), dim3(FU_THREADS), smem, st, *p, B, zx, ldzx, conv_cache,
+               state, cnt, y, ldy, yq, ldyq);
+    };
+    if (S.d_state == 128)
+      launch(mamba2_decode_fused_kernel<128>, FuCfg<128>::SMEM);
+    else
+      launch(mamba2_decode_fused_kernel<64>, FuCfg<64>::SMEM);
+    return check_launch("sq_mamba2_decode_step_int8 (fused)");
+  }
   const int vec = p->conv_kernel == 4 && C % 4 == 0 && ldzx % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(zx) & 3) == 0 && (reinterpret_cast<uintptr_t>(conv_cache) & 3) == 0;
   const int per_blk = vec ? 1024 : 256;

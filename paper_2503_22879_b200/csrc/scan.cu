@@ -220,7 +220,7 @@ static int launch_mamba2(const sq_mamba2_params* p, int B, int T, const TQ* x, i
   const int NPT = N / TPR;
   SQ_REQUIRE(P * TPR <= 256 && (TPR & (TPR - 1)) == 0 && (NPT == 16 || NPT == 32 || NPT == 64), SQ_ERR_SHAPE,
              "%s: unsupported head_dim/d_state (P=%d N=%d)", name, P, N);
-  SQ_REQUIRE(p->n_heads % p->n_groups == 0, SQ_ERR_SHAPE, "%s: heads/groups", name);
+  SQ_REQUIRE(p->n_groups >= 1, SQ_ERR_SHAPE, "%s: n_groups", name);   // heads map to groups via head_group
   if (B == 0 || T == 0) return SQ_OK;
   dim3 grid(p->n_heads, B), block(P * TPR);
 #define SQ_M2(NPTV)                                                                                           \
@@ -284,14 +284,16 @@ __global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, in
 // 4 state quarters (thread = one channel's 4 of the 16 states), so d_inner 5120 runs on 160 CTAs
 // instead of 40 one-channel-per-thread CTAs.  Time is walked in chunks of M1_TC tokens whose
 // operands are staged into shared memory by all 128 threads (cp.async, double-buffered one chunk
-// ahead): the codes are turned once per (token, channel) into Δ = softplus(Δ̂ + dt_bias), Δ·x̂ and
-// SiLU(ẑ), and B̂ | Ĉ once per token, so the sequential recurrence reads only smem.  Per step a
-// thread updates its 4 states (h = Ȧ·h + (Δx̂)·B̂, unfused like the oracle) and the channel's
-// C·h is reduced over the 4 threads with two shuffles.  The final state is requantised once.
-constexpr int M1_TC = 32;
+// ahead) and turned there, in parallel, into everything that does not depend on the state:
+// Δ = softplus(Δ̂ + dt_bias), Δ·x̂, x̂, SiLU(ẑ), B̂ | Ĉ and every Ȧ = exp(Δ·A) of the chunk
+// (16 exps per token and channel, off the recurrence's critical path).  The sequential part then
+// reads only smem: per step a thread updates its 4 states (h = Ȧ·h + (Δx̂)·B̂, unfused like the
+// oracle) and the channel's C·h is reduced over its 4 threads with two shuffles; the time loop is
+// unrolled so steps overlap.  The final state is requantised once.
+constexpr int M1_TC = 16;
 constexpr int M1_CH = 32;
 struct M1Stage {
-  float dl[M1_TC][M1_CH];      // Δ
+  float da[M1_TC][M1_CH][16];  // Ȧ
   float dx[M1_TC][M1_CH];      // Δ·x̂
   float xh[M1_TC][M1_CH];      // x̂ (the D·x skip)
   float gz[M1_TC][M1_CH];      // SiLU(ẑ)
@@ -317,82 +319,77 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
   constexpr int N = 16;
   __shared__ __align__(16) M1Raw raw[2];
   __shared__ __align__(16) M1Stage stg;
+  __shared__ float As[M1_CH][N];
   const int tid = threadIdx.x;
   const int cl = tid >> 2, qt = tid & 3;       // channel within the CTA, state quarter
   const int c0 = blockIdx.x * M1_CH, c = c0 + cl;
   const int b = blockIdx.y;
   pdl_trigger();
-  float A[4], hs[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) A[i] = p.A[c * N + qt * 4 + i];
+  for (int i = tid; i < M1_CH * N; i += 128) As[i / N][i % N] = p.A[(int64_t)c0 * N + i];
   const float sh = p.s_h[c], Dc = p.D[c];
-  // staging role constants: thread -> (token row, 16-B piece) of the raw tiles
   pdl_wait();   // inputs come from the previous grid
   int8_t* st = state + ((int64_t)b * p.d_inner + c) * N + qt * 4;
+  float hs[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) hs[i] = state_in ? __fmul_rn((float)st[i], sh) : 0.f;
   const int nch = (T + M1_TC - 1) / M1_TC;
-  auto issue = [&](int ch) {   // M1_TC rows x (x 2 + dt 2 + z 2 + bc 2) 16-B pieces, 128 threads
+  auto issue = [&](int ch) {   // M1_TC rows x (x, dt, z, bc) x 2 16-B pieces = 128 pieces: one per thread
     M1Raw& r = raw[ch & 1];
-#pragma unroll
-    for (int k = 0; k < M1_TC * 8 / 128; ++k) {
-      const int piece = tid + k * 128;
-      const int row = piece >> 3, kind = (piece >> 1) & 3, half = piece & 1;
-      const int t = ch * M1_TC + row;
-      if (t < T) {
-        const int64_t tok = (int64_t)b * T + t;
-        const int8_t* src = kind == 0 ? x + tok * ldx + c0 : kind == 1 ? dt + tok * lddt + c0
-                          : kind == 2 ? z + tok * ldz + c0 : BC + tok * ldbc;
-        int8_t* dst = kind == 0 ? r.x[row] : kind == 1 ? r.dt[row] : kind == 2 ? r.z[row] : r.bc[row];
-        cp_async16(dst + half * 16, src + half * 16);
-      }
+    const int row = tid >> 3, kind = (tid >> 1) & 3, half = tid & 1;
+    const int t = ch * M1_TC + row;
+    if (t < T) {
+      const int64_t tok = (int64_t)b * T + t;
+      const int8_t* src = kind == 0 ? x + tok * ldx + c0 : kind == 1 ? dt + tok * lddt + c0
+                        : kind == 2 ? z + tok * ldz + c0 : BC + tok * ldbc;
+      int8_t* dst = kind == 0 ? r.x[row] : kind == 1 ? r.dt[row] : kind == 2 ? r.z[row] : r.bc[row];
+      cp_async16(dst + half * 16, src + half * 16);
     }
     cp_async_commit();
   };
+  static_assert(M1_TC * 8 == 128, "one 16-B piece per thread per chunk");
   issue(0);
   for (int ch = 0; ch < nch; ++ch) {
     const int tn = min(M1_TC, T - ch * M1_TC);
     if (ch + 1 < nch) {
+      __syncthreads();   // everyone is done reading raw[(ch + 1) & 1] (chunk ch - 1's staging)
       issue(ch + 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
-    __syncthreads();   // raw[ch & 1] landed; every thread is done with the previous stage
+    __syncthreads();   // raw[ch & 1] landed; the recurrence of chunk ch - 1 is done with stg
     const M1Raw& r = raw[ch & 1];
-    // per (token, channel) operands: M1_TC x 32 items
+    // state-independent operands, all (token, channel) pairs of the chunk in parallel
     for (int i = tid; i < tn * M1_CH; i += 128) {
       const int row = i / M1_CH, cc = i % M1_CH, ch_g = c0 + cc;
       const float delta = softplus_f(__fadd_rn(__fmul_rn((float)r.dt[row][cc], p.s_dt), p.dt_bias[ch_g]));
       const float xv = __fmul_rn((float)r.x[row][cc], p.s_x[ch_g]);
-      stg.dl[row][cc] = delta;
       stg.dx[row][cc] = __fmul_rn(delta, xv);
       stg.xh[row][cc] = xv;
       stg.gz[row][cc] = silu_f(__fmul_rn((float)r.z[row][cc], p.s_z));
+#pragma unroll
+      for (int n = 0; n < N; ++n) stg.da[row][cc][n] = expf(__fmul_rn(delta, As[cc][n]));
     }
     for (int i = tid; i < tn * 32; i += 128) {
       const int row = i >> 5, n = i & 31;
       stg.bc[row][n] = __fmul_rn((float)r.bc[row][n], n < N ? p.s_B : p.s_C);
     }
     __syncthreads();
+    float* yrow = y + ((int64_t)b * T + ch * M1_TC) * ldy + c;
+#pragma unroll 4
     for (int tt = 0; tt < tn; ++tt) {
-      const float delta = stg.dl[tt][cl], dtx = stg.dx[tt][cl];
+      const float dtx = stg.dx[tt][cl];
+      const float4 av = *reinterpret_cast<const float4*>(&stg.da[tt][cl][qt * 4]);
       const float4 bv = *reinterpret_cast<const float4*>(&stg.bc[tt][qt * 4]);
       const float4 cv = *reinterpret_cast<const float4*>(&stg.bc[tt][N + qt * 4]);
-      const float bb[4] = {bv.x, bv.y, bv.z, bv.w}, cc4[4] = {cv.x, cv.y, cv.z, cv.w};
-      float acc = 0.f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float dA = expf(__fmul_rn(delta, A[i]));
-        hs[i] = __fadd_rn(__fmul_rn(dA, hs[i]), __fmul_rn(dtx, bb[i]));
-        acc = fmaf(hs[i], cc4[i], acc);
-      }
+      hs[0] = __fadd_rn(__fmul_rn(av.x, hs[0]), __fmul_rn(dtx, bv.x));
+      hs[1] = __fadd_rn(__fmul_rn(av.y, hs[1]), __fmul_rn(dtx, bv.y));
+      hs[2] = __fadd_rn(__fmul_rn(av.z, hs[2]), __fmul_rn(dtx, bv.z));
+      hs[3] = __fadd_rn(__fmul_rn(av.w, hs[3]), __fmul_rn(dtx, bv.w));
+      float acc = fmaf(hs[3], cv.w, fmaf(hs[2], cv.z, fmaf(hs[1], cv.y, hs[0] * cv.x)));
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (qt == 0) {
-        const float yv = __fadd_rn(acc, __fmul_rn(Dc, stg.xh[tt][cl]));
-        y[((int64_t)b * T + ch * M1_TC + tt) * ldy + c] = __fmul_rn(yv, stg.gz[tt][cl]);
-      }
+      if (qt == 0) yrow[(int64_t)tt * ldy] = __fmul_rn(__fadd_rn(acc, __fmul_rn(Dc, stg.xh[tt][cl])), stg.gz[tt][cl]);
     }
   }
 #pragma unroll
@@ -722,7 +719,7 @@ extern "C" int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T, const fl
                                const float* z, int64_t ldz, float* state, int state_in, float* y, int64_t ldy,
                                void* stream) {
   if (p && B > 0 && T > 0 && p->head_dim % 32 == 0 && (p->d_state == 64 || p->d_state == 128 || p->d_state == 256) &&
-      p->n_heads % p->n_groups == 0 && ldbc % 2 == 0 && (reinterpret_cast<uintptr_t>(Bm) & 7) == 0 &&
+      p->n_groups >= 1 && ldbc % 2 == 0 && (reinterpret_cast<uintptr_t>(Bm) & 7) == 0 &&
       (reinterpret_cast<uintptr_t>(Cm) & 7) == 0 && (reinterpret_cast<uintptr_t>(state) & 7) == 0) {
     const dim3 grid(p->n_heads, B, p->head_dim / 32);
     cudaStream_t st = as_stream(stream);
@@ -836,7 +833,7 @@ extern "C" int sq_selective_scan2_pre_f32(const sq_mamba2_params* p, int B, int 
                                           int state_in, float* y, int64_t ldy, void* stream) {
   SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_selective_scan2_pre_f32: bad args");
   const int N = p ? p->d_state : 0;
-  SQ_REQUIRE(p->n_heads % p->n_groups == 0 && (N == 16 || N == 32 || ((N == 64 || N == 128 || N == 256) &&
+  SQ_REQUIRE(p->n_groups >= 1 && (N == 16 || N == 32 || ((N == 64 || N == 128 || N == 256) &&
                                                                       p->head_dim % 8 == 0 && ldbc % 2 == 0)),
              SQ_ERR_SHAPE, "sq_selective_scan2_pre_f32: d_state in {16,32,64,128,256} (P=%d N=%d)", p->head_dim, N);
   if (B == 0 || T == 0) return SQ_OK;

@@ -35,7 +35,11 @@ def softplus(v):
     return torch.where(v > 20.0, v, torch.log1p(torch.exp(torch.clamp(v, max=20.0))))
 
 
-def rmsnorm(v, weight):
+def rmsnorm(v, weight, groups: int = 1):
+    if groups > 1:   # grouped norm (head-shard recipe): contiguous equal slices of the last axis
+        vg = v.reshape(*v.shape[:-1], groups, v.shape[-1] // groups)
+        ms = (vg.to(torch.float64) ** 2).mean(dim=-1, keepdim=True).to(torch.float32)
+        return ((vg * (1.0 / torch.sqrt(ms + np.float32(EPS_NORM)))).reshape(v.shape)) * weight
     ms = (v.to(torch.float64) ** 2).mean(dim=-1, keepdim=True).to(torch.float32)
     r = 1.0 / torch.sqrt(ms + np.float32(EPS_NORM))
     return (v * r) * weight
@@ -108,9 +112,9 @@ def block_forward_float(u, w, taps: dict | None = None, device="cuda"):
         y = torch.stack(ys) * silu(z)
         if taps is not None:
             taps.update(u=u, z=z, x_in=x, x=xc, dt_low=dt_low, B=Bm, C=Cm, dt=dt_raw, h=hmax)
-    r = rmsnorm(y, _t(w.norm_weight, dev))
+    r = rmsnorm(y, _t(w.norm_weight, dev), d.norm_groups)
     if taps is not None:
-        taps.update(y=y, r=r, y_had=fwht_blocked(r))
+        taps.update(y=y, r=r, y_had=fwht_blocked(r, d.had_block))
     return _proj(r, w.out_proj, dev)
 
 

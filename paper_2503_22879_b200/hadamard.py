@@ -72,29 +72,30 @@ def fwht(v, plan: HadamardPlan) -> torch.Tensor:
     return out
 
 
-def fwht_blocked(v) -> torch.Tensor:
-    """Unnormalised I_q ⊗ H_b along the last axis (LEDGER G9)."""
+def fwht_blocked(v, b: int | None = None) -> torch.Tensor:
+    """Unnormalised I_q ⊗ H_b along the last axis (LEDGER G9; b = largest power of two dividing n
+    by default, smaller for the shard-local transform of the head-shard recipe)."""
     v = _f32(v)
     n = v.shape[-1]
-    b = block_size(n)
+    b = block_size(n) if b is None else b
     return _butterflies(v.reshape(*v.shape[:-1], n // b, b)).reshape(v.shape)
 
 
-def _blocked_matrix(n: int) -> np.ndarray:
-    b = block_size(n)
+def _blocked_matrix(n: int, b: int | None = None) -> np.ndarray:
+    b = block_size(n) if b is None else b
     return np.kron(np.eye(n // b), hadamard_matrix(b).numpy().astype(np.float64)) / np.sqrt(b)
 
 
 # The offline fusions use float64 numpy GEMMs (the reference's numeric stack, numpy>=1.24,
 # pkg/pyproject.toml:10) so fused weights — hence weight codes — match the CPU contract bit
 # for bit.
-def fuse_hadamard_out_proj(w_out, n_in: int, n_out: int) -> torch.Tensor:
+def fuse_hadamard_out_proj(w_out, n_in: int, n_out: int, block: int | None = None) -> torch.Tensor:
     """normalised H_out · W · H_inᵀ (n_out = 1 leaves the output side)."""
     w = np.asarray(w_out, np.float64)
     d_out, d_in = w.shape
     if n_in != d_in or n_out not in (1, d_out):
         raise ShapeError("fuse_hadamard_out_proj dims")
-    r = w @ _blocked_matrix(d_in).T
+    r = w @ _blocked_matrix(d_in, block).T
     if n_out == d_out:
         r = _blocked_matrix(d_out) @ r
     return torch.from_numpy(r.astype(np.float32))
@@ -106,8 +107,8 @@ def fuse_hadamard_in_proj(w_in) -> torch.Tensor:
     return torch.from_numpy((w @ _blocked_matrix(w.shape[1]).T).astype(np.float32))
 
 
-def hadamard_quantize(y, plan: HadamardPlan, bits: int = 8) -> torch.Tensor:
+def hadamard_quantize(y, plan: HadamardPlan, bits: int = 8, block: int | None = None) -> torch.Tensor:
     """quantize(H y, s_y) in one pass (unnormalised H, LEDGER G9 blocks)."""
     if plan.fused_output_scale is None:
         raise ValueError("missing fused scale")
-    return _codes(fwht_blocked(y), torch.tensor(np.float32(plan.fused_output_scale)), bits)
+    return _codes(fwht_blocked(y, block), torch.tensor(np.float32(plan.fused_output_scale)), bits)

@@ -86,7 +86,9 @@ class QuantizedMambaLM:
               "tok": e((M,), torch.int32)}
         fused = [b for b in self.blocks if getattr(b, "fused_decode", False)]
         if fused:
-            ws["dws"] = e((ops.mamba2_decode_ws_bytes(fused[0].decode_params, M),), torch.uint8)
+            # zero-filled once: the fused decode kernel's counters live here (self-resetting)
+            ws["dws"] = torch.zeros((ops.mamba2_decode_ws_bytes(fused[0].decode_params, M),), dtype=torch.uint8,
+                                    device=dev)
         if any(not b.a8 for b in self.blocks):
             ws.update(uf=e((M, d.d_model), torch.float32), zxf=e((M, d.in_proj_out), torch.float32),
                       convf=e((M, d.conv_dim), torch.float32), r=e((M, d.d_inner), torch.float32))

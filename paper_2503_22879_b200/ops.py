@@ -308,8 +308,8 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     if y is None:
         y = torch.empty((B, di), dtype=torch.float32, device=zx.device)
     nbytes = mamba2_decode_ws_bytes(p, B)
-    if ws is None:
-        ws = torch.empty(nbytes, dtype=torch.uint8, device=zx.device)
+    if ws is None:   # zero-filled: the fused kernel's counters start (and stay) at zero
+        ws = torch.zeros(nbytes, dtype=torch.uint8, device=zx.device)
     if ws.numel() * ws.element_size() < nbytes:
         raise ShapeError(f"decode workspace needs {nbytes} bytes")
     _dev(yq, torch.int8, "yq", 2)
@@ -318,7 +318,8 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     _check(lib().sq_mamba2_decode_step_int8(C.byref(p), B, zx.data_ptr(), _ld(zx), conv_cache.data_ptr(),
                                             state.data_ptr(), ws.data_ptr(), y.data_ptr(), _ld(y), yq.data_ptr(),
                                             _ld(yq), gp, gl, _stream()),
-           3 + (gsum is not None and not (di == 8192 and p.hadamard)))   # prep, state ring, norm (+ sums)
+           1 if gsum is None and p.conv_kernel == 4 and di <= 8192 and di % 256 == 0 and (di // 256) & (di // 256 - 1) == 0
+           else 3 + (gsum is not None and not (di == 8192 and p.hadamard)))   # prep, state ring, norm (+ sums)
     return yq
 
 

@@ -35,6 +35,13 @@ class Dims:
     n_state_groups: int
     conv_kernel: int = 4
     dt_rank: int = 0
+    norm_groups: int = 1      # gated-RMSNorm groups: 1 = full d_inner; > 1 = head-shard recipe
+
+    @property
+    def had_block(self):
+        """Online Hadamard block: largest power of two dividing d_inner / norm_groups (LEDGER G9)."""
+        g = self.d_inner // self.norm_groups
+        return g & (-g)
 
     @property
     def conv_dim(self):
@@ -213,6 +220,9 @@ class DeviceBlock:
 
     def __init__(self, qb, dev="cuda"):
         d = qb.dims
+        if getattr(d, "norm_groups", 1) != 1:
+            raise ShapeError("a block with norm_groups > 1 runs head-sharded (parallel.HeadShardedBlock): the "
+                             "gated-norm / Hadamard kernels normalise whole rows")
         self.dims = d
         self.profile = qb.profile
         self.a8 = qb.profile in ("W8A8", "W4A8")
@@ -521,7 +531,15 @@ def block_forward_float(u, w: SsmBlockWeights, state: SsmState | None = None, ch
         dt_raw = _gemm_f(xd[:, :R].contiguous(), w.dt_proj)
         dA, dt = discretize(dt_raw, w.dt_bias, A)
         y, h = selective_scan(xc, dA, dt, xd[:, R:R + N], xd[:, R + N:R + 2 * N], w.d_param, z=z, state=h0)
-    r = ops.rmsnorm_f32(y.contiguous(), _f32(w.norm_weight, dev).contiguous(), EPS_NORM)
+    gam = _f32(w.norm_weight, dev).contiguous()
+    y = y.contiguous()
+    if d.norm_groups == 1:
+        r = ops.rmsnorm_f32(y, gam, EPS_NORM)
+    else:   # grouped norm (head-shard recipe): one strided column slice per group
+        r = torch.empty_like(y)
+        gw = d.d_inner // d.norm_groups
+        for g in range(d.norm_groups):
+            ops.rmsnorm_f32(y[:, g * gw:(g + 1) * gw], gam[g * gw:(g + 1) * gw], EPS_NORM, r[:, g * gw:(g + 1) * gw])
     return _gemm_f(r, w.out_proj), SsmState(h, cache)
 
 

@@ -46,7 +46,7 @@ def random_qblock(d: Dims, profile: str, seed: int = 0) -> QBlock:
     kind = {"W8A8": "w8", "W4A8": "w4a8", "W4A16": "w4a16"}[profile]
     di = d.d_inner
     s = np.float32(4.0 / 127)
-    hb = di & -di
+    hb = d.had_block
     s_y = np.float32(4.5 * np.sqrt(hb) / 127)
     inp = _analytic_qlinear(r, d.in_proj_out, d.d_model, kind, 128, 1.0, U_STD_CODES, s)
     out = _analytic_qlinear(r, d.d_model, di, kind, 128, 0.1, 127.0 / 4.0, s_y)

@@ -185,3 +185,30 @@ def test_generate_per_step_logits(cuda, profile):
         rl, rst = opl.quant_forward(qm, [nxt], rst)
         assert _rel(lg.cpu().numpy()[0], rl[-1]) <= 1e-2, step
         nxt = int(np.argmax(rl[-1]))                  # teacher forcing on the oracle's greedy token
+
+
+@pytest.mark.parametrize("profile,world", [("W8A8", 2), ("W4A8", 4)])
+def test_head_shard_block_on_gpu(cuda, profile, world):
+    """Head-shard mode on the GPU kernels (one device, the ranks' shards run in turn and their
+    out_proj partials are summed as the all-reduce would): prefill + 8 decode steps against the
+    unsharded oracle block of the same shard-local recipe (norm_groups = world)."""
+    from paper_2503_22879_b200 import cli, parallel
+    from paper_2503_22879_b200.ssm_block import DeviceBlock, Dims, block_forward_quantized
+    d = Dims("mamba2", 256, 1024, 64, 16, 64, 4, 4, norm_groups=world)
+    fm = cli.cmd_gen_toy(d, 1, seed=26)
+    qb = cli.cmd_quantize(fm, cli.calib_tokens(512, 2, 48), profile, device="cuda").blocks[0]
+    oqb = _oracle_block(qb)
+    shards = [DeviceBlock(parallel.shard_qblock(qb, world, r), cuda) for r in range(world)]
+    u = np.random.default_rng(26).standard_normal((48, d.d_model)).astype(np.float32)
+    states = [None] * world
+    ost = None
+    for lo, hi in [(0, 40)] + [(t, t + 1) for t in range(40, 48)]:
+        tot = 0
+        for r, blk in enumerate(shards):
+            out, states[r] = block_forward_quantized(torch.as_tensor(u[lo:hi], device=cuda), blk, state=states[r])
+            tot = tot + out.cpu().numpy()
+        ro, ost = oq.block_forward_quantized(u[lo:hi], oqb, ost)
+        assert _rel(tot, ro) < 5e-2, (lo, _rel(tot, ro))
+    h = np.concatenate([s.h[0].cpu().numpy() for s in states])
+    mx, frac = _codes(h, ost.h)
+    assert mx <= 1 and frac < 2e-2
