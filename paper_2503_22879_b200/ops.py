@@ -318,7 +318,7 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     _check(lib().sq_mamba2_decode_step_int8(C.byref(p), B, zx.data_ptr(), _ld(zx), conv_cache.data_ptr(),
                                             state.data_ptr(), ws.data_ptr(), y.data_ptr(), _ld(y), yq.data_ptr(),
                                             _ld(yq), gp, gl, _stream()),
-           1 if gsum is None and p.conv_kernel == 4 and di <= 8192 and di % 256 == 0 and (di // 256) & (di // 256 - 1) == 0
+           1 if gsum is None and p.conv_kernel == 4 and di <= 8192 and p.ssm.n_groups <= 128 and di % 512 == 0 and (di // 512) & (di // 512 - 1) == 0
            else 3 + (gsum is not None and not (di == 8192 and p.hadamard)))   # prep, state ring, norm (+ sums)
     return yq
 
