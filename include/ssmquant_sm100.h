@@ -167,9 +167,11 @@ int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T,
  *   int8 SSM state update h' = exp(dt*A) h + dt*x*B, y = C.h' + D*x, y*SiLU(z)
  *   (selective_scan T=1) -> y,
  *   RMSNorm over d_inner + Sylvester FWHT + quant with s_y -> yq.
- * Three launches on `stream`.  State and conv cache are updated in place; ws
- * (sq_mamba2_decode_ws_bytes) and y [B x d_inner] f32 are caller-owned (y holds the gated
- * SSM output). */
+ * Two launches on `stream` when d_inner = 256 * 2^k <= 8192 and yq_gsum is NULL (the norm runs
+ * inside the state kernel, as each row completes), else three (sq_mamba2_decode_launches).
+ * State and conv cache are updated in place; ws (sq_mamba2_decode_ws_bytes) and y
+ * [B x d_inner] f32 are caller-owned (y holds the gated SSM output).  ws must be zero-filled
+ * before its first use (its row counters are left zero by every call). */
 typedef struct {
   sq_mamba2_params ssm;
   int conv_kernel;
@@ -183,6 +185,7 @@ typedef struct {
 } sq_mamba2_decode_params;
 
 int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, int B);
+int sq_mamba2_decode_launches(const sq_mamba2_decode_params* p, int B, int with_gsum);
 int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
                                int8_t* conv_cache /*[B x (Kc-1) x conv_dim]*/, int8_t* state,
                                void* ws, float* y, int64_t ldy, int8_t* yq, int64_t ldyq,

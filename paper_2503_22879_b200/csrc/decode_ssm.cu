@@ -38,11 +38,6 @@ using namespace sm100;
 
 constexpr int DS_P = 64;
 // profiling builds only (-DSQ_DECODE_STAGES=m): bitmask of the launches issued, 1 prep | 2 state | 4 norm
-// -DSQ_DECODE_FUSED=1 selects the one-launch fused step (mamba2_decode_fused_kernel): parity-green
-// but slower than the three launches on B200, so off by default
-#ifndef SQ_DECODE_FUSED
-#define SQ_DECODE_FUSED 0
-#endif
 #ifndef SQ_DECODE_STAGES
 #define SQ_DECODE_STAGES 7
 #endif
@@ -686,50 +681,37 @@ __global__ void __launch_bounds__(256) norm_had8192_kernel(const sq_mamba2_decod
   }
 }
 
-// ------------------------------------------------------------------ fused decode step (one launch)
-// K5d + K9 + K6 in one persistent kernel (N1 decode: no f32 operand workspace, no y round trip
-// through a separate norm launch).  Work units are runs of FU_UH heads of one sequence, dealt to
-// the CTAs round-robin (unit u = blockIdx.x + k * gridDim.x), so each wave of the grid covers
-// consecutive rows and a row's units finish close together.  Warp roles:
-//   warps 0-7    consumers: the scaled-unit int8 state update of state_ring_kernel, y to HBM/L2
-//   warp 8       producer: bulk TMA of the int8 state tile (P x N) into a NSLOT-deep smem ring
-//   warps 9-10   x operands of a tile's 64 channels (alternate tiles): conv-cache stepping + SiLU +
-//                requant to the clustered x scale (prep_kernel's op order), x̂, Δx̂/s_h, SiLU(ẑ),
-//                s_h, Ȧ, D -> slot; the x channels' cache window is written here (one writer each)
-//   warp 11      B̂ | Ĉ of the head's state group (conv + SiLU + requant + dequant), recomputed
-//                when (sequence, group) changes.  A group's cache window is shared by its heads,
-//                so it is rewritten by the CTA whose run completes the per-(sequence, group) count
-//   warp 12      row counter: after the consumers finish a unit it adds the unit's heads to the
-//                row's counter (gpu-scope fence first); the CTA that completes a row queues it,
-//                and the consumers run that row's gated RMSNorm + FWHT + quant at their next
-//                unit boundary.  No CTA ever waits on another, so the grid size is free.
-// Counters live in the caller's workspace (zeroed once, reset by their last user), so the step
+// ------------------------------------------------------------------ K9 + K6: state update with the row norm
+// state_ring_kernel plus the gated RMSNorm + FWHT + quant of each row (N1 in decode: no separate
+// norm launch).  Tiles are dealt round-robin (t = blockIdx.x + i * gridDim.x), so each wave of the
+// grid covers consecutive rows and rows complete progressively.  Warp roles:
+//   warps 0-7   consumers (as state_ring_kernel), y to L2; every RN_CHK tiles they run the norms of
+//               the rows published to this CTA so far
+//   warp 8      producer (as state_ring_kernel)
+//   warp 9      row counter: after the consumers finish a tile it adds 1 to the row's counter
+//               (release: their y stores, observed through the cta-scope acquire, precede it), and
+//               it watches the counters of this CTA's rows (b = blockIdx.x + j * gridDim.x), publishing
+//               each to the consumers once all nh heads are in.  No CTA ever waits on another's
+//               progress except for its own rows' completion, so the grid size is free.
+// Row counters live in the caller's workspace (zeroed once, reset by their norm CTA), so the step
 // is graph-replayable.
-constexpr int FU_CONSUMERS = 16;   // one state row (x N/8 columns) per consumer thread
-constexpr int FU_XW = 4;           // x-operand warps (tiles round-robin: latency hiding)
-constexpr int FU_BCW = 2;          // B̂ | Ĉ warps (alternate units)
-constexpr int FU_MAXG = 128;       // state groups (per-group head counts in smem)
-constexpr int FU_MAXH = 256;       // heads (per-head scalars in smem)
-constexpr int FU_WPROD = FU_CONSUMERS, FU_WX = FU_CONSUMERS + 1, FU_WBC = FU_WX + FU_XW, FU_WCNT = FU_WBC + FU_BCW;
-constexpr int FU_THREADS = (FU_WCNT + 1) * 32;
-constexpr int FU_MAXD = 8192;      // d_inner handled by one CTA's gated norm
-constexpr int FU_UH = 4;           // heads per work unit
-constexpr int FU_QN = 8;           // ring of rows ready for this CTA's norm
+constexpr int RN_CONS = 8;
+constexpr int RN_THREADS = (RN_CONS + 2) * 32;
+constexpr int RN_NSLOT = 7;
+constexpr int RN_MAXD = 8192;   // d_inner normalised by one CTA
+constexpr int RN_QN = 8;        // ring of rows ready for this CTA's norm
+constexpr int RN_CHK = 4;       // tiles between checks for ready rows
 template <int N>
-struct FuCfg {
+struct RnCfg {
   static constexpr int TILE = DS_P * N;
   static constexpr int ROWB = DS_ROWF * 4;
   static constexpr int BCB = 2 * N * 4;
   static constexpr int SLOT = TILE + ROWB + BCB;
-  static constexpr int NSLOT = 10;
-  static constexpr int OFF_NORM = NSLOT * SLOT;
-  static constexpr int OFF_BAR = OFF_NORM + (FU_MAXD + FU_MAXD / 32) * 4;   // norm row, one pad word per 32
-  static constexpr int OFF_CTL = OFF_BAR + 2 * NSLOT * 8;   // units_done, nready, snap[2], handled, rows[QN]
-  static constexpr int OFF_HG = OFF_CTL + 64;                 // heads per state group [FU_MAXG]
-  static_assert((5 + FU_QN) * 4 <= 64, "control words");
-  static constexpr int OFF_HT = OFF_HG + FU_MAXG * 4;         // per head: dt_bias, A, D, rs clamp
-  static constexpr int OFF_HGID = OFF_HT + FU_MAXH * 16;      // per head: state group
-  static constexpr int SMEM = OFF_HGID + FU_MAXH * 4 + 128;
+  static constexpr int OFF_NORM = RN_NSLOT * SLOT;
+  static constexpr int OFF_BAR = OFF_NORM + (RN_MAXD + RN_MAXD / 32) * 4;   // norm row, one pad word per 32
+  static constexpr int OFF_CTL = OFF_BAR + 2 * RN_NSLOT * 8;  // tiles_done, nready, snap[2], handled, rows[QN]
+  static constexpr int SMEM = OFF_CTL + 64 + 128;
+  static_assert((5 + RN_QN) * 4 <= 64, "control words");
   static_assert(SLOT % 16 == 0, "slot alignment");
 };
 
@@ -753,73 +735,22 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   return v;
 }
 
-// one conv channel, Kc = 4, operands preloaded: acc = b + Σ_j w_j·(q_j·s_in) in tap order (IEEE
-// RN, the oracle's order), SiLU, requant to s_out (bit-exact quant8 via the tie re-check)
-__device__ __forceinline__ int conv1_code(float4 w, float si, float bias, float so, const int8_t q[4]) {
-  float acc = bias;
-  acc = __fadd_rn(acc, __fmul_rn(w.x, __fmul_rn((float)q[0], si)));
-  acc = __fadd_rn(acc, __fmul_rn(w.y, __fmul_rn((float)q[1], si)));
-  acc = __fadd_rn(acc, __fmul_rn(w.z, __fmul_rn((float)q[2], si)));
-  acc = __fadd_rn(acc, __fmul_rn(w.w, __fmul_rn((float)q[3], si)));
-  const float v = silu_approx(acc);
-  bool tie = false;
-  int8_t code = quant8_fast(v, rcp_approx(so), tie);
-  if (tie) code = quant8(v, so);
-  return code;
+__host__ __device__ constexpr int rn_lg(int v) { return v <= 1 ? 0 : 1 + rn_lg(v / 2); }
+// FWHT phase schedule: bases S_0 = 0, S_{p+1} = min(S_p + lgE, L - lgE) until S_p + lgE >= L
+__host__ __device__ constexpr int rn_next_s(int s, int lgE, int L) { return s + lgE < L - lgE ? s + lgE : L - lgE; }
+__host__ __device__ constexpr int rn_last_s(int s, int lgE, int L) {
+  return s + lgE >= L ? s : rn_last_s(rn_next_s(s, lgE, L), lgE, L);
 }
-
-#ifdef SQ_FU_TRACE
-// per-CTA timeline (globaltimer ns): start, producer / x / B|C / counter / consumer-loop / drain end,
-// norms run, ns inside norms, ns waiting: producer / x / B|C on empty, consumers on full
-// (profiling builds only)
-__device__ unsigned long long g_fu_tr[1024][13];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define FU_TR(slot, v) g_fu_tr[blockIdx.x & 1023][slot] = (v)
-// CTA 0 event log of its first 64 tiles: producer issue, x arrive, B|C arrive, consumer warp 0
-// got full, consumer warp 0 / warp FU_CONSUMERS-1 released the slot
-__device__ unsigned long long g_fu_ev[64][6];
-__device__ unsigned long long g_fu_nt[8];   // CTA 0's first norm: phase end times
-#define FU_NT(k) \
-  if (blockIdx.x == 0 && threadIdx.x == 0) g_fu_nt[k] = gtime();
-#define FU_EV(i, k) \
-  if (blockIdx.x == 0 && (i) < 64) g_fu_ev[i][k] = gtime();
-#define FU_WAIT(acc, stmt)                  \
-  {                                         \
-    const unsigned long long w0_ = gtime(); \
-    stmt;                                   \
-    acc += gtime() - w0_;                   \
-  }
-#else
-#define FU_TR(slot, v)
-#define FU_WAIT(acc, stmt) stmt;
-#define FU_EV(i, k)
-#define FU_NT(k)
-#endif
-
-// Gated RMSNorm (f64 sum of squares) + FWHT (Sylvester stages in ascending stride, the oracle's
-// order) + quant of row b by the FU_CONSUMERS warps (named barrier 1); y of the row is complete
-// in L2.  di = 256·E (E a power of two <= 32).  Each thread holds E values whose row index bits
-// [s, s + lgE) are the register index: phase 1 (s = 0) is the contiguous load layout, and each
-// later phase moves the next lgE index bits into registers through smem (one pad word per 32:
-// every transposition is bank-conflict free), so every butterfly stage runs in registers.
-__host__ __device__ constexpr int fu_lg(int v) { return v <= 1 ? 0 : 1 + fu_lg(v / 2); }
-// phase schedule: phase bases S_0 = 0, S_{p+1} = min(S_p + lgE, L - lgE) until S_p + lgE >= L
-__host__ __device__ constexpr int fu_next_s(int s, int lgE, int L) { return s + lgE < L - lgE ? s + lgE : L - lgE; }
-__host__ __device__ constexpr int fu_last_s(int s, int lgE, int L) { return s + lgE >= L ? s : fu_last_s(fu_next_s(s, lgE, L), lgE, L); }
-// row index of register e of thread t when the registers hold index bits [S, S + lgE)
+// row index of register e of thread t is base | (e << S) when the registers hold index bits [S, S + lgE)
 template <int S, int lgE>
-__device__ __forceinline__ int fu_base(int t) {
+__device__ __forceinline__ int rn_base(int t) {
   return ((t >> S) << (S + lgE)) | (t & ((1 << S) - 1));
 }
 // FWHT phases from base S (bits below DONE already transformed): butterflies on the register
 // bits, then a conflict-free transposition through smem to the next phase's layout
-template <int E, int S, int DONE>
-__device__ __forceinline__ void fu_fwht(float (&v)[E], int tid, float* nbuf) {
-  constexpr int lgE = fu_lg(E), L = 9 + lgE;
+template <int E, int NT, int S, int DONE>
+__device__ __forceinline__ void rn_fwht(float (&v)[E], int tid, float* nbuf) {
+  constexpr int lgE = rn_lg(E), L = rn_lg(NT) + lgE;
 #pragma unroll
   for (int j = 0; j < lgE; ++j)
     if (S + j >= DONE) {
@@ -832,364 +763,173 @@ __device__ __forceinline__ void fu_fwht(float (&v)[E], int tid, float* nbuf) {
         }
     }
   if constexpr (S + lgE < L) {
-    constexpr int S2 = fu_next_s(S, lgE, L);
-    const int b1 = fu_base<S, lgE>(tid), b2 = fu_base<S2, lgE>(tid);
+    constexpr int S2 = rn_next_s(S, lgE, L);
+    const int b1 = rn_base<S, lgE>(tid), b2 = rn_base<S2, lgE>(tid);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int ix = b1 | (e << S);
       nbuf[ix + (ix >> 5)] = v[e];
     }
-    named_bar(1, FU_CONSUMERS * 32);
+    named_bar(1, NT);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int ix = b2 | (e << S2);
       v[e] = nbuf[ix + (ix >> 5)];
     }
-    named_bar(1, FU_CONSUMERS * 32);   // reads done before the next transposition (or row) writes
-    fu_fwht<E, S2, S + lgE>(v, tid, nbuf);
+    named_bar(1, NT);   // reads done before the next transposition (or row) writes
+    rn_fwht<E, NT, S2, S + lgE>(v, tid, nbuf);
   }
 }
 
 // Gated RMSNorm (f64 sum of squares) + FWHT (Sylvester stages in ascending stride, the oracle's
-// order) + quant of row b by the FU_CONSUMERS warps (named barrier 1); y of the row is complete
-// in L2.  di = 512·E (E a power of two <= 16).  Each thread holds E values whose row index bits
-// [S, S + lgE) are the register index: phase 0 (S = 0) is the contiguous load layout, and each
-// later phase moves the next lgE index bits into registers through smem (one pad word per 32:
-// every transposition is bank-conflict free), so every butterfly runs in registers.  The phase
-// schedule is static (templates), so all index arithmetic folds to per-thread bases.
-template <int E>
-__device__ __noinline__ void fused_row_norm(const float* norm_w, float eps, int hadamard, float s_y, int b,
-                                           const float* y, int64_t ldy, int8_t* yq, int64_t ldyq, float* nbuf) {
-  constexpr int di = E * FU_CONSUMERS * 32, lgE = fu_lg(E), L = 9 + lgE;
-  static_assert((1 << L) == di, "d_inner = 512 * E");
+// order) + quant of row b by NT threads (named barrier 1); y of the row is complete in L2.
+// di = NT·E (E a power of two >= 2).  Each thread holds E values whose row index bits [S, S + lgE)
+// are the register index: phase 0 (S = 0) is the contiguous load layout, and each later phase
+// moves the next lgE index bits into registers through smem (one pad word per 32: every
+// transposition is bank-conflict free), so every butterfly runs in registers.  The phase schedule
+// is static, so the index arithmetic folds to per-thread bases.
+template <int E, int NT>
+__device__ __noinline__ void rn_row_norm(const float* norm_w, float eps, int hadamard, float s_y, int b,
+                                        const float* y, int64_t ldy, int8_t* yq, int64_t ldyq, float* nbuf) {
+  constexpr int di = E * NT, lgE = rn_lg(E), L = rn_lg(NT) + lgE;
+  static_assert(E >= 2 && (1 << L) == di, "d_inner = NT * 2^k");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  FU_NT(0)
   const float* yr = y + (int64_t)b * ldy + tid * E;
-  float v[E], w[E];
-  if constexpr (E >= 4) {
-#pragma unroll
-    for (int e = 0; e < E; e += 4) {
-      const float4 q = __ldcg(reinterpret_cast<const float4*>(yr + e));
-      const float4 g = __ldg(reinterpret_cast<const float4*>(norm_w + tid * E + e));
-      v[e] = q.x; v[e + 1] = q.y; v[e + 2] = q.z; v[e + 3] = q.w;
-      w[e] = g.x; w[e + 1] = g.y; w[e + 2] = g.z; w[e + 3] = g.w;
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      v[e] = __ldcg(yr + e);
-      w[e] = __ldg(norm_w + tid * E + e);
-    }
-  }
+  const float* wr = norm_w + tid * E;
+  float v[E];
   double ss = 0.0;
 #pragma unroll
+  for (int e = 0; e < E; e += 2) {
+    const float2 q = __ldcg(reinterpret_cast<const float2*>(yr + e));
+    v[e] = q.x;
+    v[e + 1] = q.y;
+  }
+#pragma unroll
   for (int e = 0; e < E; ++e) ss += (double)v[e] * (double)v[e];
-  FU_NT(1)
   ss = warp_sum_d(ss);
   double* red = reinterpret_cast<double*>(nbuf);   // nbuf is free until the FWHT stage
   if (lane == 0) red[warp] = ss;
-  named_bar(1, FU_CONSUMERS * 32);
+  named_bar(1, NT);
   double tot = 0.0;
 #pragma unroll
-  for (int k = 0; k < FU_CONSUMERS; ++k) tot += red[k];
-  named_bar(1, FU_CONSUMERS * 32);
+  for (int k = 0; k < NT / 32; ++k) tot += red[k];
+  named_bar(1, NT);
   const float ms = (float)(tot / (double)di);
   const float rfac = __fdiv_rn(1.0f, sqrtf(__fadd_rn(ms, eps)));
 #pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = __fmul_rn(__fmul_rn(v[e], rfac), w[e]);
-  FU_NT(2)
+  for (int e = 0; e < E; e += 2) {
+    const float2 g = __ldg(reinterpret_cast<const float2*>(wr + e));
+    v[e] = __fmul_rn(__fmul_rn(v[e], rfac), g.x);
+    v[e + 1] = __fmul_rn(__fmul_rn(v[e + 1], rfac), g.y);
+  }
   int8_t* out = yq + (int64_t)b * ldyq;
   const float inv = __frcp_rn(s_y);
   if (hadamard) {
-    if constexpr (E == 1) {   // one value per thread: every stage through smem
-      nbuf[tid] = v[0];
-      named_bar(1, FU_CONSUMERS * 32);
-#pragma unroll 1
-      for (int hh = 1; hh < di; hh <<= 1) {
-        if (tid < di / 2) {
-          const int i0 = (tid / hh) * 2 * hh + (tid % hh);
-          const float x0 = nbuf[i0], x1 = nbuf[i0 + hh];
-          nbuf[i0] = __fadd_rn(x0, x1);
-          nbuf[i0 + hh] = __fsub_rn(x0, x1);
-        }
-        named_bar(1, FU_CONSUMERS * 32);
-      }
-      v[0] = nbuf[tid];
-      named_bar(1, FU_CONSUMERS * 32);
-      FU_NT(3)
-      out[tid] = quant8_inv(v[0], s_y, inv);
-    } else {
-      fu_fwht<E, 0, 0>(v, tid, nbuf);
-      FU_NT(3)
-      constexpr int SL = fu_last_s(0, lgE, L);
-      const int bl = fu_base<SL, lgE>(tid);
+    rn_fwht<E, NT, 0, 0>(v, tid, nbuf);
+    constexpr int SL = rn_last_s(0, lgE, L);
+    const int bl = rn_base<SL, lgE>(tid);
 #pragma unroll
-      for (int e = 0; e < E; ++e) out[bl | (e << SL)] = quant8_inv(v[e], s_y, inv);
-    }
+    for (int e = 0; e < E; ++e) out[bl | (e << SL)] = quant8_inv(v[e], s_y, inv);
   } else {
 #pragma unroll
     for (int e = 0; e < E; ++e) out[tid * E + e] = quant8_inv(v[e], s_y, inv);
   }
-  FU_NT(4)
 }
 
+#ifdef SQ_RN_TRACE
+// per-CTA timeline (globaltimer ns; profiling builds only): start, consumer loop end, drain end,
+// ns in norms, counter warp end, counter warp ns in the gpu-scope ops, norms run
+__device__ unsigned long long g_rn_tr[1024][8];
+__device__ __forceinline__ unsigned long long rn_time() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define RN_TR(k, v) g_rn_tr[blockIdx.x & 1023][k] = (v)
+#endif
+
 template <int N>
-__global__ void __launch_bounds__(FU_THREADS, 1)
-    mamba2_decode_fused_kernel(const sq_mamba2_decode_params P, int B, const int8_t* zx, int64_t ldzx,
-                               int8_t* conv_cache, int8_t* state, int* cnt, float* y, int64_t ldy, int8_t* yq,
-                               int64_t ldyq) {
-  using Cfg = FuCfg<N>;
+__global__ void __launch_bounds__(RN_THREADS, 2)
+    state_ring_norm_kernel(const sq_mamba2_decode_params P, int B, const float* __restrict__ ws,
+                           int8_t* __restrict__ state, float* y, int64_t ldy, int8_t* yq, int64_t ldyq,
+                           int* cnt_row) {
+  using Cfg = RnCfg<N>;
   const sq_mamba2_params& S = P.ssm;
-  constexpr int CPT = N / 8, VW = CPT / 4;
+  constexpr int CPT = N / 8;   // state columns per thread
+  constexpr int VW = CPT / 4;  // 32-bit words per row piece
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint64_t* empty = full + Cfg::NSLOT;
+  uint64_t* empty = full + RN_NSLOT;
   uint32_t* ctl = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_CTL);
-  uint32_t* units_done = ctl;   // consumer warps x units finished (monotonic)
+  uint32_t* tiles_done = ctl;   // consumer warps x tiles finished (monotonic)
   uint32_t* nready = ctl + 1;   // rows published to this CTA's norm ring (monotonic)
-  uint32_t* snap = ctl + 2;     // [2] consumer-agreed nready snapshots (double-buffered per unit)
-  uint32_t* handled_pub = ctl + 4;                 // rows normalised (frees ring entries)
-  int* rows = reinterpret_cast<int*>(ctl + 5);     // [FU_QN] ring of rows ready for the norm
+  uint32_t* snap = ctl + 2;     // [2] consumer-agreed nready snapshots (double-buffered)
+  uint32_t* handled_pub = ctl + 4;              // rows normalised (frees ring entries)
+  int* rows = reinterpret_cast<int*>(ctl + 5);  // [RN_QN] rows ready for the norm
   float* nbuf = reinterpret_cast<float*>(smem + Cfg::OFF_NORM);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nh = S.n_heads, G = S.n_groups, di = nh * DS_P, GN = G * N, C = di + 2 * GN;
-  const int nhb = (nh + FU_UH - 1) / FU_UH, nunits = B * nhb;
-  int* cnt_bg = cnt;            // [B * G]
-  int* cnt_row = cnt + B * G;   // [B]
+  const int nh = S.n_heads, di = nh * DS_P;
+  const int ntiles_all = B * nh;
+  const int ntiles = (ntiles_all - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int my_rows = (int)blockIdx.x < B ? (B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   pdl_trigger();
   if (tid == 0) {
-    for (int s = 0; s < Cfg::NSLOT; ++s) {
-      mbar_init(&full[s], 3);                // producer (tx) + x-operand warp + B|C warp
-      mbar_init(&empty[s], FU_CONSUMERS);
+    for (int i = 0; i < RN_NSLOT; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], RN_CONS);
     }
     ctl[0] = ctl[1] = ctl[2] = ctl[3] = ctl[4] = 0;
     fence_barrier_init();
   }
-  int* hgc = reinterpret_cast<int*>(smem + Cfg::OFF_HG);
-  if (tid < FU_MAXG) hgc[tid] = 0;
   __syncthreads();
-  float4* ht = reinterpret_cast<float4*>(smem + Cfg::OFF_HT);
-  // per-head tables (weights: safe before the grid dependency wait)
-  if (warp == FU_WBC)
-    for (int hh = lane; hh < nh; hh += 32) atomicAdd(&hgc[__ldg(S.head_group + hh)], 1);
-  int* hgid = reinterpret_cast<int*>(smem + Cfg::OFF_HGID);
-  if (tid < nh) hgid[tid] = __ldg(S.head_group + tid);
-  if (tid < nh)
-    ht[tid] = make_float4(__ldg(S.dt_bias + tid), __ldg(S.A + tid), __ldg(S.D + tid),
-                          2097152.0f / (128.0f * __ldg(S.s_B + __ldg(S.head_group + tid))));
-  __syncthreads();
-  pdl_wait();   // zx from in_proj; state / caches last written by earlier grids
-#ifdef SQ_FU_TRACE
-  if (tid == 0) FU_TR(0, gtime());
-  unsigned long long wt = 0;
+  pdl_wait();   // prep outputs (ws), the state and y / yq: produced / last used by earlier grids
+#ifdef SQ_RN_TRACE
+  if (tid == 0) RN_TR(0, rn_time());
+  unsigned long long tacc = 0;
 #endif
-  if (warp == FU_WPROD) {
-    // ---------------- producer: the int8 state tiles
+  const float* bc_all = ws + ds_rows_floats(B, nh);
+  if (warp == RN_CONS) {
+    // ---------------- producer: state tile + row scalars + B̂|Ĉ of the head's group
     if (lane == 0) {
-      for (int u = blockIdx.x, k = 0, i = 0; u < nunits; u += gridDim.x, ++k) {
-        const int b = u / nhb, h0 = (u - b * nhb) * FU_UH, h1 = min(nh, h0 + FU_UH);
-        for (int h = h0; h < h1; ++h, ++i) {
-        const int slot = i % Cfg::NSLOT;
-        if (i >= Cfg::NSLOT) FU_WAIT(wt, mbar_wait(&empty[slot], ((i / Cfg::NSLOT) - 1) & 1))
-        FU_EV(i, 0)
-        mbar_arrive_expect_tx(&full[slot], Cfg::TILE);
-        bulk_load(smem + slot * Cfg::SLOT, state + ((int64_t)b * nh + h) * Cfg::TILE, Cfg::TILE, &full[slot]);
-        }
+      for (int i = 0; i < ntiles; ++i) {
+        const int t = blockIdx.x + i * gridDim.x;
+        const int b = t / nh, h = t % nh;
+        const int slot = i % RN_NSLOT;
+        if (i >= RN_NSLOT) mbar_wait(&empty[slot], ((i / RN_NSLOT) - 1) & 1);
+        uint8_t* dst = smem + slot * Cfg::SLOT;
+        mbar_arrive_expect_tx(&full[slot], Cfg::SLOT);
+        bulk_load(dst, state + (int64_t)t * Cfg::TILE, Cfg::TILE, &full[slot]);
+        bulk_load(dst + Cfg::TILE, ws + (int64_t)t * DS_ROWF, Cfg::ROWB, &full[slot]);
+        bulk_load(dst + Cfg::TILE + Cfg::ROWB, bc_all + ((int64_t)b * S.n_groups + S.head_group[h]) * 2 * N,
+                  Cfg::BCB, &full[slot]);
       }
-#ifdef SQ_FU_TRACE
-      FU_TR(1, gtime());
-      FU_TR(9, wt);
-#endif
     }
     return;
   }
-  if (warp >= FU_WX && warp < FU_WX + FU_XW) {
-    // ---------------- x operands of the tile's 64 channels (2 per lane); tiles alternate warps
-    const int xw = warp - FU_WX;
-    for (int u = blockIdx.x, k = 0, i = 0; u < nunits; u += gridDim.x, ++k) {
-      const int b = u / nhb, h0 = (u - b * nhb) * FU_UH, h1 = min(nh, h0 + FU_UH);
-      for (int h = h0; h < h1; ++h, ++i) {
-      if (i % FU_XW != xw) continue;
-      const int8_t* zrow = zx + (int64_t)b * ldzx;
-      int8_t* cache_b = conv_cache + (int64_t)b * 3 * C;
-      const int p0 = 2 * lane, c = h * DS_P + p0;
-      // every global operand first (independent loads in flight together)
-      const uint16_t c0 = *reinterpret_cast<const uint16_t*>(cache_b + c);
-      const uint16_t c1 = *reinterpret_cast<const uint16_t*>(cache_b + C + c);
-      const uint16_t c2 = *reinterpret_cast<const uint16_t*>(cache_b + 2 * C + c);
-      const uint16_t xn = *reinterpret_cast<const uint16_t*>(zrow + di + c);
-      const uint16_t zc = *reinterpret_cast<const uint16_t*>(zrow + c);
-      const int8_t dcode = zrow[2 * di + 2 * GN + h];
-      const float4 w0 = __ldg(reinterpret_cast<const float4*>(P.conv_w) + c);
-      const float4 w1 = __ldg(reinterpret_cast<const float4*>(P.conv_w) + c + 1);
-      const float2 si = __ldg(reinterpret_cast<const float2*>(P.conv_s_in + c));
-      const float2 bi = __ldg(reinterpret_cast<const float2*>(P.conv_b + c));
-      const float2 so = __ldg(reinterpret_cast<const float2*>(P.conv_s_out + c));
-      const float2 sh = __ldg(reinterpret_cast<const float2*>(S.s_h + c));
-      const int slot = i % Cfg::NSLOT;
-      if (i >= Cfg::NSLOT) FU_WAIT(wt, mbar_wait(&empty[slot], ((i / Cfg::NSLOT) - 1) & 1))
-      float* rf = reinterpret_cast<float*>(smem + slot * Cfg::SLOT + Cfg::TILE);
-      const float4 hp = ht[h];   // dt_bias, A, D, rs clamp
-      const float delta = softplus_f(__fadd_rn(__fmul_rn((float)dcode, S.s_dt), hp.x));
-      const float rsmax = hp.w;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int8_t q[4] = {(int8_t)(c0 >> (8 * e)), (int8_t)(c1 >> (8 * e)), (int8_t)(c2 >> (8 * e)),
-                             (int8_t)(xn >> (8 * e))};
-        const float soe = e ? so.y : so.x, she = e ? sh.y : sh.x;
-        const int code = conv1_code(e ? w1 : w0, e ? si.y : si.x, e ? bi.y : bi.x, soe, q);
-        const float xh = __fmul_rn((float)code, soe);
-        rf[p0 + e] = xh;
-        rf[DS_P + p0 + e] = fminf(fmaxf(__fmul_rn(__fmul_rn(delta, xh), __frcp_rn(she)), -rsmax), rsmax);
-        rf[2 * DS_P + p0 + e] = silu_approx(__fmul_rn((float)(int8_t)(zc >> (8 * e)), S.s_z));
-        rf[3 * DS_P + p0 + e] = she;
-      }
-      if (lane == 0) {
-        rf[4 * DS_P] = expf(__fmul_rn(delta, hp.y));
-        rf[4 * DS_P + 1] = hp.z;
-      }
-      // shift the x channels' cache window (this tile is their only reader and writer)
-      *reinterpret_cast<uint16_t*>(cache_b + c) = c1;
-      *reinterpret_cast<uint16_t*>(cache_b + C + c) = c2;
-      *reinterpret_cast<uint16_t*>(cache_b + 2 * C + c) = xn;
-      __syncwarp();
-      if (lane == 0) {
-        FU_EV(i, 1)
-        mbar_arrive(&full[slot]);
-      }
-      }
-    }
-#ifdef SQ_FU_TRACE
+  if (warp == RN_CONS + 1) {
+    // ---------------- row counter
     if (lane == 0) {
-      FU_TR(2, gtime());
-      FU_TR(10, wt);
-    }
-#endif
-    return;
-  }
-  if (warp >= FU_WBC && warp < FU_WBC + FU_BCW) {
-    // ---------------- B̂ | Ĉ of the head's state group (N / 32 channels of B and of C per lane);
-    // units alternate between the FU_BCW warps
-    constexpr int PL = N / 32;
-    const int bw = warp - FU_WBC;
-    float bv[PL], cv[PL];
-    int cur_b = -1, cur_g = -1, run = 0;
-    // a (sequence, group) run ends: count its heads; the run that completes the group's count
-    // is the last reader of the group's old cache window and shifts it
-    auto flush = [&]() {
-      if (run == 0) return;
-      int last = 0;
-      if (lane == 0) {
-        __threadfence();
-        last = atomicAdd(&cnt_bg[cur_b * G + cur_g], run) + run == hgc[cur_g];
-        if (last) cnt_bg[cur_b * G + cur_g] = 0;
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        int8_t* cache_b = conv_cache + (int64_t)cur_b * 3 * C;
-        const int8_t* zrow = zx + (int64_t)cur_b * ldzx + di;
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk)
-#pragma unroll
-          for (int e = 0; e < PL; ++e) {
-            const int cc = di + kk * GN + cur_g * N + lane + 32 * e;
-            const int8_t a1 = cache_b[C + cc], a2 = cache_b[2 * C + cc], an = zrow[cc];
-            cache_b[cc] = a1;
-            cache_b[C + cc] = a2;
-            cache_b[2 * C + cc] = an;
-          }
-      }
-      run = 0;
-    };
-    for (int u = blockIdx.x, k = 0, i = 0; u < nunits; u += gridDim.x, ++k) {
-      const int b = u / nhb, h0 = (u - b * nhb) * FU_UH, h1 = min(nh, h0 + FU_UH);
-      if (k % FU_BCW != bw) {
-        i += h1 - h0;
-        continue;
-      }
-      for (int h = h0; h < h1; ++h, ++i) {
-        const int g = __ldg(S.head_group + h);
-        if (b != cur_b || g != cur_g) {
-          flush();
-          int8_t* cache_b = conv_cache + (int64_t)b * 3 * C;
-          const int8_t* zrow = zx + (int64_t)b * ldzx + di;
-#pragma unroll
-          for (int kk = 0; kk < 2; ++kk) {   // B then C: operands of the lane's PL channels first
-            int8_t q[PL][4];
-            float4 w[PL];
-            float si[PL], bi[PL], so[PL];
-#pragma unroll
-            for (int e = 0; e < PL; ++e) {
-              const int cc = di + kk * GN + g * N + lane + 32 * e;
-              q[e][0] = cache_b[cc];
-              q[e][1] = cache_b[C + cc];
-              q[e][2] = cache_b[2 * C + cc];
-              q[e][3] = zrow[cc];
-              w[e] = __ldg(reinterpret_cast<const float4*>(P.conv_w) + cc);
-              si[e] = __ldg(P.conv_s_in + cc);
-              bi[e] = __ldg(P.conv_b + cc);
-              so[e] = __ldg(P.conv_s_out + cc);
-            }
-#pragma unroll
-            for (int e = 0; e < PL; ++e) {
-              const float v = __fmul_rn((float)conv1_code(w[e], si[e], bi[e], so[e], q[e]), so[e]);
-              if (kk == 0) bv[e] = v; else cv[e] = v;
-            }
-          }
-          cur_b = b;
-          cur_g = g;
-        }
-        const int slot = i % Cfg::NSLOT;
-        if (i >= Cfg::NSLOT) FU_WAIT(wt, mbar_wait(&empty[slot], ((i / Cfg::NSLOT) - 1) & 1))
-        float* bcs = reinterpret_cast<float*>(smem + slot * Cfg::SLOT + Cfg::TILE + Cfg::ROWB);
-#pragma unroll
-        for (int e = 0; e < PL; ++e) {
-          bcs[bc_swz(lane + 32 * e, N)] = bv[e];
-          bcs[N + bc_swz(lane + 32 * e, N)] = cv[e];
-        }
-        __syncwarp();
-        if (lane == 0) {
-          FU_EV(i, 2)
-          mbar_arrive(&full[slot]);
-        }
-        ++run;
-      }
-    }
-    flush();
-#ifdef SQ_FU_TRACE
-    if (lane == 0 && bw == 0) {
-      FU_TR(3, gtime());
-      FU_TR(11, wt);
-    }
-#endif
-    return;
-  }
-  // rows normalised by this CTA: b = blockIdx.x + j * gridDim.x (spread over the grid, at most
-  // ceil(B / grid) each, whichever CTA completes them)
-  const int my_rows = (int)blockIdx.x < B ? (B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-  if (warp == FU_WCNT) {
-    // ---------------- row counter: after the consumers finish unit k, add its heads to the row's
-    // counter (release: their y stores, observed through the cta-scope acquire, precede it); and
-    // watch the counters of this CTA's rows, publishing each to the consumers once complete
-    if (lane == 0) {
-      const int K = (nunits - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
       int k = 0, j = 0;
       uint32_t published = 0;
-      while (k < K || j < my_rows) {
+      while (k < ntiles || j < my_rows) {
         bool moved = false;
-        if (k < K && ld_acquire_cta(units_done) >= (uint32_t)(FU_CONSUMERS * (k + 1))) {
-          const int u = (int)blockIdx.x + k * (int)gridDim.x;
-          const int b = u / nhb, h0 = (u - b * nhb) * FU_UH, h1 = min(nh, h0 + FU_UH);
-          red_add_release_gpu(&cnt_row[b], h1 - h0);
+        if (k < ntiles && ld_acquire_cta(tiles_done) >= (uint32_t)(RN_CONS * (k + 1))) {
+#ifdef SQ_RN_TRACE
+          const unsigned long long t0 = rn_time();
+#endif
+          red_add_release_gpu(&cnt_row[((int)blockIdx.x + k * (int)gridDim.x) / nh], 1);
+#ifdef SQ_RN_TRACE
+          tacc += rn_time() - t0;
+#endif
           ++k;
           moved = true;
         }
-        if (j < my_rows && published - ld_acquire_cta(handled_pub) < (uint32_t)FU_QN) {
+        if (j < my_rows && published - ld_acquire_cta(handled_pub) < (uint32_t)RN_QN) {
           const int rb = (int)blockIdx.x + j * (int)gridDim.x;
           if (ld_acquire_gpu(&cnt_row[rb]) >= nh) {   // acquire: every CTA's y stores of row rb
             cnt_row[rb] = 0;                           // self-reset for the next launch
-            rows[published % FU_QN] = rb;
+            rows[published % RN_QN] = rb;
             st_release_cta(nready, ++published);
             ++j;
             moved = true;
@@ -1197,145 +937,142 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
         }
         if (!moved) __nanosleep(64);
       }
-#ifdef SQ_FU_TRACE
-      FU_TR(4, gtime());
+#ifdef SQ_RN_TRACE
+      RN_TR(4, rn_time());
+      RN_TR(5, tacc);
 #endif
     }
     return;
   }
-  // ---------------- consumers: thread = (state row R, column chunk)
-  const int chunk = tid & 7, R = tid >> 3;
-  const float2 MG = make_float2(-8388736.0f, -8388736.0f);
-  const float2 RM = make_float2(12582912.0f, 12582912.0f);
-  const uint32_t full0 = smem_u32(full);
+  // ---------------- consumers: thread = (row quad rq, column chunk); rows rq and rq + 32
   int handled = 0;
-#ifdef SQ_FU_TRACE
-  unsigned long long nn = 0, nt = 0;
-#endif
-  // norms of the published rows [handled, upto) (consumer-uniform); frees their ring entries
   auto run_norms = [&](int upto) {
     for (; handled < upto; ++handled) {
-#ifdef SQ_FU_TRACE
-      const unsigned long long t0 = gtime();
+      const int rb = rows[handled % RN_QN];
+#ifdef SQ_RN_TRACE
+      const unsigned long long t0 = rn_time();
 #endif
-      const int rb = rows[handled % FU_QN];
-      switch (di / (FU_CONSUMERS * 32)) {   // values per consumer thread (fused d_inner = 512 * 2^k)
-        case 1: fused_row_norm<1>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-        case 2: fused_row_norm<2>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-        case 4: fused_row_norm<4>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-        case 8: fused_row_norm<8>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-        default: fused_row_norm<16>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
+      switch (di / (RN_CONS * 32)) {   // values per consumer thread (d_inner = 256 * 2^k)
+        case 2: rn_row_norm<2, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
+        case 4: rn_row_norm<4, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
+        case 8: rn_row_norm<8, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
+        case 16: rn_row_norm<16, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
+        default: rn_row_norm<32, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
       }
-#ifdef SQ_FU_TRACE
-      nn += 1;
-      nt += gtime() - t0;
+#ifdef SQ_RN_TRACE
+      tacc += rn_time() - t0;
 #endif
       if (tid == 0) st_release_cta(handled_pub, (uint32_t)(handled + 1));
     }
   };
-  int cb = -1, cg = -1;            // (sequence, group) whose B̂ | Ĉ the registers hold
-  float2 bv[CPT / 2], cv[CPT / 2];
-  for (int u = blockIdx.x, k = 0, i = 0; u < nunits; u += gridDim.x, ++k) {
-    const int b = u / nhb, h0 = (u - b * nhb) * FU_UH, h1 = min(nh, h0 + FU_UH);
-    for (int h = h0; h < h1; ++h, ++i) {
-      const int t = b * nh + h;
-      const int slot = i % Cfg::NSLOT;
-      const uint8_t* sl = smem + slot * Cfg::SLOT;
-      const float* rf = reinterpret_cast<const float*>(sl + Cfg::TILE);
-      const float* bcs = reinterpret_cast<const float*>(sl + Cfg::TILE + Cfg::ROWB);
-      FU_WAIT(wt, mbar_wait_addr(full0 + slot * 8, (i / Cfg::NSLOT) & 1))
-      if (tid == 0) { FU_EV(i, 3) }
-      if (const int g = hgid[h]; b != cb || g != cg) {   // B̂ | Ĉ change with (sequence, group) only
+  const int chunk = tid & 7, rq = tid >> 3;
+  const float2 MG = make_float2(-8388736.0f, -8388736.0f);
+  const float2 RM = make_float2(12582912.0f, 12582912.0f);
+  const int gstep = gridDim.x;
+  const int db = gstep / nh, dh = gstep % nh;   // tile t -> (b, h) advanced incrementally
+  int b = blockIdx.x / nh, h = blockIdx.x % nh;
+  const uint32_t full0 = smem_u32(full);
+  for (int i = 0; i < ntiles; ++i) {
+    const int t = b * nh + h;
+    const int slot = i % RN_NSLOT;
+    const uint8_t* sl = smem + slot * Cfg::SLOT;
+    const float* rf = reinterpret_cast<const float*>(sl + Cfg::TILE);
+    const float* bcs = reinterpret_cast<const float*>(sl + Cfg::TILE + Cfg::ROWB);
+    mbar_wait_addr(full0 + slot * 8, (i / RN_NSLOT) & 1);
+    float2 bv[CPT / 2], cv[CPT / 2];
 #pragma unroll
-        for (int e = 0; e < CPT / 4; ++e) {
-          const float4 b4 = *reinterpret_cast<const float4*>(bcs + ((e * 8 + chunk) << 2));
-          const float4 c4 = *reinterpret_cast<const float4*>(bcs + N + ((e * 8 + chunk) << 2));
-          bv[e * 2] = make_float2(b4.x, b4.y);
-          bv[e * 2 + 1] = make_float2(b4.z, b4.w);
-          cv[e * 2] = make_float2(c4.x, c4.y);
-          cv[e * 2 + 1] = make_float2(c4.z, c4.w);
-        }
-        cb = b;
-        cg = g;
-      }
-      const float dA = rf[4 * DS_P], Dh = rf[4 * DS_P + 1];
-      const float2 dA2 = make_float2(dA, dA);
-      int8_t* st = state + (int64_t)t * Cfg::TILE + chunk * CPT;
-      {
-        const float rs = rf[DS_P + R];
-        const float2 rs2 = make_float2(rs, rs);
-        uint32_t raw[VW];
-        if constexpr (VW == 4) {
-          const uint4 v = *reinterpret_cast<const uint4*>(sl + R * N + chunk * CPT);
-          raw[0] = v.x; raw[1] = v.y; raw[2] = v.z; raw[3] = v.w;
-        } else {
-          const uint2 v = *reinterpret_cast<const uint2*>(sl + R * N + chunk * CPT);
-          raw[0] = v.x; raw[1] = v.y;
-        }
-        uint32_t outw[VW];
-        float2 acc2 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int e = 0; e < VW; ++e) {
-          const uint32_t uu = raw[e] ^ 0x80808080u;
-          int qi[4];
-#pragma unroll
-          for (int i2 = 0; i2 < 4; i2 += 2) {
-            const int n2 = e * 2 + i2 / 2;
-            const float2 hq = __fadd2_rn(make_float2(s8_raw(uu, i2), s8_raw(uu, i2 + 1)), MG);
-            const float2 tt = __ffma2_rn(dA2, hq, __fmul2_rn(rs2, bv[n2]));
-            acc2 = __ffma2_rn(tt, cv[n2], acc2);
-            const float2 rr = __fadd2_rn(tt, RM);   // bits = 0x4B400000 + rint(t), |t| < 2^22
-            qi[i2] = __float_as_int(rr.x) - 0x4B400000;
-            qi[i2 + 1] = __float_as_int(rr.y) - 0x4B400000;
-          }
-          outw[e] = pack4_sat(qi[0], qi[1], qi[2], qi[3]);
-        }
-        if constexpr (VW == 4)
-          *reinterpret_cast<uint4*>(st + R * N) = make_uint4(outw[0], outw[1], outw[2], outw[3]);
-        else
-          *reinterpret_cast<uint2*>(st + R * N) = make_uint2(outw[0], outw[1]);
-        float acc = __fadd_rn(acc2.x, acc2.y);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-        if (chunk == 0)
-          y[(int64_t)b * ldy + h * DS_P + R] =
-              __fmul_rn(__fadd_rn(__fmul_rn(rf[3 * DS_P + R], acc), __fmul_rn(Dh, rf[R])), rf[2 * DS_P + R]);
-      }
-      fence_proxy_async_smem();   // our generic reads of the slot precede the next bulk copy into it
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (tid == 0) { FU_EV(i, 4) }
-      if (tid == FU_CONSUMERS * 32 - 32) { FU_EV(i, 5) }
+    for (int e = 0; e < CPT / 4; ++e) {
+      const float4 b4 = *reinterpret_cast<const float4*>(bcs + ((e * 8 + chunk) << 2));
+      const float4 c4 = *reinterpret_cast<const float4*>(bcs + N + ((e * 8 + chunk) << 2));
+      bv[e * 2] = make_float2(b4.x, b4.y);
+      bv[e * 2 + 1] = make_float2(b4.z, b4.w);
+      cv[e * 2] = make_float2(c4.x, c4.y);
+      cv[e * 2 + 1] = make_float2(c4.z, c4.w);
     }
-    // unit k done: hand it to the row counter, then run the norms of the rows published so far
+    const float dA = rf[4 * DS_P], Dh = rf[4 * DS_P + 1];
+    const float2 dA2 = make_float2(dA, dA);
+    int8_t* st = state + (int64_t)t * Cfg::TILE + chunk * CPT;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int R = rq + 32 * k;
+      const float rs = rf[DS_P + R];
+      const float2 rs2 = make_float2(rs, rs);
+      uint32_t raw[VW];
+      if constexpr (VW == 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(sl + R * N + chunk * CPT);
+        raw[0] = v.x; raw[1] = v.y; raw[2] = v.z; raw[3] = v.w;
+      } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(sl + R * N + chunk * CPT);
+        raw[0] = v.x; raw[1] = v.y;
+      }
+      uint32_t outw[VW];
+      float2 acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int e = 0; e < VW; ++e) {
+        const uint32_t u = raw[e] ^ 0x80808080u;
+        int qi[4];
+#pragma unroll
+        for (int i2 = 0; i2 < 4; i2 += 2) {
+          const int n2 = e * 2 + i2 / 2;
+          const float2 hq = __fadd2_rn(make_float2(s8_raw(u, i2), s8_raw(u, i2 + 1)), MG);
+          const float2 tt = __ffma2_rn(dA2, hq, __fmul2_rn(rs2, bv[n2]));
+          acc2 = __ffma2_rn(tt, cv[n2], acc2);
+          const float2 rr = __fadd2_rn(tt, RM);   // bits = 0x4B400000 + rint(t), |t| < 2^22
+          qi[i2] = __float_as_int(rr.x) - 0x4B400000;
+          qi[i2 + 1] = __float_as_int(rr.y) - 0x4B400000;
+        }
+        outw[e] = pack4_sat(qi[0], qi[1], qi[2], qi[3]);
+      }
+      if constexpr (VW == 4)
+        *reinterpret_cast<uint4*>(st + R * N) = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+      else
+        *reinterpret_cast<uint2*>(st + R * N) = make_uint2(outw[0], outw[1]);
+      float acc = __fadd_rn(acc2.x, acc2.y);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (chunk == 0)
+        y[(int64_t)b * ldy + h * DS_P + R] =
+            __fmul_rn(__fadd_rn(__fmul_rn(rf[3 * DS_P + R], acc), __fmul_rn(Dh, rf[R])), rf[2 * DS_P + R]);
+    }
+    fence_proxy_async_smem();   // our generic reads of the slot precede the next bulk copy into it
     __syncwarp();
-    if (lane == 0) red_add_release_cta(units_done, 1);
-    if (tid == 0) snap[k & 1] = ld_acquire_cta(nready);
-    named_bar(1, FU_CONSUMERS * 32);
-    run_norms((int)snap[k & 1]);
+    if (lane == 0) {
+      mbar_arrive(&empty[slot]);
+      red_add_release_cta(tiles_done, 1);   // this warp's y stores precede the row count
+    }
+    h += dh;
+    b += db;
+    if (h >= nh) {
+      h -= nh;
+      ++b;
+    }
+    if (i % RN_CHK == RN_CHK - 1) {   // run the norms of the rows published so far
+      if (tid == 0) snap[(i / RN_CHK) & 1] = ld_acquire_cta(nready);
+      named_bar(1, RN_CONS * 32);
+      run_norms((int)snap[(i / RN_CHK) & 1]);
+    }
   }
   // drain: this CTA's remaining rows, as they complete
-#ifdef SQ_FU_TRACE
-  if (tid == 0) FU_TR(5, gtime());
+#ifdef SQ_RN_TRACE
+  if (tid == 0) RN_TR(1, rn_time());
 #endif
-  named_bar(1, FU_CONSUMERS * 32);   // every consumer read its last snapshot
+  named_bar(1, RN_CONS * 32);   // every consumer read its last snapshot
   while (handled < my_rows) {
     if (tid == 0) {
       while ((int)ld_acquire_cta(nready) <= handled) __nanosleep(64);
       snap[0] = ld_acquire_cta(nready);
     }
-    named_bar(1, FU_CONSUMERS * 32);
+    named_bar(1, RN_CONS * 32);
     const int upto = (int)snap[0];
-    named_bar(1, FU_CONSUMERS * 32);
+    named_bar(1, RN_CONS * 32);
     run_norms(upto);
   }
-#ifdef SQ_FU_TRACE
+#ifdef SQ_RN_TRACE
   if (tid == 0) {
-    FU_TR(6, gtime());
-    FU_TR(7, nn);
-    FU_TR(8, nt);
-    FU_TR(12, wt);
+    RN_TR(2, rn_time());
+    RN_TR(3, tacc);
+    RN_TR(6, handled);
   }
 #endif
 }
@@ -1344,28 +1081,37 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
 
 using namespace sq;
 
-#ifdef SQ_FU_TRACE
-extern "C" int sq_probe_fu_trace(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, sq::g_fu_tr, sizeof(sq::g_fu_tr)) == cudaSuccess ? 0 : -3;
-}
-extern "C" int sq_probe_fu_norm(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, sq::g_fu_nt, sizeof(sq::g_fu_nt)) == cudaSuccess ? 0 : -3;
-}
-extern "C" int sq_probe_fu_events(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, sq::g_fu_ev, sizeof(sq::g_fu_ev)) == cudaSuccess ? 0 : -3;
+
+#ifdef SQ_RN_TRACE
+extern "C" int sq_probe_rn_trace(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, sq::g_rn_tr, sizeof(sq::g_rn_tr)) == cudaSuccess ? 0 : -3;
 }
 #endif
 
-// Workspace: [f32 operands of the three-launch path][int32 counters of the fused path: B*G
-// (sequence, group) + B rows].  The counter region must be zero before the first call; the fused
-// kernel leaves it zero (each counter is reset by its last user).
+// Workspace: [f32 operands written by prep_kernel][int32 row counters of state_ring_norm_kernel, B].
+// The counter region must be zero before the first call; the kernel leaves it zero (each counter
+// is reset by the CTA that normalises its row).
 static int64_t ds_counter_off(int B, const sq_mamba2_params& S) {
   return ((ds_ws_floats(B, S.n_heads, S.n_groups, S.d_state) * 4 + 255) / 256) * 256;
 }
 
 extern "C" int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, int B) {
   if (!p || B < 0) return -1;
-  return ds_counter_off(B, p->ssm) + (int64_t)(B * p->ssm.n_groups + B) * 4;
+  return ds_counter_off(B, p->ssm) + (int64_t)B * 4;
+}
+
+// the row norm runs inside the state kernel when d_inner = 256 * 2^k (<= 8192) and no group sums
+static bool ds_norm_fused(const sq_mamba2_decode_params* p, int with_gsum) {
+  const int di = p->ssm.n_heads * DS_P, e = di / (RN_CONS * 32);
+  return !with_gsum && di <= RN_MAXD && di % (RN_CONS * 32) == 0 && e >= 2 && (e & (e - 1)) == 0;
+}
+
+extern "C" int sq_mamba2_decode_launches(const sq_mamba2_decode_params* p, int B, int with_gsum) {
+  if (!p || B < 0) return -1;
+  if (B == 0) return 0;
+  if (ds_norm_fused(p, with_gsum)) return 2;
+  const int di = p->ssm.n_heads * DS_P;
+  return 3 + (with_gsum && !(di == 8192 && p->hadamard));
 }
 
 extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
@@ -1399,39 +1145,6 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
   cudaStream_t st = as_stream(stream);
   float* wsf = reinterpret_cast<float*>(ws);
   constexpr int stages = SQ_DECODE_STAGES;
-  // one fused launch (conv + state update + gated norm + FWHT + quant) when the shape allows
-  const int fe = di / (FU_CONSUMERS * 32);   // values per consumer thread in the row norm (a power of two)
-  const bool fused = SQ_DECODE_FUSED && stages == 7 && p->conv_kernel == 4 && di <= FU_MAXD && S.n_groups <= FU_MAXG &&
-                     S.n_heads <= FU_MAXH && di % (FU_CONSUMERS * 32) == 0 &&
-                     fe <= 16 && (fe & (fe - 1)) == 0 && ldzx % 2 == 0 && !yq_gsum &&
-                     !(reinterpret_cast<uintptr_t>(zx) & 1) && !(reinterpret_cast<uintptr_t>(p->conv_w) & 15);
-  if (fused) {
-    int* cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ds_counter_off(B, S));
-    auto launch = [&](auto kern, int smem) {
-      static std::once_flag once[2][64];
-      static int grid_cache[2][64];
-      int dev = 0;
-      cudaGetDevice(&dev);
-      const int kind = S.d_state == 128 ? 1 : 0;
-      std::call_once(once[kind][dev & 63], [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        int per_sm = 0, sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, FU_THREADS, smem) != cudaSuccess || per_sm < 1)
-          per_sm = 1;
-        grid_cache[kind][dev & 63] = sms * per_sm;   // one wave of persistent CTAs (one per SM)
-      });
-      const int units = B * ((S.n_heads + FU_UH - 1) / FU_UH);
-      const int g = grid_cache[kind][dev & 63];
-      launch_k(PDL_RING, kern, dim3(units < g ? units : g), dim3(FU_THREADS), smem, st, *p, B, zx, ldzx, conv_cache,
-               state, cnt, y, ldy, yq, ldyq);
-    };
-    if (S.d_state == 128)
-      launch(mamba2_decode_fused_kernel<128>, FuCfg<128>::SMEM);
-    else
-      launch(mamba2_decode_fused_kernel<64>, FuCfg<64>::SMEM);
-    return check_launch("sq_mamba2_decode_step_int8 (fused)");
-  }
   const int vec = p->conv_kernel == 4 && C % 4 == 0 && ldzx % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(zx) & 3) == 0 && (reinterpret_cast<uintptr_t>(conv_cache) & 3) == 0;
   const int per_blk = vec ? 1024 : 256;
@@ -1457,6 +1170,35 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
     const int tiles = B * S.n_heads;
     launch_k(PDL_RING, kern, dim3(tiles < g ? tiles : g), dim3(SR_THREADS), smem, st, S, B, (const float*)wsf, state, y, ldy);
   };
+  if (stages == 7 && ds_norm_fused(p, yq_gsum != nullptr)) {
+    // state update + row norm in one launch (state_ring_norm_kernel)
+    int* cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ds_counter_off(B, S));
+    auto ring_norm = [&](auto kern, int smem) {
+      static std::once_flag once[2][64];
+      static int grid_cache[2][64];
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const int kind = smem == RnCfg<128>::SMEM ? 1 : 0;
+      std::call_once(once[kind][dev & 63], [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int per_sm = 0, sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RN_THREADS, smem) != cudaSuccess ||
+            per_sm < 1)
+          per_sm = 1;
+        grid_cache[kind][dev & 63] = sms * per_sm;
+      });
+      const int g = grid_cache[kind][dev & 63];
+      const int tiles = B * S.n_heads;
+      launch_k(PDL_RING, kern, dim3(tiles < g ? tiles : g), dim3(RN_THREADS), smem, st, *p, B, (const float*)wsf,
+               state, y, ldy, yq, ldyq, cnt);
+    };
+    if (S.d_state == 128)
+      ring_norm(state_ring_norm_kernel<128>, RnCfg<128>::SMEM);
+    else
+      ring_norm(state_ring_norm_kernel<64>, RnCfg<64>::SMEM);
+    return check_launch("sq_mamba2_decode_step_int8");
+  }
   if (stages & 2) {
     if (S.d_state == 128)
       ring(state_ring_kernel<128>, SrCfg<128>::SMEM);

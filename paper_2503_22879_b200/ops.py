@@ -308,7 +308,7 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     if y is None:
         y = torch.empty((B, di), dtype=torch.float32, device=zx.device)
     nbytes = mamba2_decode_ws_bytes(p, B)
-    if ws is None:   # zero-filled: the fused kernel's counters start (and stay) at zero
+    if ws is None:   # zero-filled: the row counters start (and stay) at zero
         ws = torch.zeros(nbytes, dtype=torch.uint8, device=zx.device)
     if ws.numel() * ws.element_size() < nbytes:
         raise ShapeError(f"decode workspace needs {nbytes} bytes")
@@ -318,8 +318,7 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     _check(lib().sq_mamba2_decode_step_int8(C.byref(p), B, zx.data_ptr(), _ld(zx), conv_cache.data_ptr(),
                                             state.data_ptr(), ws.data_ptr(), y.data_ptr(), _ld(y), yq.data_ptr(),
                                             _ld(yq), gp, gl, _stream()),
-           1 if gsum is None and p.conv_kernel == 4 and di <= 8192 and p.ssm.n_groups <= 128 and di % 512 == 0 and (di // 512) & (di // 512 - 1) == 0
-           else 3 + (gsum is not None and not (di == 8192 and p.hadamard)))   # prep, state ring, norm (+ sums)
+           int(lib().sq_mamba2_decode_launches(C.byref(p), B, int(gsum is not None))))
     return yq
 
 

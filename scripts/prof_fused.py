@@ -26,3 +26,13 @@ for _ in range(20):
 e.record()
 torch.cuda.synchronize()
 print("fused decode step us", s.elapsed_time(e) / 20 * 1e3)
+gs = torch.zeros((B, d.d_inner // 128), dtype=torch.int32, device="cuda")
+for _ in range(3):
+    ops.mamba2_decode_step_int8(blk.decode_params, B, zx, c, h, y=y, ws=ws, gsum=gs)
+torch.cuda.synchronize()
+s.record()
+for _ in range(20):
+    ops.mamba2_decode_step_int8(blk.decode_params, B, zx, c, h, y=y, ws=ws, gsum=gs)
+e.record()
+torch.cuda.synchronize()
+print("three-launch decode step (+ group sums) us", s.elapsed_time(e) / 20 * 1e3)
