@@ -167,11 +167,10 @@ int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T,
  *   int8 SSM state update h' = exp(dt*A) h + dt*x*B, y = C.h' + D*x, y*SiLU(z)
  *   (selective_scan T=1) -> y,
  *   RMSNorm over d_inner + Sylvester FWHT + quant with s_y -> yq.
- * Two launches on `stream` when d_inner = 256 * 2^k <= 8192 and yq_gsum is NULL (the norm runs
- * inside the state kernel, as each row completes), else three (sq_mamba2_decode_launches).
- * State and conv cache are updated in place; ws (sq_mamba2_decode_ws_bytes) and y
- * [B x d_inner] f32 are caller-owned (y holds the gated SSM output).  ws must be zero-filled
- * before its first use (its row counters are left zero by every call). */
+ * Three launches on `stream` (four with yq_gsum unless the 8192-wide Hadamard norm emits the
+ * sums: sq_mamba2_decode_launches).  State and conv cache are updated in place; ws
+ * (sq_mamba2_decode_ws_bytes) and y [B x d_inner] f32 are caller-owned (y holds the gated SSM
+ * output). */
 typedef struct {
   sq_mamba2_params ssm;
   int conv_kernel;

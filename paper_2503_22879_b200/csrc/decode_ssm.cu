@@ -681,436 +681,20 @@ __global__ void __launch_bounds__(256) norm_had8192_kernel(const sq_mamba2_decod
   }
 }
 
-// ------------------------------------------------------------------ K9 + K6: state update with the row norm
-// state_ring_kernel plus the gated RMSNorm + FWHT + quant of each row (N1 in decode: no separate
-// norm launch).  Tiles are dealt round-robin (t = blockIdx.x + i * gridDim.x), so each wave of the
-// grid covers consecutive rows and rows complete progressively.  Warp roles:
-//   warps 0-7   consumers (as state_ring_kernel), y to L2; every RN_CHK tiles they run the norms of
-//               the rows published to this CTA so far
-//   warp 8      producer (as state_ring_kernel)
-//   warp 9      row counter: after the consumers finish a tile it adds 1 to the row's counter
-//               (release: their y stores, observed through the cta-scope acquire, precede it), and
-//               it watches the counters of this CTA's rows (b = blockIdx.x + j * gridDim.x), publishing
-//               each to the consumers once all nh heads are in.  No CTA ever waits on another's
-//               progress except for its own rows' completion, so the grid size is free.
-// Row counters live in the caller's workspace (zeroed once, reset by their norm CTA), so the step
-// is graph-replayable.
-constexpr int RN_CONS = 8;
-constexpr int RN_THREADS = (RN_CONS + 2) * 32;
-constexpr int RN_NSLOT = 7;
-constexpr int RN_MAXD = 8192;   // d_inner normalised by one CTA
-constexpr int RN_QN = 8;        // ring of rows ready for this CTA's norm
-constexpr int RN_CHK = 4;       // tiles between checks for ready rows
-template <int N>
-struct RnCfg {
-  static constexpr int TILE = DS_P * N;
-  static constexpr int ROWB = DS_ROWF * 4;
-  static constexpr int BCB = 2 * N * 4;
-  static constexpr int SLOT = TILE + ROWB + BCB;
-  static constexpr int OFF_NORM = RN_NSLOT * SLOT;
-  static constexpr int OFF_BAR = OFF_NORM + (RN_MAXD + RN_MAXD / 32) * 4;   // norm row, one pad word per 32
-  static constexpr int OFF_CTL = OFF_BAR + 2 * RN_NSLOT * 8;  // tiles_done, nready, snap[2], handled, rows[QN]
-  static constexpr int SMEM = OFF_CTL + 64 + 128;
-  static_assert((5 + RN_QN) * 4 <= 64, "control words");
-  static_assert(SLOT % 16 == 0, "slot alignment");
-};
-
-__device__ __forceinline__ void red_add_release_cta(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_cta(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_add_release_gpu(int* p, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__host__ __device__ constexpr int rn_lg(int v) { return v <= 1 ? 0 : 1 + rn_lg(v / 2); }
-// FWHT phase schedule: bases S_0 = 0, S_{p+1} = min(S_p + lgE, L - lgE) until S_p + lgE >= L
-__host__ __device__ constexpr int rn_next_s(int s, int lgE, int L) { return s + lgE < L - lgE ? s + lgE : L - lgE; }
-__host__ __device__ constexpr int rn_last_s(int s, int lgE, int L) {
-  return s + lgE >= L ? s : rn_last_s(rn_next_s(s, lgE, L), lgE, L);
-}
-// row index of register e of thread t is base | (e << S) when the registers hold index bits [S, S + lgE)
-template <int S, int lgE>
-__device__ __forceinline__ int rn_base(int t) {
-  return ((t >> S) << (S + lgE)) | (t & ((1 << S) - 1));
-}
-// FWHT phases from base S (bits below DONE already transformed): butterflies on the register
-// bits, then a conflict-free transposition through smem to the next phase's layout
-template <int E, int NT, int S, int DONE>
-__device__ __forceinline__ void rn_fwht(float (&v)[E], int tid, float* nbuf) {
-  constexpr int lgE = rn_lg(E), L = rn_lg(NT) + lgE;
-#pragma unroll
-  for (int j = 0; j < lgE; ++j)
-    if (S + j >= DONE) {
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (((e >> j) & 1) == 0) {
-          const float x0 = v[e], x1 = v[e + (1 << j)];
-          v[e] = __fadd_rn(x0, x1);
-          v[e + (1 << j)] = __fsub_rn(x0, x1);
-        }
-    }
-  if constexpr (S + lgE < L) {
-    constexpr int S2 = rn_next_s(S, lgE, L);
-    const int b1 = rn_base<S, lgE>(tid), b2 = rn_base<S2, lgE>(tid);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int ix = b1 | (e << S);
-      nbuf[ix + (ix >> 5)] = v[e];
-    }
-    named_bar(1, NT);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int ix = b2 | (e << S2);
-      v[e] = nbuf[ix + (ix >> 5)];
-    }
-    named_bar(1, NT);   // reads done before the next transposition (or row) writes
-    rn_fwht<E, NT, S2, S + lgE>(v, tid, nbuf);
-  }
-}
-
-// Gated RMSNorm (f64 sum of squares) + FWHT (Sylvester stages in ascending stride, the oracle's
-// order) + quant of row b by NT threads (named barrier 1); y of the row is complete in L2.
-// di = NT·E (E a power of two >= 2).  Each thread holds E values whose row index bits [S, S + lgE)
-// are the register index: phase 0 (S = 0) is the contiguous load layout, and each later phase
-// moves the next lgE index bits into registers through smem (one pad word per 32: every
-// transposition is bank-conflict free), so every butterfly runs in registers.  The phase schedule
-// is static, so the index arithmetic folds to per-thread bases.
-template <int E, int NT>
-__device__ __noinline__ void rn_row_norm(const float* norm_w, float eps, int hadamard, float s_y, int b,
-                                        const float* y, int64_t ldy, int8_t* yq, int64_t ldyq, float* nbuf) {
-  constexpr int di = E * NT, lgE = rn_lg(E), L = rn_lg(NT) + lgE;
-  static_assert(E >= 2 && (1 << L) == di, "d_inner = NT * 2^k");
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const float* yr = y + (int64_t)b * ldy + tid * E;
-  const float* wr = norm_w + tid * E;
-  float v[E];
-  double ss = 0.0;
-#pragma unroll
-  for (int e = 0; e < E; e += 2) {
-    const float2 q = __ldcg(reinterpret_cast<const float2*>(yr + e));
-    v[e] = q.x;
-    v[e + 1] = q.y;
-  }
-#pragma unroll
-  for (int e = 0; e < E; ++e) ss += (double)v[e] * (double)v[e];
-  ss = warp_sum_d(ss);
-  double* red = reinterpret_cast<double*>(nbuf);   // nbuf is free until the FWHT stage
-  if (lane == 0) red[warp] = ss;
-  named_bar(1, NT);
-  double tot = 0.0;
-#pragma unroll
-  for (int k = 0; k < NT / 32; ++k) tot += red[k];
-  named_bar(1, NT);
-  const float ms = (float)(tot / (double)di);
-  const float rfac = __fdiv_rn(1.0f, sqrtf(__fadd_rn(ms, eps)));
-#pragma unroll
-  for (int e = 0; e < E; e += 2) {
-    const float2 g = __ldg(reinterpret_cast<const float2*>(wr + e));
-    v[e] = __fmul_rn(__fmul_rn(v[e], rfac), g.x);
-    v[e + 1] = __fmul_rn(__fmul_rn(v[e + 1], rfac), g.y);
-  }
-  int8_t* out = yq + (int64_t)b * ldyq;
-  const float inv = __frcp_rn(s_y);
-  if (hadamard) {
-    rn_fwht<E, NT, 0, 0>(v, tid, nbuf);
-    constexpr int SL = rn_last_s(0, lgE, L);
-    const int bl = rn_base<SL, lgE>(tid);
-#pragma unroll
-    for (int e = 0; e < E; ++e) out[bl | (e << SL)] = quant8_inv(v[e], s_y, inv);
-  } else {
-#pragma unroll
-    for (int e = 0; e < E; ++e) out[tid * E + e] = quant8_inv(v[e], s_y, inv);
-  }
-}
-
-#ifdef SQ_RN_TRACE
-// per-CTA timeline (globaltimer ns; profiling builds only): start, consumer loop end, drain end,
-// ns in norms, counter warp end, counter warp ns in the gpu-scope ops, norms run
-__device__ unsigned long long g_rn_tr[1024][8];
-__device__ __forceinline__ unsigned long long rn_time() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define RN_TR(k, v) g_rn_tr[blockIdx.x & 1023][k] = (v)
-#endif
-
-template <int N>
-__global__ void __launch_bounds__(RN_THREADS, 2)
-    state_ring_norm_kernel(const sq_mamba2_decode_params P, int B, const float* __restrict__ ws,
-                           int8_t* __restrict__ state, float* y, int64_t ldy, int8_t* yq, int64_t ldyq,
-                           int* cnt_row) {
-  using Cfg = RnCfg<N>;
-  const sq_mamba2_params& S = P.ssm;
-  constexpr int CPT = N / 8;   // state columns per thread
-  constexpr int VW = CPT / 4;  // 32-bit words per row piece
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint64_t* empty = full + RN_NSLOT;
-  uint32_t* ctl = reinterpret_cast<uint32_t*>(smem + Cfg::OFF_CTL);
-  uint32_t* tiles_done = ctl;   // consumer warps x tiles finished (monotonic)
-  uint32_t* nready = ctl + 1;   // rows published to this CTA's norm ring (monotonic)
-  uint32_t* snap = ctl + 2;     // [2] consumer-agreed nready snapshots (double-buffered)
-  uint32_t* handled_pub = ctl + 4;              // rows normalised (frees ring entries)
-  int* rows = reinterpret_cast<int*>(ctl + 5);  // [RN_QN] rows ready for the norm
-  float* nbuf = reinterpret_cast<float*>(smem + Cfg::OFF_NORM);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nh = S.n_heads, di = nh * DS_P;
-  const int ntiles_all = B * nh;
-  const int ntiles = (ntiles_all - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-  const int my_rows = (int)blockIdx.x < B ? (B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-  pdl_trigger();
-  if (tid == 0) {
-    for (int i = 0; i < RN_NSLOT; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], RN_CONS);
-    }
-    ctl[0] = ctl[1] = ctl[2] = ctl[3] = ctl[4] = 0;
-    fence_barrier_init();
-  }
-  __syncthreads();
-  pdl_wait();   // prep outputs (ws), the state and y / yq: produced / last used by earlier grids
-#ifdef SQ_RN_TRACE
-  if (tid == 0) RN_TR(0, rn_time());
-  unsigned long long tacc = 0;
-#endif
-  const float* bc_all = ws + ds_rows_floats(B, nh);
-  if (warp == RN_CONS) {
-    // ---------------- producer: state tile + row scalars + B̂|Ĉ of the head's group
-    if (lane == 0) {
-      for (int i = 0; i < ntiles; ++i) {
-        const int t = blockIdx.x + i * gridDim.x;
-        const int b = t / nh, h = t % nh;
-        const int slot = i % RN_NSLOT;
-        if (i >= RN_NSLOT) mbar_wait(&empty[slot], ((i / RN_NSLOT) - 1) & 1);
-        uint8_t* dst = smem + slot * Cfg::SLOT;
-        mbar_arrive_expect_tx(&full[slot], Cfg::SLOT);
-        bulk_load(dst, state + (int64_t)t * Cfg::TILE, Cfg::TILE, &full[slot]);
-        bulk_load(dst + Cfg::TILE, ws + (int64_t)t * DS_ROWF, Cfg::ROWB, &full[slot]);
-        bulk_load(dst + Cfg::TILE + Cfg::ROWB, bc_all + ((int64_t)b * S.n_groups + S.head_group[h]) * 2 * N,
-                  Cfg::BCB, &full[slot]);
-      }
-    }
-    return;
-  }
-  if (warp == RN_CONS + 1) {
-    // ---------------- row counter
-    if (lane == 0) {
-      int k = 0, j = 0;
-      uint32_t published = 0;
-      while (k < ntiles || j < my_rows) {
-        bool moved = false;
-        if (k < ntiles && ld_acquire_cta(tiles_done) >= (uint32_t)(RN_CONS * (k + 1))) {
-#ifdef SQ_RN_TRACE
-          const unsigned long long t0 = rn_time();
-#endif
-          red_add_release_gpu(&cnt_row[((int)blockIdx.x + k * (int)gridDim.x) / nh], 1);
-#ifdef SQ_RN_TRACE
-          tacc += rn_time() - t0;
-#endif
-          ++k;
-          moved = true;
-        }
-        if (j < my_rows && published - ld_acquire_cta(handled_pub) < (uint32_t)RN_QN) {
-          const int rb = (int)blockIdx.x + j * (int)gridDim.x;
-          if (ld_acquire_gpu(&cnt_row[rb]) >= nh) {   // acquire: every CTA's y stores of row rb
-            cnt_row[rb] = 0;                           // self-reset for the next launch
-            rows[published % RN_QN] = rb;
-            st_release_cta(nready, ++published);
-            ++j;
-            moved = true;
-          }
-        }
-        if (!moved) __nanosleep(64);
-      }
-#ifdef SQ_RN_TRACE
-      RN_TR(4, rn_time());
-      RN_TR(5, tacc);
-#endif
-    }
-    return;
-  }
-  // ---------------- consumers: thread = (row quad rq, column chunk); rows rq and rq + 32
-  int handled = 0;
-  auto run_norms = [&](int upto) {
-    for (; handled < upto; ++handled) {
-      const int rb = rows[handled % RN_QN];
-#ifdef SQ_RN_TRACE
-      const unsigned long long t0 = rn_time();
-#endif
-      switch (di / (RN_CONS * 32)) {   // values per consumer thread (d_inner = 256 * 2^k)
-        case 2: rn_row_norm<2, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-        case 4: rn_row_norm<4, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-        case 8: rn_row_norm<8, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-        case 16: rn_row_norm<16, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-        default: rn_row_norm<32, RN_CONS * 32>(P.norm_w, P.eps, P.hadamard, P.s_y, rb, y, ldy, yq, ldyq, nbuf); break;
-      }
-#ifdef SQ_RN_TRACE
-      tacc += rn_time() - t0;
-#endif
-      if (tid == 0) st_release_cta(handled_pub, (uint32_t)(handled + 1));
-    }
-  };
-  const int chunk = tid & 7, rq = tid >> 3;
-  const float2 MG = make_float2(-8388736.0f, -8388736.0f);
-  const float2 RM = make_float2(12582912.0f, 12582912.0f);
-  const int gstep = gridDim.x;
-  const int db = gstep / nh, dh = gstep % nh;   // tile t -> (b, h) advanced incrementally
-  int b = blockIdx.x / nh, h = blockIdx.x % nh;
-  const uint32_t full0 = smem_u32(full);
-  for (int i = 0; i < ntiles; ++i) {
-    const int t = b * nh + h;
-    const int slot = i % RN_NSLOT;
-    const uint8_t* sl = smem + slot * Cfg::SLOT;
-    const float* rf = reinterpret_cast<const float*>(sl + Cfg::TILE);
-    const float* bcs = reinterpret_cast<const float*>(sl + Cfg::TILE + Cfg::ROWB);
-    mbar_wait_addr(full0 + slot * 8, (i / RN_NSLOT) & 1);
-    float2 bv[CPT / 2], cv[CPT / 2];
-#pragma unroll
-    for (int e = 0; e < CPT / 4; ++e) {
-      const float4 b4 = *reinterpret_cast<const float4*>(bcs + ((e * 8 + chunk) << 2));
-      const float4 c4 = *reinterpret_cast<const float4*>(bcs + N + ((e * 8 + chunk) << 2));
-      bv[e * 2] = make_float2(b4.x, b4.y);
-      bv[e * 2 + 1] = make_float2(b4.z, b4.w);
-      cv[e * 2] = make_float2(c4.x, c4.y);
-      cv[e * 2 + 1] = make_float2(c4.z, c4.w);
-    }
-    const float dA = rf[4 * DS_P], Dh = rf[4 * DS_P + 1];
-    const float2 dA2 = make_float2(dA, dA);
-    int8_t* st = state + (int64_t)t * Cfg::TILE + chunk * CPT;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int R = rq + 32 * k;
-      const float rs = rf[DS_P + R];
-      const float2 rs2 = make_float2(rs, rs);
-      uint32_t raw[VW];
-      if constexpr (VW == 4) {
-        const uint4 v = *reinterpret_cast<const uint4*>(sl + R * N + chunk * CPT);
-        raw[0] = v.x; raw[1] = v.y; raw[2] = v.z; raw[3] = v.w;
-      } else {
-        const uint2 v = *reinterpret_cast<const uint2*>(sl + R * N + chunk * CPT);
-        raw[0] = v.x; raw[1] = v.y;
-      }
-      uint32_t outw[VW];
-      float2 acc2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int e = 0; e < VW; ++e) {
-        const uint32_t u = raw[e] ^ 0x80808080u;
-        int qi[4];
-#pragma unroll
-        for (int i2 = 0; i2 < 4; i2 += 2) {
-          const int n2 = e * 2 + i2 / 2;
-          const float2 hq = __fadd2_rn(make_float2(s8_raw(u, i2), s8_raw(u, i2 + 1)), MG);
-          const float2 tt = __ffma2_rn(dA2, hq, __fmul2_rn(rs2, bv[n2]));
-          acc2 = __ffma2_rn(tt, cv[n2], acc2);
-          const float2 rr = __fadd2_rn(tt, RM);   // bits = 0x4B400000 + rint(t), |t| < 2^22
-          qi[i2] = __float_as_int(rr.x) - 0x4B400000;
-          qi[i2 + 1] = __float_as_int(rr.y) - 0x4B400000;
-        }
-        outw[e] = pack4_sat(qi[0], qi[1], qi[2], qi[3]);
-      }
-      if constexpr (VW == 4)
-        *reinterpret_cast<uint4*>(st + R * N) = make_uint4(outw[0], outw[1], outw[2], outw[3]);
-      else
-        *reinterpret_cast<uint2*>(st + R * N) = make_uint2(outw[0], outw[1]);
-      float acc = __fadd_rn(acc2.x, acc2.y);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      if (chunk == 0)
-        y[(int64_t)b * ldy + h * DS_P + R] =
-            __fmul_rn(__fadd_rn(__fmul_rn(rf[3 * DS_P + R], acc), __fmul_rn(Dh, rf[R])), rf[2 * DS_P + R]);
-    }
-    fence_proxy_async_smem();   // our generic reads of the slot precede the next bulk copy into it
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&empty[slot]);
-      red_add_release_cta(tiles_done, 1);   // this warp's y stores precede the row count
-    }
-    h += dh;
-    b += db;
-    if (h >= nh) {
-      h -= nh;
-      ++b;
-    }
-    if (i % RN_CHK == RN_CHK - 1) {   // run the norms of the rows published so far
-      if (tid == 0) snap[(i / RN_CHK) & 1] = ld_acquire_cta(nready);
-      named_bar(1, RN_CONS * 32);
-      run_norms((int)snap[(i / RN_CHK) & 1]);
-    }
-  }
-  // drain: this CTA's remaining rows, as they complete
-#ifdef SQ_RN_TRACE
-  if (tid == 0) RN_TR(1, rn_time());
-#endif
-  named_bar(1, RN_CONS * 32);   // every consumer read its last snapshot
-  while (handled < my_rows) {
-    if (tid == 0) {
-      while ((int)ld_acquire_cta(nready) <= handled) __nanosleep(64);
-      snap[0] = ld_acquire_cta(nready);
-    }
-    named_bar(1, RN_CONS * 32);
-    const int upto = (int)snap[0];
-    named_bar(1, RN_CONS * 32);
-    run_norms(upto);
-  }
-#ifdef SQ_RN_TRACE
-  if (tid == 0) {
-    RN_TR(2, rn_time());
-    RN_TR(3, tacc);
-    RN_TR(6, handled);
-  }
-#endif
-}
-
 }  // namespace sq
 
 using namespace sq;
 
-
-#ifdef SQ_RN_TRACE
-extern "C" int sq_probe_rn_trace(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, sq::g_rn_tr, sizeof(sq::g_rn_tr)) == cudaSuccess ? 0 : -3;
-}
-#endif
-
-// Workspace: [f32 operands written by prep_kernel][int32 row counters of state_ring_norm_kernel, B].
-// The counter region must be zero before the first call; the kernel leaves it zero (each counter
-// is reset by the CTA that normalises its row).
-static int64_t ds_counter_off(int B, const sq_mamba2_params& S) {
-  return ((ds_ws_floats(B, S.n_heads, S.n_groups, S.d_state) * 4 + 255) / 256) * 256;
-}
-
 extern "C" int64_t sq_mamba2_decode_ws_bytes(const sq_mamba2_decode_params* p, int B) {
   if (!p || B < 0) return -1;
-  return ds_counter_off(B, p->ssm) + (int64_t)B * 4;
-}
-
-// the row norm runs inside the state kernel when d_inner = 256 * 2^k (<= 8192) and no group sums
-static bool ds_norm_fused(const sq_mamba2_decode_params* p, int with_gsum) {
-  const int di = p->ssm.n_heads * DS_P, e = di / (RN_CONS * 32);
-  return !with_gsum && di <= RN_MAXD && di % (RN_CONS * 32) == 0 && e >= 2 && (e & (e - 1)) == 0;
+  return ds_ws_floats(B, p->ssm.n_heads, p->ssm.n_groups, p->ssm.d_state) * 4;
 }
 
 extern "C" int sq_mamba2_decode_launches(const sq_mamba2_decode_params* p, int B, int with_gsum) {
   if (!p || B < 0) return -1;
   if (B == 0) return 0;
-  if (ds_norm_fused(p, with_gsum)) return 2;
   const int di = p->ssm.n_heads * DS_P;
+  // prep + state ring + norm, plus the group-sum pass unless the 8192-wide Hadamard norm fuses it
   return 3 + (with_gsum && !(di == 8192 && p->hadamard));
 }
 
@@ -1170,35 +754,6 @@ extern "C" int sq_mamba2_decode_step_int8(const sq_mamba2_decode_params* p, int 
     const int tiles = B * S.n_heads;
     launch_k(PDL_RING, kern, dim3(tiles < g ? tiles : g), dim3(SR_THREADS), smem, st, S, B, (const float*)wsf, state, y, ldy);
   };
-  if (stages == 7 && ds_norm_fused(p, yq_gsum != nullptr)) {
-    // state update + row norm in one launch (state_ring_norm_kernel)
-    int* cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + ds_counter_off(B, S));
-    auto ring_norm = [&](auto kern, int smem) {
-      static std::once_flag once[2][64];
-      static int grid_cache[2][64];
-      int dev = 0;
-      cudaGetDevice(&dev);
-      const int kind = smem == RnCfg<128>::SMEM ? 1 : 0;
-      std::call_once(once[kind][dev & 63], [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        int per_sm = 0, sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RN_THREADS, smem) != cudaSuccess ||
-            per_sm < 1)
-          per_sm = 1;
-        grid_cache[kind][dev & 63] = sms * per_sm;
-      });
-      const int g = grid_cache[kind][dev & 63];
-      const int tiles = B * S.n_heads;
-      launch_k(PDL_RING, kern, dim3(tiles < g ? tiles : g), dim3(RN_THREADS), smem, st, *p, B, (const float*)wsf,
-               state, y, ldy, yq, ldyq, cnt);
-    };
-    if (S.d_state == 128)
-      ring_norm(state_ring_norm_kernel<128>, RnCfg<128>::SMEM);
-    else
-      ring_norm(state_ring_norm_kernel<64>, RnCfg<64>::SMEM);
-    return check_launch("sq_mamba2_decode_step_int8");
-  }
   if (stages & 2) {
     if (S.d_state == 128)
       ring(state_ring_kernel<128>, SrCfg<128>::SMEM);

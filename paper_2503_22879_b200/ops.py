@@ -308,8 +308,8 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     if y is None:
         y = torch.empty((B, di), dtype=torch.float32, device=zx.device)
     nbytes = mamba2_decode_ws_bytes(p, B)
-    if ws is None:   # zero-filled: the row counters start (and stay) at zero
-        ws = torch.zeros(nbytes, dtype=torch.uint8, device=zx.device)
+    if ws is None:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=zx.device)
     if ws.numel() * ws.element_size() < nbytes:
         raise ShapeError(f"decode workspace needs {nbytes} bytes")
     _dev(yq, torch.int8, "yq", 2)
