@@ -14,10 +14,11 @@
 //   warp 0     activation TMA producer: [NTOK x 128 B] K-blocks, SWIZZLE_128B
 //   warp 1     TMEM allocator + single-thread MMA issuer (4 x K=32 kind::i8 per group)
 //   warp 2     weight stream: contiguous 8 KB packed (n-tile, k-block) tiles by 1-D bulk copy
-//   warps 4-7  converters: nibble v -> int8 16*v with one AND (high nibble) / SHF+AND (low),
-//              stored straight into a TMEM A stage (kind::i8 A-from-TMEM).  The x16 is exact
-//              (|16*v| <= 128) and is undone by s_a/16 in the epilogue (a power of two).
-//   warps 8-15 promotion + epilogue: tcgen05.ld of the group's int32 tile, then f32(acc) without
+//   converters (warps 4-7 for 64 tokens, 4-11 for 16/32): nibble v -> int8 16*v with one AND
+//              (high nibble) / SHF+AND (low), stored straight into a TMEM A stage (kind::i8
+//              A-from-TMEM).  The x16 is exact (|16*v| <= 128) and is undone by s_a/16 in the
+//              epilogue (a power of two).
+//   promotion + epilogue (the remaining warps up to 15): tcgen05.ld of the group's int32 tile, then f32(acc) without
 //              an I2F: acc + 0x4B400000 is the bit pattern of the f32 1.5*2^23 + acc (|acc| <= 2^21),
 //              so one IADD and one FADD2 per pair recover it exactly; p = fma(s_w, f32(acc), p).
 // No weight byte is read twice and no scale is rounded: the kernel streams 0.5 B per weight
@@ -61,6 +62,12 @@ constexpr int AST = SQ_W4_AST;          // activation stages (steps)
 constexpr int TST = 4;                  // TMEM A stages (steps)
 constexpr int NACC = 2;                 // accumulator buffers (steps)
 constexpr uint32_t MAGIC = 0x4B400000u; // bit pattern of 1.5 * 2^23
+// Converter / promotion split of warps 4-15: the promotion work per step scales with the token
+// tile, the conversion work does not.  64 tokens: 4 converters (both groups of a step each) + 8
+// promotion warps (32 token columns each); 16 / 32 tokens: 8 converters (two sets, one group of the
+// step each) + 4 promotion warps (all columns).  Same-box A/B (scripts/probe_w4.py): in_proj b=1
+// 12.0 -> 10.8 us with 8 converters, b=64 14.7 -> 16.1 us, so the split follows the tile.
+__host__ __device__ constexpr int n_conv(int ntok) { return ntok <= 32 ? 8 : 4; }
 
 template <int NTOK>
 struct Cfg {
@@ -76,7 +83,10 @@ struct Cfg {
   static constexpr int A_COL = NACC * GS * NTOK;
   static constexpr int COLS_USED = A_COL + TST * GS * 32;
   static constexpr int TMEM_COLS = COLS_USED <= 256 ? 256 : 512;
-  static constexpr int HALF = NTOK / 2;   // token columns per promotion warp
+  static constexpr int NCONV = n_conv(NTOK);     // converter warps
+  static constexpr int PROMO0 = 4 + NCONV;        // first promotion warp
+  static constexpr int NPROMO = 16 - PROMO0;      // promotion warps (8 or 4)
+  static constexpr int HALF = NPROMO == 8 ? NTOK / 2 : NTOK;   // token columns per promotion thread
   static_assert(NTOK * BN * 4 <= OFF_ACT, "split-K partial tile must fit the weight ring");
 };
 
@@ -170,14 +180,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&aempty[i], 1);
     }
     for (int i = 0; i < TST; ++i) {
-      mbar_init(&tfull[i], 4);
+      mbar_init(&tfull[i], C::NCONV);
       mbar_init(&tempty[i], 1);
     }
     for (int i = 0; i < NACC; ++i) {
       mbar_init(&cfull[i], 1);
-      mbar_init(&cempty[i], 8);
+      mbar_init(&cempty[i], C::NPROMO);
     }
-    for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 8); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::NPROMO); }
     fence_barrier_init();
     tma_prefetch(&tm_act);
   }
@@ -263,42 +273,46 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < C::PROMO0) {
     // ------------------------------------------------ converters: packed nibbles -> TMEM A stages
-    const int qd = warp & 3;
+    // (8 converters: set 0 converts the step's first group, set 1 its second, in parallel)
+    const int qd = warp & 3, set = C::NCONV == 8 ? (warp - 4) >> 2 : 0;
+    constexpr int GPW = C::NCONV == 8 ? 1 : GS;   // groups per converter warp and step
     const int row = qd * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(qd * 32) << 16) + C::A_COL;
     int j = 0, q = 0;
     for (int u = u_first; u < args.units; u += u_step) {
       for (int k = 0; k < nst; ++k, ++q) {
         const int t = q % TST, ng = min(GS, nkb - k * GS);
-        uint32_t wv[GS][32];
-        uint4 p[GS][4];
+        uint32_t wv[GPW][32];
+        uint4 p[GPW][4];
         // the step's tiles: every smem read issued before one proxy fence and the slot releases
 #pragma unroll
-        for (int g = 0; g < GS; ++g) {
+        for (int gg = 0; gg < GPW; ++gg) {
+          const int g = set + gg;
           if (g < ng) {
             const int r = (j + g) % RAW;
             mbar_wait(&rfull[r], ((j + g) / RAW) & 1);
             if (warp == 4 && lane == 0 && g == 0) TL(2, q);
 #pragma unroll
             for (int c = 0; c < 4; ++c)
-              p[g][c] = *reinterpret_cast<const uint4*>(raw + r * TILE_BYTES + c * 2048 + row * 16);
+              p[gg][c] = *reinterpret_cast<const uint4*>(raw + r * TILE_BYTES + c * 2048 + row * 16);
           }
         }
         fence_proxy_async_smem();   // generic reads of the slots precede the bulk copies that refill them
         __syncwarp();
         if (lane == 0)
-          for (int g = 0; g < ng; ++g) mbar_arrive(&rempty[(j + g) % RAW]);
+          for (int gg = 0; gg < GPW; ++gg)
+            if (set + gg < ng) mbar_arrive(&rempty[(j + set + gg) % RAW]);
 #pragma unroll
-        for (int g = 0; g < GS; ++g) {
-          if (g < ng) {
+        for (int gg = 0; gg < GPW; ++gg) {
+          if (set + gg < ng) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              to_s8x16(p[g][c].x, wv[g][c * 8 + 0], wv[g][c * 8 + 1]);
-              to_s8x16(p[g][c].y, wv[g][c * 8 + 2], wv[g][c * 8 + 3]);
-              to_s8x16(p[g][c].z, wv[g][c * 8 + 4], wv[g][c * 8 + 5]);
-              to_s8x16(p[g][c].w, wv[g][c * 8 + 6], wv[g][c * 8 + 7]);
+              to_s8x16(p[gg][c].x, wv[gg][c * 8 + 0], wv[gg][c * 8 + 1]);
+              to_s8x16(p[gg][c].y, wv[gg][c * 8 + 2], wv[gg][c * 8 + 3]);
+              to_s8x16(p[gg][c].z, wv[gg][c * 8 + 4], wv[gg][c * 8 + 5]);
+              to_s8x16(p[gg][c].w, wv[gg][c * 8 + 6], wv[gg][c * 8 + 7]);
             }
           }
         }
@@ -308,8 +322,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
 #ifndef SQ_W4_PROBE_NOCONV   // profiling builds only: the A stage is left as is
 #pragma unroll
-        for (int g = 0; g < GS; ++g)
-          if (g < ng) tmem_st_x32(lane_base + (t * GS + g) * 32, wv[g]);
+        for (int gg = 0; gg < GPW; ++gg)
+          if (set + gg < ng) tmem_st_x32(lane_base + (t * GS + set + gg) * 32, wv[gg]);
         tmem_wait_st();
 #endif
         tc_fence_before();
@@ -322,9 +336,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // the promotion warps' writes (compute-sanitizer racecheck: the mbarrier / tcgen05.commit
     // chain between them is not a generic-proxy happens-before)
     if (SPLITS > 1) named_bar(2, 384);
-  } else if (warp >= 8) {
+  } else if (warp >= C::PROMO0) {
     // ------------------------------------------------ promotion + epilogue
-    const int qd = warp & 3, h = (warp - 8) >> 2;
+    const int qd = warp & 3, h = C::NPROMO == 8 ? (warp - C::PROMO0) >> 2 : 0;
     const int row = qd * 32 + lane;
     const uint32_t acc_base = tmem + ((uint32_t)(qd * 32) << 16) + C::ACC_COL + h * C::HALF;
     int q = 0, ui = 0;
@@ -344,33 +358,37 @@ __global__ void __launch_bounds__(THREADS, 1)
 
         tc_fence_after();
         const float2 nm = make_float2(-12582912.0f, -12582912.0f);
+        constexpr int CW = C::HALF < 32 ? C::HALF : 32;   // columns per TMEM load
 #pragma unroll
         for (int g = 0; g < GS; ++g) {
           if (g < ng) {
-            uint32_t v[C::HALF];
-#ifndef SQ_W4_PROBE_NOPROMO  // profiling builds only: accumulators not read
-            tmem_ld_cols<C::HALF>(acc_base + (c * GS + g) * NTOK, v);
-            tmem_wait_ld();
-#else
-#pragma unroll
-            for (int e = 0; e < C::HALF; ++e) v[e] = 0u;
-#endif
-            if (g == ng - 1) {   // every accumulator of the step is in registers: release the buffers
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&cempty[c]);
-            }
             const float s0 = ssl[(k * GS + g) * BN];
             const float2 sv = make_float2(s0, s0);
 #pragma unroll
-            for (int e = 0; e < C::HALF; e += 2) {
-              // f32(acc) without I2F: the int32 + 0x4B400000 bit pattern is the float 1.5·2^23 + acc
-              // (|acc| <= 2^21)
-              const float2 f = __fadd2_rn(
-                  make_float2(__uint_as_float(v[e] + MAGIC), __uint_as_float(v[e + 1] + MAGIC)), nm);
-              const float2 r2 = __ffma2_rn(sv, f, make_float2(p[e], p[e + 1]));
-              p[e] = r2.x;
-              p[e + 1] = r2.y;
+            for (int c0 = 0; c0 < C::HALF; c0 += CW) {
+              uint32_t v[CW];
+#ifndef SQ_W4_PROBE_NOPROMO  // profiling builds only: accumulators not read
+              tmem_ld_cols<CW>(acc_base + (c * GS + g) * NTOK + c0, v);
+              tmem_wait_ld();
+#else
+#pragma unroll
+              for (int e = 0; e < CW; ++e) v[e] = 0u;
+#endif
+              if (g == ng - 1 && c0 + CW == C::HALF) {   // the step's accumulators are read: release
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&cempty[c]);
+              }
+#pragma unroll
+              for (int e = 0; e < CW; e += 2) {
+                // f32(acc) without I2F: the int32 + 0x4B400000 bit pattern is the float 1.5·2^23 +
+                // acc (|acc| <= 2^21)
+                const float2 f = __fadd2_rn(
+                    make_float2(__uint_as_float(v[e] + MAGIC), __uint_as_float(v[e + 1] + MAGIC)), nm);
+                const float2 r2 = __ffma2_rn(sv, f, make_float2(p[c0 + e], p[c0 + e + 1]));
+                p[c0 + e] = r2.x;
+                p[c0 + e + 1] = r2.y;
+              }
             }
           }
         }

@@ -8,6 +8,8 @@ import torch  # noqa: E402
 from paper_2503_22879_b200 import _lib, ops  # noqa: E402
 
 SHAPES = [("in_proj", 64, 18560, 4096), ("out_proj", 64, 4096, 8192), ("head", 64, 256000, 4096), ("in b1", 1, 18560, 4096)]
+if os.environ.get("PROBE_LONGK"):   # steady state: one unit per SM, 4x the K of in_proj
+    SHAPES = [("long K", 64, 18560, 8192), ("in_proj", 64, 18560, 4096)]
 dev = "cuda"
 for name in sys.argv[1:]:
     _lib._lib = _lib.load(os.path.join(os.path.dirname(_lib.LIB_PATH), "..", "probe", f"probe_{name}.so"))
