@@ -25,7 +25,9 @@ step of the A8 path (LEDGER G5, G6, G11, G16):
 Mamba1: x_proj consumes clustered-scale x, so the per-channel activation scale
 is folded into the x_proj weight columns before per-channel quantisation
 (s_a = 1 in its epilogue).  W4A16 runs the float path with dequantised
-per-group weights and float (fp32) state.
+per-group weights and float (fp32) state; its projections take bf16
+activations (north_star (a): int4-weight x bf16-activation GEMV): x is rounded to
+bf16 (RN-even) before the product, everything else stays f32.
 """
 from __future__ import annotations
 
@@ -125,8 +127,16 @@ def qlinear_a8(a_codes, ql: QLinear, s_a, splits: int | None = None) -> tuple[np
     return promote_groups(accg, ql.s_group, s_a, splits), accg.sum(axis=0)
 
 
+def round_bf16(a) -> np.ndarray:
+    """f32 -> bfloat16 (round to nearest even), returned as f32 (finite inputs)."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
 def qlinear_a16(a, ql: QLinear) -> np.ndarray:
-    return matmul_fast(np.asarray(a, np.float32), ql.dequant().T)
+    """W4A16 projection: bf16(a) @ dequant(w).T with f32 accumulation."""
+    return matmul_fast(round_bf16(a), ql.dequant().T)
 
 
 @dataclass

@@ -105,7 +105,7 @@ struct Args {
 
 #ifdef SQ_W4_PROBE_TIMELINE
 // profiling builds only: global-timer stamps of CTA 0's pipeline events (scripts/probe_w4.py)
-__device__ unsigned long long g_tl[8][80];
+__device__ unsigned long long g_tl[12][80];
 #define TL(row, idx) \
   if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (idx) < 80) g_tl[row][idx] = gtimer();
 #else
@@ -213,10 +213,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < nst; ++k, ++q) {
           const int s = q % AST, ng = min(GS, nkb - k * GS);
           mbar_wait_lazy(&aempty[s], ((q / AST) & 1) ^ 1);
+#ifdef SQ_W4_PROBE_NOACT   // profiling builds only: no activation traffic (the MMA reads stale smem)
+          mbar_arrive(&afull[s]);
+#else
           mbar_arrive_expect_tx(&afull[s], ng * C::ACT_BYTES);
           for (int g = 0; g < ng; ++g)
             tma_load_2d(act + (s * GS + g) * C::ACT_BYTES, &tm_act, &afull[s], (kb0 + k * GS + g) * BK,
                         m_tile * NTOK);
+#endif
         }
       }
     }
@@ -268,6 +272,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < nkb; ++i, ++j) {
           const int r = j % RAW;
           mbar_wait_lazy(&rempty[r], ((j / RAW) & 1) ^ 1);
+          if ((j & 1) == 0) TL(8, j >> 1);
           mbar_arrive_expect_tx(&rfull[r], TILE_BYTES);
           bulk_load(raw + r * TILE_BYTES, src + (size_t)i * TILE_BYTES, TILE_BYTES, &rfull[r]);
         }
@@ -299,6 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               p[gg][c] = *reinterpret_cast<const uint4*>(raw + r * TILE_BYTES + c * 2048 + row * 16);
           }
         }
+        if (warp == 4 && lane == 0) TL(9, q);
         fence_proxy_async_smem();   // generic reads of the slots precede the bulk copies that refill them
         __syncwarp();
         if (lane == 0)
@@ -319,6 +325,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         j += ng;
         if (warp == 4 && lane == 0) TL(3, q);
         mbar_wait(&tempty[t], ((q / TST) & 1) ^ 1);
+        if (warp == 4 && lane == 0) TL(10, q);
         tc_fence_after();
 #ifndef SQ_W4_PROBE_NOCONV   // profiling builds only: the A stage is left as is
 #pragma unroll
@@ -394,6 +401,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       __syncwarp();
+      if (warp == C::PROMO0 && lane == 0) TL(0, 2);
       if (lane == 0) mbar_arrive(&sempty[sb]);   // slab read: the stream warp may refill it
       if (!waited) {
         pdl_wait();   // outputs / residual belong to earlier grids too
@@ -426,6 +434,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       } else {
+        if (warp == C::PROMO0 && lane == 0) TL(0, 3);
         named_bar(2, 384);   // converters are past their last read of the ring
         float* red = reinterpret_cast<float*>(raw);   // [NTOK][128]; the weight ring is idle now
 #pragma unroll
@@ -437,7 +446,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (SPLITS > 1) {
     pdl_wait();
     __syncwarp();
+    if (threadIdx.x == 0) TL(0, 4);
     cluster_sync();
+    if (threadIdx.x == 0) TL(0, 5);
     const uint32_t rank = cluster_rank();
     constexpr int TPR = NTOK / SPLITS;
     const int n_tile = unit_n(u_first), m_tile = unit_m(u_first);
@@ -454,6 +465,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (m < args.M && n < args.N)
         store_out(args, m, n, __fmul_rn(sum, args.sa16), args.epi == SQ_EPI_QUANT ? args.col_scale[n] : 1.f);
     }
+    if (threadIdx.x == 0) TL(0, 6);
     cluster_sync();
   }
   if (threadIdx.x == 0) TL(0, 1);

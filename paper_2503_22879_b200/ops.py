@@ -71,6 +71,20 @@ def repack_w4(u4packed: torch.Tensor, N: int, K: int) -> torch.Tensor:
     return out
 
 
+def w4a16_bytes(N: int, K: int, group: int) -> int:
+    return int(lib().sq_w4a16_bytes(N, K, group))
+
+
+def repack_w4a16(u4packed: torch.Tensor, N: int, K: int, group: int) -> torch.Tensor:
+    """u4packed [N x K/2] (SPEC order) -> the W4A16 GEMV layout (sq_repack_w4a16)."""
+    _dev(u4packed, torch.uint8, "u4packed")
+    if u4packed.numel() != N * K // 2:
+        raise ShapeError(f"u4packed must hold {N * K // 2} bytes")
+    out = torch.empty(w4a16_bytes(N, K, group), dtype=torch.uint8, device=u4packed.device)
+    _check(lib().sq_repack_w4a16(u4packed.data_ptr(), N, K, group, out.data_ptr(), _stream()))
+    return out
+
+
 def unpack_w4(w: torch.Tensor, N: int, K: int) -> torch.Tensor:
     _dev(w, torch.uint8, "w4")
     out = torch.empty((N, K // 2), dtype=torch.uint8, device=w.device)
@@ -229,9 +243,16 @@ def gemm_w4a8(a, w4, w_scale, group, s_a, N, epi=EPI_F32, out=None, col_scale=No
 
 
 def gemv_w4a16(x, w4, s_group, group, N, out=None, resid=False):
+    """W4A16 projection: x f32 [M x K] (rounded to bf16 on load), w4 in the sq_repack_w4a16
+    layout, s_group f32 [N x K/group]; out f32 [M x N] (+= when resid)."""
     _dev(x, torch.float32, "x", 2)
     _dev(w4, torch.uint8, "w4")
     M, K = x.shape
+    if w4.numel() < w4a16_bytes(N, K, group):
+        raise ShapeError(f"w4 must hold {w4a16_bytes(N, K, group)} bytes")
+    _dev(s_group, torch.float32, "s_group", 2)
+    if tuple(s_group.shape) != (N, K // group):
+        raise ShapeError(f"s_group must be [{N} x {K // group}]")
     if out is None:
         out = torch.empty((M, N), dtype=torch.float32, device=x.device)
     _dev(out, torch.float32, "out", 2)

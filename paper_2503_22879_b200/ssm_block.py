@@ -173,7 +173,8 @@ class DeviceLinear:
                 self.w = _t(ql.codes.astype(np.int8), torch.int8, dev)
             else:
                 packed = _t(pack_u4_host(ql.codes), torch.uint8, dev)
-                self.w = ops.repack_w4(packed, self.N, self.K)
+                self.w = (ops.repack_w4a16(packed, self.N, self.K, int(ql.group)) if self.kind == "w4a16"
+                          else ops.repack_w4(packed, self.N, self.K))
         if self.kind in ("w4a8", "w4a16"):
             sgr = ql.s_group
             self.s_group = sgr if isinstance(sgr, torch.Tensor) else _t(np.asarray(sgr, np.float32), torch.float32, dev)

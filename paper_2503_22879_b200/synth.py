@@ -106,7 +106,8 @@ def _device_ql(g: torch.Generator, n, k, kind, dev, group=128, in_code_std=U_STD
         s_ch = np.full(n, out_std / (s_a * np.sqrt(k) * in_code_std * 73.3), np.float32)
         return DeviceQL("w8", (n, k), k, w, s_ch=s_ch)
     from . import ops
-    w = torch.randint(0, 256, (ops.w4_bytes(n, k),), generator=g, device=dev, dtype=torch.uint8)   # kernel layout (rows padded to 128)
+    nbytes = ops.w4_bytes(n, k) if kind == "w4a8" else ops.w4a16_bytes(n, k, group)   # kernel layout
+    w = torch.randint(0, 256, (nbytes,), generator=g, device=dev, dtype=torch.uint8)
     std_in = in_code_std * s_a if kind == "w4a8" else 1.0
     s_group = torch.rand((n, k // group), generator=g, device=dev, dtype=torch.float32).add_(0.5).mul_(
         out_std / (np.sqrt(k) * 4.6 * std_in))

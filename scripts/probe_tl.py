@@ -23,14 +23,15 @@ for sname, M, N, K in [("in_proj", 64, 18560, 4096), ("out_proj", 64, 4096, 8192
     for i in range(3):
         ops.gemm_w4a8(a, w4[i], ws[i], 128, 0.01, N, ops.EPI_F32, out)
         torch.cuda.synchronize()
-    buf = np.zeros((8, 80), np.uint64)
+    buf = np.zeros((12, 80), np.uint64)
     lib.sq_probe_w4_timeline(buf.ctypes.data_as(ctypes.c_void_p))
     t0 = buf[0, 0]
     rel = (buf.astype(np.int64) - np.int64(t0)) / 1e3
     names = ["entry/exit", "mma committed", "conv got w0", "conv converted", "conv pub", "mma issued", "mma wait0",
-             "mma got act"]
-    print(f"== {sname}: exit at {rel[0, 1]:.2f} us")
+             "mma got act", "stream issue", "conv loaded", "conv tempty"]
+    print(f"== {sname}: exit at {rel[0, 1]:.2f} us; promotion done {rel[0, 2]:.2f}, split-K: partial staged "
+          f"{rel[0, 3]:.2f}, pre-sync {rel[0, 4]:.2f}, synced {rel[0, 5]:.2f}, reduced {rel[0, 6]:.2f}")
     G = (K // 128 if sname == "in_proj" else K // 128 // ops.gemm_w4a8_splits(M, N, K)) // 2   # steps
-    for r in range(1, 8):
+    for r in range(1, 11):
         vals = rel[r, :G]
         print(f"{names[r]:12s}", " ".join(f"{v:6.2f}" for v in vals))

@@ -52,10 +52,10 @@ def test_bad_shapes_and_layouts_raise(cuda):
     # non-positive scale
     with pytest.raises((ShapeError, ValueError, RuntimeError)):
         ops.quantize_f32(torch.zeros((4, 16), device=dev), 0.0)
-    # W4A16 GEMV: K not a multiple of 32
+    # W4A16 GEMV: the group must divide K
     with pytest.raises((ShapeError, RuntimeError)):
         ops.gemv_w4a16(torch.zeros((1, 48), device=dev), torch.zeros(48, dtype=torch.uint8, device=dev),
-                       torch.ones((2, 1), device=dev), 48, 2)
+                       torch.ones((2, 1), device=dev), 32, 2)
     # conv kernel longer than supported
     with pytest.raises((ShapeError, RuntimeError)):
         ops.conv1d_int8(torch.zeros((4, 8), dtype=torch.int8, device=dev), torch.zeros((8, 9), device=dev),

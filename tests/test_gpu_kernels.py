@@ -117,8 +117,13 @@ def test_gemm_w4a8_exact(cuda, M, N, K, group):
     _same(tres.cpu().numpy(), (res + y).astype(np.float32), "RESID")
 
 
-@pytest.mark.parametrize("M,N,K,group", [(1, 18560 // 4, 4096, 128), (3, 512, 8192, 128), (16, 200, 160, 32)])
+@pytest.mark.parametrize("M,N,K,group", [(1, 18560, 4096, 128), (1, 4096, 8192, 128), (3, 512, 8192, 128),
+                                         (8, 1000, 4096, 64), (5, 100, 256, 16), (11, 33, 192, 32),
+                                         (16, 200, 160, 32)])
 def test_gemv_w4a16(cuda, M, N, K, group):
+    """W4A16 GEMV (bf16 activations, f32 accumulation) vs the oracle (x rounded to bf16 the
+    same way): mma.sync fragment layout for K % 64 == 0, group 64 / 128 (ragged N, several
+    token passes, one or two quads per group), row-major fallback for groups 16 / 32 and K = 160."""
     ops = _ops()
     from paper_2503_22879_b200.ssm_block import pack_u4_host
     r = _rng(3, M, N)
@@ -127,10 +132,16 @@ def test_gemv_w4a16(cuda, M, N, K, group):
     sgrp = r.uniform(1e-3, 1e-2, (N, K // group)).astype(np.float32)
     ql = oq.QLinear("w4a16", codes, s_group=sgrp, group=group)
     ref = oq.qlinear_a16(x, ql)
-    tw = ops.repack_w4(torch.as_tensor(pack_u4_host(codes), device=cuda), N, K)
+    tw = ops.repack_w4a16(torch.as_tensor(pack_u4_host(codes), device=cuda), N, K, group)
     got = ops.gemv_w4a16(torch.as_tensor(x, device=cuda), tw, torch.as_tensor(sgrp, device=cuda), group, N)
     got = got.cpu().numpy()
     assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max() + 1e-6
+    # resid accumulates in place
+    base = r.standard_normal((M, N)).astype(np.float32)
+    tb = torch.as_tensor(base, device=cuda)
+    ops.gemv_w4a16(torch.as_tensor(x, device=cuda), tw, torch.as_tensor(sgrp, device=cuda), group, N, out=tb,
+                   resid=True)
+    assert np.abs(tb.cpu().numpy() - (base + got)).max() <= 1e-6 * np.abs(base + got).max() + 1e-6
 
 
 @pytest.mark.parametrize("M,D", [(5, 256), (64, 4096), (3, 2560)])
