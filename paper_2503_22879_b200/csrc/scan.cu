@@ -325,7 +325,9 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
   const int c0 = blockIdx.x * M1_CH, c = c0 + cl;
   const int b = blockIdx.y;
   pdl_trigger();
-  for (int i = tid; i < M1_CH * N; i += 128) As[i / N][i % N] = p.A[(int64_t)c0 * N + i];
+  // Ȧ = exp(Δ·A) = 2^(Δ·A·log2 e) on the SFU (a few ulp from expf: the scan output is compared
+  // within tolerance and the state is requantised)
+  for (int i = tid; i < M1_CH * N; i += 128) As[i / N][i % N] = p.A[(int64_t)c0 * N + i] * 1.4426950408889634f;
   const float sh = p.s_h[c], Dc = p.D[c];
   pdl_wait();   // inputs come from the previous grid
   int8_t* st = state + ((int64_t)b * p.d_inner + c) * N + qt * 4;
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
       stg.xh[row][cc] = xv;
       stg.gz[row][cc] = silu_f(__fmul_rn((float)r.z[row][cc], p.s_z));
 #pragma unroll
-      for (int n = 0; n < N; ++n) stg.da[row][cc][n] = expf(__fmul_rn(delta, As[cc][n]));
+      for (int n = 0; n < N; ++n) stg.da[row][cc][n] = ex2_approx(__fmul_rn(delta, As[cc][n]));   // As = A·log2 e
     }
     for (int i = tid; i < tn * 32; i += 128) {
       const int row = i >> 5, n = i & 31;
