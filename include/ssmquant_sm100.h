@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQ_ABI_VERSION 3
+#define SQ_ABI_VERSION 4
 
 typedef enum {
   SQ_OK = 0,
@@ -206,11 +206,14 @@ typedef struct {
 } sq_mamba1_params;
 
 /* Mamba1 prefill (T>=1; T=1 is decode): codes x [B*T x d], dt [B*T x d], B/C [B*T x N]
- * (row stride ldbc, C at +N), z [B*T x d]; state int8 [B x d x N]. */
+ * (row stride ldbc, C at +N), z [B*T x d]; state int8 [B x d x N].  ws (16-B aligned,
+ * sq_selective_scan_int8_ws_bytes, may be NULL) enables the time-chunked two-pass scan for long
+ * prompts (two launches instead of one). */
+int64_t sq_selective_scan_int8_ws_bytes(const sq_mamba1_params* p, int B, int T);
 int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T,
                            const int8_t* x, int64_t ldx, const int8_t* dt, int64_t lddt,
                            const int8_t* BC, int64_t ldbc, const int8_t* z, int64_t ldz,
-                           int8_t* state, int state_in, float* y, int64_t ldy, void* stream);
+                           int8_t* state, int state_in, float* y, int64_t ldy, void* ws, void* stream);
 
 /* Mamba1 W4A16 scan on floats: x / dt_raw / z [B*T x d], B|C rows [B*T x 2N] (stride ldbc,
  * C at +N), state f32 [B x d x N].  Replaces the reference's float selective_scan for the

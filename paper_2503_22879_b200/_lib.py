@@ -10,7 +10,7 @@ import os
 
 LIB_NAME = "libssmquant_sm100.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _i8p = C.c_void_p
 _f32p = C.c_void_p
@@ -66,8 +66,9 @@ _SIGS = {
                               _vp, _vp, _i64, _vp], _int),
     "sq_ssd_scan_f32": ([C.POINTER(Mamba2Params), _int, _int, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
                          _vp, _int, _vp, _i64, _vp], _int),
+    "sq_selective_scan_int8_ws_bytes": ([C.POINTER(Mamba1Params), _int, _int], _i64),
     "sq_selective_scan_int8": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
-                                _vp, _int, _vp, _i64, _vp], _int),
+                                _vp, _int, _vp, _i64, _vp, _vp], _int),
     "sq_selective_scan_f32": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                                 _vp, _int, _vp, _i64, _vp], _int),
     "sq_mamba2_decode_ws_bytes": ([C.POINTER(Mamba2DecodeParams), _int], _i64),

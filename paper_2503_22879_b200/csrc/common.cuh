@@ -117,6 +117,15 @@ __device__ __forceinline__ float softplus_f(float v) {
   return v > 20.f ? v : log1pf(expf(v));
 }
 
+// softplus on the SFU (ex2 / lg2 approximations): identity above 20, e^v below -10 (relative error
+// < e^v / 2 there), log(1 + e^v) between; a few ulp from softplus_f elsewhere.  For operands that
+// feed tolerance-compared float math (the Mamba1 scan's Δ), not bit-exact paths.
+__device__ __forceinline__ float softplus_approx(float v) {
+  if (v > 20.f) return v;
+  const float e = __expf(v);
+  return v < -10.f ? e : __logf(1.f + e);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

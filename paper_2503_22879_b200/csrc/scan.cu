@@ -311,11 +311,19 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int NW>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NW) : "memory"); }
 
+// Time-chunked parallel form (MODE 1 / 2, gridDim.z = time chunks): the recurrence h_t = Ȧ_t h_{t-1}
+// + b_t is linear, so pass 1 (MODE 1) runs every chunk from h = 0 (chunk 0 from the real initial
+// state) and keeps its end state and its decay product Π Ȧ; pass 2 (MODE 2) starts chunk j from
+// the folded carry h = Π_j ⊙ h + h_end_j of the chunks before it and re-runs the chunk with the y
+// output; the last chunk requantises the final state.  MODE 0 is the single pass.  The carried
+// start state is the sequential one up to f32 rounding (tolerance-compared, like the oracle's
+// chunked SSD).
+template <int MODE>
 __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_params p, int B, int T, const int8_t* x,
                                                                  int64_t ldx, const int8_t* dt, int64_t lddt,
                                                                  const int8_t* BC, int64_t ldbc, const int8_t* z,
                                                                  int64_t ldz, int8_t* state, int state_in, float* y,
-                                                                 int64_t ldy) {
+                                                                 int64_t ldy, float* ws, int tchunk) {
   constexpr int N = 16;
   __shared__ __align__(16) M1Raw raw[2];
   __shared__ __align__(16) M1Stage stg;
@@ -331,15 +339,32 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
   const float sh = p.s_h[c], Dc = p.D[c];
   pdl_wait();   // inputs come from the previous grid
   int8_t* st = state + ((int64_t)b * p.d_inner + c) * N + qt * 4;
-  float hs[4];
+  const int tc = blockIdx.z, nz = gridDim.z;
+  const int t0 = tc * tchunk, t1 = min(T, t0 + tchunk);   // this CTA's time range
+  // per-chunk summaries [2][nz][B][d_inner][N]: end state (from 0; chunk 0 from the initial state)
+  // and decay product
+  const int64_t cell = ((int64_t)b * p.d_inner + c) * N + qt * 4, zst = (int64_t)B * p.d_inner * N;
+  float hs[4], pr[4] = {1.f, 1.f, 1.f, 1.f};
 #pragma unroll
-  for (int i = 0; i < 4; ++i) hs[i] = state_in ? __fmul_rn((float)st[i], sh) : 0.f;
-  const int nch = (T + M1_TC - 1) / M1_TC;
+  for (int i = 0; i < 4; ++i) hs[i] = (state_in && (MODE == 0 || tc == 0)) ? __fmul_rn((float)st[i], sh) : 0.f;
+  if (MODE == 2 && tc > 0) {   // carry: fold the chunks before this one
+    const float4 h0 = *reinterpret_cast<const float4*>(ws + cell);
+    hs[0] = h0.x; hs[1] = h0.y; hs[2] = h0.z; hs[3] = h0.w;
+    for (int j = 1; j < tc; ++j) {
+      const float4 he = *reinterpret_cast<const float4*>(ws + j * zst + cell);
+      const float4 pj = *reinterpret_cast<const float4*>(ws + (nz + j) * zst + cell);
+      hs[0] = __fadd_rn(__fmul_rn(pj.x, hs[0]), he.x);
+      hs[1] = __fadd_rn(__fmul_rn(pj.y, hs[1]), he.y);
+      hs[2] = __fadd_rn(__fmul_rn(pj.z, hs[2]), he.z);
+      hs[3] = __fadd_rn(__fmul_rn(pj.w, hs[3]), he.w);
+    }
+  }
+  const int nch = (t1 - t0 + M1_TC - 1) / M1_TC;
   auto issue = [&](int ch) {   // M1_TC rows x (x, dt, z, bc) x 2 16-B pieces = 128 pieces: one per thread
     M1Raw& r = raw[ch & 1];
     const int row = tid >> 3, kind = (tid >> 1) & 3, half = tid & 1;
-    const int t = ch * M1_TC + row;
-    if (t < T) {
+    const int t = t0 + ch * M1_TC + row;
+    if (t < t1) {
       const int64_t tok = (int64_t)b * T + t;
       const int8_t* src = kind == 0 ? x + tok * ldx + c0 : kind == 1 ? dt + tok * lddt + c0
                         : kind == 2 ? z + tok * ldz + c0 : BC + tok * ldbc;
@@ -351,7 +376,7 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
   static_assert(M1_TC * 8 == 128, "one 16-B piece per thread per chunk");
   issue(0);
   for (int ch = 0; ch < nch; ++ch) {
-    const int tn = min(M1_TC, T - ch * M1_TC);
+    const int tn = min(M1_TC, t1 - t0 - ch * M1_TC);
     if (ch + 1 < nch) {
       __syncthreads();   // everyone is done reading raw[(ch + 1) & 1] (chunk ch - 1's staging)
       issue(ch + 1);
@@ -361,14 +386,16 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
     }
     __syncthreads();   // raw[ch & 1] landed; the recurrence of chunk ch - 1 is done with stg
     const M1Raw& r = raw[ch & 1];
-    // state-independent operands, all (token, channel) pairs of the chunk in parallel
+    // state-independent operands, all (token, channel) pairs of the chunk in parallel (4 per thread,
+    // unrolled: independent softplus / SiLU / exp chains interleave)
+#pragma unroll 4
     for (int i = tid; i < tn * M1_CH; i += 128) {
       const int row = i / M1_CH, cc = i % M1_CH, ch_g = c0 + cc;
-      const float delta = softplus_f(__fadd_rn(__fmul_rn((float)r.dt[row][cc], p.s_dt), p.dt_bias[ch_g]));
+      const float delta = softplus_approx(__fadd_rn(__fmul_rn((float)r.dt[row][cc], p.s_dt), p.dt_bias[ch_g]));
       const float xv = __fmul_rn((float)r.x[row][cc], p.s_x[ch_g]);
       stg.dx[row][cc] = __fmul_rn(delta, xv);
       stg.xh[row][cc] = xv;
-      stg.gz[row][cc] = silu_f(__fmul_rn((float)r.z[row][cc], p.s_z));
+      stg.gz[row][cc] = silu_approx(__fmul_rn((float)r.z[row][cc], p.s_z));
 #pragma unroll
       for (int n = 0; n < N; ++n) stg.da[row][cc][n] = ex2_approx(__fmul_rn(delta, As[cc][n]));   // As = A·log2 e
     }
@@ -377,25 +404,51 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
       stg.bc[row][n] = __fmul_rn((float)r.bc[row][n], n < N ? p.s_B : p.s_C);
     }
     __syncthreads();
-    float* yrow = y + ((int64_t)b * T + ch * M1_TC) * ldy + c;
+    float* yrow = y + ((int64_t)b * T + t0 + ch * M1_TC) * ldy + c;
 #pragma unroll 4
     for (int tt = 0; tt < tn; ++tt) {
       const float dtx = stg.dx[tt][cl];
       const float4 av = *reinterpret_cast<const float4*>(&stg.da[tt][cl][qt * 4]);
       const float4 bv = *reinterpret_cast<const float4*>(&stg.bc[tt][qt * 4]);
-      const float4 cv = *reinterpret_cast<const float4*>(&stg.bc[tt][N + qt * 4]);
       hs[0] = __fadd_rn(__fmul_rn(av.x, hs[0]), __fmul_rn(dtx, bv.x));
       hs[1] = __fadd_rn(__fmul_rn(av.y, hs[1]), __fmul_rn(dtx, bv.y));
       hs[2] = __fadd_rn(__fmul_rn(av.z, hs[2]), __fmul_rn(dtx, bv.z));
       hs[3] = __fadd_rn(__fmul_rn(av.w, hs[3]), __fmul_rn(dtx, bv.w));
-      float acc = fmaf(hs[3], cv.w, fmaf(hs[2], cv.z, fmaf(hs[1], cv.y, hs[0] * cv.x)));
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (qt == 0) yrow[(int64_t)tt * ldy] = __fmul_rn(__fadd_rn(acc, __fmul_rn(Dc, stg.xh[tt][cl])), stg.gz[tt][cl]);
+      if constexpr (MODE == 1) {
+        pr[0] = __fmul_rn(pr[0], av.x);
+        pr[1] = __fmul_rn(pr[1], av.y);
+        pr[2] = __fmul_rn(pr[2], av.z);
+        pr[3] = __fmul_rn(pr[3], av.w);
+      } else {
+        const float4 cv = *reinterpret_cast<const float4*>(&stg.bc[tt][N + qt * 4]);
+        float acc = fmaf(hs[3], cv.w, fmaf(hs[2], cv.z, fmaf(hs[1], cv.y, hs[0] * cv.x)));
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        if (qt == 0)
+          yrow[(int64_t)tt * ldy] = __fmul_rn(__fadd_rn(acc, __fmul_rn(Dc, stg.xh[tt][cl])), stg.gz[tt][cl]);
+      }
     }
   }
+  if constexpr (MODE == 1) {
+    *reinterpret_cast<float4*>(ws + tc * zst + cell) = make_float4(hs[0], hs[1], hs[2], hs[3]);
+    *reinterpret_cast<float4*>(ws + (nz + tc) * zst + cell) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+  } else if (MODE == 0 || tc == nz - 1) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) st[i] = quant8(hs[i], sh);
+    for (int i = 0; i < 4; ++i) st[i] = quant8(hs[i], sh);
+  }
+}
+
+// time chunks of the two-pass form: up to 16, chunks >= 64 tokens
+static int m1_time_chunks(int d_inner, int B, int T) {
+#ifdef SQ_M1_PROBE_NZ   // profiling builds only: fixed chunk count
+  if (T / SQ_M1_PROBE_NZ >= M1_TC) return SQ_M1_PROBE_NZ;
+#endif
+  // same-box sweep at the 2.8B prefill shape (B=1, T=1024, 160 channel blocks; scripts/probe_m1.py):
+  // 1 / 4 / 8 / 16 chunks -> 250 / 292 / 248 / 224 us
+  const int ctas = (d_inner / M1_CH) * B;
+  int nz = 1;
+  while (nz < 16 && ctas * nz < 16 * 148 && T / (nz * 2) >= 64) nz *= 2;
+  return nz;
 }
 
 // Mamba1 W4A16 (float) scan: the same recurrence on f32 operands and an f32 state
@@ -737,18 +790,37 @@ extern "C" int sq_ssd_scan_f32(const sq_mamba2_params* p, int B, int T, const fl
                               as_stream(stream), "sq_ssd_scan_f32");
 }
 
+extern "C" int64_t sq_selective_scan_int8_ws_bytes(const sq_mamba1_params* p, int B, int T) {
+  if (!p || B < 0 || T < 0) return -1;
+  const int nz = m1_time_chunks(p->d_inner, B, T);
+  return nz > 1 ? (int64_t)2 * nz * B * p->d_inner * p->d_state * 4 : 0;
+}
+
 extern "C" int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T, const int8_t* x, int64_t ldx,
                                       const int8_t* dt, int64_t lddt, const int8_t* BC, int64_t ldbc,
                                       const int8_t* z, int64_t ldz, int8_t* state, int state_in, float* y,
-                                      int64_t ldy, void* stream) {
+                                      int64_t ldy, void* ws, void* stream) {
   SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_selective_scan_int8: bad args");
   SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan_int8: d_state must be 16 (got %d)", p->d_state);
   if (B == 0 || T == 0) return SQ_OK;
   if (T > 1 && p->d_inner % M1_CH == 0 && ldx % 16 == 0 && lddt % 16 == 0 && ldz % 16 == 0 && ldbc % 16 == 0 &&
       !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dt) | reinterpret_cast<uintptr_t>(z) |
          reinterpret_cast<uintptr_t>(BC)) & 15)) {
-    launch_k(PDL_SMALL8, mamba1_scan_staged_kernel, dim3(p->d_inner / M1_CH, B), dim3(128), 0, as_stream(stream), *p,
-             B, T, x, ldx, dt, lddt, BC, ldbc, z, ldz, state, state_in, y, ldy);
+    cudaStream_t st = as_stream(stream);
+    const int nz = ws ? m1_time_chunks(p->d_inner, B, T) : 1;
+    const int tchunk = ((T + nz - 1) / nz + M1_TC - 1) / M1_TC * M1_TC;
+    const dim3 grid(p->d_inner / M1_CH, B, (T + tchunk - 1) / tchunk);
+    if (grid.z == 1) {
+      launch_k(PDL_SMALL8, mamba1_scan_staged_kernel<0>, grid, dim3(128), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc,
+               z, ldz, state, state_in, y, ldy, (float*)nullptr, tchunk);
+    } else {
+      SQ_REQUIRE((reinterpret_cast<uintptr_t>(ws) & 15) == 0, SQ_ERR_LAYOUT, "sq_selective_scan_int8: ws alignment");
+      float* wsf = reinterpret_cast<float*>(ws);
+      launch_k(PDL_SMALL8, mamba1_scan_staged_kernel<1>, grid, dim3(128), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc,
+               z, ldz, state, state_in, y, ldy, wsf, tchunk);
+      launch_k(PDL_SMALL8, mamba1_scan_staged_kernel<2>, grid, dim3(128), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc,
+               z, ldz, state, state_in, y, ldy, wsf, tchunk);
+    }
     return check_launch("sq_selective_scan_int8");
   }
   dim3 grid((p->d_inner + 127) / 128, B);

@@ -380,13 +380,22 @@ def ssd_scan_f32(p, B, T, x, Bm, Cm, dt, z, state, state_in, y):
     return y
 
 
-def selective_scan_int8(p, B, T, x, dt, BC, z, state, state_in, y):
+def selective_scan_int8(p, B, T, x, dt, BC, z, state, state_in, y, ws=None):
+    """Mamba1 int8 selective scan; long prompts run the time-chunked two-pass form in a
+    workspace of sq_selective_scan_int8_ws_bytes (allocated here unless given)."""
     for n, t in (("x", x), ("dt", dt), ("BC", BC), ("z", z)):
         _dev(t, torch.int8, n, 2)
     _dev(state, torch.int8, "state")
+    nb = int(lib().sq_selective_scan_int8_ws_bytes(C.byref(p), B, T))
+    if nb > 0 and ws is None:
+        ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+    if ws is not None and ws.numel() * ws.element_size() < nb:
+        raise ShapeError(f"selective scan workspace needs {nb} bytes")
     _check(lib().sq_selective_scan_int8(C.byref(p), B, T, x.data_ptr(), _ld(x), dt.data_ptr(), _ld(dt),
                                         BC.data_ptr(), _ld(BC), z.data_ptr(), _ld(z), state.data_ptr(),
-                                        int(bool(state_in)), y.data_ptr(), _ld(y), _stream()))
+                                        int(bool(state_in)), y.data_ptr(), _ld(y),
+                                        ws.data_ptr() if nb > 0 else None, _stream()),
+           2 if nb > 0 else 1)
     return y
 
 

@@ -373,3 +373,37 @@ def test_ssd_scan_f32_vs_oracle(cuda, B, T, nh, G, N):
             assert rel <= 1e-4, (state_in, bi, rel)
             hrel = np.abs(st[bi] - rh).max() / np.abs(rh).max()
             assert hrel <= 1e-5, (state_in, bi, hrel)
+
+
+@pytest.mark.parametrize("B,T,d_inner", [(1, 1024, 128), (2, 700, 64)])
+def test_mamba1_scan_time_chunked_matches_single_pass(cuda, B, T, d_inner):
+    """The time-chunked two-pass Mamba1 int8 scan (ws given: chunk end states + decay products,
+    then the carried start states) equals the single pass (oracle-tested above) up to f32
+    rounding of the carried states: y rel <= 1e-5, final state codes within one step."""
+    ops = _ops()
+    from paper_2503_22879_b200 import synth
+    from paper_2503_22879_b200.ssm_block import DeviceBlock, Dims
+    d = Dims("mamba1", 64, d_inner, 16, 1, d_inner, 1, 4, dt_rank=8)
+    blk = DeviceBlock(synth.random_qblock(d, "W8A8", 4), cuda)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(B * T)
+    x, dt, z = (torch.randint(-100, 100, (B * T, d_inner), dtype=torch.int8, device=cuda, generator=g) for _ in range(3))
+    bc = torch.randint(-100, 100, (B * T, 32), dtype=torch.int8, device=cuda, generator=g)
+    nb = int(ops.lib().sq_selective_scan_int8_ws_bytes(ops.C.byref(blk.params), B, T))
+    assert nb > 0   # this shape takes the chunked path
+    h0 = torch.randint(-60, 60, (B, d_inner, 16), dtype=torch.int8, device=cuda, generator=g)
+    outs = []
+    for chunked in (False, True):
+        st = h0.clone()
+        y = torch.empty((B * T, d_inner), device=cuda)
+        if chunked:
+            ops.selective_scan_int8(blk.params, B, T, x, dt, bc, z, st, True, y)
+        else:   # single pass: no workspace
+            ops._check(ops.lib().sq_selective_scan_int8(ops.C.byref(blk.params), B, T, x.data_ptr(), d_inner,
+                                                        dt.data_ptr(), d_inner, bc.data_ptr(), 32, z.data_ptr(),
+                                                        d_inner, st.data_ptr(), 1, y.data_ptr(), d_inner, None,
+                                                        ops._stream()))
+        outs.append((y, st))
+    (y1, s1), (y2, s2) = outs
+    assert ((y2 - y1).abs().max() / y1.abs().max()).item() <= 1e-5
+    assert (s2.int() - s1.int()).abs().max().item() <= 1
