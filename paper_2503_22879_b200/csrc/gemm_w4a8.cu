@@ -75,7 +75,7 @@ struct Cfg {
   static constexpr int OFF_RAW = 0;
   static constexpr int OFF_ACT = RAW * TILE_BYTES;
   static constexpr int OFF_BAR = OFF_ACT + AST * GS * ACT_BYTES;
-  static constexpr int NBAR = 2 * RAW + 2 * AST + 2 * TST + 2 * NACC + 4;
+  static constexpr int NBAR = 2 * RAW + 2 * AST + 2 * TST + 2 * NACC + 4 + 1;
   static constexpr int OFF_SCL = (OFF_BAR + NBAR * 8 + 16 + 127) & ~127;   // 2 unit slabs of group scales
   // dynamic smem = SMEM0 + 2 * nkb * 512 (each unit's [nkb][128] f32 scales, one bulk copy)
   static constexpr int SMEM0 = 1024 + OFF_SCL;
@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* cempty = cfull + NACC;
   uint64_t* sfull = cempty + NACC;      // [2] unit scale slabs
   uint64_t* sempty = sfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 2);
+  uint64_t* cdone = sempty + 2;         // split-K: every converter is past its last ring read
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cdone + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = args.K / BK;
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&cempty[i], C::NPROMO);
     }
     for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::NPROMO); }
+    mbar_init(cdone, C::NCONV * 32);
     fence_barrier_init();
     tma_prefetch(&tm_act);
   }
@@ -341,8 +343,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     // split-K: the partial tile reuses the weight ring; order every converter read of it before
     // the promotion warps' writes (compute-sanitizer racecheck: the mbarrier / tcgen05.commit
-    // chain between them is not a generic-proxy happens-before)
-    if (SPLITS > 1) named_bar(2, 384);
+    // chain between them is not a generic-proxy happens-before) -- an mbarrier arrive (release)
+    // that the promotion warps wait on (acquire)
+    if (SPLITS > 1) mbar_arrive(cdone);   // every converter thread: its own reads precede its arrive
   } else if (warp >= C::PROMO0) {
     // ------------------------------------------------ promotion + epilogue
     const int qd = warp & 3, h = C::NPROMO == 8 ? (warp - C::PROMO0) >> 2 : 0;
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       } else {
         if (warp == C::PROMO0 && lane == 0) TL(0, 3);
-        named_bar(2, 384);   // converters are past their last read of the ring
+        mbar_wait(cdone, 0);   // converters are past their last read of the ring
         float* red = reinterpret_cast<float*>(raw);   // [NTOK][128]; the weight ring is idle now
 #pragma unroll
         for (int e = 0; e < C::HALF; ++e) red[(h * C::HALF + e) * BN + row] = p[e];

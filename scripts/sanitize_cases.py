@@ -1,7 +1,8 @@
 """Small-shape invocations of every mbarrier / TMA / TMEM kernel, one launch each, for
 compute-sanitizer (scripts/sanitize.sh): W4A8 GEMM (persistent and split-K cluster), W8A8 GEMM
 (single and split-K), the fused decode step (prep + state ring + norm), both chunked-SSD engines,
-the int8 conv and the gated norm."""
+the int8 conv and the gated norm, the W4A16 bf16 GEMV (mma.sync and row fallback) and the Mamba1
+int8 scan (single pass and the time-chunked two-pass form)."""
 import os
 import sys
 
@@ -62,7 +63,28 @@ def ssd():
     ops.ssd_scan_int8(blk.params, 1, T, xq, bc, bc, dt, xq, h, False, y, chunk=128)   # tcgen05 engine
 
 
+def w4a16():
+    from paper_2503_22879_b200.ssm_block import pack_u4_host
+    for M, N, K, group in ((1, 100, 256, 128), (5, 64, 512, 64), (3, 40, 160, 32)):
+        codes = np.random.default_rng(0).integers(-8, 8, (N, K)).astype(np.int8)
+        w = ops.repack_w4a16(torch.as_tensor(pack_u4_host(codes), device=dev), N, K, group)
+        x = torch.randn(M, K, device=dev, generator=g)
+        ops.gemv_w4a16(x, w, torch.rand(N, K // group, device=dev, generator=g), group, N)
+
+
+def m1():
+    d = Dims("mamba1", 64, 64, 16, 1, 64, 1, 4, dt_rank=8)
+    blk = DeviceBlock(synth.random_qblock(d, "W8A8", 3), dev)
+    for T in (48, 700):   # single pass / time-chunked
+        x, dt, z = (torch.randint(-100, 100, (T, 64), dtype=torch.int8, device=dev, generator=g) for _ in range(3))
+        bc = torch.randint(-100, 100, (T, 32), dtype=torch.int8, device=dev, generator=g)
+        st = torch.zeros((1, 64, 16), dtype=torch.int8, device=dev)
+        ops.selective_scan_int8(blk.params, 1, T, x, dt, bc, z, st, False, torch.empty((T, 64), device=dev))
+
+
 run("w4a8", w4a8)
 run("w8a8", w8a8)
 run("decode", decode)
 run("ssd", ssd)
+run("w4a16", w4a16)
+run("m1", m1)
