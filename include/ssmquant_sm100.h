@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQ_ABI_VERSION 4
+#define SQ_ABI_VERSION 5
 
 typedef enum {
   SQ_OK = 0,
@@ -107,13 +107,15 @@ int sq_gemm_w4a8_splits(int M, int N, int K);
 /* group scales [N x G] row-major -> tiled [ceil(N/128)][G][128] (sq_group_scale_elems floats) */
 int64_t sq_group_scale_elems(int N, int G);
 int sq_tile_group_scales(const float* s_group, int N, int G, float* dst, void* stream);
-/* W4A16: y[m,n] (+)= sum_g s_group[n,g] * sum_{k in g} w4[n,k] * bf16(x[m,k])  (f32 accumulation;
- * x is f32 in memory and rounded to bf16, RN, on load; resid!=0 adds in place).  w4 is the
- * sq_repack_w4a16 layout (sq_w4a16_bytes): mma.sync bf16 fragment order when K % 64 == 0 and
- * group is 64 or 128, else row-major u4packed. */
+/* W4A16: y[m,n] (+)= sum_g s_group[n,g] * sum_{k in g} w4[n,k] * bf16(x'[m,k])  (f32 accumulation;
+ * x is f32 in memory and rounded to bf16, RN, on load; resid!=0 adds in place).  With norm_w
+ * (nullable) x' = RMSNorm(x) = x * rsqrt(mean_k x^2 + eps) * norm_w (sq_rmsnorm_f32's math), else
+ * x' = x.  w4 is the sq_repack_w4a16 layout (sq_w4a16_bytes): mma.sync bf16 fragment order when
+ * K % 64 == 0 and group is 64 or 128, else row-major u4packed. */
 int64_t sq_w4a16_bytes(int N, int K, int group);
 int sq_repack_w4a16(const uint8_t* u4packed, int N, int K, int group, uint8_t* dst, void* stream);
-int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4 /*sq_repack_w4a16 layout*/,
+int sq_gemv_w4a16(const float* x, int64_t ldx, const float* norm_w /*[K] or NULL*/, float eps,
+                  const uint8_t* w4 /*sq_repack_w4a16 layout*/,
                   const float* s_group /*[N x K/group]*/, int group, int M, int N, int K,
                   float* out, int64_t ldo, int resid, void* stream);
 

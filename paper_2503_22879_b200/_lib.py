@@ -10,7 +10,7 @@ import os
 
 LIB_NAME = "libssmquant_sm100.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _i8p = C.c_void_p
 _f32p = C.c_void_p
@@ -56,7 +56,7 @@ _SIGS = {
     "sq_tile_group_scales": ([_vp, _int, _int, _vp, _vp], _int),
     "sq_w4a16_bytes": ([_int, _int, _int], _i64),
     "sq_repack_w4a16": ([_vp, _int, _int, _int, _vp, _vp], _int),
-    "sq_gemv_w4a16": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _int, _vp], _int),
+    "sq_gemv_w4a16": ([_vp, _i64, _vp, _flt, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _int, _vp], _int),
     "sq_conv1d_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _i64, _vp], _int),
     "sq_conv1d_update_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _vp, _vp, _i64, _vp], _int),
     "sq_conv1d_f32": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _i64, _vp], _int),

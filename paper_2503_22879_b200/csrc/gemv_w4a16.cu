@@ -6,6 +6,9 @@
 // int4 weights are exact in bf16, so every product is exact and only the f32 summation order
 // differs from the oracle (oracle/qblock.py qlinear_a16 rounds x the same way).
 //
+// With norm_w the input rows are RMS-normalised on the way in (the block's gated norm before
+// out_proj, the model's pre-norm before in_proj: one launch fewer each at b=1).
+//
 // Tensor-core path (K % 64 == 0, group 64 or 128): mma.sync m16n8k16 bf16 -> f32 with the weights
 // as the 16-row A operand and up to 8 tokens as the N side.  sq_repack_w4a16 stores the nibbles in
 // fragment order -- per (16-row block, 64-wide K quad) one 16-byte word per lane, one 32-bit word
@@ -72,6 +75,7 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a
 // tokens; the pad keeps the B-fragment reads conflict-free) + the warps' partial tiles.
 template <int NW, int QPG, int DG>
 __global__ void __launch_bounds__(NW * 32) gemv_w4a16_mma_kernel(const float* x, int64_t ldx,
+                                                                const float* __restrict__ norm_w, float eps,
                                                                 const uint8_t* __restrict__ w,
                                                                 const float* __restrict__ sgrp, int M, int N,
                                                                 int K, float* out, int64_t ldo, int resid) {
@@ -109,6 +113,42 @@ __global__ void __launch_bounds__(NW * 32) gemv_w4a16_mma_kernel(const float* x,
 #pragma unroll
   for (int i = 0; i < 4; ++i) sc[i] = g0 < g1 ? __ldg(srow[i] + g0) : 0.f;
   pdl_wait();   // x / out come from earlier grids
+  if (norm_w) {
+    // fused RMSNorm of the input rows (rmsnorm_f32's math: f64 Σx², r = x·rfac·γ): pass 1 sums
+    // the row, pass 2 re-reads it (L1 / L2) and stores bf16(r)
+    __shared__ double red[NW];
+    __shared__ float rfac_s;
+    for (int m = 0; m < M; ++m) {
+      const float* xr = x + (int64_t)m * ldx;
+      double ss = 0.0;
+#pragma unroll 4
+      for (int k = threadIdx.x * 4; k < K; k += NW * 32 * 4) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + k);
+        ss += (double)v.x * (double)v.x + (double)v.y * (double)v.y + (double)v.z * (double)v.z +
+              (double)v.w * (double)v.w;
+      }
+      ss = warp_sum_d(ss);
+      if (lane == 0) red[warp] = ss;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < NW; ++i) t += red[i];
+        const float ms = (float)(t / (double)K);
+        rfac_s = __fdiv_rn(1.0f, sqrtf(__fadd_rn(ms, eps)));
+      }
+      __syncthreads();
+      const float rf = rfac_s;
+#pragma unroll 4
+      for (int k = threadIdx.x * 4; k < K; k += NW * 32 * 4) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + k);
+        const float4 g = __ldg(reinterpret_cast<const float4*>(norm_w + k));
+        *reinterpret_cast<uint2*>(xs + (size_t)m * KP + k) =
+            make_uint2(bf16_rn_pair(__fmul_rn(__fmul_rn(v.x, rf), g.x), __fmul_rn(__fmul_rn(v.y, rf), g.y)),
+                       bf16_rn_pair(__fmul_rn(__fmul_rn(v.z, rf), g.z), __fmul_rn(__fmul_rn(v.w, rf), g.w)));
+      }
+      __syncthreads();   // red / rfac_s reused by the next row
+    }
+  } else {
   // activation staging (the loads are independent: the compiler keeps several in flight)
 #ifndef SQ_GV_PROBE_NOSTAGE   // profiling builds only: x left unstaged
 #pragma unroll 4
@@ -118,6 +158,7 @@ __global__ void __launch_bounds__(NW * 32) gemv_w4a16_mma_kernel(const float* x,
     *reinterpret_cast<uint2*>(xs + (size_t)m * KP + k) = make_uint2(bf16_rn_pair(v.x, v.y), bf16_rn_pair(v.z, v.w));
   }
 #endif
+  }
   for (int i = threadIdx.x * 2; i < K; i += NW * 32 * 2) *reinterpret_cast<uint32_t*>(xs + (size_t)M * KP + i) = 0u;
   __syncthreads();
   const uint32_t* xrow = reinterpret_cast<const uint32_t*>(xs + (size_t)(gid < M ? gid : M) * KP) + t4;
@@ -198,13 +239,36 @@ __global__ void __launch_bounds__(NW * 32) gemv_w4a16_mma_kernel(const float* x,
 // Fallback (other K / group): one warp per output row, row-major u4packed
 // weights (low nibble = even k), bf16-rounded activations in smem.
 __global__ void __launch_bounds__(256) gemv_w4a16_rows_kernel(const float* x, int64_t ldx,
+                                                              const float* __restrict__ norm_w, float eps,
                                                               const uint8_t* __restrict__ w,
                                                               const float* __restrict__ sgrp, int group, int M,
                                                               int N, int K, float* out, int64_t ldo, int resid) {
   extern __shared__ float xr[];  // [M][K] bf16-rounded, kept in f32
+  __shared__ double red[8];
+  __shared__ float rfs[GV_TOK];
+  if (norm_w) {   // fused RMSNorm (rmsnorm_f32's math) of each input row
+    for (int m = 0; m < M; ++m) {
+      double ss = 0.0;
+      for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        const float v = x[(int64_t)m * ldx + k];
+        ss += (double)v * (double)v;
+      }
+      ss = warp_sum_d(ss);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        rfs[m] = __fdiv_rn(1.0f, sqrtf(__fadd_rn((float)(t / (double)K), eps)));
+      }
+      __syncthreads();
+    }
+  }
   for (int i = threadIdx.x; i < M * K; i += blockDim.x) {
     const int m = i / K, k = i % K;
-    xr[i] = __bfloat162float(__float2bfloat16_rn(x[(int64_t)m * ldx + k]));
+    float v = x[(int64_t)m * ldx + k];
+    if (norm_w) v = __fmul_rn(__fmul_rn(v, rfs[m]), __ldg(norm_w + k));
+    xr[i] = __bfloat162float(__float2bfloat16_rn(v));
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warps = blockDim.x >> 5;
@@ -282,8 +346,9 @@ extern "C" int sq_repack_w4a16(const uint8_t* u4packed, int N, int K, int group,
   return check_launch("sq_repack_w4a16");
 }
 
-extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4, const float* s_group, int group, int M,
-                             int N, int K, float* out, int64_t ldo, int resid, void* stream) {
+extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const float* norm_w, float eps, const uint8_t* w4,
+                             const float* s_group, int group, int M, int N, int K, float* out, int64_t ldo, int resid,
+                             void* stream) {
   SQ_REQUIRE(x && w4 && s_group && out && M >= 0 && N > 0 && K > 0 && group > 0 && K % group == 0 && K % 2 == 0,
              SQ_ERR_SHAPE, "sq_gemv_w4a16: bad shape M=%d N=%d K=%d group=%d", M, N, K, group);
   cudaStream_t st = as_stream(stream);
@@ -306,8 +371,8 @@ extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4, con
       SQ_REQUIRE(smem <= 227 * 1024, SQ_ERR_SHAPE, "sq_gemv_w4a16: K too large");
       auto launch = [&](auto kern) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        launch_k(PDL_SMALL, kern, dim3(cta), dim3(nw * 32), smem, st, x + (int64_t)m0 * ldx, ldx, w4, s_group, mc, N,
-                 K, out + (int64_t)m0 * ldo, ldo, resid);
+        launch_k(PDL_SMALL, kern, dim3(cta), dim3(nw * 32), smem, st, x + (int64_t)m0 * ldx, ldx, norm_w, eps, w4,
+                 s_group, mc, N, K, out + (int64_t)m0 * ldo, ldo, resid);
       };
 #ifndef SQ_GV_DG
 #define SQ_GV_DG 3
@@ -332,8 +397,8 @@ extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const uint8_t* w4, con
       cudaFuncSetAttribute(gemv_w4a16_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = (N + 7) / 8;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    gemv_w4a16_rows_kernel<<<blocks, 256, smem, st>>>(x + (int64_t)m0 * ldx, ldx, w4, s_group, group, mc, N, K,
-                                                      out + (int64_t)m0 * ldo, ldo, resid);
+    gemv_w4a16_rows_kernel<<<blocks, 256, smem, st>>>(x + (int64_t)m0 * ldx, ldx, norm_w, eps, w4, s_group, group,
+                                                      mc, N, K, out + (int64_t)m0 * ldo, ldo, resid);
   }
   return check_launch("sq_gemv_w4a16");
 }

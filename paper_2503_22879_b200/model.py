@@ -110,8 +110,8 @@ class QuantizedMambaLM:
                 ops.rmsnorm_quant(h, self.layer_norms[l], EPS_NORM, blk.s_u, ws["u"])
                 blk.forward_codes(ws["u"], B, T, st, state_in, resid=h, ws=ws)
             else:
-                ops.rmsnorm_f32(h, self.layer_norms[l], EPS_NORM, ws["uf"])
-                blk.forward_a16(ws["uf"], B, T, st, state_in, resid=h, ws=ws)
+                # the pre-norm runs inside the in_proj GEMV (h is read before out_proj adds to it)
+                blk.forward_a16(h, B, T, st, state_in, resid=h, ws=ws, u_norm=self.layer_norms[l])
         if all_logits:
             hs = h
             hq, lg = ws["hq"], ws["logits"]

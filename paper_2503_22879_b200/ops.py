@@ -242,9 +242,10 @@ def gemm_w4a8(a, w4, w_scale, group, s_a, N, epi=EPI_F32, out=None, col_scale=No
     return out
 
 
-def gemv_w4a16(x, w4, s_group, group, N, out=None, resid=False):
-    """W4A16 projection: x f32 [M x K] (rounded to bf16 on load), w4 in the sq_repack_w4a16
-    layout, s_group f32 [N x K/group]; out f32 [M x N] (+= when resid)."""
+def gemv_w4a16(x, w4, s_group, group, N, out=None, resid=False, norm_w=None, eps=1e-5):
+    """W4A16 projection: x f32 [M x K] (rounded to bf16 on load; RMS-normalised with norm_w
+    first when given), w4 in the sq_repack_w4a16 layout, s_group f32 [N x K/group]; out f32
+    [M x N] (+= when resid)."""
     _dev(x, torch.float32, "x", 2)
     _dev(w4, torch.uint8, "w4")
     M, K = x.shape
@@ -253,11 +254,16 @@ def gemv_w4a16(x, w4, s_group, group, N, out=None, resid=False):
     _dev(s_group, torch.float32, "s_group", 2)
     if tuple(s_group.shape) != (N, K // group):
         raise ShapeError(f"s_group must be [{N} x {K // group}]")
+    if norm_w is not None:
+        _dev(norm_w, torch.float32, "norm_w", 1)
+        if norm_w.numel() != K:
+            raise ShapeError(f"norm_w must hold {K} values")
     if out is None:
         out = torch.empty((M, N), dtype=torch.float32, device=x.device)
     _dev(out, torch.float32, "out", 2)
-    _check(lib().sq_gemv_w4a16(x.data_ptr(), _ld(x), w4.data_ptr(), s_group.data_ptr(), group, M, N, K,
-                               out.data_ptr(), _ld(out), int(bool(resid)), _stream()))
+    _check(lib().sq_gemv_w4a16(x.data_ptr(), _ld(x), norm_w.data_ptr() if norm_w is not None else None,
+                               float(eps), w4.data_ptr(), s_group.data_ptr(), group, M, N, K, out.data_ptr(),
+                               _ld(out), int(bool(resid)), _stream()))
     return out
 
 

@@ -203,8 +203,9 @@ class DeviceLinear:
             return ops.gemm_w4a8(a_codes, self.w, self.ws, self.group, self.s_a, self.N, epi, out, col_scale)
         raise ShapeError("A8 GEMM on a W4A16 projection")
 
-    def a16(self, x, out=None, resid=False):
-        return ops.gemv_w4a16(x, self.w, self.s_group, self.group, self.N, out, resid)
+    def a16(self, x, out=None, resid=False, norm_w=None):
+        """W4A16 projection of x (RMS-normalised with norm_w on the way in when given)."""
+        return ops.gemv_w4a16(x, self.w, self.s_group, self.group, self.N, out, resid, norm_w, EPS_NORM)
 
     @property
     def nbytes(self):
@@ -351,12 +352,14 @@ class DeviceBlock:
             return self.out_proj.a8(yq, ops.EPI_RESID, resid)
         return self.out_proj.a8(yq, ops.EPI_F32, ws.get("out"))
 
-    def forward_a16(self, u, B, T, state: SsmState, state_in: bool, resid=None, ws=None):
-        """W4A16 float path on f32 input u [B*T × d_model]."""
+    def forward_a16(self, u, B, T, state: SsmState, state_in: bool, resid=None, ws=None, u_norm=None):
+        """W4A16 float path on f32 input u [B*T × d_model] (when ``u_norm`` is given, u is the raw
+        residual stream and the in_proj GEMV applies the model's pre-norm on the way in).  The
+        gated RMSNorm runs inside the out_proj GEMV's input staging."""
         d = self.dims
         di = d.d_inner
         ws = ws if ws is not None else {}
-        zx = self.in_proj.a16(u, ws.get("zxf"))
+        zx = self.in_proj.a16(u, ws.get("zxf"), norm_w=u_norm)
         if d.variant == "mamba1":   # in_proj rows z | x; x_proj rows Δ_low | B | C (LEDGER G4)
             R = d.dt_rank
             cv = ops.conv1d_f32(zx[:, di:], self.conv_w, self.conv_b, B, T, state.conv_cache, state_in,
@@ -367,22 +370,18 @@ class DeviceBlock:
             if y is None:
                 y = torch.empty((B * T, di), dtype=torch.float32, device=u.device)
             ops.selective_scan_f32(self.params, B, T, cv, dtr, xd[:, R:], zx[:, :di], state.h, state_in, y)
-            r = ops.rmsnorm_f32(y, self.norm_w, EPS_NORM, ws.get("r"))
-            if resid is not None:
-                return self.out_proj.a16(r, resid, resid=True)
-            return self.out_proj.a16(r, ws.get("out"))
-        gn = d.n_state_groups * d.d_state
-        xbc = zx[:, di:2 * di + 2 * gn]
-        cv = ops.conv1d_f32(xbc, self.conv_w, self.conv_b, B, T, state.conv_cache, state_in, ws.get("convf"))
-        y = ws.get("y")
-        if y is None:
-            y = torch.empty((B * T, di), dtype=torch.float32, device=u.device)
-        ops.ssd_scan_f32(self.params, B, T, cv[:, :di], cv[:, di:di + gn], cv[:, di + gn:], zx[:, 2 * di + 2 * gn:],
-                         zx[:, :di], state.h, state_in, y)
-        r = ops.rmsnorm_f32(y, self.norm_w, EPS_NORM, ws.get("r"))
+        else:
+            gn = d.n_state_groups * d.d_state
+            xbc = zx[:, di:2 * di + 2 * gn]
+            cv = ops.conv1d_f32(xbc, self.conv_w, self.conv_b, B, T, state.conv_cache, state_in, ws.get("convf"))
+            y = ws.get("y")
+            if y is None:
+                y = torch.empty((B * T, di), dtype=torch.float32, device=u.device)
+            ops.ssd_scan_f32(self.params, B, T, cv[:, :di], cv[:, di:di + gn], cv[:, di + gn:],
+                             zx[:, 2 * di + 2 * gn:], zx[:, :di], state.h, state_in, y)
         if resid is not None:
-            return self.out_proj.a16(r, resid, resid=True)
-        return self.out_proj.a16(r, ws.get("out"))
+            return self.out_proj.a16(y, resid, resid=True, norm_w=self.norm_w)
+        return self.out_proj.a16(y, ws.get("out"), norm_w=self.norm_w)
 
 
 # ============================================================== SPEC float ops on the GPU

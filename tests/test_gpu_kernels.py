@@ -136,6 +136,12 @@ def test_gemv_w4a16(cuda, M, N, K, group):
     got = ops.gemv_w4a16(torch.as_tensor(x, device=cuda), tw, torch.as_tensor(sgrp, device=cuda), group, N)
     got = got.cpu().numpy()
     assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max() + 1e-6
+    # fused RMSNorm of the input rows (the block's gated norm / the model's pre-norm)
+    gam = r.uniform(0.5, 1.5, K).astype(np.float32)
+    refn = oq.qlinear_a16(osb.rmsnorm(x, gam), ql)
+    gotn = ops.gemv_w4a16(torch.as_tensor(x, device=cuda), tw, torch.as_tensor(sgrp, device=cuda), group, N,
+                          norm_w=torch.as_tensor(gam, device=cuda)).cpu().numpy()
+    assert np.abs(gotn - refn).max() <= 2e-5 * np.abs(refn).max() + 1e-6
     # resid accumulates in place
     base = r.standard_normal((M, N)).astype(np.float32)
     tb = torch.as_tensor(base, device=cuda)
