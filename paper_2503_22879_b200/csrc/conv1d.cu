@@ -183,6 +183,31 @@ __global__ void conv1d_cache_kernel(const T_* x, int64_t ldx, int B, int T, int 
   for (int j = 0; j < Kc - 1; ++j) cache[((int64_t)b * (Kc - 1) + j) * C + c] = nv[j];
 }
 
+// f32 decode step (T = 1): the window is the cache (or zeros) + the new input; the output and the
+// shifted cache in one launch (conv1d_prefill_kernel's op order: acc = b + Σ_j w_j·win_j, SiLU)
+__global__ void conv1d_update_f32_kernel(const float* x, int64_t ldx, const float* __restrict__ w,
+                                         const float* __restrict__ bias, int B, int C, int Kc, float* cache,
+                                         int cache_in, float* out, int64_t ldo) {
+  pdl_trigger();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (c >= C) return;
+  float wc[kMaxK];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) wc[j] = j < Kc ? w[c * Kc + j] : 0.f;
+  const float bc = bias[c];
+  pdl_wait();   // x and the cache come from earlier grids
+  float* cr = cache + (int64_t)b * (Kc - 1) * C + c;
+  float win[kMaxK];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) win[j] = (j < Kc - 1 && cache_in) ? cr[(int64_t)j * C] : 0.f;
+  win[Kc - 1] = x[(int64_t)b * ldx + c];
+  float acc = bc;
+  for (int j = 0; j < Kc; ++j) acc = __fadd_rn(acc, __fmul_rn(wc[j], win[j]));
+  out[(int64_t)b * ldo + c] = silu_f(acc);
+  for (int j = 0; j < Kc - 1; ++j) cr[(int64_t)j * C] = win[j + 1];
+}
+
 __global__ void conv1d_update_kernel(const int8_t* x, int64_t ldx, const float* __restrict__ w,
                                      const float* __restrict__ bias, const float* __restrict__ s_in,
                                      const float* __restrict__ s_out, int B, int C, int Kc, int8_t* cache,
@@ -231,6 +256,11 @@ extern "C" int sq_conv1d_f32(const float* x, int64_t ldx, const float* w, const 
   SQ_REQUIRE(B >= 0 && T >= 0 && C > 0 && Kc >= 1 && Kc <= kMaxK, SQ_ERR_SHAPE, "sq_conv1d_f32: bad shape");
   if (B == 0 || T == 0) return SQ_OK;
   cudaStream_t st = as_stream(stream);
+  if (T == 1 && Kc > 1) {   // decode step: output + cache shift in one launch
+    launch_k(PDL_SMALL, conv1d_update_f32_kernel, dim3((C + 127) / 128, B), dim3(128), 0, st, x, ldx, w, bias, B, C, Kc,
+             cache, cache_in, out, ldo);
+    return check_launch("sq_conv1d_f32");
+  }
   dim3 g((C + 127) / 128, (T + kSeg - 1) / kSeg, B);
   launch_k(PDL_SMALL, conv1d_prefill_kernel<float, float, false>, g, dim3(128), 0, st, x, ldx, w, bias, (const float*)nullptr, (const float*)nullptr, B, T, C, Kc, cache,
                                                                 cache_in, out, ldo);

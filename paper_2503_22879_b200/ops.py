@@ -296,7 +296,7 @@ def conv1d_f32(x, w, bias, B, T, cache, cache_in=False, out=None):
     C_, Kc = w.shape
     out = torch.empty((B * T, C_), dtype=torch.float32, device=x.device) if out is None else out
     _check(lib().sq_conv1d_f32(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), B, T, C_, Kc, cache.data_ptr(),
-                               int(bool(cache_in)), out.data_ptr(), _ld(out), _stream()), 1 + (Kc > 1))
+                               int(bool(cache_in)), out.data_ptr(), _ld(out), _stream()), 1 + (Kc > 1 and T > 1))
     return out
 
 
