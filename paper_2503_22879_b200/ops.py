@@ -35,6 +35,17 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+def _need(t: torch.Tensor, n: int, name: str):
+    """Buffers the kernels index by the launch dimensions must hold at least n elements."""
+    if t.numel() < n:
+        raise ShapeError(f"{name} must hold at least {n} elements, got {t.numel()}")
+
+
+def _rows(t: torch.Tensor, n: int, name: str):
+    if t.dim() >= 1 and t.shape[0] < n:
+        raise ShapeError(f"{name} must have at least {n} rows, got {t.shape[0]}")
+
+
 def _dev(t: torch.Tensor, dtype, name, dims=None):
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise LayoutError(f"{name} must be a CUDA tensor (no CPU fallback)")
@@ -272,7 +283,10 @@ def conv1d_int8(x, w, bias, s_in, s_out, B, T, cache, cache_in=False, out=None):
     _dev(x, torch.int8, "x", 2)
     _dev(cache, torch.int8, "cache")
     C_, Kc = w.shape
+    _rows(x, B * T, "x")
+    _need(cache, B * (Kc - 1) * C_, "cache [B x (K-1) x C]")
     out = torch.empty((B * T, C_), dtype=torch.int8, device=x.device) if out is None else out
+    _rows(out, B * T, "out")
     _check(lib().sq_conv1d_int8(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), s_in.data_ptr(),
                                 s_out.data_ptr(), B, T, C_, Kc, cache.data_ptr(), int(bool(cache_in)),
                                 out.data_ptr(), _ld(out), _stream()), 1 + (Kc > 1))
@@ -284,7 +298,9 @@ def conv1d_update_int8(x, w, bias, s_in, s_out, cache, out=None):
     _dev(cache, torch.int8, "cache")
     B = x.shape[0]
     C_, Kc = w.shape
+    _need(cache, B * (Kc - 1) * C_, "cache [B x (K-1) x C]")
     out = torch.empty((B, C_), dtype=torch.int8, device=x.device) if out is None else out
+    _rows(out, B, "out")
     _check(lib().sq_conv1d_update_int8(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), s_in.data_ptr(),
                                        s_out.data_ptr(), B, C_, Kc, cache.data_ptr(), out.data_ptr(), _ld(out),
                                        _stream()))
@@ -293,8 +309,12 @@ def conv1d_update_int8(x, w, bias, s_in, s_out, cache, out=None):
 
 def conv1d_f32(x, w, bias, B, T, cache, cache_in=False, out=None):
     _dev(x, torch.float32, "x", 2)
+    _dev(cache, torch.float32, "cache")
     C_, Kc = w.shape
+    _rows(x, B * T, "x")
+    _need(cache, B * (Kc - 1) * C_, "cache [B x (K-1) x C]")
     out = torch.empty((B * T, C_), dtype=torch.float32, device=x.device) if out is None else out
+    _rows(out, B * T, "out")
     _check(lib().sq_conv1d_f32(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), B, T, C_, Kc, cache.data_ptr(),
                                int(bool(cache_in)), out.data_ptr(), _ld(out), _stream()), 1 + (Kc > 1 and T > 1))
     return out
@@ -330,6 +350,10 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     _dev(conv_cache, torch.int8, "conv_cache")
     _dev(state, torch.int8, "state")
     di = p.ssm.n_heads * p.ssm.head_dim
+    conv_dim = di + 2 * p.ssm.n_groups * p.ssm.d_state
+    _rows(zx, B, "zx")
+    _need(state, B * p.ssm.n_heads * p.ssm.head_dim * p.ssm.d_state, "state [B x nh x P x N]")
+    _need(conv_cache, B * (p.conv_kernel - 1) * conv_dim, "conv_cache [B x (K-1) x conv_dim]")
     if yq is None:
         yq = torch.empty((B, di), dtype=torch.int8, device=zx.device)
     if y is None:
@@ -358,6 +382,7 @@ def ssd_scan_int8(p, B, T, x, Bm, Cm, dt, z, state, state_in, y, chunk=256):
     for n, t in (("x", x), ("B", Bm), ("C", Cm), ("dt", dt), ("z", z)):
         _dev(t, torch.int8, n, 2)
     _dev(state, torch.int8, "state")
+    _need(state, B * p.n_heads * p.head_dim * p.d_state, "state [B x nh x P x N]")
     _dev(y, torch.float32, "y", 2)
     _check(lib().sq_ssd_scan_int8(C.byref(p), B, T, x.data_ptr(), _ld(x), Bm.data_ptr(), Cm.data_ptr(), _ld(Bm),
                                   dt.data_ptr(), _ld(dt), z.data_ptr(), _ld(z), state.data_ptr(),
@@ -369,6 +394,7 @@ def state_update_int8(p, B, x, Bm, Cm, dt, z, state, y):
     for n, t in (("x", x), ("B", Bm), ("C", Cm), ("dt", dt), ("z", z)):
         _dev(t, torch.int8, n, 2)
     _dev(state, torch.int8, "state")
+    _need(state, B * p.n_heads * p.head_dim * p.d_state, "state [B x nh x P x N]")
     _dev(y, torch.float32, "y", 2)
     _check(lib().sq_state_update_int8(C.byref(p), B, x.data_ptr(), _ld(x), Bm.data_ptr(), Cm.data_ptr(), _ld(Bm),
                                       dt.data_ptr(), _ld(dt), z.data_ptr(), _ld(z), state.data_ptr(), y.data_ptr(),
@@ -380,6 +406,7 @@ def ssd_scan_f32(p, B, T, x, Bm, Cm, dt, z, state, state_in, y):
     for n, t in (("x", x), ("B", Bm), ("C", Cm), ("dt", dt), ("z", z)):
         _dev(t, torch.float32, n, 2)
     _dev(state, torch.float32, "state")
+    _need(state, B * p.n_heads * p.head_dim * p.d_state, "state [B x nh x P x N]")
     _check(lib().sq_ssd_scan_f32(C.byref(p), B, T, x.data_ptr(), _ld(x), Bm.data_ptr(), Cm.data_ptr(), _ld(Bm),
                                  dt.data_ptr(), _ld(dt), z.data_ptr(), _ld(z), state.data_ptr(), int(bool(state_in)),
                                  y.data_ptr(), _ld(y), _stream()))
@@ -392,6 +419,7 @@ def selective_scan_int8(p, B, T, x, dt, BC, z, state, state_in, y, ws=None):
     for n, t in (("x", x), ("dt", dt), ("BC", BC), ("z", z)):
         _dev(t, torch.int8, n, 2)
     _dev(state, torch.int8, "state")
+    _need(state, B * p.d_inner * p.d_state, "state [B x d_inner x N]")
     nb = int(lib().sq_selective_scan_int8_ws_bytes(C.byref(p), B, T))
     if nb > 0 and ws is None:
         ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
@@ -410,6 +438,7 @@ def selective_scan_f32(p, B, T, x, dt, BC, z, state, state_in, y):
     for n, t in (("x", x), ("dt", dt), ("BC", BC), ("z", z), ("y", y)):
         _dev(t, torch.float32, n, 2)
     _dev(state, torch.float32, "state")
+    _need(state, B * p.d_inner * p.d_state, "state [B x d_inner x N]")
     _check(lib().sq_selective_scan_f32(C.byref(p), B, T, x.data_ptr(), _ld(x), dt.data_ptr(), _ld(dt),
                                        BC.data_ptr(), _ld(BC), z.data_ptr(), _ld(z), state.data_ptr(),
                                        int(bool(state_in)), y.data_ptr(), _ld(y), _stream()))

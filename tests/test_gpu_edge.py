@@ -56,6 +56,22 @@ def test_bad_shapes_and_layouts_raise(cuda):
     with pytest.raises((ShapeError, RuntimeError)):
         ops.gemv_w4a16(torch.zeros((1, 48), device=dev), torch.zeros(48, dtype=torch.uint8, device=dev),
                        torch.ones((2, 1), device=dev), 32, 2)
+    # state / cache buffers smaller than the launch dimensions (would be out-of-bounds writes)
+    C = 64
+    wt, bt, sc = torch.randn((C, 4), device=dev), torch.zeros(C, device=dev), torch.full((C,), 0.02, device=dev)
+    with pytest.raises(ShapeError):
+        ops.conv1d_int8(torch.zeros((2 * 5, C), dtype=torch.int8, device=dev), wt, bt, sc, sc, 2, 5,
+                        torch.zeros((1, 3, C), dtype=torch.int8, device=dev))
+    with pytest.raises(ShapeError):
+        ops.conv1d_update_int8(torch.zeros((3, C), dtype=torch.int8, device=dev), wt, bt, sc, sc,
+                               torch.zeros((2, 3, C), dtype=torch.int8, device=dev))
+    from paper_2503_22879_b200 import synth
+    from paper_2503_22879_b200.ssm_block import DeviceBlock, Dims
+    blk = DeviceBlock(synth.random_qblock(Dims("mamba2", 256, 512, 64, 8, 64, 2, 4), "W8A8", 1), dev)
+    st = blk.new_state(2, dev)
+    zx = torch.zeros((3, blk.dims.in_proj_out), dtype=torch.int8, device=dev)
+    with pytest.raises(ShapeError):   # state and conv cache for 2 sequences, step for 3
+        ops.mamba2_decode_step_int8(blk.decode_params, 3, zx, st.conv_cache, st.h)
     # conv kernel longer than supported
     with pytest.raises((ShapeError, RuntimeError)):
         ops.conv1d_int8(torch.zeros((4, 8), dtype=torch.int8, device=dev), torch.zeros((8, 9), device=dev),

@@ -32,9 +32,10 @@ def code_diff(a, b):
     return int(d.max(initial=0)), float((d > 0).mean()) if d.size else 0.0
 
 
-# K % 128 != 0 runs the mma.sync kernel, the rest the tcgen05 kernels
+# K % 128 != 0 with M > 16 runs the mma.sync kernel, the rest the tcgen05 kernels
 @pytest.mark.parametrize("M,N,K", [(1, 128, 64), (64, 18560 // 8, 4096), (37, 300, 160), (256, 1024, 512),
-                                   (64, 4096, 8192), (200, 2560, 5120), (1, 5120, 256)])
+                                   (64, 4096, 8192), (200, 2560, 5120), (1, 5120, 256), (1, 5120, 160),
+                                   (3, 192, 5120), (8, 1000, 2560), (5, 10240, 2560)])
 def test_gemm_w8a8_exact(cuda, M, N, K):
     ops = _ops()
     r = _rng(1, M, N)
