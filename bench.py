@@ -445,14 +445,26 @@ def run_decode(args, wl, world, rank, local):
     torch.cuda.set_device(dev)
     d = Dims(*wl["dims"])
     from paper_2503_22879_b200 import dist as pdist
-    if args.global_batch:   # strong scaling: a fixed global batch sharded over the ranks
+    tp_group = None
+    if args.parallel == "heads":   # head shard: every rank runs the whole batch on nh/W heads per layer
+        if d.variant != "mamba2":
+            raise SystemExit("--parallel heads needs a Mamba2 workload")
+        B = args.global_batch or wl["batch"]
+        global_batch, scaling = B, "strong"
+        if world > 1:
+            import torch.distributed as tdist
+            tp_group = tdist.group.WORLD
+        parallelism = f"tp{world} (head shards, one NCCL all_reduce of the out_proj partials per layer)"
+    elif args.global_batch:   # strong scaling: a fixed global batch sharded over the ranks
         lo, hi = pdist.shard_range(args.global_batch, world, rank)
         B = hi - lo
         global_batch, scaling = args.global_batch, "strong"
+        parallelism = f"dp{world} (batch-shard replicas, no collective)"
     else:                   # weak scaling: wl["batch"] sequences per GPU
         B = wl["batch"]
         global_batch, scaling = B * world, "weak"
-    lm = synth.synthetic_lm(d, wl["layers"], wl["profile"], wl["vocab"], dev, seed=rank)
+        parallelism = f"dp{world} (batch-shard replicas, no collective)"
+    lm = synth.synthetic_lm(d, wl["layers"], wl["profile"], wl["vocab"], dev, seed=rank, tp_group=tp_group)
     states = lm.new_states(B)
     g = torch.Generator(device=dev)
     g.manual_seed(7 + rank)
@@ -509,6 +521,7 @@ def run_decode(args, wl, world, rank, local):
     # K6 gated norm + FWHT + quant), timed live with CUDA events on the launch stream, cycling
     # through all layers' states (67 MB each at b=64, so every launch streams from HBM, not L2)
     blk = lm.blocks[0]
+    d = blk.dims   # the blocks' dims (a head shard's under --parallel heads)
     di, gn = d.d_inner, d.n_state_groups * d.d_state
     reps = 2 * len(lm.blocks)
     k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -533,8 +546,8 @@ def run_decode(args, wl, world, rank, local):
                      + 2 * B * (d.conv_kernel - 1) * d.conv_dim
                      + B * d.in_proj_out + B * di)
     else:
-        # W4A16: the in_proj GEMV streams the most bytes of the step (61% of the launch list)
-        dom_name = "gemv_w4a16_q_kernel (in_proj W4A16, decode weight stream)"
+        # W4A16: the in_proj GEMV streams the most bytes of the step (42% of the launch list)
+        dom_name = "gemv_w4a16_mma_kernel (in_proj W4A16, decode weight stream)"
 
         def dom(i):
             b_ = lm.blocks[i % len(lm.blocks)]
@@ -582,7 +595,7 @@ def run_decode(args, wl, world, rank, local):
                 "config": {"workload": args.workload, "desc": wl["desc"], "model": wl.get("model", "Mamba2-8B-shaped"),
                            "global_batch": global_batch, "batch_per_gpu": B, "seq_len": 1, "layers": wl["layers"],
                            "vocab": wl["vocab"],
-                           "parallelism": f"dp{world} (batch-shard replicas, no collective)",
+                           "parallelism": parallelism,
                            "l2": "inputs larger than L2 (weights+state stream every step), no flush",
                            "step_bytes": step_bytes,
                            "step_hbm_frac": step_bytes / (ms / 1e3) / 1e9 / hbm},
@@ -607,6 +620,8 @@ def main():
     ap.add_argument("--workload", default="decode8b", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="decode8b: skip the configs[1] prefill sub-record")
+    ap.add_argument("--parallel", default="batch", choices=["batch", "heads"],
+                    help="decode: batch-shard replicas (default) or head-shard tensor parallelism (NCCL all_reduce)")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="decode: shard this many sequences over the ranks (strong scaling); default 64 per GPU")
     args = ap.parse_args()

@@ -37,7 +37,14 @@ class HostModel:
 
 
 class QuantizedMambaLM:
-    def __init__(self, hm, device="cuda"):
+    """``tp_group`` (a torch.distributed group, head-shard mode, parallel.py): the blocks are this
+    rank's head shards (shard-local norm / Hadamard recipe); each block's out_proj partial is
+    summed over the group by one all_reduce (NCCL over NVLink on GPUs) before it joins the
+    residual stream.  Embedding, pre-norms and the head are replicated."""
+
+    def __init__(self, hm, device="cuda", tp_group=None):
+        self.tp_group = tp_group
+        self.tp_world = torch.distributed.get_world_size(tp_group) if tp_group is not None else 1
         self.dims = hm.dims
         self.device = torch.device(device)
         dev = self.device
@@ -94,6 +101,8 @@ class QuantizedMambaLM:
                       convf=e((M, d.conv_dim), torch.float32), r=e((M, d.d_inner), torch.float32))
         if d.variant == "mamba1":
             ws.update(xd=e((M, d.dt_rank + 2 * d.d_state), torch.int8), dtq=e((M, d.d_inner), torch.int8))
+        if self.tp_world > 1:
+            ws["out"] = e((M, d.d_model), torch.float32)   # a block's out_proj partial before the all_reduce
         return ws
 
     # ------------------------------------------------------------------ forward
@@ -106,7 +115,12 @@ class QuantizedMambaLM:
             ops.embed_int8(self.emb_codes, self.emb_scale, tok, h)
         for l, blk in enumerate(self.blocks):
             st = states[l]
-            if blk.a8:
+            if blk.a8 and self.tp_world > 1:   # head shard: partial -> all_reduce -> residual
+                ops.rmsnorm_quant(h, self.layer_norms[l], EPS_NORM, blk.s_u, ws["u"])
+                part = blk.forward_codes(ws["u"], B, T, st, state_in, ws=ws)
+                torch.distributed.all_reduce(part, op=torch.distributed.ReduceOp.SUM, group=self.tp_group)
+                h.add_(part)
+            elif blk.a8:
                 ops.rmsnorm_quant(h, self.layer_norms[l], EPS_NORM, blk.s_u, ws["u"])
                 blk.forward_codes(ws["u"], B, T, st, state_in, resid=h, ws=ws)
             else:

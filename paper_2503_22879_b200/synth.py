@@ -147,8 +147,22 @@ class SynthHost:
     s_head: float
 
 
-def synthetic_lm(d: Dims, n_layers: int, profile: str, vocab: int, dev="cuda", seed: int = 0, head_kind="w4a8"):
+def head_shard_dims(d: Dims, world: int) -> Dims:
+    """Block dims of one rank's head shard (parallel.shard_qblock's shape): nh/W heads, their
+    d_inner/W channels and G/W state groups, the norm / Hadamard local to the shard."""
+    if d.variant != "mamba2" or d.n_heads % world or d.n_state_groups % world:
+        raise ValueError(f"{d.n_heads} heads / {d.n_state_groups} groups do not split over {world} ranks")
+    return Dims("mamba2", d.d_model, d.d_inner // world, d.d_state, d.n_heads // world, d.head_dim,
+                d.n_state_groups // world, d.conv_kernel)
+
+
+def synthetic_lm(d: Dims, n_layers: int, profile: str, vocab: int, dev="cuda", seed: int = 0, head_kind="w4a8",
+                 tp_group=None):
+    """Random-init model in HBM.  With ``tp_group`` the blocks are this rank's head shards of
+    ``d`` (head_shard_dims) and the model all-reduces their out_proj partials."""
     from .model import QuantizedMambaLM
+    if tp_group is not None:
+        d = head_shard_dims(d, torch.distributed.get_world_size(tp_group))
     g = torch.Generator(device=dev)
     g.manual_seed(seed + 1000)
     emb = torch.randint(-127, 128, (vocab, d.d_model), generator=g, device=dev, dtype=torch.int8)
@@ -157,4 +171,4 @@ def synthetic_lm(d: Dims, n_layers: int, profile: str, vocab: int, dev="cuda", s
     head = _device_ql(g, vocab, d.d_model, head_kind, dev, s_a=np.float32(4.0 / 127))
     host = SynthHost(d, [profile] * n_layers, emb, es, [np.ones(d.d_model, np.float32)] * n_layers, blocks,
                      np.ones(d.d_model, np.float32), head, np.float32(4.0 / 127))
-    return QuantizedMambaLM(host, dev)
+    return QuantizedMambaLM(host, dev, tp_group=tp_group)

@@ -144,3 +144,75 @@ def test_4bit_embedding_logits(cuda, profile):
     lg, _ = lm.prefill(torch.as_tensor(toks[:1, :40], device=cuda), all_logits=True)
     rel = np.abs(lg.cpu().numpy() - ref).max() / np.abs(ref).max()
     assert rel < 1e-2, rel
+
+
+def _tp_worker(rank, world, port, q, profile):
+    """One rank of the head-shard model: its blocks are head shards, the out_proj partials are
+    all-reduced over the group (gloo here: both ranks share cuda:0; NCCL on a multi-GPU box)."""
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import dataclasses
+    import numpy as np
+    import torch
+    from oracle import pipeline as opl
+    from oracle import qblock as oq
+    from oracle import ssm_block as osb
+    from paper_2503_22879_b200 import cli, parallel
+    from paper_2503_22879_b200 import dist as pdist
+    from paper_2503_22879_b200.model import QuantizedMambaLM
+    from paper_2503_22879_b200.ssm_block import Dims
+    pdist.init("gloo")
+    try:
+        dev = torch.device("cuda", 0)
+        d = Dims("mamba2", 256, 512, 64, 8, 64, 2, 4, norm_groups=world)   # shard-local recipe
+        fm = cli.cmd_gen_toy(d, 2, seed=31)
+        toks = cli.calib_tokens(512, 2, 32)
+        qm = cli.cmd_quantize(fm, toks, profile, device="cuda")
+        shard = dataclasses.replace(qm, dims=parallel.shard_qblock(qm.blocks[0], world, rank).dims,
+                                    blocks=[parallel.shard_qblock(b, world, rank) for b in qm.blocks])
+        lm = QuantizedMambaLM(shard, dev, tp_group=torch.distributed.group.WORLD)
+        prompt = np.asarray(toks[0, :12])
+        gl, gst = lm.prefill(torch.as_tensor(prompt[None], device=dev))
+        nxt = int(torch.argmax(gl[0]).item())
+        gl2 = lm.decode_step(torch.tensor([nxt], dtype=torch.int32, device=dev), gst)
+        if rank == 0:   # the unsharded oracle model of the same recipe
+            ql = lambda x: None if x is None else oq.QLinear(x.kind, x.codes, x.s_ch, x.s_group, x.group)  # noqa: E731
+            ob = [oq.QBlock(osb.Dims(**vars(b.dims)), b.profile, ql(b.in_proj), ql(b.out_proj), b.conv_weight,
+                            b.conv_bias, b.a_log, b.d_param, b.dt_bias, b.norm_weight, b.head_group, s_u=b.s_u,
+                            in_out_scale=b.in_out_scale, conv_in_scale=b.conv_in_scale,
+                            conv_out_scale=b.conv_out_scale, state_scale=b.state_scale, s_y=b.s_y,
+                            hadamard=b.hadamard) for b in qm.blocks]
+            om = opl.QuantModel(osb.Dims(**vars(qm.dims)), qm.profiles, np.asarray(qm.emb_codes),
+                                np.asarray(qm.emb_scale), [np.asarray(w) for w in qm.layer_norms], ob,
+                                np.asarray(qm.final_norm), ql(qm.head), np.float32(qm.s_head))
+            rl, rst = opl.quant_forward(om, prompt)
+            rl2, _ = opl.quant_forward(om, [nxt], rst)
+            rel = lambda a, b: float(np.abs(a - b).max() / np.abs(b).max())   # noqa: E731
+            q.put((rel(gl.cpu().numpy()[0], rl[-1]), rel(gl2.cpu().numpy()[0], rl2[-1])))
+        pdist.barrier(world)
+    finally:
+        torch.distributed.destroy_process_group()
+
+
+@pytest.mark.parametrize("profile", ["W8A8", "W4A8"])
+def test_head_shard_model_world2(cuda, profile):
+    """QuantizedMambaLM in head-shard mode (tp_group): 2 ranks (gloo, one GPU) each run their
+    heads of every block and all-reduce the out_proj partials; prefill and a decode step give the
+    unsharded oracle model's logits (rel <= 1e-2, north_star)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_tp_worker, args=(r, 2, port, q, profile)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    r1, r2 = q.get(timeout=5)
+    assert r1 <= 1e-2 and r2 <= 1e-2, (r1, r2)
