@@ -1,4 +1,6 @@
-"""Fused decode step vs the three-launch path on identical inputs (debug)."""
+"""A/B parity of two decode-step paths on identical inputs: sq_mamba2_decode_step_int8 without and
+with the group-sum output (the harness used for the fused-kernel experiments of
+profiles/r02_decode_fusion.txt; those kernels are in commits 6df4bab and 3e7018f)."""
 import os
 import sys
 

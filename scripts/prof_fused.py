@@ -1,4 +1,5 @@
-"""One 8B-shaped fused decode step (B=64) for ncu capture of mamba2_decode_fused_kernel."""
+"""Eager timing of the 8B-shaped decode SSM step (B=64), with and without group sums (the
+harness of profiles/r02_decode_fusion.txt)."""
 import os
 import sys
 
@@ -25,7 +26,7 @@ for _ in range(20):
     ops.mamba2_decode_step_int8(blk.decode_params, B, zx, c, h, y=y, ws=ws)
 e.record()
 torch.cuda.synchronize()
-print("fused decode step us", s.elapsed_time(e) / 20 * 1e3)
+print("decode step us", s.elapsed_time(e) / 20 * 1e3)
 gs = torch.zeros((B, d.d_inner // 128), dtype=torch.int32, device="cuda")
 for _ in range(3):
     ops.mamba2_decode_step_int8(blk.decode_params, B, zx, c, h, y=y, ws=ws, gsum=gs)
