@@ -26,9 +26,11 @@ int check_launch(const char* what) {
 }
 
 // Kernel classes launched with programmatic dependent launch: a build-time choice
-// (-DSQ_PDL_MASK=m for A/B builds); default GEMMs, decode prep, state ring, b=1 f32 chain.
+// (-DSQ_PDL_MASK=m for A/B builds); default GEMMs, decode prep, state ring, the b=1 f32 chain and
+// the b=1 int8 chain (the latter since its kernels load their parameters before the dependency
+// wait: Mamba1-2.8B decode 431 -> 443 tok/s same-box, where it had been slower without that).
 #ifndef SQ_PDL_MASK
-#define SQ_PDL_MASK 54
+#define SQ_PDL_MASK 118
 #endif
 bool pdl_enabled(int cls) { return (SQ_PDL_MASK & cls) != 0; }
 

@@ -160,9 +160,9 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// SQ_PDL: bitmask of kernel classes launched with PDL (default PDL_GEMM | PDL_PREP | PDL_RING | PDL_SMALL;
-// 0 disables)
-// PDL_SMALL: the f32 (W4A16) b=1 chain; PDL_SMALL8: the int8 b=1 chain (off by default: slower in the A/B)
+// SQ_PDL_MASK (capi.cu): bitmask of kernel classes launched with PDL (default PDL_GEMM | PDL_PREP |
+// PDL_RING | PDL_SMALL | PDL_SMALL8; 0 disables)
+// PDL_SMALL: the f32 (W4A16) b=1 chain; PDL_SMALL8: the int8 b=1 chain
 enum { PDL_ROW = 1, PDL_PREP = 2, PDL_RING = 4, PDL_NORM = 8, PDL_GEMM = 16, PDL_SMALL = 32, PDL_SMALL8 = 64 };
 bool pdl_enabled(int cls);
 

@@ -213,18 +213,22 @@ __global__ void conv1d_update_kernel(const int8_t* x, int64_t ldx, const float* 
                                      const float* __restrict__ s_out, int B, int C, int Kc, int8_t* cache,
                                      int8_t* out, int64_t ldo) {
   pdl_trigger();
-  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (c >= C) return;
-  const float si = s_in[c];
+  // parameters before the grid dependency wait (static); codes and cache after it
+  const float si = s_in[c], so = s_out[c], bc = bias[c];
+  float wc[kMaxK];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) wc[j] = j < Kc ? w[c * Kc + j] : 0.f;
+  pdl_wait();
   int8_t* cr = cache + (int64_t)b * (Kc - 1) * C + c;
   int8_t q[kMaxK];
   for (int j = 0; j < Kc - 1; ++j) q[j] = cr[(int64_t)j * C];
   q[Kc - 1] = x[(int64_t)b * ldx + c];
-  float acc = bias[c];
-  for (int j = 0; j < Kc; ++j) acc = __fadd_rn(acc, __fmul_rn(w[c * Kc + j], __fmul_rn((float)q[j], si)));
-  out[(int64_t)b * ldo + c] = quant8(silu_f(acc), s_out[c]);
+  float acc = bc;
+  for (int j = 0; j < Kc; ++j) acc = __fadd_rn(acc, __fmul_rn(wc[j], __fmul_rn((float)q[j], si)));
+  out[(int64_t)b * ldo + c] = quant8(silu_f(acc), so);
   for (int j = 0; j < Kc - 1; ++j) cr[(int64_t)j * C] = q[j + 1];
 }
 

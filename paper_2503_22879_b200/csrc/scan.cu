@@ -280,6 +280,44 @@ __global__ void __launch_bounds__(128) mamba1_scan_kernel(sq_mamba1_params p, in
   for (int n = 0; n < N; ++n) st[n] = quant8(hs[n], sh);
 }
 
+// Mamba1 int8 decode step (T = 1): thread = (sequence, channel, state), 16 threads per channel,
+// so d_inner 5120 runs on 320 CTAs instead of 40 one-channel-per-thread CTAs.  Per state the
+// update is mamba1_scan_kernel's (h = Ȧ·h + (Δx̂)·B̂, unfused f32, requantised with s_h); the
+// channel's C·h is reduced over its 16 threads with shuffles (a different f32 summation order
+// than the sequential kernel: tolerance-compared).  Parameters are read before the grid
+// dependency wait.
+__global__ void __launch_bounds__(256) mamba1_step_kernel(sq_mamba1_params p, int B, const int8_t* x, int64_t ldx,
+                                                          const int8_t* dt, int64_t lddt, const int8_t* BC,
+                                                          int64_t ldbc, const int8_t* z, int64_t ldz, int8_t* state,
+                                                          int state_in, float* y, int64_t ldy) {
+  constexpr int N = 16;
+  pdl_trigger();
+  const int n = threadIdx.x & (N - 1);
+  const int c = blockIdx.x * (256 / N) + (threadIdx.x >> 4);
+  const int b = blockIdx.y;
+  const bool live = c < p.d_inner;
+  const int cc = live ? c : 0;
+  const float An = p.A[(int64_t)cc * N + n], dtb = p.dt_bias[cc], sx = p.s_x[cc], sh = p.s_h[cc], Dc = p.D[cc];
+  pdl_wait();   // codes and the cached state come from earlier grids
+  if (!live) return;
+  const float delta = softplus_f(__fadd_rn(__fmul_rn((float)dt[(int64_t)b * lddt + c], p.s_dt), dtb));
+  const float xh = __fmul_rn((float)x[(int64_t)b * ldx + c], sx);
+  const float dtx = __fmul_rn(delta, xh);
+  const int8_t* bc = BC + (int64_t)b * ldbc;
+  const float bn = __fmul_rn((float)bc[n], p.s_B), cn = __fmul_rn((float)bc[N + n], p.s_C);
+  int8_t* st = state + ((int64_t)b * p.d_inner + c) * N + n;
+  const float h0 = state_in ? __fmul_rn((float)*st, sh) : 0.f;
+  const float h = __fadd_rn(__fmul_rn(expf(__fmul_rn(delta, An)), h0), __fmul_rn(dtx, bn));
+  float acc = __fmul_rn(h, cn);
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  *st = quant8(h, sh);
+  if (n == 0) {
+    const float yv = __fadd_rn(acc, __fmul_rn(Dc, xh));
+    y[(int64_t)b * ldy + c] = __fmul_rn(yv, silu_f(__fmul_rn((float)z[(int64_t)b * ldz + c], p.s_z)));
+  }
+}
+
 // Mamba1 int8 selective scan, staged (K8): CTA = 32 channels x
 // 4 state quarters (thread = one channel's 4 of the 16 states), so d_inner 5120 runs on 160 CTAs
 // instead of 40 one-channel-per-thread CTAs.  Time is walked in chunks of M1_TC tokens whose
@@ -821,6 +859,11 @@ extern "C" int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T, c
       launch_k(PDL_SMALL8, mamba1_scan_staged_kernel<2>, grid, dim3(128), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc,
                z, ldz, state, state_in, y, ldy, wsf, tchunk);
     }
+    return check_launch("sq_selective_scan_int8");
+  }
+  if (T == 1) {   // decode step: 16 threads per channel
+    launch_k(PDL_SMALL8, mamba1_step_kernel, dim3((p->d_inner + 15) / 16, B), dim3(256), 0, as_stream(stream), *p, B, x,
+             ldx, dt, lddt, BC, ldbc, z, ldz, state, state_in, y, ldy);
     return check_launch("sq_selective_scan_int8");
   }
   dim3 grid((p->d_inner + 127) / 128, B);
