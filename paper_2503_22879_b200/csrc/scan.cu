@@ -138,14 +138,15 @@ __global__ void __launch_bounds__(128) mamba2_scan_f32_rows_kernel(sq_mamba2_par
                                                                    int64_t lddt, const float* z, int64_t ldz,
                                                                    float* state, int state_in, float* y, int64_t ldy) {
   pdl_trigger();
-  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   const int h = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int P = p.head_dim, N = p.d_state;   // N == 32 * CPL
   const int r0 = blockIdx.z * 32 + warp * 8;
   if (r0 >= P) return;                        // P % 8 == 0; whole warps idle past the last row
+  // parameters before the grid dependency wait (static); state and operands after it
   const int g = p.head_group[h];
   const float A = PRE ? 0.f : p.A[h], Dh = p.D[h], dtb = PRE ? 0.f : p.dt_bias[h];
+  pdl_wait();   // inputs come from the previous grid (launched with PDL_SMALL)
   float* st = state + (((int64_t)b * p.n_heads + h) * P + r0) * N + lane * CPL;
   float hs[8][CPL];
 #pragma unroll
