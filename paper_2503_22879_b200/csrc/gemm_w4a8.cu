@@ -43,7 +43,6 @@ using namespace sm100;
 namespace w4pg {
 constexpr int BN = 128;                 // weight rows per tile (MMA M)
 constexpr int BK = 128;                 // K per group / k-block
-constexpr int THREADS = 512;
 constexpr int TILE_BYTES = BN * BK / 2; // 8 KB packed weights per (n-tile, k-block)
 #ifndef SQ_W4_RAW
 #define SQ_W4_RAW 8
@@ -62,12 +61,16 @@ constexpr int AST = SQ_W4_AST;          // activation stages (steps)
 constexpr int TST = 4;                  // TMEM A stages (steps)
 constexpr int NACC = 2;                 // accumulator buffers (steps)
 constexpr uint32_t MAGIC = 0x4B400000u; // bit pattern of 1.5 * 2^23
+#ifndef SQ_W4_CONV64
+#define SQ_W4_CONV64 4   // converters at 64 tokens (8 = 20 warps per CTA)
+#endif
 // Converter / promotion split of warps 4-15: the promotion work per step scales with the token
 // tile, the conversion work does not.  64 tokens: 4 converters (both groups of a step each) + 8
 // promotion warps (32 token columns each); 16 / 32 tokens: 8 converters (two sets, one group of the
 // step each) + 4 promotion warps (all columns).  Same-box A/B (scripts/probe_w4.py): in_proj b=1
 // 12.0 -> 10.8 us with 8 converters, b=64 14.7 -> 16.1 us, so the split follows the tile.
-__host__ __device__ constexpr int n_conv(int ntok) { return ntok <= 32 ? 8 : 4; }
+__host__ __device__ constexpr int n_conv(int ntok) { return ntok <= 32 ? 8 : SQ_W4_CONV64; }
+__host__ __device__ constexpr int n_promo(int ntok) { return ntok <= 32 ? 4 : 8; }
 
 template <int NTOK>
 struct Cfg {
@@ -85,7 +88,8 @@ struct Cfg {
   static constexpr int TMEM_COLS = COLS_USED <= 256 ? 256 : 512;
   static constexpr int NCONV = n_conv(NTOK);     // converter warps
   static constexpr int PROMO0 = 4 + NCONV;        // first promotion warp
-  static constexpr int NPROMO = 16 - PROMO0;      // promotion warps (8 or 4)
+  static constexpr int NPROMO = n_promo(NTOK);    // promotion warps (8 or 4)
+  static constexpr int THREADS = (PROMO0 + NPROMO) * 32;
   static constexpr int HALF = NPROMO == 8 ? NTOK / 2 : NTOK;   // token columns per promotion thread
   static_assert(NTOK * BN * 4 <= OFF_ACT, "split-K partial tile must fit the weight ring");
 };
@@ -140,7 +144,7 @@ __device__ __forceinline__ void store_out(const Args& a, int m, int n, float y, 
 }
 
 template <int NTOK, int SPLITS>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(Cfg<NTOK>::THREADS, 1)
     gemm_w4a8_pg_kernel(const __grid_constant__ CUtensorMap tm_act, Args args) {
   using C = Cfg<NTOK>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp != 2) {   // (the stream warp never touches TMEM)
     if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
     tc_fence_before();
-    named_bar(1, THREADS - 32);
+    named_bar(1, C::THREADS - 32);
     tc_fence_after();
     tmem = *tmem_holder;
   }
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr int TPR = NTOK / SPLITS;
     const int n_tile = unit_n(u_first), m_tile = unit_m(u_first);
     const uint32_t red_addr = smem_u32(raw);
-    for (int idx = threadIdx.x; idx < TPR * BN; idx += THREADS) {
+    for (int idx = threadIdx.x; idx < TPR * BN; idx += C::THREADS) {
       const int tl = rank * TPR + idx / BN, r = idx % BN;
       const int m = m_tile * NTOK + tl, n = n_tile * BN + r;
       float part[SPLITS];
@@ -535,7 +539,7 @@ static int launch_w4pg(const CUtensorMap& tm, const w4pg::Args& a, cudaStream_t 
     cfg.gridDim = dim3(SPLITS, a.n_tiles, m_tiles);
   else
     cfg.gridDim = dim3(std::min(a.units, sm_count()));
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(C::THREADS);
   const int nkb = (a.K / BK + SPLITS - 1) / SPLITS;
   cfg.dynamicSmemBytes = C::SMEM0 + 2 * nkb * BN * 4;
   cfg.stream = st;
