@@ -136,25 +136,30 @@ class Clocks:
 
 def ncu_traffic(kernel_name, pattern=None):
     """dram read+write bytes per launch of `kernel_name` from the newest committed ncu --set full
-    summary (profiles/*.txt written by scripts/summarize_profiles.py), or None."""
+    summary (profiles/*.txt written by scripts/summarize_profiles.py), or None.  For the decode SSM
+    step (prep_kernel + state_ring_kernel + norm_had8192_kernel) the three kernels' bytes are summed."""
     import glob
     import re
+    step = kernel_name.startswith("mamba2_decode_step_int8")
     if pattern is None:
-        pattern = "*prof_ring*.txt" if kernel_name.startswith("state_ring") else "*prof_prefill*.txt"
+        pattern = "*prof_ring*.txt" if step or kernel_name.startswith("state_ring") else "*prof_prefill*.txt"
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", pattern)))
     if not files:
         return None
     txt = open(files[-1]).read()
-    key = kernel_name.split()[0]
-    ids = [m.group(1) for m in re.finditer(r"## ID (\d+): (?:void )?(\S+)", txt) if m.group(2).startswith(key)]
-    if not ids:
-        return None
-    m = re.search(r"## raw ID %s: dram__bytes_read.sum=([0-9.]+) (\w+); dram__bytes_write.sum=([0-9.]+) (\w+)" % ids[0],
-                  txt)
-    if not m:
-        return None
+    keys = ("prep_kernel", "state_ring_kernel", "norm_had8192_kernel") if step else (kernel_name.split()[0],)
     unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    return float(m.group(1)) * unit.get(m.group(2), 1) + float(m.group(3)) * unit.get(m.group(4), 1)
+    total = 0.0
+    for key in keys:
+        ids = [m.group(1) for m in re.finditer(r"## ID (\d+): (?:void )?(\S+)", txt) if m.group(2).startswith(key)]
+        if not ids:
+            return None
+        m = re.search(r"## raw ID %s: dram__bytes_read.sum=([0-9.]+) (\w+); dram__bytes_write.sum=([0-9.]+) (\w+)"
+                      % ids[0], txt)
+        if not m:
+            return None
+        total += float(m.group(1)) * unit.get(m.group(2), 1) + float(m.group(3)) * unit.get(m.group(4), 1)
+    return total
 
 
 def dist_init():

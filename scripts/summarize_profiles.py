@@ -1,6 +1,6 @@
 """Summarise a gpurun_out/ pass into profiles/<tag>_*.txt (committed evidence).
 
-    python scripts/summarize_profiles.py r01
+    python scripts/summarize_profiles.py r01 [report_dir]
 Reads gpurun_out/launches.csv (ncu --metrics gpu__time_duration.sum launch list of the
 bench's timed steps) and every gpurun_out/*.ncu-rep (ncu --set full captures).
 """
@@ -52,8 +52,8 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg", "sm__cycles_elapsed.avg"]
 
 
-def ncu_reports(tag):
-    for rep in sorted(glob.glob(os.path.join(OUT, "*.ncu-rep"))):
+def ncu_reports(tag, src=OUT):
+    for rep in sorted(glob.glob(os.path.join(src, "*.ncu-rep"))):
         base = os.path.basename(rep)[:-8]
         det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -83,6 +83,9 @@ def ncu_reports(tag):
 if __name__ == "__main__":
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
+    if len(sys.argv) > 2:   # only the ncu reports of one directory (e.g. gpurun_out/prof)
+        ncu_reports(tag, sys.argv[2])
+        sys.exit(0)
     launches(tag)
     launches(tag, "launches_prefill.csv", "launches_prefill")
     ncu_reports(tag)
