@@ -324,15 +324,15 @@ __global__ void __launch_bounds__(256) mamba1_step_kernel(sq_mamba1_params p, in
 // instead of 40 one-channel-per-thread CTAs.  Time is walked in chunks of M1_TC tokens whose
 // operands are staged into shared memory by all 128 threads (cp.async, double-buffered one chunk
 // ahead) and turned there, in parallel, into everything that does not depend on the state:
-// Δ = softplus(Δ̂ + dt_bias), Δ·x̂, x̂, SiLU(ẑ), B̂ | Ĉ and every Ȧ = exp(Δ·A) of the chunk
-// (16 exps per token and channel, off the recurrence's critical path).  The sequential part then
-// reads only smem: per step a thread updates its 4 states (h = Ȧ·h + (Δx̂)·B̂, unfused like the
-// oracle) and the channel's C·h is reduced over its 4 threads with two shuffles; the time loop is
-// unrolled so steps overlap.  The final state is requantised once.
+// Δ = softplus(Δ̂ + dt_bias), Δ·x̂, x̂, SiLU(ẑ), B̂ | Ĉ.  The sequential part then reads only smem:
+// per step a thread forms its 4 Ȧ = 2^(Δ·A·log2 e) on the SFU (independent of the state, so off
+// the recurrence's chain), updates its 4 states (h = Ȧ·h + (Δx̂)·B̂, unfused like the oracle) and
+// the channel's C·h is reduced over its 4 threads with two shuffles; the time loop is unrolled so
+// steps overlap.  The final state is requantised once.  16 KB of smem per CTA.
 constexpr int M1_TC = 16;
 constexpr int M1_CH = 32;
 struct M1Stage {
-  float da[M1_TC][M1_CH][16];  // Ȧ
+  float dl[M1_TC][M1_CH];      // Δ (Ȧ = 2^(Δ·A·log2 e) is formed in the recurrence loop, off its chain)
   float dx[M1_TC][M1_CH];      // Δ·x̂
   float xh[M1_TC][M1_CH];      // x̂ (the D·x skip)
   float gz[M1_TC][M1_CH];      // SiLU(ẑ)
@@ -399,6 +399,10 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
     }
   }
   const int nch = (t1 - t0 + M1_TC - 1) / M1_TC;
+  __syncthreads();   // As staged
+  float a2[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a2[i] = As[cl][qt * 4 + i];   // this thread's A·log2 e
   auto issue = [&](int ch) {   // M1_TC rows x (x, dt, z, bc) x 2 16-B pieces = 128 pieces: one per thread
     M1Raw& r = raw[ch & 1];
     const int row = tid >> 3, kind = (tid >> 1) & 3, half = tid & 1;
@@ -435,8 +439,7 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
       stg.dx[row][cc] = __fmul_rn(delta, xv);
       stg.xh[row][cc] = xv;
       stg.gz[row][cc] = silu_approx(__fmul_rn((float)r.z[row][cc], p.s_z));
-#pragma unroll
-      for (int n = 0; n < N; ++n) stg.da[row][cc][n] = ex2_approx(__fmul_rn(delta, As[cc][n]));   // As = A·log2 e
+      stg.dl[row][cc] = delta;
     }
     for (int i = tid; i < tn * 32; i += 128) {
       const int row = i >> 5, n = i & 31;
@@ -446,8 +449,9 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
     float* yrow = y + ((int64_t)b * T + t0 + ch * M1_TC) * ldy + c;
 #pragma unroll 4
     for (int tt = 0; tt < tn; ++tt) {
-      const float dtx = stg.dx[tt][cl];
-      const float4 av = *reinterpret_cast<const float4*>(&stg.da[tt][cl][qt * 4]);
+      const float dtx = stg.dx[tt][cl], dl = stg.dl[tt][cl];
+      const float4 av = make_float4(ex2_approx(__fmul_rn(dl, a2[0])), ex2_approx(__fmul_rn(dl, a2[1])),
+                                    ex2_approx(__fmul_rn(dl, a2[2])), ex2_approx(__fmul_rn(dl, a2[3])));
       const float4 bv = *reinterpret_cast<const float4*>(&stg.bc[tt][qt * 4]);
       hs[0] = __fadd_rn(__fmul_rn(av.x, hs[0]), __fmul_rn(dtx, bv.x));
       hs[1] = __fadd_rn(__fmul_rn(av.y, hs[1]), __fmul_rn(dtx, bv.y));
@@ -477,16 +481,16 @@ __global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_param
   }
 }
 
-// time chunks of the two-pass form: up to 16, chunks >= 64 tokens
+// time chunks of the two-pass form: up to 16, chunks >= 32 tokens
 static int m1_time_chunks(int d_inner, int B, int T) {
 #ifdef SQ_M1_PROBE_NZ   // profiling builds only: fixed chunk count
   if (T / SQ_M1_PROBE_NZ >= M1_TC) return SQ_M1_PROBE_NZ;
 #endif
   // same-box sweep at the 2.8B prefill shape (B=1, T=1024, 160 channel blocks; scripts/probe_m1.py):
-  // 1 / 4 / 8 / 16 chunks -> 250 / 292 / 248 / 224 us
+  // 1 / 2 / 4 / 8 / 16 chunks -> 203 / 259 / 137 / 111 / 108 us (16 KB smem per CTA)
   const int ctas = (d_inner / M1_CH) * B;
   int nz = 1;
-  while (nz < 16 && ctas * nz < 16 * 148 && T / (nz * 2) >= 64) nz *= 2;
+  while (nz < 16 && ctas * nz < 16 * 148 && T / (nz * 2) >= 32) nz *= 2;
   return nz;
 }
 
