@@ -462,12 +462,22 @@ int gemm_a8_tc(const int8_t* a, int64_t lda, const uint8_t* w, const float* alph
   if (K % 16 != 0 || lda % 16 != 0 || (reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(w) & 15))
     return SQ_ERR_ARG;
   if (!get_encoder()) return SQ_ERR_ARG;
-  const int ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
-  const int tiles = ((N + TC_BN - 1) / TC_BN) * ((M + ntok - 1) / ntok);
+  int ntok = M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
   const int nkb = (K + TC_BK - 1) / TC_BK;
-  int splits = 1;
-  const int slots = ntok <= 32 ? 2 * 148 : 148;   // resident CTAs (see launch_tc BUDGET)
-  while (splits < 8 && tiles * splits * 2 <= slots && nkb / (splits * 2) >= 4 && ntok % (splits * 2) == 0) splits *= 2;
+  auto pick_splits = [&](int nt) {
+    const int tiles = ((N + TC_BN - 1) / TC_BN) * ((M + nt - 1) / nt);
+    const int slots = nt <= 32 ? 2 * 148 : 148;   // resident CTAs (see launch_tc BUDGET)
+    int s = 1;
+    while (s < 8 && tiles * s * 2 <= slots && nkb / (s * 2) >= 4 && nt % (s * 2) == 0) s *= 2;
+    return s;
+  };
+  int splits = pick_splits(ntok);
+  // mid-size M with few 256-token tiles (e.g. the 2.8B out_proj at 1024 tokens: 80 tiles, 37 us)
+  // fills more SMs with 128-token tiles (160 tiles, 22.5 us; scripts/probe_tc.py)
+  if (ntok == 256 && splits == 1 && ((N + TC_BN - 1) / TC_BN) * ((M + 255) / 256) < 148) {
+    ntok = 128;
+    splits = pick_splits(ntok);
+  }
   TcArgs args{alpha, M, N, K, epi, out, ldo, col_scale};
   switch (splits) {
     case 1: return dispatch_ntok<1>(ntok, a, lda, w, args, st);
