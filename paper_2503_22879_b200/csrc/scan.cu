@@ -319,29 +319,25 @@ __global__ void __launch_bounds__(256) mamba1_step_kernel(sq_mamba1_params p, in
   }
 }
 
-// Mamba1 int8 selective scan, staged (K8): CTA = 32 channels x
-// 4 state quarters (thread = one channel's 4 of the 16 states), so d_inner 5120 runs on 160 CTAs
-// instead of 40 one-channel-per-thread CTAs.  Time is walked in chunks of M1_TC tokens whose
-// operands are staged into shared memory by all 128 threads (cp.async, double-buffered one chunk
-// ahead) and turned there, in parallel, into everything that does not depend on the state:
-// Δ = softplus(Δ̂ + dt_bias), Δ·x̂, x̂, SiLU(ẑ), B̂ | Ĉ.  The sequential part then reads only smem:
-// per step a thread forms its 4 Ȧ = 2^(Δ·A·log2 e) on the SFU (independent of the state, so off
-// the recurrence's chain), updates its 4 states (h = Ȧ·h + (Δx̂)·B̂, unfused like the oracle) and
-// the channel's C·h is reduced over its 4 threads with two shuffles; the time loop is unrolled so
-// steps overlap.  The final state is requantised once.  16 KB of smem per CTA.
+// Mamba1 int8 selective scan (K8): thread = one channel with
+// all 16 states in registers, CTA = CH channels (128 at the 2.8B shape: 40 channel blocks x 16 time
+// chunks = 640 CTAs).  Time is walked in chunks of M1_TC tokens whose int8 codes are staged into
+// shared memory by cp.async one chunk ahead; B̂ | Ĉ are dequantised once per chunk into f32 for the
+// whole CTA.  Per token a thread forms Δ = softplus(Δ̂ + dt_bias), x̂, SiLU(ẑ) and its 16
+// Ȧ = 2^(Δ·A·log2 e) (SFU, off the recurrence chain), then updates the 16 states with packed
+// f32x2 arithmetic (h = Ȧ·h + (Δx̂)·B̂, unfused like the oracle).  The states sit in the
+// permuted order m1_perm so each f32x2 pair holds the same position of two 4-state quarters, and
+// C·h is two packed FMA chains whose lanes are exactly the four quarter sums of the
+// one-quarter-per-thread form, added as (q0 + q1) + (q2 + q3).  Codes are widened with the
+// 1.5·2^23 magic add (integer + FMA pipes) instead of I2F, which shares the SFU's issue port.
+// The final state is requantised once.
 constexpr int M1_TC = 16;
-constexpr int M1_CH = 32;
-struct M1Stage {
-  float dl[M1_TC][M1_CH];      // Δ (Ȧ = 2^(Δ·A·log2 e) is formed in the recurrence loop, off its chain)
-  float dx[M1_TC][M1_CH];      // Δ·x̂
-  float xh[M1_TC][M1_CH];      // x̂ (the D·x skip)
-  float gz[M1_TC][M1_CH];      // SiLU(ẑ)
-  float bc[M1_TC][32];         // B̂[16] | Ĉ[16]
-};
-struct M1Raw {                 // int8 codes of one chunk (cp.async targets)
-  int8_t x[M1_TC][M1_CH], dt[M1_TC][M1_CH], z[M1_TC][M1_CH], bc[M1_TC][32];
-};
-
+#ifndef SQ_M1_UNROLL
+#define SQ_M1_UNROLL 4
+#endif
+constexpr int M1_UNROLL = SQ_M1_UNROLL;   // tokens per unrolled recurrence step
+__host__ __device__ constexpr int m1_perm(int p) { return (p >> 3) * 8 + ((p >> 1) & 3) + 4 * (p & 1); }
+__device__ __forceinline__ float s8f(int v) { return __fsub_rn(__int_as_float(0x4B400000 + v), 12582912.0f); }
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g)
                : "memory");
@@ -351,144 +347,166 @@ template <int NW>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(NW) : "memory"); }
 
 // Time-chunked parallel form (MODE 1 / 2, gridDim.z = time chunks): the recurrence h_t = Ȧ_t h_{t-1}
-// + b_t is linear, so pass 1 (MODE 1) runs every chunk from h = 0 (chunk 0 from the real initial
-// state) and keeps its end state and its decay product Π Ȧ; pass 2 (MODE 2) starts chunk j from
-// the folded carry h = Π_j ⊙ h + h_end_j of the chunks before it and re-runs the chunk with the y
-// output; the last chunk requantises the final state.  MODE 0 is the single pass.  The carried
-// start state is the sequential one up to f32 rounding (tolerance-compared, like the oracle's
-// chunked SSD).
-template <int MODE>
-__global__ void __launch_bounds__(128) mamba1_scan_staged_kernel(sq_mamba1_params p, int B, int T, const int8_t* x,
-                                                                 int64_t ldx, const int8_t* dt, int64_t lddt,
-                                                                 const int8_t* BC, int64_t ldbc, const int8_t* z,
-                                                                 int64_t ldz, int8_t* state, int state_in, float* y,
-                                                                 int64_t ldy, float* ws, int tchunk) {
+// + b_t is linear, so pass 1 (MODE 1) runs every chunk but the last from h = 0 (chunk 0 from the
+// real initial state) and keeps its end state and its decay product Π Ȧ; pass 2 (MODE 2) starts
+// chunk j from the folded carry h = Π_j ⊙ h + h_end_j of the chunks before it and re-runs the
+// chunk with the y output; the last chunk requantises the final state.  MODE 0 is the single pass.
+// The carried start state is the sequential one up to f32 rounding (tolerance-compared, like the
+// oracle's chunked SSD).
+template <int MODE, int CH>
+__global__ void __launch_bounds__(CH) mamba1_scan_chunk_kernel(sq_mamba1_params p, int B, int T, const int8_t* x,
+                                                               int64_t ldx, const int8_t* dt, int64_t lddt,
+                                                               const int8_t* BC, int64_t ldbc, const int8_t* z,
+                                                               int64_t ldz, int8_t* state, int state_in, float* y,
+                                                               int64_t ldy, float* ws, int tchunk) {
   constexpr int N = 16;
-  __shared__ __align__(16) M1Raw raw[2];
-  __shared__ __align__(16) M1Stage stg;
-  __shared__ float As[M1_CH][N];
+  __shared__ __align__(16) int8_t raw[2][M1_TC][3 * CH + 32];
+  __shared__ __align__(16) float bcf[2][M1_TC][32];   // B̂ | Ĉ (f32, m1_perm order)
   const int tid = threadIdx.x;
-  const int cl = tid >> 2, qt = tid & 3;       // channel within the CTA, state quarter
-  const int c0 = blockIdx.x * M1_CH, c = c0 + cl;
+  const int c0 = blockIdx.x * CH, c = c0 + tid;
   const int b = blockIdx.y;
-  pdl_trigger();
-  // Ȧ = exp(Δ·A) = 2^(Δ·A·log2 e) on the SFU (a few ulp from expf: the scan output is compared
-  // within tolerance and the state is requantised)
-  for (int i = tid; i < M1_CH * N; i += 128) As[i / N][i % N] = p.A[(int64_t)c0 * N + i] * 1.4426950408889634f;
-  const float sh = p.s_h[c], Dc = p.D[c];
-  pdl_wait();   // inputs come from the previous grid
-  int8_t* st = state + ((int64_t)b * p.d_inner + c) * N + qt * 4;
   const int tc = blockIdx.z, nz = gridDim.z;
-  const int t0 = tc * tchunk, t1 = min(T, t0 + tchunk);   // this CTA's time range
-  // per-chunk summaries [2][nz][B][d_inner][N]: end state (from 0; chunk 0 from the initial state)
-  // and decay product
-  const int64_t cell = ((int64_t)b * p.d_inner + c) * N + qt * 4, zst = (int64_t)B * p.d_inner * N;
-  float hs[4], pr[4] = {1.f, 1.f, 1.f, 1.f};
+  pdl_trigger();
+  if (MODE == 1 && tc == nz - 1) return;   // the last chunk's summary is never read
+  float2 A2[8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) hs[i] = (state_in && (MODE == 0 || tc == 0)) ? __fmul_rn((float)st[i], sh) : 0.f;
-  if (MODE == 2 && tc > 0) {   // carry: fold the chunks before this one
-    const float4 h0 = *reinterpret_cast<const float4*>(ws + cell);
-    hs[0] = h0.x; hs[1] = h0.y; hs[2] = h0.z; hs[3] = h0.w;
+  for (int k = 0; k < 8; ++k)
+    A2[k] = make_float2(p.A[(int64_t)c * N + m1_perm(2 * k)] * 1.4426950408889634f,
+                        p.A[(int64_t)c * N + m1_perm(2 * k + 1)] * 1.4426950408889634f);
+  const float sh = p.s_h[c], Dc = p.D[c], sx = p.s_x[c], dtb = p.dt_bias[c];
+  const float s_dt = p.s_dt, s_z = p.s_z, s_B = p.s_B, s_C = p.s_C;
+  pdl_wait();   // inputs come from the previous grid
+  int8_t* st = state + ((int64_t)b * p.d_inner + c) * N;
+  const int t0 = tc * tchunk, t1 = min(T, t0 + tchunk);   // this CTA's time range
+  // per-chunk summaries [2][nz][B][d_inner][N] (natural state order): end state (from 0; chunk 0
+  // from the initial state) and decay product
+  const int64_t cell = ((int64_t)b * p.d_inner + c) * N, zst = (int64_t)B * p.d_inner * N;
+  float2 H[8], P2[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    P2[k] = make_float2(1.f, 1.f);
+    H[k] = (state_in && (MODE == 0 || tc == 0))
+               ? make_float2(__fmul_rn((float)st[m1_perm(2 * k)], sh), __fmul_rn((float)st[m1_perm(2 * k + 1)], sh))
+               : make_float2(0.f, 0.f);
+  }
+  if (MODE == 2 && tc > 0) {   // carry: fold the chunks before this one (16-B loads, 4 chunks in flight)
+    float e[N];
+    auto ld16 = [&](const float* src, float (&d)[N]) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(src + 4 * i);
+        d[4 * i] = v.x; d[4 * i + 1] = v.y; d[4 * i + 2] = v.z; d[4 * i + 3] = v.w;
+      }
+    };
+    ld16(ws + cell, e);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) H[k] = make_float2(e[m1_perm(2 * k)], e[m1_perm(2 * k + 1)]);
+#pragma unroll 4
     for (int j = 1; j < tc; ++j) {
-      const float4 he = *reinterpret_cast<const float4*>(ws + j * zst + cell);
-      const float4 pj = *reinterpret_cast<const float4*>(ws + (nz + j) * zst + cell);
-      hs[0] = __fadd_rn(__fmul_rn(pj.x, hs[0]), he.x);
-      hs[1] = __fadd_rn(__fmul_rn(pj.y, hs[1]), he.y);
-      hs[2] = __fadd_rn(__fmul_rn(pj.z, hs[2]), he.z);
-      hs[3] = __fadd_rn(__fmul_rn(pj.w, hs[3]), he.w);
+      float q[N];
+      ld16(ws + j * zst + cell, e);
+      ld16(ws + (nz + j) * zst + cell, q);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        H[k] = __fadd2_rn(__fmul2_rn(make_float2(q[m1_perm(2 * k)], q[m1_perm(2 * k + 1)]), H[k]),
+                          make_float2(e[m1_perm(2 * k)], e[m1_perm(2 * k + 1)]));
     }
   }
   const int nch = (t1 - t0 + M1_TC - 1) / M1_TC;
-  __syncthreads();   // As staged
-  float a2[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) a2[i] = As[cl][qt * 4 + i];   // this thread's A·log2 e
-  auto issue = [&](int ch) {   // M1_TC rows x (x, dt, z, bc) x 2 16-B pieces = 128 pieces: one per thread
-    M1Raw& r = raw[ch & 1];
-    const int row = tid >> 3, kind = (tid >> 1) & 3, half = tid & 1;
+  auto issue = [&](int ch) {   // x | dt | z: one 16-B piece of each per thread; B̂Ĉ: 32 pieces
+    constexpr int PPR = CH / 16;   // pieces per token row
+    const int row = tid / PPR, off = (tid % PPR) * 16;
     const int t = t0 + ch * M1_TC + row;
     if (t < t1) {
       const int64_t tok = (int64_t)b * T + t;
-      const int8_t* src = kind == 0 ? x + tok * ldx + c0 : kind == 1 ? dt + tok * lddt + c0
-                        : kind == 2 ? z + tok * ldz + c0 : BC + tok * ldbc;
-      int8_t* dst = kind == 0 ? r.x[row] : kind == 1 ? r.dt[row] : kind == 2 ? r.z[row] : r.bc[row];
-      cp_async16(dst + half * 16, src + half * 16);
+      cp_async16(&raw[ch & 1][row][off], x + tok * ldx + c0 + off);
+      cp_async16(&raw[ch & 1][row][CH + off], dt + tok * lddt + c0 + off);
+      cp_async16(&raw[ch & 1][row][2 * CH + off], z + tok * ldz + c0 + off);
+    }
+    if (tid < 2 * M1_TC) {
+      const int rb = tid >> 1, hb = (tid & 1) * 16;
+      const int tb = t0 + ch * M1_TC + rb;
+      if (tb < t1) cp_async16(&raw[ch & 1][rb][3 * CH + hb], BC + ((int64_t)b * T + tb) * ldbc + hb);
     }
     cp_async_commit();
   };
-  static_assert(M1_TC * 8 == 128, "one 16-B piece per thread per chunk");
+  static_assert(M1_TC * (CH / 16) == CH && 2 * M1_TC <= CH, "one x|dt|z piece per thread per chunk");
   issue(0);
   for (int ch = 0; ch < nch; ++ch) {
     const int tn = min(M1_TC, t1 - t0 - ch * M1_TC);
-    if (ch + 1 < nch) {
-      __syncthreads();   // everyone is done reading raw[(ch + 1) & 1] (chunk ch - 1's staging)
-      issue(ch + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();   // raw[ch & 1] landed; the recurrence of chunk ch - 1 is done with stg
-    const M1Raw& r = raw[ch & 1];
-    // state-independent operands, all (token, channel) pairs of the chunk in parallel (4 per thread,
-    // unrolled: independent softplus / SiLU / exp chains interleave)
-#pragma unroll 4
-    for (int i = tid; i < tn * M1_CH; i += 128) {
-      const int row = i / M1_CH, cc = i % M1_CH, ch_g = c0 + cc;
-      const float delta = softplus_approx(__fadd_rn(__fmul_rn((float)r.dt[row][cc], p.s_dt), p.dt_bias[ch_g]));
-      const float xv = __fmul_rn((float)r.x[row][cc], p.s_x[ch_g]);
-      stg.dx[row][cc] = __fmul_rn(delta, xv);
-      stg.xh[row][cc] = xv;
-      stg.gz[row][cc] = silu_approx(__fmul_rn((float)r.z[row][cc], p.s_z));
-      stg.dl[row][cc] = delta;
-    }
-    for (int i = tid; i < tn * 32; i += 128) {
-      const int row = i >> 5, n = i & 31;
-      stg.bc[row][n] = __fmul_rn((float)r.bc[row][n], n < N ? p.s_B : p.s_C);
+    cp_async_wait<0>();
+    __syncthreads();   // raw[ch & 1] landed; every thread is done with chunk ch - 1 (raw and bcf)
+    if (ch + 1 < nch) issue(ch + 1);
+    const int8_t(*r)[3 * CH + 32] = raw[ch & 1];
+    float(*bf)[32] = bcf[ch & 1];
+    for (int i = tid; i < tn * 32; i += CH) {
+      const int row = i >> 5, q = i & 31;
+      const int src = q < N ? m1_perm(q) : N + m1_perm(q - N);
+      bf[row][q] = __fmul_rn(s8f(r[row][3 * CH + src]), q < N ? s_B : s_C);
     }
     __syncthreads();
     float* yrow = y + ((int64_t)b * T + t0 + ch * M1_TC) * ldy + c;
-#pragma unroll 4
+#pragma unroll M1_UNROLL
     for (int tt = 0; tt < tn; ++tt) {
-      const float dtx = stg.dx[tt][cl], dl = stg.dl[tt][cl];
-      const float4 av = make_float4(ex2_approx(__fmul_rn(dl, a2[0])), ex2_approx(__fmul_rn(dl, a2[1])),
-                                    ex2_approx(__fmul_rn(dl, a2[2])), ex2_approx(__fmul_rn(dl, a2[3])));
-      const float4 bv = *reinterpret_cast<const float4*>(&stg.bc[tt][qt * 4]);
-      hs[0] = __fadd_rn(__fmul_rn(av.x, hs[0]), __fmul_rn(dtx, bv.x));
-      hs[1] = __fadd_rn(__fmul_rn(av.y, hs[1]), __fmul_rn(dtx, bv.y));
-      hs[2] = __fadd_rn(__fmul_rn(av.z, hs[2]), __fmul_rn(dtx, bv.z));
-      hs[3] = __fadd_rn(__fmul_rn(av.w, hs[3]), __fmul_rn(dtx, bv.w));
-      if constexpr (MODE == 1) {
-        pr[0] = __fmul_rn(pr[0], av.x);
-        pr[1] = __fmul_rn(pr[1], av.y);
-        pr[2] = __fmul_rn(pr[2], av.z);
-        pr[3] = __fmul_rn(pr[3], av.w);
-      } else {
-        const float4 cv = *reinterpret_cast<const float4*>(&stg.bc[tt][N + qt * 4]);
-        float acc = fmaf(hs[3], cv.w, fmaf(hs[2], cv.z, fmaf(hs[1], cv.y, hs[0] * cv.x)));
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-        if (qt == 0)
-          yrow[(int64_t)tt * ldy] = __fmul_rn(__fadd_rn(acc, __fmul_rn(Dc, stg.xh[tt][cl])), stg.gz[tt][cl]);
+      const float delta = softplus_approx(__fadd_rn(__fmul_rn(s8f(r[tt][CH + tid]), s_dt), dtb));
+      const float xv = __fmul_rn(s8f(r[tt][tid]), sx);
+      const float dx = __fmul_rn(delta, xv);
+      const float2 dl2 = make_float2(delta, delta), dx2 = make_float2(dx, dx);
+      const float4* b4 = reinterpret_cast<const float4*>(bf[tt]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float2 t = __fmul2_rn(dl2, A2[k]);
+        const float2 av = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+        const float4 bq = b4[k >> 1];
+        const float2 bv = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
+        H[k] = __fadd2_rn(__fmul2_rn(av, H[k]), __fmul2_rn(dx2, bv));
+        if constexpr (MODE == 1) P2[k] = __fmul2_rn(P2[k], av);
+      }
+      if constexpr (MODE != 1) {
+        const float gz = silu_approx(__fmul_rn(s8f(r[tt][2 * CH + tid]), s_z));
+        const float4 cq0 = b4[4], cq1 = b4[5], cq2 = b4[6], cq3 = b4[7];
+        float2 a01 = __fmul2_rn(H[0], make_float2(cq0.x, cq0.y));
+        a01 = __ffma2_rn(H[1], make_float2(cq0.z, cq0.w), a01);
+        a01 = __ffma2_rn(H[2], make_float2(cq1.x, cq1.y), a01);
+        a01 = __ffma2_rn(H[3], make_float2(cq1.z, cq1.w), a01);
+        float2 a23 = __fmul2_rn(H[4], make_float2(cq2.x, cq2.y));
+        a23 = __ffma2_rn(H[5], make_float2(cq2.z, cq2.w), a23);
+        a23 = __ffma2_rn(H[6], make_float2(cq3.x, cq3.y), a23);
+        a23 = __ffma2_rn(H[7], make_float2(cq3.z, cq3.w), a23);
+        const float acc = __fadd_rn(__fadd_rn(a01.x, a01.y), __fadd_rn(a23.x, a23.y));
+        yrow[(int64_t)tt * ldy] = __fmul_rn(__fadd_rn(acc, __fmul_rn(Dc, xv)), gz);
       }
     }
   }
   if constexpr (MODE == 1) {
-    *reinterpret_cast<float4*>(ws + tc * zst + cell) = make_float4(hs[0], hs[1], hs[2], hs[3]);
-    *reinterpret_cast<float4*>(ws + (nz + tc) * zst + cell) = make_float4(pr[0], pr[1], pr[2], pr[3]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      ws[tc * zst + cell + m1_perm(2 * k)] = H[k].x;
+      ws[tc * zst + cell + m1_perm(2 * k + 1)] = H[k].y;
+      ws[(nz + tc) * zst + cell + m1_perm(2 * k)] = P2[k].x;
+      ws[(nz + tc) * zst + cell + m1_perm(2 * k + 1)] = P2[k].y;
+    }
   } else if (MODE == 0 || tc == nz - 1) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) st[i] = quant8(hs[i], sh);
+    for (int k = 0; k < 8; ++k) {
+      st[m1_perm(2 * k)] = quant8(H[k].x, sh);
+      st[m1_perm(2 * k + 1)] = quant8(H[k].y, sh);
+    }
   }
 }
 
 // time chunks of the two-pass form: up to 16, chunks >= 32 tokens
+static int m1_ch(int d_inner) {
+#ifdef SQ_M1_PROBE_CH   // profiling builds only
+  if (d_inner % SQ_M1_PROBE_CH == 0) return SQ_M1_PROBE_CH;
+#endif
+  return d_inner % 128 == 0 ? 128 : d_inner % 64 == 0 ? 64 : 32;
+}
 static int m1_time_chunks(int d_inner, int B, int T) {
 #ifdef SQ_M1_PROBE_NZ   // profiling builds only: fixed chunk count
   if (T / SQ_M1_PROBE_NZ >= M1_TC) return SQ_M1_PROBE_NZ;
 #endif
-  // same-box sweep at the 2.8B prefill shape (B=1, T=1024, 160 channel blocks; scripts/probe_m1.py):
-  // 1 / 2 / 4 / 8 / 16 chunks -> 203 / 259 / 137 / 111 / 108 us (16 KB smem per CTA)
-  const int ctas = (d_inner / M1_CH) * B;
+  const int ctas = (d_inner / m1_ch(d_inner)) * B;
   int nz = 1;
   while (nz < 16 && ctas * nz < 16 * 148 && T / (nz * 2) >= 32) nz *= 2;
   return nz;
@@ -846,24 +864,36 @@ extern "C" int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T, c
   SQ_REQUIRE(p && B >= 0 && T >= 0, SQ_ERR_ARG, "sq_selective_scan_int8: bad args");
   SQ_REQUIRE(p->d_state == 16, SQ_ERR_SHAPE, "sq_selective_scan_int8: d_state must be 16 (got %d)", p->d_state);
   if (B == 0 || T == 0) return SQ_OK;
-  if (T > 1 && p->d_inner % M1_CH == 0 && ldx % 16 == 0 && lddt % 16 == 0 && ldz % 16 == 0 && ldbc % 16 == 0 &&
+  if (T > 1 && p->d_inner % 32 == 0 && ldx % 16 == 0 && lddt % 16 == 0 && ldz % 16 == 0 && ldbc % 16 == 0 &&
       !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dt) | reinterpret_cast<uintptr_t>(z) |
          reinterpret_cast<uintptr_t>(BC)) & 15)) {
     cudaStream_t st = as_stream(stream);
     const int nz = ws ? m1_time_chunks(p->d_inner, B, T) : 1;
     const int tchunk = ((T + nz - 1) / nz + M1_TC - 1) / M1_TC * M1_TC;
-    const dim3 grid(p->d_inner / M1_CH, B, (T + tchunk - 1) / tchunk);
-    if (grid.z == 1) {
-      launch_k(PDL_SMALL8, mamba1_scan_staged_kernel<0>, grid, dim3(128), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc,
-               z, ldz, state, state_in, y, ldy, (float*)nullptr, tchunk);
+    const int chn = m1_ch(p->d_inner);
+    const dim3 grid(p->d_inner / chn, B, (T + tchunk - 1) / tchunk);
+    float* wsf = reinterpret_cast<float*>(ws);
+    SQ_REQUIRE(grid.z == 1 || (reinterpret_cast<uintptr_t>(ws) & 15) == 0, SQ_ERR_LAYOUT,
+               "sq_selective_scan_int8: ws alignment");
+#define SQ_M1_LAUNCH(MODE, C)                                                                                     \
+  launch_k(PDL_SMALL8, mamba1_scan_chunk_kernel<MODE, C>, grid, dim3(C), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc, \
+           z, ldz, state, state_in, y, ldy, wsf, tchunk)
+#define SQ_M1_PASSES(C)            \
+  if (grid.z == 1) {               \
+    SQ_M1_LAUNCH(0, C);            \
+  } else {                         \
+    SQ_M1_LAUNCH(1, C);            \
+    SQ_M1_LAUNCH(2, C);            \
+  }
+    if (chn == 128) {
+      SQ_M1_PASSES(128)
+    } else if (chn == 64) {
+      SQ_M1_PASSES(64)
     } else {
-      SQ_REQUIRE((reinterpret_cast<uintptr_t>(ws) & 15) == 0, SQ_ERR_LAYOUT, "sq_selective_scan_int8: ws alignment");
-      float* wsf = reinterpret_cast<float*>(ws);
-      launch_k(PDL_SMALL8, mamba1_scan_staged_kernel<1>, grid, dim3(128), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc,
-               z, ldz, state, state_in, y, ldy, wsf, tchunk);
-      launch_k(PDL_SMALL8, mamba1_scan_staged_kernel<2>, grid, dim3(128), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc,
-               z, ldz, state, state_in, y, ldy, wsf, tchunk);
+      SQ_M1_PASSES(32)
     }
+#undef SQ_M1_PASSES
+#undef SQ_M1_LAUNCH
     return check_launch("sq_selective_scan_int8");
   }
   if (T == 1) {   // decode step: 16 threads per channel
