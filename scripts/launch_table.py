@@ -11,7 +11,7 @@ agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[hi + 1:]:
     if len(r) > vi:
         v = float(r[vi].replace(",", ""))
-        v = v / 1000 if r[ui] == "nsecond" else v * 1000 if r[ui] == "msecond" else v
+        v = v / 1000 if r[ui] in ("nsecond", "ns") else v * 1000 if r[ui] in ("msecond", "ms") else v
         agg[r[ki][:80]][0] += 1
         agg[r[ki][:80]][1] += v
 tot = sum(t for _, t in agg.values())
