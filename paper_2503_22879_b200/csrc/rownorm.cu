@@ -306,6 +306,29 @@ constexpr int N1K_WARP_FLOATS = 2 * 32 * N1K_LD + 256;   // data tile, γ tile, 
 
 __device__ __forceinline__ int n1k_off(int p) { return (p >> 5) * N1K_LD + (p & 31); }   // element p -> tile
 
+// Sylvester stages h = 1..16 over 32 registers (element bits 0..4 = register index), the oracle's
+// stage order: h = 1 scalar (its pairs are adjacent registers), h >= 2 on packed f32x2 pairs
+// (v[i], v[i+1]) vs (v[i+h], v[i+h+1]); a - b as fma(b, -1, a) rounds like the subtraction.
+__device__ __forceinline__ void had32_regs(float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const float a = v[i], b = v[i + 1];
+    v[i] = __fadd_rn(a, b);
+    v[i + 1] = __fsub_rn(a, b);
+  }
+  const float2 M1 = make_float2(-1.f, -1.f);
+#pragma unroll
+  for (int h = 2; h < 32; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 2)
+      if ((i & h) == 0) {
+        const float2 a = make_float2(v[i], v[i + 1]), b = make_float2(v[i + h], v[i + h + 1]);
+        const float2 sm = __fadd2_rn(a, b), df = __ffma2_rn(b, M1, a);
+        v[i] = sm.x; v[i + 1] = sm.y; v[i + h] = df.x; v[i + h + 1] = df.y;
+      }
+  }
+}
+
 __global__ void __launch_bounds__(512) gate_norm_had1k_kernel(const float* y, int64_t ldy,
                                                                const float* __restrict__ gamma, float eps, float s_y,
                                                                int D, int M, int8_t* out, int64_t ldo) {
@@ -363,16 +386,7 @@ __global__ void __launch_bounds__(512) gate_norm_had1k_kernel(const float* y, in
       v[k * 4] = t0.x; v[k * 4 + 1] = t0.y; v[k * 4 + 2] = t1.x; v[k * 4 + 3] = t1.y;
     }
     // stages h = 1..16 (element bits 0..4 = register index)
-#pragma unroll
-    for (int h = 1; h < 32; h <<= 1) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if ((i & h) == 0) {
-          const float a = v[i], b = v[i + h];
-          v[i] = __fadd_rn(a, b);
-          v[i + h] = __fsub_rn(a, b);
-        }
-    }
+    had32_regs(v);
     __syncwarp();   // every lane has read its row of the tile
 #pragma unroll
     for (int k = 0; k < 8; ++k)
@@ -381,16 +395,7 @@ __global__ void __launch_bounds__(512) gate_norm_had1k_kernel(const float* y, in
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = s[i * N1K_LD + lane];   // lane l: elements i·32 + l
     // stages h = 32..512 (element bits 5..9 = register index)
-#pragma unroll
-    for (int h = 1; h < 32; h <<= 1) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if ((i & h) == 0) {
-          const float a = v[i], b = v[i + h];
-          v[i] = __fadd_rn(a, b);
-          v[i + h] = __fsub_rn(a, b);
-        }
-    }
+    had32_regs(v);
     const float is = __frcp_rn(s_y);
     const float2 is2 = make_float2(is, is);
     bool tie = false;
