@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQ_ABI_VERSION 5
+#define SQ_ABI_VERSION 6
 
 typedef enum {
   SQ_OK = 0,
@@ -206,6 +206,37 @@ typedef struct {
   const float* s_x;            /* [d_inner]                                            */
   const float* s_h;            /* [d_inner]                                            */
 } sq_mamba1_params;
+
+/* Mamba1 W8A8 decode step (T = 1, B <= 8), SSM half of a block in ONE launch (decode_m1.cu):
+ * conv update + cache shift -> x_proj -> dt_proj (both W8A8 int8 [N x K] row-major, EPI_QUANT
+ * epilogue quant8(f32(acc)*alpha[n], cs[n])) -> int8 scan step -> gated RMSNorm + FWHT + quant.
+ * Replaces sq_conv1d_update_int8 + 2x sq_gemm_w8a8 + sq_selective_scan_int8 (T=1) +
+ * sq_gate_norm_had_quant on the reference's decode path.
+ * zx [B x 2*d_inner] in_proj codes (z | x); ws: sq_mamba1_decode_ws_bytes bytes, 16-B aligned,
+ * ZEROED ONCE before first use (grid barrier counters, self-resetting); yq [B x d_inner]. */
+typedef struct {
+  sq_mamba1_params ssm;
+  int conv_kernel;
+  const float* conv_w;        /* [d_inner x conv_kernel]                              */
+  const float* conv_b;        /* [d_inner]                                            */
+  const float* conv_s_in;     /* [d_inner] in_proj x code scales                      */
+  const float* conv_s_out;    /* [d_inner] conv output scales                         */
+  int dt_rank;
+  const int8_t* xproj_w;      /* [dt_rank + 2N x d_inner]                             */
+  const float* xproj_alpha;   /* [dt_rank + 2N]  s_w[n] * s_a                          */
+  const float* xproj_cs;      /* [dt_rank + 2N]  output code scales                   */
+  const int8_t* dtproj_w;     /* [d_inner x dt_rank]                                  */
+  const float* dtproj_alpha;  /* [d_inner]                                            */
+  const float* dtproj_cs;     /* [d_inner]                                            */
+  const float* norm_w;        /* [d_inner]                                            */
+  float eps, s_y;
+  int hadamard;
+} sq_mamba1_decode_params;
+
+int64_t sq_mamba1_decode_ws_bytes(const sq_mamba1_decode_params* p, int B);
+int sq_mamba1_decode_step_int8(const sq_mamba1_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
+                               int8_t* conv_cache /*[B x (Kc-1) x d_inner]*/, int8_t* state /*[B x d_inner x 16]*/,
+                               void* ws, int8_t* yq, int64_t ldyq, void* stream);
 
 /* Mamba1 prefill (T>=1; T=1 is decode): codes x [B*T x d], dt [B*T x d], B/C [B*T x N]
  * (row stride ldbc, C at +N), z [B*T x d]; state int8 [B x d x N].  ws (16-B aligned,

@@ -10,7 +10,7 @@ import os
 
 LIB_NAME = "libssmquant_sm100.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _i8p = C.c_void_p
 _f32p = C.c_void_p
@@ -34,6 +34,13 @@ class Mamba2DecodeParams(C.Structure):
 class Mamba1Params(C.Structure):
     _fields_ = [("d_inner", _int), ("d_state", _int), ("A", _vp), ("D", _vp), ("dt_bias", _vp),
                 ("s_dt", _flt), ("s_z", _flt), ("s_B", _flt), ("s_C", _flt), ("s_x", _vp), ("s_h", _vp)]
+
+
+class Mamba1DecodeParams(C.Structure):
+    _fields_ = [("ssm", Mamba1Params), ("conv_kernel", _int), ("conv_w", _vp), ("conv_b", _vp), ("conv_s_in", _vp),
+                ("conv_s_out", _vp), ("dt_rank", _int), ("xproj_w", _vp), ("xproj_alpha", _vp), ("xproj_cs", _vp),
+                ("dtproj_w", _vp), ("dtproj_alpha", _vp), ("dtproj_cs", _vp), ("norm_w", _vp), ("eps", _flt),
+                ("s_y", _flt), ("hadamard", _int)]
 
 
 _SIGS = {
@@ -71,6 +78,9 @@ _SIGS = {
                                 _vp, _int, _vp, _i64, _vp, _vp], _int),
     "sq_selective_scan_f32": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                                 _vp, _int, _vp, _i64, _vp], _int),
+    "sq_mamba1_decode_ws_bytes": ([C.POINTER(Mamba1DecodeParams), _int], _i64),
+    "sq_mamba1_decode_step_int8": ([C.POINTER(Mamba1DecodeParams), _int, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp],
+                                   _int),
     "sq_mamba2_decode_ws_bytes": ([C.POINTER(Mamba2DecodeParams), _int], _i64),
     "sq_mamba2_decode_launches": ([C.POINTER(Mamba2DecodeParams), _int, _int], _int),
     "sq_mamba2_decode_step_int8": ([C.POINTER(Mamba2DecodeParams), _int, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp,

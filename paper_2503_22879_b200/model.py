@@ -96,6 +96,11 @@ class QuantizedMambaLM:
             # zero-filled once: the fused decode kernel's counters live here (self-resetting)
             ws["dws"] = torch.zeros((ops.mamba2_decode_ws_bytes(fused[0].decode_params, M),), dtype=torch.uint8,
                                     device=dev)
+        m1f = [b for b in self.blocks if getattr(b, "m1_fused_decode", False)]
+        if m1f and M <= 8:
+            # zero-filled once: the one-launch Mamba1 decode keeps its grid-barrier counters here
+            ws["m1ws"] = torch.zeros((ops.mamba1_decode_ws_bytes(m1f[0].m1_decode_params, M),), dtype=torch.uint8,
+                                     device=dev)
         if any(not b.a8 for b in self.blocks):
             ws.update(uf=e((M, d.d_model), torch.float32), zxf=e((M, d.in_proj_out), torch.float32),
                       convf=e((M, d.conv_dim), torch.float32), r=e((M, d.d_inner), torch.float32))

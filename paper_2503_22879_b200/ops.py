@@ -373,6 +373,45 @@ def mamba2_decode_step_int8(p, B, zx, conv_cache, state, yq=None, y=None, ws=Non
     return yq
 
 
+def mamba1_decode_params(ssm: _lib.Mamba1Params, conv_w, conv_b, conv_s_in, conv_s_out, dt_rank, xproj_w,
+                         xproj_alpha, xproj_cs, dtproj_w, dtproj_alpha, dtproj_cs, norm_w, eps, s_y,
+                         hadamard=True) -> _lib.Mamba1DecodeParams:
+    """Parameter struct of the one-launch Mamba1 W8A8 decode step; keeps no tensor references."""
+    return _lib.Mamba1DecodeParams(ssm, int(conv_w.shape[1]), conv_w.data_ptr(), conv_b.data_ptr(),
+                                   conv_s_in.data_ptr(), conv_s_out.data_ptr(), int(dt_rank), xproj_w.data_ptr(),
+                                   xproj_alpha.data_ptr(), xproj_cs.data_ptr(), dtproj_w.data_ptr(),
+                                   dtproj_alpha.data_ptr(), dtproj_cs.data_ptr(), norm_w.data_ptr(), float(eps),
+                                   float(s_y), int(bool(hadamard)))
+
+
+def mamba1_decode_ws_bytes(p, B) -> int:
+    return int(lib().sq_mamba1_decode_ws_bytes(C.byref(p), B))
+
+
+def mamba1_decode_step_int8(p, B, zx, conv_cache, state, ws, yq=None):
+    """Mamba1 W8A8 decode step, SSM half of a block in one launch (conv update, x_proj, dt_proj,
+    int8 scan step, gated norm + FWHT + quant).  zx int8 [B x 2*d_inner] (z | x); conv_cache int8
+    [B x (K-1) x d_inner] and state int8 [B x d_inner x 16] are updated in place; ``ws`` (uint8,
+    mamba1_decode_ws_bytes) must have been zero-filled once (grid-barrier counters).  Returns
+    yq int8 [B x d_inner]."""
+    _dev(zx, torch.int8, "zx", 2)
+    _dev(conv_cache, torch.int8, "conv_cache")
+    _dev(state, torch.int8, "state")
+    di = p.ssm.d_inner
+    _rows(zx, B, "zx")
+    _need(state, B * di * p.ssm.d_state, "state [B x d_inner x N]")
+    _need(conv_cache, B * (p.conv_kernel - 1) * di, "conv_cache [B x (K-1) x d_inner]")
+    if yq is None:
+        yq = torch.empty((B, di), dtype=torch.int8, device=zx.device)
+    _dev(yq, torch.int8, "yq", 2)
+    nbytes = mamba1_decode_ws_bytes(p, B)
+    if ws is None or ws.numel() * ws.element_size() < nbytes:
+        raise ShapeError(f"Mamba1 decode workspace needs {nbytes} zero-initialised bytes")
+    _check(lib().sq_mamba1_decode_step_int8(C.byref(p), B, zx.data_ptr(), _ld(zx), conv_cache.data_ptr(),
+                                            state.data_ptr(), ws.data_ptr(), yq.data_ptr(), _ld(yq), _stream()), 1)
+    return yq
+
+
 def mamba1_params(d_inner, d_state, A, D, dt_bias, s_dt, s_z, s_B, s_C, s_x, s_h) -> _lib.Mamba1Params:
     return _lib.Mamba1Params(d_inner, d_state, A.data_ptr(), D.data_ptr(), dt_bias.data_ptr(), float(s_dt),
                              float(s_z), float(s_B), float(s_C), s_x.data_ptr(), s_h.data_ptr())

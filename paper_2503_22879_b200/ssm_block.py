@@ -274,6 +274,14 @@ class DeviceBlock:
                 self.s_x = f(qb.conv_out_scale)
                 self.params = ops.mamba1_params(di, N, self.A, self.D, self.dt_bias, np.float32(qb.s_dt), ios[0],
                                                 xos[R], xos[R + N], self.s_x, self.state_scale)
+                # one-launch decode (conv, x_proj, dt_proj, scan step, norm; decode_m1.cu) for W8 projections
+                self.m1_fused_decode = (self.x_proj.kind == "w8" and self.dt_proj.kind == "w8" and N == 16
+                                        and R % 4 == 0 and di % 16 == 0)
+                if self.m1_fused_decode:
+                    self.m1_decode_params = ops.mamba1_decode_params(
+                        self.params, self.conv_w, self.conv_b, self.conv_in_scale, self.conv_out_scale, R,
+                        self.x_proj.w, self.x_proj.alpha, self.xproj_out_scale, self.dt_proj.w, self.dt_proj.alpha,
+                        self.dt_scale, self.norm_w, EPS_NORM, self.s_y, self.hadamard)
         else:
             if d.variant == "mamba2":
                 self.params = ops.mamba2_params(d.n_heads, d.head_dim, d.d_state, d.n_state_groups,
@@ -338,6 +346,16 @@ class DeviceBlock:
         else:
             R, N = d.dt_rank, d.d_state
             xin = zx[:, di:]
+            if T == 1 and state_in and getattr(self, "m1_fused_decode", False) and B <= 8:
+                m1ws = ws.get("m1ws")
+                if m1ws is None:   # zero-filled: the kernel's grid-barrier counters live here
+                    m1ws = torch.zeros(ops.mamba1_decode_ws_bytes(self.m1_decode_params, B), dtype=torch.uint8,
+                                       device=u_codes.device)
+                yq = ops.mamba1_decode_step_int8(self.m1_decode_params, B, zx, state.conv_cache, state.h, m1ws,
+                                                 ws.get("yq"))
+                if resid is not None:
+                    return self.out_proj.a8(yq, ops.EPI_RESID, resid)
+                return self.out_proj.a8(yq, ops.EPI_F32, ws.get("out"))
             if T == 1 and state_in:
                 cv = ops.conv1d_update_int8(xin, self.conv_w, self.conv_b, self.conv_in_scale, self.conv_out_scale,
                                             state.conv_cache, ws.get("conv"))

@@ -97,3 +97,70 @@ def test_fused_decode_repeat_deterministic(cuda):
     for o in outs[1:]:
         for a, b in zip(o, outs[0]):
             assert torch.equal(a, b)
+
+
+M1_SHAPES = {
+    "tiny": (("mamba1", 256, 512, 16, 1, 512, 1, 4, 32), 3),
+    "m1_2p8b": (("mamba1", 2560, 5120, 16, 1, 5120, 1, 4, 160), 1),
+    "m1_2p8b_b8": (("mamba1", 2560, 5120, 16, 1, 5120, 1, 4, 160), 8),
+}
+
+
+@pytest.mark.parametrize("shape", sorted(M1_SHAPES))
+def test_mamba1_fused_decode_matches_launch_chain(cuda, shape):
+    """The one-launch Mamba1 W8A8 decode step (sq_mamba1_decode_step_int8: conv update, x_proj,
+    dt_proj, scan step, gated norm + FWHT + quant behind grid barriers) against the five-launch
+    chain it replaces (sq_conv1d_update_int8, two tcgen05 W8A8 GEMMs, the T=1 scan kernel,
+    sq_gate_norm_had_quant), three steps in a row on the same codes: conv cache and int8 state
+    bit-exact, yq within one step (Σy² is summed in another fixed order), mismatch < 1e-3."""
+    from paper_2503_22879_b200 import ops, synth
+    from paper_2503_22879_b200.ssm_block import EPS_NORM, DeviceBlock, Dims
+    dims, B = M1_SHAPES[shape]
+    d = Dims(*dims)
+    blk = DeviceBlock(synth.random_qblock(d, "W8A8", seed=7), cuda)
+    assert blk.m1_fused_decode
+    di, R = d.d_inner, d.dt_rank
+    g = torch.Generator(device=cuda)
+    g.manual_seed(11)
+    h0 = torch.randint(-100, 100, (B, 1, di, 16), dtype=torch.int8, device=cuda, generator=g)
+    c0 = torch.randint(-100, 100, (B, d.conv_kernel - 1, di), dtype=torch.int8, device=cuda, generator=g)
+    hf, cf, hu, cu = h0.clone(), c0.clone(), h0.clone(), c0.clone()
+    ws = torch.zeros(ops.mamba1_decode_ws_bytes(blk.m1_decode_params, B), dtype=torch.uint8, device=cuda)
+    for step in range(3):
+        zx = torch.randint(-128, 128, (B, 2 * di), dtype=torch.int8, device=cuda, generator=g)
+        yf = ops.mamba1_decode_step_int8(blk.m1_decode_params, B, zx, cf, hf, ws)
+        cv = ops.conv1d_update_int8(zx[:, di:], blk.conv_w, blk.conv_b, blk.conv_in_scale, blk.conv_out_scale, cu)
+        xd = blk.x_proj.a8(cv, ops.EPI_QUANT, None, blk.xproj_out_scale)
+        dtq = blk.dt_proj.a8(xd[:, :R].contiguous(), ops.EPI_QUANT, None, blk.dt_scale)
+        y = torch.empty((B, di), device=cuda)
+        ops.selective_scan_int8(blk.params, B, 1, cv, dtq, xd[:, R:], zx[:, :di], hu, True, y)
+        yu = ops.gate_norm_had_quant(y, blk.norm_w, EPS_NORM, blk.s_y, blk.hadamard)
+        torch.cuda.synchronize()
+        assert torch.equal(cf, cu), step
+        assert torch.equal(hf, hu), step
+        mx, frac = _diff(yf.cpu().numpy(), yu.cpu().numpy())
+        assert mx <= 1 and frac < 1e-3, (step, mx, frac)
+
+
+def test_mamba1_fused_decode_repeat_deterministic(cuda):
+    """The grid-barrier counters reset themselves: repeated launches on one workspace agree bit
+    for bit."""
+    from paper_2503_22879_b200 import ops, synth
+    from paper_2503_22879_b200.ssm_block import DeviceBlock, Dims
+    d = Dims(*M1_SHAPES["m1_2p8b"][0])
+    blk = DeviceBlock(synth.random_qblock(d, "W8A8", seed=3), cuda)
+    B = 2
+    g = torch.Generator(device=cuda)
+    g.manual_seed(5)
+    zx = torch.randint(-128, 128, (B, 2 * d.d_inner), dtype=torch.int8, device=cuda, generator=g)
+    h = torch.randint(-100, 100, (B, 1, d.d_inner, 16), dtype=torch.int8, device=cuda, generator=g)
+    cc = torch.randint(-100, 100, (B, 3, d.d_inner), dtype=torch.int8, device=cuda, generator=g)
+    ws = torch.zeros(ops.mamba1_decode_ws_bytes(blk.m1_decode_params, B), dtype=torch.uint8, device=cuda)
+    outs = []
+    for _ in range(4):
+        h1, c1 = h.clone(), cc.clone()
+        yq = ops.mamba1_decode_step_int8(blk.m1_decode_params, B, zx, c1, h1, ws)
+        outs.append((yq.cpu(), h1.cpu(), c1.cpu()))
+    for o in outs[1:]:
+        for a, b in zip(o, outs[0]):
+            assert torch.equal(a, b)
