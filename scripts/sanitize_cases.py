@@ -2,7 +2,7 @@
 compute-sanitizer (scripts/sanitize.sh): W4A8 GEMM (persistent and split-K cluster), W8A8 GEMM
 (single and split-K), the fused decode step (prep + state ring + norm), both chunked-SSD engines,
 the int8 conv and the gated norm, the W4A16 bf16 GEMV (mma.sync and row fallback) and the Mamba1
-int8 scan (single pass and the time-chunked two-pass form)."""
+int8 scan (single pass and the time-chunked two-pass form) and the one-launch Mamba1 decode step."""
 import os
 import sys
 
@@ -80,6 +80,14 @@ def m1():
         bc = torch.randint(-100, 100, (T, 32), dtype=torch.int8, device=dev, generator=g)
         st = torch.zeros((1, 64, 16), dtype=torch.int8, device=dev)
         ops.selective_scan_int8(blk.params, 1, T, x, dt, bc, z, st, False, torch.empty((T, 64), device=dev))
+    # one-launch decode step (grid barriers), twice on one workspace (self-resetting counters)
+    B = 2
+    zx = torch.randint(-100, 100, (B, 128), dtype=torch.int8, device=dev, generator=g)
+    st = torch.zeros((B, 1, 64, 16), dtype=torch.int8, device=dev)
+    cc = torch.zeros((B, 3, 64), dtype=torch.int8, device=dev)
+    ws = torch.zeros(ops.mamba1_decode_ws_bytes(blk.m1_decode_params, B), dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        ops.mamba1_decode_step_int8(blk.m1_decode_params, B, zx, cc, st, ws)
 
 
 run("w4a8", w4a8)
