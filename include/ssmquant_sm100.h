@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQ_ABI_VERSION 6
+#define SQ_ABI_VERSION 7
 
 typedef enum {
   SQ_OK = 0,
@@ -118,6 +118,23 @@ int sq_gemv_w4a16(const float* x, int64_t ldx, const float* norm_w /*[K] or NULL
                   const uint8_t* w4 /*sq_repack_w4a16 layout*/,
                   const float* s_group /*[N x K/group]*/, int group, int M, int N, int K,
                   float* out, int64_t ldo, int resid, void* stream);
+/* sq_gemv_w4a16 with the depthwise causal conv (T = 1 decode update) fused into
+ * the epilogue: for output columns n in [c0, c0 + C) the token's conv channel c = n - c0 takes
+ * win = cache[m][0..Kc-2][c] | out[m][n], writes silu(bias[c] + Σ_j w[c][j]·win[j]) (unfused f32,
+ * j ascending, as sq_conv1d_f32) to conv_out[m][c] and shifts the cache; the GEMV output itself
+ * is written as before.  Replaces the sq_conv1d_f32 (T=1) launch of the W4A16 decode step. */
+typedef struct {
+  const float* w;      /* [C x Kc] */
+  const float* b;      /* [C]      */
+  int kc, c0, C;
+  float* cache;        /* [M x (Kc-1) x C] */
+  int cache_in;
+  float* out;          /* [M x ldo]       */
+  int64_t ldo;
+} sq_conv_epilogue;
+int sq_gemv_w4a16_conv(const float* x, int64_t ldx, const float* norm_w, float eps, const uint8_t* w4,
+                       const float* s_group, int group, int M, int N, int K, float* out, int64_t ldo, int resid,
+                       const sq_conv_epilogue* conv, void* stream);
 
 /* ---- causal conv1d (+SiLU +requant) ------------------------------------------------- */
 /* x codes [B*T x C] (row stride ldx), cache codes [B x (Kc-1) x C] (read as the initial

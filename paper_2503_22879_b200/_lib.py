@@ -10,7 +10,7 @@ import os
 
 LIB_NAME = "libssmquant_sm100.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 _i8p = C.c_void_p
 _f32p = C.c_void_p
@@ -43,6 +43,11 @@ class Mamba1DecodeParams(C.Structure):
                 ("s_y", _flt), ("hadamard", _int)]
 
 
+class ConvEpilogue(C.Structure):
+    _fields_ = [("w", _vp), ("b", _vp), ("kc", _int), ("c0", _int), ("C", _int), ("cache", _vp), ("cache_in", _int),
+                ("out", _vp), ("ldo", _i64)]
+
+
 _SIGS = {
     "sq_abi_version": ([], _int),
     "sq_last_error": ([], C.c_char_p),
@@ -64,6 +69,8 @@ _SIGS = {
     "sq_w4a16_bytes": ([_int, _int, _int], _i64),
     "sq_repack_w4a16": ([_vp, _int, _int, _int, _vp, _vp], _int),
     "sq_gemv_w4a16": ([_vp, _i64, _vp, _flt, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _int, _vp], _int),
+    "sq_gemv_w4a16_conv": ([_vp, _i64, _vp, _flt, _vp, _vp, _int, _int, _int, _int, _vp, _i64, _int,
+                            C.POINTER(ConvEpilogue), _vp], _int),
     "sq_conv1d_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _i64, _vp], _int),
     "sq_conv1d_update_int8": ([_vp, _i64, _vp, _vp, _vp, _vp, _int, _int, _int, _vp, _vp, _i64, _vp], _int),
     "sq_conv1d_f32": ([_vp, _i64, _vp, _vp, _int, _int, _int, _int, _vp, _int, _vp, _i64, _vp], _int),

@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(NW * 32) gemv_w4a16_mma_kernel(const float* x,
                                                                 const float* __restrict__ norm_w, float eps,
                                                                 const uint8_t* __restrict__ w,
                                                                 const float* __restrict__ sgrp, int M, int N,
-                                                                int K, float* out, int64_t ldo, int resid) {
+                                                                int K, float* out, int64_t ldo, int resid,
+                                                                sq_conv_epilogue conv) {
   pdl_trigger();
   extern __shared__ __align__(16) uint8_t gv_smem[];
   const int KP = K + 8;
@@ -231,7 +232,27 @@ __global__ void __launch_bounds__(NW * 32) gemv_w4a16_mma_kernel(const float* x,
 #pragma unroll
       for (int ww = 1; ww < NW; ++ww) v = __fadd_rn(v, part[ww * 32 * GV_TOK + i]);
       float* o = out + (int64_t)m * ldo + n;
-      *o = resid ? __fadd_rn(*o, v) : v;
+      v = resid ? __fadd_rn(*o, v) : v;
+      *o = v;
+      const int c = n - conv.c0;
+      if (c >= 0 && c < conv.C) {   // fused conv update of channel c (sq_conv1d_f32's T = 1 math)
+        const int kc = conv.kc;
+        float* cr = conv.cache + (int64_t)m * (kc - 1) * conv.C + c;
+        float win[8], wc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          wc[j] = j < kc ? __ldg(conv.w + c * kc + j) : 0.f;
+          win[j] = (j < kc - 1 && conv.cache_in) ? cr[(int64_t)j * conv.C] : 0.f;
+        }
+        float acc = __ldg(conv.b + c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < kc) acc = __fadd_rn(acc, __fmul_rn(wc[j], j == kc - 1 ? v : win[j]));
+        conv.out[(int64_t)m * conv.ldo + c] = silu_f(acc);
+#pragma unroll
+        for (int j = 0; j + 1 < 8; ++j)
+          if (j + 1 < kc) cr[(int64_t)j * conv.C] = j + 1 == kc - 1 ? v : win[j + 1];
+      }
     }
   }
 }
@@ -346,9 +367,17 @@ extern "C" int sq_repack_w4a16(const uint8_t* u4packed, int N, int K, int group,
   return check_launch("sq_repack_w4a16");
 }
 
-extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const float* norm_w, float eps, const uint8_t* w4,
-                             const float* s_group, int group, int M, int N, int K, float* out, int64_t ldo, int resid,
-                             void* stream) {
+extern "C" int sq_gemv_w4a16_conv(const float* x, int64_t ldx, const float* norm_w, float eps, const uint8_t* w4,
+                                  const float* s_group, int group, int M, int N, int K, float* out, int64_t ldo,
+                                  int resid, const sq_conv_epilogue* conv_in, void* stream) {
+  sq_conv_epilogue conv{};
+  if (conv_in) {
+    conv = *conv_in;
+    SQ_REQUIRE(conv.w && conv.b && conv.cache && conv.out && conv.kc >= 1 && conv.kc <= 8 && conv.c0 >= 0 &&
+                   conv.C > 0 && conv.c0 + conv.C <= N,
+               SQ_ERR_SHAPE, "sq_gemv_w4a16_conv: bad conv epilogue (kc %d, columns %d + %d of %d)", conv.kc,
+               conv.c0, conv.C, N);
+  }
   SQ_REQUIRE(x && w4 && s_group && out && M >= 0 && N > 0 && K > 0 && group > 0 && K % group == 0 && K % 2 == 0,
              SQ_ERR_SHAPE, "sq_gemv_w4a16: bad shape M=%d N=%d K=%d group=%d", M, N, K, group);
   cudaStream_t st = as_stream(stream);
@@ -371,8 +400,13 @@ extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const float* norm_w, f
       SQ_REQUIRE(smem <= 227 * 1024, SQ_ERR_SHAPE, "sq_gemv_w4a16: K too large");
       auto launch = [&](auto kern) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sq_conv_epilogue cv = conv;   // this pass's tokens m0 .. m0 + mc - 1
+        if (cv.C > 0) {
+          cv.cache += (int64_t)m0 * (cv.kc - 1) * cv.C;
+          cv.out += (int64_t)m0 * cv.ldo;
+        }
         launch_k(PDL_SMALL, kern, dim3(cta), dim3(nw * 32), smem, st, x + (int64_t)m0 * ldx, ldx, norm_w, eps, w4,
-                 s_group, mc, N, K, out + (int64_t)m0 * ldo, ldo, resid);
+                 s_group, mc, N, K, out + (int64_t)m0 * ldo, ldo, resid, cv);
       };
 #ifndef SQ_GV_DG
 #define SQ_GV_DG 3
@@ -400,5 +434,17 @@ extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const float* norm_w, f
     gemv_w4a16_rows_kernel<<<blocks, 256, smem, st>>>(x + (int64_t)m0 * ldx, ldx, norm_w, eps, w4, s_group, group,
                                                       mc, N, K, out + (int64_t)m0 * ldo, ldo, resid);
   }
+  if (conv.C > 0) {   // the row-major fallback has no fused epilogue: the separate conv update
+    const int rc = check_launch("sq_gemv_w4a16");
+    if (rc != SQ_OK) return rc;
+    return sq_conv1d_f32(out + conv.c0, ldo, conv.w, conv.b, M, 1, conv.C, conv.kc, conv.cache, conv.cache_in,
+                         conv.out, conv.ldo, stream);
+  }
   return check_launch("sq_gemv_w4a16");
+}
+
+extern "C" int sq_gemv_w4a16(const float* x, int64_t ldx, const float* norm_w, float eps, const uint8_t* w4,
+                             const float* s_group, int group, int M, int N, int K, float* out, int64_t ldo, int resid,
+                             void* stream) {
+  return sq_gemv_w4a16_conv(x, ldx, norm_w, eps, w4, s_group, group, M, N, K, out, ldo, resid, nullptr, stream);
 }

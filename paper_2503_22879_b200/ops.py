@@ -253,10 +253,12 @@ def gemm_w4a8(a, w4, w_scale, group, s_a, N, epi=EPI_F32, out=None, col_scale=No
     return out
 
 
-def gemv_w4a16(x, w4, s_group, group, N, out=None, resid=False, norm_w=None, eps=1e-5):
+def gemv_w4a16(x, w4, s_group, group, N, out=None, resid=False, norm_w=None, eps=1e-5, conv=None):
     """W4A16 projection: x f32 [M x K] (rounded to bf16 on load; RMS-normalised with norm_w
     first when given), w4 in the sq_repack_w4a16 layout, s_group f32 [N x K/group]; out f32
-    [M x N] (+= when resid)."""
+    [M x N] (+= when resid).  ``conv`` = (w [C x Kc], bias [C], c0, cache [M x (Kc-1) x C],
+    cache_in, conv_out [M x C]) fuses the T = 1 causal-conv update of output columns
+    c0 .. c0+C-1 into the epilogue (sq_gemv_w4a16_conv)."""
     _dev(x, torch.float32, "x", 2)
     _dev(w4, torch.uint8, "w4")
     M, K = x.shape
@@ -272,9 +274,23 @@ def gemv_w4a16(x, w4, s_group, group, N, out=None, resid=False, norm_w=None, eps
     if out is None:
         out = torch.empty((M, N), dtype=torch.float32, device=x.device)
     _dev(out, torch.float32, "out", 2)
-    _check(lib().sq_gemv_w4a16(x.data_ptr(), _ld(x), norm_w.data_ptr() if norm_w is not None else None,
-                               float(eps), w4.data_ptr(), s_group.data_ptr(), group, M, N, K, out.data_ptr(),
-                               _ld(out), int(bool(resid)), _stream()))
+    if conv is None:
+        _check(lib().sq_gemv_w4a16(x.data_ptr(), _ld(x), norm_w.data_ptr() if norm_w is not None else None,
+                                   float(eps), w4.data_ptr(), s_group.data_ptr(), group, M, N, K, out.data_ptr(),
+                                   _ld(out), int(bool(resid)), _stream()))
+        return out
+    cw, cb, c0, cache, cache_in, cout = conv
+    _dev(cw, torch.float32, "conv w", 2)
+    _dev(cache, torch.float32, "conv cache")
+    _dev(cout, torch.float32, "conv out", 2)
+    Cc, Kc = cw.shape
+    _need(cache, M * (Kc - 1) * Cc, "conv cache [M x (K-1) x C]")
+    _rows(cout, M, "conv out")
+    ep = _lib.ConvEpilogue(cw.data_ptr(), cb.data_ptr(), Kc, int(c0), Cc, cache.data_ptr(), int(bool(cache_in)),
+                           cout.data_ptr(), _ld(cout))
+    _check(lib().sq_gemv_w4a16_conv(x.data_ptr(), _ld(x), norm_w.data_ptr() if norm_w is not None else None,
+                                    float(eps), w4.data_ptr(), s_group.data_ptr(), group, M, N, K, out.data_ptr(),
+                                    _ld(out), int(bool(resid)), C.byref(ep), _stream()))
     return out
 
 

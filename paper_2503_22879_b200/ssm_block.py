@@ -203,9 +203,10 @@ class DeviceLinear:
             return ops.gemm_w4a8(a_codes, self.w, self.ws, self.group, self.s_a, self.N, epi, out, col_scale)
         raise ShapeError("A8 GEMM on a W4A16 projection")
 
-    def a16(self, x, out=None, resid=False, norm_w=None):
-        """W4A16 projection of x (RMS-normalised with norm_w on the way in when given)."""
-        return ops.gemv_w4a16(x, self.w, self.s_group, self.group, self.N, out, resid, norm_w, EPS_NORM)
+    def a16(self, x, out=None, resid=False, norm_w=None, conv=None):
+        """W4A16 projection of x (RMS-normalised with norm_w on the way in when given; ``conv`` fuses
+        the T = 1 conv update of a column range into the epilogue, ops.gemv_w4a16)."""
+        return ops.gemv_w4a16(x, self.w, self.s_group, self.group, self.N, out, resid, norm_w, EPS_NORM, conv)
 
     @property
     def nbytes(self):
@@ -377,11 +378,18 @@ class DeviceBlock:
         d = self.dims
         di = d.d_inner
         ws = ws if ws is not None else {}
-        zx = self.in_proj.a16(u, ws.get("zxf"), norm_w=u_norm)
+        conv = None
+        if T == 1:   # decode: the conv update runs in the in_proj GEMV's epilogue (sq_gemv_w4a16_conv)
+            cv = ws.get("convf")
+            if cv is None:
+                cv = torch.empty((B, d.conv_dim), dtype=torch.float32, device=u.device)
+            conv = (self.conv_w, self.conv_b, di, state.conv_cache, state_in, cv)
+        zx = self.in_proj.a16(u, ws.get("zxf"), norm_w=u_norm, conv=conv)
         if d.variant == "mamba1":   # in_proj rows z | x; x_proj rows Δ_low | B | C (LEDGER G4)
             R = d.dt_rank
-            cv = ops.conv1d_f32(zx[:, di:], self.conv_w, self.conv_b, B, T, state.conv_cache, state_in,
-                                ws.get("convf"))
+            if conv is None:
+                cv = ops.conv1d_f32(zx[:, di:], self.conv_w, self.conv_b, B, T, state.conv_cache, state_in,
+                                    ws.get("convf"))
             xd = self.x_proj.a16(cv)
             dtr = self.dt_proj.a16(xd[:, :R])
             y = ws.get("y")
@@ -391,7 +399,8 @@ class DeviceBlock:
         else:
             gn = d.n_state_groups * d.d_state
             xbc = zx[:, di:2 * di + 2 * gn]
-            cv = ops.conv1d_f32(xbc, self.conv_w, self.conv_b, B, T, state.conv_cache, state_in, ws.get("convf"))
+            if conv is None:
+                cv = ops.conv1d_f32(xbc, self.conv_w, self.conv_b, B, T, state.conv_cache, state_in, ws.get("convf"))
             y = ws.get("y")
             if y is None:
                 y = torch.empty((B * T, di), dtype=torch.float32, device=u.device)

@@ -151,6 +151,35 @@ def test_gemv_w4a16(cuda, M, N, K, group):
     assert np.abs(tb.cpu().numpy() - (base + got)).max() <= 1e-6 * np.abs(base + got).max() + 1e-6
 
 
+@pytest.mark.parametrize("M,N,K,group", [(1, 1280, 512, 128), (3, 1000, 512, 64), (9, 1280, 256, 128),
+                                          (2, 1280, 160, 32)])
+def test_gemv_w4a16_conv_epilogue(cuda, M, N, K, group):
+    """The T = 1 conv update fused into the W4A16 GEMV epilogue (sq_gemv_w4a16_conv) equals the
+    GEMV followed by sq_conv1d_f32 bit for bit (GEMV output, conv output, shifted cache), on the
+    mma.sync path (one and two token passes) and the row-major fallback (separate conv launch)."""
+    ops = _ops()
+    from paper_2503_22879_b200.ssm_block import pack_u4_host
+    r = _rng(9, M, N)
+    x = torch.as_tensor(r.standard_normal((M, K)).astype(np.float32), device=cuda)
+    codes = r.integers(-8, 8, (N, K)).astype(np.int8)
+    sgrp = torch.as_tensor(r.uniform(1e-3, 1e-2, (N, K // group)).astype(np.float32), device=cuda)
+    tw = ops.repack_w4a16(torch.as_tensor(pack_u4_host(codes), device=cuda), N, K, group)
+    c0, C, Kc = 200, 640, 4
+    cw = torch.as_tensor(r.standard_normal((C, Kc)).astype(np.float32), device=cuda)
+    cb = torch.as_tensor(r.standard_normal(C).astype(np.float32), device=cuda)
+    cache = torch.as_tensor(r.standard_normal((M, Kc - 1, C)).astype(np.float32), device=cuda)
+    ref_out = ops.gemv_w4a16(x, tw, sgrp, group, N)
+    ref_cache = cache.clone()
+    ref_conv = ops.conv1d_f32(ref_out[:, c0:c0 + C], cw, cb, M, 1, ref_cache, True)
+    cache2 = cache.clone()
+    conv_out = torch.empty((M, C), device=cuda)
+    out = ops.gemv_w4a16(x, tw, sgrp, group, N, conv=(cw, cb, c0, cache2, True, conv_out))
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref_out)
+    assert torch.equal(conv_out, ref_conv)
+    assert torch.equal(cache2, ref_cache)
+
+
 @pytest.mark.parametrize("M,D", [(5, 256), (64, 4096), (3, 2560)])
 def test_rmsnorm_quant(cuda, M, D):
     ops = _ops()
