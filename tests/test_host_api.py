@@ -222,3 +222,74 @@ def test_quant_archive_roundtrip(tmp_path, profile, dims, emb_bits):
             fa, fb = getattr(x, f), getattr(y, f)
             assert (fa is None) == (fb is None) and (fa is None or np.array_equal(np.asarray(fa), np.asarray(fb))), f
         assert (x.s_u, x.s_y, x.s_dt, x.hadamard, x.profile) == (y.s_u, y.s_y, y.s_dt, y.hadamard, y.profile)
+
+
+# ---------------------------------------------------------------- oracle-independent properties
+# The bit-exact comparisons above check the product against the numpy restatement.  These check
+# the product's host transforms against the MATH they must satisfy, so a shared misreading of
+# SPEC in both restatements would still fail here.
+
+def _as_oracle_weights(w):
+    from oracle import ssm_block as osb
+    fields = {f: getattr(w, f) for f in osb.SsmBlockWeights.__dataclass_fields__ if hasattr(w, f)}
+    fields["dims"] = osb.Dims(**vars(w.dims))
+    return osb.SsmBlockWeights(**fields)
+
+
+@pytest.mark.parametrize("dims", [TINY2, TINY1], ids=["mamba2", "mamba1"])
+def test_reorder_preserves_the_block_function(dims):
+    """reordering is a relabelling of the block's channels (and heads), so the
+    float block maps the same input to the same output and the final state is the permuted one
+    (permute_state)."""
+    from oracle import ssm_block as osb
+    d = Dims(*dims)
+    w = cli.gen_block(d, 5, 0)
+    nh, P = (1, d.d_inner) if d.variant == "mamba1" else (d.n_heads, d.head_dim)
+    r = np.random.default_rng(4)
+    cm = calibrate.sort_and_cluster(calibrate.CalibStats(np.exp(r.uniform(-3, 3, nh * P)).astype(np.float32), 1),
+                                    nh, P)
+    plan = reorder.build_reorder_plan(cm, d)
+    assert not np.array_equal(plan.pi, np.arange(d.d_inner))   # a real permutation
+    w2 = reorder.apply_reorder(w, plan)
+    u = r.standard_normal((24, d.d_model)).astype(np.float32)
+    y1, s1 = osb.block_forward_float(u, _as_oracle_weights(w))
+    y2, s2 = osb.block_forward_float(u, _as_oracle_weights(w2))
+    assert np.abs(y2 - y1).max() <= 1e-5 * np.abs(y1).max()
+    h1 = np.asarray(s1.h).reshape(nh, P, -1)
+    h2 = np.asarray(s2.h).reshape(nh, P, -1)
+    assert np.abs(reorder.permute_state(h1, plan) - h2).max() <= 1e-5 * np.abs(h1).max()
+    inv = plan.inverse()
+    assert np.array_equal(plan.pi[inv.pi], np.arange(d.d_inner))
+
+
+def test_hadamard_transforms_are_orthogonal_fusions():
+    """H_b H_b = b·I for the unnormalised butterflies, and the fused out_proj
+    W·H̃ᵀ applied to H̃ y reproduces W y (H̃ = I_q ⊗ H_b / sqrt(b), the block-diagonal transform
+    of LEDGER G9) — checked in float64 against the plain product, not against the oracle."""
+    r = np.random.default_rng(6)
+    for n, b in ((512, None), (5120, None), (384, 64)):
+        v = torch.as_tensor(r.standard_normal((3, n)).astype(np.float32))
+        bs = hadamard.block_size(n) if b is None else b
+        twice = hadamard.fwht_blocked(hadamard.fwht_blocked(v, b), b)
+        assert (twice - v * bs).abs().max() <= 1e-5 * (v * bs).abs().max()
+    w = r.standard_normal((48, 384)).astype(np.float32)
+    y = r.standard_normal((5, 384)).astype(np.float64)
+    wf = hadamard.fuse_hadamard_out_proj(w, 384, 1).numpy().astype(np.float64)
+    hy = hadamard.fwht_blocked(torch.as_tensor(y.astype(np.float32))).numpy().astype(np.float64) / np.sqrt(128)
+    assert np.abs(hy @ wf.T - y @ w.T.astype(np.float64)).max() <= 1e-4 * np.abs(y @ w.T).max()
+
+
+def test_weight_quantizers_round_trip_bounds():
+    """Eq. 1: every code is in range, and dequantised weights
+    are within half a step of the originals per scale group (per channel for W8, per 128-wide
+    group for W4); the largest |w| of each group maps to ±(2^(b-1) - 1)."""
+    r = np.random.default_rng(8)
+    w = (r.standard_normal((64, 512)) * np.exp(r.uniform(-3, 1, (64, 1)))).astype(np.float32)
+    for q, lo, hi in ((quantizer.quantize_weight_w8(w), -128, 127), (quantizer.quantize_weight_w4(w, 128), -8, 7)):
+        c = _np(q.payload).astype(np.float64)
+        s = _np(q.layout.expand(w.shape)).astype(np.float64)   # the scale of every element
+        assert c.min() >= lo and c.max() <= hi
+        assert np.all(np.abs(c * s - w) <= s / 2 * (1 + 1e-6))
+        # the group's largest |w| lands on the top code (max|w| / (2^(b-1) - 1) is the scale)
+        top = np.abs(c).reshape(64, -1, 128 if hi == 7 else 512).max(-1)
+        assert np.all(top == hi)
