@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __re
                                                               const float* __restrict__ bias,
                                                               const float* __restrict__ s_in,
                                                               const float* __restrict__ s_out, int T, int C,
-                                                              const int8_t* __restrict__ cache, int cache_in,
+                                                              int8_t* __restrict__ cache, int cache_in,
                                                               int8_t* __restrict__ out, int64_t ldo) {
   const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int b = blockIdx.z;
@@ -120,6 +120,22 @@ __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __re
       for (int k = 0; k < KC - 1; ++k) win[pr][k] = win[pr][k + 1];
       win[pr][KC - 1] = __fmul2_rn(q[pr], si[pr]);
     }
+  }
+  if (blockIdx.y == 0 && KC > 1) {
+    // the first segment owns the cache: only its threads read the old window (above, their own
+    // 4 channels), so they alone may overwrite it with the sequence's last KC-1 input codes
+    // (for T < KC-1 the kept old entries are read before any write)
+    uint32_t nv[KC > 1 ? KC - 1 : 1];
+#pragma unroll
+    for (int j = 0; j < KC - 1; ++j) {
+      const int t = T - (KC - 1) + j;
+      nv[j] = t >= 0 ? *reinterpret_cast<const uint32_t*>(x + ((int64_t)b * T + t) * ldx + c0)
+            : cache_in ? *reinterpret_cast<const uint32_t*>(cache + ((int64_t)b * (KC - 1) + (KC - 1 + t)) * C + c0)
+                       : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < KC - 1; ++j)
+      *reinterpret_cast<uint32_t*>(cache + ((int64_t)b * (KC - 1) + j) * C + c0) = nv[j];
   }
   const float2 RM = make_float2(12582912.0f, 12582912.0f), NRM = make_float2(-12582912.0f, -12582912.0f);
   for (int tb = t0; tb < t1; tb += 8) {
@@ -246,6 +262,7 @@ extern "C" int sq_conv1d_int8(const int8_t* x, int64_t ldx, const float* w, cons
   if (Kc == 4 && C % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0 && ((uintptr_t)x & 3) == 0 && ((uintptr_t)out & 3) == 0) {
     dim3 g((C / 4 + 127) / 128, (T + kSeg4 - 1) / kSeg4, B);
     conv1d_prefill4_kernel<4><<<g, 128, 0, st>>>(x, ldx, w, bias, s_in, s_out, T, C, cache, cache_in, out, ldo);
+    return check_launch("sq_conv1d_int8");   // the cache window is written by the first segment
   } else {
     dim3 g((C + 127) / 128, (T + kSeg - 1) / kSeg, B);
     launch_k(PDL_SMALL, conv1d_prefill_kernel<int8_t, int8_t, true>, g, dim3(128), 0, st, x, ldx, w, bias, s_in, s_out, B, T, C, Kc, cache,

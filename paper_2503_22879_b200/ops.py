@@ -305,7 +305,9 @@ def conv1d_int8(x, w, bias, s_in, s_out, B, T, cache, cache_in=False, out=None):
     _rows(out, B * T, "out")
     _check(lib().sq_conv1d_int8(x.data_ptr(), _ld(x), w.data_ptr(), bias.data_ptr(), s_in.data_ptr(),
                                 s_out.data_ptr(), B, T, C_, Kc, cache.data_ptr(), int(bool(cache_in)),
-                                out.data_ptr(), _ld(out), _stream()), 1 + (Kc > 1))
+                                out.data_ptr(), _ld(out), _stream()),
+           1 if (Kc == 4 and C_ % 4 == 0 and _ld(x) % 4 == 0 and _ld(out) % 4 == 0 and x.data_ptr() % 4 == 0
+                 and out.data_ptr() % 4 == 0) else 1 + (Kc > 1))   # 4-channel kernel writes the cache itself
     return out
 
 

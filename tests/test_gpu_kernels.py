@@ -214,10 +214,11 @@ def test_gate_norm_had_quant(cuda, M, D, had):
     assert mx <= 1 and frac < 1e-3
 
 
-def test_conv1d_prefill_and_update(cuda):
+@pytest.mark.parametrize("T", [150, 2])   # T < K-1: the new cache window keeps old entries
+def test_conv1d_prefill_and_update(cuda, T):
     ops = _ops()
-    r = _rng(6)
-    B, T, C, K = 3, 150, 384, 4
+    r = _rng(6, T)
+    B, C, K = 3, 384, 4
     x = r.integers(-128, 128, (B * T, C)).astype(np.int8)
     w = (r.standard_normal((C, K)) * 0.3).astype(np.float32)
     b = (r.standard_normal(C) * 0.05).astype(np.float32)
