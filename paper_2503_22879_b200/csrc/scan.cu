@@ -353,75 +353,88 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // chunk with the y output; the last chunk requantises the final state.  MODE 0 is the single pass.
 // The carried start state is the sequential one up to f32 rounding (tolerance-compared, like the
 // oracle's chunked SSD).
-template <int MODE, int CH>
-__global__ void __launch_bounds__(CH) mamba1_scan_chunk_kernel(sq_mamba1_params p, int B, int T, const int8_t* x,
-                                                               int64_t ldx, const int8_t* dt, int64_t lddt,
-                                                               const int8_t* BC, int64_t ldbc, const int8_t* z,
-                                                               int64_t ldz, int8_t* state, int state_in, float* y,
-                                                               int64_t ldy, float* ws, int tchunk) {
+template <int MODE, int CH, int TPC>
+__global__ void __launch_bounds__(CH * TPC) mamba1_scan_chunk_kernel(sq_mamba1_params p, int B, int T, const int8_t* x,
+                                                                     int64_t ldx, const int8_t* dt, int64_t lddt,
+                                                                     const int8_t* BC, int64_t ldbc, const int8_t* z,
+                                                                     int64_t ldz, int8_t* state, int state_in, float* y,
+                                                                     int64_t ldy, float* ws, int tchunk) {
   constexpr int N = 16;
+  constexpr int NT = CH * TPC;    // threads: TPC per channel
+  constexpr int KP = 8 / TPC;     // f32x2 state pairs per thread (pairs hf*KP .. hf*KP+KP-1)
   __shared__ __align__(16) int8_t raw[2][M1_TC][3 * CH + 32];
   __shared__ __align__(16) float bcf[2][M1_TC][32];   // B̂ | Ĉ (f32, m1_perm order)
   const int tid = threadIdx.x;
-  const int c0 = blockIdx.x * CH, c = c0 + tid;
+  const int cl = tid / TPC, hf = tid % TPC;   // channel within the CTA, state half
+  const int c0 = blockIdx.x * CH, c = c0 + cl;
   const int b = blockIdx.y;
   const int tc = blockIdx.z, nz = gridDim.z;
   pdl_trigger();
   if (MODE == 1 && tc == nz - 1) return;   // the last chunk's summary is never read
-  float2 A2[8];
+  float2 A2[KP];
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    A2[k] = make_float2(p.A[(int64_t)c * N + m1_perm(2 * k)] * 1.4426950408889634f,
-                        p.A[(int64_t)c * N + m1_perm(2 * k + 1)] * 1.4426950408889634f);
+  for (int k = 0; k < KP; ++k)
+    A2[k] = make_float2(p.A[(int64_t)c * N + m1_perm(2 * (hf * KP + k))] * 1.4426950408889634f,
+                        p.A[(int64_t)c * N + m1_perm(2 * (hf * KP + k) + 1)] * 1.4426950408889634f);
   const float sh = p.s_h[c], Dc = p.D[c], sx = p.s_x[c], dtb = p.dt_bias[c];
   const float s_dt = p.s_dt, s_z = p.s_z, s_B = p.s_B, s_C = p.s_C;
   pdl_wait();   // inputs come from the previous grid
   int8_t* st = state + ((int64_t)b * p.d_inner + c) * N;
   const int t0 = tc * tchunk, t1 = min(T, t0 + tchunk);   // this CTA's time range
   // per-chunk summaries [2][nz][B][d_inner][N] (natural state order): end state (from 0; chunk 0
-  // from the initial state) and decay product
+  // from the initial state) and decay product.  The thread's pairs hold states hf*16/TPC .. +16/TPC.
+  constexpr int SPT = N / TPC;    // states per thread (a contiguous natural range)
   const int64_t cell = ((int64_t)b * p.d_inner + c) * N, zst = (int64_t)B * p.d_inner * N;
-  float2 H[8], P2[8];
+  const int sb = hf * SPT;        // first natural state of this thread
+  float2 H[KP], P2[KP];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < KP; ++k) {
+    const int kg = hf * KP + k;
     P2[k] = make_float2(1.f, 1.f);
     H[k] = (state_in && (MODE == 0 || tc == 0))
-               ? make_float2(__fmul_rn((float)st[m1_perm(2 * k)], sh), __fmul_rn((float)st[m1_perm(2 * k + 1)], sh))
+               ? make_float2(__fmul_rn((float)st[m1_perm(2 * kg)], sh), __fmul_rn((float)st[m1_perm(2 * kg + 1)], sh))
                : make_float2(0.f, 0.f);
   }
   if (MODE == 2 && tc > 0) {   // carry: fold the chunks before this one (16-B loads, 4 chunks in flight)
-    float e[N];
-    auto ld16 = [&](const float* src, float (&d)[N]) {
+    float e[SPT];
+    auto ld = [&](const float* src, float (&d)[SPT]) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 v = *reinterpret_cast<const float4*>(src + 4 * i);
+      for (int i = 0; i < SPT / 4; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(src + sb + 4 * i);
         d[4 * i] = v.x; d[4 * i + 1] = v.y; d[4 * i + 2] = v.z; d[4 * i + 3] = v.w;
       }
     };
-    ld16(ws + cell, e);
+    ld(ws + cell, e);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) H[k] = make_float2(e[m1_perm(2 * k)], e[m1_perm(2 * k + 1)]);
+    for (int k = 0; k < KP; ++k) {
+      const int kg = hf * KP + k;
+      H[k] = make_float2(e[m1_perm(2 * kg) - sb], e[m1_perm(2 * kg + 1) - sb]);
+    }
 #pragma unroll 4
     for (int j = 1; j < tc; ++j) {
-      float q[N];
-      ld16(ws + j * zst + cell, e);
-      ld16(ws + (nz + j) * zst + cell, q);
+      float q[SPT];
+      ld(ws + j * zst + cell, e);
+      ld(ws + (nz + j) * zst + cell, q);
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        H[k] = __fadd2_rn(__fmul2_rn(make_float2(q[m1_perm(2 * k)], q[m1_perm(2 * k + 1)]), H[k]),
-                          make_float2(e[m1_perm(2 * k)], e[m1_perm(2 * k + 1)]));
+      for (int k = 0; k < KP; ++k) {
+        const int kg = hf * KP + k;
+        H[k] = __fadd2_rn(__fmul2_rn(make_float2(q[m1_perm(2 * kg) - sb], q[m1_perm(2 * kg + 1) - sb]), H[k]),
+                          make_float2(e[m1_perm(2 * kg) - sb], e[m1_perm(2 * kg + 1) - sb]));
+      }
     }
   }
   const int nch = (t1 - t0 + M1_TC - 1) / M1_TC;
-  auto issue = [&](int ch) {   // x | dt | z: one 16-B piece of each per thread; B̂Ĉ: 32 pieces
-    constexpr int PPR = CH / 16;   // pieces per token row
-    const int row = tid / PPR, off = (tid % PPR) * 16;
-    const int t = t0 + ch * M1_TC + row;
-    if (t < t1) {
-      const int64_t tok = (int64_t)b * T + t;
-      cp_async16(&raw[ch & 1][row][off], x + tok * ldx + c0 + off);
-      cp_async16(&raw[ch & 1][row][CH + off], dt + tok * lddt + c0 + off);
-      cp_async16(&raw[ch & 1][row][2 * CH + off], z + tok * ldz + c0 + off);
+  auto issue = [&](int ch) {   // x | dt | z codes (CH bytes per token row each) and the B̂Ĉ row, 16-B pieces
+    constexpr int PPR = CH / 16;   // pieces per token row and kind
+    for (int i = tid; i < 3 * M1_TC * PPR; i += NT) {
+      const int kind = i / (M1_TC * PPR), j = i % (M1_TC * PPR);
+      const int row = j / PPR, off = (j % PPR) * 16;
+      const int t = t0 + ch * M1_TC + row;
+      if (t < t1) {
+        const int64_t tok = (int64_t)b * T + t;
+        const int8_t* src = kind == 0 ? x + tok * ldx : kind == 1 ? dt + tok * lddt : z + tok * ldz;
+        cp_async16(&raw[ch & 1][row][kind * CH + off], src + c0 + off);
+      }
     }
     if (tid < 2 * M1_TC) {
       const int rb = tid >> 1, hb = (tid & 1) * 16;
@@ -430,7 +443,7 @@ __global__ void __launch_bounds__(CH) mamba1_scan_chunk_kernel(sq_mamba1_params 
     }
     cp_async_commit();
   };
-  static_assert(M1_TC * (CH / 16) == CH && 2 * M1_TC <= CH, "one x|dt|z piece per thread per chunk");
+  static_assert(2 * M1_TC <= NT && CH % 16 == 0, "B|C pieces: one per thread of the first 32");
   issue(0);
   for (int ch = 0; ch < nch; ++ch) {
     const int tn = min(M1_TC, t1 - t0 - ch * M1_TC);
@@ -439,7 +452,7 @@ __global__ void __launch_bounds__(CH) mamba1_scan_chunk_kernel(sq_mamba1_params 
     if (ch + 1 < nch) issue(ch + 1);
     const int8_t(*r)[3 * CH + 32] = raw[ch & 1];
     float(*bf)[32] = bcf[ch & 1];
-    for (int i = tid; i < tn * 32; i += CH) {
+    for (int i = tid; i < tn * 32; i += NT) {
       const int row = i >> 5, q = i & 31;
       const int src = q < N ? m1_perm(q) : N + m1_perm(q - N);
       bf[row][q] = __fmul_rn(s8f(r[row][3 * CH + src]), q < N ? s_B : s_C);
@@ -448,58 +461,77 @@ __global__ void __launch_bounds__(CH) mamba1_scan_chunk_kernel(sq_mamba1_params 
     float* yrow = y + ((int64_t)b * T + t0 + ch * M1_TC) * ldy + c;
 #pragma unroll M1_UNROLL
     for (int tt = 0; tt < tn; ++tt) {
-      const float delta = softplus_approx(__fadd_rn(__fmul_rn(s8f(r[tt][CH + tid]), s_dt), dtb));
-      const float xv = __fmul_rn(s8f(r[tt][tid]), sx);
+      const float delta = softplus_approx(__fadd_rn(__fmul_rn(s8f(r[tt][CH + cl]), s_dt), dtb));
+      const float xv = __fmul_rn(s8f(r[tt][cl]), sx);
       const float dx = __fmul_rn(delta, xv);
       const float2 dl2 = make_float2(delta, delta), dx2 = make_float2(dx, dx);
       const float4* b4 = reinterpret_cast<const float4*>(bf[tt]);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < KP; ++k) {
+        const int kg = hf * KP + k;
         const float2 t = __fmul2_rn(dl2, A2[k]);
         const float2 av = make_float2(ex2_approx(t.x), ex2_approx(t.y));
-        const float4 bq = b4[k >> 1];
-        const float2 bv = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
+        const float4 bq = b4[kg >> 1];
+        const float2 bv = (kg & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
         H[k] = __fadd2_rn(__fmul2_rn(av, H[k]), __fmul2_rn(dx2, bv));
         if constexpr (MODE == 1) P2[k] = __fmul2_rn(P2[k], av);
       }
       if constexpr (MODE != 1) {
-        const float gz = silu_approx(__fmul_rn(s8f(r[tt][2 * CH + tid]), s_z));
-        const float4 cq0 = b4[4], cq1 = b4[5], cq2 = b4[6], cq3 = b4[7];
-        float2 a01 = __fmul2_rn(H[0], make_float2(cq0.x, cq0.y));
-        a01 = __ffma2_rn(H[1], make_float2(cq0.z, cq0.w), a01);
-        a01 = __ffma2_rn(H[2], make_float2(cq1.x, cq1.y), a01);
-        a01 = __ffma2_rn(H[3], make_float2(cq1.z, cq1.w), a01);
-        float2 a23 = __fmul2_rn(H[4], make_float2(cq2.x, cq2.y));
-        a23 = __ffma2_rn(H[5], make_float2(cq2.z, cq2.w), a23);
-        a23 = __ffma2_rn(H[6], make_float2(cq3.x, cq3.y), a23);
-        a23 = __ffma2_rn(H[7], make_float2(cq3.z, cq3.w), a23);
-        const float acc = __fadd_rn(__fadd_rn(a01.x, a01.y), __fadd_rn(a23.x, a23.y));
-        yrow[(int64_t)tt * ldy] = __fmul_rn(__fadd_rn(acc, __fmul_rn(Dc, xv)), gz);
+        // quarter sums: pairs 4m .. 4m+3 form the f32x2 chain of quarters (2m, 2m+1)
+        float part[2 / TPC];
+#pragma unroll
+        for (int m = 0; m < 2 / TPC; ++m) {
+          const int kg0 = hf * KP + 4 * m;
+          const float4 cqa = b4[4 + (kg0 >> 1)], cqb = b4[5 + (kg0 >> 1)];
+          float2 aq = __fmul2_rn(H[4 * m], make_float2(cqa.x, cqa.y));
+          aq = __ffma2_rn(H[4 * m + 1], make_float2(cqa.z, cqa.w), aq);
+          aq = __ffma2_rn(H[4 * m + 2], make_float2(cqb.x, cqb.y), aq);
+          aq = __ffma2_rn(H[4 * m + 3], make_float2(cqb.z, cqb.w), aq);
+          part[m] = __fadd_rn(aq.x, aq.y);
+        }
+        float acc;
+        if constexpr (TPC == 1) {
+          acc = __fadd_rn(part[0], part[1]);
+        } else {   // (q0 + q1) from the even lane, (q2 + q3) from the odd lane, added in that order
+          const float other = __shfl_xor_sync(0xffffffffu, part[0], 1);
+          acc = __fadd_rn(hf == 0 ? part[0] : other, hf == 0 ? other : part[0]);
+        }
+        if (hf == 0) {
+          const float gz = silu_approx(__fmul_rn(s8f(r[tt][2 * CH + cl]), s_z));
+          yrow[(int64_t)tt * ldy] = __fmul_rn(__fadd_rn(acc, __fmul_rn(Dc, xv)), gz);
+        }
       }
     }
   }
   if constexpr (MODE == 1) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      ws[tc * zst + cell + m1_perm(2 * k)] = H[k].x;
-      ws[tc * zst + cell + m1_perm(2 * k + 1)] = H[k].y;
-      ws[(nz + tc) * zst + cell + m1_perm(2 * k)] = P2[k].x;
-      ws[(nz + tc) * zst + cell + m1_perm(2 * k + 1)] = P2[k].y;
+    for (int k = 0; k < KP; ++k) {
+      const int kg = hf * KP + k;
+      ws[tc * zst + cell + m1_perm(2 * kg)] = H[k].x;
+      ws[tc * zst + cell + m1_perm(2 * kg + 1)] = H[k].y;
+      ws[(nz + tc) * zst + cell + m1_perm(2 * kg)] = P2[k].x;
+      ws[(nz + tc) * zst + cell + m1_perm(2 * kg + 1)] = P2[k].y;
     }
   } else if (MODE == 0 || tc == nz - 1) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      st[m1_perm(2 * k)] = quant8(H[k].x, sh);
-      st[m1_perm(2 * k + 1)] = quant8(H[k].y, sh);
+    for (int k = 0; k < KP; ++k) {
+      const int kg = hf * KP + k;
+      st[m1_perm(2 * kg)] = quant8(H[k].x, sh);
+      st[m1_perm(2 * kg + 1)] = quant8(H[k].y, sh);
     }
   }
 }
 
 // time chunks of the two-pass form: up to 16, chunks >= 32 tokens
+#ifndef SQ_M1_TPC
+#define SQ_M1_TPC 1
+#endif
+constexpr int M1_TPC = SQ_M1_TPC;   // threads per channel of the chunked scan
 static int m1_ch(int d_inner) {
 #ifdef SQ_M1_PROBE_CH   // profiling builds only
   if (d_inner % SQ_M1_PROBE_CH == 0) return SQ_M1_PROBE_CH;
 #endif
+  if (M1_TPC == 2) return d_inner % 64 == 0 ? 64 : 32;
   return d_inner % 128 == 0 ? 128 : d_inner % 64 == 0 ? 64 : 32;
 }
 static int m1_time_chunks(int d_inner, int B, int T) {
@@ -876,7 +908,8 @@ extern "C" int sq_selective_scan_int8(const sq_mamba1_params* p, int B, int T, c
     SQ_REQUIRE(grid.z == 1 || (reinterpret_cast<uintptr_t>(ws) & 15) == 0, SQ_ERR_LAYOUT,
                "sq_selective_scan_int8: ws alignment");
 #define SQ_M1_LAUNCH(MODE, C)                                                                                     \
-  launch_k(PDL_SMALL8, mamba1_scan_chunk_kernel<MODE, C>, grid, dim3(C), 0, st, *p, B, T, x, ldx, dt, lddt, BC, ldbc, \
+  launch_k(PDL_SMALL8, mamba1_scan_chunk_kernel<MODE, C, M1_TPC>, grid, dim3(C * M1_TPC), 0, st, *p, B, T, x, ldx, dt, \
+           lddt, BC, ldbc, \
            z, ldz, state, state_in, y, ldy, wsf, tchunk)
 #define SQ_M1_PASSES(C)            \
   if (grid.z == 1) {               \
