@@ -190,11 +190,16 @@ def calibrate_site_scale(stats: CalibStats, bits: int = 8, clip_percentile=None)
 SITES = ("u", "z", "x_in", "B_in", "C_in", "dt", "x", "B", "C", "h", "dt_low", "y", "r", "y_had", "head_in")
 
 
-def collect_stats(model, tokens, sites=None, device="cuda"):
+ROW_SITES = ("u", "x", "dt_low", "r")   # projection inputs: in_proj, x_proj, dt_proj, out_proj
+
+
+def collect_stats(model, tokens, sites=None, device="cuda", keep_rows: int = 0):
     """per layer, per calibration site, channel maxima over all samples.
     Runs the float model (``float_path.float_forward``) on ``device``; returns one dict of
     CalibStats per block plus the head input site at index -1.  ``sites``
-    restricts the taps kept (names in ``SITES``); None keeps every site."""
+    restricts the taps kept (names in ``SITES``); None keeps every site.  ``keep_rows`` > 0 also
+    keeps the first ``keep_rows`` activation rows of every projection input (``ROW_SITES``, on
+    ``device``) under ``stats[l]["_rows"]``: the calibration inputs of GPTQ."""
     if sites is not None:
         unknown = set(sites) - set(SITES)
         if unknown:
@@ -209,12 +214,21 @@ def collect_stats(model, tokens, sites=None, device="cuda"):
         taps = []
         float_forward(model, tokens[s], taps, device=device)
         for l in range(L + 1):
+            if keep_rows > 0 and l < L:
+                rows = stats[l].setdefault("_rows", {})
+                for k in ROW_SITES:
+                    if k in taps[l]:
+                        have = rows.get(k)
+                        need = keep_rows - (0 if have is None else have.shape[0])
+                        if need > 0:
+                            v = taps[l][k][:need].detach()
+                            rows[k] = v if have is None else torch.cat([have, v])
             for k, v in taps[l].items():
                 if sites is not None and k not in sites:
                     continue
                 ch = tuple(v.shape) if k == "h" else tuple(v.shape[1:])
                 st = stats_of(v[None] if k == "h" else v, ch)
                 stats[l][k] = st if k not in stats[l] else stats[l][k].merge(st)
-    if sites is None and any(not s for s in stats):
+    if sites is None and any(not [k for k in s if k != "_rows"] for s in stats):
         raise ShapeError("calibration produced no statistics")
     return stats

@@ -21,12 +21,13 @@ import sys
 from dataclasses import dataclass, field
 
 import numpy as np
+import torch
 
 from . import calibrate as cal
 from . import hadamard as had
 from . import reorder as ro
 from .errors import PipelineError, SsmQuantError
-from .quantizer import compute_scale, quantize_weight_w4, quantize_weight_w4a8, quantize_weight_w8
+from .quantizer import compute_scale, gptq_quantize_weight, quantize_weight_w4, quantize_weight_w4a8, quantize_weight_w8
 from .ssm_block import Dims, QBlock, QLinear, SsmBlockWeights
 from .tensor import make_rng
 
@@ -90,7 +91,9 @@ def _gemm_group(k: int) -> int:
     return 128 if k % 128 == 0 else (32 if k % 32 == 0 else k)
 
 
-def make_qlinear(w, kind: str, group: int = 128) -> QLinear:
+def make_qlinear(w, kind: str, group: int = 128, calib=None) -> QLinear:
+    """``calib`` (rows of this projection's input, in the weight's column basis) switches the
+    4-bit kinds from round-to-nearest to GPTQ (the Table 7 "GPTQ" toggle)."""
     w = np.asarray(w, np.float32)
     group = min(group, w.shape[1])
     n = lambda t: t.cpu().numpy()   # noqa: E731
@@ -98,7 +101,10 @@ def make_qlinear(w, kind: str, group: int = 128) -> QLinear:
         q = quantize_weight_w8(w)
         return QLinear("w8", n(q.payload), s_ch=n(q.extra["s_ch"]), group=w.shape[1])
     if kind in ("w4a8", "w4a16"):
-        q = quantize_weight_w4a8(w, group) if kind == "w4a8" else quantize_weight_w4(w, group)
+        if calib is not None:
+            q = gptq_quantize_weight(w, calib, 4, group, device=getattr(calib, "device", None))
+        else:
+            q = quantize_weight_w4a8(w, group) if kind == "w4a8" else quantize_weight_w4(w, group)
         return QLinear(kind, n(q.payload), s_group=n(q.extra["s_group"]), group=group)
     raise PipelineError(f"unknown weight kind {kind}")
 
@@ -118,8 +124,11 @@ class QuantModel:
     extra: dict = field(default_factory=dict)
 
 
-def quantize_block(blk: SsmBlockWeights, st: dict, profile: str, m=4, n=4, hadamard=True, reorder=True, seed=0):
-    """SPEC.md:591 stages for one block from its calibration stats."""
+def quantize_block(blk: SsmBlockWeights, st: dict, profile: str, m=4, n=4, hadamard=True, reorder=True, seed=0,
+                   gptq=False):
+    """SPEC.md:591 stages for one block from its calibration stats.  ``gptq`` (4-bit profiles):
+    the projections are rounded by GPTQ on the calibration rows kept by collect_stats(keep_rows),
+    each mapped into its weight's column basis (reordered, Hadamard-rotated, cluster-scaled)."""
     d = blk.dims
     di = d.d_inner
     nh, P = (d.n_heads, d.head_dim) if d.variant == "mamba2" else (1, d.d_inner)
@@ -133,13 +142,21 @@ def quantize_block(blk: SsmBlockWeights, st: dict, profile: str, m=4, n=4, hadam
         cells = c0
     kind = {"W8A8": "w8", "W4A8": "w4a8", "W4A16": "w4a16"}[profile]
     extra = {"cmap": cmap, "plan": plan}
+    rows = st.get("_rows") if (gptq and kind != "w8") else None
+    if gptq and kind != "w8" and not rows:
+        raise PipelineError("gptq needs calibration rows: collect_stats(..., keep_rows=N)")
+    pi = plan.pi if reorder else np.arange(di)
+    cal_in = rows["u"].float() if rows else None                           # in_proj input
+    cal_dtl = rows["dt_low"].float() if rows and "dt_low" in rows else None   # Mamba1 dt_proj input
+    cal_r = rows["r"].float()[:, torch.as_tensor(pi, device=rows["r"].device)] if rows else None
+    cal_x = rows["x"].float()[:, torch.as_tensor(pi, device=rows["x"].device)] if rows and d.variant == "mamba1" else None
     if profile == "W4A16":
-        qb = QBlock(d, profile, make_qlinear(w.in_proj, kind, _gemm_group(d.d_model)),
-                    make_qlinear(w.out_proj, kind, _gemm_group(di)), w.conv_weight, w.conv_bias, w.a_log,
+        qb = QBlock(d, profile, make_qlinear(w.in_proj, kind, _gemm_group(d.d_model), cal_in),
+                    make_qlinear(w.out_proj, kind, _gemm_group(di), cal_r), w.conv_weight, w.conv_bias, w.a_log,
                     w.d_param, w.dt_bias, w.norm_weight, w.head_group, extra=extra)
         if d.variant == "mamba1":
-            qb.x_proj = make_qlinear(w.x_proj, kind, _gemm_group(di))
-            qb.dt_proj = make_qlinear(w.dt_proj, kind, _gemm_group(d.dt_rank))
+            qb.x_proj = make_qlinear(w.x_proj, kind, _gemm_group(di), cal_x)
+            qb.dt_proj = make_qlinear(w.dt_proj, kind, _gemm_group(d.dt_rank), cal_dtl)
         return qb
     s_u = cal.calibrate_site_scale(st["u"])
     s_z = compute_scale(st["z"].channel_max, 8)
@@ -166,31 +183,37 @@ def quantize_block(blk: SsmBlockWeights, st: dict, profile: str, m=4, n=4, hadam
         conv_out = x_cell_scale
         ssg = cal.build_state_group_scales(st["B"], st["C"], 1, d.d_state, st["h"], cmap)
     state_scale = ssg.scales_state.reshape(-1)[cells].astype(np.float32)
-    qb = QBlock(d, profile, make_qlinear(w.in_proj, kind, _gemm_group(d.d_model)),
-                make_qlinear(out_w, kind, _gemm_group(di)), w.conv_weight, w.conv_bias, w.a_log, w.d_param,
+    if cal_r is not None and hadamard:   # out_proj sees the unnormalised blocked FWHT of r
+        cal_r = had.fwht_blocked(cal_r, d.had_block)
+    qb = QBlock(d, profile, make_qlinear(w.in_proj, kind, _gemm_group(d.d_model), cal_in),
+                make_qlinear(out_w, kind, _gemm_group(di), cal_r), w.conv_weight, w.conv_bias, w.a_log, w.d_param,
                 w.dt_bias, w.norm_weight, w.head_group, s_u=s_u, in_out_scale=in_out, conv_in_scale=conv_in,
                 conv_out_scale=conv_out, state_scale=state_scale, s_y=s_y, hadamard=hadamard,
                 extra=dict(extra, ssg=ssg))
     if d.variant == "mamba1":
         R, N = d.dt_rank, d.d_state
-        qb.x_proj = make_qlinear((w.x_proj * x_cell_scale[None, :]).astype(np.float32), kind, _gemm_group(di))
+        if cal_x is not None:   # x_proj's GEMM input is x / (clustered x scale)
+            cal_x = cal_x / torch.as_tensor(x_cell_scale, device=cal_x.device)[None, :]
+        qb.x_proj = make_qlinear((w.x_proj * x_cell_scale[None, :]).astype(np.float32), kind, _gemm_group(di), cal_x)
         s_dtl = compute_scale(st["dt_low"].channel_max, 8)
         qb.xproj_out_scale = np.concatenate([np.full(R, s_dtl), np.full(N, compute_scale(st["B"].channel_max, 8)),
                                              np.full(N, compute_scale(st["C"].channel_max, 8))]).astype(np.float32)
-        qb.dt_proj = make_qlinear(w.dt_proj, kind, _gemm_group(R))
+        qb.dt_proj = make_qlinear(w.dt_proj, kind, _gemm_group(R), cal_dtl)
         qb.s_dt = compute_scale(st["dt"].channel_max, 8)
     return qb
 
 
 def cmd_quantize(model: FloatModel, tokens, profiles, m=4, n=4, hadamard=True, reorder=True, seed=0,
-                 head_bits=4, emb_bits=8, device="cuda", stats=None) -> QuantModel:
-    """SPEC.md:588-596 over a whole model (``profiles``: one per block or a single name)."""
+                 head_bits=4, emb_bits=8, device="cuda", stats=None, gptq=False, gptq_rows=512) -> QuantModel:
+    """SPEC.md:588-596 over a whole model (``profiles``: one per block or a single name).
+    ``gptq``: 4-bit projections by GPTQ on ``gptq_rows`` calibration rows per projection."""
     if isinstance(profiles, str):
         profiles = [profiles] * len(model.blocks)
     if len(profiles) != len(model.blocks):
         raise PipelineError("one profile per block")
-    stats = stats if stats is not None else cal.collect_stats(model, tokens, device=device)
-    blocks = [quantize_block(b, stats[l], profiles[l], m, n, hadamard, reorder, seed)
+    stats = stats if stats is not None else cal.collect_stats(model, tokens, device=device,
+                                                               keep_rows=gptq_rows if gptq else 0)
+    blocks = [quantize_block(b, stats[l], profiles[l], m, n, hadamard, reorder, seed, gptq)
               for l, b in enumerate(model.blocks)]
     emb = np.asarray(model.embedding, np.float32)
     es = np.array([compute_scale(emb[v], emb_bits) for v in range(emb.shape[0])], np.float32)
@@ -219,6 +242,7 @@ def main(argv=None) -> int:
     q.add_argument("--seq-len", type=int, default=64)
     q.add_argument("--no-hadamard", action="store_true")
     q.add_argument("--no-reorder", action="store_true")
+    q.add_argument("--gptq", action="store_true", help="GPTQ for the 4-bit projections (SPEC.md:146)")
     q.add_argument("--out", required=True)
     i = sub.add_parser("inspect")
     i.add_argument("archive")
@@ -235,7 +259,8 @@ def main(argv=None) -> int:
             toks = calib_tokens(fm.embedding.shape[0], a.samples, a.seq_len)
             import torch
             dev = "cuda" if torch.cuda.is_available() else "cpu"   # offline calibration forward
-            qm = cmd_quantize(fm, toks, a.profile, hadamard=not a.no_hadamard, reorder=not a.no_reorder, device=dev)
+            qm = cmd_quantize(fm, toks, a.profile, hadamard=not a.no_hadamard, reorder=not a.no_reorder, device=dev,
+                              gptq=a.gptq)
             archive.write_quant_model(qm, a.out)
         else:
             print(json.dumps(archive.inspect(a.archive), indent=1))

@@ -24,7 +24,7 @@ import torch
 from .errors import LayoutError, ShapeError
 
 __all__ = ["ScaleLayout", "QTensor", "compute_scale", "quantize", "dequantize", "fuse_scales",
-           "quantize_weight_w8", "quantize_weight_w4", "quantize_weight_w4a8", "qrange"]
+           "quantize_weight_w8", "quantize_weight_w4", "quantize_weight_w4a8", "gptq_quantize_weight", "qrange"]
 
 
 def qrange(bits: int):
@@ -164,3 +164,81 @@ def quantize_weight_w4a8(w, group: int = 128) -> QTensor:
     """W4A8 weights: SPEC PerGroup 4-bit with float group scales, the
     W4A16 format; only the activation precision differs (LEDGER G11)."""
     return quantize_weight_w4(w, group)
+
+
+def gptq_quantize_weight(w, calib_inputs, bits: int = 4, group_size: int = 128, damp_ratio: float = 0.01,
+                         device=None, block: int | None = None) -> QTensor:
+    """SPEC.md:146-154 (GPTQ, Frantar et al.; PAPER.md Appendix "Implementation"): quantize the
+    columns left to right, each group's scales recomputed per Eq. 1 over the group's CURRENT
+    (error-compensated) weights, and every column's rounding error propagated to the columns on
+    its right through the inverse Hessian H = 2·XᵀX + damp·I, damp = damp_ratio·mean(diag H).
+
+    Runs on the GPU (``device``, default cuda when available): H and its inverse Cholesky factor
+    in float64 (torch.linalg), the column sweep in float32 in blocks of ``block`` columns (default:
+    the group size) whose accumulated errors update the remaining columns with one GEMM (the
+    "lazy batch" form of the GPTQ paper).  A Hessian that stays singular after damping falls back
+    to round-to-nearest (reported as a RuntimeWarning).  Returns the same QTensor
+    layout as quantize_weight_w4 (bits 4) / PerGroup 8-bit (bits 8): codes int8 [out × in],
+    scales [out × in/group]."""
+    import warnings
+
+    if bits not in (4, 8):
+        raise ValueError("bits must be 4 or 8")
+    dev = torch.device(device) if device is not None else (
+        torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu"))
+    W = _f32(w).to(dev).clone()
+    X = _f32(calib_inputs).to(dev)
+    if W.dim() != 2 or X.dim() != 2 or X.shape[1] != W.shape[1] or X.shape[0] < 1:
+        raise ShapeError("gptq: w [out x in], calib_inputs [samples x in] with samples >= 1")
+    n_out, n_in = W.shape
+    g = min(group_size, n_in)
+    if n_in % g:
+        raise ShapeError("gptq: group_size must divide in")
+    qmax = float(qrange(bits)[1])
+    lo, hi = qrange(bits)
+    H = 2.0 * (X.double().T @ X.double())
+    damp = damp_ratio * float(torch.diagonal(H).mean())
+    H += damp * torch.eye(n_in, dtype=torch.float64, device=dev)
+    try:
+        Hinv = torch.cholesky_inverse(torch.linalg.cholesky(H))
+        U = torch.linalg.cholesky(Hinv, upper=True).to(torch.float32)   # upper factor of H^-1
+    except RuntimeError:   # torch.linalg raises on a non-positive-definite matrix
+        warnings.warn("gptq: Hessian singular after damping; round-to-nearest for this layer", RuntimeWarning)
+        return quantize_weight_w4(W, g) if bits == 4 else _rtn_per_group(W, g, bits)
+    B = block or g
+    codes = torch.empty((n_out, n_in), dtype=torch.int8, device=dev)
+    scales = torch.empty((n_out, n_in // g), dtype=torch.float32, device=dev)
+    for i0 in range(0, n_in, B):
+        i1 = min(i0 + B, n_in)
+        W1 = W[:, i0:i1].clone()
+        E1 = torch.zeros_like(W1)
+        U1 = U[i0:i1, i0:i1]
+        for i in range(i1 - i0):
+            col = i0 + i
+            if col % g == 0:   # Eq. 1 over the group's current weights (its columns past this block
+                # have received every earlier block's update; B is a multiple of g or g of B)
+                grp = torch.cat([W1[:, i:], W[:, i1:col + g]], dim=1)[:, :g] if col + g > i1 else W1[:, i:i + g]
+                m = grp.abs().amax(dim=1)
+                s = torch.where(m == 0, torch.ones_like(m), m / np.float32(qmax))
+                scales[:, col // g] = s
+            s = scales[:, col // g]
+            wc = W1[:, i]
+            q = torch.round(wc / s).clamp_(lo, hi)
+            codes[:, col] = q.to(torch.int8)
+            err = (wc - q * s) / U1[i, i]
+            if i + 1 < i1 - i0:
+                W1[:, i + 1:] -= err[:, None] * U1[i, i + 1:][None, :]
+            E1[:, i] = err
+        if i1 < n_in:
+            W[:, i1:] -= E1 @ U[i0:i1, i1:]
+    return QTensor((n_out, n_in), bits, codes, ScaleLayout("PerGroup", scales.reshape(-1), axis=1, group_size=g),
+                   extra={"s_group": scales, "group": g, "gptq": True})
+
+
+def _rtn_per_group(w: torch.Tensor, group: int, bits: int) -> QTensor:
+    n, k = w.shape
+    wg = w.reshape(n, k // group, group)
+    s = _group_absmax_scale(wg, bits)
+    codes = _codes(wg, s[:, :, None], bits).reshape(n, k)
+    return QTensor((n, k), bits, codes, ScaleLayout("PerGroup", s.reshape(-1), axis=1, group_size=group),
+                   extra={"s_group": s, "group": group})
