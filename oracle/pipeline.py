@@ -32,7 +32,7 @@ from oracle.quantizer import compute_scale, quantize_codes
 from oracle.ssm_block import Dims, SsmBlockWeights, block_forward_float, rmsnorm, zero_state
 from oracle.tensor_core import make_rng, matmul_fast
 
-T_IN, T_CONV_W, T_CONV_B, T_ALOG, T_DTB, T_NORM, T_OUT, T_XPROJ, T_DTPROJ, T_MULT = range(10)
+T_IN, T_CONV_W, T_CONV_B, T_ALOG, T_DTB, T_NORM, T_OUT, T_XPROJ, T_DTPROJ, T_MULT, T_BCG, T_NOUT = range(12)
 
 
 def _gemm_group(k: int) -> int:
@@ -45,6 +45,14 @@ def gen_block(d: Dims, seed: int, layer: int, n_layers: int = 1) -> SsmBlockWeig
     inp = (r(T_IN).standard_normal((d.in_proj_out, dm)) / np.sqrt(dm)).astype(np.float32)
     mult = np.exp(r(T_MULT).uniform(np.log(0.1), np.log(10.0), di)).astype(np.float32)
     inp[di:2 * di] *= mult[:, None]
+    if d.variant == "mamba2" and d.n_state_groups > 1:
+        # state groups of different magnitude (B rows of group g scaled by a factor of 0.01-10x, C rows by its inverse):
+        # what per-state-group B/C scales exploit (Fig. 3e-f; SPEC.md acceptance 8, 10)
+        gn = d.n_state_groups * d.d_state
+        gmul = np.exp(r(T_BCG).uniform(np.log(0.01), np.log(10.0), d.n_state_groups)).astype(np.float32)
+        gm = np.repeat(gmul, d.d_state)
+        inp[2 * di:2 * di + gn] *= gm[:, None]
+        inp[2 * di + gn:2 * di + 2 * gn] /= gm[:, None]   # C inversely: every group's C·h stays O(1)
     K = d.conv_kernel
     conv_w = (r(T_CONV_W).standard_normal((d.conv_dim, K)) * 0.5 / np.sqrt(K)).astype(np.float32)
     conv_b = (r(T_CONV_B).standard_normal(d.conv_dim) * 0.05).astype(np.float32)
@@ -58,6 +66,10 @@ def gen_block(d: Dims, seed: int, layer: int, n_layers: int = 1) -> SsmBlockWeig
                        * r(T_ALOG).uniform(0.5, 1.5, (di, 1))).astype(np.float32)
         dpar = np.ones(di, np.float32)
     norm = (1.0 + 0.1 * r(T_NORM).standard_normal(di)).astype(np.float32)
+    # a few outlier channels of the gated-norm output (the out_proj input): what the Hadamard
+    # rotation before the out_proj quantizer spreads out (§3.3; SPEC.md acceptance 10)
+    hot = r(T_NOUT).choice(di, max(1, di // 64), replace=False)
+    norm[hot] *= np.float32(100.0)
     out = (r(T_OUT).standard_normal((dm, di)) / np.sqrt(di) / np.sqrt(2 * n_layers)).astype(np.float32)
     xp = dtp = None
     if d.variant == "mamba1":

@@ -104,7 +104,8 @@ def zero_state(d: Dims) -> SsmState:
 
 def silu(v):
     v = np.asarray(v, np.float32)
-    return (v / (np.float32(1.0) + np.exp(-v))).astype(np.float32)
+    with np.errstate(over="ignore"):   # exp(-v) = inf for v << 0: silu -> -0, the right limit
+        return (v / (np.float32(1.0) + np.exp(-v))).astype(np.float32)
 
 
 def softplus(v):

@@ -16,6 +16,7 @@ embedding, W4A8 head).  The result feeds model.QuantizedMambaLM.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import sys
 from dataclasses import dataclass, field
@@ -31,7 +32,7 @@ from .quantizer import compute_scale, gptq_quantize_weight, quantize_weight_w4, 
 from .ssm_block import Dims, QBlock, QLinear, SsmBlockWeights
 from .tensor import make_rng
 
-T_IN, T_CONV_W, T_CONV_B, T_ALOG, T_DTB, T_NORM, T_OUT, T_XPROJ, T_DTPROJ, T_MULT = range(10)
+T_IN, T_CONV_W, T_CONV_B, T_ALOG, T_DTB, T_NORM, T_OUT, T_XPROJ, T_DTPROJ, T_MULT, T_BCG, T_NOUT = range(12)
 
 
 def gen_block(d: Dims, seed: int, layer: int, n_layers: int = 1) -> SsmBlockWeights:
@@ -40,6 +41,14 @@ def gen_block(d: Dims, seed: int, layer: int, n_layers: int = 1) -> SsmBlockWeig
     inp = (r(T_IN).standard_normal((d.in_proj_out, dm)) / np.sqrt(dm)).astype(np.float32)
     mult = np.exp(r(T_MULT).uniform(np.log(0.1), np.log(10.0), di)).astype(np.float32)
     inp[di:2 * di] *= mult[:, None]
+    if d.variant == "mamba2" and d.n_state_groups > 1:
+        # state groups of different magnitude (B rows of group g scaled by a factor of 0.01-10x, C rows by its inverse):
+        # what per-state-group B/C scales exploit (Fig. 3e-f; SPEC.md acceptance 8, 10)
+        gn = d.n_state_groups * d.d_state
+        gmul = np.exp(r(T_BCG).uniform(np.log(0.01), np.log(10.0), d.n_state_groups)).astype(np.float32)
+        gm = np.repeat(gmul, d.d_state)
+        inp[2 * di:2 * di + gn] *= gm[:, None]
+        inp[2 * di + gn:2 * di + 2 * gn] /= gm[:, None]   # C inversely: every group's C·h stays O(1)
     conv_w = (r(T_CONV_W).standard_normal((d.conv_dim, K)) * 0.5 / np.sqrt(K)).astype(np.float32)
     conv_b = (r(T_CONV_B).standard_normal(d.conv_dim) * 0.05).astype(np.float32)
     dtv = r(T_DTB).uniform(1e-3, 1e-1, d.n_heads if d.variant == "mamba2" else di)
@@ -52,6 +61,10 @@ def gen_block(d: Dims, seed: int, layer: int, n_layers: int = 1) -> SsmBlockWeig
                        * r(T_ALOG).uniform(0.5, 1.5, (di, 1))).astype(np.float32)
         dpar = np.ones(di, np.float32)
     norm = (1.0 + 0.1 * r(T_NORM).standard_normal(di)).astype(np.float32)
+    # a few outlier channels of the gated-norm output (the out_proj input): what the Hadamard
+    # rotation before the out_proj quantizer spreads out (§3.3; SPEC.md acceptance 10)
+    hot = r(T_NOUT).choice(di, max(1, di // 64), replace=False)
+    norm[hot] *= np.float32(100.0)
     out = (r(T_OUT).standard_normal((dm, di)) / np.sqrt(di) / np.sqrt(2 * n_layers)).astype(np.float32)
     xp = dtp = None
     if d.variant == "mamba1":
@@ -125,13 +138,18 @@ class QuantModel:
 
 
 def quantize_block(blk: SsmBlockWeights, st: dict, profile: str, m=4, n=4, hadamard=True, reorder=True, seed=0,
-                   gptq=False):
+                   gptq=False, persg=True, snc=True):
     """SPEC.md:591 stages for one block from its calibration stats.  ``gptq`` (4-bit profiles):
     the projections are rounded by GPTQ on the calibration rows kept by collect_stats(keep_rows),
-    each mapped into its weight's column basis (reordered, Hadamard-rotated, cluster-scaled)."""
+    each mapped into its weight's column basis (reordered, Hadamard-rotated, cluster-scaled).
+    Table 7 ablation toggles: ``persg=False`` gives B / C one per-tensor scale
+    each instead of per-state-group scales, ``snc=False`` one x scale (m = n = 1) instead of the
+    sort-and-cluster cells."""
     d = blk.dims
     di = d.d_inner
     nh, P = (d.n_heads, d.head_dim) if d.variant == "mamba2" else (1, d.d_inner)
+    if not snc:
+        m = n = 1
     cmap = cal.sort_and_cluster(st["x"], nh, P, m, n, seed)
     plan = ro.build_reorder_plan(cmap, d)
     w = ro.apply_reorder(blk, plan) if reorder else blk
@@ -172,6 +190,9 @@ def quantize_block(blk: SsmBlockWeights, st: dict, profile: str, m=4, n=4, hadam
         s_Bin, s_Cin = compute_scale(st["B_in"].channel_max, 8), compute_scale(st["C_in"].channel_max, 8)
         s_dt = compute_scale(st["dt"].channel_max, 8)
         ssg = cal.build_state_group_scales(st["B"], st["C"], d.n_state_groups, d.d_state, st["h"], cmap)
+        if not persg:   # one B and one C scale over every state group
+            ssg = dataclasses.replace(ssg, scales_B=np.full_like(ssg.scales_B, ssg.scales_B.max()),
+                                      scales_C=np.full_like(ssg.scales_C, ssg.scales_C.max()))
         in_out = np.concatenate([np.full(di, s_z), np.full(di, s_xin), np.full(gn, s_Bin), np.full(gn, s_Cin),
                                  np.full(d.n_heads, s_dt)]).astype(np.float32)
         conv_in = in_out[di:2 * di + 2 * gn].copy()

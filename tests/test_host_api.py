@@ -392,3 +392,40 @@ def _float_weight(blk, qb, name, d, profile):
         return (hadamard.fuse_hadamard_out_proj(w.out_proj, d.d_inner, 1, b).numpy() / np.float32(np.sqrt(b))).astype(
             np.float64)
     return np.asarray(getattr(w, name), np.float64)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_acceptance10_table7_ablation_monotone(seed):
+    """SPEC.md acceptance 10 / :617: the five Table 7 toggle rows of the W4A8 pipeline, in the
+    paper's order -- fail (no Hadamard) < PerG + Had < + GPTQ < + PerSG < + SnC -- give strictly
+    improving block-output SQNR on the outlier toy model (gen-toy: heavy-tailed x channels, B / C
+    state groups of different magnitude, outlier channels of the gated-norm output), and the
+    no-Hadamard row is the minimum.  Quantized with the product pipeline, evaluated with the
+    oracle's quantized block forward against the float block on held-out tokens."""
+    from oracle import pipeline as opl
+    from oracle import qblock as oq
+    from oracle import ssm_block as osb
+    dims = ("mamba2", 128, 256, 32, 16, 16, 4, 4)
+    d = Dims(*dims)
+    fm = cli.cmd_gen_toy(d, 1, seed, 64)
+    stats = calibrate.collect_stats(fm, cli.calib_tokens(64, 8, 32), device="cpu", keep_rows=256)
+    ofm = opl.cmd_gen_toy(osb.Dims(*dims), 1, seed, 64)
+    ev = opl.calib_tokens(64, 2, 48, seed=9)
+    u = osb.rmsnorm(ofm.embedding[ev[0]], ofm.layer_norms[0])
+    ref, _ = osb.block_forward_float(u, ofm.blocks[0], fast=True)
+    rows = [dict(hadamard=False, gptq=False, persg=False, snc=False),   # "fail"
+            dict(hadamard=True, gptq=False, persg=False, snc=False),    # PerG + Had
+            dict(hadamard=True, gptq=True, persg=False, snc=False),     # + GPTQ
+            dict(hadamard=True, gptq=True, persg=True, snc=False),      # + PerSG
+            dict(hadamard=True, gptq=True, persg=True, snc=True)]       # + SnC (the full pipeline)
+    sq = []
+    for kw in rows:
+        p = cli.quantize_block(fm.blocks[0], stats[0], "W4A8", **kw)
+        qb = oq.QBlock(osb.Dims(*dims), p.profile, oq.QLinear(**vars(p.in_proj)), oq.QLinear(**vars(p.out_proj)),
+                       p.conv_weight, p.conv_bias, p.a_log, p.d_param, p.dt_bias, p.norm_weight, p.head_group,
+                       s_u=p.s_u, in_out_scale=p.in_out_scale, conv_in_scale=p.conv_in_scale,
+                       conv_out_scale=p.conv_out_scale, state_scale=p.state_scale, s_y=p.s_y, hadamard=p.hadamard)
+        out, _ = oq.block_forward_quantized(u, qb)
+        sq.append(10 * np.log10((ref ** 2).sum() / ((out - ref) ** 2).sum()))
+    assert all(b > a for a, b in zip(sq, sq[1:])), sq
+    assert sq[0] == min(sq)
