@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQ_ABI_VERSION 7
+#define SQ_ABI_VERSION 8
 
 typedef enum {
   SQ_OK = 0,
@@ -251,6 +251,24 @@ typedef struct {
 } sq_mamba1_decode_params;
 
 int64_t sq_mamba1_decode_ws_bytes(const sq_mamba1_decode_params* p, int B);
+/* Whole Mamba1 W8A8 decode layer in ONE launch (B <= 8): the model's pre-norm + quant of the
+ * residual stream h (sq_rmsnorm_quant's math and order), in_proj (W8, EPI_QUANT), the SSM half of
+ * sq_mamba1_decode_step_int8, and out_proj (W8, EPI_RESID into h).  Replaces the four launches
+ * sq_rmsnorm_quant + sq_gemm_w8a8 + sq_mamba1_decode_step_int8 + sq_gemm_w8a8 of a layer.
+ * ws as sq_mamba1_decode_ws_bytes (zeroed once). */
+typedef struct {
+  const float* ln_w;          /* [d_model] the model's pre-norm weight */
+  float ln_eps, s_u;          /* its eps; in_proj input code scale     */
+  int d_model;
+  const int8_t* in_w;         /* [2*d_inner x d_model]                 */
+  const float* in_alpha;      /* [2*d_inner]                           */
+  const float* in_cs;         /* [2*d_inner] output code scales        */
+  const int8_t* out_w;        /* [d_model x d_inner]                   */
+  const float* out_alpha;     /* [d_model]                             */
+} sq_mamba1_layer_params;
+int sq_mamba1_decode_layer_int8(const sq_mamba1_decode_params* p, const sq_mamba1_layer_params* lp, int B,
+                                float* h, int64_t ldh, int8_t* conv_cache, int8_t* state, void* ws, void* stream);
+
 int sq_mamba1_decode_step_int8(const sq_mamba1_decode_params* p, int B, const int8_t* zx, int64_t ldzx,
                                int8_t* conv_cache /*[B x (Kc-1) x d_inner]*/, int8_t* state /*[B x d_inner x 16]*/,
                                void* ws, int8_t* yq, int64_t ldyq, void* stream);

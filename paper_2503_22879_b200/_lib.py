@@ -10,7 +10,7 @@ import os
 
 LIB_NAME = "libssmquant_sm100.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 _i8p = C.c_void_p
 _f32p = C.c_void_p
@@ -41,6 +41,11 @@ class Mamba1DecodeParams(C.Structure):
                 ("conv_s_out", _vp), ("dt_rank", _int), ("xproj_w", _vp), ("xproj_alpha", _vp), ("xproj_cs", _vp),
                 ("dtproj_w", _vp), ("dtproj_alpha", _vp), ("dtproj_cs", _vp), ("norm_w", _vp), ("eps", _flt),
                 ("s_y", _flt), ("hadamard", _int)]
+
+
+class Mamba1LayerParams(C.Structure):
+    _fields_ = [("ln_w", _vp), ("ln_eps", _flt), ("s_u", _flt), ("d_model", _int), ("in_w", _vp), ("in_alpha", _vp),
+                ("in_cs", _vp), ("out_w", _vp), ("out_alpha", _vp)]
 
 
 class ConvEpilogue(C.Structure):
@@ -86,6 +91,8 @@ _SIGS = {
     "sq_selective_scan_f32": ([C.POINTER(Mamba1Params), _int, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                                 _vp, _int, _vp, _i64, _vp], _int),
     "sq_mamba1_decode_ws_bytes": ([C.POINTER(Mamba1DecodeParams), _int], _i64),
+    "sq_mamba1_decode_layer_int8": ([C.POINTER(Mamba1DecodeParams), C.POINTER(Mamba1LayerParams), _int, _vp, _i64,
+                                     _vp, _vp, _vp, _vp], _int),
     "sq_mamba1_decode_step_int8": ([C.POINTER(Mamba1DecodeParams), _int, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _vp],
                                    _int),
     "sq_mamba2_decode_ws_bytes": ([C.POINTER(Mamba2DecodeParams), _int], _i64),

@@ -81,19 +81,29 @@ struct M1DecodeArgs {
   uint8_t* ws;
   int8_t* yq;
   int64_t ldyq;
+  // whole-layer mode (sq_mamba1_decode_layer_int8): pre-norm + in_proj before, out_proj after
+  int layer;
+  sq_mamba1_layer_params lp;
+  float* h;
+  int64_t ldh;
 };
 
-// workspace: [0, 256) barrier words | xc int8 [B x di] | xd int8 [B x NX] | y f32 [B x di]
+// workspace: [0, 256) barrier words | xc int8 [B x di] | xd int8 [B x NX] | y f32 [B x di] |
+// zx int8 [B x 2 di] | yq int8 [B x di] (the last two in whole-layer mode)
 struct M1Ws {
-  int64_t xc, xd, y, total;
+  int64_t xc, xd, y, zx, yq, total;
   __host__ __device__ M1Ws(int B, int di, int nx) {
     auto up = [](int64_t v) { return (v + 255) & ~(int64_t)255; };
     xc = 256;
     xd = xc + up((int64_t)B * di);
     y = xd + up((int64_t)B * nx);
-    total = y + up((int64_t)B * di * 4);
+    zx = y + up((int64_t)B * di * 4);
+    yq = zx + up((int64_t)B * 2 * di);
+    total = yq + up((int64_t)B * di);
   }
 };
+constexpr int M1D_MAXK16 = 16;   // 16-B weight pieces per lane and row of out_proj (K = d_inner <= 8192)
+constexpr int M1D_MAXKIN = 8;    // ... of in_proj (K = d_model <= 4096; double-buffered)
 
 __global__ void __launch_bounds__(M1D_THREADS, 1) mamba1_decode_fused_kernel(M1DecodeArgs a) {
   const sq_mamba1_decode_params& P = a.p;
@@ -156,6 +166,87 @@ __global__ void __launch_bounds__(M1D_THREADS, 1) mamba1_decode_fused_kernel(M1D
   M1D_MARK(0);
   pdl_wait();   // zx and the cached conv inputs / state come from earlier grids
   M1D_MARK(1);
+  const int xrows = (NX + G - 1) / G;
+  int8_t* xs_base = xw + (int64_t)xrows * di;          // xc staging [B x di] (phase 2)
+  int8_t* us = xs_base + (int64_t)B * di;              // u codes [B x d_model] (phase 0)
+  if (a.layer) {
+    // ---------------- phase 0: the model's pre-norm + quant of h (rmsnorm16_kernel's math and
+    // summation order: D/16 threads x 16 contiguous elements, f64 squares, warp xor trees, warps
+    // in order), every CTA for itself; then in_proj rows, one per warp, dp4a over the u codes
+    const sq_mamba1_layer_params& lp = a.lp;
+    const int dm = lp.d_model, nthr = dm / 16, nwr = (nthr + 31) / 32;
+    __shared__ double lred[M1D_THREADS / 32];
+    for (int b = 0; b < B; ++b) {
+      float v[16];
+      double ss = 0.0;
+      if (tid < nthr) {
+        const float* hr = a.h + (int64_t)b * a.ldh + tid * 16;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float4 f = *reinterpret_cast<const float4*>(hr + e * 4);
+          v[e * 4] = f.x; v[e * 4 + 1] = f.y; v[e * 4 + 2] = f.z; v[e * 4 + 3] = f.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ss += (double)v[i] * (double)v[i];
+      }
+      if (warp < nwr) {
+        ss = warp_sum_d(ss);
+        if (lane == 0) lred[warp] = ss;
+      }
+      __syncthreads();
+      double tot = 0.0;
+      for (int w = 0; w < nwr; ++w) tot += lred[w];
+      const float r = rms_factor_m1(tot, dm, lp.ln_eps);
+      if (tid < nthr) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          us[(int64_t)b * dm + tid * 16 + i] = quant8(__fmul_rn(__fmul_rn(v[i], r), lp.ln_w[tid * 16 + i]), lp.s_u);
+      }
+      __syncthreads();   // lred reused by the next row; u codes visible
+    }
+    int8_t* zxw = const_cast<int8_t*>(a.zx);
+    // rows of this warp, software-pipelined: the next row's weights and epilogue scales are in
+    // flight while the current row is reduced
+    const int nstep = G * (M1D_THREADS / 32);
+    int n = blockIdx.x * (M1D_THREADS / 32) + warp;
+    int4 wv[M1D_MAXKIN], wn[M1D_MAXKIN];
+    float al = 0.f, cs = 1.f, aln = 0.f, csn = 1.f;
+    auto load_row = [&](int row, int4 (&dst)[M1D_MAXKIN], float& a_, float& c_) {
+      const int8_t* wr = lp.in_w + (int64_t)row * dm;
+#pragma unroll
+      for (int j = 0; j < M1D_MAXKIN; ++j)
+        dst[j] = lane * 16 + j * 512 < dm ? __ldg(reinterpret_cast<const int4*>(wr + lane * 16 + j * 512))
+                                          : make_int4(0, 0, 0, 0);
+      a_ = __ldg(lp.in_alpha + row);
+      c_ = __ldg(lp.in_cs + row);
+    };
+    if (n < 2 * di) load_row(n, wv, al, cs);
+    for (; n < 2 * di; n += nstep) {
+      if (n + nstep < 2 * di) load_row(n + nstep, wn, aln, csn);
+      for (int b = 0; b < B; ++b) {
+        int acc = 0;
+#pragma unroll
+        for (int j = 0; j < M1D_MAXKIN; ++j) {
+          if (lane * 16 + j * 512 < dm) {
+            const int4 x = *reinterpret_cast<const int4*>(us + (int64_t)b * dm + lane * 16 + j * 512);
+            acc = __dp4a(wv[j].x, x.x, acc);
+            acc = __dp4a(wv[j].y, x.y, acc);
+            acc = __dp4a(wv[j].z, x.z, acc);
+            acc = __dp4a(wv[j].w, x.w, acc);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) zxw[(int64_t)b * a.ldzx + n] = quant8(__fmul_rn((float)acc, al), cs);
+      }
+#pragma unroll
+      for (int j = 0; j < M1D_MAXKIN; ++j) wv[j] = wn[j];
+      al = aln;
+      cs = csn;
+    }
+    M1D_MARK(9);
+    grid_sync(bar);
+  }
 
   // ---------------- phase 1: conv update (+ cache shift), one (sequence, channel) per thread
   for (int i = i1; i < B * di; i += gthreads) {
@@ -180,7 +271,7 @@ __global__ void __launch_bounds__(M1D_THREADS, 1) mamba1_decode_fused_kernel(M1D
   M1D_MARK(3);
 
   // ---------------- phase 2: x_proj, one output row per warp (weights and xc from shared memory, dp4a)
-  int8_t* xs = xw + (int64_t)((NX + G - 1) / G) * di;   // xc [B x di] staged once per CTA
+  int8_t* xs = xs_base;   // xc [B x di] staged once per CTA
   if (blockIdx.x < NX) {   // CTA-uniform: the CTA owns at least one row
     for (int k = tid * 16; k < B * di; k += M1D_THREADS * 16) cp_async16_m1(xs + k, xc + k);
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -325,6 +416,52 @@ __global__ void __launch_bounds__(M1D_THREADS, 1) mamba1_decode_fused_kernel(M1D
     }
     __syncthreads();   // red / hs reused by the next (sequence, block)
   }
+  if (a.layer) {
+    // ---------------- phase 5: out_proj rows, one per warp, over the yq codes staged in shared
+    // memory; the GEMM's residual epilogue h += f32(acc) * alpha
+    grid_sync(bar);
+    const sq_mamba1_layer_params& lp = a.lp;
+    const int dm = lp.d_model;
+    int8_t* ys = xs_base;   // xc staging and u codes are dead: stage yq [B x di] over them
+    for (int k = tid * 16; k < B * di; k += M1D_THREADS * 16) cp_async16_m1(ys + k, a.yq + k);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int n = blockIdx.x * (M1D_THREADS / 32) + warp; n < dm; n += G * (M1D_THREADS / 32)) {
+      const int8_t* wr = lp.out_w + (int64_t)n * di;
+      const float oal = __ldg(lp.out_alpha + n);
+      float hv[M1D_MAXB];
+#pragma unroll
+      for (int b = 0; b < M1D_MAXB; ++b) hv[b] = (lane == 0 && b < B) ? a.h[(int64_t)b * a.ldh + n] : 0.f;
+      int4 wv[M1D_MAXK16];
+#pragma unroll
+      for (int j = 0; j < M1D_MAXK16; ++j)
+        wv[j] = lane * 16 + j * 512 < di ? __ldg(reinterpret_cast<const int4*>(wr + lane * 16 + j * 512))
+                                         : make_int4(0, 0, 0, 0);
+      for (int b = 0; b < B; ++b) {
+        int acc = 0;
+#pragma unroll
+        for (int j = 0; j < M1D_MAXK16; ++j) {
+          if (lane * 16 + j * 512 < di) {
+            const int4 x = *reinterpret_cast<const int4*>(ys + (int64_t)b * di + lane * 16 + j * 512);
+            acc = __dp4a(wv[j].x, x.x, acc);
+            acc = __dp4a(wv[j].y, x.y, acc);
+            acc = __dp4a(wv[j].z, x.z, acc);
+            acc = __dp4a(wv[j].w, x.w, acc);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+          float hb = hv[0];
+#pragma unroll
+          for (int bb = 1; bb < M1D_MAXB; ++bb)
+            if (bb == b) hb = hv[bb];
+          a.h[(int64_t)b * a.ldh + n] = __fadd_rn(hb, __fmul_rn((float)acc, oal));
+        }
+      }
+    }
+  }
   M1D_MARK(8);
 }
 
@@ -365,7 +502,44 @@ extern "C" int sq_mamba1_decode_step_int8(const sq_mamba1_decode_params* p, int 
   std::call_once(once[dev & 63], [] {
     cudaFuncSetAttribute(mamba1_decode_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   });
-  M1DecodeArgs a{*p, B, zx, ldzx, conv_cache, state, reinterpret_cast<uint8_t*>(ws), yq, ldyq};
+  M1DecodeArgs a{*p, B, zx, ldzx, conv_cache, state, reinterpret_cast<uint8_t*>(ws), yq, ldyq, 0, {}, nullptr, 0};
   launch_k(PDL_SMALL8, mamba1_decode_fused_kernel, dim3(G), dim3(M1D_THREADS), smem, as_stream(stream), a);
   return check_launch("sq_mamba1_decode_step_int8");
+}
+
+extern "C" int sq_mamba1_decode_layer_int8(const sq_mamba1_decode_params* p, const sq_mamba1_layer_params* lp, int B,
+                                           float* h, int64_t ldh, int8_t* conv_cache, int8_t* state, void* ws,
+                                           void* stream) {
+  SQ_REQUIRE(p && lp && h && B >= 0, SQ_ERR_ARG, "sq_mamba1_decode_layer_int8: bad args");
+  if (B == 0) return SQ_OK;
+  const int di = p->ssm.d_inner, R = p->dt_rank, dm = lp->d_model;
+  const int blk = p->hadamard ? (di & -di) : di;
+  SQ_REQUIRE(p->ssm.d_state == 16 && B <= M1D_MAXB && di % 16 == 0 && di <= 8192 && R % 4 == 0 && R > 0 &&
+                 p->conv_kernel >= 1 && p->conv_kernel <= 8 && (!p->hadamard || blk <= M1D_MAXBLK) &&
+                 dm % 16 == 0 && dm / 16 <= M1D_THREADS && dm <= 512 * M1D_MAXKIN && di <= 512 * M1D_MAXK16 &&
+                 ldh % 4 == 0,
+             SQ_ERR_SHAPE, "sq_mamba1_decode_layer_int8: unsupported shape");
+  SQ_REQUIRE(!((reinterpret_cast<uintptr_t>(p->xproj_w) | reinterpret_cast<uintptr_t>(p->dtproj_w) |
+                reinterpret_cast<uintptr_t>(lp->in_w) | reinterpret_cast<uintptr_t>(lp->out_w) |
+                reinterpret_cast<uintptr_t>(h) | reinterpret_cast<uintptr_t>(ws)) & 15),
+             SQ_ERR_LAYOUT, "sq_mamba1_decode_layer_int8: weights / h / workspace must be 16-B aligned");
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (sms[dev & 63] == 0) cudaDeviceGetAttribute(&sms[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  const int G = sms[dev & 63];
+  const int nx = R + 2 * p->ssm.d_state;
+  const M1Ws L(B, di, nx);
+  // x_proj rows + xc staging + u codes; phase 5 stages yq over the last two
+  const size_t smem = (size_t)((nx + G - 1) / G) * di + (size_t)B * di + (size_t)B * dm;
+  SQ_REQUIRE(smem <= 160 * 1024, SQ_ERR_SHAPE, "sq_mamba1_decode_layer_int8: shared memory");
+  static std::once_flag once[64];
+  std::call_once(once[dev & 63], [] {
+    cudaFuncSetAttribute(mamba1_decode_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  });
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
+  M1DecodeArgs a{*p, B, reinterpret_cast<const int8_t*>(w8 + L.zx), 2 * di, conv_cache, state, w8,
+                 reinterpret_cast<int8_t*>(w8 + L.yq), di, 1, *lp, h, ldh};
+  launch_k(PDL_SMALL8, mamba1_decode_fused_kernel, dim3(G), dim3(M1D_THREADS), smem, as_stream(stream), a);
+  return check_launch("sq_mamba1_decode_layer_int8");
 }

@@ -69,6 +69,10 @@ class QuantizedMambaLM:
         self.head = hm.head if isinstance(hm.head, DeviceLinear) else DeviceLinear(hm.head, dev, self.s_head)
         self.vocab = self.head.N
         self._graphs = {}
+        # Mamba1 W8A8 decode, one launch per whole layer (sq_mamba1_decode_layer_int8): bit-exact with
+        # the 4-launch chain but not faster on B200 (32.0 vs 31.8 us per 2.8B layer with L2-warm
+        # weights, 417 vs 454 tok/s in the bench with weights from HBM), so off
+        self.fuse_layers = False
 
     @property
     def n_layers(self):
@@ -111,6 +115,20 @@ class QuantizedMambaLM:
         return ws
 
     # ------------------------------------------------------------------ forward
+    def _m1_layer(self, l, blk):
+        """Layer parameters of the one-launch Mamba1 decode layer (W8 in/out projections and the
+        one-launch SSM half), built once per block; None when the block does not qualify."""
+        if not self.fuse_layers or not getattr(blk, "m1_fused_decode", False):
+            return None
+        if blk.in_proj.kind != "w8" or blk.out_proj.kind != "w8":
+            return None
+        lp = getattr(blk, "_m1_layer_params", None)
+        if lp is None:
+            lp = ops.mamba1_layer_params(self.layer_norms[l], EPS_NORM, blk.s_u, self.dims.d_model, blk.in_proj.w,
+                                         blk.in_proj.alpha, blk.in_out_scale, blk.out_proj.w, blk.out_proj.alpha)
+            blk._m1_layer_params = lp
+        return lp
+
     def _run(self, tok, B, T, states, state_in, ws, all_logits):
         """tok int32 [B*T] (b-major) → logits; every launch on the current stream."""
         h = ws["h"]
@@ -120,6 +138,10 @@ class QuantizedMambaLM:
             ops.embed_int8(self.emb_codes, self.emb_scale, tok, h)
         for l, blk in enumerate(self.blocks):
             st = states[l]
+            lp = self._m1_layer(l, blk) if (T == 1 and state_in and self.tp_world == 1 and "m1ws" in ws) else None
+            if lp is not None:   # Mamba1 W8A8 decode: the whole layer in one launch (decode_m1.cu)
+                ops.mamba1_decode_layer_int8(blk.m1_decode_params, lp, B, h, st.conv_cache, st.h, ws["m1ws"])
+                continue
             if blk.a8 and self.tp_world > 1:   # head shard: partial -> all_reduce -> residual
                 ops.rmsnorm_quant(h, self.layer_norms[l], EPS_NORM, blk.s_u, ws["u"])
                 part = blk.forward_codes(ws["u"], B, T, st, state_in, ws=ws)

@@ -430,6 +430,30 @@ def mamba1_decode_step_int8(p, B, zx, conv_cache, state, ws, yq=None):
     return yq
 
 
+def mamba1_layer_params(ln_w, eps, s_u, d_model, in_w, in_alpha, in_cs, out_w, out_alpha) -> _lib.Mamba1LayerParams:
+    return _lib.Mamba1LayerParams(ln_w.data_ptr(), float(eps), float(s_u), int(d_model), in_w.data_ptr(),
+                                  in_alpha.data_ptr(), in_cs.data_ptr(), out_w.data_ptr(), out_alpha.data_ptr())
+
+
+def mamba1_decode_layer_int8(p, lp, B, h, conv_cache, state, ws):
+    """A whole Mamba1 W8A8 decode layer in one launch: h f32 [B x d_model] (the residual stream,
+    updated in place: pre-norm + in_proj + SSM half + out_proj residual add); ``ws`` as
+    mamba1_decode_step_int8's (zeroed once)."""
+    _dev(h, torch.float32, "h", 2)
+    _dev(conv_cache, torch.int8, "conv_cache")
+    _dev(state, torch.int8, "state")
+    _rows(h, B, "h")
+    di = p.ssm.d_inner
+    _need(state, B * di * p.ssm.d_state, "state [B x d_inner x N]")
+    _need(conv_cache, B * (p.conv_kernel - 1) * di, "conv_cache [B x (K-1) x d_inner]")
+    nbytes = mamba1_decode_ws_bytes(p, B)
+    if ws is None or ws.numel() * ws.element_size() < nbytes:
+        raise ShapeError(f"Mamba1 decode workspace needs {nbytes} zero-initialised bytes")
+    _check(lib().sq_mamba1_decode_layer_int8(C.byref(p), C.byref(lp), B, h.data_ptr(), _ld(h),
+                                             conv_cache.data_ptr(), state.data_ptr(), ws.data_ptr(), _stream()), 1)
+    return h
+
+
 def mamba1_params(d_inner, d_state, A, D, dt_bias, s_dt, s_z, s_B, s_C, s_x, s_h) -> _lib.Mamba1Params:
     return _lib.Mamba1Params(d_inner, d_state, A.data_ptr(), D.data_ptr(), dt_bias.data_ptr(), float(s_dt),
                              float(s_z), float(s_B), float(s_C), s_x.data_ptr(), s_h.data_ptr())

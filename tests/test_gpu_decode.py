@@ -164,3 +164,46 @@ def test_mamba1_fused_decode_repeat_deterministic(cuda):
     for o in outs[1:]:
         for a, b in zip(o, outs[0]):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dims,B", [(("mamba1", 256, 512, 16, 1, 512, 1, 4, 32), 2),
+                                    (("mamba1", 2560, 5120, 16, 1, 5120, 1, 4, 160), 1)], ids=["tiny", "m1_2p8b"])
+def test_mamba1_decode_layer_in_one_launch(cuda, dims, B):
+    """Whole-layer Mamba1 W8A8 decode (sq_mamba1_decode_layer_int8: pre-norm + quant in the
+    rmsnorm16 summation order, in_proj, the SSM half, out_proj residual) equals the four-launch
+    chain per decode step: residual stream, conv caches and int8 states bit-exact over 4 steps
+    of a 3-layer model; the CUDA-graph generate agrees token for token."""
+    from paper_2503_22879_b200 import ops, synth
+    from paper_2503_22879_b200.ssm_block import Dims
+    d = Dims(*dims)
+    m = synth.synthetic_lm(d, 3, "W8A8", 512, cuda, seed=4, head_kind="w8")
+    assert all(b.m1_fused_decode for b in m.blocks)
+    g = torch.Generator(device=cuda)
+    g.manual_seed(8)
+    prompt = torch.randint(0, 512, (B, 12), generator=g, device=cuda)
+    _, st0 = m.prefill(prompt)
+    runs = []
+    for fuse in (True, False):
+        m.fuse_layers = fuse
+        sts = [type(s)(s.h.clone(), s.conv_cache.clone()) for s in st0]
+        ws = m._workspace(B)
+        tok = torch.empty(B, dtype=torch.int32, device=cuda)
+        tok.copy_(prompt[:, -1])
+        lgs = []
+        for _ in range(4):
+            lg = m.decode_step(tok, sts, ws)
+            lgs.append(lg.clone())
+            tok = ops.argmax(lg)
+        torch.cuda.synchronize()
+        runs.append((lgs, sts))
+    (lf, sf), (lu, su) = runs
+    for a, b in zip(lf, lu):
+        assert torch.equal(a, b)
+    for a, b in zip(sf, su):
+        assert torch.equal(a.h, b.h) and torch.equal(a.conv_cache, b.conv_cache)
+    m.fuse_layers = True
+    out_f = m.generate(prompt, 6)
+    m.fuse_layers = False
+    out_u = m.generate(prompt, 6)
+    assert torch.equal(out_f, out_u)
+    assert not synth.synthetic_lm(d, 1, "W8A8", 512, cuda, seed=5, head_kind="w8").fuse_layers   # default off
