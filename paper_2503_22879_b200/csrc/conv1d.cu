@@ -162,8 +162,11 @@ __global__ void __launch_bounds__(128) conv1d_prefill4_kernel(const int8_t* __re
         sv[pr] = silu2_approx(acc);
         // quant8_fast on the pair: t = v / s (by reciprocal), magic-number rint, tie flag
         float2 t = __fmul2_rn(sv[pr], iso[pr]);
-        // no float clamp: rint as an int, saturated by cvt.pack.sat below (a |t| too large for the
-        // magic add fails the tie check and takes the exact path); bit-identical codes, 7% faster
+        // rint as an int, saturated by cvt.pack.sat below instead of clamping to [-128, 127] and
+        // packing bytes (bit-identical codes).  Only the low side is clamped, at -2^22: the magic
+        // add then keeps r > 0, so every t <= -128.5 saturates to -128 and every t >= 127.5 to 127
+        t.x = fmaxf(t.x, -4194304.f);
+        t.y = fmaxf(t.y, -4194304.f);
         const float2 r = __fadd2_rn(t, RM);
         const float2 d = __ffma2_rn(__fadd2_rn(r, NRM), make_float2(-1.f, -1.f), t);   // t - rint(t)
         tie |= fabsf(d.x) > 0.4999f || fabsf(d.y) > 0.4999f;
